@@ -1,0 +1,216 @@
+/*
+ * lcnn_cuda.h -- C ABI of the B200 (sm_100a) memory-bound CNN layer path.
+ *
+ * This is the drop-in boundary between the reference's C++ operator API
+ * (/root/reference/proj/include/lcnn/ headers) and hand-written CUDA kernels.
+ * Every entry point takes caller-owned DEVICE pointers plus a cudaStream_t
+ * (passed as void* so this header needs no CUDA include), validates its
+ * parameters synchronously on the host with the reference's rules, and then
+ * enqueues stream-ordered kernels.  Nothing here allocates or frees device
+ * memory; nothing here synchronises the stream.
+ *
+ * Each entry cites the reference interface it replaces (file:line relative to
+ * /root/reference/proj).  Errors map 1:1 onto the reference exception types
+ * of include/lcnn/errors.hpp:8-56; the C++ host layer (host/include/lcnn/)
+ * rethrows them with the same message text (lcnn_last_error()).
+ *
+ * Tensor layouts use the reference's codes (tensor.hpp:16): the last-named
+ * dimension is contiguous.
+ */
+#ifndef LCNN_CUDA_H_
+#define LCNN_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LCNN_ABI_VERSION 1
+
+/* Status codes; one per exception class of errors.hpp:8-56 plus CUDA/arg. */
+typedef enum lcnn_status {
+  LCNN_OK = 0,
+  LCNN_ESHAPE = 1,        /* ShapeError        errors.hpp:13 */
+  LCNN_EINDEX = 2,        /* IndexError        errors.hpp:18 */
+  LCNN_ELAYOUT = 3,       /* LayoutError       errors.hpp:23 */
+  LCNN_EPLAN = 4,         /* PlanError         errors.hpp:28 */
+  LCNN_EFORMAT = 5,       /* FormatError       errors.hpp:33 */
+  LCNN_EDOMAIN = 6,       /* DomainError       errors.hpp:38 */
+  LCNN_EUNSUPPORTED = 7,  /* UnsupportedError  errors.hpp:43 */
+  LCNN_EVALIDATION = 8,   /* ValidationError   errors.hpp:48 */
+  LCNN_ECALIBRATION = 9,  /* CalibrationError  errors.hpp:53 */
+  LCNN_ECUDA = 10,        /* CUDA runtime failure (launch, bad pointer) */
+  LCNN_EINVAL = 11        /* null pointer / bad enum at the ABI level */
+} lcnn_status;
+
+/* Layout codes == lcnn::Layout (tensor.hpp:16) and the T4D1 layout byte. */
+typedef enum lcnn_layout {
+  LCNN_NCHW = 0,
+  LCNN_CHWN = 1,
+  LCNN_NHWC = 2,
+  LCNN_HWCN = 3
+} lcnn_layout;
+
+/* == lcnn::PoolMode (pool.hpp:11). */
+typedef enum lcnn_pool_mode { LCNN_POOL_MAX = 0, LCNN_POOL_AVG = 1 } lcnn_pool_mode;
+
+/* == lcnn::AccessReport (pool.hpp:30-34).  Computed analytically on the host
+ * with the reference's counting rules; the kernels themselves are measured
+ * with ncu (dram__bytes_*). */
+typedef struct lcnn_access_report {
+  uint64_t input_loads;
+  uint64_t output_stores;
+  uint64_t distinct_inputs;
+} lcnn_access_report;
+
+/* == lcnn::PassReport (softmax.hpp:21-24). */
+typedef struct lcnn_pass_report {
+  uint32_t materializations;
+  uint32_t full_matrix_sweeps;
+} lcnn_pass_report;
+
+/* ---- library ----------------------------------------------------------- */
+int lcnn_abi_version(void);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* lcnn_last_error(void);
+const char* lcnn_status_name(int status);
+/* 1 if a CUDA device of compute capability 10.x is usable, else 0. */
+int lcnn_device_ok(void);
+
+/* ---- layout transform (layout.hpp:12-40, layout.cpp:72-144) ------------ */
+/* == flattenable_pair (layout.cpp:72-75). */
+int lcnn_flattenable_pair(int src_layout, int dst_layout);
+
+/* == transform (layout.cpp:138-144): CHWN<->NCHW run as a 2D transpose
+ * [C*H*W]x[N] <-> [N]x[C*H*W]; other pairs run the generic 4D permute;
+ * src == dst is a copy.  Bit-exact (pure data movement).  src and dst must
+ * not overlap. */
+lcnn_status lcnn_transform(const float* src, float* dst, uint32_t n, uint32_t c,
+                           uint32_t h, uint32_t w, int src_layout,
+                           int dst_layout, void* stream);
+
+/* == transform_tiled (layout.cpp:99-120) with validate_plan's PlanError rules
+ * (layout.cpp:13-26): pair must flatten, tile a power of two in [8,128],
+ * wide_copy requires n >= 64.  On the GPU the tile and wide flags are hints:
+ * the kernel always moves 128-bit vectors where alignment allows. */
+lcnn_status lcnn_transform_tiled(const float* src, float* dst, uint32_t n,
+                                 uint32_t c, uint32_t h, uint32_t w,
+                                 int src_layout, int dst_layout, uint32_t tile,
+                                 int wide_copy, void* stream);
+
+/* == transform_naive (layout.cpp:77-97): element-wise 4D permutation for any
+ * layout pair (the generic kernel; no 2D flattening). */
+lcnn_status lcnn_transform_naive(const float* src, float* dst, uint32_t n,
+                                 uint32_t c, uint32_t h, uint32_t w,
+                                 int src_layout, int dst_layout, void* stream);
+
+/* ---- pooling (pool.hpp:36-65, pool.cpp:19-270) -------------------------- */
+/* == pool_output_extents (pool.cpp:44-47) plus check_window (pool.cpp:19-26)
+ * so a caller can size the output before launching. */
+lcnn_status lcnn_pool_output_extents(uint32_t h, uint32_t w, uint32_t win_h,
+                                     uint32_t win_w, uint32_t stride,
+                                     uint32_t* h_out, uint32_t* w_out);
+
+/* == pool_layout (pool.cpp:172-176 -> pool_plain :98-163).  layout must be
+ * CHWN or NCHW (LayoutError otherwise, pool.cpp:165); output keeps the input
+ * layout.  Max: bit-exact with acc = (acc < v) ? v : acc from -inf in (y,x)
+ * tap order.  Average: fp32 adds from 0.0f in (y,x) order, then CHWN
+ * multiplies by 1.0f/(wh*ww) while NCHW divides by float(wh*ww), as the
+ * reference does.  report may be NULL. */
+lcnn_status lcnn_pool_layout(const float* src, float* dst, uint32_t n,
+                             uint32_t c, uint32_t h, uint32_t w, int layout,
+                             uint32_t win_h, uint32_t win_w, uint32_t stride,
+                             int mode, lcnn_access_report* report,
+                             void* stream);
+
+/* == pool_coarsened (pool.cpp:178-270): CHWN only (LayoutError otherwise),
+ * PlanError if fh or fw < 1 or fh*fw > 64 (kCoarseningCap, pool.hpp:28).
+ * Each thread keeps an fh x fw block of outputs in registers and loads the
+ * receptive-field union once.  report uses the union-count formula. */
+lcnn_status lcnn_pool_coarsened(const float* src, float* dst, uint32_t n,
+                                uint32_t c, uint32_t h, uint32_t w, int layout,
+                                uint32_t win_h, uint32_t win_w, uint32_t stride,
+                                int mode, uint32_t fh, uint32_t fw,
+                                lcnn_access_report* report, void* stream);
+
+/* GPU extension (not in the reference API, which rejects NCHW coarsening,
+ * pool.cpp:189-191): the register-coarsened NCHW kernel.  Same output bits
+ * as lcnn_pool_layout on NCHW; report counts the union loads. */
+lcnn_status lcnn_pool_coarsened_nchw(const float* src, float* dst, uint32_t n,
+                                     uint32_t c, uint32_t h, uint32_t w,
+                                     uint32_t win_h, uint32_t win_w,
+                                     uint32_t stride, int mode, uint32_t fh,
+                                     uint32_t fw, lcnn_access_report* report,
+                                     void* stream);
+
+/* == pool_oracle (pool.cpp:49-84): any input layout, NCHW output, fp64
+ * accumulation, max seeded from the first tap.  Ground truth, not a hot op. */
+lcnn_status lcnn_pool_oracle(const float* src, float* dst, uint32_t n,
+                             uint32_t c, uint32_t h, uint32_t w, int layout,
+                             uint32_t win_h, uint32_t win_w, uint32_t stride,
+                             int mode, void* stream);
+
+/* ---- softmax (softmax.hpp:28-39, softmax.cpp:36-180) -------------------- */
+/* == softmax_fused (softmax.cpp:100-180).  One kernel: the row is staged in
+ * registers (or shared memory for wide rows), max and sum reduced with warp
+ * shuffles + shared memory, no intermediate touches HBM.  Rows wider than
+ * local_buffer_limit are reported as the streaming schedule (5 sweeps), as
+ * the reference does.  d_nonfinite (device int, may be NULL) is zeroed on
+ * the stream and set to 1 if any input is inf/NaN: the host wrapper reads it
+ * and raises DomainError (softmax.cpp:15-19).  report may be NULL. */
+lcnn_status lcnn_softmax_fused(const float* src, float* dst, uint32_t rows,
+                               uint32_t cols, uint32_t local_buffer_limit,
+                               int* d_nonfinite, lcnn_pass_report* report,
+                               void* stream);
+
+/* Device scratch (bytes) the five-pass path needs for (rows, cols). */
+size_t lcnn_softmax_reference_scratch_bytes(uint32_t rows, uint32_t cols);
+
+/* == softmax_reference (softmax.cpp:36-98): five kernels (max, subtract,
+ * exp, blocked sum, normalise) each materialising its intermediate in the
+ * caller's scratch -- the paper's multi-kernel baseline. */
+lcnn_status lcnn_softmax_reference(const float* src, float* dst,
+                                   uint32_t rows, uint32_t cols,
+                                   void* d_scratch, size_t scratch_bytes,
+                                   int* d_nonfinite, lcnn_pass_report* report,
+                                   void* stream);
+
+/* ---- convolution / fully-connected (conv.hpp:17-54, softmax.cpp:182) ---- */
+/* == conv_output_extents (conv.cpp:22-33). */
+lcnn_status lcnn_conv_output_extents(uint32_t h, uint32_t w, uint32_t f_h,
+                                     uint32_t f_w, uint32_t stride,
+                                     uint32_t pad, uint32_t* h_out,
+                                     uint32_t* w_out);
+
+/* Precision of the tensor-core paths. */
+typedef enum lcnn_precision {
+  LCNN_PREC_TF32 = 0,   /* 1 tcgen05 kind::tf32 MMA per tile (fastest)     */
+  LCNN_PREC_3XTF32 = 1  /* big*big + big*small + small*big: ~fp32 accuracy */
+} lcnn_precision;
+
+/* Bytes of device workspace lcnn_conv_forward needs (repacked filters). */
+size_t lcnn_conv_workspace_bytes(uint32_t c_o, uint32_t c_i, uint32_t f_h,
+                                 uint32_t f_w);
+
+/* == conv_direct (conv.cpp:200-213, CHWN) and conv_gemm (conv.cpp:306-332,
+ * NCHW): implicit-GEMM convolution on tcgen05 tensor cores, output in the
+ * input's layout.  filters are (c_o, c_i, f_h, f_w) (tensor.hpp:77-103). */
+lcnn_status lcnn_conv_forward(const float* src, const float* filters,
+                              float* dst, uint32_t n, uint32_t c_i, uint32_t h,
+                              uint32_t w, int layout, uint32_t c_o,
+                              uint32_t f_h, uint32_t f_w, uint32_t stride,
+                              uint32_t pad, int precision, void* d_workspace,
+                              size_t workspace_bytes, void* stream);
+
+/* == gemm_blocked (conv.cpp:252-304) / fc_forward (softmax.cpp:182-184):
+ * c (m x n) = a (m x k) * b (k x n), all row-major fp32. */
+lcnn_status lcnn_gemm(const float* a, const float* b, float* c, uint64_t m,
+                      uint64_t n, uint64_t k, int precision, void* stream);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* LCNN_CUDA_H_ */

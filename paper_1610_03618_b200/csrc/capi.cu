@@ -1,0 +1,348 @@
+// C ABI (include/lcnn_cuda.h): host-side validation with the reference's
+// rules and messages, analytic access/pass reports, kernel dispatch.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "../../include/lcnn_cuda.h"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+lcnn_status fail(lcnn_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+lcnn_status ok() {
+  g_last_error.clear();
+  return LCNN_OK;
+}
+
+lcnn_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(LCNN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+bool valid_layout(int l) { return l >= LCNN_NCHW && l <= LCNN_HWCN; }
+
+// checked_volume (tensor.cpp:16-29)
+lcnn_status check_volume(uint32_t n, uint32_t c, uint32_t h, uint32_t w, const char* what) {
+  if (n == 0 || c == 0 || h == 0 || w == 0)
+    return fail(LCNN_ESHAPE, std::string(what) + ": all dims must be >= 1");
+  const uint64_t v = uint64_t{n} * c * uint64_t{h} * w;
+  if (v > 0xffffffffull) return fail(LCNN_ESHAPE, std::string(what) + ": dim product overflows");
+  return LCNN_OK;
+}
+
+bool power_of_two(uint32_t v) { return v != 0 && (v & (v - 1)) == 0; }
+
+// check_window (pool.cpp:19-26)
+lcnn_status check_window(uint32_t h, uint32_t w, uint32_t wh, uint32_t ww, uint32_t s) {
+  if (wh < 1 || ww < 1 || s < 1) return fail(LCNN_ESHAPE, "pool: window and stride must be >= 1");
+  if (wh > h || ww > w) return fail(LCNN_ESHAPE, "pool: window larger than image");
+  return LCNN_OK;
+}
+
+// covered_extent (pool.cpp:29-33)
+uint64_t covered_extent(uint32_t out, uint32_t win, uint32_t stride) {
+  if (stride >= win) return uint64_t{out} * win;
+  return uint64_t{stride} * (out - 1) + win;
+}
+
+void plain_report(lcnn_access_report* r, uint32_t n, uint32_t c, uint32_t ho, uint32_t wo,
+                  uint32_t wh, uint32_t ww, uint32_t s) {
+  if (!r) return;
+  const uint64_t outs = uint64_t{n} * c * ho * wo;
+  r->output_stores = outs;
+  r->input_loads = outs * wh * ww;
+  r->distinct_inputs = uint64_t{n} * c * covered_extent(ho, wh, s) * covered_extent(wo, ww, s);
+}
+
+// union-load formula of pool_coarsened (pool.cpp:216-236)
+void coarsened_report(lcnn_access_report* r, uint32_t n, uint32_t c, uint32_t ho, uint32_t wo,
+                      uint32_t wh, uint32_t ww, uint32_t s, uint32_t fh, uint32_t fw) {
+  if (!r) return;
+  uint64_t total = 0;
+  for (uint32_t oh0 = 0; oh0 < ho; oh0 += fh) {
+    const uint32_t bh = (fh < ho - oh0) ? fh : ho - oh0;
+    for (uint32_t ow0 = 0; ow0 < wo; ow0 += fw) {
+      const uint32_t bw = (fw < wo - ow0) ? fw : wo - ow0;
+      total += uint64_t{s * (bh - 1) + wh} * (s * (bw - 1) + ww);
+    }
+  }
+  r->input_loads = total * n * c;
+  r->output_stores = uint64_t{n} * c * ho * wo;
+  r->distinct_inputs = uint64_t{n} * c * covered_extent(ho, wh, s) * covered_extent(wo, ww, s);
+}
+
+lcnn_status pool_common(const float* src, float* dst, uint32_t n, uint32_t c, uint32_t h,
+                        uint32_t w, uint32_t wh, uint32_t ww, uint32_t s, int mode,
+                        uint32_t* ho, uint32_t* wo) {
+  if (!src || !dst) return fail(LCNN_EINVAL, "pool: null tensor pointer");
+  if (mode != LCNN_POOL_MAX && mode != LCNN_POOL_AVG) return fail(LCNN_EINVAL, "pool: bad mode");
+  lcnn_status st = check_volume(n, c, h, w, "Tensor4D");
+  if (st != LCNN_OK) return st;
+  st = check_window(h, w, wh, ww, s);
+  if (st != LCNN_OK) return st;
+  *ho = (h - wh) / s + 1;  // pool_output_extents (pool.cpp:44-47)
+  *wo = (w - ww) / s + 1;
+  return LCNN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lcnn_abi_version(void) { return LCNN_ABI_VERSION; }
+
+const char* lcnn_last_error(void) { return g_last_error.c_str(); }
+
+const char* lcnn_status_name(int status) {
+  switch (status) {
+    case LCNN_OK: return "ok";
+    case LCNN_ESHAPE: return "ShapeError";
+    case LCNN_EINDEX: return "IndexError";
+    case LCNN_ELAYOUT: return "LayoutError";
+    case LCNN_EPLAN: return "PlanError";
+    case LCNN_EFORMAT: return "FormatError";
+    case LCNN_EDOMAIN: return "DomainError";
+    case LCNN_EUNSUPPORTED: return "UnsupportedError";
+    case LCNN_EVALIDATION: return "ValidationError";
+    case LCNN_ECALIBRATION: return "CalibrationError";
+    case LCNN_ECUDA: return "CudaError";
+    case LCNN_EINVAL: return "InvalidArgument";
+    default: return "unknown";
+  }
+}
+
+int lcnn_device_ok(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  int dev = 0, major = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+    return 0;
+  return major == 10 ? 1 : 0;
+}
+
+int lcnn_flattenable_pair(int src, int dst) {
+  return (src == LCNN_CHWN && dst == LCNN_NCHW) || (src == LCNN_NCHW && dst == LCNN_CHWN);
+}
+
+lcnn_status lcnn_transform_naive(const float* src, float* dst, uint32_t n, uint32_t c,
+                                 uint32_t h, uint32_t w, int src_layout, int dst_layout,
+                                 void* stream) {
+  if (!src || !dst) return fail(LCNN_EINVAL, "transform: null tensor pointer");
+  if (!valid_layout(src_layout) || !valid_layout(dst_layout))
+    return fail(LCNN_EINVAL, "transform: bad layout code");
+  lcnn_status st = check_volume(n, c, h, w, "Tensor4D");
+  if (st != LCNN_OK) return st;
+  cudaError_t e = lcnn_impl::launch_permute4d(src, dst, n, c, h, w, src_layout, dst_layout,
+                                              S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "transform_naive");
+  return ok();
+}
+
+lcnn_status lcnn_transform_tiled(const float* src, float* dst, uint32_t n, uint32_t c,
+                                 uint32_t h, uint32_t w, int src_layout, int dst_layout,
+                                 uint32_t tile, int wide_copy, void* stream) {
+  if (!src || !dst) return fail(LCNN_EINVAL, "transform: null tensor pointer");
+  if (!valid_layout(src_layout) || !valid_layout(dst_layout))
+    return fail(LCNN_EINVAL, "transform: bad layout code");
+  lcnn_status st = check_volume(n, c, h, w, "Tensor4D");
+  if (st != LCNN_OK) return st;
+  // validate_plan (layout.cpp:13-26)
+  if (!lcnn_flattenable_pair(src_layout, dst_layout))
+    return fail(LCNN_EPLAN,
+                "transform_tiled: unsupported layout pair (only CHWN<->NCHW flattens)");
+  if (!power_of_two(tile) || tile < 8 || tile > 128)
+    return fail(LCNN_EPLAN, "transform_tiled: tile must be a power of two in [8, 128]");
+  if (wide_copy && n < 64) return fail(LCNN_EPLAN, "transform_tiled: wide copy requires N >= 64");
+  const uint64_t flat = uint64_t{c} * h * w;
+  // CHWN: [CHW][N] -> [N][CHW];  NCHW: [N][CHW] -> [CHW][N]
+  const uint64_t rows = src_layout == LCNN_CHWN ? flat : n;
+  const uint64_t cols = src_layout == LCNN_CHWN ? n : flat;
+  cudaError_t e = lcnn_impl::launch_transpose2d(src, dst, rows, cols, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "transform_tiled");
+  return ok();
+}
+
+lcnn_status lcnn_transform(const float* src, float* dst, uint32_t n, uint32_t c, uint32_t h,
+                           uint32_t w, int src_layout, int dst_layout, void* stream) {
+  if (!src || !dst) return fail(LCNN_EINVAL, "transform: null tensor pointer");
+  if (!valid_layout(src_layout) || !valid_layout(dst_layout))
+    return fail(LCNN_EINVAL, "transform: bad layout code");
+  // make_plan (layout.cpp:122-136) + dispatch (layout.cpp:138-144)
+  if (lcnn_flattenable_pair(src_layout, dst_layout))
+    return lcnn_transform_tiled(src, dst, n, c, h, w, src_layout, dst_layout, 32, n >= 64, stream);
+  if (src_layout == dst_layout) {
+    lcnn_status st = check_volume(n, c, h, w, "Tensor4D");
+    if (st != LCNN_OK) return st;
+    cudaError_t e = cudaMemcpyAsync(dst, src, uint64_t{n} * c * h * w * sizeof(float),
+                                    cudaMemcpyDeviceToDevice, S(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "transform");
+    return ok();
+  }
+  return lcnn_transform_naive(src, dst, n, c, h, w, src_layout, dst_layout, stream);
+}
+
+lcnn_status lcnn_pool_output_extents(uint32_t h, uint32_t w, uint32_t win_h, uint32_t win_w,
+                                     uint32_t stride, uint32_t* h_out, uint32_t* w_out) {
+  if (!h_out || !w_out) return fail(LCNN_EINVAL, "pool: null output pointer");
+  lcnn_status st = check_window(h, w, win_h, win_w, stride);
+  if (st != LCNN_OK) return st;
+  *h_out = (h - win_h) / stride + 1;
+  *w_out = (w - win_w) / stride + 1;
+  return ok();
+}
+
+lcnn_status lcnn_pool_layout(const float* src, float* dst, uint32_t n, uint32_t c, uint32_t h,
+                             uint32_t w, int layout, uint32_t win_h, uint32_t win_w,
+                             uint32_t stride, int mode, lcnn_access_report* report,
+                             void* stream) {
+  uint32_t ho = 0, wo = 0;
+  lcnn_status st = pool_common(src, dst, n, c, h, w, win_h, win_w, stride, mode, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  if (layout != LCNN_CHWN && layout != LCNN_NCHW)
+    return fail(LCNN_ELAYOUT, "pool_layout: only CHWN and NCHW kernels exist");
+  lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
+                        mode == LCNN_POOL_AVG, 1, 1};
+  cudaError_t e = layout == LCNN_CHWN ? lcnn_impl::launch_pool_chwn(a, S(stream))
+                                      : lcnn_impl::launch_pool_nchw(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pool_layout");
+  plain_report(report, n, c, ho, wo, win_h, win_w, stride);
+  return ok();
+}
+
+lcnn_status lcnn_pool_coarsened(const float* src, float* dst, uint32_t n, uint32_t c,
+                                uint32_t h, uint32_t w, int layout, uint32_t win_h,
+                                uint32_t win_w, uint32_t stride, int mode, uint32_t fh,
+                                uint32_t fw, lcnn_access_report* report, void* stream) {
+  uint32_t ho = 0, wo = 0;
+  lcnn_status st = pool_common(src, dst, n, c, h, w, win_h, win_w, stride, mode, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  // pool.cpp:182-191, same order as the reference
+  if (fh < 1 || fw < 1) return fail(LCNN_EPLAN, "pool_coarsened: factors must be >= 1");
+  if (uint64_t{fh} * fw > 64)
+    return fail(LCNN_EPLAN, "pool_coarsened: fh*fw exceeds accumulator cap of 64");
+  if (layout != LCNN_CHWN) return fail(LCNN_ELAYOUT, "pool_coarsened: input must be CHWN");
+  lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
+                        mode == LCNN_POOL_AVG, fh, fw};
+  cudaError_t e = lcnn_impl::launch_pool_chwn(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pool_coarsened");
+  coarsened_report(report, n, c, ho, wo, win_h, win_w, stride, fh, fw);
+  return ok();
+}
+
+lcnn_status lcnn_pool_coarsened_nchw(const float* src, float* dst, uint32_t n, uint32_t c,
+                                     uint32_t h, uint32_t w, uint32_t win_h, uint32_t win_w,
+                                     uint32_t stride, int mode, uint32_t fh, uint32_t fw,
+                                     lcnn_access_report* report, void* stream) {
+  uint32_t ho = 0, wo = 0;
+  lcnn_status st = pool_common(src, dst, n, c, h, w, win_h, win_w, stride, mode, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  if (fh < 1 || fw < 1) return fail(LCNN_EPLAN, "pool_coarsened: factors must be >= 1");
+  if (uint64_t{fh} * fw > 64)
+    return fail(LCNN_EPLAN, "pool_coarsened: fh*fw exceeds accumulator cap of 64");
+  lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
+                        mode == LCNN_POOL_AVG, fh, fw};
+  cudaError_t e = lcnn_impl::launch_pool_nchw(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pool_coarsened_nchw");
+  coarsened_report(report, n, c, ho, wo, win_h, win_w, stride, fh, fw);
+  return ok();
+}
+
+lcnn_status lcnn_pool_oracle(const float* src, float* dst, uint32_t n, uint32_t c, uint32_t h,
+                             uint32_t w, int layout, uint32_t win_h, uint32_t win_w,
+                             uint32_t stride, int mode, void* stream) {
+  uint32_t ho = 0, wo = 0;
+  lcnn_status st = pool_common(src, dst, n, c, h, w, win_h, win_w, stride, mode, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  if (!valid_layout(layout)) return fail(LCNN_EINVAL, "pool_oracle: bad layout code");
+  // layout_strides (tensor.cpp:55-85)
+  uint64_t sn, sc, sh, sw;
+  switch (layout) {
+    case LCNN_NCHW: sw = 1; sh = w; sc = uint64_t{h} * w; sn = uint64_t{c} * h * w; break;
+    case LCNN_CHWN: sn = 1; sw = n; sh = uint64_t{w} * n; sc = uint64_t{h} * w * n; break;
+    case LCNN_NHWC: sc = 1; sw = c; sh = uint64_t{w} * c; sn = uint64_t{h} * w * c; break;
+    default: sn = 1; sc = n; sw = uint64_t{c} * n; sh = uint64_t{w} * c * n; break;
+  }
+  lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
+                        mode == LCNN_POOL_AVG, 1, 1};
+  cudaError_t e = lcnn_impl::launch_pool_oracle(a, sn, sc, sh, sw, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pool_oracle");
+  return ok();
+}
+
+lcnn_status lcnn_softmax_fused(const float* src, float* dst, uint32_t rows, uint32_t cols,
+                               uint32_t local_buffer_limit, int* d_nonfinite,
+                               lcnn_pass_report* report, void* stream) {
+  if (rows < 1 || cols < 1) return fail(LCNN_ESHAPE, "softmax: empty matrix");
+  if (!src || !dst) return fail(LCNN_EINVAL, "softmax: null matrix pointer");
+  if (uint64_t{rows} * cols > 0xffffffffull)
+    return fail(LCNN_ESHAPE, "softmax: matrix too large");
+  cudaError_t e = cudaSuccess;
+  if (d_nonfinite) {
+    e = cudaMemsetAsync(d_nonfinite, 0, sizeof(int), S(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "softmax_fused");
+  }
+  e = lcnn_impl::launch_softmax_fused(src, dst, rows, cols, d_nonfinite, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "softmax_fused");
+  if (report) {  // softmax.cpp:142, 178
+    report->materializations = 0;
+    report->full_matrix_sweeps = cols <= local_buffer_limit ? 2 : 5;
+  }
+  return ok();
+}
+
+size_t lcnn_softmax_reference_scratch_bytes(uint32_t rows, uint32_t cols) {
+  return (2 * uint64_t{rows} + 2 * uint64_t{rows} * cols) * sizeof(float);
+}
+
+lcnn_status lcnn_softmax_reference(const float* src, float* dst, uint32_t rows, uint32_t cols,
+                                   void* d_scratch, size_t scratch_bytes, int* d_nonfinite,
+                                   lcnn_pass_report* report, void* stream) {
+  if (rows < 1 || cols < 1) return fail(LCNN_ESHAPE, "softmax: empty matrix");
+  if (!src || !dst || !d_scratch) return fail(LCNN_EINVAL, "softmax: null pointer");
+  if (uint64_t{rows} * cols > 0xffffffffull)
+    return fail(LCNN_ESHAPE, "softmax: matrix too large");
+  if (scratch_bytes < lcnn_softmax_reference_scratch_bytes(rows, cols))
+    return fail(LCNN_EINVAL, "softmax_reference: scratch too small");
+  cudaError_t e = cudaSuccess;
+  if (d_nonfinite) {
+    e = cudaMemsetAsync(d_nonfinite, 0, sizeof(int), S(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "softmax_reference");
+  }
+  e = lcnn_impl::launch_softmax_five_pass(src, dst, rows, cols, static_cast<float*>(d_scratch),
+                                          d_nonfinite, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "softmax_reference");
+  if (report) {  // softmax.cpp:61-94
+    report->materializations = 3;
+    report->full_matrix_sweeps = 8;
+  }
+  return ok();
+}
+
+lcnn_status lcnn_conv_output_extents(uint32_t h, uint32_t w, uint32_t f_h, uint32_t f_w,
+                                     uint32_t stride, uint32_t pad, uint32_t* h_out,
+                                     uint32_t* w_out) {
+  if (!h_out || !w_out) return fail(LCNN_EINVAL, "conv: null output pointer");
+  if (stride < 1) return fail(LCNN_ESHAPE, "conv: stride must be >= 1");  // conv.cpp:25
+  const int64_t span_h = int64_t{h} + 2 * int64_t{pad} - f_h;
+  const int64_t span_w = int64_t{w} + 2 * int64_t{pad} - f_w;
+  if (span_h < 0 || span_w < 0) return fail(LCNN_ESHAPE, "conv: window larger than padded input");
+  *h_out = static_cast<uint32_t>(span_h / stride + 1);
+  *w_out = static_cast<uint32_t>(span_w / stride + 1);
+  return ok();
+}
+
+}  // extern "C"

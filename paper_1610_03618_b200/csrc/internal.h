@@ -1,0 +1,60 @@
+// Host-side launcher interface between the C ABI (capi.cu) and the kernel
+// translation units.  Launchers assume validated parameters and return the
+// cudaError_t of the launch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lcnn_impl {
+
+// --- transform.cu -------------------------------------------------------
+// dst[C][R] = transpose(src[R][C]), both row-major fp32.
+cudaError_t launch_transpose2d(const float* src, float* dst, uint64_t rows,
+                               uint64_t cols, cudaStream_t s);
+// Generic 4D permutation between any two of the four layout codes.
+cudaError_t launch_permute4d(const float* src, float* dst, uint32_t n,
+                             uint32_t c, uint32_t h, uint32_t w, int src_layout,
+                             int dst_layout, cudaStream_t s);
+
+// --- pool.cu ------------------------------------------------------------
+struct PoolArgs {
+  const float* src;
+  float* dst;
+  uint32_t n, c, h, w;      // logical input extents
+  uint32_t ho, wo;          // output extents
+  uint32_t win_h, win_w, stride;
+  bool avg;
+  uint32_t fh, fw;          // coarsening factors (1,1 = plain kernel)
+};
+cudaError_t launch_pool_chwn(const PoolArgs& a, cudaStream_t s);
+cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t s);
+// fp64 oracle kernel: any layout in (strides in elements), NCHW out.
+cudaError_t launch_pool_oracle(const PoolArgs& a, uint64_t sn, uint64_t sc,
+                               uint64_t sh, uint64_t sw, cudaStream_t s);
+
+// --- softmax.cu ---------------------------------------------------------
+cudaError_t launch_softmax_fused(const float* src, float* dst, uint32_t rows,
+                                 uint32_t cols, int* flag, cudaStream_t s);
+cudaError_t launch_softmax_five_pass(const float* src, float* dst,
+                                     uint32_t rows, uint32_t cols,
+                                     float* scratch, int* flag,
+                                     cudaStream_t s);
+
+// --- conv.cu / gemm.cu ---------------------------------------------------
+struct ConvArgs {
+  const float* src;
+  const float* filters;
+  float* dst;
+  uint32_t n, ci, h, w;
+  uint32_t co, fh, fw, stride, pad;
+  uint32_t ho, wo;
+  int layout;  // LCNN_CHWN or LCNN_NCHW
+  int precision;
+  void* workspace;
+};
+cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s);
+cudaError_t launch_gemm(const float* a, const float* b, float* c, uint64_t m,
+                        uint64_t n, uint64_t k, int precision, cudaStream_t s);
+
+}  // namespace lcnn_impl

@@ -1,0 +1,552 @@
+// Max / average pooling in CHWN and NCHW on sm_100a.
+//
+// Reference: /root/reference/proj/src/pool.cpp
+//   pool_plain CHWN   :98-134   lane buffer over the contiguous batch
+//   pool_plain NCHW   :135-163  window loop per output
+//   pool_coarsened    :178-270  fh x fw outputs per task, union staged once
+//   pool_oracle       :49-84    fp64 ground truth, NCHW out
+// Paper: PAPER.md Sec. 5 (coalescing along the fastest dimension; register
+// coarsening of overlapped windows, auto-tuned factors).
+//
+// Bit-exactness contract (checked against the CPU reference by memcmp):
+//   max : acc = (acc < v) ? v : acc, acc from -inf, taps in (y,x) order;
+//   avg : fp32 adds from 0.0f in (y,x) order (no FMA contraction), then CHWN
+//         multiplies by 1.0f/(wh*ww) (pool.cpp:104,129,261) while NCHW
+//         divides by float(wh*ww) (pool.cpp:158).
+// Register coarsening never changes a single output's tap order: union rows
+// are visited top to bottom and each row left to right, so every output sees
+// its own window in (y,x) order.
+//
+// CHWN kernel: lanes run along N with 128-bit loads (4 images per thread), so
+// one warp instruction reads 512 contiguous bytes of a tap; each thread owns
+// an FH x FW block of outputs and loads the receptive-field union of that
+// block exactly once (UH x UW float4 loads for FH*FW outputs).
+// NCHW kernel: a CTA stages a contiguous band of input rows of one (n,c)
+// plane in shared memory (row-major, so the global read is one contiguous
+// span), then threads compute FW consecutive outputs each from shared memory
+// and write contiguous output rows.
+#include <float.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace lcnn_dev {
+
+struct ChwnGeom {
+  const float* src;
+  float* dst;
+  uint32_t N, H, W, Ho, Wo;
+  uint32_t nbh, nbw;   // output blocks along h and w
+  FastDiv div_nv, div_nbw, div_nbh;
+  uint32_t total;      // threads = C * nbh * nbw * NV
+  float inv;           // 1.0f / (wh*ww) (average only)
+  uint32_t wh, ww, s;  // runtime window (generic kernel only)
+};
+
+template <int VEC>
+__device__ __forceinline__ typename Vec<VEC>::T load_tap(const float* p) {
+  if constexpr (VEC == 4) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+  } else {
+    return __ldg(p);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_out(float* p, typename Vec<VEC>::T v) {
+  if constexpr (VEC == 4) {
+    stg_stream(reinterpret_cast<float4*>(p), v);
+  } else {
+    stg_stream(p, v);
+  }
+}
+
+template <int WH, int WW, int S, int FH, int FW, int VEC, bool AVG>
+__global__ void __launch_bounds__(kThreads)
+    pool_chwn_kernel(ChwnGeom g) {
+  using T = typename Vec<VEC>::T;
+  constexpr int UH = S * (FH - 1) + WH;
+  constexpr int UW = S * (FW - 1) + WW;
+  const uint32_t gid = blockIdx.x * kThreads + threadIdx.x;
+  if (gid >= g.total) return;
+  uint32_t item, nv, t, bw, bh, c;
+  g.div_nv.divmod(gid, item, nv);
+  g.div_nbw.divmod(item, t, bw);
+  g.div_nbh.divmod(t, c, bh);
+  const uint32_t oh0 = bh * FH, ow0 = bw * FW;
+  const uint32_t ih0 = oh0 * S, iw0 = ow0 * S;
+  const uint64_t N = g.N;
+  const float* base =
+      g.src + ((static_cast<uint64_t>(c) * g.H + ih0) * g.W + iw0) * N + nv * VEC;
+
+  T acc[FH][FW];
+#pragma unroll
+  for (int by = 0; by < FH; ++by)
+#pragma unroll
+    for (int bx = 0; bx < FW; ++bx) acc[by][bx] = splat<VEC>(AVG ? 0.0f : -INFINITY);
+
+#pragma unroll
+  for (int y = 0; y < UH; ++y) {
+    if (ih0 + y >= g.H) break;  // rows that only feed absent outputs
+    T v[UW];
+#pragma unroll
+    for (int x = 0; x < UW; ++x) {
+      v[x] = splat<VEC>(AVG ? 0.0f : -INFINITY);
+      if (iw0 + x < g.W) v[x] = load_tap<VEC>(base + (static_cast<uint64_t>(y) * g.W + x) * N);
+    }
+#pragma unroll
+    for (int by = 0; by < FH; ++by) {
+      const int dy = y - by * S;
+      if (dy < 0 || dy >= WH) continue;  // resolved at compile time
+#pragma unroll
+      for (int bx = 0; bx < FW; ++bx) {
+#pragma unroll
+        for (int xx = 0; xx < WW; ++xx) {
+          if constexpr (AVG) {
+            acc[by][bx] = add_tap(acc[by][bx], v[bx * S + xx]);
+          } else {
+            acc[by][bx] = max_tap(acc[by][bx], v[bx * S + xx]);
+          }
+        }
+      }
+    }
+  }
+
+  float* obase = g.dst + ((static_cast<uint64_t>(c) * g.Ho + oh0) * g.Wo + ow0) * N + nv * VEC;
+#pragma unroll
+  for (int by = 0; by < FH; ++by) {
+#pragma unroll
+    for (int bx = 0; bx < FW; ++bx) {
+      if (oh0 + by < g.Ho && ow0 + bx < g.Wo) {
+        T o = acc[by][bx];
+        if constexpr (AVG) o = scale_out(o, g.inv);
+        store_out<VEC>(obase + (static_cast<uint64_t>(by) * g.Wo + bx) * N, o);
+      }
+    }
+  }
+}
+
+// Any window / stride, one output per thread (plain semantics).
+template <int VEC, bool AVG>
+__global__ void __launch_bounds__(kThreads) pool_chwn_generic_kernel(ChwnGeom g) {
+  using T = typename Vec<VEC>::T;
+  const uint32_t gid = blockIdx.x * kThreads + threadIdx.x;
+  if (gid >= g.total) return;
+  uint32_t item, nv, t, ow, oh, c;
+  g.div_nv.divmod(gid, item, nv);
+  g.div_nbw.divmod(item, t, ow);
+  g.div_nbh.divmod(t, c, oh);
+  const uint64_t N = g.N;
+  const float* base =
+      g.src + ((static_cast<uint64_t>(c) * g.H + oh * g.s) * g.W + ow * g.s) * N + nv * VEC;
+  T acc = splat<VEC>(AVG ? 0.0f : -INFINITY);
+  for (uint32_t y = 0; y < g.wh; ++y) {
+    for (uint32_t x = 0; x < g.ww; ++x) {
+      const T v = load_tap<VEC>(base + (static_cast<uint64_t>(y) * g.W + x) * N);
+      if constexpr (AVG) acc = add_tap(acc, v); else acc = max_tap(acc, v);
+    }
+  }
+  if constexpr (AVG) acc = scale_out(acc, g.inv);
+  store_out<VEC>(g.dst + ((static_cast<uint64_t>(c) * g.Ho + oh) * g.Wo + ow) * N + nv * VEC, acc);
+}
+
+// ---------------------------------------------------------------- NCHW ----
+struct NchwGeom {
+  const float* src;
+  float* dst;
+  uint32_t H, W, Ho, Wo;
+  uint32_t band;       // output rows per CTA
+  uint32_t nbands;     // bands per plane
+  uint32_t nbw;        // output column blocks (of FW) per row
+  FastDiv div_nbw;
+  float divisor;       // float(wh*ww) (average only)
+  uint32_t wh, ww, s;  // runtime window (generic kernel only)
+};
+
+// Stage `count` contiguous floats of global memory into shared memory.  The
+// span is placed at smem offset (gp/4 mod 4) so that every 16-byte global
+// vector lands on a 16-byte shared slot (conflict-free 128-bit stores); the
+// caller indexes the staged span from the returned offset.
+__device__ __forceinline__ uint32_t stage_span(float* sm, const float* gp, uint32_t count) {
+  const uint32_t mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(gp) >> 2) & 3u);
+  uint32_t head = (4u - mis) & 3u;
+  if (head > count) head = count;
+  if (threadIdx.x < head) sm[mis + threadIdx.x] = __ldg(gp + threadIdx.x);
+  const uint32_t nvec = (count - head) >> 2;
+  const float4* g4 = reinterpret_cast<const float4*>(gp + head);
+  float4* s4 = reinterpret_cast<float4*>(sm + mis + head);  // mis+head is 0 or 4
+  uint32_t i = threadIdx.x;
+  for (; i + 3 * kThreads < nvec; i += 4 * kThreads) {
+    const float4 a = ldg_stream(g4 + i);
+    const float4 b = ldg_stream(g4 + i + kThreads);
+    const float4 c = ldg_stream(g4 + i + 2 * kThreads);
+    const float4 d = ldg_stream(g4 + i + 3 * kThreads);
+    s4[i] = a;
+    s4[i + kThreads] = b;
+    s4[i + 2 * kThreads] = c;
+    s4[i + 3 * kThreads] = d;
+  }
+  for (; i < nvec; i += kThreads) s4[i] = ldg_stream(g4 + i);
+  const uint32_t done = head + 4 * nvec;
+  if (threadIdx.x < count - done) sm[mis + done + threadIdx.x] = __ldg(gp + done + threadIdx.x);
+  return mis;
+}
+
+// Coarsening runs vertically first: a thread owns FH outputs of one column
+// block, so lanes still walk consecutive output columns (stride-S shared
+// reads) while the union rows shared by vertically adjacent windows are read
+// once.  FW > 1 widens the block horizontally (more bank conflicts; offered
+// for the auto-tuner to measure).
+template <int WH, int WW, int S, int FH, int FW, bool AVG>
+__global__ void __launch_bounds__(kThreads) pool_nchw_kernel(NchwGeom g) {
+  extern __shared__ float sm[];
+  constexpr int UH = S * (FH - 1) + WH;
+  constexpr int UW = S * (FW - 1) + WW;
+  const uint32_t plane = blockIdx.x / g.nbands;
+  const uint32_t b = blockIdx.x - plane * g.nbands;
+  const uint32_t oh_begin = b * g.band;
+  const uint32_t oh_cnt = min(g.band, g.Ho - oh_begin);
+  const uint32_t ih_begin = oh_begin * S;
+  const uint32_t ih_cnt = min(g.H - ih_begin, (oh_cnt - 1) * S + WH);
+  const uint64_t hw = static_cast<uint64_t>(g.H) * g.W;
+  const uint32_t off =
+      stage_span(sm, g.src + plane * hw + static_cast<uint64_t>(ih_begin) * g.W, ih_cnt * g.W);
+  __syncthreads();
+
+  float* obase = g.dst + plane * static_cast<uint64_t>(g.Ho) * g.Wo +
+                 static_cast<uint64_t>(oh_begin) * g.Wo;
+  const uint32_t nrb = (oh_cnt + FH - 1) / FH;
+  const uint32_t items = nrb * g.nbw;
+  for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+    uint32_t rb, bw;
+    g.div_nbw.divmod(it, rb, bw);
+    const uint32_t r0 = rb * FH, ow0 = bw * FW;
+    const float* win = sm + off + (r0 * S) * g.W + ow0 * S;
+    float acc[FH][FW];
+#pragma unroll
+    for (int by = 0; by < FH; ++by)
+#pragma unroll
+      for (int bx = 0; bx < FW; ++bx) acc[by][bx] = AVG ? 0.0f : -INFINITY;
+#pragma unroll
+    for (int y = 0; y < UH; ++y) {
+      if (r0 * S + y >= ih_cnt) break;  // rows that only feed absent outputs
+      float v[UW];
+#pragma unroll
+      for (int x = 0; x < UW; ++x) {
+        v[x] = (FW == 1 || ow0 * S + x < g.W) ? win[y * g.W + x] : 0.0f;
+      }
+#pragma unroll
+      for (int by = 0; by < FH; ++by) {
+        const int dy = y - by * S;
+        if (dy < 0 || dy >= WH) continue;  // resolved at compile time
+#pragma unroll
+        for (int bx = 0; bx < FW; ++bx)
+#pragma unroll
+          for (int xx = 0; xx < WW; ++xx) {
+            if constexpr (AVG) acc[by][bx] = add_tap(acc[by][bx], v[bx * S + xx]);
+            else acc[by][bx] = max_tap(acc[by][bx], v[bx * S + xx]);
+          }
+      }
+    }
+#pragma unroll
+    for (int by = 0; by < FH; ++by) {
+      if (r0 + by >= oh_cnt) break;
+      float* orow = obase + static_cast<uint64_t>(r0 + by) * g.Wo + ow0;
+#pragma unroll
+      for (int bx = 0; bx < FW; ++bx) {
+        if (ow0 + bx < g.Wo) {
+          const float o = AVG ? divide_out(acc[by][bx], g.divisor) : acc[by][bx];
+          stg_stream(orow + bx, o);
+        }
+      }
+    }
+  }
+}
+
+// Runtime window, staged the same way, one output per thread.
+template <bool AVG>
+__global__ void __launch_bounds__(kThreads) pool_nchw_generic_kernel(NchwGeom g) {
+  extern __shared__ float sm[];
+  const uint32_t plane = blockIdx.x / g.nbands;
+  const uint32_t b = blockIdx.x - plane * g.nbands;
+  const uint32_t oh_begin = b * g.band;
+  const uint32_t oh_cnt = min(g.band, g.Ho - oh_begin);
+  const uint32_t ih_begin = oh_begin * g.s;
+  const uint32_t ih_cnt = min(g.H - ih_begin, (oh_cnt - 1) * g.s + g.wh);
+  const uint64_t hw = static_cast<uint64_t>(g.H) * g.W;
+  const uint32_t off =
+      stage_span(sm, g.src + plane * hw + static_cast<uint64_t>(ih_begin) * g.W, ih_cnt * g.W);
+  __syncthreads();
+  float* obase = g.dst + plane * static_cast<uint64_t>(g.Ho) * g.Wo +
+                 static_cast<uint64_t>(oh_begin) * g.Wo;
+  const uint32_t items = oh_cnt * g.Wo;
+  for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+    uint32_t r, ow;
+    g.div_nbw.divmod(it, r, ow);
+    const float* win = sm + off + (r * g.s) * g.W + ow * g.s;
+    float acc = AVG ? 0.0f : -INFINITY;
+    for (uint32_t y = 0; y < g.wh; ++y)
+      for (uint32_t x = 0; x < g.ww; ++x) {
+        const float v = win[y * g.W + x];
+        if constexpr (AVG) acc = add_tap(acc, v); else acc = max_tap(acc, v);
+      }
+    stg_stream(obase + static_cast<uint64_t>(r) * g.Wo + ow, AVG ? divide_out(acc, g.divisor) : acc);
+  }
+}
+
+// Unstaged NCHW fallback for rows too wide to stage (W*wh*4 > smem budget).
+template <bool AVG>
+__global__ void __launch_bounds__(kThreads)
+    pool_nchw_direct_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                            uint64_t total, uint32_t H, uint32_t W, uint32_t Ho,
+                            uint32_t Wo, uint32_t wh, uint32_t ww, uint32_t s,
+                            float divisor) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * kThreads) {
+    const uint64_t ow = i % Wo;
+    const uint64_t t = i / Wo;
+    const uint64_t oh = t % Ho;
+    const uint64_t plane = t / Ho;
+    const float* win = src + (plane * H + oh * s) * W + ow * s;
+    float acc = AVG ? 0.0f : -INFINITY;
+    for (uint32_t y = 0; y < wh; ++y)
+      for (uint32_t x = 0; x < ww; ++x) {
+        const float v = __ldg(win + static_cast<uint64_t>(y) * W + x);
+        if constexpr (AVG) acc = add_tap(acc, v); else acc = max_tap(acc, v);
+      }
+    dst[i] = AVG ? divide_out(acc, divisor) : acc;
+  }
+}
+
+// fp64 oracle (pool.cpp:49-84): any layout in via strides, NCHW out.
+__global__ void pool_oracle_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                   uint32_t N, uint32_t C, uint32_t Ho, uint32_t Wo,
+                                   uint64_t sn, uint64_t sc, uint64_t sh, uint64_t sw,
+                                   uint32_t wh, uint32_t ww, uint32_t s, bool avg) {
+  const uint64_t total = static_cast<uint64_t>(N) * C * Ho * Wo;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t ow = i % Wo;
+    uint64_t t = i / Wo;
+    const uint64_t oh = t % Ho;
+    t /= Ho;
+    const uint64_t c = t % C;
+    const uint64_t n = t / C;
+    const uint64_t base = n * sn + c * sc;
+    double sum = 0.0;
+    float best = src[base + oh * s * sh + ow * s * sw];
+    for (uint32_t y = 0; y < wh; ++y)
+      for (uint32_t x = 0; x < ww; ++x) {
+        const float v = src[base + (oh * s + y) * sh + (ow * s + x) * sw];
+        sum += v;
+        best = max_tap(best, v);
+      }
+    dst[i] = avg ? static_cast<float>(sum / wh / ww) : best;
+  }
+}
+
+}  // namespace lcnn_dev
+
+namespace lcnn_impl {
+
+using namespace lcnn_dev;
+
+namespace {
+
+constexpr uint32_t kStageBudget = 24 * 1024;  // bytes of input rows per CTA
+
+inline uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+template <int WH, int WW, int S, int FH, int FW, int VEC>
+cudaError_t chwn_launch(const ChwnGeom& g, bool avg, cudaStream_t st) {
+  const uint32_t blocks = cdiv(g.total, kThreads);
+  if (avg) pool_chwn_kernel<WH, WW, S, FH, FW, VEC, true><<<blocks, kThreads, 0, st>>>(g);
+  else pool_chwn_kernel<WH, WW, S, FH, FW, VEC, false><<<blocks, kThreads, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+template <int WH, int WW, int S, int VEC>
+bool chwn_dispatch_f(uint32_t fh, uint32_t fw, const ChwnGeom& g, bool avg,
+                     cudaStream_t st, cudaError_t* err) {
+#define LCNN_F(FH_, FW_)                                               \
+  if (fh == FH_ && fw == FW_) {                                        \
+    *err = chwn_launch<WH, WW, S, FH_, FW_, VEC>(g, avg, st);          \
+    return true;                                                       \
+  }
+  LCNN_F(1, 1) LCNN_F(1, 2) LCNN_F(1, 3) LCNN_F(1, 4)
+  LCNN_F(2, 1) LCNN_F(2, 2) LCNN_F(2, 3) LCNN_F(2, 4)
+  LCNN_F(3, 1) LCNN_F(3, 2) LCNN_F(3, 3) LCNN_F(3, 4)
+  LCNN_F(4, 1) LCNN_F(4, 2) LCNN_F(4, 3) LCNN_F(4, 4)
+#undef LCNN_F
+  return false;
+}
+
+template <int VEC>
+bool chwn_dispatch(const PoolArgs& a, const ChwnGeom& g, cudaStream_t st, cudaError_t* err) {
+  if (a.win_h == 2 && a.win_w == 2 && a.stride == 2)
+    return chwn_dispatch_f<2, 2, 2, VEC>(a.fh, a.fw, g, a.avg, st, err);
+  if (a.win_h == 3 && a.win_w == 3 && a.stride == 2)
+    return chwn_dispatch_f<3, 3, 2, VEC>(a.fh, a.fw, g, a.avg, st, err);
+  if (a.win_h == 3 && a.win_w == 3 && a.stride == 1)
+    return chwn_dispatch_f<3, 3, 1, VEC>(a.fh, a.fw, g, a.avg, st, err);
+  return false;
+}
+
+}  // namespace
+
+cudaError_t launch_pool_chwn(const PoolArgs& a, cudaStream_t st) {
+  const bool vec = (a.n % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.src) & 15u) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(a.dst) & 15u) == 0);
+  const uint32_t VEC = vec ? 4 : 1;
+  ChwnGeom g;
+  g.src = a.src;
+  g.dst = a.dst;
+  g.N = a.n;
+  g.H = a.h;
+  g.W = a.w;
+  g.Ho = a.ho;
+  g.Wo = a.wo;
+  g.inv = 1.0f / static_cast<float>(a.win_h * a.win_w);  // pool.cpp:104
+  g.wh = a.win_h;
+  g.ww = a.win_w;
+  g.s = a.stride;
+  const uint32_t nv = a.n / VEC;
+  g.div_nv = FastDiv(nv);
+
+  cudaError_t err = cudaSuccess;
+  // register-coarsened specialisations
+  g.nbh = cdiv(a.ho, a.fh);
+  g.nbw = cdiv(a.wo, a.fw);
+  g.div_nbw = FastDiv(g.nbw);
+  g.div_nbh = FastDiv(g.nbh);
+  g.total = a.c * g.nbh * g.nbw * nv;
+  if (g.total == 0) return cudaSuccess;
+  if (vec ? chwn_dispatch<4>(a, g, st, &err) : chwn_dispatch<1>(a, g, st, &err)) return err;
+
+  // generic: one output per thread, runtime window (same output bits)
+  g.nbh = a.ho;
+  g.nbw = a.wo;
+  g.div_nbw = FastDiv(g.nbw);
+  g.div_nbh = FastDiv(g.nbh);
+  g.total = a.c * a.ho * a.wo * nv;
+  const uint32_t blocks = cdiv(g.total, kThreads);
+  if (vec) {
+    if (a.avg) pool_chwn_generic_kernel<4, true><<<blocks, kThreads, 0, st>>>(g);
+    else pool_chwn_generic_kernel<4, false><<<blocks, kThreads, 0, st>>>(g);
+  } else {
+    if (a.avg) pool_chwn_generic_kernel<1, true><<<blocks, kThreads, 0, st>>>(g);
+    else pool_chwn_generic_kernel<1, false><<<blocks, kThreads, 0, st>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+namespace {
+
+template <int WH, int WW, int S, int FH, int FW>
+cudaError_t nchw_launch(const NchwGeom& g, uint32_t blocks, uint32_t smem, bool avg,
+                        cudaStream_t st) {
+  auto kern = avg ? pool_nchw_kernel<WH, WW, S, FH, FW, true>
+                  : pool_nchw_kernel<WH, WW, S, FH, FW, false>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<blocks, kThreads, smem, st>>>(g);
+  return cudaGetLastError();
+}
+
+template <int WH, int WW, int S>
+bool nchw_dispatch_f(uint32_t fh, uint32_t fw, const NchwGeom& g, uint32_t blocks,
+                     uint32_t smem, bool avg, cudaStream_t st, cudaError_t* err) {
+#define LCNN_F(FH_, FW_)                                                  \
+  if (fh == FH_ && fw == FW_) {                                           \
+    *err = nchw_launch<WH, WW, S, FH_, FW_>(g, blocks, smem, avg, st);    \
+    return true;                                                          \
+  }
+  LCNN_F(1, 1) LCNN_F(2, 1) LCNN_F(3, 1) LCNN_F(4, 1)
+  LCNN_F(1, 2) LCNN_F(2, 2) LCNN_F(3, 2) LCNN_F(4, 2)
+#undef LCNN_F
+  return false;
+}
+
+}  // namespace
+
+cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t st) {
+  const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
+  if (planes == 0 || a.ho == 0 || a.wo == 0) return cudaSuccess;
+  const uint64_t row_bytes = static_cast<uint64_t>(a.w) * 4;
+  // output rows per CTA so that the staged input band fits the budget
+  uint32_t band = 1;
+  if (static_cast<uint64_t>(a.win_h) * row_bytes <= kStageBudget) {
+    const uint64_t rows_fit = kStageBudget / row_bytes;  // >= win_h
+    band = static_cast<uint32_t>((rows_fit - a.win_h) / a.stride + 1);
+  }
+  if (band > a.ho) band = a.ho;
+  const uint64_t in_rows = static_cast<uint64_t>(band - 1) * a.stride + a.win_h;
+  const uint64_t smem = in_rows * row_bytes + 16;  // + alignment slack
+  if (smem > 200 * 1024) {
+    const uint64_t total = planes * a.ho * a.wo;
+    uint64_t blocks = (total + kThreads - 1) / kThreads;
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    const float div = static_cast<float>(a.win_h * a.win_w);
+    if (a.avg)
+      pool_nchw_direct_kernel<true><<<static_cast<uint32_t>(blocks), kThreads, 0, st>>>(
+          a.src, a.dst, total, a.h, a.w, a.ho, a.wo, a.win_h, a.win_w, a.stride, div);
+    else
+      pool_nchw_direct_kernel<false><<<static_cast<uint32_t>(blocks), kThreads, 0, st>>>(
+          a.src, a.dst, total, a.h, a.w, a.ho, a.wo, a.win_h, a.win_w, a.stride, div);
+    return cudaGetLastError();
+  }
+  NchwGeom g;
+  g.src = a.src;
+  g.dst = a.dst;
+  g.H = a.h;
+  g.W = a.w;
+  g.Ho = a.ho;
+  g.Wo = a.wo;
+  g.band = band;
+  g.nbands = cdiv(a.ho, band);
+  g.divisor = static_cast<float>(a.win_h * a.win_w);  // pool.cpp:158
+  g.wh = a.win_h;
+  g.ww = a.win_w;
+  g.s = a.stride;
+  const uint64_t blocks64 = planes * g.nbands;
+  if (blocks64 > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  const uint32_t blocks = static_cast<uint32_t>(blocks64);
+  const uint32_t smem32 = static_cast<uint32_t>(smem);
+
+  cudaError_t err = cudaSuccess;
+  g.nbw = cdiv(a.wo, a.fw);
+  g.div_nbw = FastDiv(g.nbw);
+  bool done = false;
+  if (a.win_h == 2 && a.win_w == 2 && a.stride == 2)
+    done = nchw_dispatch_f<2, 2, 2>(a.fh, a.fw, g, blocks, smem32, a.avg, st, &err);
+  else if (a.win_h == 3 && a.win_w == 3 && a.stride == 2)
+    done = nchw_dispatch_f<3, 3, 2>(a.fh, a.fw, g, blocks, smem32, a.avg, st, &err);
+  else if (a.win_h == 3 && a.win_w == 3 && a.stride == 1)
+    done = nchw_dispatch_f<3, 3, 1>(a.fh, a.fw, g, blocks, smem32, a.avg, st, &err);
+  if (done) return err;
+
+  g.nbw = a.wo;
+  g.div_nbw = FastDiv(g.nbw);
+  auto kern = a.avg ? pool_nchw_generic_kernel<true> : pool_nchw_generic_kernel<false>;
+  if (smem32 > 48 * 1024) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem32);
+    if (err != cudaSuccess) return err;
+  }
+  kern<<<blocks, kThreads, smem32, st>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pool_oracle(const PoolArgs& a, uint64_t sn, uint64_t sc, uint64_t sh,
+                               uint64_t sw, cudaStream_t st) {
+  const uint64_t total = static_cast<uint64_t>(a.n) * a.c * a.ho * a.wo;
+  if (total == 0) return cudaSuccess;
+  uint64_t blocks = (total + 255) / 256;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  pool_oracle_kernel<<<static_cast<uint32_t>(blocks), 256, 0, st>>>(
+      a.src, a.dst, a.n, a.c, a.ho, a.wo, sn, sc, sh, sw, a.win_h, a.win_w, a.stride, a.avg);
+  return cudaGetLastError();
+}
+
+}  // namespace lcnn_impl

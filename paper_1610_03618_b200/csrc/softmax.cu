@@ -1,0 +1,387 @@
+// Softmax classifier on sm_100a: the fused single kernel and the five-kernel
+// multi-pass baseline.
+//
+// Reference: /root/reference/proj/src/softmax.cpp
+//   softmax_reference :36-98   max; x-max -> midv1; exp -> midv2; blocked sum;
+//                              x (1/sum)  (8 full-matrix sweeps, 3 arrays)
+//   softmax_fused     :100-145 row staged once, blocked max then exp+sum,
+//                              out = e * (1/sum)  (2 sweeps)
+//   streaming         :146-178 rows wider than the local buffer
+//   check_finite      :15-19   DomainError on inf/NaN
+// Paper: PAPER.md Fig. 9 (one kernel, shared-memory reductions).
+//
+// Numerics follow the reference: accurate expf (not __expf), inv = 1/sum in
+// IEEE division, out = e * inv.  The reduction order differs from the CPU's
+// 256-blocked sequential sum (parallel tree), which is the only source of
+// difference; the parity bound is approx_equal 1e-6 (tensor.cpp:157-187).
+//
+// Fused kernel shapes (all one launch, one HBM read + one HBM write):
+//   cols <= 2048      : LPR lanes per row (4..32), values held in registers,
+//                       128-bit loads when cols % 4 == 0, shuffle reductions;
+//   cols <= 16384     : one CTA (256 threads) per row, registers + a
+//                       shared-memory cross-warp reduction;
+//   wider             : one CTA per row, online (max, sum) pass then a
+//                       normalise pass (input read twice).
+#include <float.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace lcnn_dev {
+
+__device__ __forceinline__ void flag_nonfinite(int* flag, bool bad) {
+  if (bad && flag) *reinterpret_cast<volatile int*>(flag) = 1;
+}
+
+template <int LPR>
+__device__ __forceinline__ float group_max(float v, unsigned mask) {
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(mask, v, o));
+  return v;
+}
+template <int LPR>
+__device__ __forceinline__ float group_sum(float v, unsigned mask) {
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+// LPR lanes own one row; each lane holds VPL values.
+template <int LPR, int VPL, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    softmax_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                        uint32_t rows, uint32_t cols, int* flag) {
+  constexpr int kGroups = kThreads / LPR;
+  const uint32_t row = blockIdx.x * kGroups + threadIdx.x / LPR;
+  const int lane = threadIdx.x % LPR;
+  const int wl = threadIdx.x & 31;
+  const unsigned mask =
+      LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (wl & ~(LPR - 1)));
+  if (row >= rows) return;  // uniform per group
+  const float* in = src + static_cast<uint64_t>(row) * cols;
+  float* out = dst + static_cast<uint64_t>(row) * cols;
+
+  float v[VPL];
+  bool bad = false;
+  float m = -INFINITY;
+  if constexpr (VEC) {
+#pragma unroll
+    for (int k = 0; k < VPL / 4; ++k) {
+      const uint32_t col = (lane + k * LPR) * 4;
+      if (col < cols) {
+        const float4 q = ldg_stream(reinterpret_cast<const float4*>(in + col));
+        v[4 * k + 0] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+      } else {
+        v[4 * k + 0] = v[4 * k + 1] = v[4 * k + 2] = v[4 * k + 3] = -INFINITY;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const uint32_t col = lane + k * LPR;
+      v[k] = col < cols ? __ldg(in + col) : -INFINITY;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const uint32_t col = VEC ? (lane + (k / 4) * LPR) * 4 + (k % 4) : lane + k * LPR;
+    if (col < cols) {
+      bad |= !isfinite(v[k]);
+      m = fmaxf(m, v[k]);
+    }
+  }
+  flag_nonfinite(flag, bad);
+  m = group_max<LPR>(m, mask);
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const uint32_t col = VEC ? (lane + (k / 4) * LPR) * 4 + (k % 4) : lane + k * LPR;
+    const float e = col < cols ? expf(v[k] - m) : 0.0f;
+    v[k] = e;
+    s += e;
+  }
+  s = group_sum<LPR>(s, mask);
+  const float inv = 1.0f / s;
+  if constexpr (VEC) {
+#pragma unroll
+    for (int k = 0; k < VPL / 4; ++k) {
+      const uint32_t col = (lane + k * LPR) * 4;
+      if (col < cols)
+        stg_stream(reinterpret_cast<float4*>(out + col),
+                   make_float4(v[4 * k] * inv, v[4 * k + 1] * inv, v[4 * k + 2] * inv,
+                               v[4 * k + 3] * inv));
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const uint32_t col = lane + k * LPR;
+      if (col < cols) stg_stream(out + col, v[k] * inv);
+    }
+  }
+}
+
+__device__ __forceinline__ float block_reduce_max(float v, float* red) {
+  v = group_max<32>(v, 0xffffffffu);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int i = 1; i < kThreads / 32; ++i) r = fmaxf(r, red[i]);
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ float block_reduce_sum(float v, float* red) {
+  v = group_sum<32>(v, 0xffffffffu);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int i = 1; i < kThreads / 32; ++i) r += red[i];
+  __syncthreads();
+  return r;
+}
+
+// One CTA per row, VPL values per thread in registers (cols <= 256 * VPL).
+template <int VPL, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    softmax_wide_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                        uint32_t cols, int* flag) {
+  __shared__ float red[kThreads / 32];
+  const float* in = src + static_cast<uint64_t>(blockIdx.x) * cols;
+  float* out = dst + static_cast<uint64_t>(blockIdx.x) * cols;
+  const int t = threadIdx.x;
+  float v[VPL];
+  bool bad = false;
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < VPL / 4; ++k) {
+    const uint32_t col = (t + k * kThreads) * 4;
+    if constexpr (VEC) {
+      if (col < cols) {
+        const float4 q = ldg_stream(reinterpret_cast<const float4*>(in + col));
+        v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+      } else {
+        v[4 * k] = v[4 * k + 1] = v[4 * k + 2] = v[4 * k + 3] = -INFINITY;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[4 * k + j] = col + j < cols ? __ldg(in + col + j) : -INFINITY;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const uint32_t col = (t + (k / 4) * kThreads) * 4 + (k % 4);
+    if (col < cols) {
+      bad |= !isfinite(v[k]);
+      m = fmaxf(m, v[k]);
+    }
+  }
+  flag_nonfinite(flag, bad);
+  m = block_reduce_max(m, red);
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const uint32_t col = (t + (k / 4) * kThreads) * 4 + (k % 4);
+    const float e = col < cols ? expf(v[k] - m) : 0.0f;
+    v[k] = e;
+    s += e;
+  }
+  s = block_reduce_sum(s, red);
+  const float inv = 1.0f / s;
+#pragma unroll
+  for (int k = 0; k < VPL / 4; ++k) {
+    const uint32_t col = (t + k * kThreads) * 4;
+    if constexpr (VEC) {
+      if (col < cols)
+        stg_stream(reinterpret_cast<float4*>(out + col),
+                   make_float4(v[4 * k] * inv, v[4 * k + 1] * inv, v[4 * k + 2] * inv,
+                               v[4 * k + 3] * inv));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (col + j < cols) stg_stream(out + col + j, v[4 * k + j] * inv);
+    }
+  }
+}
+
+// One CTA per row of any width: online (max, sum) then normalise.
+__global__ void __launch_bounds__(kThreads)
+    softmax_stream_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                          uint32_t cols, int* flag) {
+  __shared__ float red_m[kThreads / 32], red_s[kThreads / 32];
+  const float* in = src + static_cast<uint64_t>(blockIdx.x) * cols;
+  float* out = dst + static_cast<uint64_t>(blockIdx.x) * cols;
+  float m = -INFINITY, s = 0.0f;
+  bool bad = false;
+  for (uint32_t j = threadIdx.x; j < cols; j += kThreads) {
+    const float x = __ldg(in + j);
+    bad |= !isfinite(x);
+    if (x > m) {
+      s = s * expf(m - x) + 1.0f;
+      m = x;
+    } else {
+      s += expf(x - m);
+    }
+  }
+  flag_nonfinite(flag, bad);
+  // merge (m, s) pairs: warp then block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float mo = __shfl_xor_sync(0xffffffffu, m, o);
+    const float so = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mn = fmaxf(m, mo);
+    s = (m == -INFINITY ? 0.0f : s * expf(m - mn)) + (mo == -INFINITY ? 0.0f : so * expf(mo - mn));
+    m = mn;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red_m[w] = m;
+    red_s[w] = s;
+  }
+  __syncthreads();
+  float M = red_m[0];
+  for (int i = 1; i < kThreads / 32; ++i) M = fmaxf(M, red_m[i]);
+  float S = 0.0f;
+  for (int i = 0; i < kThreads / 32; ++i)
+    S += red_m[i] == -INFINITY ? 0.0f : red_s[i] * expf(red_m[i] - M);
+  const float inv = 1.0f / S;
+  for (uint32_t j = threadIdx.x; j < cols; j += kThreads)
+    stg_stream(out + j, expf(__ldg(in + j) - M) * inv);
+}
+
+// ---- five-pass baseline (softmax.cpp:36-98), one kernel per step ---------
+template <int LPR>
+__global__ void __launch_bounds__(kThreads)
+    row_max_kernel(const float* __restrict__ in, float* __restrict__ maxv, uint32_t rows,
+                   uint32_t cols, int* flag) {
+  const uint32_t row = blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
+  const int lane = threadIdx.x % LPR;
+  const int wl = threadIdx.x & 31;
+  const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (wl & ~(LPR - 1)));
+  if (row >= rows) return;
+  const float* r = in + static_cast<uint64_t>(row) * cols;
+  float m = -INFINITY;
+  bool bad = false;
+  for (uint32_t j = lane; j < cols; j += LPR) {
+    const float x = r[j];
+    bad |= !isfinite(x);
+    m = fmaxf(m, x);
+  }
+  flag_nonfinite(flag, bad);
+  m = group_max<LPR>(m, mask);
+  if (lane == 0) maxv[row] = m;
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(kThreads)
+    row_sum_kernel(const float* __restrict__ in, float* __restrict__ sumv, uint32_t rows,
+                   uint32_t cols) {
+  const uint32_t row = blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
+  const int lane = threadIdx.x % LPR;
+  const int wl = threadIdx.x & 31;
+  const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (wl & ~(LPR - 1)));
+  if (row >= rows) return;
+  const float* r = in + static_cast<uint64_t>(row) * cols;
+  float s = 0.0f;
+  for (uint32_t j = lane; j < cols; j += LPR) s += r[j];
+  s = group_sum<LPR>(s, mask);
+  if (lane == 0) sumv[row] = s;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    sub_rowvec_kernel(const float* __restrict__ in, const float* __restrict__ maxv,
+                      float* __restrict__ out, uint64_t total, FastDiv div_cols) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * kThreads)
+    out[i] = in[i] - maxv[div_cols.div(static_cast<uint32_t>(i))];
+}
+
+__global__ void __launch_bounds__(kThreads)
+    exp_kernel(const float* __restrict__ in, float* __restrict__ out, uint64_t total) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * kThreads)
+    out[i] = expf(in[i]);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    scale_rowvec_kernel(const float* __restrict__ in, const float* __restrict__ sumv,
+                        float* __restrict__ out, uint64_t total, FastDiv div_cols) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * kThreads)
+    out[i] = in[i] * (1.0f / sumv[div_cols.div(static_cast<uint32_t>(i))]);
+}
+
+}  // namespace lcnn_dev
+
+namespace lcnn_impl {
+
+using namespace lcnn_dev;
+
+namespace {
+
+template <int LPR, int VPL>
+cudaError_t rows_launch(const float* src, float* dst, uint32_t rows, uint32_t cols, bool vec,
+                        int* flag, cudaStream_t st) {
+  constexpr int kGroups = kThreads / LPR;
+  const uint32_t blocks = (rows + kGroups - 1) / kGroups;
+  if (vec) softmax_rows_kernel<LPR, VPL, true><<<blocks, kThreads, 0, st>>>(src, dst, rows, cols, flag);
+  else softmax_rows_kernel<LPR, VPL, false><<<blocks, kThreads, 0, st>>>(src, dst, rows, cols, flag);
+  return cudaGetLastError();
+}
+
+template <int VPL>
+cudaError_t wide_launch(const float* src, float* dst, uint32_t rows, uint32_t cols, bool vec,
+                        int* flag, cudaStream_t st) {
+  if (vec) softmax_wide_kernel<VPL, true><<<rows, kThreads, 0, st>>>(src, dst, cols, flag);
+  else softmax_wide_kernel<VPL, false><<<rows, kThreads, 0, st>>>(src, dst, cols, flag);
+  return cudaGetLastError();
+}
+
+uint32_t grid_for(uint64_t total) {
+  uint64_t b = (total + kThreads - 1) / kThreads;
+  if (b > 148ull * 16) b = 148ull * 16;
+  return static_cast<uint32_t>(b ? b : 1);
+}
+
+}  // namespace
+
+cudaError_t launch_softmax_fused(const float* src, float* dst, uint32_t rows, uint32_t cols,
+                                 int* flag, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  const bool vec = (cols % 4 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+  // register-resident rows: choose lanes-per-row so each lane holds <= 64
+  if (cols <= 16) return rows_launch<4, 4>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 64) return rows_launch<8, 8>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 256) return rows_launch<16, 16>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 512) return rows_launch<32, 16>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 1024) return rows_launch<32, 32>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 2048) return rows_launch<32, 64>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 4096) return wide_launch<16>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 8192) return wide_launch<32>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 16384) return wide_launch<64>(src, dst, rows, cols, vec, flag, st);
+  softmax_stream_kernel<<<rows, kThreads, 0, st>>>(src, dst, cols, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_five_pass(const float* src, float* dst, uint32_t rows, uint32_t cols,
+                                     float* scratch, int* flag, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  const uint64_t total = static_cast<uint64_t>(rows) * cols;
+  float* maxv = scratch;
+  float* sumv = scratch + rows;
+  float* midv1 = scratch + 2 * static_cast<uint64_t>(rows);
+  float* midv2 = midv1 + total;
+  const FastDiv dc(cols);
+  const uint32_t row_blocks = (rows + 7) / 8;  // 8 rows (warps) per CTA
+  row_max_kernel<32><<<row_blocks, kThreads, 0, st>>>(src, maxv, rows, cols, flag);
+  sub_rowvec_kernel<<<grid_for(total), kThreads, 0, st>>>(src, maxv, midv1, total, dc);
+  exp_kernel<<<grid_for(total), kThreads, 0, st>>>(midv1, midv2, total);
+  row_sum_kernel<32><<<row_blocks, kThreads, 0, st>>>(midv2, sumv, rows, cols);
+  scale_rowvec_kernel<<<grid_for(total), kThreads, 0, st>>>(midv2, sumv, dst, total, dc);
+  return cudaGetLastError();
+}
+
+}  // namespace lcnn_impl

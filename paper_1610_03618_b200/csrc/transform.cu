@@ -1,0 +1,244 @@
+// NCHW <-> CHWN layout transformation on sm_100a.
+//
+// Reference: /root/reference/proj/src/layout.cpp
+//   transform_tiled  :99-120  flattens CHWN<->NCHW to a 2D transpose of the
+//                             [C*H*W] x [N] view through a tile^2 scratch
+//   transpose2d_tiled:31-68   the tile loop (scalar or 8-byte "wide" copies)
+//   transform_naive  :77-97   4-loop permutation for any layout pair
+// Paper: PAPER.md Fig. 7b (shared-memory tile + float2 when N >= 64).
+//
+// B200 design.  The op is pure data movement, so the roofline is HBM copy
+// bandwidth: 2 x N*C*H*W*4 bytes per call (bench.cpp:202).  Each CTA moves a
+// TR x TC tile:
+//   * load phase: every warp reads 4 source rows x 128 B with 128-bit loads
+//     (L1::no_allocate: the data is touched once);
+//   * the tile lands in shared memory with a row pitch of TC+1 words, which
+//     makes both the transposed scalar stores and the column reads
+//     conflict-free (pitch == 1 mod 32 banks);
+//   * store phase: every warp writes 4 destination rows x 128 B with 128-bit
+//     streaming stores.
+// When a row length is not a multiple of 4 floats (e.g. AlexNet's 3x227x227
+// input, or odd batches) the affected side falls back to scalar 32-bit
+// accesses, still one full 128-byte line per warp instruction.
+#include "common.cuh"
+#include "internal.h"
+
+namespace lcnn_dev {
+
+template <int TR, int TC, bool VLD, bool VST>
+__global__ void __launch_bounds__(kThreads)
+    transpose2d_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                       uint32_t R, uint32_t C, uint32_t tiles_c) {
+  static_assert(TR % 32 == 0 && TC % 32 == 0, "tile edges are warp multiples");
+  constexpr int P = TC + 1;  // shared-memory pitch, == 1 (mod 32)
+  __shared__ float tile[TR * P];
+
+  const uint32_t t = blockIdx.x;
+  const uint32_t tr = t / tiles_c;
+  const uint32_t tc = t - tr * tiles_c;
+  const uint32_t r0 = tr * TR;
+  const uint32_t c0 = tc * TC;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  constexpr int kWarps = kThreads / 32;
+
+  // ---- load: src[r0 .. r0+TR) x [c0 .. c0+TC) -> tile[r][c] -------------
+  if constexpr (VLD) {
+    // warp slot = 4 rows x 8 float4 (128 B per row)
+    constexpr int kSlotsC = TC / 32;          // float4 column groups of 8
+    constexpr int kSlots = (TR / 4) * kSlotsC;
+    float4 v[kSlots / kWarps];
+#pragma unroll
+    for (int i = 0; i < kSlots / kWarps; ++i) {
+      const int ws = warp + i * kWarps;
+      const int c4 = (ws % kSlotsC) * 8 + (lane & 7);
+      const int r = (ws / kSlotsC) * 4 + (lane >> 3);
+      const uint32_t gr = r0 + r, gc = c0 + c4 * 4;
+      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < R && gc < C) {
+        v[i] = ldg_stream(reinterpret_cast<const float4*>(
+            src + static_cast<uint64_t>(gr) * C + gc));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kSlots / kWarps; ++i) {
+      const int ws = warp + i * kWarps;
+      const int c4 = (ws % kSlotsC) * 8 + (lane & 7);
+      const int r = (ws / kSlotsC) * 4 + (lane >> 3);
+      float* row = tile + r * P + c4 * 4;
+      row[0] = v[i].x;
+      row[1] = v[i].y;
+      row[2] = v[i].z;
+      row[3] = v[i].w;
+    }
+  } else {
+    // warp slot = 1 row x 32 floats
+    constexpr int kSlotsC = TC / 32;
+    constexpr int kSlots = TR * kSlotsC;
+    float v[kSlots / kWarps];
+#pragma unroll
+    for (int i = 0; i < kSlots / kWarps; ++i) {
+      const int ws = warp + i * kWarps;
+      const int c = (ws % kSlotsC) * 32 + lane;
+      const int r = ws / kSlotsC;
+      const uint32_t gr = r0 + r, gc = c0 + c;
+      v[i] = 0.f;
+      if (gr < R && gc < C) v[i] = __ldg(src + static_cast<uint64_t>(gr) * C + gc);
+    }
+#pragma unroll
+    for (int i = 0; i < kSlots / kWarps; ++i) {
+      const int ws = warp + i * kWarps;
+      const int c = (ws % kSlotsC) * 32 + lane;
+      const int r = ws / kSlotsC;
+      tile[r * P + c] = v[i];
+    }
+  }
+  __syncthreads();
+
+  // ---- store: dst[c0 .. c0+TC) x [r0 .. r0+TR) <- tile[r][c] -------------
+  if constexpr (VST) {
+    // warp slot = 4 dst rows (source columns) x 8 float4 (128 B per row)
+    constexpr int kSlotsR = TR / 32;
+    constexpr int kSlots = (TC / 4) * kSlotsR;
+#pragma unroll
+    for (int i = 0; i < kSlots / kWarps; ++i) {
+      const int ws = warp + i * kWarps;
+      const int r4 = (ws % kSlotsR) * 8 + (lane & 7);
+      const int c = (ws / kSlotsR) * 4 + (lane >> 3);
+      const uint32_t gr = r0 + r4 * 4, gc = c0 + c;
+      if (gr < R && gc < C) {
+        float4 o;
+        o.x = tile[(r4 * 4 + 0) * P + c];
+        o.y = tile[(r4 * 4 + 1) * P + c];
+        o.z = tile[(r4 * 4 + 2) * P + c];
+        o.w = tile[(r4 * 4 + 3) * P + c];
+        stg_stream(reinterpret_cast<float4*>(dst + static_cast<uint64_t>(gc) * R + gr), o);
+      }
+    }
+  } else {
+    constexpr int kSlotsR = TR / 32;
+    constexpr int kSlots = TC * kSlotsR;
+#pragma unroll
+    for (int i = 0; i < kSlots / kWarps; ++i) {
+      const int ws = warp + i * kWarps;
+      const int r = (ws % kSlotsR) * 32 + lane;
+      const int c = ws / kSlotsR;
+      const uint32_t gr = r0 + r, gc = c0 + c;
+      if (gr < R && gc < C) {
+        stg_stream(dst + static_cast<uint64_t>(gc) * R + gr, tile[r * P + c]);
+      }
+    }
+  }
+}
+
+// Generic permutation: one thread per destination element, source offset from
+// the logical (n,c,h,w) coordinates (layout.cpp:77-97 semantics).
+struct Dims4 {
+  // destination extents in memory order (outermost first) and the source
+  // stride for each of those destination dimensions
+  uint32_t e1, e2, e3;  // extents of the three inner dst dims
+  FastDiv d1, d2, d3;
+  uint64_t s0, s1, s2, s3;  // source strides of dst dims 0..3
+};
+
+__global__ void __launch_bounds__(kThreads)
+    permute4d_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                     uint64_t total, Dims4 d) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+       i < total; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    // total < 2^32 (Tensor4D caps element counts at UINT32_MAX)
+    uint32_t x = static_cast<uint32_t>(i), q3, q2, q1, i3, i2, i1;
+    d.d3.divmod(x, q3, i3);
+    d.d2.divmod(q3, q2, i2);
+    d.d1.divmod(q2, q1, i1);
+    const uint64_t so = q1 * d.s0 + i1 * d.s1 + i2 * d.s2 + i3 * d.s3;
+    dst[i] = __ldg(src + so);
+  }
+}
+
+}  // namespace lcnn_dev
+
+namespace lcnn_impl {
+
+using namespace lcnn_dev;
+
+namespace {
+
+template <int TR, int TC>
+cudaError_t launch_tile(const float* src, float* dst, uint32_t R, uint32_t C,
+                        bool vld, bool vst, cudaStream_t s) {
+  const uint32_t tiles_r = (R + TR - 1) / TR;
+  const uint32_t tiles_c = (C + TC - 1) / TC;
+  const uint64_t tiles = static_cast<uint64_t>(tiles_r) * tiles_c;
+  if (tiles > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  const dim3 grid(static_cast<uint32_t>(tiles));
+  if (vld && vst)
+    transpose2d_kernel<TR, TC, true, true><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+  else if (vld)
+    transpose2d_kernel<TR, TC, true, false><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+  else if (vst)
+    transpose2d_kernel<TR, TC, false, true><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+  else
+    transpose2d_kernel<TR, TC, false, false><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+  return cudaGetLastError();
+}
+
+bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+}  // namespace
+
+cudaError_t launch_transpose2d(const float* src, float* dst, uint64_t rows,
+                               uint64_t cols, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  const uint32_t R = static_cast<uint32_t>(rows);
+  const uint32_t C = static_cast<uint32_t>(cols);
+  // 128-bit accesses need every row start 16-byte aligned.
+  const bool vld = (C % 4 == 0) && aligned16(src);
+  const bool vst = (R % 4 == 0) && aligned16(dst);
+  if (C >= 64) {
+    if (R >= 64) return launch_tile<64, 64>(src, dst, R, C, vld, vst, s);
+    return launch_tile<32, 64>(src, dst, R, C, vld, vst, s);
+  }
+  if (R >= 64) return launch_tile<64, 32>(src, dst, R, C, vld, vst, s);
+  return launch_tile<32, 32>(src, dst, R, C, vld, vst, s);
+}
+
+cudaError_t launch_permute4d(const float* src, float* dst, uint32_t n,
+                             uint32_t c, uint32_t h, uint32_t w, int src_layout,
+                             int dst_layout, cudaStream_t s) {
+  // logical extents, indexed n=0, c=1, h=2, w=3
+  const uint32_t ext[4] = {n, c, h, w};
+  // memory order (outermost..innermost) per layout code, tensor.hpp:16
+  static const int order[4][4] = {{0, 1, 2, 3},   // NCHW
+                                  {1, 2, 3, 0},   // CHWN
+                                  {0, 2, 3, 1},   // NHWC
+                                  {2, 3, 1, 0}};  // HWCN
+  uint64_t ss[4];  // source stride of each logical dim (layout_strides)
+  uint64_t acc = 1;
+  for (int k = 3; k >= 0; --k) {
+    ss[order[src_layout][k]] = acc;
+    acc *= ext[order[src_layout][k]];
+  }
+  const int* od = order[dst_layout];
+  Dims4 d;
+  d.e1 = ext[od[1]];
+  d.e2 = ext[od[2]];
+  d.e3 = ext[od[3]];
+  d.d1 = FastDiv(d.e1);
+  d.d2 = FastDiv(d.e2);
+  d.d3 = FastDiv(d.e3);
+  d.s0 = ss[od[0]];
+  d.s1 = ss[od[1]];
+  d.s2 = ss[od[2]];
+  d.s3 = ss[od[3]];
+  const uint64_t total = static_cast<uint64_t>(n) * c * h * w;
+  if (total == 0) return cudaSuccess;
+  uint64_t blocks = (total + kThreads - 1) / kThreads;
+  if (blocks > 148ull * 64) blocks = 148ull * 64;
+  permute4d_kernel<<<static_cast<uint32_t>(blocks), kThreads, 0, s>>>(src, dst, total, d);
+  return cudaGetLastError();
+}
+
+}  // namespace lcnn_impl
