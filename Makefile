@@ -7,13 +7,13 @@ NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
 PKG     := paper_1610_03618_b200
 SRC     := $(PKG)/csrc
 OBJDIR  := build/obj
-CU      := transform pool softmax conv capi
+CU      := transform pool softmax gemm conv capi
 OBJS    := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU)))
 LIB     := $(PKG)/lib/liblcnn_cuda.so
 
 all: $(LIB) oracle
 
-$(OBJDIR)/%.o: $(SRC)/%.cu $(SRC)/common.cuh $(SRC)/internal.h include/lcnn_cuda.h
+$(OBJDIR)/%.o: $(SRC)/%.cu $(SRC)/common.cuh $(SRC)/internal.h $(SRC)/tc.cuh $(SRC)/tc_gemm.cuh include/lcnn_cuda.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

@@ -184,19 +184,25 @@ lcnn_status lcnn_conv_output_extents(uint32_t h, uint32_t w, uint32_t f_h,
                                      uint32_t pad, uint32_t* h_out,
                                      uint32_t* w_out);
 
-/* Precision of the tensor-core paths. */
+/* Arithmetic of the dense paths. */
 typedef enum lcnn_precision {
-  LCNN_PREC_TF32 = 0,   /* 1 tcgen05 kind::tf32 MMA per tile (fastest)     */
-  LCNN_PREC_3XTF32 = 1  /* big*big + big*small + small*big: ~fp32 accuracy */
+  LCNN_PREC_TF32 = 0,   /* tcgen05 kind::tf32, one MMA chain (fastest)       */
+  LCNN_PREC_3XTF32 = 1, /* tcgen05, hi*hi + hi*lo + lo*hi: ~fp32 accuracy    */
+  LCNN_PREC_FP32 = 2    /* CUDA-core FFMA: fp32 products, fp32 accumulation  */
 } lcnn_precision;
 
-/* Bytes of device workspace lcnn_conv_forward needs (repacked filters). */
-size_t lcnn_conv_workspace_bytes(uint32_t c_o, uint32_t c_i, uint32_t f_h,
-                                 uint32_t f_w);
+/* Bytes of device workspace lcnn_conv_forward needs (packed filters, and the
+ * split operand copies in 3xTF32 mode). */
+size_t lcnn_conv_workspace_bytes(uint32_t n, uint32_t c_i, uint32_t h,
+                                 uint32_t w, uint32_t c_o, uint32_t f_h,
+                                 uint32_t f_w, int precision);
 
-/* == conv_direct (conv.cpp:200-213, CHWN) and conv_gemm (conv.cpp:306-332,
- * NCHW): implicit-GEMM convolution on tcgen05 tensor cores, output in the
- * input's layout.  filters are (c_o, c_i, f_h, f_w) (tensor.hpp:77-103). */
+/* == conv_direct (conv.cpp:200-213) and conv_gemm (conv.cpp:306-332): the
+ * convolution of an (n, c_i, h, w) input in CHWN or NCHW (LayoutError
+ * otherwise), output (n, c_o, h_out, w_out) in the input's layout.  filters
+ * are (c_o, c_i, f_h, f_w) (tensor.hpp:77-103).  CHWN with n % 32 == 0 runs
+ * the implicit-GEMM tcgen05 kernel (TF32 / 3xTF32); FP32 precision and the
+ * remaining shapes run the fp32 CUDA-core kernel. */
 lcnn_status lcnn_conv_forward(const float* src, const float* filters,
                               float* dst, uint32_t n, uint32_t c_i, uint32_t h,
                               uint32_t w, int layout, uint32_t c_o,
@@ -204,10 +210,17 @@ lcnn_status lcnn_conv_forward(const float* src, const float* filters,
                               uint32_t pad, int precision, void* d_workspace,
                               size_t workspace_bytes, void* stream);
 
+/* Bytes of device workspace lcnn_gemm needs (0 unless 3xTF32). */
+size_t lcnn_gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k,
+                                 int precision);
+
 /* == gemm_blocked (conv.cpp:252-304) / fc_forward (softmax.cpp:182-184):
- * c (m x n) = a (m x k) * b (k x n), all row-major fp32. */
+ * c (m x n) = a (m x k) * b (k x n), all row-major fp32.  TF32 / 3xTF32 run
+ * the tcgen05 kernel when k and n are multiples of 4 (TMA pitch rule), else
+ * the fp32 CUDA-core kernel. */
 lcnn_status lcnn_gemm(const float* a, const float* b, float* c, uint64_t m,
-                      uint64_t n, uint64_t k, int precision, void* stream);
+                      uint64_t n, uint64_t k, int precision, void* d_workspace,
+                      size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

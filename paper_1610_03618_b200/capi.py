@@ -22,7 +22,7 @@ HEADER_PATH = os.path.join(os.path.dirname(PKG_DIR), "include", "lcnn_cuda.h")
 NCHW, CHWN, NHWC, HWCN = 0, 1, 2, 3
 LAYOUT_NAMES = {NCHW: "nchw", CHWN: "chwn", NHWC: "nhwc", HWCN: "hwcn"}
 POOL_MAX, POOL_AVG = 0, 1
-PREC_TF32, PREC_3XTF32 = 0, 1
+PREC_TF32, PREC_3XTF32, PREC_FP32 = 0, 1, 2
 
 
 class AccessReport(ctypes.Structure):
@@ -65,10 +65,11 @@ _SIGNATURES = {
     "lcnn_softmax_reference": (c_int, [_P, _P, _U32, _U32, _P, c_size_t, _P, POINTER(PassReport), _P]),
     "lcnn_conv_output_extents": (c_int, [_U32, _U32, _U32, _U32, _U32, _U32, POINTER(_U32),
                                          POINTER(_U32)]),
-    "lcnn_conv_workspace_bytes": (c_size_t, [_U32, _U32, _U32, _U32]),
+    "lcnn_conv_workspace_bytes": (c_size_t, [_U32] * 7 + [c_int]),
     "lcnn_conv_forward": (c_int, [_P, _P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32,
                                   _U32, c_int, _P, c_size_t, _P]),
-    "lcnn_gemm": (c_int, [_P, _P, _P, c_uint64, c_uint64, c_uint64, c_int, _P]),
+    "lcnn_gemm_workspace_bytes": (c_size_t, [c_uint64, c_uint64, c_uint64, c_int]),
+    "lcnn_gemm": (c_int, [_P, _P, _P, c_uint64, c_uint64, c_uint64, c_int, _P, c_size_t, _P]),
 }
 
 _lib = None
@@ -117,5 +118,5 @@ def call(name: str, *args) -> int:
 __all__ = [
     "AccessReport", "PassReport", "lib", "call", "check", "declared_symbols", "LIB_PATH",
     "NCHW", "CHWN", "NHWC", "HWCN", "POOL_MAX", "POOL_AVG", "PREC_TF32", "PREC_3XTF32",
-    "LAYOUT_NAMES", "c_double",
+    "LAYOUT_NAMES", "c_double", "PREC_FP32",
 ]

@@ -345,4 +345,55 @@ lcnn_status lcnn_conv_output_extents(uint32_t h, uint32_t w, uint32_t f_h, uint3
   return ok();
 }
 
+size_t lcnn_conv_workspace_bytes(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, uint32_t c_o,
+                                 uint32_t f_h, uint32_t f_w, int precision) {
+  return lcnn_impl::conv_workspace_bytes(n, c_i, h, w, c_o, f_h, f_w, precision);
+}
+
+lcnn_status lcnn_conv_forward(const float* src, const float* filters, float* dst, uint32_t n,
+                              uint32_t c_i, uint32_t h, uint32_t w, int layout, uint32_t c_o,
+                              uint32_t f_h, uint32_t f_w, uint32_t stride, uint32_t pad,
+                              int precision, void* d_workspace, size_t workspace_bytes,
+                              void* stream) {
+  if (!src || !filters || !dst) return fail(LCNN_EINVAL, "conv: null pointer");
+  if (precision < LCNN_PREC_TF32 || precision > LCNN_PREC_FP32)
+    return fail(LCNN_EINVAL, "conv: bad precision");
+  lcnn_status st = check_volume(n, c_i, h, w, "Tensor4D");
+  if (st != LCNN_OK) return st;
+  st = check_volume(c_o, c_i, f_h, f_w, "FilterBank");
+  if (st != LCNN_OK) return st;
+  uint32_t ho = 0, wo = 0;
+  st = lcnn_conv_output_extents(h, w, f_h, f_w, stride, pad, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  if (layout != LCNN_CHWN && layout != LCNN_NCHW)
+    return fail(LCNN_ELAYOUT, "conv_direct: only CHWN and NCHW kernels exist");  // conv.cpp:211
+  if (precision != LCNN_PREC_FP32 &&
+      workspace_bytes < lcnn_conv_workspace_bytes(n, c_i, h, w, c_o, f_h, f_w, precision))
+    return fail(LCNN_EINVAL, "conv: workspace too small");
+  lcnn_impl::ConvArgs a{src, filters, dst, n, c_i, h, w, c_o, f_h, f_w, stride, pad, ho, wo,
+                        layout, precision, d_workspace};
+  cudaError_t e = lcnn_impl::launch_conv(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "conv_forward");
+  return ok();
+}
+
+lcnn_status lcnn_gemm(const float* a, const float* b, float* c, uint64_t m, uint64_t n,
+                      uint64_t k, int precision, void* d_workspace, size_t workspace_bytes,
+                      void* stream) {
+  if (!a || !b || !c) return fail(LCNN_EINVAL, "gemm: null pointer");
+  if (m == 0 || n == 0 || k == 0) return fail(LCNN_ESHAPE, "gemm: empty operand");
+  if (precision < LCNN_PREC_TF32 || precision > LCNN_PREC_FP32)
+    return fail(LCNN_EINVAL, "gemm: bad precision");
+  cudaError_t e;
+  if (precision != LCNN_PREC_FP32 && lcnn_impl::tc_gemm_supported(m, n, k, a, b)) {
+    if (workspace_bytes < lcnn_impl::gemm_workspace_bytes(m, n, k, precision))
+      return fail(LCNN_EINVAL, "gemm: workspace too small");
+    e = lcnn_impl::launch_gemm_tc(a, b, c, m, n, k, precision, d_workspace, S(stream));
+  } else {
+    e = lcnn_impl::launch_gemm_fp32(a, b, c, m, n, k, S(stream));
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "gemm");
+  return ok();
+}
+
 }  // extern "C"

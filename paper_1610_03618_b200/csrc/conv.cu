@@ -1,26 +1,344 @@
-// Convolution / fully-connected entry points (conv.hpp:17-54).
-// The tcgen05 implicit-GEMM kernels land in a later milestone; until then
-// these entry points report UnsupportedError instead of silently falling back.
-#include <cuda_runtime.h>
+// Convolution for the whole-network path (conv.hpp:17-54).
+//
+// Reference: /root/reference/proj/src/conv.cpp
+//   conv_direct_chwn  :102-152  CHWN, image block innermost
+//   conv_direct_nchw  :157-196  NCHW, window innermost
+//   conv_gemm + im2col:215-332  materialised unroll + blocked GEMM
+//   conv_oracle       :53-93    fp64 ground truth
+//
+// B200 design -- CHWN implicit GEMM on tcgen05 (no im2col in HBM):
+//   D[co][(oh, ow, n)] = sum_k Wpack[co][k] * X[k][(oh, ow, n)]
+// The GEMM N index (oh, ow, n) is exactly the CHWN output order, so the
+// accumulator tile stores straight into the output.  B tiles are TMA boxes of
+// the 4D input (n, w, h, c) -- the batch is contiguous, so every k-row of a
+// tile is 32 images (128 B) of one input pixel: an MN-major SW128 operand.
+// Padding is TMA out-of-bounds zero fill (negative / overflowing h, w
+// coordinates).  Two K orderings:
+//   CI  (C_i % 32 == 0): k = (fh, fw, ci); a k-block is 32 channels of one
+//        filter tap: box {32 n, 1 w, 1 h, 32 c}.
+//   WIN (F_w <= 16):     k = (fh, ci, fw'); fw padded to FP in {4, 8, 16};
+//        a k-block is 32/FP channels x FP taps of one filter row:
+//        box {32 n, FP w, 1 h, 32/FP c}; padded taps get zero weights.
+// Filters are packed once per call into the matching K-major [co][K] matrix.
+// 3xTF32 mode chains hi*hi + hi*lo + lo*hi over split copies of both operands.
+//
+// The fp32 SIMT kernels serve LCNN_PREC_FP32 (bit-level fp32 products, the
+// host API's default for reference-tolerance parity) and every shape the
+// tensor-core path does not cover (NCHW, batches that are not a multiple of
+// 32, rectangular windows wider than 16).
+#include <cuda.h>
 
 #include "../../include/lcnn_cuda.h"
+#include "common.cuh"
 #include "internal.h"
+#include "tc_gemm.cuh"
 
-extern "C" {
+namespace lcnn_dev {
 
-size_t lcnn_conv_workspace_bytes(uint32_t c_o, uint32_t c_i, uint32_t f_h, uint32_t f_w) {
-  return static_cast<size_t>(c_o) * c_i * f_h * f_w * sizeof(float) * 2;
+using namespace lcnn_tc;
+
+enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1 };
+
+struct ConvGeomTc {
+  uint32_t N, Ci, H, W, Co, FH, FW, S, P, Ho, Wo;
+  uint32_t mode, FP, CIB, CiP;
+};
+
+// Wpack[co][k] in the loader's K order, zero for padded (ci, fw) slots.
+__global__ void pack_filters_kernel(const float* __restrict__ f, float* __restrict__ hi,
+                                    float* __restrict__ lo, ConvGeomTc g, uint32_t K) {
+  const uint64_t total = static_cast<uint64_t>(g.Co) * K;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t co = static_cast<uint32_t>(i / K);
+    const uint32_t k = static_cast<uint32_t>(i % K);
+    uint32_t ci, fh, fw;
+    bool valid = true;
+    if (g.mode == kModeCI) {
+      ci = k % g.Ci;
+      const uint32_t tap = k / g.Ci;
+      fh = tap / g.FW;
+      fw = tap % g.FW;
+    } else {
+      fw = k % g.FP;
+      const uint32_t t = k / g.FP;
+      ci = t % g.CiP;
+      fh = t / g.CiP;
+      valid = fw < g.FW && ci < g.Ci;
+    }
+    float v = 0.0f;
+    if (valid) v = f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw];
+    if (lo) {
+      uint32_t r;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+      const float h = __uint_as_float(r);
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v - h));
+      hi[i] = h;
+      lo[i] = __uint_as_float(r);
+    } else {
+      hi[i] = v;
+    }
+  }
 }
 
-lcnn_status lcnn_conv_forward(const float*, const float*, float*, uint32_t, uint32_t, uint32_t,
-                              uint32_t, int, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                              int, void*, size_t, void*) {
-  return LCNN_EUNSUPPORTED;
+struct ChwnConvLoader {
+  CUtensorMap a[2];  // packed filters hi / lo  (2D: {K, Co}, box {32, 128})
+  CUtensorMap b[2];  // input hi / lo           (4D: {N, W, H, Ci})
+  ConvGeomTc g;
+  uint32_t kb, segs, ncols;  // ncols = Ho*Wo*N
+  static constexpr bool kBMajorMN = true;
+  __device__ uint32_t kblocks() const { return kb; }
+  __device__ uint32_t segments() const { return segs; }
+  __device__ void prefetch() const {
+    tma_prefetch(&a[0]);
+    tma_prefetch(&b[0]);
+  }
+  __device__ void load(uint32_t seg, uint32_t k, void* sa, void* sb, uint64_t* bar, uint32_t m0,
+                       uint32_t ntile) const {
+    tma_load_2d(sa, &a[seg == 2 ? 1 : 0], bar, k * kTcBK, m0);
+    uint32_t fh, wofs, c0;
+    if (g.mode == kModeCI) {
+      const uint32_t cbn = g.Ci / 32;
+      const uint32_t tap = k / cbn;
+      c0 = (k % cbn) * 32;
+      fh = tap / g.FW;
+      wofs = tap % g.FW;
+    } else {
+      const uint32_t cbn = g.CiP / g.CIB;
+      fh = k / cbn;
+      c0 = (k % cbn) * g.CIB;
+      wofs = 0;
+    }
+    const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
+#pragma unroll
+    for (int j = 0; j < kTcBN / 32; ++j) {
+      const uint32_t col = ntile * kTcBN + 32 * j;
+      const uint32_t pos = col / g.N;
+      const uint32_t n0 = col - pos * g.N;
+      const uint32_t oh = pos / g.Wo, ow = pos - (pos / g.Wo) * g.Wo;
+      int32_t y = static_cast<int32_t>(ow * g.S + wofs) - static_cast<int32_t>(g.P);
+      int32_t z = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
+      if (col >= ncols) z = -(1 << 20);  // beyond the last output: all-OOB box (zeros)
+      tma_load_4d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, static_cast<int32_t>(n0), y, z,
+                  static_cast<int32_t>(c0));
+    }
+  }
+};
+
+struct RowsOut {  // C[m][col] row-major, ldc = ncols
+  float* c;
+  uint64_t ldc;
+  uint32_t M, N;
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t ntile, uint32_t col,
+                                          const float* v) const {
+    if (m >= M) return;
+    const uint32_t n0 = ntile * kTcBN + col;
+    float* row = c + m * ldc + n0;
+    if (n0 + 32 <= N) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(row + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) row[j] = v[j];
+    }
+  }
+};
+
+// ---- fp32 SIMT direct convolution (any shape, CHWN or NCHW) --------------
+struct ConvGeomSimt {
+  uint32_t N, Ci, H, W, Co, FH, FW, S, P, Ho, Wo;
+};
+
+__global__ void __launch_bounds__(256)
+    conv_chwn_simt_kernel(const float* __restrict__ x, const float* __restrict__ f,
+                          float* __restrict__ y, ConvGeomSimt g) {
+  const uint64_t total = static_cast<uint64_t>(g.Co) * g.Ho * g.Wo * g.N;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t n = static_cast<uint32_t>(i % g.N);
+    uint64_t t = i / g.N;
+    const uint32_t ow = static_cast<uint32_t>(t % g.Wo);
+    t /= g.Wo;
+    const uint32_t oh = static_cast<uint32_t>(t % g.Ho);
+    const uint32_t co = static_cast<uint32_t>(t / g.Ho);
+    float acc = 0.0f;
+    for (uint32_t ci = 0; ci < g.Ci; ++ci)
+      for (uint32_t fh = 0; fh < g.FH; ++fh) {
+        const int32_t ih = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
+        if (ih < 0 || ih >= static_cast<int32_t>(g.H)) continue;
+        for (uint32_t fw = 0; fw < g.FW; ++fw) {
+          const int32_t iw = static_cast<int32_t>(ow * g.S + fw) - static_cast<int32_t>(g.P);
+          if (iw < 0 || iw >= static_cast<int32_t>(g.W)) continue;
+          acc = fmaf(__ldg(x + ((static_cast<uint64_t>(ci) * g.H + ih) * g.W + iw) * g.N + n),
+                     __ldg(f + ((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw),
+                     acc);
+        }
+      }
+    y[i] = acc;
+  }
 }
 
-lcnn_status lcnn_gemm(const float*, const float*, float*, uint64_t, uint64_t, uint64_t, int,
-                      void*) {
-  return LCNN_EUNSUPPORTED;
+__global__ void __launch_bounds__(256)
+    conv_nchw_simt_kernel(const float* __restrict__ x, const float* __restrict__ f,
+                          float* __restrict__ y, ConvGeomSimt g) {
+  const uint64_t total = static_cast<uint64_t>(g.N) * g.Co * g.Ho * g.Wo;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t ow = static_cast<uint32_t>(i % g.Wo);
+    uint64_t t = i / g.Wo;
+    const uint32_t oh = static_cast<uint32_t>(t % g.Ho);
+    t /= g.Ho;
+    const uint32_t co = static_cast<uint32_t>(t % g.Co);
+    const uint32_t n = static_cast<uint32_t>(t / g.Co);
+    float acc = 0.0f;
+    for (uint32_t ci = 0; ci < g.Ci; ++ci) {
+      const float* plane = x + (static_cast<uint64_t>(n) * g.Ci + ci) * g.H * g.W;
+      for (uint32_t fh = 0; fh < g.FH; ++fh) {
+        const int32_t ih = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
+        if (ih < 0 || ih >= static_cast<int32_t>(g.H)) continue;
+        for (uint32_t fw = 0; fw < g.FW; ++fw) {
+          const int32_t iw = static_cast<int32_t>(ow * g.S + fw) - static_cast<int32_t>(g.P);
+          if (iw < 0 || iw >= static_cast<int32_t>(g.W)) continue;
+          acc = fmaf(__ldg(plane + static_cast<uint64_t>(ih) * g.W + iw),
+                     __ldg(f + ((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw),
+                     acc);
+        }
+      }
+    }
+    y[i] = acc;
+  }
 }
 
-}  // extern "C"
+}  // namespace lcnn_dev
+
+namespace lcnn_impl {
+
+using namespace lcnn_dev;
+
+bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer,
+                  uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer);
+bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t* dims,
+               const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides);
+cudaError_t launch_split_hilo(const float* x, float* hi, float* lo, uint64_t count,
+                              cudaStream_t s);
+
+namespace {
+
+struct TcPlan {
+  bool ok = false;
+  ConvGeomTc g{};
+  uint32_t K = 0;  // packed K (multiple of 32)
+};
+
+TcPlan plan_tc(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, int layout, uint32_t co,
+               uint32_t fh, uint32_t fw, uint32_t stride, uint32_t pad, uint32_t ho,
+               uint32_t wo) {
+  TcPlan p;
+  if (layout != LCNN_CHWN || n % 32 != 0) return p;
+  ConvGeomTc& g = p.g;
+  g = ConvGeomTc{n, ci, h, w, co, fh, fw, stride, pad, ho, wo, 0, 0, 0, 0};
+  const uint64_t ncols = static_cast<uint64_t>(ho) * wo * n;
+  if (ncols >= (1ull << 31) || static_cast<uint64_t>(h) * w * n * ci >= (1ull << 32)) return p;
+  if (ci % 32 == 0) {
+    g.mode = kModeCI;
+    p.K = fh * fw * ci;
+  } else if (fw <= 16) {
+    g.mode = kModeWIN;
+    g.FP = fw <= 4 ? 4 : (fw <= 8 ? 8 : 16);
+    g.CIB = 32 / g.FP;
+    g.CiP = (ci + g.CIB - 1) / g.CIB * g.CIB;
+    p.K = fh * g.CiP * g.FP;
+  } else {
+    return p;
+  }
+  p.ok = true;
+  return p;
+}
+
+}  // namespace
+
+size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, uint32_t co,
+                            uint32_t fh, uint32_t fw, int precision) {
+  // packed filters for the widest packing (WIN with FP=16, CiP rounded to 2)
+  const uint64_t kmax = static_cast<uint64_t>(fh) * ((ci + 1) / 2 * 2) * 16 + fh * fw * ci;
+  uint64_t bytes = static_cast<uint64_t>(co) * kmax * 4 + 256;
+  if (precision == LCNN_PREC_3XTF32)
+    bytes = 2 * bytes + 2ull * n * ci * h * w * 4 + 256;
+  return bytes;
+}
+
+cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
+  const bool want_tc = a.precision != LCNN_PREC_FP32;
+  TcPlan p = want_tc ? plan_tc(a.n, a.ci, a.h, a.w, a.layout, a.co, a.fh, a.fw, a.stride, a.pad,
+                               a.ho, a.wo)
+                     : TcPlan{};
+  if (!p.ok) {
+    ConvGeomSimt g{a.n, a.ci, a.h, a.w, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo};
+    const uint64_t total = static_cast<uint64_t>(a.n) * a.co * a.ho * a.wo;
+    uint64_t blocks = (total + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    if (a.layout == LCNN_CHWN)
+      conv_chwn_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, a.filters,
+                                                                          a.dst, g);
+    else
+      conv_nchw_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, a.filters,
+                                                                          a.dst, g);
+    return cudaGetLastError();
+  }
+  const bool x3 = a.precision == LCNN_PREC_3XTF32;
+  float* ws = static_cast<float*>(a.workspace);
+  const uint64_t apack = static_cast<uint64_t>(a.co) * p.K;
+  float* a_hi = ws;
+  float* a_lo = x3 ? a_hi + apack : nullptr;
+  const float* b_hi = a.src;
+  const float* b_lo = a.src;
+  if (x3) {
+    float* bh = a_lo + apack;
+    bh = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(bh) + 255) & ~uintptr_t(255));
+    const uint64_t nx = static_cast<uint64_t>(a.n) * a.ci * a.h * a.w;
+    float* bl = bh + nx;
+    bl = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(bl) + 255) & ~uintptr_t(255));
+    cudaError_t e = launch_split_hilo(a.src, bh, bl, nx, s);
+    if (e != cudaSuccess) return e;
+    b_hi = bh;
+    b_lo = bl;
+  }
+  pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, p.K);
+  ChwnConvLoader L;
+  const uint64_t K = p.K;
+  if (!make_tmap_2d(&L.a[0], a_hi, K, a.co, K * 4, kTcBK, kTcBM) ||
+      !make_tmap_2d(&L.a[1], x3 ? a_lo : a_hi, K, a.co, K * 4, kTcBK, kTcBM))
+    return cudaErrorInvalidValue;
+  const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
+  const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
+                             static_cast<uint64_t>(a.h) * a.w * a.n * 4};
+  uint32_t box[4];
+  if (p.g.mode == kModeCI) {
+    box[0] = 32; box[1] = 1; box[2] = 1; box[3] = 32;
+  } else {
+    box[0] = 32; box[1] = p.g.FP; box[2] = 1; box[3] = p.g.CIB;
+  }
+  if (!make_tmap(&L.b[0], b_hi, 4, dims, pitch, box, nullptr) ||
+      !make_tmap(&L.b[1], b_lo, 4, dims, pitch, box, nullptr))
+    return cudaErrorInvalidValue;
+  L.g = p.g;
+  L.kb = p.K / kTcBK;
+  L.segs = x3 ? 3 : 1;
+  L.ncols = a.ho * a.wo * a.n;
+  RowsOut O{a.dst, L.ncols, a.co, L.ncols};
+  auto kern = tc_gemm_kernel<ChwnConvLoader, RowsOut>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kTcSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid((L.ncols + kTcBN - 1) / kTcBN, (a.co + kTcBM - 1) / kTcBM);
+  kern<<<grid, kTcThreads, kTcSmem, s>>>(L, O);
+  return cudaGetLastError();
+}
+
+}  // namespace lcnn_impl

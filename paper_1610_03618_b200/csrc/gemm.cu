@@ -1,0 +1,278 @@
+// Tensor-core (tcgen05, kind::tf32) GEMM on sm_100a, plus the fp32 SIMT
+// path used when bit-level fp32 accuracy is requested.
+//
+// Reference: /root/reference/proj/src/conv.cpp:252-304 gemm_blocked (64^3
+// blocks, fp32 partials flushed to fp64 every 16 k) and softmax.cpp:182-184
+// fc_forward.  C (m x n) = A (m x k) * B (k x n), all row-major fp32.
+//
+// B200 design (one CTA per 128 x 128 output tile, warp-specialised):
+//   warp 0      : TMA producer -- A tile 128(M) x 32(K) K-major and B tile
+//                 32(K) x 128(N) MN-major (4 boxes of 32 N), SWIZZLE_128B,
+//                 into a STAGES-deep shared-memory ring (mbarrier full/empty);
+//   warp 1      : one elected thread issues tcgen05.mma.kind::tf32
+//                 (M=128, N=128, K=8) x 4 per stage into a 128-column TMEM
+//                 accumulator; tcgen05.commit frees the smem stage;
+//   warps 2..5  : epilogue -- tcgen05.ld 32x32b.x32 TMEM -> registers ->
+//                 global (each warp owns the 32 TMEM lanes of its quarter).
+// Row-major B (N contiguous) is consumed as an MN-major operand directly, so
+// neither operand is ever transposed or re-packed in HBM.
+//
+// Precision modes: TF32 (one MMA chain); 3xTF32 runs the same kernel over a
+// K' = 3K problem [A_hi | A_hi | A_lo] x [B_hi ; B_lo ; B_hi] built by a split
+// kernel (hi = x rounded to tf32, lo = x - hi), giving ~fp32 accuracy.
+#include <cuda.h>
+#include <stdio.h>
+
+#include "../../include/lcnn_cuda.h"
+#include "common.cuh"
+#include "internal.h"
+#include "tc_gemm.cuh"
+
+namespace lcnn_dev {
+
+using namespace lcnn_tc;
+
+// Plain GEMM operands: A (m x k) K-major, B (k x n) MN-major, both via 2D TMA
+// (A box 32x128, B four boxes 32x32).  seg selects (A_hi,B_hi) (A_hi,B_lo)
+// (A_lo,B_hi) in 3xTF32 mode; in TF32 mode only segment 0 exists.
+struct GemmLoader {
+  CUtensorMap a[2];
+  CUtensorMap b[2];
+  uint32_t kb;
+  uint32_t segs;
+  static constexpr bool kBMajorMN = true;
+  __device__ uint32_t kblocks() const { return kb; }
+  __device__ uint32_t segments() const { return segs; }
+  __device__ void prefetch() const {
+    tma_prefetch(&a[0]);
+    tma_prefetch(&b[0]);
+  }
+  __device__ void load(uint32_t seg, uint32_t k, void* sa, void* sb, uint64_t* bar, uint32_t m0,
+                       uint32_t ntile) const {
+    const CUtensorMap* am = &a[seg == 2 ? 1 : 0];
+    const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
+    tma_load_2d(sa, am, bar, k * kTcBK, m0);
+#pragma unroll
+    for (int j = 0; j < kTcBN / 32; ++j)
+      tma_load_2d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, ntile * kTcBN + 32 * j, k * kTcBK);
+  }
+};
+
+struct GemmOut {
+  float* c;
+  uint64_t ldc;
+  uint32_t M, N;
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t ntile, uint32_t col,
+                                          const float* v) const {
+    if (m >= M) return;
+    const uint32_t n0 = ntile * kTcBN + col;
+    float* row = c + m * ldc + n0;
+    if (n0 + 32 <= N && ((reinterpret_cast<uintptr_t>(row) & 15u) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(row + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) row[j] = v[j];
+    }
+  }
+};
+
+// 3xTF32 operand split: hi = x rounded to tf32 (low 13 mantissa bits zero,
+// so the tensor core consumes it exactly), lo = tf32(x - hi).
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void split_hilo_kernel(const float* __restrict__ x, float* __restrict__ hi,
+                                  float* __restrict__ lo, uint64_t count) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    const float h = to_tf32(v);
+    hi[i] = h;
+    lo[i] = to_tf32(v - h);
+  }
+}
+
+// fp32 CUDA-core GEMM (64x64 tile, 4x4 per thread): exact fp32 products and
+// fp32 accumulation, for LCNN_PREC_FP32 and shapes TMA cannot describe.
+__global__ void __launch_bounds__(256)
+    gemm_fp32_simt_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                          float* __restrict__ c, uint64_t M, uint64_t N, uint64_t K) {
+  __shared__ float sa[16][64 + 4];
+  __shared__ float sb[16][64 + 4];
+  const uint64_t m0 = blockIdx.y * 64ull, n0 = blockIdx.x * 64ull;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (uint64_t k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      const int kk = i % 16, mm = i / 16;
+      sa[kk][mm] = (m0 + mm < M && k0 + kk < K) ? a[(m0 + mm) * K + k0 + kk] : 0.0f;
+      const int nn = i % 64, kb = i / 64;
+      sb[kb][nn] = (n0 + nn < N && k0 + kb < K) ? b[(k0 + kb) * N + n0 + nn] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = sa[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = sb[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < N) c[m * N + n] = acc[i][j];
+    }
+}
+
+}  // namespace lcnn_dev
+
+namespace lcnn_impl {
+
+using namespace lcnn_dev;
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+// 2D fp32 tensor map: dims {inner, outer}, row pitch in bytes, box {bi, bo}.
+bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer,
+                  uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {pitch_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t* dims,
+               const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t d[5];
+  cuuint64_t s[4];
+  cuuint32_t b[5], e[5];
+  for (uint32_t i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = estrides ? estrides[i] : 1;
+    if (i + 1 < rank) s[i] = pitches_bytes[i];
+  }
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base), d, s, b, e,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a, const void* b) {
+  // TMA: 16-byte aligned bases and row pitches
+  return m > 0 && n > 0 && k > 0 && (k % 4 == 0) && (n % 4 == 0) &&
+         ((reinterpret_cast<uintptr_t>(a) & 15u) == 0) &&
+         ((reinterpret_cast<uintptr_t>(b) & 15u) == 0) && m < (1ull << 31) && n < (1ull << 31) &&
+         k < (1ull << 31);
+}
+
+cudaError_t launch_split_hilo(const float* x, float* hi, float* lo, uint64_t count,
+                              cudaStream_t s) {
+  uint64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  split_hilo_kernel<<<static_cast<uint32_t>(blocks ? blocks : 1), 256, 0, s>>>(x, hi, lo, count);
+  return cudaGetLastError();
+}
+
+size_t gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k, int precision) {
+  if (precision != LCNN_PREC_3XTF32) return 0;
+  return (2 * m * k + 2 * k * n) * sizeof(float) + 64;
+}
+
+// precision TF32: a, b used directly.  3XTF32: ws holds a_hi, a_lo, b_hi, b_lo.
+cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m, uint64_t n,
+                           uint64_t k, int precision, void* ws, cudaStream_t s) {
+  GemmLoader L;
+  const float *a0 = a, *a1 = a, *b0 = b, *b1 = b;
+  if (precision == LCNN_PREC_3XTF32) {
+    float* w = static_cast<float*>(ws);
+    float* ahi = w;
+    float* alo = ahi + m * k;
+    float* bhi = alo + m * k;
+    float* blo = bhi + k * n;
+    cudaError_t e = launch_split_hilo(a, ahi, alo, m * k, s);
+    if (e == cudaSuccess) e = launch_split_hilo(b, bhi, blo, k * n, s);
+    if (e != cudaSuccess) return e;
+    a0 = ahi; a1 = alo; b0 = bhi; b1 = blo;
+  }
+  if (!make_tmap_2d(&L.a[0], a0, k, m, k * 4, kTcBK, kTcBM) ||
+      !make_tmap_2d(&L.a[1], a1, k, m, k * 4, kTcBK, kTcBM) ||
+      !make_tmap_2d(&L.b[0], b0, n, k, n * 4, 32, kTcBK) ||
+      !make_tmap_2d(&L.b[1], b1, n, k, n * 4, 32, kTcBK))
+    return cudaErrorInvalidValue;
+  L.kb = static_cast<uint32_t>((k + kTcBK - 1) / kTcBK);
+  L.segs = precision == LCNN_PREC_3XTF32 ? 3 : 1;
+  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
+  auto kern = tc_gemm_kernel<GemmLoader, GemmOut>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kTcSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid(static_cast<uint32_t>((n + kTcBN - 1) / kTcBN),
+                  static_cast<uint32_t>((m + kTcBM - 1) / kTcBM));
+  kern<<<grid, kTcThreads, kTcSmem, s>>>(L, O);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_fp32(const float* a, const float* b, float* c, uint64_t m, uint64_t n,
+                             uint64_t k, cudaStream_t s) {
+  const dim3 grid(static_cast<uint32_t>((n + 63) / 64), static_cast<uint32_t>((m + 63) / 64));
+  gemm_fp32_simt_kernel<<<grid, 256, 0, s>>>(a, b, c, m, n, k);
+  return cudaGetLastError();
+}
+
+}  // namespace lcnn_impl
+
+extern "C" {
+
+size_t lcnn_gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k, int precision) {
+  return lcnn_impl::gemm_workspace_bytes(m, n, k, precision);
+}
+
+}  // extern "C"

@@ -54,7 +54,15 @@ struct ConvArgs {
   void* workspace;
 };
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s);
-cudaError_t launch_gemm(const float* a, const float* b, float* c, uint64_t m,
-                        uint64_t n, uint64_t k, int precision, cudaStream_t s);
+size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w,
+                            uint32_t co, uint32_t fh, uint32_t fw, int precision);
+bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a,
+                       const void* b);
+size_t gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k, int precision);
+cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
+                           uint64_t n, uint64_t k, int precision, void* ws,
+                           cudaStream_t s);
+cudaError_t launch_gemm_fp32(const float* a, const float* b, float* c, uint64_t m,
+                             uint64_t n, uint64_t k, cudaStream_t s);
 
 }  // namespace lcnn_impl

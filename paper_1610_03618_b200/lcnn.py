@@ -313,7 +313,52 @@ def softmax_reference(m: DeviceMatrix, out=None, scratch=None, check=True, strea
     return o, rep
 
 
-__all__ = [
+# ------------------------------------------------------- conv / gemm ------
+TF32, X3TF32, FP32 = capi.PREC_TF32, capi.PREC_3XTF32, capi.PREC_FP32
+
+
+def conv_output_extents(h, w, fh, fw, stride, pad):
+    ho, wo = ctypes.c_uint32(), ctypes.c_uint32()
+    capi.call("lcnn_conv_output_extents", h, w, fh, fw, stride, pad, ctypes.byref(ho),
+              ctypes.byref(wo))
+    return ho.value, wo.value
+
+
+def conv_forward(x: DeviceTensor4D, filters, c_o, f_h, f_w, stride=1, pad=0, precision=FP32,
+                 out=None, workspace=None, stream=None) -> DeviceTensor4D:
+    """conv_direct (CHWN) / conv_gemm (NCHW) on the GPU; filters is a CUDA
+    float32 tensor in (c_o, c_i, f_h, f_w) order (tensor.hpp:77-103)."""
+    torch = _torch()
+    ho, wo = conv_output_extents(x.h, x.w, f_h, f_w, stride, pad)
+    if out is None:
+        out = DeviceTensor4D(x.n, c_o, ho, wo, x.layout,
+                             torch.empty(x.n * c_o * ho * wo, dtype=torch.float32,
+                                         device=x.data.device))
+    nbytes = capi.lib().lcnn_conv_workspace_bytes(x.n, x.c, x.h, x.w, c_o, f_h, f_w, precision)
+    if workspace is None or workspace.numel() * 4 < nbytes:
+        workspace = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32,
+                                device=x.data.device)
+    capi.call("lcnn_conv_forward", x.ptr(), filters.data_ptr(), out.ptr(), x.n, x.c, x.h, x.w,
+              x.layout, c_o, f_h, f_w, stride, pad, precision, workspace.data_ptr(),
+              workspace.numel() * 4, _stream(stream))
+    return out
+
+
+def gemm(a, b, m, n, k, precision=FP32, out=None, workspace=None, stream=None):
+    """c (m x n) = a (m x k) * b (k x n), row-major fp32 CUDA tensors
+    (gemm_blocked conv.cpp:252-304 / fc_forward softmax.cpp:182-184)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(m * n, dtype=torch.float32, device=a.device)
+    nbytes = capi.lib().lcnn_gemm_workspace_bytes(m, n, k, precision)
+    if workspace is None or workspace.numel() * 4 < nbytes:
+        workspace = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32, device=a.device)
+    capi.call("lcnn_gemm", a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, k, precision,
+              workspace.data_ptr(), workspace.numel() * 4, _stream(stream))
+    return out
+
+
+__all__ = ["TF32", "X3TF32", "FP32", "conv_forward", "gemm", "conv_output_extents",
     "NCHW", "CHWN", "NHWC", "HWCN", "MAX", "AVERAGE", "DeviceTensor4D", "DeviceMatrix",
     "TransformPlan", "PoolParams", "CoarseningPlan", "AccessReport", "PassReport",
     "flattenable_pair", "make_plan", "transform", "transform_tiled", "transform_naive",

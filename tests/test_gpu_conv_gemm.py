@@ -1,0 +1,131 @@
+"""GPU parity for the dense whole-network path: the tcgen05 implicit-GEMM
+convolution (CHWN), the tcgen05 GEMM (fc layers), and the fp32 CUDA-core
+kernels, against float64 references.
+
+Stated tolerances:
+  FP32 and 3xTF32 : approx_equal 1e-5 against the fp64 oracle -- the
+                    reference's own bar (acceptance.cpp:113-118, test_conv.cpp).
+  TF32            : |y - y64| <= 2^-10 * (|x| conv |w|) + 1e-6 elementwise, the
+                    rounding bound of two tf32 operand roundings (2^-11 each)
+                    per product with fp32 accumulation.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import CHWN, NCHW, C, approx_equal, rng_uniform
+from paper_1610_03618_b200 import lcnn
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch_conv64(x_nchw, f, stride, pad):
+    import torch
+
+    return torch.nn.functional.conv2d(x_nchw.double(), f.double(), stride=stride, padding=pad)
+
+
+def _check_conv(cuda, n, ci, h, w, co, fh, fw, stride, pad, layout, precision, seed=0):
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(seed)
+    x = torch.rand(n, ci, h, w, device=cuda, generator=g) * 2 - 1
+    f = torch.rand(co, ci, fh, fw, device=cuda, generator=g) * 2 - 1
+    want = _torch_conv64(x, f, stride, pad)
+    bound = _torch_conv64(x.abs(), f.abs(), stride, pad)
+    xin = x if layout == NCHW else x.permute(1, 2, 3, 0).contiguous()
+    t = lcnn.DeviceTensor4D(n, ci, h, w, layout, xin.reshape(-1))
+    out = lcnn.conv_forward(t, f.contiguous(), co, fh, fw, stride, pad, precision)
+    ho, wo = want.shape[2], want.shape[3]
+    got = out.data.view(n, co, ho, wo) if layout == NCHW else \
+        out.data.view(co, ho, wo, n).permute(3, 0, 1, 2)
+    got = got.double()
+    err = (got - want).abs()
+    if precision == lcnn.TF32:
+        ok = bool((err <= bound * 2.0 ** -10 + 1e-6).all())
+    else:
+        scale = torch.maximum(torch.maximum(got.abs(), want.abs()), torch.ones_like(got))
+        ok = bool((err <= 1e-5 * scale).all())
+    assert ok, (n, ci, h, w, co, fh, fw, stride, pad, layout, precision, float(err.max()))
+
+
+CASES = [  # (n, ci, h, w, co, f, stride, pad)
+    (32, 32, 9, 9, 64, 3, 1, 1),      # CI-mode K order
+    (32, 64, 13, 13, 96, 3, 1, 1),
+    (64, 3, 35, 35, 96, 11, 4, 0),    # conv1-like, WIN mode FP=16
+    (32, 96, 13, 13, 64, 5, 1, 2),    # WIN FP=8 (ci % 32 == 0 -> CI mode actually)
+    (32, 16, 10, 10, 48, 5, 2, 2),    # WIN FP=8
+    (32, 3, 12, 12, 20, 3, 1, 1),     # WIN FP=4, co < 128
+    (128, 32, 6, 6, 160, 1, 1, 0),    # 1x1, co > 128
+    (96, 64, 7, 7, 64, 3, 2, 0),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("precision", [0, 1, 2])
+def test_conv_chwn(cuda, case, precision):
+    _check_conv(cuda, *case, CHWN, precision)
+
+
+@pytest.mark.parametrize("case", [(5, 3, 9, 9, 7, 3, 1, 1), (3, 4, 11, 11, 6, 5, 2, 2),
+                                  (32, 8, 13, 13, 16, 3, 1, 1), (7, 2, 7, 7, 5, 1, 1, 0)])
+@pytest.mark.parametrize("precision", [0, 2])
+def test_conv_nchw_and_odd_batches(cuda, case, precision):
+    _check_conv(cuda, *case, NCHW, precision)
+    _check_conv(cuda, *case, CHWN, precision)
+
+
+def test_conv_reference_fixtures(cuda, ref_vectors):
+    """conv_oracle outputs from the reference binary (tests/golden)."""
+    import torch
+
+    v = ref_vectors
+    keys = sorted({k.split("_")[1] for k in v.files if k.startswith("conv_")}, key=int)
+    for k in keys:
+        n, ci, h, w, co, f, stride, pad = v[f"conv_{k}_meta"].tolist()
+        x = v[f"conv_{k}_in"]
+        filt = torch.from_numpy(v[f"conv_{k}_filt"]).to(cuda)
+        for layout in (NCHW, CHWN):
+            xin = x if layout == NCHW else C.transform(x, n, ci, h, w, NCHW, CHWN)
+            t = lcnn.DeviceTensor4D.from_host(xin, n, ci, h, w, layout, device=cuda)
+            for prec in (lcnn.FP32, lcnn.X3TF32):
+                out = lcnn.conv_forward(t, filt, co, f, f, stride, pad, prec)
+                got = out.to_host()
+                if layout == CHWN:
+                    ho = (h + 2 * pad - f) // stride + 1
+                    wo = (w + 2 * pad - f) // stride + 1
+                    got = C.transform(got, n, co, ho, wo, CHWN, NCHW)
+                assert approx_equal(got, v[f"conv_{k}_oracle"], 1e-5), (k, layout, prec)
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 128, 128), (96, 300, 64), (257, 129, 200),
+                                   (128, 4096, 9216), (1000, 128, 4096), (33, 17, 13),
+                                   (64, 1000, 4096)])
+@pytest.mark.parametrize("precision", [0, 1, 2])
+def test_gemm(cuda, m, n, k, precision):
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(m * n + k)
+    a = torch.rand(m, k, device=cuda, generator=g) * 2 - 1
+    b = torch.rand(k, n, device=cuda, generator=g) * 2 - 1
+    want = a.double() @ b.double()
+    got = lcnn.gemm(a.reshape(-1), b.reshape(-1), m, n, k, precision).view(m, n).double()
+    err = (got - want).abs()
+    if precision == lcnn.TF32:
+        bound = a.abs().double() @ b.abs().double()
+        assert bool((err <= bound * 2.0 ** -10 + 1e-6).all()), float(err.max())
+    else:
+        scale = torch.maximum(torch.maximum(got.abs(), want.abs()), torch.ones_like(got))
+        assert bool((err <= 1e-5 * scale).all()), float(err.max())
+
+
+def test_fc_identity_and_hand_product(cuda):
+    """test_softmax.cpp:156-190: identity weights are exact, [1 2]x[3;4] = 11."""
+    import torch
+
+    x = torch.from_numpy(rng_uniform(9, 24, -5, 5)).to(cuda)
+    eye = torch.eye(6, device=cuda).reshape(-1)
+    assert torch.equal(lcnn.gemm(x, eye, 4, 6, 6, lcnn.FP32), x)
+    a = torch.tensor([1.0, 2.0], device=cuda)
+    b = torch.tensor([3.0, 4.0], device=cuda)
+    for prec in (0, 1, 2):
+        assert float(lcnn.gemm(a, b, 1, 1, 2, prec)[0]) == 11.0
