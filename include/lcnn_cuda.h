@@ -210,6 +210,21 @@ lcnn_status lcnn_conv_forward(const float* src, const float* filters,
                               uint32_t pad, int precision, void* d_workspace,
                               size_t workspace_bytes, void* stream);
 
+/* == conv_oracle (conv.cpp:53-93): fp64 accumulation, any input layout,
+ * NCHW output.  Ground truth, not a hot op. */
+lcnn_status lcnn_conv_oracle(const float* src, const float* filters, float* dst,
+                             uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                             int layout, uint32_t c_o, uint32_t f_h,
+                             uint32_t f_w, uint32_t stride, uint32_t pad,
+                             void* stream);
+
+/* == im2col (conv.cpp:215-250): NCHW input (LayoutError otherwise) unrolled
+ * to a (c_i*f_h*f_w) x (n*h_out*w_out) row-major matrix, padded taps 0. */
+lcnn_status lcnn_im2col(const float* src, float* dst, uint32_t n, uint32_t c_i,
+                        uint32_t h, uint32_t w, int layout, uint32_t f_h,
+                        uint32_t f_w, uint32_t stride, uint32_t pad,
+                        void* stream);
+
 /* Bytes of device workspace lcnn_gemm needs (0 unless 3xTF32). */
 size_t lcnn_gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k,
                                  int precision);

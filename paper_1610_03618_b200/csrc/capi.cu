@@ -377,6 +377,50 @@ lcnn_status lcnn_conv_forward(const float* src, const float* filters, float* dst
   return ok();
 }
 
+lcnn_status lcnn_conv_oracle(const float* src, const float* filters, float* dst, uint32_t n,
+                             uint32_t c_i, uint32_t h, uint32_t w, int layout, uint32_t c_o,
+                             uint32_t f_h, uint32_t f_w, uint32_t stride, uint32_t pad,
+                             void* stream) {
+  if (!src || !filters || !dst) return fail(LCNN_EINVAL, "conv: null pointer");
+  if (!valid_layout(layout)) return fail(LCNN_EINVAL, "conv_oracle: bad layout code");
+  lcnn_status st = check_volume(n, c_i, h, w, "Tensor4D");
+  if (st != LCNN_OK) return st;
+  st = check_volume(c_o, c_i, f_h, f_w, "FilterBank");
+  if (st != LCNN_OK) return st;
+  uint32_t ho = 0, wo = 0;
+  st = lcnn_conv_output_extents(h, w, f_h, f_w, stride, pad, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  uint64_t sn, sc, sh, sw;
+  switch (layout) {
+    case LCNN_NCHW: sw = 1; sh = w; sc = uint64_t{h} * w; sn = uint64_t{c_i} * h * w; break;
+    case LCNN_CHWN: sn = 1; sw = n; sh = uint64_t{w} * n; sc = uint64_t{h} * w * n; break;
+    case LCNN_NHWC: sc = 1; sw = c_i; sh = uint64_t{w} * c_i; sn = uint64_t{h} * w * c_i; break;
+    default: sn = 1; sc = n; sw = uint64_t{c_i} * n; sh = uint64_t{w} * c_i * n; break;
+  }
+  lcnn_impl::ConvArgs a{src, filters, dst, n, c_i, h, w, c_o, f_h, f_w, stride, pad, ho, wo,
+                        layout, LCNN_PREC_FP32, nullptr};
+  cudaError_t e = lcnn_impl::launch_conv_oracle(a, sn, sc, sh, sw, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "conv_oracle");
+  return ok();
+}
+
+lcnn_status lcnn_im2col(const float* src, float* dst, uint32_t n, uint32_t c_i, uint32_t h,
+                        uint32_t w, int layout, uint32_t f_h, uint32_t f_w, uint32_t stride,
+                        uint32_t pad, void* stream) {
+  if (!src || !dst) return fail(LCNN_EINVAL, "im2col: null pointer");
+  if (layout != LCNN_NCHW) return fail(LCNN_ELAYOUT, "im2col: input must be NCHW");
+  lcnn_status st = check_volume(n, c_i, h, w, "Tensor4D");
+  if (st != LCNN_OK) return st;
+  uint32_t ho = 0, wo = 0;
+  st = lcnn_conv_output_extents(h, w, f_h, f_w, stride, pad, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  lcnn_impl::ConvArgs a{src, nullptr, dst, n, c_i, h, w, 1, f_h, f_w, stride, pad, ho, wo,
+                        layout, LCNN_PREC_FP32, nullptr};
+  cudaError_t e = lcnn_impl::launch_im2col(a, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "im2col");
+  return ok();
+}
+
 lcnn_status lcnn_gemm(const float* a, const float* b, float* c, uint64_t m, uint64_t n,
                       uint64_t k, int precision, void* d_workspace, size_t workspace_bytes,
                       void* stream) {

@@ -11,7 +11,8 @@
 // The GEMM N index (oh, ow, n) is exactly the CHWN output order, so the
 // accumulator tile stores straight into the output.  B tiles are TMA boxes of
 // the 4D input (n, w, h, c) -- the batch is contiguous, so every k-row of a
-// tile is 32 images (128 B) of one input pixel: an MN-major SW128 operand.
+// tile is 32 images (128 B) of one input pixel: an MN-major operand in the
+// SWIZZLE_128B_BASE32B layout tf32 requires.
 // Padding is TMA out-of-bounds zero fill (negative / overflowing h, w
 // coordinates).  Two K orderings:
 //   CI  (C_i % 32 == 0): k = (fh, fw, ci); a k-block is 32 channels of one
@@ -163,8 +164,9 @@ __global__ void __launch_bounds__(256)
     t /= g.Wo;
     const uint32_t oh = static_cast<uint32_t>(t % g.Ho);
     const uint32_t co = static_cast<uint32_t>(t / g.Ho);
-    float acc = 0.0f;
-    for (uint32_t ci = 0; ci < g.Ci; ++ci)
+    double total = 0.0;  // conv.cpp:121-139: fp32 window sums, fp64 total
+    for (uint32_t ci = 0; ci < g.Ci; ++ci) {
+      float acc = 0.0f;
       for (uint32_t fh = 0; fh < g.FH; ++fh) {
         const int32_t ih = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
         if (ih < 0 || ih >= static_cast<int32_t>(g.H)) continue;
@@ -176,7 +178,9 @@ __global__ void __launch_bounds__(256)
                      acc);
         }
       }
-    y[i] = acc;
+      total += acc;
+    }
+    y[i] = static_cast<float>(total);
   }
 }
 
@@ -192,8 +196,9 @@ __global__ void __launch_bounds__(256)
     t /= g.Ho;
     const uint32_t co = static_cast<uint32_t>(t % g.Co);
     const uint32_t n = static_cast<uint32_t>(t / g.Co);
-    float acc = 0.0f;
+    double total = 0.0;  // conv.cpp:175-189: fp32 window sums, fp64 total
     for (uint32_t ci = 0; ci < g.Ci; ++ci) {
+      float acc = 0.0f;
       const float* plane = x + (static_cast<uint64_t>(n) * g.Ci + ci) * g.H * g.W;
       for (uint32_t fh = 0; fh < g.FH; ++fh) {
         const int32_t ih = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
@@ -206,8 +211,62 @@ __global__ void __launch_bounds__(256)
                      acc);
         }
       }
+      total += acc;
     }
-    y[i] = acc;
+    y[i] = static_cast<float>(total);
+  }
+}
+
+// fp64 ground truth (conv.cpp:53-93): any input layout via strides, NCHW out.
+__global__ void conv_oracle_kernel(const float* __restrict__ x, const float* __restrict__ f,
+                                   float* __restrict__ y, ConvGeomSimt g, uint64_t sn, uint64_t sc,
+                                   uint64_t sh, uint64_t sw) {
+  const uint64_t total = static_cast<uint64_t>(g.N) * g.Co * g.Ho * g.Wo;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t ow = static_cast<uint32_t>(i % g.Wo);
+    uint64_t t = i / g.Wo;
+    const uint32_t oh = static_cast<uint32_t>(t % g.Ho);
+    t /= g.Ho;
+    const uint32_t co = static_cast<uint32_t>(t % g.Co);
+    const uint32_t n = static_cast<uint32_t>(t / g.Co);
+    double acc = 0.0;
+    for (uint32_t ci = 0; ci < g.Ci; ++ci)
+      for (uint32_t fh = 0; fh < g.FH; ++fh) {
+        const int32_t ih = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
+        if (ih < 0 || ih >= static_cast<int32_t>(g.H)) continue;
+        for (uint32_t fw = 0; fw < g.FW; ++fw) {
+          const int32_t iw = static_cast<int32_t>(ow * g.S + fw) - static_cast<int32_t>(g.P);
+          if (iw < 0 || iw >= static_cast<int32_t>(g.W)) continue;
+          acc += static_cast<double>(x[n * sn + ci * sc + ih * sh + iw * sw]) *
+                 static_cast<double>(f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw]);
+        }
+      }
+    y[i] = static_cast<float>(acc);
+  }
+}
+
+// Receptive-field unroll of NCHW input (conv.cpp:215-250): rows (ci, fh, fw),
+// columns (n, oh, ow); padded taps are zero.
+__global__ void im2col_kernel(const float* __restrict__ x, float* __restrict__ m, ConvGeomSimt g) {
+  const uint64_t cols = static_cast<uint64_t>(g.N) * g.Ho * g.Wo;
+  const uint64_t total = static_cast<uint64_t>(g.Ci) * g.FH * g.FW * cols;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t col = i % cols, row = i / cols;
+    const uint32_t ow = static_cast<uint32_t>(col % g.Wo);
+    const uint64_t t = col / g.Wo;
+    const uint32_t oh = static_cast<uint32_t>(t % g.Ho);
+    const uint32_t n = static_cast<uint32_t>(t / g.Ho);
+    const uint32_t fw = static_cast<uint32_t>(row % g.FW);
+    const uint32_t fh = static_cast<uint32_t>((row / g.FW) % g.FH);
+    const uint32_t ci = static_cast<uint32_t>(row / (static_cast<uint64_t>(g.FW) * g.FH));
+    const int32_t ih = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
+    const int32_t iw = static_cast<int32_t>(ow * g.S + fw) - static_cast<int32_t>(g.P);
+    float v = 0.0f;
+    if (ih >= 0 && ih < static_cast<int32_t>(g.H) && iw >= 0 && iw < static_cast<int32_t>(g.W))
+      v = x[((static_cast<uint64_t>(n) * g.Ci + ci) * g.H + ih) * g.W + iw];
+    m[i] = v;
   }
 }
 
@@ -215,12 +274,26 @@ __global__ void __launch_bounds__(256)
 
 namespace lcnn_impl {
 
+cudaError_t launch_conv_oracle(const ConvArgs& a, uint64_t sn, uint64_t sc, uint64_t sh,
+                               uint64_t sw, cudaStream_t s) {
+  lcnn_dev::ConvGeomSimt g{a.n, a.ci, a.h, a.w, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo};
+  lcnn_dev::conv_oracle_kernel<<<148 * 16, 256, 0, s>>>(a.src, a.filters, a.dst, g, sn, sc, sh, sw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_im2col(const ConvArgs& a, cudaStream_t s) {
+  lcnn_dev::ConvGeomSimt g{a.n, a.ci, a.h, a.w, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo};
+  lcnn_dev::im2col_kernel<<<148 * 16, 256, 0, s>>>(a.src, a.dst, g);
+  return cudaGetLastError();
+}
+
 using namespace lcnn_dev;
 
 bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer,
-                  uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer);
+                  uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer, bool mn_major);
 bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t* dims,
-               const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides);
+               const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides,
+               bool mn_major);
 cudaError_t launch_split_hilo(const float* x, float* hi, float* lo, uint64_t count,
                               cudaStream_t s);
 
@@ -308,8 +381,8 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, p.K);
   ChwnConvLoader L;
   const uint64_t K = p.K;
-  if (!make_tmap_2d(&L.a[0], a_hi, K, a.co, K * 4, kTcBK, kTcBM) ||
-      !make_tmap_2d(&L.a[1], x3 ? a_lo : a_hi, K, a.co, K * 4, kTcBK, kTcBM))
+  if (!make_tmap_2d(&L.a[0], a_hi, K, a.co, K * 4, kTcBK, kTcBM, false) ||
+      !make_tmap_2d(&L.a[1], x3 ? a_lo : a_hi, K, a.co, K * 4, kTcBK, kTcBM, false))
     return cudaErrorInvalidValue;
   const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
   const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
@@ -320,8 +393,8 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   } else {
     box[0] = 32; box[1] = p.g.FP; box[2] = 1; box[3] = p.g.CIB;
   }
-  if (!make_tmap(&L.b[0], b_hi, 4, dims, pitch, box, nullptr) ||
-      !make_tmap(&L.b[1], b_lo, 4, dims, pitch, box, nullptr))
+  if (!make_tmap(&L.b[0], b_hi, 4, dims, pitch, box, nullptr, true) ||
+      !make_tmap(&L.b[1], b_lo, 4, dims, pitch, box, nullptr, true))
     return cudaErrorInvalidValue;
   L.g = p.g;
   L.kb = p.K / kTcBK;

@@ -17,9 +17,9 @@
 // Row-major B (N contiguous) is consumed as an MN-major operand directly, so
 // neither operand is ever transposed or re-packed in HBM.
 //
-// Precision modes: TF32 (one MMA chain); 3xTF32 runs the same kernel over a
-// K' = 3K problem [A_hi | A_hi | A_lo] x [B_hi ; B_lo ; B_hi] built by a split
-// kernel (hi = x rounded to tf32, lo = x - hi), giving ~fp32 accuracy.
+// Precision modes: TF32 (one MMA chain); 3xTF32 chains three operand sets
+// hi*hi + hi*lo + lo*hi into the same accumulator (hi = x rounded to tf32,
+// lo = tf32(x - hi), split by one elementwise kernel), giving ~fp32 accuracy.
 #include <cuda.h>
 #include <stdio.h>
 
@@ -98,8 +98,10 @@ __global__ void split_hilo_kernel(const float* __restrict__ x, float* __restrict
   }
 }
 
-// fp32 CUDA-core GEMM (64x64 tile, 4x4 per thread): exact fp32 products and
-// fp32 accumulation, for LCNN_PREC_FP32 and shapes TMA cannot describe.
+// fp32 CUDA-core GEMM (64x64 tile, 4x4 per thread) with the reference's
+// accumulation split (conv.cpp:252-293): fp32 products and 16-deep fp32
+// partial sums, flushed into an fp64 running total -- for LCNN_PREC_FP32 and
+// shapes TMA cannot describe.
 __global__ void __launch_bounds__(256)
     gemm_fp32_simt_kernel(const float* __restrict__ a, const float* __restrict__ b,
                           float* __restrict__ c, uint64_t M, uint64_t N, uint64_t K) {
@@ -107,8 +109,9 @@ __global__ void __launch_bounds__(256)
   __shared__ float sb[16][64 + 4];
   const uint64_t m0 = blockIdx.y * 64ull, n0 = blockIdx.x * 64ull;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  float acc[4][4] = {};
+  double master[4][4] = {};
   for (uint64_t k0 = 0; k0 < K; k0 += 16) {
+    float acc[4][4] = {};
     for (int i = threadIdx.x; i < 16 * 64; i += 256) {
       const int kk = i % 16, mm = i / 16;
       sa[kk][mm] = (m0 + mm < M && k0 + kk < K) ? a[(m0 + mm) * K + k0 + kk] : 0.0f;
@@ -128,6 +131,10 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) master[i][j] += acc[i][j];
     __syncthreads();
   }
 #pragma unroll
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint64_t m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
-      if (m < M && n < N) c[m * N + n] = acc[i][j];
+      if (m < M && n < N) c[m * N + n] = static_cast<float>(master[i][j]);
     }
 }
 
@@ -169,7 +176,7 @@ EncodeTiledFn encode_fn() {
 
 // 2D fp32 tensor map: dims {inner, outer}, row pitch in bytes, box {bi, bo}.
 bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer,
-                  uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+                  uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer, bool mn_major) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[2] = {inner, outer};
@@ -177,13 +184,15 @@ bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t ou
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
-             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
 bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t* dims,
-               const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides) {
+               const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides,
+               bool mn_major) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t d[5];
@@ -196,7 +205,8 @@ bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t*
     if (i + 1 < rank) s[i] = pitches_bytes[i];
   }
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base), d, s, b, e,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
@@ -238,10 +248,10 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
     if (e != cudaSuccess) return e;
     a0 = ahi; a1 = alo; b0 = bhi; b1 = blo;
   }
-  if (!make_tmap_2d(&L.a[0], a0, k, m, k * 4, kTcBK, kTcBM) ||
-      !make_tmap_2d(&L.a[1], a1, k, m, k * 4, kTcBK, kTcBM) ||
-      !make_tmap_2d(&L.b[0], b0, n, k, n * 4, 32, kTcBK) ||
-      !make_tmap_2d(&L.b[1], b1, n, k, n * 4, 32, kTcBK))
+  if (!make_tmap_2d(&L.a[0], a0, k, m, k * 4, kTcBK, kTcBM, false) ||
+      !make_tmap_2d(&L.a[1], a1, k, m, k * 4, kTcBK, kTcBM, false) ||
+      !make_tmap_2d(&L.b[0], b0, n, k, n * 4, 32, kTcBK, true) ||
+      !make_tmap_2d(&L.b[1], b1, n, k, n * 4, 32, kTcBK, true))
     return cudaErrorInvalidValue;
   L.kb = static_cast<uint32_t>((k + kTcBK - 1) / kTcBK);
   L.segs = precision == LCNN_PREC_3XTF32 ? 3 : 1;

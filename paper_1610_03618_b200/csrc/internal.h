@@ -54,6 +54,9 @@ struct ConvArgs {
   void* workspace;
 };
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s);
+cudaError_t launch_conv_oracle(const ConvArgs& a, uint64_t sn, uint64_t sc, uint64_t sh,
+                               uint64_t sw, cudaStream_t s);
+cudaError_t launch_im2col(const ConvArgs& a, cudaStream_t s);
 size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w,
                             uint32_t co, uint32_t fh, uint32_t fw, int precision);
 bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a,

@@ -5,7 +5,9 @@
 // Descriptor encodings follow the PTX ISA "tcgen05 matrix descriptors"
 // (cross-checked against the vendored CuTe header cute/arch/mma_sm100_desc.hpp):
 //   smem desc : [0,14) start>>4 | [16,30) LBO>>4 | [32,46) SBO>>4 |
-//               [46,48) version=1 | [61,64) layout (2 = SWIZZLE_128B)
+//               [46,48) version=1 | [61,64) layout (2 = SWIZZLE_128B,
+//               1 = SWIZZLE_128B_BASE32B for MN-major tf32, verified on B200
+//               with scripts/tc_debug.cu)
 //   idesc     : [4,6) D fmt (1=f32) | [7,10) A fmt | [10,13) B fmt (2=tf32) |
 //               [15] A major (0=K) | [16] B major (1=MN) | [17,23) N>>3 |
 //               [24,29) M>>4
@@ -136,18 +138,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 }
 
 // ---- descriptors ----------------------------------------------------------
+// layout: 2 = SWIZZLE_128B (K-major operands), 1 = SWIZZLE_128B_BASE32B (the
+// only legal 128-byte swizzle for MN-major 32-bit operands: 32-byte swizzle
+// atoms, 4-row groups; filled by TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p, uint32_t lbo_bytes,
-                                                    uint32_t sbo_bytes) {
+                                                    uint32_t sbo_bytes, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((smem_u32(p) >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= static_cast<uint64_t>(1) << 46;  // version (Blackwell)
-  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  d |= static_cast<uint64_t>(layout & 7) << 61;
   return d;
 }
 
-constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, bool a_mn_major, bool b_mn_major) {
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn_major ? 1u : 0u) << 15) |
          ((b_mn_major ? 1u : 0u) << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }

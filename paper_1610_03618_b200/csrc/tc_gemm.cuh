@@ -10,8 +10,9 @@
 // thread), warps 2..5 = epilogue (TMEM lane quarter = warp % 4).
 // A stage is BK = 32 fp32 of K: A 16 KB + B 16 KB; kStages deep ring.
 // A K-step of the MMA is 8 tf32 (32 bytes): K-major operands advance their
-// descriptor start by 32 B inside the 128-B swizzle row, MN-major operands
-// by one 8-row swizzle atom (1024 B).
+// descriptor start by 32 B inside the 128-B swizzle row (SWIZZLE_128B),
+// MN-major operands by 8 rows (1024 B) of the SWIZZLE_128B_BASE32B layout
+// that tf32 requires for MN-major (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
 // The pipeline can chain several "segments" (sets of operands) into one
 // accumulator -- used by the 3xTF32 mode (hi*hi + hi*lo + lo*hi).
 #pragma once
@@ -94,7 +95,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int k = 0; k < kTcBK / 8; ++k) {
         const uint64_t ad = smem_desc_sw128(sa + k * 32, 16, 1024);
-        const uint64_t bd = Loader::kBMajorMN ? smem_desc_sw128(sb + k * 1024, 4096, 1024)
+        // MN-major B: 32-float atoms 4096 B apart along N, 4-row groups 512 B
+        // apart along K (BASE32B); one MMA K-step = 8 rows = 1024 B.
+        const uint64_t bd = Loader::kBMajorMN ? smem_desc_sw128(sb + k * 1024, 4096, 512, 1)
                                               : smem_desc_sw128(sb + k * 32, 16, 1024);
         mma_tf32(tmem, ad, bd, idesc, (it | k) != 0);
       }

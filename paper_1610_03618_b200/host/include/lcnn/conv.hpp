@@ -1,0 +1,46 @@
+// Convolution (drop-in for the reference's conv.hpp).  conv_direct (CHWN and
+// NCHW) and conv_gemm run on the GPU (tcgen05 implicit GEMM for CHWN in the
+// TF32 modes, fp32 CUDA cores in the default FP32 mode, see device.hpp);
+// conv_oracle is the fp64 ground truth; conv_fft keeps its contract (stride 1
+// only) and is served by the same GPU convolution -- no FFT is performed.
+#pragma once
+
+#include <cstdint>
+#include <utility>
+
+#include "lcnn/device.hpp"
+#include "lcnn/tensor.hpp"
+
+namespace lcnn {
+
+struct ConvParams {
+  std::uint32_t stride = 1;
+  std::uint32_t pad = 0;
+};
+
+std::pair<std::uint32_t, std::uint32_t> conv_output_extents(
+    std::uint32_t h, std::uint32_t w, std::uint32_t f_h, std::uint32_t f_w,
+    const ConvParams& p);
+
+Tensor4D conv_oracle(const Tensor4D& in, const FilterBank& f,
+                     const ConvParams& p);
+Tensor4D conv_direct(const Tensor4D& in, const FilterBank& f,
+                     const ConvParams& p);
+Matrix im2col(const Tensor4D& in, std::uint32_t f_h, std::uint32_t f_w,
+              const ConvParams& p);
+Tensor4D conv_gemm(const Tensor4D& in, const FilterBank& f,
+                   const ConvParams& p);
+Tensor4D conv_fft(const Tensor4D& in, const FilterBank& f,
+                  const ConvParams& p);
+
+void gemm_blocked(const float* a, const float* b, float* c, std::uint64_t m,
+                  std::uint64_t n, std::uint64_t k);
+Matrix gemm_blocked(const Matrix& a, const Matrix& b);
+
+// Device-resident convolution; filters already in HBM as (c_o, c_i, f_h, f_w).
+DeviceTensor4D conv_forward(const DeviceTensor4D& in, const float* d_filters,
+                            std::uint32_t c_o, std::uint32_t f_h,
+                            std::uint32_t f_w, const ConvParams& p,
+                            int precision);
+
+}  // namespace lcnn

@@ -1,0 +1,86 @@
+// Device-resident extension of the lcnn API (not in the reference): HBM
+// buffers, a per-host-thread CUDA stream, and device overloads of the hot
+// ops so whole networks run without host round trips.  Host-tensor calls in
+// layout.hpp / pool.hpp / softmax.hpp / conv.hpp are thin wrappers: upload,
+// one C-ABI kernel call (include/lcnn_cuda.h), download.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+
+#include "lcnn/tensor.hpp"
+
+namespace lcnn {
+
+// Owning HBM allocation served from a per-device caching pool; returning a
+// block to the pool does not synchronise.
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t bytes);
+  ~DeviceBuffer();
+  DeviceBuffer(DeviceBuffer&& o) noexcept;
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+
+  float* f() const { return static_cast<float*>(ptr_); }
+  void* get() const { return ptr_; }
+  std::size_t bytes() const { return bytes_; }
+
+ private:
+  void* ptr_ = nullptr;
+  std::size_t bytes_ = 0;
+};
+
+// The stream every lcnn call issued from this host thread is ordered on.
+void* current_stream();
+// Block until the calling thread's stream has drained.
+void synchronize();
+// Throw the lcnn exception matching a non-OK lcnn_status (with the library's
+// message), e.g. PlanError for LCNN_EPLAN.
+void throw_status(int status);
+inline void check_status(int status) {
+  if (status != 0) throw_status(status);
+}
+
+class DeviceTensor4D {
+ public:
+  DeviceTensor4D(std::uint32_t n, std::uint32_t c, std::uint32_t h,
+                 std::uint32_t w, Layout layout);
+  static DeviceTensor4D upload(const Tensor4D& t);
+  Tensor4D download() const;
+
+  std::uint32_t n() const { return n_; }
+  std::uint32_t c() const { return c_; }
+  std::uint32_t h() const { return h_; }
+  std::uint32_t w() const { return w_; }
+  Layout layout() const { return layout_; }
+  void set_layout_tag(Layout l) { layout_ = l; }
+  std::uint64_t size() const { return std::uint64_t{n_} * c_ * h_ * w_; }
+  float* data() const { return buf_->f(); }
+
+ private:
+  std::uint32_t n_, c_, h_, w_;
+  Layout layout_;
+  std::shared_ptr<DeviceBuffer> buf_;
+};
+
+struct DeviceMatrix {
+  std::uint32_t rows = 0, cols = 0;
+  std::shared_ptr<DeviceBuffer> buf;
+  DeviceMatrix() = default;
+  DeviceMatrix(std::uint32_t r, std::uint32_t c);
+  static DeviceMatrix upload(const Matrix& m);
+  Matrix download() const;
+  float* data() const { return buf->f(); }
+};
+
+// Convolution / GEMM arithmetic for the host API (lcnn_precision codes).
+// Default FP32 keeps the reference's 1e-5 tolerances; the whole-network
+// benchmark selects TF32 (tensor cores) explicitly.
+void set_dense_precision(int precision);
+int dense_precision();
+
+}  // namespace lcnn

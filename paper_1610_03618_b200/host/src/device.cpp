@@ -1,0 +1,185 @@
+// Per-thread device context: the CUDA stream every lcnn call of this host
+// thread is ordered on, a caching HBM pool (blocks are recycled on the same
+// stream, so reuse is stream-ordered and never needs a sync), and the
+// status -> exception mapping of the C ABI.
+#include "lcnn/device.hpp"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "lcnn_cuda.h"
+
+namespace lcnn {
+
+namespace {
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct ThreadContext {
+  cudaStream_t stream = nullptr;
+  int device = -1;
+  std::multimap<std::size_t, void*> free_blocks;
+  ~ThreadContext() {
+    // Process teardown: the CUDA runtime may already be gone; leak quietly.
+  }
+};
+
+thread_local ThreadContext g_ctx;
+
+ThreadContext& ctx() {
+  int dev = 0;
+  cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+  if (g_ctx.stream == nullptr || g_ctx.device != dev) {
+    cuda_ok(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking),
+            "cudaStreamCreate");
+    g_ctx.device = dev;
+    g_ctx.free_blocks.clear();
+  }
+  return g_ctx;
+}
+
+std::size_t round_bytes(std::size_t b) {
+  if (b < 256) return 256;
+  if (b < (1u << 20)) {  // powers of two below 1 MiB
+    std::size_t r = 256;
+    while (r < b) r <<= 1;
+    return r;
+  }
+  const std::size_t mb = 1u << 20;  // 1 MiB granules above
+  return (b + mb - 1) / mb * mb;
+}
+
+int initial_precision() {
+  const char* env = std::getenv("LCNN_DENSE_PRECISION");
+  if (!env) return LCNN_PREC_FP32;
+  if (std::strcmp(env, "tf32") == 0) return LCNN_PREC_TF32;
+  if (std::strcmp(env, "3xtf32") == 0) return LCNN_PREC_3XTF32;
+  return LCNN_PREC_FP32;
+}
+
+std::atomic<int> g_precision{initial_precision()};
+
+}  // namespace
+
+DeviceBuffer::DeviceBuffer(std::size_t bytes) {
+  ThreadContext& c = ctx();
+  bytes_ = round_bytes(bytes);
+  auto it = c.free_blocks.lower_bound(bytes_);
+  if (it != c.free_blocks.end() && it->first <= bytes_ * 2) {
+    ptr_ = it->second;
+    bytes_ = it->first;
+    c.free_blocks.erase(it);
+    return;
+  }
+  cudaError_t e = cudaMalloc(&ptr_, bytes_);
+  if (e != cudaSuccess) {
+    // release cached blocks and retry once
+    cudaStreamSynchronize(c.stream);
+    for (auto& kv : c.free_blocks) cudaFree(kv.second);
+    c.free_blocks.clear();
+    cudaGetLastError();
+    cuda_ok(cudaMalloc(&ptr_, bytes_), "cudaMalloc");
+  }
+}
+
+DeviceBuffer::~DeviceBuffer() {
+  if (ptr_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
+}
+
+DeviceBuffer::DeviceBuffer(DeviceBuffer&& o) noexcept : ptr_(o.ptr_), bytes_(o.bytes_) {
+  o.ptr_ = nullptr;
+  o.bytes_ = 0;
+}
+
+DeviceBuffer& DeviceBuffer::operator=(DeviceBuffer&& o) noexcept {
+  if (this != &o) {
+    if (ptr_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
+    ptr_ = o.ptr_;
+    bytes_ = o.bytes_;
+    o.ptr_ = nullptr;
+    o.bytes_ = 0;
+  }
+  return *this;
+}
+
+void* current_stream() { return ctx().stream; }
+
+void synchronize() { cuda_ok(cudaStreamSynchronize(ctx().stream), "cudaStreamSynchronize"); }
+
+void throw_status(int status) {
+  const std::string msg = lcnn_last_error();
+  switch (status) {
+    case LCNN_ESHAPE: throw ShapeError(msg);
+    case LCNN_EINDEX: throw IndexError(msg);
+    case LCNN_ELAYOUT: throw LayoutError(msg);
+    case LCNN_EPLAN: throw PlanError(msg);
+    case LCNN_EFORMAT: throw FormatError(msg);
+    case LCNN_EDOMAIN: throw DomainError(msg);
+    case LCNN_EUNSUPPORTED: throw UnsupportedError(msg);
+    case LCNN_EVALIDATION: throw ValidationError(msg);
+    case LCNN_ECALIBRATION: throw CalibrationError(msg);
+    default: throw Error(std::string(lcnn_status_name(status)) + ": " + msg);
+  }
+}
+
+DeviceTensor4D::DeviceTensor4D(std::uint32_t n, std::uint32_t c, std::uint32_t h,
+                               std::uint32_t w, Layout layout)
+    : n_(n), c_(c), h_(h), w_(w), layout_(layout) {
+  if (!n || !c || !h || !w) throw ShapeError("Tensor4D: all dims must be >= 1");
+  if (std::uint64_t{n} * c * h * w > 0xffffffffull)
+    throw ShapeError("Tensor4D: dim product overflows");
+  buf_ = std::make_shared<DeviceBuffer>(size() * sizeof(float));
+}
+
+DeviceTensor4D DeviceTensor4D::upload(const Tensor4D& t) {
+  DeviceTensor4D d(t.n(), t.c(), t.h(), t.w(), t.layout());
+  cuda_ok(cudaMemcpyAsync(d.data(), t.data(), t.size() * sizeof(float), cudaMemcpyHostToDevice,
+                          static_cast<cudaStream_t>(current_stream())),
+          "upload");
+  return d;
+}
+
+Tensor4D DeviceTensor4D::download() const {
+  Tensor4D t(n_, c_, h_, w_, layout_);
+  cuda_ok(cudaMemcpyAsync(t.data(), data(), size() * sizeof(float), cudaMemcpyDeviceToHost,
+                          static_cast<cudaStream_t>(current_stream())),
+          "download");
+  synchronize();
+  return t;
+}
+
+DeviceMatrix::DeviceMatrix(std::uint32_t r, std::uint32_t c)
+    : rows(r), cols(c),
+      buf(std::make_shared<DeviceBuffer>(std::uint64_t{r} * c * sizeof(float) + 16)) {}
+
+DeviceMatrix DeviceMatrix::upload(const Matrix& m) {
+  DeviceMatrix d(m.rows, m.cols);
+  if (!m.data.empty())
+    cuda_ok(cudaMemcpyAsync(d.data(), m.data.data(), m.data.size() * sizeof(float),
+                            cudaMemcpyHostToDevice, static_cast<cudaStream_t>(current_stream())),
+            "upload");
+  return d;
+}
+
+Matrix DeviceMatrix::download() const {
+  Matrix m(rows, cols);
+  if (!m.data.empty())
+    cuda_ok(cudaMemcpyAsync(m.data.data(), data(), m.data.size() * sizeof(float),
+                            cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(current_stream())),
+            "download");
+  synchronize();
+  return m;
+}
+
+void set_dense_precision(int precision) { g_precision.store(precision); }
+int dense_precision() { return g_precision.load(); }
+
+}  // namespace lcnn
