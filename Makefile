@@ -10,8 +10,23 @@ OBJDIR  := build/obj
 CU      := transform pool softmax gemm conv capi
 OBJS    := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU)))
 LIB     := $(PKG)/lib/liblcnn_cuda.so
+# C++ drop-in host API (lcnn:: of the reference headers) over the C ABI
+CXX     ?= g++
+CUDA    ?= /usr/local/cuda
+HOSTSRC := $(wildcard $(PKG)/host/src/*.cpp)
+HOSTOBJ := $(patsubst $(PKG)/host/src/%.cpp,$(OBJDIR)/host_%.o,$(HOSTSRC))
+HOSTLIB := $(PKG)/lib/liblcnn.so
+HOSTFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -I$(PKG)/host/include -Iinclude -I$(CUDA)/include
 
-all: $(LIB) oracle
+all: $(LIB) $(HOSTLIB) oracle
+
+$(OBJDIR)/host_%.o: $(PKG)/host/src/%.cpp $(wildcard $(PKG)/host/include/lcnn/*.hpp) $(PKG)/host/src/json_lite.hpp include/lcnn_cuda.h
+	@mkdir -p $(OBJDIR)
+	$(CXX) $(HOSTFLAGS) -c $< -o $@
+
+$(HOSTLIB): $(HOSTOBJ) $(LIB)
+	$(CXX) -shared -o $@ $(HOSTOBJ) -L$(PKG)/lib -llcnn_cuda -Wl,-rpath,'$$ORIGIN' \
+	  -L$(CUDA)/lib64 -lcudart_static -lpthread -ldl -lrt
 
 $(OBJDIR)/%.o: $(SRC)/%.cu $(SRC)/common.cuh $(SRC)/internal.h $(SRC)/tc.cuh $(SRC)/tc_gemm.cuh include/lcnn_cuda.h
 	@mkdir -p $(OBJDIR)

@@ -60,6 +60,7 @@ class DeviceTensor4D {
   void set_layout_tag(Layout l) { layout_ = l; }
   std::uint64_t size() const { return std::uint64_t{n_} * c_ * h_ * w_; }
   float* data() const { return buf_->f(); }
+  const std::shared_ptr<DeviceBuffer>& buffer() const { return buf_; }
 
  private:
   std::uint32_t n_, c_, h_, w_;
