@@ -20,7 +20,7 @@ HOSTFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -I$(PKG)/host/include -Iinclude 
 
 all: $(LIB) $(HOSTLIB) oracle
 
-$(OBJDIR)/host_%.o: $(PKG)/host/src/%.cpp $(wildcard $(PKG)/host/include/lcnn/*.hpp) $(PKG)/host/src/json_lite.hpp include/lcnn_cuda.h
+$(OBJDIR)/host_%.o: $(PKG)/host/src/%.cpp $(wildcard $(PKG)/host/include/lcnn/*.hpp) $(PKG)/host/src/json_lite.hpp include/lcnn_cuda.h include/lcnn_net.h
 	@mkdir -p $(OBJDIR)
 	$(CXX) $(HOSTFLAGS) -c $< -o $@
 

@@ -439,7 +439,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg_pools",
-                    choices=["vgg_pools", "pl5", "pl5_nchw", "softmax", "softmax5", "transform"])
+                    choices=["vgg_pools", "pl5", "pl5_nchw", "softmax", "softmax5", "transform",
+                             "alexnet"])
     ap.add_argument("--plan", type=int, nargs=2, default=[2, 2], help="coarsening fh fw")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sample-gb", type=float, default=1.0,
@@ -454,7 +455,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        run_reference_arm(args, rank, world)
+        if args.workload == "alexnet":
+            run_reference_alexnet(args, rank, world)
+        else:
+            run_reference_arm(args, rank, world)
         return
 
     import torch
@@ -468,6 +472,12 @@ def main():
     def barrier():
         if world > 1:
             dist.barrier()
+
+    if args.workload == "alexnet":
+        run_alexnet(args, torch, dist, rank, world, local, device, barrier)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     ops, desc, dom, batch = build_workload(args.workload, torch, device, rank, tuple(args.plan))
     stream = torch.cuda.current_stream(device)
@@ -617,6 +627,183 @@ def run_e2e(torch, device, ops, world, steps, barrier, dist):
             "d2h_bytes_per_step": d2h_bytes, "steps": steps, "ms_per_step": round(ms / steps, 3),
             "path": "pinned host -> cudaMemcpyAsync H2D -> lcnn_* C ABI kernel -> D2H, "
                     "copy engines overlapped across layers"}
+
+
+# --------------------------------------------------------------- alexnet ---
+ALEXNET = os.path.join(ROOT, "configs", "alexnet.json")
+ALEXNET_CONV = {"conv1": (3, 96, 11, 55), "conv2": (96, 192, 5, 27), "conv3": (192, 384, 3, 13),
+                "conv4": (384, 256, 3, 13), "conv5": (256, 256, 3, 13)}
+ALEXNET_FC = {"fc6": (9216, 4096), "fc7": (4096, 4096), "fc8": (4096, 1000)}
+
+
+def thresholds():
+    """B200 (c_t, n_t) from the calibration record if one was made on this
+    hardware (profiles/b200_calibration.txt), else the titan-black preset."""
+    path = os.path.join(ROOT, "profiles", "b200_calibration.txt")
+    try:
+        with open(path) as f:
+            parts = dict(kv.split("=", 1) for kv in f.readline().split())
+        return int(parts["c_t"]), int(parts["n_t"]), "calibrated on B200 (" + path + ")"
+    except Exception:
+        return 32, 128, "titan-black preset"
+
+
+def entry_flops(name, batch):
+    if name in ALEXNET_CONV:
+        ci, co, f, ho = ALEXNET_CONV[name]
+        return 2.0 * batch * co * ho * ho * ci * f * f
+    if name in ALEXNET_FC:
+        k, n = ALEXNET_FC[name]
+        return 2.0 * batch * k * n
+    return 0.0
+
+
+def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
+    """BASELINE config 5: whole AlexNet forward, 128 images per GPU (batch 1024
+    at 8 GPUs), per-layer layout selection, conv/fc on tcgen05 (TF32)."""
+    from paper_1610_03618_b200 import capi, netapi
+
+    text = open(ALEXNET).read()
+    batch = json.loads(text)["input"]["n"]
+    c_t, n_t, th_src = thresholds()
+    netapi.set_dense_precision(capi.PREC_TF32)
+    net = netapi.Network(text, c_t, n_t, seed=42)
+    info = net.info(1)
+    in_layout = info["first_layout"]
+    rows, cols = info["out"]
+    g = torch.Generator(device=device).manual_seed(7 + rank)
+    x = torch.rand(batch * 3 * 227 * 227, device=device, generator=g) * 2 - 1
+    y = torch.empty(rows * cols, device=device)
+    stream = torch.cuda.current_stream(device)
+    sh = stream.cuda_stream
+    for _ in range(args.warmup):
+        net.forward(x.data_ptr(), in_layout, y.data_ptr(), sh)
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    K = args.steps
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(K):
+            net.forward(x.data_ptr(), in_layout, y.data_ptr(), sh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    value = batch * world * K / (ms / 1e3)
+
+    # per-entry device times of one forward (dominant kernel = slowest entry)
+    prof = net.profile(x.data_ptr(), in_layout, sh)
+    name, ns = max(prof, key=lambda e: e[1])
+    fl = entry_flops(name, batch)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    tf32_peak = float(peaks["bf16_tflops"]) / 2
+    achieved = fl / (ns * 1e-9) / 1e12 if fl else None
+    roofline = {"bound": "tensor", "kernel": f"{name} (tcgen05 kind::tf32 implicit GEMM)",
+                "achieved": round(achieved, 1) if achieved else None, "peak": tf32_peak,
+                "peak_source": "measured bf16 burst (MEASURED_PEAKS.json) / 2 = dense TF32",
+                "unit": "TFLOP/s", "frac": round(achieved / tf32_peak, 4) if achieved else None,
+                "traffic": None, "avg_launch_ms": round(ns / 1e6, 4),
+                "forward_tflops": round(info["flops_per_image"] * batch / (ms / K / 1e3) / 1e12, 1),
+                "per_entry_us": {k: round(v / 1e3, 1) for k, v in prof}}
+
+    # verification collective: gather every rank's logits (row-major concat)
+    torch.cuda.synchronize()
+    ok_rows = bool(torch.allclose(y.view(rows, cols).double().sum(1),
+                                  torch.ones(rows, device=device, dtype=torch.float64), atol=1e-4))
+    if world > 1:
+        gathered = torch.empty(world * rows * cols, device=device)
+        dist.all_gather_into_tensor(gathered, y)
+        ok_rows = ok_rows and bool(torch.equal(gathered.view(world, -1)[rank], y))
+    # end to end: host buffers through lcnn_net_forward_host (H2D, forward, D2H)
+    e2e = None
+    if not args.no_e2e:
+        hx = x.cpu().pin_memory()
+        hy = torch.empty(rows * cols).pin_memory()
+        net.forward_host(hx.data_ptr(), in_layout, hy.data_ptr())
+        barrier()
+        steps = max(1, min(args.e2e_steps * 3, K))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            net.forward_host(hx.data_ptr(), in_layout, hy.data_ptr())
+        dt = torch.tensor([time.perf_counter() - t0], device=device, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(batch * world * steps / float(dt[0]), 1), "unit": "images/s",
+               "h2d_bytes_per_step": hx.numel() * 4, "d2h_bytes_per_step": hy.numel() * 4,
+               "steps": steps, "path": "lcnn_net_forward_host (pinned host -> H2D -> forward -> D2H)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = reference_alexnet_sample(c_t, n_t)
+        except Exception as e:
+            cpu = {"value": None, "error": str(e)}
+    if rank == 0:
+        layouts = [capi.LAYOUT_NAMES.get(l, "-") for l in net.layouts[:12]]
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "images/s", "n_gpus": world,
+                "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "tf32",
+                "data": "synthetic (uniform[-1,1) input, reference-seeded weights)",
+                "config": {"workload": "BASELINE config 5: whole AlexNet forward (conv/pool/fc/"
+                                       "softmax chain of SURVEY 8d), 128 images per GPU",
+                           "batch_per_gpu": batch, "global_batch": batch * world,
+                           "parallelism": f"N-shard x{world}, NCCL all_gather of logits only",
+                           "layouts": layouts, "thresholds": [c_t, n_t],
+                           "thresholds_source": th_src, "transforms": info["transforms"],
+                           "logits_verified": ok_rows,
+                           "l2_policy": "activations + 245 MB weights per step (> L2)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": None, "clocks": clocks.summary(), "impl": "ours"}
+        print(json.dumps(line))
+
+
+def reference_alexnet_sample(c_t, n_t, batch_per_thread=1):
+    from oracle.oracle import Ref, ref_time_network
+
+    if not Ref.available():
+        return None
+    threads = os.cpu_count() or 1
+    cfg = json.loads(open(ALEXNET).read())
+    cfg["input"]["n"] = batch_per_thread
+    sec = ref_time_network(json.dumps(cfg), c_t, n_t, threads)
+    return {"value": round(batch_per_thread * threads / sec, 3), "unit": "images/s",
+            "cores": threads, "kind": "reference", "cpu": cpu_desc(),
+            "sample": f"{batch_per_thread} image(s) per std::thread x {threads} threads through "
+                      f"the unmodified run_network ({sec:.2f} s)"}
+
+
+def run_reference_alexnet(args, rank, world):
+    if rank != 0:
+        return
+    from oracle.oracle import Ref
+
+    if not Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    c_t, n_t, _ = thresholds()
+    total_img, total_s = 0, 0.0
+    for i in range(args.warmup + args.steps):
+        r = reference_alexnet_sample(c_t, n_t)
+        if i >= args.warmup:
+            total_img += r["cores"]
+            total_s += r["cores"] / r["value"]
+    v = total_img / total_s
+    threads = os.cpu_count() or 1
+    print(json.dumps({"metric": METRIC, "value": round(v, 3), "unit": "images/s",
+                      "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": round(1e3 * total_s / args.steps, 1),
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                      "dtype": "f32", "data": "synthetic", "impl": "reference",
+                      "config": {"workload": "BASELINE config 5: whole AlexNet forward"},
+                      "cpu_baseline": {"value": round(v, 3), "unit": "images/s", "cores": threads,
+                                       "kind": "reference", "cpu": cpu_desc(),
+                                       "sample": f"1 image per thread x {threads} threads"},
+                      "e2e": {"value": round(v, 3), "unit": "images/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}))
 
 
 if __name__ == "__main__":

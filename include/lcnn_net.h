@@ -1,0 +1,57 @@
+/*
+ * lcnn_net.h -- C ABI of the network runtime (liblcnn.so), the B200 form of
+ * the reference's run_network / annotate_layouts / plan_transforms
+ * (proj/include/lcnn/net.hpp:58-131).  A handle owns the parsed, annotated
+ * network and its weights resident in HBM; forward runs on a caller stream
+ * with device buffers (value) or host buffers (end to end).
+ */
+#ifndef LCNN_NET_H_
+#define LCNN_NET_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lcnn_net lcnn_net;
+
+/* parse_network (net.cpp:51-118) + annotate_layouts (net.cpp:186-195) with
+ * thresholds (c_t, n_t) for layers whose layout is "auto" (c_t == 0 selects
+ * the titan-black preset), weights from the reference's seeded streams
+ * (net.cpp:398-420) uploaded once.  Returns an lcnn_status. */
+int lcnn_net_create(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
+                    lcnn_net** out);
+void lcnn_net_destroy(lcnn_net* net);
+const char* lcnn_net_last_error(void);
+
+/* Input dims, the layout the first 4D layer consumes, output matrix dims,
+ * forward flops per image, transforms executed for an input in in_layout. */
+int lcnn_net_info(const lcnn_net* net, int in_layout, uint32_t dims[4],
+                  int* first_layout, uint32_t* out_rows, uint32_t* out_cols,
+                  uint64_t* flops_per_image, uint32_t* transforms);
+/* Per-layer layout codes after annotation (-1 for fc/softmax). */
+int lcnn_net_layouts(const lcnn_net* net, int* layouts, uint32_t max_layers);
+
+/* Forward with device buffers on `stream` (a cudaStream_t). */
+int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout,
+                     float* d_output, void* stream);
+/* Forward with host buffers: H2D, forward, D2H (synchronous). */
+int lcnn_net_forward_host(const lcnn_net* net, const float* h_input,
+                          int in_layout, float* h_output);
+
+/* One forward with per-entry CUDA-event device times (layers and inserted
+ * transforms, in execution order): nanos[i], names comma-separated. */
+int lcnn_net_profile(const lcnn_net* net, const float* d_input, int in_layout,
+                     void* stream, uint64_t* nanos, uint32_t max_entries,
+                     char* names, size_t names_len, uint32_t* count);
+
+/* lcnn_precision of the conv / fc layers (default FP32). */
+void lcnn_set_dense_precision(int precision);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LCNN_NET_H_ */

@@ -200,6 +200,8 @@ class Ref:
             dll.ref_session_run.argtypes = [c_void_p]
             dll.ref_session_destroy.argtypes = [c_void_p]
             dll.ref_gemm_blocked.argtypes = [c_void_p] * 3 + [c_uint64] * 3
+            dll.ref_time_network.restype = c_double
+            dll.ref_time_network.argtypes = [c_char_p, c_uint32, c_uint32, c_int]
             cls._lib = dll
         return cls._lib
 
@@ -330,6 +332,15 @@ class Ref:
         N-shards (ref_shim.cpp ref_session_*); inputs are built once."""
         return RefSession(cls.lib(), op, n, c, h, w, layout, dst_layout, wh, ww, s, avg, fh, fw,
                           threads)
+
+
+def ref_time_network(json_text: str, c_t: int, n_t: int, threads: int) -> float:
+    """Seconds of the reference run_network with `threads` concurrent shards
+    (each shard's batch is the config's n)."""
+    t = Ref.lib().ref_time_network(json_text.encode(), c_t, n_t, threads)
+    if t < 0:
+        raise OracleError(11, Ref.lib().ref_last_error().decode())
+    return t
 
 
 class RefSession:

@@ -365,4 +365,49 @@ double ref_session_run(void* handle) {
 
 void ref_session_destroy(void* handle) { delete static_cast<RefSession*>(handle); }
 
+// Whole-network reference forward: `threads` std::threads, each parsing the
+// config (batch = its shard), annotating with (c_t, n_t) and calling the
+// unmodified run_network on a seeded input of the first 4D layer's layout.
+// Returns the wall seconds of the slowest thread's run_network (inputs and
+// weights built before timing).
+double ref_time_network(const char* json, uint32_t c_t, uint32_t n_t, int threads) {
+  try {
+    if (threads < 1) threads = 1;
+    std::vector<double> secs(threads, 0.0);
+    std::vector<std::string> errs(threads);
+    auto work = [&](int t) {
+      try {
+        R::NetworkSpec spec = R::annotate_layouts(R::parse_network(json),
+                                                  R::HeuristicThresholds{c_t, n_t});
+        R::Layout first = R::Layout::NCHW;
+        for (const auto& l : spec.layers)
+          if ((l.kind == R::LayerKind::Convolution || l.kind == R::LayerKind::Pooling) &&
+              l.layout_field) {
+            first = *l.layout_field;
+            break;
+          }
+        R::Tensor4D in(spec.n, spec.c, spec.h, spec.w, first);
+        std::mt19937 rng(42 + t);
+        std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+        for (uint64_t i = 0; i < in.size(); ++i) in.data()[i] = dist(rng);
+        const auto t0 = std::chrono::steady_clock::now();
+        (void)R::run_network(spec, in);
+        secs[t] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      } catch (const std::exception& e) {
+        errs[t] = e.what();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (const auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+    return *std::max_element(secs.begin(), secs.end());
+  } catch (...) {
+    map_current_exception();
+    return -1.0;
+  }
+}
+
 }  // extern "C"

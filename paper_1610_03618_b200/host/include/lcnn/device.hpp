@@ -19,6 +19,8 @@ class DeviceBuffer {
  public:
   DeviceBuffer() = default;
   explicit DeviceBuffer(std::size_t bytes);
+  // Non-owning view of caller memory (never returned to the pool).
+  static DeviceBuffer borrow(void* ptr, std::size_t bytes);
   ~DeviceBuffer();
   DeviceBuffer(DeviceBuffer&& o) noexcept;
   DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
@@ -32,10 +34,14 @@ class DeviceBuffer {
  private:
   void* ptr_ = nullptr;
   std::size_t bytes_ = 0;
+  bool owned_ = true;
 };
 
 // The stream every lcnn call issued from this host thread is ordered on.
 void* current_stream();
+// Order this thread's lcnn calls on a caller-owned stream (nullptr restores
+// the library's own stream).
+void set_current_stream(void* stream);
 // Block until the calling thread's stream has drained.
 void synchronize();
 // Throw the lcnn exception matching a non-OK lcnn_status (with the library's
@@ -50,6 +56,9 @@ class DeviceTensor4D {
   DeviceTensor4D(std::uint32_t n, std::uint32_t c, std::uint32_t h,
                  std::uint32_t w, Layout layout);
   static DeviceTensor4D upload(const Tensor4D& t);
+  // View of caller-owned device memory in the given layout (not copied).
+  static DeviceTensor4D wrap(float* data, std::uint32_t n, std::uint32_t c, std::uint32_t h,
+                             std::uint32_t w, Layout layout);
   Tensor4D download() const;
 
   std::uint32_t n() const { return n_; }
@@ -63,8 +72,9 @@ class DeviceTensor4D {
   const std::shared_ptr<DeviceBuffer>& buffer() const { return buf_; }
 
  private:
-  std::uint32_t n_, c_, h_, w_;
-  Layout layout_;
+  DeviceTensor4D() = default;
+  std::uint32_t n_ = 0, c_ = 0, h_ = 0, w_ = 0;
+  Layout layout_ = Layout::NCHW;
   std::shared_ptr<DeviceBuffer> buf_;
 };
 

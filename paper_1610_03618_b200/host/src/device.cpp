@@ -25,6 +25,7 @@ void cuda_ok(cudaError_t e, const char* what) {
 
 struct ThreadContext {
   cudaStream_t stream = nullptr;
+  cudaStream_t external = nullptr;  // caller-provided stream, if any
   int device = -1;
   std::multimap<std::size_t, void*> free_blocks;
   ~ThreadContext() {
@@ -90,29 +91,52 @@ DeviceBuffer::DeviceBuffer(std::size_t bytes) {
   }
 }
 
-DeviceBuffer::~DeviceBuffer() {
-  if (ptr_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
+DeviceBuffer DeviceBuffer::borrow(void* ptr, std::size_t bytes) {
+  DeviceBuffer b;
+  b.ptr_ = ptr;
+  b.bytes_ = bytes;
+  b.owned_ = false;
+  return b;
 }
 
-DeviceBuffer::DeviceBuffer(DeviceBuffer&& o) noexcept : ptr_(o.ptr_), bytes_(o.bytes_) {
+DeviceBuffer::~DeviceBuffer() {
+  if (ptr_ && owned_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
+}
+
+DeviceBuffer::DeviceBuffer(DeviceBuffer&& o) noexcept
+    : ptr_(o.ptr_), bytes_(o.bytes_), owned_(o.owned_) {
   o.ptr_ = nullptr;
   o.bytes_ = 0;
 }
 
 DeviceBuffer& DeviceBuffer::operator=(DeviceBuffer&& o) noexcept {
   if (this != &o) {
-    if (ptr_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
+    if (ptr_ && owned_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
     ptr_ = o.ptr_;
     bytes_ = o.bytes_;
+    owned_ = o.owned_;
     o.ptr_ = nullptr;
     o.bytes_ = 0;
   }
   return *this;
 }
 
-void* current_stream() { return ctx().stream; }
+void* current_stream() {
+  ThreadContext& c = ctx();
+  return c.external ? c.external : c.stream;
+}
 
-void synchronize() { cuda_ok(cudaStreamSynchronize(ctx().stream), "cudaStreamSynchronize"); }
+void set_current_stream(void* stream) {
+  // drain the stream being left: pooled blocks freed on it may be reused on
+  // the new one
+  synchronize();
+  ctx().external = static_cast<cudaStream_t>(stream);
+}
+
+void synchronize() {
+  cuda_ok(cudaStreamSynchronize(static_cast<cudaStream_t>(current_stream())),
+          "cudaStreamSynchronize");
+}
 
 void throw_status(int status) {
   const std::string msg = lcnn_last_error();
@@ -137,6 +161,19 @@ DeviceTensor4D::DeviceTensor4D(std::uint32_t n, std::uint32_t c, std::uint32_t h
   if (std::uint64_t{n} * c * h * w > 0xffffffffull)
     throw ShapeError("Tensor4D: dim product overflows");
   buf_ = std::make_shared<DeviceBuffer>(size() * sizeof(float));
+}
+
+DeviceTensor4D DeviceTensor4D::wrap(float* data, std::uint32_t n, std::uint32_t c,
+                                    std::uint32_t h, std::uint32_t w, Layout layout) {
+  DeviceTensor4D d;
+  d.n_ = n;
+  d.c_ = c;
+  d.h_ = h;
+  d.w_ = w;
+  d.layout_ = layout;
+  d.buf_ = std::make_shared<DeviceBuffer>(
+      DeviceBuffer::borrow(data, std::uint64_t{n} * c * h * w * sizeof(float)));
+  return d;
 }
 
 DeviceTensor4D DeviceTensor4D::upload(const Tensor4D& t) {

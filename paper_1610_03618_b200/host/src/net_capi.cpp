@@ -1,0 +1,169 @@
+// C ABI of the network runtime (include/lcnn_net.h).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "lcnn/net.hpp"
+#include "lcnn_cuda.h"
+#include "lcnn_net.h"
+
+struct lcnn_net {
+  std::unique_ptr<lcnn::Network> net;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int status_of_current() {
+  try {
+    throw;
+  } catch (const lcnn::ShapeError& e) {
+    g_err = e.what();
+    return LCNN_ESHAPE;
+  } catch (const lcnn::LayoutError& e) {
+    g_err = e.what();
+    return LCNN_ELAYOUT;
+  } catch (const lcnn::PlanError& e) {
+    g_err = e.what();
+    return LCNN_EPLAN;
+  } catch (const lcnn::DomainError& e) {
+    g_err = e.what();
+    return LCNN_EDOMAIN;
+  } catch (const lcnn::UnsupportedError& e) {
+    g_err = e.what();
+    return LCNN_EUNSUPPORTED;
+  } catch (const lcnn::ValidationError& e) {
+    g_err = e.what();
+    return LCNN_EVALIDATION;
+  } catch (const lcnn::Error& e) {
+    g_err = e.what();
+    return LCNN_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LCNN_EINVAL;
+  }
+}
+
+#define NET_GUARD(...)            \
+  try {                           \
+    __VA_ARGS__;                  \
+    g_err.clear();                \
+    return LCNN_OK;               \
+  } catch (...) {                 \
+    return status_of_current();   \
+  }
+
+lcnn::Layout L(int code) { return static_cast<lcnn::Layout>(code); }
+
+}  // namespace
+
+extern "C" {
+
+const char* lcnn_net_last_error(void) { return g_err.c_str(); }
+
+void lcnn_set_dense_precision(int precision) { lcnn::set_dense_precision(precision); }
+
+int lcnn_net_create(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed, lcnn_net** out) {
+  NET_GUARD({
+    lcnn::NetworkSpec spec = lcnn::parse_network(json);
+    lcnn::HeuristicThresholds th = c_t ? lcnn::HeuristicThresholds{c_t, n_t} : lcnn::kTitanBlack;
+    spec = lcnn::annotate_layouts(spec, th);
+    lcnn::RunOptions opt;
+    opt.seed = seed;
+    auto* h = new lcnn_net{std::make_unique<lcnn::Network>(std::move(spec), opt)};
+    *out = h;
+  })
+}
+
+void lcnn_net_destroy(lcnn_net* net) { delete net; }
+
+int lcnn_net_info(const lcnn_net* net, int in_layout, uint32_t dims[4], int* first_layout,
+                  uint32_t* out_rows, uint32_t* out_cols, uint64_t* flops_per_image,
+                  uint32_t* transforms) {
+  NET_GUARD({
+    const lcnn::NetworkSpec& s = net->net->spec();
+    dims[0] = s.n;
+    dims[1] = s.c;
+    dims[2] = s.h;
+    dims[3] = s.w;
+    *first_layout = static_cast<int>(net->net->input_layout());
+    const auto shapes = lcnn::infer_shapes(s);
+    const lcnn::StageShape& o = shapes.back();
+    *out_rows = o.n;
+    *out_cols = o.c * o.h * o.w;
+    *flops_per_image = net->net->flops_per_image();
+    *transforms = static_cast<uint32_t>(net->net->transform_count(L(in_layout)));
+  })
+}
+
+int lcnn_net_layouts(const lcnn_net* net, int* layouts, uint32_t max_layers) {
+  NET_GUARD({
+    const auto& layers = net->net->spec().layers;
+    for (uint32_t i = 0; i < max_layers && i < layers.size(); ++i)
+      layouts[i] = layers[i].layout_field ? static_cast<int>(*layers[i].layout_field) : -1;
+  })
+}
+
+int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout, float* d_output,
+                     void* stream) {
+  NET_GUARD({
+    lcnn::set_current_stream(stream);
+    const lcnn::NetworkSpec& s = net->net->spec();
+    const lcnn::DeviceTensor4D in = lcnn::DeviceTensor4D::wrap(const_cast<float*>(d_input), s.n,
+                                                               s.c, s.h, s.w, L(in_layout));
+    const lcnn::DeviceMatrix out = net->net->forward(in);
+    const cudaError_t e =
+        cudaMemcpyAsync(d_output, out.data(), std::size_t{out.rows} * out.cols * sizeof(float),
+                        cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+  })
+}
+
+int lcnn_net_forward_host(const lcnn_net* net, const float* h_input, int in_layout,
+                          float* h_output) {
+  NET_GUARD({
+    lcnn::set_current_stream(nullptr);
+    const lcnn::NetworkSpec& s = net->net->spec();
+    cudaStream_t st = static_cast<cudaStream_t>(lcnn::current_stream());
+    lcnn::DeviceTensor4D in(s.n, s.c, s.h, s.w, L(in_layout));
+    cudaError_t e = cudaMemcpyAsync(in.data(), h_input, in.size() * sizeof(float),
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+    const lcnn::DeviceMatrix out = net->net->forward(in);
+    e = cudaMemcpyAsync(h_output, out.data(), std::size_t{out.rows} * out.cols * sizeof(float),
+                        cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+    lcnn::synchronize();
+  })
+}
+
+int lcnn_net_profile(const lcnn_net* net, const float* d_input, int in_layout, void* stream,
+                     uint64_t* nanos, uint32_t max_entries, char* names, size_t names_len,
+                     uint32_t* count) {
+  NET_GUARD({
+    lcnn::set_current_stream(stream);
+    const lcnn::NetworkSpec& s = net->net->spec();
+    const lcnn::DeviceTensor4D in = lcnn::DeviceTensor4D::wrap(const_cast<float*>(d_input), s.n,
+                                                               s.c, s.h, s.w, L(in_layout));
+    lcnn::TimingReport rep;
+    (void)net->net->forward(in, &rep);
+    std::string joined;
+    uint32_t k = 0;
+    for (const lcnn::LayerTiming& e : rep.entries) {
+      if (k < max_entries) nanos[k] = e.nanos;
+      ++k;
+      if (!joined.empty()) joined += ',';
+      joined += e.name;
+    }
+    *count = k;
+    if (names && names_len) {
+      std::strncpy(names, joined.c_str(), names_len - 1);
+      names[names_len - 1] = 0;
+    }
+  })
+}
+
+}  // extern "C"
