@@ -94,34 +94,56 @@ struct ChwnConvLoader {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
   }
-  __device__ void load(uint32_t seg, uint32_t k, void* sa, void* sb, uint64_t* bar, uint32_t m0,
-                       uint32_t ntile) const {
-    tma_load_2d(sa, &a[seg == 2 ? 1 : 0], bar, k * kTcBK, m0);
-    uint32_t fh, wofs, c0;
-    if (g.mode == kModeCI) {
-      const uint32_t cbn = g.Ci / 32;
-      const uint32_t tap = k / cbn;
-      c0 = (k % cbn) * 32;
-      fh = tap / g.FW;
-      wofs = tap % g.FW;
-    } else {
-      const uint32_t cbn = g.CiP / g.CIB;
-      fh = k / cbn;
-      c0 = (k % cbn) * g.CIB;
-      wofs = 0;
-    }
-    const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
+  // Per tile: the four 32-column boxes' (n0, w origin, h origin) decoded once;
+  // per k-block: the tap / channel-block counters advance incrementally.
+  struct State {
+    uint32_t m0;
+    int32_t n0[4], y0[4], z0[4];
+    uint32_t fh, wofs, c0;  // K decode of the next k-block
+  };
+  __device__ State begin(uint32_t m0, uint32_t ntile) const {
+    State st;
+    st.m0 = m0;
 #pragma unroll
     for (int j = 0; j < kTcBN / 32; ++j) {
       const uint32_t col = ntile * kTcBN + 32 * j;
       const uint32_t pos = col / g.N;
-      const uint32_t n0 = col - pos * g.N;
-      const uint32_t oh = pos / g.Wo, ow = pos - (pos / g.Wo) * g.Wo;
-      int32_t y = static_cast<int32_t>(ow * g.S + wofs) - static_cast<int32_t>(g.P);
-      int32_t z = static_cast<int32_t>(oh * g.S + fh) - static_cast<int32_t>(g.P);
-      if (col >= ncols) z = -(1 << 20);  // beyond the last output: all-OOB box (zeros)
-      tma_load_4d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, static_cast<int32_t>(n0), y, z,
-                  static_cast<int32_t>(c0));
+      const uint32_t oh = pos / g.Wo, ow = pos - oh * g.Wo;
+      st.n0[j] = static_cast<int32_t>(col - pos * g.N);
+      st.y0[j] = static_cast<int32_t>(ow * g.S) - static_cast<int32_t>(g.P);
+      // beyond the last output: an all-out-of-bounds box (zeros)
+      st.z0[j] = col >= ncols ? -(1 << 20)
+                              : static_cast<int32_t>(oh * g.S) - static_cast<int32_t>(g.P);
+    }
+    st.fh = st.wofs = st.c0 = 0;
+    return st;
+  }
+  __device__ void load(State& st, uint32_t seg, uint32_t k, void* sa, void* sb,
+                       uint64_t* bar) const {
+    if (k == 0) st.fh = st.wofs = st.c0 = 0;  // a new segment restarts K
+    tma_load_2d(sa, &a[seg == 2 ? 1 : 0], bar, k * kTcBK, st.m0);
+    const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
+#pragma unroll
+    for (int j = 0; j < kTcBN / 32; ++j)
+      tma_load_4d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, st.n0[j],
+                  st.y0[j] + static_cast<int32_t>(st.wofs), st.z0[j] + static_cast<int32_t>(st.fh),
+                  static_cast<int32_t>(st.c0));
+    // advance: CI mode k = (fh, fw, ci/32); WIN mode k = (fh, ci/CIB)
+    if (g.mode == kModeCI) {
+      st.c0 += 32;
+      if (st.c0 == g.Ci) {
+        st.c0 = 0;
+        if (++st.wofs == g.FW) {
+          st.wofs = 0;
+          ++st.fh;
+        }
+      }
+    } else {
+      st.c0 += g.CIB;
+      if (st.c0 == g.CiP) {
+        st.c0 = 0;
+        ++st.fh;
+      }
     }
   }
 };

@@ -38,23 +38,34 @@ using namespace lcnn_tc;
 struct GemmLoader {
   CUtensorMap a[2];
   CUtensorMap b[2];
-  uint32_t kb;
+  uint32_t kb;        // k-blocks of the whole K
+  uint32_t split_kb;  // k-blocks per split (blockIdx.z); == kb without split-K
   uint32_t segs;
   static constexpr bool kBMajorMN = true;
-  __device__ uint32_t kblocks() const { return kb; }
+  __device__ uint32_t kblocks() const {
+    const uint32_t k0 = blockIdx.z * split_kb;
+    return min(split_kb, kb - k0);
+  }
   __device__ uint32_t segments() const { return segs; }
   __device__ void prefetch() const {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
   }
-  __device__ void load(uint32_t seg, uint32_t k, void* sa, void* sb, uint64_t* bar, uint32_t m0,
-                       uint32_t ntile) const {
+  struct State {
+    uint32_t m0, n0, k0;
+  };
+  __device__ State begin(uint32_t m0, uint32_t ntile) const {
+    return State{m0, ntile * kTcBN, blockIdx.z * split_kb};
+  }
+  __device__ void load(State& st, uint32_t seg, uint32_t kk, void* sa, void* sb,
+                       uint64_t* bar) const {
+    const uint32_t k = st.k0 + kk;
     const CUtensorMap* am = &a[seg == 2 ? 1 : 0];
     const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
-    tma_load_2d(sa, am, bar, k * kTcBK, m0);
+    tma_load_2d(sa, am, bar, k * kTcBK, st.m0);
 #pragma unroll
     for (int j = 0; j < kTcBN / 32; ++j)
-      tma_load_2d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, ntile * kTcBN + 32 * j, k * kTcBK);
+      tma_load_2d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, st.n0 + 32 * j, k * kTcBK);
   }
 };
 
@@ -62,11 +73,18 @@ struct GemmOut {
   float* c;
   uint64_t ldc;
   uint32_t M, N;
+  bool accumulate;  // split-K: partial tiles are added into a zeroed C
   __device__ __forceinline__ void store32(uint32_t m, uint32_t ntile, uint32_t col,
                                           const float* v) const {
     if (m >= M) return;
     const uint32_t n0 = ntile * kTcBN + col;
     float* row = c + m * ldc + n0;
+    if (accumulate) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) atomicAdd(row + j, v[j]);
+      return;
+    }
     if (n0 + 32 <= N && ((reinterpret_cast<uintptr_t>(row) & 15u) == 0)) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4)
@@ -255,7 +273,20 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
     return cudaErrorInvalidValue;
   L.kb = static_cast<uint32_t>((k + kTcBK - 1) / kTcBK);
   L.segs = precision == LCNN_PREC_3XTF32 ? 3 : 1;
-  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
+  // split-K when the output tiles cannot fill the 148 SMs (skinny fc layers)
+  const uint64_t tiles = ((n + kTcBN - 1) / kTcBN) * ((m + kTcBM - 1) / kTcBM);
+  uint32_t splits = 1;
+  if (tiles < 148) {
+    splits = static_cast<uint32_t>((148 + tiles - 1) / tiles);
+    splits = splits > L.kb / 8 ? (L.kb / 8 ? L.kb / 8 : 1) : splits;
+  }
+  L.split_kb = (L.kb + splits - 1) / splits;
+  splits = (L.kb + L.split_kb - 1) / L.split_kb;
+  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n), splits > 1};
+  if (splits > 1) {
+    cudaError_t e = cudaMemsetAsync(c, 0, m * n * sizeof(float), s);
+    if (e != cudaSuccess) return e;
+  }
   auto kern = tc_gemm_kernel<GemmLoader, GemmOut>;
   static bool attr = false;
   if (!attr) {
@@ -265,7 +296,7 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
     attr = true;
   }
   const dim3 grid(static_cast<uint32_t>((n + kTcBN - 1) / kTcBN),
-                  static_cast<uint32_t>((m + kTcBM - 1) / kTcBM));
+                  static_cast<uint32_t>((m + kTcBM - 1) / kTcBM), splits);
   kern<<<grid, kTcThreads, kTcSmem, s>>>(L, O);
   return cudaGetLastError();
 }

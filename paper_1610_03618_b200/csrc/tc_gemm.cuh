@@ -35,12 +35,15 @@ struct TcCtl {
   uint32_t tmem_addr;
 };
 
-// Loader concept:
+// Loader concept (the producer thread calls begin() once per tile, then
+// load() for k-blocks 0..kblocks()-1 of each segment in order, so loaders can
+// decode K incrementally instead of dividing per stage):
 //   uint32_t kblocks() const;                 // k-blocks of BK per segment
 //   uint32_t segments() const;                // chained operand sets (1 or 3)
 //   void prefetch() const;                    // tensor-map prefetch
-//   void load(uint32_t seg, uint32_t kb, void* sa, void* sb, uint64_t* bar,
-//             uint32_t m0, uint32_t ntile) const;   // issues TMA, total kTcStageBytes
+//   State begin(uint32_t m0, uint32_t ntile) const;
+//   void load(State& st, uint32_t seg, uint32_t kb, void* sa, void* sb,
+//             uint64_t* bar) const;          // issues TMA, total kTcStageBytes
 //   static constexpr bool kBMajorMN;          // B operand major-ness
 // Out concept:
 //   void store32(uint32_t m, uint32_t ntile, uint32_t col, const float* v) const;
@@ -77,18 +80,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t tmem = ctl->tmem_addr;
 
   if (warp == 0 && lane == 0) {
+    auto st = ld.begin(m0, ntile);
+    uint32_t seg = 0, kb = 0, s = 0, phase = 0;
     for (uint32_t it = 0; it < total; ++it) {
-      const int s = it % kTcStages;
-      mbar_wait(&ctl->empty[s], ((it / kTcStages) & 1) ^ 1);
+      mbar_wait(&ctl->empty[s], phase ^ 1);
       uint8_t* sa = smem + s * kTcStageBytes;
       mbar_arrive_expect_tx(&ctl->full[s], kTcStageBytes);
-      ld.load(it / kb_per_seg, it % kb_per_seg, sa, sa + kTcABytes, &ctl->full[s], m0, ntile);
+      ld.load(st, seg, kb, sa, sa + kTcABytes, &ctl->full[s]);
+      if (++kb == kb_per_seg) {
+        kb = 0;
+        ++seg;
+      }
+      if (++s == kTcStages) {
+        s = 0;
+        phase ^= 1;
+      }
     }
   } else if (warp == 1 && lane == 0) {
     constexpr uint32_t idesc = idesc_tf32(kTcBM, kTcBN, false, Loader::kBMajorMN);
+    uint32_t s = 0, phase = 0;
     for (uint32_t it = 0; it < total; ++it) {
-      const int s = it % kTcStages;
-      mbar_wait(&ctl->full[s], (it / kTcStages) & 1);
+      mbar_wait(&ctl->full[s], phase);
       tc_fence_after();
       const uint8_t* sa = smem + s * kTcStageBytes;
       const uint8_t* sb = sa + kTcABytes;
@@ -102,6 +114,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mma_tf32(tmem, ad, bd, idesc, (it | k) != 0);
       }
       tc_commit(&ctl->empty[s]);
+      if (++s == kTcStages) {
+        s = 0;
+        phase ^= 1;
+      }
     }
     tc_commit(&ctl->tmem_full);
   } else if (warp >= 2) {
