@@ -263,6 +263,86 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_kernel(NchwGeom g) {
   }
 }
 
+// Stride-2 windows, vertical coarsening (FW = 1).  Each staged input row is
+// stored de-interleaved -- even columns at [0, E), odd columns at [odd, odd+W/2)
+// with odd == 16 (mod 32) words -- so lanes that walk consecutive output
+// columns read consecutive words for every tap (no 2-way bank conflict), and
+// the staging stores of a warp (32 consecutive input columns) split into two
+// 16-word runs on disjoint bank halves.
+template <int WH, int WW, int FH, bool AVG>
+__global__ void __launch_bounds__(kThreads) pool_nchw_s2_kernel(NchwGeom g, uint32_t pitch,
+                                                                 uint32_t odd) {
+  extern __shared__ float sm[];
+  constexpr int S = 2;
+  constexpr int UH = S * (FH - 1) + WH;
+  const uint32_t plane = blockIdx.x / g.nbands;
+  const uint32_t b = blockIdx.x - plane * g.nbands;
+  const uint32_t oh_begin = b * g.band;
+  const uint32_t oh_cnt = min(g.band, g.Ho - oh_begin);
+  const uint32_t ih_begin = oh_begin * S;
+  const uint32_t ih_cnt = min(g.H - ih_begin, (oh_cnt - 1) * S + WH);
+  const float* src = g.src + plane * static_cast<uint64_t>(g.H) * g.W +
+                     static_cast<uint64_t>(ih_begin) * g.W;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kThreads / 32;
+  // stage: warp-per-row, 4 rows' loads in flight per warp
+  for (uint32_t r0 = warp; r0 < ih_cnt; r0 += 4 * kWarps) {
+    for (uint32_t x0 = 0; x0 < g.W; x0 += 32) {
+      const uint32_t x = x0 + lane;
+      float v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t r = r0 + i * kWarps;
+        v[i] = (r < ih_cnt && x < g.W) ? __ldg(src + static_cast<uint64_t>(r) * g.W + x) : 0.0f;
+      }
+      const uint32_t col = (x & 1) ? odd + (x >> 1) : (x >> 1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t r = r0 + i * kWarps;
+        if (r < ih_cnt && x < g.W) sm[r * pitch + col] = v[i];
+      }
+    }
+  }
+  __syncthreads();
+
+  float* obase = g.dst + plane * static_cast<uint64_t>(g.Ho) * g.Wo +
+                 static_cast<uint64_t>(oh_begin) * g.Wo;
+  const uint32_t nrb = (oh_cnt + FH - 1) / FH;
+  const uint32_t items = nrb * g.Wo;
+  for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+    uint32_t rb, ow;
+    g.div_nbw.divmod(it, rb, ow);
+    const uint32_t r0 = rb * FH;
+    float acc[FH];
+#pragma unroll
+    for (int by = 0; by < FH; ++by) acc[by] = AVG ? 0.0f : -INFINITY;
+#pragma unroll
+    for (int y = 0; y < UH; ++y) {
+      if (r0 * S + y >= ih_cnt) break;  // rows that only feed absent outputs
+      const float* row = sm + (r0 * S + y) * pitch;
+      float v[WW];
+#pragma unroll
+      for (int x = 0; x < WW; ++x) v[x] = (x & 1) ? row[odd + ow + (x >> 1)] : row[ow + (x >> 1)];
+#pragma unroll
+      for (int by = 0; by < FH; ++by) {
+        const int dy = y - by * S;
+        if (dy < 0 || dy >= WH) continue;
+#pragma unroll
+        for (int x = 0; x < WW; ++x) {
+          if constexpr (AVG) acc[by] = add_tap(acc[by], v[x]);
+          else acc[by] = max_tap(acc[by], v[x]);
+        }
+      }
+    }
+#pragma unroll
+    for (int by = 0; by < FH; ++by) {
+      if (r0 + by >= oh_cnt) break;
+      const float o = AVG ? divide_out(acc[by], g.divisor) : acc[by];
+      stg_stream(obase + static_cast<uint64_t>(r0 + by) * g.Wo + ow, o);
+    }
+  }
+}
+
 // Runtime window, staged the same way, one output per thread.
 template <bool AVG>
 __global__ void __launch_bounds__(kThreads) pool_nchw_generic_kernel(NchwGeom g) {
@@ -471,9 +551,63 @@ bool nchw_dispatch_f(uint32_t fh, uint32_t fw, const NchwGeom& g, uint32_t block
 
 }  // namespace
 
+template <int WH, int FH>
+cudaError_t s2_launch(const NchwGeom& g, uint32_t blocks, uint32_t smem, uint32_t pitch,
+                      uint32_t odd, bool avg, cudaStream_t st) {
+  auto kern = avg ? pool_nchw_s2_kernel<WH, WH, FH, true> : pool_nchw_s2_kernel<WH, WH, FH, false>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<blocks, kThreads, smem, st>>>(g, pitch, odd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pool_nchw_s2(const PoolArgs& a, cudaStream_t st) {
+  const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
+  const uint32_t even = (a.w + 1) / 2;
+  const uint32_t odd = (even + 31) / 32 * 32 + 16;          // == 16 (mod 32)
+  const uint32_t pitch = odd + (a.w / 2 + 15) / 16 * 16 + 16;  // keeps rows 16-aligned
+  const uint64_t row_bytes = static_cast<uint64_t>(pitch) * 4;
+  if (static_cast<uint64_t>(a.win_h) * row_bytes > kStageBudget) return cudaErrorNotSupported;
+  uint32_t band = static_cast<uint32_t>((kStageBudget / row_bytes - a.win_h) / 2 + 1);
+  if (band > a.ho) band = a.ho;
+  const uint64_t in_rows = static_cast<uint64_t>(band - 1) * 2 + a.win_h;
+  const uint32_t smem = static_cast<uint32_t>(in_rows * row_bytes);
+  NchwGeom g;
+  g.src = a.src;
+  g.dst = a.dst;
+  g.H = a.h;
+  g.W = a.w;
+  g.Ho = a.ho;
+  g.Wo = a.wo;
+  g.band = band;
+  g.nbands = (a.ho + band - 1) / band;
+  g.nbw = a.wo;
+  g.div_nbw = FastDiv(a.wo);
+  g.divisor = static_cast<float>(a.win_h * a.win_w);  // pool.cpp:158
+  g.wh = a.win_h;
+  g.ww = a.win_w;
+  g.s = 2;
+  const uint64_t blocks64 = planes * g.nbands;
+  if (blocks64 > 0x7fffffffull) return cudaErrorNotSupported;
+  const uint32_t blocks = static_cast<uint32_t>(blocks64);
+#define LCNN_S2(WH_, FH_) \
+  if (a.win_h == WH_ && a.fh == FH_) return s2_launch<WH_, FH_>(g, blocks, smem, pitch, odd, a.avg, st);
+  LCNN_S2(2, 1) LCNN_S2(2, 2) LCNN_S2(2, 3) LCNN_S2(2, 4)
+  LCNN_S2(3, 1) LCNN_S2(3, 2) LCNN_S2(3, 3) LCNN_S2(3, 4)
+#undef LCNN_S2
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t st) {
   const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
   if (planes == 0 || a.ho == 0 || a.wo == 0) return cudaSuccess;
+  if (a.stride == 2 && a.fw == 1 && a.fh <= 4 && a.win_h == a.win_w &&
+      (a.win_h == 2 || a.win_h == 3)) {
+    const cudaError_t e = launch_pool_nchw_s2(a, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const uint64_t row_bytes = static_cast<uint64_t>(a.w) * 4;
   // output rows per CTA so that the staged input band fits the budget
   uint32_t band = 1;

@@ -1,0 +1,51 @@
+"""Coarsening-plan sweep of the pooling kernels on B200 (CUDA-graph timed),
+the measurement behind the autotuner's default plans."""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1610_03618_b200 import capi, lcnn  # noqa: E402
+
+dev = torch.device("cuda:0")
+lib = capi.lib()
+
+
+def gbs(layout, n, c, hw, win, s, fh, fw, K=50):
+    x = torch.rand(n * c * hw * hw, device=dev)
+    ho = (hw - win) // s + 1
+    y = torch.empty(n * c * ho * ho, device=dev)
+    fn = lib.lcnn_pool_coarsened if layout == capi.CHWN else None
+
+    def launch(st):
+        if layout == capi.CHWN:
+            capi.check(lib.lcnn_pool_coarsened(x.data_ptr(), y.data_ptr(), n, c, hw, hw, layout, win,
+                                               win, s, 0, fh, fw, None, st))
+        else:
+            capi.check(lib.lcnn_pool_coarsened_nchw(x.data_ptr(), y.data_ptr(), n, c, hw, hw, win,
+                                                    win, s, 0, fh, fw, None, st))
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cap):
+        for _ in range(K):
+            launch(torch.cuda.current_stream().cuda_stream)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / K
+    return round((x.numel() + y.numel()) * 4 / ms / 1e6, 1)
+
+
+out = {}
+for name, (n, c, hw, win, s) in {"PL5": (128, 96, 55, 3, 2), "VGG1": (256, 64, 224, 2, 2),
+                                 "PL7": (128, 256, 13, 3, 2)}.items():
+    for fh, fw in [(1, 1), (1, 2), (2, 1), (2, 2), (1, 3), (3, 1), (1, 4), (4, 1), (2, 4), (4, 2)]:
+        out[f"{name}_chwn_{fh}x{fw}"] = gbs(capi.CHWN, n, c, hw, win, s, fh, fw)
+    for fh in (1, 2, 3, 4):
+        out[f"{name}_nchw_{fh}x1"] = gbs(capi.NCHW, n, c, hw, win, s, fh, 1)
+print(json.dumps(out, indent=1))
