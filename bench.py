@@ -223,30 +223,35 @@ def build_workload(name, torch, device, rank, plan):
     """Returns (ops, description dict, dominant op index, per-GPU batch)."""
     CHWN, NCHW = 1, 0
     seed = 1234 + 17 * rank
-    if name == "vgg_pools":
+    if name in ("vgg_pools", "vgg_pools_nchw"):
         b = 256
-        ops = [PoolOp(torch, device, b, c, hw, hw, CHWN, 2, 2, False, plan, seed + i)
+        layout = CHWN if name == "vgg_pools" else NCHW
+        plan = plan or ((1, 1) if layout == CHWN else (3, 1))
+        ops = [PoolOp(torch, device, b, c, hw, hw, layout, 2, 2, False, plan, seed + i)
                for i, (c, hw) in enumerate(VGG_POOLS)]
-        desc = {"workload": "BASELINE config 4: VGG-16 pool1..pool5, max 2x2/s2, CHWN "
-                            "(selector's pooling layout), 256 images per GPU, N-sharded",
+        lname = "CHWN (selector's pooling layout)" if layout == CHWN else "NCHW"
+        desc = {"workload": f"BASELINE config 4: VGG-16 pool1..pool5, max 2x2/s2, {lname}, "
+                            "256 images per GPU, N-sharded",
                 "batch_per_gpu": b, "layers": [f"{b}x{c}x{hw}x{hw}" for c, hw in VGG_POOLS],
-                "kernel": f"lcnn_pool_coarsened fh,fw={plan[0]},{plan[1]}"}
+                "kernel": f"coarsened fh,fw={plan[0]},{plan[1]}"}
         return ops, desc, 0, b
     if name in ("pl5", "pl5_nchw"):
         layout = CHWN if name == "pl5" else NCHW
-        p = (2, 2) if layout == CHWN else (2, 1)
+        p = plan or ((2, 2) if layout == CHWN else (2, 1))
         ops = [PoolOp(torch, device, 128, 96, 55, 55, layout, 3, 2, False, p, seed)]
         desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) max 3x3/s2, "
                             f"128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",
                 "batch_per_gpu": 128, "kernel": f"coarsened fh,fw={p[0]},{p[1]}"}
         return ops, desc, 0, 128
-    if name in ("softmax", "softmax5"):
-        fused = name == "softmax"
-        ops = [SoftmaxOp(torch, device, 4096, 1000, fused, seed)]
-        desc = {"workload": f"BASELINE config 2: softmax classifier 4096x1000, "
-                            f"{'fused single kernel' if fused else 'five-kernel baseline'}",
-                "batch_per_gpu": 4096}
-        return ops, desc, 0, 4096
+    if name in ("softmax", "softmax5", "softmax_64k"):
+        fused = name != "softmax5"
+        rows = 65536 if name == "softmax_64k" else 4096
+        ops = [SoftmaxOp(torch, device, rows, 1000, fused, seed)]
+        desc = {"workload": f"BASELINE config 2: softmax classifier {rows}x1000, "
+                            f"{'fused single kernel' if fused else 'five-kernel baseline'}"
+                            + (" (HBM asymptote beyond the 4096-row config)" if rows > 4096 else ""),
+                "batch_per_gpu": rows}
+        return ops, desc, 0, rows
     if name == "transform":
         b = 128
         ops = [TransformOp(torch, device, b, c, h, w, CHWN, NCHW, seed + i)
@@ -368,7 +373,8 @@ def run_reference_arm(args, rank, world):
         return
     threads = os.cpu_count() or 1
     # describe the same workload as our arm (shapes only; no GPU needed)
-    ops, desc, _, _ = build_workload(args.workload, _FakeTorch(), "cpu", 0, tuple(args.plan))
+    ops, desc, _, _ = build_workload(args.workload, _FakeTorch(), "cpu", 0,
+                                     tuple(args.plan) if args.plan else None)
     batch = ref_sample_batch(ops, threads, args.ref_sample_gb * GB)
     gbs, sec, sample_bytes = time_reference(ops, threads, batch, args.steps, args.warmup)
     line = {"metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world,
@@ -439,9 +445,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg_pools",
-                    choices=["vgg_pools", "pl5", "pl5_nchw", "softmax", "softmax5", "transform",
-                             "alexnet"])
-    ap.add_argument("--plan", type=int, nargs=2, default=[2, 2], help="coarsening fh fw")
+                    choices=["vgg_pools", "vgg_pools_nchw", "pl5", "pl5_nchw", "softmax", "softmax5",
+                             "softmax_64k", "transform", "alexnet"])
+    ap.add_argument("--plan", type=int, nargs=2, default=None,
+                    help="coarsening fh fw (default: (1,1) for non-overlapping 2x2/s2 VGG pools, "
+                         "(2,2) for overlapping 3x3/s2, measured best on B200)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sample-gb", type=float, default=1.0,
                     help="algorithmic GB per reference sample step")
@@ -481,7 +489,8 @@ def main():
             dist.destroy_process_group()
         return
 
-    ops, desc, dom, batch = build_workload(args.workload, torch, device, rank, tuple(args.plan))
+    ops, desc, dom, batch = build_workload(args.workload, torch, device, rank,
+                                           tuple(args.plan) if args.plan else None)
     stream = torch.cuda.current_stream(device)
     sh = stream.cuda_stream
     step_bytes = sum(op.bytes for op in ops)

@@ -263,66 +263,112 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_kernel(NchwGeom g) {
   }
 }
 
-// Stride-2 windows, vertical coarsening (FW = 1).  Each staged input row is
-// stored de-interleaved -- even columns at [0, E), odd columns at [odd, odd+W/2)
-// with odd == 16 (mod 32) words -- so lanes that walk consecutive output
-// columns read consecutive words for every tap (no 2-way bank conflict), and
-// the staging stores of a warp (32 consecutive input columns) split into two
-// 16-word runs on disjoint bank halves.
-template <int WH, int WW, int FH, bool AVG>
-__global__ void __launch_bounds__(kThreads) pool_nchw_s2_kernel(NchwGeom g, uint32_t pitch,
-                                                                 uint32_t odd) {
+// Stride-2 windows, vertical coarsening (FW = 1).  A CTA owns either a group
+// of whole (n,c) planes (small maps: PL7's 13x13 planes are 676 B) or one band
+// of output rows of a large plane -- in both cases one contiguous input span,
+// which is read with 128-bit loads, all issued before any is consumed.  Each
+// staged input row is stored de-interleaved -- even columns at [0, E), odd
+// columns at [odd, odd + W/2) -- so lanes walking consecutive output columns
+// read consecutive words for every tap.
+struct NchwS2Geom {
+  const float* src;
+  float* dst;
+  uint32_t H, W, Ho, Wo;
+  uint32_t planes;      // N*C
+  uint32_t per_cta;     // planes per CTA (whole-plane mode) or 1 (band mode)
+  uint32_t band;        // output rows per CTA (== Ho in whole-plane mode)
+  uint32_t nbands;      // bands per plane (1 in whole-plane mode)
+  uint32_t pitch, odd;  // staged row pitch, odd-column offset (words)
+  FastDiv div_w, div_wo, div_plane_items;
+  float divisor;
+};
+
+template <int WH, int FH, bool AVG>
+__global__ void __launch_bounds__(kThreads) pool_nchw_s2_kernel(NchwS2Geom g) {
   extern __shared__ float sm[];
-  constexpr int S = 2;
+  constexpr int S = 2, WW = WH;
   constexpr int UH = S * (FH - 1) + WH;
-  const uint32_t plane = blockIdx.x / g.nbands;
-  const uint32_t b = blockIdx.x - plane * g.nbands;
-  const uint32_t oh_begin = b * g.band;
-  const uint32_t oh_cnt = min(g.band, g.Ho - oh_begin);
-  const uint32_t ih_begin = oh_begin * S;
-  const uint32_t ih_cnt = min(g.H - ih_begin, (oh_cnt - 1) * S + WH);
-  const float* src = g.src + plane * static_cast<uint64_t>(g.H) * g.W +
-                     static_cast<uint64_t>(ih_begin) * g.W;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kWarps = kThreads / 32;
-  // stage: warp-per-row, 4 rows' loads in flight per warp
-  for (uint32_t r0 = warp; r0 < ih_cnt; r0 += 4 * kWarps) {
-    for (uint32_t x0 = 0; x0 < g.W; x0 += 32) {
-      const uint32_t x = x0 + lane;
-      float v[4];
+  const uint32_t unit = blockIdx.x;
+  uint32_t plane0, np, oh_begin, oh_cnt, ih_begin, ih_rows;
+  if (g.nbands == 1) {
+    plane0 = unit * g.per_cta;
+    np = min(g.per_cta, g.planes - plane0);
+    oh_begin = 0;
+    oh_cnt = g.Ho;
+    ih_begin = 0;
+    ih_rows = np * g.H;
+  } else {
+    plane0 = unit / g.nbands;
+    np = 1;
+    oh_begin = (unit - plane0 * g.nbands) * g.band;
+    oh_cnt = min(g.band, g.Ho - oh_begin);
+    ih_begin = oh_begin * S;
+    ih_rows = min(g.H - ih_begin, (oh_cnt - 1) * S + WH);
+  }
+  const float* span = g.src + static_cast<uint64_t>(plane0) * g.H * g.W +
+                      static_cast<uint64_t>(ih_begin) * g.W;
+  const uint32_t count = ih_rows * g.W;
+
+  // ---- stage: 128-bit loads of the whole span first, then scatter --------
+  const uint32_t mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(span) >> 2) & 3u);
+  const uint32_t head = min((4u - mis) & 3u, count);
+  const uint32_t nvec = (count - head) >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(span + head);
+  auto put = [&](uint32_t idx, float v) {
+    uint32_t r, c;
+    g.div_w.divmod(idx, r, c);
+    sm[r * g.pitch + ((c & 1) ? g.odd + (c >> 1) : (c >> 1))] = v;
+  };
+  constexpr int kBatch = 8;
+  for (uint32_t base = threadIdx.x; base < nvec; base += kBatch * kThreads) {
+    float4 v[kBatch];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t r = r0 + i * kWarps;
-        v[i] = (r < ih_cnt && x < g.W) ? __ldg(src + static_cast<uint64_t>(r) * g.W + x) : 0.0f;
-      }
-      const uint32_t col = (x & 1) ? odd + (x >> 1) : (x >> 1);
+    for (int i = 0; i < kBatch; ++i) {
+      const uint32_t q = base + i * kThreads;
+      if (q < nvec) v[i] = ldg_stream(s4 + q);
+    }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t r = r0 + i * kWarps;
-        if (r < ih_cnt && x < g.W) sm[r * pitch + col] = v[i];
+    for (int i = 0; i < kBatch; ++i) {
+      const uint32_t q = base + i * kThreads;
+      if (q < nvec) {
+        const uint32_t e = head + 4 * q;
+        put(e, v[i].x);
+        put(e + 1, v[i].y);
+        put(e + 2, v[i].z);
+        put(e + 3, v[i].w);
       }
     }
   }
+  if (threadIdx.x < head) put(threadIdx.x, __ldg(span + threadIdx.x));
+  const uint32_t done = head + 4 * nvec;
+  if (threadIdx.x < count - done) put(done + threadIdx.x, __ldg(span + done + threadIdx.x));
   __syncthreads();
 
-  float* obase = g.dst + plane * static_cast<uint64_t>(g.Ho) * g.Wo +
-                 static_cast<uint64_t>(oh_begin) * g.Wo;
+  // ---- compute: item = (plane, row block, output column) ----------------
   const uint32_t nrb = (oh_cnt + FH - 1) / FH;
-  const uint32_t items = nrb * g.Wo;
+  const uint32_t items = np * nrb * g.Wo;
   for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
-    uint32_t rb, ow;
-    g.div_nbw.divmod(it, rb, ow);
+    uint32_t p, rest, rb, ow;
+    if (np == 1) {
+      p = 0;
+      rest = it;
+    } else {
+      g.div_plane_items.divmod(it, p, rest);
+    }
+    g.div_wo.divmod(rest, rb, ow);
     const uint32_t r0 = rb * FH;
+    const uint32_t prow = p * g.H;  // staged-row offset of this plane
     float acc[FH];
 #pragma unroll
     for (int by = 0; by < FH; ++by) acc[by] = AVG ? 0.0f : -INFINITY;
 #pragma unroll
     for (int y = 0; y < UH; ++y) {
-      if (r0 * S + y >= ih_cnt) break;  // rows that only feed absent outputs
-      const float* row = sm + (r0 * S + y) * pitch;
+      const uint32_t rr = r0 * S + y;
+      if (np == 1 ? rr >= ih_rows : rr >= g.H) break;  // rows of absent outputs
+      const float* row = sm + (prow + rr) * g.pitch;
       float v[WW];
 #pragma unroll
-      for (int x = 0; x < WW; ++x) v[x] = (x & 1) ? row[odd + ow + (x >> 1)] : row[ow + (x >> 1)];
+      for (int x = 0; x < WW; ++x) v[x] = (x & 1) ? row[g.odd + ow + (x >> 1)] : row[ow + (x >> 1)];
 #pragma unroll
       for (int by = 0; by < FH; ++by) {
         const int dy = y - by * S;
@@ -334,11 +380,13 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_s2_kernel(NchwGeom g, uint
         }
       }
     }
+    float* orow = g.dst + static_cast<uint64_t>(plane0 + p) * g.Ho * g.Wo +
+                  static_cast<uint64_t>(oh_begin + r0) * g.Wo + ow;
 #pragma unroll
     for (int by = 0; by < FH; ++by) {
       if (r0 + by >= oh_cnt) break;
       const float o = AVG ? divide_out(acc[by], g.divisor) : acc[by];
-      stg_stream(obase + static_cast<uint64_t>(r0 + by) * g.Wo + ow, o);
+      stg_stream(orow + static_cast<uint64_t>(by) * g.Wo, o);
     }
   }
 }
@@ -552,48 +600,61 @@ bool nchw_dispatch_f(uint32_t fh, uint32_t fw, const NchwGeom& g, uint32_t block
 }  // namespace
 
 template <int WH, int FH>
-cudaError_t s2_launch(const NchwGeom& g, uint32_t blocks, uint32_t smem, uint32_t pitch,
-                      uint32_t odd, bool avg, cudaStream_t st) {
-  auto kern = avg ? pool_nchw_s2_kernel<WH, WH, FH, true> : pool_nchw_s2_kernel<WH, WH, FH, false>;
+cudaError_t s2_launch(const NchwS2Geom& g, uint32_t blocks, uint32_t smem, bool avg,
+                      cudaStream_t st) {
+  auto kern = avg ? pool_nchw_s2_kernel<WH, FH, true> : pool_nchw_s2_kernel<WH, FH, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<blocks, kThreads, smem, st>>>(g, pitch, odd);
+  kern<<<blocks, kThreads, smem, st>>>(g);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pool_nchw_s2(const PoolArgs& a, cudaStream_t st) {
   const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
   const uint32_t even = (a.w + 1) / 2;
-  const uint32_t odd = (even + 31) / 32 * 32 + 16;          // == 16 (mod 32)
-  const uint32_t pitch = odd + (a.w / 2 + 15) / 16 * 16 + 16;  // keeps rows 16-aligned
+  const uint32_t odd = (even + 31) / 32 * 32 + 16;  // == 16 (mod 32)
+  const uint32_t pitch = odd + a.w / 2 + 1;
   const uint64_t row_bytes = static_cast<uint64_t>(pitch) * 4;
+  const uint64_t plane_bytes = row_bytes * a.h;
   if (static_cast<uint64_t>(a.win_h) * row_bytes > kStageBudget) return cudaErrorNotSupported;
-  uint32_t band = static_cast<uint32_t>((kStageBudget / row_bytes - a.win_h) / 2 + 1);
-  if (band > a.ho) band = a.ho;
-  const uint64_t in_rows = static_cast<uint64_t>(band - 1) * 2 + a.win_h;
-  const uint32_t smem = static_cast<uint32_t>(in_rows * row_bytes);
-  NchwGeom g;
+  if (planes > 0xffffffffull) return cudaErrorNotSupported;
+  NchwS2Geom g;
   g.src = a.src;
   g.dst = a.dst;
   g.H = a.h;
   g.W = a.w;
   g.Ho = a.ho;
   g.Wo = a.wo;
-  g.band = band;
-  g.nbands = (a.ho + band - 1) / band;
-  g.nbw = a.wo;
-  g.div_nbw = FastDiv(a.wo);
+  g.planes = static_cast<uint32_t>(planes);
+  g.pitch = pitch;
+  g.odd = odd;
+  g.div_w = FastDiv(a.w);
+  g.div_wo = FastDiv(a.wo);
   g.divisor = static_cast<float>(a.win_h * a.win_w);  // pool.cpp:158
-  g.wh = a.win_h;
-  g.ww = a.win_w;
-  g.s = 2;
-  const uint64_t blocks64 = planes * g.nbands;
-  if (blocks64 > 0x7fffffffull) return cudaErrorNotSupported;
-  const uint32_t blocks = static_cast<uint32_t>(blocks64);
+  uint64_t units;
+  uint32_t smem;
+  if (plane_bytes <= kStageBudget) {  // whole planes, as many as fit
+    g.per_cta = static_cast<uint32_t>(kStageBudget / plane_bytes);
+    g.band = a.ho;
+    g.nbands = 1;
+    units = (planes + g.per_cta - 1) / g.per_cta;
+    smem = static_cast<uint32_t>(plane_bytes * g.per_cta);
+  } else {  // bands of output rows of one plane
+    g.per_cta = 1;
+    g.band = static_cast<uint32_t>((kStageBudget / row_bytes - a.win_h) / 2 + 1);
+    if (g.band > a.ho) g.band = a.ho;
+    g.nbands = (a.ho + g.band - 1) / g.band;
+    units = planes * g.nbands;
+    smem = static_cast<uint32_t>((static_cast<uint64_t>(g.band - 1) * 2 + a.win_h) * row_bytes);
+  }
+  const uint32_t nrb = (g.band + a.fh - 1) / a.fh;
+  g.div_plane_items = FastDiv(nrb * a.wo);
+  if (units > 0x7fffffffull) return cudaErrorNotSupported;
+  const uint32_t blocks = static_cast<uint32_t>(units);
 #define LCNN_S2(WH_, FH_) \
-  if (a.win_h == WH_ && a.fh == FH_) return s2_launch<WH_, FH_>(g, blocks, smem, pitch, odd, a.avg, st);
+  if (a.win_h == WH_ && a.fh == FH_) return s2_launch<WH_, FH_>(g, blocks, smem, a.avg, st);
   LCNN_S2(2, 1) LCNN_S2(2, 2) LCNN_S2(2, 3) LCNN_S2(2, 4)
   LCNN_S2(3, 1) LCNN_S2(3, 2) LCNN_S2(3, 3) LCNN_S2(3, 4)
 #undef LCNN_S2

@@ -46,9 +46,10 @@ __device__ __forceinline__ float group_sum(float v, unsigned mask) {
   return v;
 }
 
-// LPR lanes own one row; each lane holds VPL values.
+// LPR lanes own one row; each lane holds VPL values.  Capped at 64 registers
+// (4 CTAs = 32 warps per SM) so a 4096-row batch runs in a single wave.
 template <int LPR, int VPL, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     softmax_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
                         uint32_t rows, uint32_t cols, int* flag) {
   constexpr int kGroups = kThreads / LPR;
