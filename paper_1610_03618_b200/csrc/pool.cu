@@ -263,131 +263,172 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_kernel(NchwGeom g) {
   }
 }
 
-// Stride-2 windows, vertical coarsening (FW = 1).  A CTA owns either a group
-// of whole (n,c) planes (small maps: PL7's 13x13 planes are 676 B) or one band
-// of output rows of a large plane -- in both cases one contiguous input span,
-// which is read with 128-bit loads, all issued before any is consumed.  Each
-// staged input row is stored de-interleaved -- even columns at [0, E), odd
-// columns at [odd, odd + W/2) -- so lanes walking consecutive output columns
-// read consecutive words for every tap.
-struct NchwS2Geom {
+// Persistent, pipelined NCHW kernel (strides 1 and 2, vertical coarsening).
+// A work unit is either a group of whole (n,c) planes (small maps) or one
+// band of output rows of a large plane; either way one contiguous input
+// span.  One thread streams the spans of the next units into a kPipe-deep
+// shared-memory ring with TMA bulk copies (cp.async.bulk + mbarrier
+// complete_tx), so HBM reads of unit i+2 overlap the arithmetic of unit i.
+// Spans are copied 16-byte aligned; the <= 3 trailing floats a 16-byte
+// granule cannot cover are read from global by the (rare) taps that need them.
+constexpr int kPipe = 3;
+
+struct NchwPipeGeom {
   const float* src;
   float* dst;
   uint32_t H, W, Ho, Wo;
-  uint32_t planes;      // N*C
-  uint32_t per_cta;     // planes per CTA (whole-plane mode) or 1 (band mode)
-  uint32_t band;        // output rows per CTA (== Ho in whole-plane mode)
-  uint32_t nbands;      // bands per plane (1 in whole-plane mode)
-  uint32_t pitch, odd;  // staged row pitch, odd-column offset (words)
-  FastDiv div_w, div_wo, div_plane_items;
+  uint32_t planes;    // N*C
+  uint32_t per_cta;   // planes per unit (whole-plane mode) or 1 (band mode)
+  uint32_t band;      // output rows per unit (== Ho in whole-plane mode)
+  uint32_t nbands;    // bands per plane (1 in whole-plane mode)
+  uint32_t units;
+  uint32_t stage_floats;  // ring slot size (multiple of 4)
+  FastDiv div_wo, div_plane_items;
   float divisor;
 };
 
-template <int WH, int FH, bool AVG>
-__global__ void __launch_bounds__(kThreads) pool_nchw_s2_kernel(NchwS2Geom g) {
-  extern __shared__ float sm[];
-  constexpr int S = 2, WW = WH;
-  constexpr int UH = S * (FH - 1) + WH;
-  const uint32_t unit = blockIdx.x;
-  uint32_t plane0, np, oh_begin, oh_cnt, ih_begin, ih_rows;
-  if (g.nbands == 1) {
-    plane0 = unit * g.per_cta;
-    np = min(g.per_cta, g.planes - plane0);
-    oh_begin = 0;
-    oh_cnt = g.Ho;
-    ih_begin = 0;
-    ih_rows = np * g.H;
-  } else {
-    plane0 = unit / g.nbands;
-    np = 1;
-    oh_begin = (unit - plane0 * g.nbands) * g.band;
-    oh_cnt = min(g.band, g.Ho - oh_begin);
-    ih_begin = oh_begin * S;
-    ih_rows = min(g.H - ih_begin, (oh_cnt - 1) * S + WH);
-  }
-  const float* span = g.src + static_cast<uint64_t>(plane0) * g.H * g.W +
-                      static_cast<uint64_t>(ih_begin) * g.W;
-  const uint32_t count = ih_rows * g.W;
+struct PipeUnit {
+  uint32_t plane0, np, oh_begin, oh_cnt, ih_rows;
+  const float* span;
+  uint32_t count;
+};
 
-  // ---- stage: 128-bit loads of the whole span first, then scatter --------
-  const uint32_t mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(span) >> 2) & 3u);
-  const uint32_t head = min((4u - mis) & 3u, count);
-  const uint32_t nvec = (count - head) >> 2;
-  const float4* s4 = reinterpret_cast<const float4*>(span + head);
-  auto put = [&](uint32_t idx, float v) {
-    uint32_t r, c;
-    g.div_w.divmod(idx, r, c);
-    sm[r * g.pitch + ((c & 1) ? g.odd + (c >> 1) : (c >> 1))] = v;
-  };
-  constexpr int kBatch = 8;
-  for (uint32_t base = threadIdx.x; base < nvec; base += kBatch * kThreads) {
-    float4 v[kBatch];
-#pragma unroll
-    for (int i = 0; i < kBatch; ++i) {
-      const uint32_t q = base + i * kThreads;
-      if (q < nvec) v[i] = ldg_stream(s4 + q);
-    }
-#pragma unroll
-    for (int i = 0; i < kBatch; ++i) {
-      const uint32_t q = base + i * kThreads;
-      if (q < nvec) {
-        const uint32_t e = head + 4 * q;
-        put(e, v[i].x);
-        put(e + 1, v[i].y);
-        put(e + 2, v[i].z);
-        put(e + 3, v[i].w);
-      }
-    }
+__device__ __forceinline__ PipeUnit pipe_unit(const NchwPipeGeom& g, uint32_t u, uint32_t S,
+                                              uint32_t WH) {
+  PipeUnit pu;
+  if (g.nbands == 1) {
+    pu.plane0 = u * g.per_cta;
+    pu.np = min(g.per_cta, g.planes - pu.plane0);
+    pu.oh_begin = 0;
+    pu.oh_cnt = g.Ho;
+    pu.ih_rows = pu.np * g.H;
+  } else {
+    pu.plane0 = u / g.nbands;
+    pu.np = 1;
+    pu.oh_begin = (u - pu.plane0 * g.nbands) * g.band;
+    pu.oh_cnt = min(g.band, g.Ho - pu.oh_begin);
+    pu.ih_rows = min(g.H - pu.oh_begin * S, (pu.oh_cnt - 1) * S + WH);
   }
-  if (threadIdx.x < head) put(threadIdx.x, __ldg(span + threadIdx.x));
-  const uint32_t done = head + 4 * nvec;
-  if (threadIdx.x < count - done) put(done + threadIdx.x, __ldg(span + done + threadIdx.x));
+  pu.span = g.src + static_cast<uint64_t>(pu.plane0) * g.H * g.W +
+            static_cast<uint64_t>(pu.oh_begin) * S * g.W;
+  pu.count = pu.ih_rows * g.W;
+  return pu;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+template <int WH, int S, int FH, bool AVG>
+__global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g) {
+  extern __shared__ __align__(16) float ring[];
+  __shared__ __align__(8) uint64_t bar[kPipe];
+  __shared__ uint32_t meta[kPipe][2];  // (float offset of the span, floats copied)
+  constexpr int WW = WH;
+  constexpr int UH = S * (FH - 1) + WH;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kPipe; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(&bar[k]))));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
-  // ---- compute: item = (plane, row block, output column) ----------------
-  const uint32_t nrb = (oh_cnt + FH - 1) / FH;
-  const uint32_t items = np * nrb * g.Wo;
-  for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
-    uint32_t p, rest, rb, ow;
-    if (np == 1) {
-      p = 0;
-      rest = it;
+  auto issue = [&](uint32_t i) {  // unit index i of this CTA -> ring slot i % kPipe
+    const uint32_t u = blockIdx.x + i * gridDim.x;
+    if (u >= g.units) return;
+    const PipeUnit pu = pipe_unit(g, u, S, WH);
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(pu.span);
+    const uint32_t mis = static_cast<uint32_t>((addr >> 2) & 3u);
+    const uint32_t bytes = ((mis + pu.count) * 4u) & ~15u;
+    const int k = i % kPipe;
+    meta[k][0] = mis;
+    meta[k][1] = bytes / 4;
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[k]));
+    if (bytes) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                   : "memory");
+      bulk_g2s(ring + static_cast<size_t>(k) * g.stage_floats,
+               reinterpret_cast<const void*>(addr & ~uintptr_t(15)), bytes, &bar[k]);
     } else {
-      g.div_plane_items.divmod(it, p, rest);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
     }
-    g.div_wo.divmod(rest, rb, ow);
-    const uint32_t r0 = rb * FH;
-    const uint32_t prow = p * g.H;  // staged-row offset of this plane
-    float acc[FH];
+  };
+
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kPipe - 1; ++i) issue(i);
+
+  for (uint32_t i = 0;; ++i) {
+    const uint32_t u = blockIdx.x + i * gridDim.x;
+    if (u >= g.units) break;
+    if (threadIdx.x == 0) issue(i + kPipe - 1);
+    const int k = i % kPipe;
+    {
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[k]));
+      const uint32_t parity = (i / kPipe) & 1;
+      asm volatile(
+          "{\n.reg .pred p;\nWAIT_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          "@!p bra WAIT_%=;\n}\n" ::"r"(b),
+          "r"(parity)
+          : "memory");
+    }
+    const PipeUnit pu = pipe_unit(g, u, S, WH);
+    const float* sbuf = ring + static_cast<size_t>(k) * g.stage_floats + meta[k][0];
+    const uint32_t in_smem = meta[k][1] - meta[k][0];  // span floats resident in smem
+    const uint32_t nrb = (pu.oh_cnt + FH - 1) / FH;
+    const uint32_t items = pu.np * nrb * g.Wo;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+      uint32_t p, rest, rb, ow;
+      if (pu.np == 1) {
+        p = 0;
+        rest = it;
+      } else {
+        g.div_plane_items.divmod(it, p, rest);
+      }
+      g.div_wo.divmod(rest, rb, ow);
+      const uint32_t r0 = rb * FH;
+      const uint32_t prow = p * g.H;
+      float acc[FH];
 #pragma unroll
-    for (int by = 0; by < FH; ++by) acc[by] = AVG ? 0.0f : -INFINITY;
+      for (int by = 0; by < FH; ++by) acc[by] = AVG ? 0.0f : -INFINITY;
 #pragma unroll
-    for (int y = 0; y < UH; ++y) {
-      const uint32_t rr = r0 * S + y;
-      if (np == 1 ? rr >= ih_rows : rr >= g.H) break;  // rows of absent outputs
-      const float* row = sm + (prow + rr) * g.pitch;
-      float v[WW];
-#pragma unroll
-      for (int x = 0; x < WW; ++x) v[x] = (x & 1) ? row[g.odd + ow + (x >> 1)] : row[ow + (x >> 1)];
-#pragma unroll
-      for (int by = 0; by < FH; ++by) {
-        const int dy = y - by * S;
-        if (dy < 0 || dy >= WH) continue;
+      for (int y = 0; y < UH; ++y) {
+        const uint32_t rr = r0 * S + y;
+        if (pu.np == 1 ? rr >= pu.ih_rows : rr >= g.H) break;  // rows of absent outputs
+        const uint32_t e0 = (prow + rr) * g.W + ow * S;
+        float v[WW];
 #pragma unroll
         for (int x = 0; x < WW; ++x) {
-          if constexpr (AVG) acc[by] = add_tap(acc[by], v[x]);
-          else acc[by] = max_tap(acc[by], v[x]);
+          const uint32_t e = e0 + x;
+          v[x] = e < in_smem ? sbuf[e] : __ldg(pu.span + e);
+        }
+#pragma unroll
+        for (int by = 0; by < FH; ++by) {
+          const int dy = y - by * S;
+          if (dy < 0 || dy >= WH) continue;
+#pragma unroll
+          for (int x = 0; x < WW; ++x) {
+            if constexpr (AVG) acc[by] = add_tap(acc[by], v[x]);
+            else acc[by] = max_tap(acc[by], v[x]);
+          }
         }
       }
-    }
-    float* orow = g.dst + static_cast<uint64_t>(plane0 + p) * g.Ho * g.Wo +
-                  static_cast<uint64_t>(oh_begin + r0) * g.Wo + ow;
+      float* orow = g.dst + static_cast<uint64_t>(pu.plane0 + p) * g.Ho * g.Wo +
+                    static_cast<uint64_t>(pu.oh_begin + r0) * g.Wo + ow;
 #pragma unroll
-    for (int by = 0; by < FH; ++by) {
-      if (r0 + by >= oh_cnt) break;
-      const float o = AVG ? divide_out(acc[by], g.divisor) : acc[by];
-      stg_stream(orow + static_cast<uint64_t>(by) * g.Wo, o);
+      for (int by = 0; by < FH; ++by) {
+        if (r0 + by >= pu.oh_cnt) break;
+        const float o = AVG ? divide_out(acc[by], g.divisor) : acc[by];
+        stg_stream(orow + static_cast<uint64_t>(by) * g.Wo, o);
+      }
     }
+    __syncthreads();  // slot k is refilled by the issue() of iteration i + 1
   }
 }
 
@@ -599,10 +640,10 @@ bool nchw_dispatch_f(uint32_t fh, uint32_t fw, const NchwGeom& g, uint32_t block
 
 }  // namespace
 
-template <int WH, int FH>
-cudaError_t s2_launch(const NchwS2Geom& g, uint32_t blocks, uint32_t smem, bool avg,
-                      cudaStream_t st) {
-  auto kern = avg ? pool_nchw_s2_kernel<WH, FH, true> : pool_nchw_s2_kernel<WH, FH, false>;
+template <int WH, int S, int FH>
+cudaError_t pipe_launch(const NchwPipeGeom& g, uint32_t blocks, uint32_t smem, bool avg,
+                        cudaStream_t st) {
+  auto kern = avg ? pool_nchw_pipe_kernel<WH, S, FH, true> : pool_nchw_pipe_kernel<WH, S, FH, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -611,16 +652,14 @@ cudaError_t s2_launch(const NchwS2Geom& g, uint32_t blocks, uint32_t smem, bool 
   return cudaGetLastError();
 }
 
-cudaError_t launch_pool_nchw_s2(const PoolArgs& a, cudaStream_t st) {
+cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
   const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
-  const uint32_t even = (a.w + 1) / 2;
-  const uint32_t odd = (even + 31) / 32 * 32 + 16;  // == 16 (mod 32)
-  const uint32_t pitch = odd + a.w / 2 + 1;
-  const uint64_t row_bytes = static_cast<uint64_t>(pitch) * 4;
+  const uint64_t row_bytes = static_cast<uint64_t>(a.w) * 4;
   const uint64_t plane_bytes = row_bytes * a.h;
-  if (static_cast<uint64_t>(a.win_h) * row_bytes > kStageBudget) return cudaErrorNotSupported;
+  constexpr uint64_t kSlot = 24 * 1024;  // bytes of input per ring slot
+  if (static_cast<uint64_t>(a.win_h) * row_bytes + 16 > kSlot) return cudaErrorNotSupported;
   if (planes > 0xffffffffull) return cudaErrorNotSupported;
-  NchwS2Geom g;
+  NchwPipeGeom g;
   g.src = a.src;
   g.dst = a.dst;
   g.H = a.h;
@@ -628,45 +667,51 @@ cudaError_t launch_pool_nchw_s2(const PoolArgs& a, cudaStream_t st) {
   g.Ho = a.ho;
   g.Wo = a.wo;
   g.planes = static_cast<uint32_t>(planes);
-  g.pitch = pitch;
-  g.odd = odd;
-  g.div_w = FastDiv(a.w);
   g.div_wo = FastDiv(a.wo);
   g.divisor = static_cast<float>(a.win_h * a.win_w);  // pool.cpp:158
-  uint64_t units;
-  uint32_t smem;
-  if (plane_bytes <= kStageBudget) {  // whole planes, as many as fit
-    g.per_cta = static_cast<uint32_t>(kStageBudget / plane_bytes);
+  uint64_t units, span_bytes;
+  if (plane_bytes + 16 <= kSlot) {  // whole planes, as many as fit
+    g.per_cta = static_cast<uint32_t>((kSlot - 16) / plane_bytes);
     g.band = a.ho;
     g.nbands = 1;
     units = (planes + g.per_cta - 1) / g.per_cta;
-    smem = static_cast<uint32_t>(plane_bytes * g.per_cta);
+    span_bytes = plane_bytes * g.per_cta;
   } else {  // bands of output rows of one plane
     g.per_cta = 1;
-    g.band = static_cast<uint32_t>((kStageBudget / row_bytes - a.win_h) / 2 + 1);
+    g.band = static_cast<uint32_t>(((kSlot - 16) / row_bytes - a.win_h) / a.stride + 1);
     if (g.band > a.ho) g.band = a.ho;
     g.nbands = (a.ho + g.band - 1) / g.band;
     units = planes * g.nbands;
-    smem = static_cast<uint32_t>((static_cast<uint64_t>(g.band - 1) * 2 + a.win_h) * row_bytes);
+    span_bytes = (static_cast<uint64_t>(g.band - 1) * a.stride + a.win_h) * row_bytes;
   }
+  if (units > 0xffffffffull) return cudaErrorNotSupported;
+  g.units = static_cast<uint32_t>(units);
+  g.stage_floats = static_cast<uint32_t>((span_bytes + 16 + 15) / 16 * 4);
   const uint32_t nrb = (g.band + a.fh - 1) / a.fh;
   g.div_plane_items = FastDiv(nrb * a.wo);
-  if (units > 0x7fffffffull) return cudaErrorNotSupported;
-  const uint32_t blocks = static_cast<uint32_t>(units);
-#define LCNN_S2(WH_, FH_) \
-  if (a.win_h == WH_ && a.fh == FH_) return s2_launch<WH_, FH_>(g, blocks, smem, a.avg, st);
-  LCNN_S2(2, 1) LCNN_S2(2, 2) LCNN_S2(2, 3) LCNN_S2(2, 4)
-  LCNN_S2(3, 1) LCNN_S2(3, 2) LCNN_S2(3, 3) LCNN_S2(3, 4)
-#undef LCNN_S2
+  const uint32_t smem = kPipe * g.stage_floats * 4;
+  // persistent: up to 3 CTAs per SM (72 KB rings), never more CTAs than units
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t cap = static_cast<uint64_t>(sms) * 3;
+  const uint32_t blocks = static_cast<uint32_t>(units < cap ? units : cap);
+#define LCNN_PIPE(WH_, S_, FH_)                                 \
+  if (a.win_h == WH_ && a.stride == S_ && a.fh == FH_)          \
+    return pipe_launch<WH_, S_, FH_>(g, blocks, smem, a.avg, st);
+  LCNN_PIPE(2, 2, 1) LCNN_PIPE(2, 2, 2) LCNN_PIPE(2, 2, 3) LCNN_PIPE(2, 2, 4)
+  LCNN_PIPE(3, 2, 1) LCNN_PIPE(3, 2, 2) LCNN_PIPE(3, 2, 3) LCNN_PIPE(3, 2, 4)
+  LCNN_PIPE(3, 1, 1) LCNN_PIPE(3, 1, 2) LCNN_PIPE(3, 1, 3) LCNN_PIPE(3, 1, 4)
+#undef LCNN_PIPE
   return cudaErrorNotSupported;
 }
 
 cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t st) {
   const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
   if (planes == 0 || a.ho == 0 || a.wo == 0) return cudaSuccess;
-  if (a.stride == 2 && a.fw == 1 && a.fh <= 4 && a.win_h == a.win_w &&
-      (a.win_h == 2 || a.win_h == 3)) {
-    const cudaError_t e = launch_pool_nchw_s2(a, st);
+  if (a.fw == 1 && a.fh <= 4 && a.win_h == a.win_w &&
+      ((a.stride == 2 && (a.win_h == 2 || a.win_h == 3)) || (a.stride == 1 && a.win_h == 3))) {
+    const cudaError_t e = launch_pool_nchw_pipe(a, st);
     if (e != cudaErrorNotSupported) return e;
   }
   const uint64_t row_bytes = static_cast<uint64_t>(a.w) * 4;
