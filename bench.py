@@ -226,7 +226,7 @@ def build_workload(name, torch, device, rank, plan):
     if name in ("vgg_pools", "vgg_pools_nchw"):
         b = 256
         layout = CHWN if name == "vgg_pools" else NCHW
-        plan = plan or ((1, 1) if layout == CHWN else (3, 1))
+        plan = plan or ((1, 1) if layout == CHWN else (3, 1))  # measured best (scripts/pool_plans.py)
         ops = [PoolOp(torch, device, b, c, hw, hw, layout, 2, 2, False, plan, seed + i)
                for i, (c, hw) in enumerate(VGG_POOLS)]
         lname = "CHWN (selector's pooling layout)" if layout == CHWN else "NCHW"
@@ -237,7 +237,7 @@ def build_workload(name, torch, device, rank, plan):
         return ops, desc, 0, b
     if name in ("pl5", "pl5_nchw"):
         layout = CHWN if name == "pl5" else NCHW
-        p = plan or ((2, 2) if layout == CHWN else (2, 1))
+        p = plan or ((2, 2) if layout == CHWN else (3, 1))  # measured best (scripts/pool_plans.py)
         ops = [PoolOp(torch, device, 128, 96, 55, 55, layout, 3, 2, False, p, seed)]
         desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) max 3x3/s2, "
                             f"128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",

@@ -269,8 +269,10 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_kernel(NchwGeom g) {
 // span.  One thread streams the spans of the next units into a kPipe-deep
 // shared-memory ring with TMA bulk copies (cp.async.bulk + mbarrier
 // complete_tx), so HBM reads of unit i+2 overlap the arithmetic of unit i.
-// Spans are copied 16-byte aligned; the <= 3 trailing floats a 16-byte
-// granule cannot cover are read from global by the (rare) taps that need them.
+// Spans are copied 16-byte aligned; the issuing thread patches the <= 3
+// trailing floats a 16-byte granule cannot cover into the slot with plain
+// loads (visible to the consumers through the barriers that separate issue
+// from use), so the tap loop reads shared memory unconditionally.
 constexpr int kPipe = 3;
 
 struct NchwPipeGeom {
@@ -349,6 +351,9 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
     const int k = i % kPipe;
     meta[k][0] = mis;
     meta[k][1] = bytes / 4;
+    float* slot = ring + static_cast<size_t>(k) * g.stage_floats;
+    for (uint32_t e = bytes / 4 > mis ? bytes / 4 - mis : 0; e < pu.count; ++e)
+      slot[mis + e] = __ldg(pu.span + e);
     const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[k]));
     if (bytes) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
@@ -380,7 +385,6 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
     }
     const PipeUnit pu = pipe_unit(g, u, S, WH);
     const float* sbuf = ring + static_cast<size_t>(k) * g.stage_floats + meta[k][0];
-    const uint32_t in_smem = meta[k][1] - meta[k][0];  // span floats resident in smem
     const uint32_t nrb = (pu.oh_cnt + FH - 1) / FH;
     const uint32_t items = pu.np * nrb * g.Wo;
     for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
@@ -405,8 +409,7 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
         float v[WW];
 #pragma unroll
         for (int x = 0; x < WW; ++x) {
-          const uint32_t e = e0 + x;
-          v[x] = e < in_smem ? sbuf[e] : __ldg(pu.span + e);
+          v[x] = sbuf[e0 + x];
         }
 #pragma unroll
         for (int by = 0; by < FH; ++by) {
