@@ -38,7 +38,7 @@ namespace lcnn_dev {
 
 using namespace lcnn_tc;
 
-enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1 };
+enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2 };
 
 struct ConvGeomTc {
   uint32_t N, Ci, H, W, Co, FH, FW, S, P, Ho, Wo;
@@ -60,6 +60,11 @@ __global__ void pack_filters_kernel(const float* __restrict__ f, float* __restri
       const uint32_t tap = k / g.Ci;
       fh = tap / g.FW;
       fw = tap % g.FW;
+    } else if (g.mode == kModeNAT) {  // natural (ci, fh, fw) order, K padded
+      fw = k % g.FW;
+      fh = (k / g.FW) % g.FH;
+      ci = k / (g.FW * g.FH);
+      valid = ci < g.Ci;
     } else {
       fw = k % g.FP;
       const uint32_t t = k / g.FP;
@@ -168,6 +173,166 @@ struct RowsOut {  // C[m][col] row-major, ldc = ncols
     }
   }
 };
+
+// ---- NCHW implicit GEMM on tcgen05 --------------------------------------
+//   D[co][(n, p)] = sum_k W[co][k] * X[k][(n, p)],  k = (ci, fh, fw),
+//   p = oh*Wo + ow.  NCHW rows of odd width cannot be TMA tensors (16-byte
+//   global stride rule), so the B tile is gathered: 128 producer threads each
+//   own one output column, load its 32 K-values of the stage (consecutive
+//   lanes = consecutive ow, so stride-1 convolutions read coalesced rows;
+//   padding is a bounds check), and write them as 128-bit chunks into a
+//   K-major SWIZZLE_128B image (each 8-lane phase hits 8 distinct swizzled
+//   16-byte slots: conflict-free), then fence the async proxy and arrive on
+//   the stage barrier.  Filters come by TMA (natural K order, zero-padded).
+//   Warps 0-3: B gather, warp 4: A TMA, warp 5: MMA, warps 6-9: epilogue.
+constexpr int kNchwThreads = 320;
+
+struct NchwConvParams {
+  CUtensorMap a;  // packed filters (2D: {K, Co}, box {32, 128})
+  const float* x;
+  float* y;
+  uint32_t Ci, H, W, Co, FH, FW, S, Pad, Ho, Wo, P;
+  uint32_t K, kb, ncols;  // true K, k-blocks of 32, N * Ho * Wo
+};
+
+__global__ void __launch_bounds__(kNchwThreads, 1)
+    tc_conv_nchw_kernel(const __grid_constant__ NchwConvParams prm) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw_smem) + 1023) &
+                                             ~uintptr_t(1023));
+  TcCtl* ctl = reinterpret_cast<TcCtl*>(smem + kTcStages * kTcStageBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t m0 = blockIdx.y * kTcBM;
+  const uint32_t ntile = blockIdx.x;
+  if (warp == 4) {
+    if (lane == 0) {
+      tma_prefetch(&prm.a);
+      for (int s = 0; s < kTcStages; ++s) {
+        mbar_init(&ctl->full[s], 129);  // 128 gather threads + the A TMA arrive
+        mbar_init(&ctl->empty[s], 1);
+      }
+      mbar_init(&ctl->tmem_full, 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc<128>(&ctl->tmem_addr);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_addr;
+
+  if (warp < 4) {
+    // ---------------- B gather producers ----------------
+    const uint32_t c = threadIdx.x;  // column of the tile == row of the K-major image
+    const uint32_t j = ntile * kTcBN + c;
+    const bool valid = j < prm.ncols;
+    const uint32_t n = valid ? j / prm.P : 0;
+    const uint32_t pp = valid ? j - n * prm.P : 0;
+    const uint32_t oh = pp / prm.Wo, ow = pp - oh * prm.Wo;
+    const int32_t ih0 = static_cast<int32_t>(oh * prm.S) - static_cast<int32_t>(prm.Pad);
+    const int32_t iw0 = static_cast<int32_t>(ow * prm.S) - static_cast<int32_t>(prm.Pad);
+    const float* img = prm.x + static_cast<uint64_t>(n) * prm.Ci * prm.H * prm.W;
+    const uint32_t r8 = c & 7;
+    const uint32_t row_off = (c >> 3) * 1024 + r8 * 128;
+    uint32_t ci = 0, fh = 0, fw = 0;  // decode of the next k
+    uint32_t s = 0, phase = 0;
+    for (uint32_t kb = 0; kb < prm.kb; ++kb) {
+      mbar_wait(&ctl->empty[s], phase ^ 1);
+      float v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int32_t ih = ih0 + static_cast<int32_t>(fh);
+        const int32_t iw = iw0 + static_cast<int32_t>(fw);
+        const bool in = valid && ci < prm.Ci && ih >= 0 && ih < static_cast<int32_t>(prm.H) &&
+                        iw >= 0 && iw < static_cast<int32_t>(prm.W);
+        v[q] = in ? __ldg(img + (static_cast<uint64_t>(ci) * prm.H + ih) * prm.W + iw) : 0.0f;
+        if (++fw == prm.FW) {
+          fw = 0;
+          if (++fh == prm.FH) {
+            fh = 0;
+            ++ci;
+          }
+        }
+      }
+      uint8_t* sb = smem + s * kTcStageBytes + kTcABytes + row_off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(sb + ((q ^ r8) << 4)) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&ctl->full[s]);
+      if (++s == kTcStages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp == 4 && lane == 0) {
+    // ---------------- A (filters) TMA producer ----------------
+    uint32_t s = 0, phase = 0;
+    for (uint32_t kb = 0; kb < prm.kb; ++kb) {
+      mbar_wait(&ctl->empty[s], phase ^ 1);
+      mbar_arrive_expect_tx(&ctl->full[s], kTcABytes);
+      tma_load_2d(smem + s * kTcStageBytes, &prm.a, &ctl->full[s], kb * kTcBK, m0);
+      if (++s == kTcStages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp == 5 && lane == 0) {
+    // ---------------- MMA issuer (both operands K-major SW128) ----------------
+    constexpr uint32_t idesc = idesc_tf32(kTcBM, kTcBN, false, false);
+    uint32_t s = 0, phase = 0;
+    for (uint32_t kb = 0; kb < prm.kb; ++kb) {
+      mbar_wait(&ctl->full[s], phase);
+      tc_fence_after();
+      const uint8_t* sa = smem + s * kTcStageBytes;
+      const uint8_t* sb = sa + kTcABytes;
+#pragma unroll
+      for (int k = 0; k < kTcBK / 8; ++k)
+        mma_tf32(tmem, smem_desc_sw128(sa + k * 32, 16, 1024), smem_desc_sw128(sb + k * 32, 16, 1024),
+                 idesc, (kb | k) != 0);
+      tc_commit(&ctl->empty[s]);
+      if (++s == kTcStages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+    tc_commit(&ctl->tmem_full);
+  } else if (warp >= 6) {
+    // ---------------- epilogue: out[n][co][p] ----------------
+    const int q = warp & 3;
+    mbar_wait(&ctl->tmem_full, 0);
+    tc_fence_after();
+    const uint32_t co = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int cc = 0; cc < kTcBN; cc += 32) {
+      float v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + cc, v);
+      if (co >= prm.Co) continue;
+      uint32_t j = ntile * kTcBN + cc;
+      if (j >= prm.ncols) continue;
+      uint32_t n = j / prm.P, pp = j - n * prm.P;
+      float* dst = prm.y + (static_cast<uint64_t>(n) * prm.Co + co) * prm.P + pp;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if (j + t < prm.ncols) *dst = v[t];
+        ++dst;
+        if (++pp == prm.P) {  // next image: jump to its row of channel co
+          pp = 0;
+          ++n;
+          dst = prm.y + (static_cast<uint64_t>(n) * prm.Co + co) * prm.P;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<128>(tmem);
+  }
+}
 
 // ---- fp32 SIMT direct convolution (any shape, CHWN or NCHW) --------------
 struct ConvGeomSimt {
@@ -327,6 +492,44 @@ struct TcPlan {
   uint32_t K = 0;  // packed K (multiple of 32)
 };
 
+cudaError_t launch_conv_nchw_tc(const ConvArgs& a, cudaStream_t s) {
+  ConvGeomTc g{a.n, a.ci, a.h, a.w, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo, kModeNAT, 0, 0, 0};
+  const uint32_t K = a.ci * a.fh * a.fw;
+  const uint32_t Kp = (K + kTcBK - 1) / kTcBK * kTcBK;
+  float* wpack = static_cast<float*>(a.workspace);
+  pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, wpack, nullptr, g, Kp);
+  NchwConvParams prm;
+  if (!make_tmap_2d(&prm.a, wpack, Kp, a.co, static_cast<uint64_t>(Kp) * 4, kTcBK, kTcBM, false))
+    return cudaErrorInvalidValue;
+  prm.x = a.src;
+  prm.y = a.dst;
+  prm.Ci = a.ci;
+  prm.H = a.h;
+  prm.W = a.w;
+  prm.Co = a.co;
+  prm.FH = a.fh;
+  prm.FW = a.fw;
+  prm.S = a.stride;
+  prm.Pad = a.pad;
+  prm.Ho = a.ho;
+  prm.Wo = a.wo;
+  prm.P = a.ho * a.wo;
+  prm.K = K;
+  prm.kb = Kp / kTcBK;
+  prm.ncols = a.n * prm.P;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_nchw_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kTcSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid((prm.ncols + kTcBN - 1) / kTcBN, (a.co + kTcBM - 1) / kTcBM);
+  tc_conv_nchw_kernel<<<grid, kNchwThreads, kTcSmem, s>>>(prm);
+  return cudaGetLastError();
+}
+
 TcPlan plan_tc(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, int layout, uint32_t co,
                uint32_t fh, uint32_t fw, uint32_t stride, uint32_t pad, uint32_t ho,
                uint32_t wo) {
@@ -365,6 +568,9 @@ size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, uin
 }
 
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
+  if (a.layout == LCNN_NCHW && a.precision == LCNN_PREC_TF32 &&
+      static_cast<uint64_t>(a.n) * a.ho * a.wo < (1ull << 31))
+    return launch_conv_nchw_tc(a, s);
   const bool want_tc = a.precision != LCNN_PREC_FP32;
   TcPlan p = want_tc ? plan_tc(a.n, a.ci, a.h, a.w, a.layout, a.co, a.fh, a.fw, a.stride, a.pad,
                                a.ho, a.wo)

@@ -38,13 +38,14 @@ for (m, n, k) in [(8192, 8192, 8192), (4096, 4096, 4096), (128, 4096, 9216), (10
 convs = {"conv1": (3, 227, 96, 11, 4, 0), "conv2": (96, 27, 192, 5, 1, 2), "conv3": (192, 13, 384, 3, 1, 1),
          "conv4": (384, 13, 256, 3, 1, 1), "conv5": (256, 13, 256, 3, 1, 1)}
 N = 128
-for name, (ci, hw, co, f, s, p) in convs.items():
-    x = lcnn.DeviceTensor4D(N, ci, hw, hw, lcnn.CHWN, torch.rand(N * ci * hw * hw, device=dev))
-    w = torch.rand(co * ci * f * f, device=dev)
-    ho = (hw + 2 * p - f) // s + 1
-    out = lcnn.DeviceTensor4D(N, co, ho, ho, lcnn.CHWN, torch.empty(N * co * ho * ho, device=dev))
-    ws = torch.empty(64 << 20, device=dev)
-    ms = timeit(lambda: lcnn.conv_forward(x, w, co, f, f, s, p, lcnn.TF32, out=out, workspace=ws))
-    fl = 2 * N * co * ho * ho * ci * f * f
-    res[name] = {"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1)}
+for layout, tag in ((lcnn.CHWN, "chwn"), (lcnn.NCHW, "nchw")):
+    for name, (ci, hw, co, f, s, p) in convs.items():
+        x = lcnn.DeviceTensor4D(N, ci, hw, hw, layout, torch.rand(N * ci * hw * hw, device=dev))
+        w = torch.rand(co * ci * f * f, device=dev)
+        ho = (hw + 2 * p - f) // s + 1
+        out = lcnn.DeviceTensor4D(N, co, ho, ho, layout, torch.empty(N * co * ho * ho, device=dev))
+        ws = torch.empty(64 << 20, device=dev)
+        ms = timeit(lambda: lcnn.conv_forward(x, w, co, f, f, s, p, lcnn.TF32, out=out, workspace=ws))
+        fl = 2 * N * co * ho * ho * ci * f * f
+        res[f"{name}_{tag}"] = {"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1)}
 print(json.dumps(res, indent=1))
