@@ -18,7 +18,14 @@ HOSTOBJ := $(patsubst $(PKG)/host/src/%.cpp,$(OBJDIR)/host_%.o,$(HOSTSRC))
 HOSTLIB := $(PKG)/lib/liblcnn.so
 HOSTFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -I$(PKG)/host/include -Iinclude -I$(CUDA)/include
 
-all: $(LIB) $(HOSTLIB) oracle
+TOOLS   := build/tools/calibrate_b200
+
+all: $(LIB) $(HOSTLIB) $(TOOLS) oracle
+
+build/tools/%: tools/%.cpp $(HOSTLIB)
+	@mkdir -p build/tools
+	$(CXX) $(HOSTFLAGS) $< -o $@ -L$(PKG)/lib -llcnn -llcnn_cuda \
+	  -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib'
 
 $(OBJDIR)/host_%.o: $(PKG)/host/src/%.cpp $(wildcard $(PKG)/host/include/lcnn/*.hpp) $(PKG)/host/src/json_lite.hpp include/lcnn_cuda.h include/lcnn_net.h
 	@mkdir -p $(OBJDIR)
