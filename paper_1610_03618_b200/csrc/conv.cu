@@ -93,25 +93,25 @@ struct ChwnConvLoader {
   ConvGeomTc g;
   uint32_t kb, segs, ncols;  // ncols = Ho*Wo*N
   static constexpr bool kBMajorMN = true;
-  __device__ uint32_t kblocks() const { return kb; }
+  __device__ uint32_t kblocks(uint32_t) const { return kb; }
   __device__ uint32_t segments() const { return segs; }
   __device__ void prefetch() const {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
   }
-  // Per tile: the four 32-column boxes' (n0, w origin, h origin) decoded once;
-  // per k-block: the tap / channel-block counters advance incrementally.
+  // Per tile: the eight 32-column boxes' (n0, w origin, h origin) decoded
+  // once; per k-block: the tap / channel-block counters advance incrementally.
   struct State {
     uint32_t m0;
-    int32_t n0[4], y0[4], z0[4];
+    int32_t n0[kPBN / 32], y0[kPBN / 32], z0[kPBN / 32];
     uint32_t fh, wofs, c0;  // K decode of the next k-block
   };
-  __device__ State begin(uint32_t m0, uint32_t ntile) const {
+  __device__ State begin(uint32_t m0, uint32_t ncol0, uint32_t) const {
     State st;
     st.m0 = m0;
 #pragma unroll
-    for (int j = 0; j < kTcBN / 32; ++j) {
-      const uint32_t col = ntile * kTcBN + 32 * j;
+    for (int j = 0; j < kPBN / 32; ++j) {
+      const uint32_t col = ncol0 + 32 * j;
       const uint32_t pos = col / g.N;
       const uint32_t oh = pos / g.Wo, ow = pos - oh * g.Wo;
       st.n0[j] = static_cast<int32_t>(col - pos * g.N);
@@ -129,7 +129,7 @@ struct ChwnConvLoader {
     tma_load_2d(sa, &a[seg == 2 ? 1 : 0], bar, k * kTcBK, st.m0);
     const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
 #pragma unroll
-    for (int j = 0; j < kTcBN / 32; ++j)
+    for (int j = 0; j < kPBN / 32; ++j)
       tma_load_4d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, st.n0[j],
                   st.y0[j] + static_cast<int32_t>(st.wofs), st.z0[j] + static_cast<int32_t>(st.fh),
                   static_cast<int32_t>(st.c0));
@@ -157,10 +157,8 @@ struct RowsOut {  // C[m][col] row-major, ldc = ncols
   float* c;
   uint64_t ldc;
   uint32_t M, N;
-  __device__ __forceinline__ void store32(uint32_t m, uint32_t ntile, uint32_t col,
-                                          const float* v) const {
-    if (m >= M) return;
-    const uint32_t n0 = ntile * kTcBN + col;
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v) const {
+    if (m >= M || n0 >= N) return;
     float* row = c + m * ldc + n0;
     if (n0 + 32 <= N) {
 #pragma unroll
@@ -629,16 +627,17 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   L.segs = x3 ? 3 : 1;
   L.ncols = a.ho * a.wo * a.n;
   RowsOut O{a.dst, L.ncols, a.co, L.ncols};
-  auto kern = tc_gemm_kernel<ChwnConvLoader, RowsOut>;
+  auto kern = tc_gemm_persistent<ChwnConvLoader, RowsOut>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kTcSmem));
+                                         static_cast<int>(kPSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const dim3 grid((L.ncols + kTcBN - 1) / kTcBN, (a.co + kTcBM - 1) / kTcBM);
-  kern<<<grid, kTcThreads, kTcSmem, s>>>(L, O);
+  const TileGrid tg{(a.co + kTcBM - 1) / kTcBM, (L.ncols + kPBN - 1) / kPBN, 1};
+  const uint32_t all = tg.mt * tg.nt;
+  kern<<<all < 148 ? all : 148, kTcThreads, kPSmem, s>>>(L, O, tg);
   return cudaGetLastError();
 }
 

@@ -42,10 +42,7 @@ struct GemmLoader {
   uint32_t split_kb;  // k-blocks per split (blockIdx.z); == kb without split-K
   uint32_t segs;
   static constexpr bool kBMajorMN = true;
-  __device__ uint32_t kblocks() const {
-    const uint32_t k0 = blockIdx.z * split_kb;
-    return min(split_kb, kb - k0);
-  }
+  __device__ uint32_t kblocks(uint32_t z) const { return min(split_kb, kb - z * split_kb); }
   __device__ uint32_t segments() const { return segs; }
   __device__ void prefetch() const {
     tma_prefetch(&a[0]);
@@ -54,8 +51,8 @@ struct GemmLoader {
   struct State {
     uint32_t m0, n0, k0;
   };
-  __device__ State begin(uint32_t m0, uint32_t ntile) const {
-    return State{m0, ntile * kTcBN, blockIdx.z * split_kb};
+  __device__ State begin(uint32_t m0, uint32_t n0, uint32_t z) const {
+    return State{m0, n0, z * split_kb};
   }
   __device__ void load(State& st, uint32_t seg, uint32_t kk, void* sa, void* sb,
                        uint64_t* bar) const {
@@ -64,7 +61,7 @@ struct GemmLoader {
     const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
     tma_load_2d(sa, am, bar, k * kTcBK, st.m0);
 #pragma unroll
-    for (int j = 0; j < kTcBN / 32; ++j)
+    for (int j = 0; j < kPBN / 32; ++j)
       tma_load_2d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, st.n0 + 32 * j, k * kTcBK);
   }
 };
@@ -74,10 +71,8 @@ struct GemmOut {
   uint64_t ldc;
   uint32_t M, N;
   bool accumulate;  // split-K: partial tiles are added into a zeroed C
-  __device__ __forceinline__ void store32(uint32_t m, uint32_t ntile, uint32_t col,
-                                          const float* v) const {
-    if (m >= M) return;
-    const uint32_t n0 = ntile * kTcBN + col;
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v) const {
+    if (m >= M || n0 >= N) return;
     float* row = c + m * ldc + n0;
     if (accumulate) {
 #pragma unroll
@@ -274,7 +269,7 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
   L.kb = static_cast<uint32_t>((k + kTcBK - 1) / kTcBK);
   L.segs = precision == LCNN_PREC_3XTF32 ? 3 : 1;
   // split-K when the output tiles cannot fill the 148 SMs (skinny fc layers)
-  const uint64_t tiles = ((n + kTcBN - 1) / kTcBN) * ((m + kTcBM - 1) / kTcBM);
+  const uint64_t tiles = ((n + kPBN - 1) / kPBN) * ((m + kTcBM - 1) / kTcBM);
   uint32_t splits = 1;
   if (tiles < 148) {
     splits = static_cast<uint32_t>((148 + tiles - 1) / tiles);
@@ -287,17 +282,18 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
     cudaError_t e = cudaMemsetAsync(c, 0, m * n * sizeof(float), s);
     if (e != cudaSuccess) return e;
   }
-  auto kern = tc_gemm_kernel<GemmLoader, GemmOut>;
+  auto kern = tc_gemm_persistent<GemmLoader, GemmOut>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kTcSmem));
+                                         static_cast<int>(kPSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const dim3 grid(static_cast<uint32_t>((n + kTcBN - 1) / kTcBN),
-                  static_cast<uint32_t>((m + kTcBM - 1) / kTcBM), splits);
-  kern<<<grid, kTcThreads, kTcSmem, s>>>(L, O);
+  const TileGrid tg{static_cast<uint32_t>((m + kTcBM - 1) / kTcBM),
+                    static_cast<uint32_t>((n + kPBN - 1) / kPBN), splits};
+  const uint32_t all = tg.mt * tg.nt * tg.splits;
+  kern<<<all < 148 ? all : 148, kTcThreads, kPSmem, s>>>(L, O, tg);
   return cudaGetLastError();
 }
 
