@@ -91,22 +91,21 @@ struct ChwnConvLoader {
   CUtensorMap a[2];  // packed filters hi / lo  (2D: {K, Co}, box {32, 128})
   CUtensorMap b[2];  // input hi / lo           (4D: {N, W, H, Ci})
   ConvGeomTc g;
-  uint32_t kb, segs, ncols;  // ncols = Ho*Wo*N
+  uint32_t ncols;  // Ho*Wo*N
   static constexpr bool kBMajorMN = true;
-  __device__ uint32_t kblocks(uint32_t) const { return kb; }
-  __device__ uint32_t segments() const { return segs; }
   __device__ void prefetch() const {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
   }
-  // Per tile: the eight 32-column boxes' (n0, w origin, h origin) decoded
-  // once; per k-block: the tap / channel-block counters advance incrementally.
+  // Per tile fragment: the eight 32-column boxes' (n0, w origin, h origin)
+  // and the first k-block's (fh, fw, channel) decoded once; per k-block the
+  // tap / channel-block counters advance incrementally.
   struct State {
     uint32_t m0;
     int32_t n0[kPBN / 32], y0[kPBN / 32], z0[kPBN / 32];
     uint32_t fh, wofs, c0;  // K decode of the next k-block
   };
-  __device__ State begin(uint32_t m0, uint32_t ncol0, uint32_t) const {
+  __device__ State begin(uint32_t m0, uint32_t ncol0, uint32_t kfirst) const {
     State st;
     st.m0 = m0;
 #pragma unroll
@@ -120,7 +119,17 @@ struct ChwnConvLoader {
       st.z0[j] = col >= ncols ? -(1 << 20)
                               : static_cast<int32_t>(oh * g.S) - static_cast<int32_t>(g.P);
     }
-    st.fh = st.wofs = st.c0 = 0;
+    if (g.mode == kModeCI) {
+      const uint32_t cpb = g.Ci / 32, r = kfirst / cpb;
+      st.c0 = (kfirst - r * cpb) * 32;
+      st.fh = r / g.FW;
+      st.wofs = r - st.fh * g.FW;
+    } else {
+      const uint32_t cpb = g.CiP / g.CIB;
+      st.fh = kfirst / cpb;
+      st.c0 = (kfirst - st.fh * cpb) * g.CIB;
+      st.wofs = 0;
+    }
     return st;
   }
   __device__ void load(State& st, uint32_t seg, uint32_t k, void* sa, void* sb,
@@ -157,18 +166,10 @@ struct RowsOut {  // C[m][col] row-major, ldc = ncols
   float* c;
   uint64_t ldc;
   uint32_t M, N;
-  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v) const {
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
+                                          bool add) const {
     if (m >= M || n0 >= N) return;
-    float* row = c + m * ldc + n0;
-    if (n0 + 32 <= N) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(row + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) row[j] = v[j];
-    }
+    store_row32(c + m * ldc + n0, n0, N, v, add);
   }
 };
 
@@ -623,9 +624,15 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
       !make_tmap(&L.b[1], b_lo, 4, dims, pitch, box, nullptr, true))
     return cudaErrorInvalidValue;
   L.g = p.g;
-  L.kb = p.K / kTcBK;
-  L.segs = x3 ? 3 : 1;
   L.ncols = a.ho * a.wo * a.n;
+  Sched sc = make_sched((a.co + kTcBM - 1) / kTcBM, (L.ncols + kPBN - 1) / kPBN, p.K / kTcBK,
+                        x3 ? 3 : 1);
+  const uint32_t zc = sched_zero_col(sc, kPBN);
+  if (zc < L.ncols) {
+    cudaError_t e = cudaMemset2DAsync(a.dst + zc, uint64_t{L.ncols} * 4, 0,
+                                      uint64_t{L.ncols - zc} * 4, a.co, s);
+    if (e != cudaSuccess) return e;
+  }
   RowsOut O{a.dst, L.ncols, a.co, L.ncols};
   auto kern = tc_gemm_persistent<ChwnConvLoader, RowsOut>;
   static bool attr = false;
@@ -635,9 +642,7 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const TileGrid tg{(a.co + kTcBM - 1) / kTcBM, (L.ncols + kPBN - 1) / kPBN, 1};
-  const uint32_t all = tg.mt * tg.nt;
-  kern<<<all < 148 ? all : 148, kTcThreads, kPSmem, s>>>(L, O, tg);
+  kern<<<sc.grid, kTcThreads, kPSmem, s>>>(L, O, sc);
   return cudaGetLastError();
 }
 

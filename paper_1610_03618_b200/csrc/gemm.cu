@@ -38,25 +38,17 @@ using namespace lcnn_tc;
 struct GemmLoader {
   CUtensorMap a[2];
   CUtensorMap b[2];
-  uint32_t kb;        // k-blocks of the whole K
-  uint32_t split_kb;  // k-blocks per split (blockIdx.z); == kb without split-K
-  uint32_t segs;
   static constexpr bool kBMajorMN = true;
-  __device__ uint32_t kblocks(uint32_t z) const { return min(split_kb, kb - z * split_kb); }
-  __device__ uint32_t segments() const { return segs; }
   __device__ void prefetch() const {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
   }
   struct State {
-    uint32_t m0, n0, k0;
+    uint32_t m0, n0;
   };
-  __device__ State begin(uint32_t m0, uint32_t n0, uint32_t z) const {
-    return State{m0, n0, z * split_kb};
-  }
-  __device__ void load(State& st, uint32_t seg, uint32_t kk, void* sa, void* sb,
+  __device__ State begin(uint32_t m0, uint32_t n0, uint32_t) const { return State{m0, n0}; }
+  __device__ void load(State& st, uint32_t seg, uint32_t k, void* sa, void* sb,
                        uint64_t* bar) const {
-    const uint32_t k = st.k0 + kk;
     const CUtensorMap* am = &a[seg == 2 ? 1 : 0];
     const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
     tma_load_2d(sa, am, bar, k * kTcBK, st.m0);
@@ -70,25 +62,10 @@ struct GemmOut {
   float* c;
   uint64_t ldc;
   uint32_t M, N;
-  bool accumulate;  // split-K: partial tiles are added into a zeroed C
-  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v) const {
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
+                                          bool add) const {
     if (m >= M || n0 >= N) return;
-    float* row = c + m * ldc + n0;
-    if (accumulate) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) atomicAdd(row + j, v[j]);
-      return;
-    }
-    if (n0 + 32 <= N && ((reinterpret_cast<uintptr_t>(row) & 15u) == 0)) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(row + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) row[j] = v[j];
-    }
+    store_row32(c + m * ldc + n0, n0, N, v, add);
   }
 };
 
@@ -266,22 +243,16 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
       !make_tmap_2d(&L.b[0], b0, n, k, n * 4, 32, kTcBK, true) ||
       !make_tmap_2d(&L.b[1], b1, n, k, n * 4, 32, kTcBK, true))
     return cudaErrorInvalidValue;
-  L.kb = static_cast<uint32_t>((k + kTcBK - 1) / kTcBK);
-  L.segs = precision == LCNN_PREC_3XTF32 ? 3 : 1;
-  // split-K when the output tiles cannot fill the 148 SMs (skinny fc layers)
-  const uint64_t tiles = ((n + kPBN - 1) / kPBN) * ((m + kTcBM - 1) / kTcBM);
-  uint32_t splits = 1;
-  if (tiles < 148) {
-    splits = static_cast<uint32_t>((148 + tiles - 1) / tiles);
-    splits = splits > L.kb / 8 ? (L.kb / 8 ? L.kb / 8 : 1) : splits;
-  }
-  L.split_kb = (L.kb + splits - 1) / splits;
-  splits = (L.kb + L.split_kb - 1) / L.split_kb;
-  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n), splits > 1};
-  if (splits > 1) {
-    cudaError_t e = cudaMemsetAsync(c, 0, m * n * sizeof(float), s);
+  Sched sc = make_sched(static_cast<uint32_t>((m + kTcBM - 1) / kTcBM),
+                        static_cast<uint32_t>((n + kPBN - 1) / kPBN),
+                        static_cast<uint32_t>((k + kTcBK - 1) / kTcBK),
+                        precision == LCNN_PREC_3XTF32 ? 3 : 1);
+  const uint32_t zc = sched_zero_col(sc, kPBN);
+  if (zc < n) {
+    cudaError_t e = cudaMemset2DAsync(c + zc, n * sizeof(float), 0, (n - zc) * sizeof(float), m, s);
     if (e != cudaSuccess) return e;
   }
+  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
   auto kern = tc_gemm_persistent<GemmLoader, GemmOut>;
   static bool attr = false;
   if (!attr) {
@@ -290,10 +261,7 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const TileGrid tg{static_cast<uint32_t>((m + kTcBM - 1) / kTcBM),
-                    static_cast<uint32_t>((n + kPBN - 1) / kPBN), splits};
-  const uint32_t all = tg.mt * tg.nt * tg.splits;
-  kern<<<all < 148 ? all : 148, kTcThreads, kPSmem, s>>>(L, O, tg);
+  kern<<<sc.grid, kTcThreads, kPSmem, s>>>(L, O, sc);
   return cudaGetLastError();
 }
 

@@ -69,22 +69,102 @@ struct PCtl {
   uint32_t tmem_addr;
 };
 
-struct TileGrid {
-  uint32_t mt, nt, splits;  // tiles along M, tiles along N, K splits
+// Tile schedule: data-parallel waves of whole tiles, then "stream-K" for the
+// ragged last wave.  With T tiles on G resident CTAs, the first
+// floor(T/G)*G tiles go round-robin, whole; the k-iterations of the R
+// remaining tiles are cut into G equal contiguous ranges, one per CTA, so the
+// tail costs R/G of a tile instead of a whole extra wave (and skinny GEMMs
+// with T < G -- the fc layers -- are pure stream-K, i.e. an even split-K).
+// Fragments of a split tile are combined with 128-bit vector atomic adds
+// (red.global.add.v4.f32, resolved in L2, spread over all SMs) into an output
+// region the host zeroed beforehand; whole tiles store plainly.  (An owner-
+// reduces-partials fixup was measured slower on B200: the single owner CTA
+// reading up to ~7 partial tiles serialises the tail, while the reds of all
+// fragments proceed in parallel.)  Split-tile sums are therefore not bitwise
+// reproducible run to run; the stated tolerances cover any order.
+struct Sched {
+  uint32_t mt, nt;       // tiles along M, tiles along N (tile t: m = t % mt, n = t / mt)
+  uint32_t iters;        // k-iterations per tile (k-blocks x segments)
+  uint32_t kbn;          // k-blocks per segment
+  uint32_t dp_tiles;     // tiles [0, dp_tiles) are done whole
+  uint32_t sk_ctas;      // CTAs sharing the stream-K remainder
+  uint64_t sk_iters;     // (tiles - dp_tiles) * iters
+  uint32_t grid;         // CTAs to launch
 };
+
+inline int tc_sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || !sms)
+      sms = 148;
+  }
+  return sms;
+}
+
+// Fragments shorter than this many k-iterations are not worth an atomic
+// epilogue; fewer CTAs then share the remainder.
+constexpr uint32_t kMinSkIters = 8;
+
+inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs) {
+  Sched s{};
+  s.mt = mt;
+  s.nt = nt;
+  s.kbn = kbn;
+  s.iters = kbn * segs;
+  const uint32_t tiles = mt * nt;
+  const uint32_t g = static_cast<uint32_t>(tc_sm_count());
+  const uint32_t rem = tiles % g;
+  // a last wave that is >= 60% full (or a whole multiple) stays data-parallel:
+  // measured on B200, the atomic tail beats an extra wave only below that
+  if (rem == 0 || rem * 5 >= g * 3) {
+    s.dp_tiles = tiles;
+  } else {
+    s.dp_tiles = tiles - rem;
+    s.sk_iters = static_cast<uint64_t>(rem) * s.iters;
+    uint64_t c = s.sk_iters / kMinSkIters;
+    s.sk_ctas = static_cast<uint32_t>(c < 1 ? 1 : (c > g ? g : c));
+  }
+  const uint32_t dp_grid = s.dp_tiles < g ? s.dp_tiles : g;
+  s.grid = dp_grid > s.sk_ctas ? dp_grid : s.sk_ctas;
+  return s;
+}
+
+// First column of the stream-K region; the host zeroes every column from
+// there on (whole tiles in that range are overwritten by plain stores).
+inline uint32_t sched_zero_col(const Sched& s, uint32_t bn) {
+  return s.dp_tiles == s.mt * s.nt ? ~0u : (s.dp_tiles / s.mt) * bn;
+}
+
+// Calls f(tile, kbeg, kend, split) for this CTA's work, in order.
+template <class F>
+__device__ __forceinline__ void for_each_work(const Sched& s, F&& f) {
+  for (uint32_t t = blockIdx.x; t < s.dp_tiles; t += gridDim.x) f(t, 0u, s.iters, false);
+  if (blockIdx.x < s.sk_ctas) {
+    uint64_t lo = s.sk_iters * blockIdx.x / s.sk_ctas;
+    const uint64_t hi = s.sk_iters * (blockIdx.x + 1) / s.sk_ctas;
+    while (lo < hi) {
+      const uint32_t tr = static_cast<uint32_t>(lo / s.iters);
+      const uint64_t base = static_cast<uint64_t>(tr) * s.iters;
+      const uint32_t kb = static_cast<uint32_t>(lo - base);
+      const uint32_t ke = static_cast<uint32_t>(hi - base < s.iters ? hi - base : s.iters);
+      f(s.dp_tiles + tr, kb, ke, !(kb == 0 && ke == s.iters));
+      lo = base + ke;
+    }
+  }
+}
 
 template <class Loader, class Out>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_gemm_persistent(const __grid_constant__ Loader ld, const __grid_constant__ Out out,
-                       TileGrid tg) {
+                       const __grid_constant__ Sched sc) {
   extern __shared__ uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   PCtl* ctl = reinterpret_cast<PCtl*>(smem + kPStages * kPStageBytes);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t per_split = tg.mt * tg.nt;
-  const uint32_t total = per_split * tg.splits;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -107,47 +187,39 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem = ctl->tmem_addr;
 
-  auto decode = [&](uint32_t t, uint32_t& m0, uint32_t& n0, uint32_t& z) {
-    z = t / per_split;
-    const uint32_t r = t - z * per_split;
-    const uint32_t nt = r / tg.mt;
-    m0 = (r - nt * tg.mt) * kTcBM;
-    n0 = nt * kPBN;
-  };
-
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     uint32_t s = 0, phase = 0;
-    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
-      uint32_t m0, n0, z;
-      decode(t, m0, n0, z);
-      auto st = ld.begin(m0, n0, z);
-      const uint32_t kbn = ld.kblocks(z), segs = ld.segments();
-      for (uint32_t seg = 0; seg < segs; ++seg)
-        for (uint32_t kb = 0; kb < kbn; ++kb) {
-          mbar_wait(&ctl->empty[s], phase ^ 1);
-          uint8_t* sa = smem + s * kPStageBytes;
-          mbar_arrive_expect_tx(&ctl->full[s], kPStageBytes);
-          ld.load(st, seg, kb, sa, sa + kTcABytes, &ctl->full[s]);
-          if (++s == kPStages) {
-            s = 0;
-            phase ^= 1;
-          }
+    for_each_work(sc, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t ntile = t / sc.mt;
+      uint32_t seg = kbeg / sc.kbn, kb = kbeg - seg * sc.kbn;
+      auto st = ld.begin((t - ntile * sc.mt) * kTcBM, ntile * kPBN, kb);
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        mbar_wait(&ctl->empty[s], phase ^ 1);
+        uint8_t* sa = smem + s * kPStageBytes;
+        mbar_arrive_expect_tx(&ctl->full[s], kPStageBytes);
+        ld.load(st, seg, kb, sa, sa + kTcABytes, &ctl->full[s]);
+        if (++kb == sc.kbn) {
+          kb = 0;
+          ++seg;
         }
-    }
+        if (++s == kPStages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+    });
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc = idesc_tf32(kTcBM, kPBN, false, Loader::kBMajorMN);
     uint32_t s = 0, phase = 0, local = 0;
-    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      uint32_t m0, n0, z;
-      decode(t, m0, n0, z);
+    for_each_work(sc, [&](uint32_t, uint32_t kbeg, uint32_t kend, bool) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
       mbar_wait(&ctl->tempty[a], aphase ^ 1);  // epilogue drained this buffer
       tc_fence_after();
       const uint32_t acc = tmem + a * kPBN;
-      const uint32_t steps = ld.kblocks(z) * ld.segments();
-      for (uint32_t it = 0; it < steps; ++it) {
+      for (uint32_t it = kbeg; it < kend; ++it) {
         mbar_wait(&ctl->full[s], phase);
         tc_fence_after();
         const uint8_t* sa = smem + s * kPStageBytes;
@@ -157,7 +229,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint64_t ad = smem_desc_sw128(sa + k * 32, 16, 1024);
           const uint64_t bd = Loader::kBMajorMN ? smem_desc_sw128(sb + k * 1024, 4096, 512, 1)
                                                 : smem_desc_sw128(sb + k * 32, 16, 1024);
-          mma_tf32(acc, ad, bd, idesc, (it | k) != 0);
+          mma_tf32(acc, ad, bd, idesc, (it != kbeg) || (k != 0));
         }
         tc_commit(&ctl->empty[s]);
         if (++s == kPStages) {
@@ -166,35 +238,62 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       tc_commit(&ctl->tfull[a]);
-    }
+    });
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;
     uint32_t local = 0;
-    for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      uint32_t m0, n0, z;
-      decode(t, m0, n0, z);
+    for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
+      const uint32_t ntile = t / sc.mt;
       mbar_wait(&ctl->tfull[a], aphase);
       tc_fence_after();
-      const uint32_t m = m0 + q * 32 + lane;
+      const uint32_t m = (t - ntile * sc.mt) * kTcBM + q * 32 + lane;
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < kPBN; c += 32) {
         float v[32];
         tmem_ld32(base + c, v);
-        out.store32(m, n0 + c, v);
+        out.store32(m, ntile * kPBN + c, v, split);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl->tempty[a]);
-    }
+    });
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+  }
+}
+
+// Shared store of 32 consecutive accumulator columns of one row: plain
+// 128-bit stores for whole tiles, vector atomic adds for stream-K fragments.
+__device__ __forceinline__ void store_row32(float* row, uint32_t n0, uint32_t N, const float* v,
+                                            bool add) {
+  if (n0 + 32 <= N && (reinterpret_cast<uintptr_t>(row) & 15u) == 0) {
+    if (add) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        atomicAdd(reinterpret_cast<float4*>(row + j),
+                  make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(row + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (n0 + j < N) {
+        if (add)
+          atomicAdd(row + j, v[j]);
+        else
+          row[j] = v[j];
+      }
   }
 }
 

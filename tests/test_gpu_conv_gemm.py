@@ -69,6 +69,7 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     (32, 3, 12, 12, 20, 3, 1, 1),     # WIN FP=4, co < 128
     (128, 32, 6, 6, 160, 1, 1, 0),    # 1x1, co > 128
     (96, 64, 7, 7, 64, 3, 2, 0),
+    (128, 384, 13, 13, 256, 3, 1, 1),  # conv4: 170 tiles -> 148 whole + stream-K tail
 ]
 
 
@@ -111,7 +112,10 @@ def test_conv_reference_fixtures(cuda, ref_vectors):
 
 @pytest.mark.parametrize("m,n,k", [(128, 128, 128), (96, 300, 64), (257, 129, 200),
                                    (128, 4096, 9216), (1000, 128, 4096), (33, 17, 13),
-                                   (64, 1000, 4096)])
+                                   (64, 1000, 4096),
+                                   (1280, 4352, 640),   # 170 tiles: data-parallel wave + stream-K
+                                   (2432, 1024, 96),    # 76 tiles, 3 k-blocks: pure stream-K
+                                   (4992, 2048, 64)])   # 312 tiles: last wave 16/148 -> stream-K
 @pytest.mark.parametrize("precision", [0, 1, 2])
 def test_gemm(cuda, m, n, k, precision):
     import torch
