@@ -7,9 +7,10 @@
 //   conv_oracle       :53-93    fp64 ground truth
 //
 // B200 design -- CHWN implicit GEMM on tcgen05 (no im2col in HBM):
-//   D[co][(oh, ow, n)] = sum_k Wpack[co][k] * X[k][(oh, ow, n)]
-// The GEMM N index (oh, ow, n) is exactly the CHWN output order, so the
-// accumulator tile stores straight into the output.  B tiles are TMA boxes of
+//   D[(oh, ow, n)][co] = sum_k X[(oh, ow, n)][k] * Wpack[co][k]
+// The GEMM M index (oh, ow, n) is exactly the CHWN output column order and the
+// output channels are the N side (UMMA N = C_o up to 256, so 96 / 192
+// channel layers waste nothing on a 128-row tile).  A tiles are TMA boxes of
 // the 4D input (n, w, h, c) -- the batch is contiguous, so every k-row of a
 // tile is 32 images (128 B) of one input pixel: an MN-major operand in the
 // SWIZZLE_128B_BASE32B layout tf32 requires.
@@ -87,30 +88,39 @@ __global__ void pack_filters_kernel(const float* __restrict__ f, float* __restri
   }
 }
 
+// The implicit im2col of the CHWN input is the MN-major operand: 4D TMA boxes
+// of 32 output columns (32 images of one output pixel) x 32 k-rows.  The
+// packed filters [co][K] are the K-major operand: one 2D box of 32 k x (tile
+// width) output channels.  kCoOnN picks the orientation:
+//   true : A = input (4 boxes = 128 columns), B = filters (N = bn channels)
+//   false: A = filters (128 channels),        B = input (8 boxes = 256 columns)
+template <bool kCoOnN>
 struct ChwnConvLoader {
-  CUtensorMap a[2];  // packed filters hi / lo  (2D: {K, Co}, box {32, 128})
-  CUtensorMap b[2];  // input hi / lo           (4D: {N, W, H, Ci})
+  CUtensorMap x[2];  // input hi / lo          (4D: {N, W, H, Ci})
+  CUtensorMap w[2];  // packed filters hi / lo (2D: {K, Co})
   ConvGeomTc g;
   uint32_t ncols;  // Ho*Wo*N
-  static constexpr bool kBMajorMN = true;
+  static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN;
+  static constexpr int kBoxes = kCoOnN ? kTcBM / 32 : kPBN / 32;
   __device__ void prefetch() const {
-    tma_prefetch(&a[0]);
-    tma_prefetch(&b[0]);
+    tma_prefetch(&x[0]);
+    tma_prefetch(&w[0]);
   }
-  // Per tile fragment: the eight 32-column boxes' (n0, w origin, h origin)
-  // and the first k-block's (fh, fw, channel) decoded once; per k-block the
-  // tap / channel-block counters advance incrementally.
+  // Per tile fragment: the column boxes' (n0, w origin, h origin) and the
+  // first k-block's (fh, fw, channel) decoded once; per k-block the tap /
+  // channel-block counters advance incrementally.
   struct State {
-    uint32_t m0;
-    int32_t n0[kPBN / 32], y0[kPBN / 32], z0[kPBN / 32];
+    uint32_t co0;
+    int32_t n0[kBoxes], y0[kBoxes], z0[kBoxes];
     uint32_t fh, wofs, c0;  // K decode of the next k-block
   };
-  __device__ State begin(uint32_t m0, uint32_t ncol0, uint32_t kfirst) const {
+  __device__ State begin(uint32_t m0, uint32_t n0, uint32_t kfirst) const {
     State st;
-    st.m0 = m0;
+    const uint32_t col0 = kCoOnN ? m0 : n0;
+    st.co0 = kCoOnN ? n0 : m0;
 #pragma unroll
-    for (int j = 0; j < kPBN / 32; ++j) {
-      const uint32_t col = ncol0 + 32 * j;
+    for (int j = 0; j < kBoxes; ++j) {
+      const uint32_t col = col0 + 32 * j;
       const uint32_t pos = col / g.N;
       const uint32_t oh = pos / g.Wo, ow = pos - oh * g.Wo;
       st.n0[j] = static_cast<int32_t>(col - pos * g.N);
@@ -135,13 +145,13 @@ struct ChwnConvLoader {
   __device__ void load(State& st, uint32_t seg, uint32_t k, void* sa, void* sb,
                        uint64_t* bar) const {
     if (k == 0) st.fh = st.wofs = st.c0 = 0;  // a new segment restarts K
-    tma_load_2d(sa, &a[seg == 2 ? 1 : 0], bar, k * kTcBK, st.m0);
-    const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
+    uint8_t* sx = static_cast<uint8_t*>(kCoOnN ? sa : sb);
+    const CUtensorMap* xm = &x[seg == 1 ? 1 : 0];
 #pragma unroll
-    for (int j = 0; j < kPBN / 32; ++j)
-      tma_load_4d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, st.n0[j],
-                  st.y0[j] + static_cast<int32_t>(st.wofs), st.z0[j] + static_cast<int32_t>(st.fh),
-                  static_cast<int32_t>(st.c0));
+    for (int j = 0; j < kBoxes; ++j)
+      tma_load_4d(sx + j * 4096, xm, bar, st.n0[j], st.y0[j] + static_cast<int32_t>(st.wofs),
+                  st.z0[j] + static_cast<int32_t>(st.fh), static_cast<int32_t>(st.c0));
+    tma_load_2d(kCoOnN ? sb : sa, &w[seg == 2 ? 1 : 0], bar, k * kTcBK, st.co0);
     // advance: CI mode k = (fh, fw, ci/32); WIN mode k = (fh, ci/CIB)
     if (g.mode == kModeCI) {
       st.c0 += 32;
@@ -162,7 +172,7 @@ struct ChwnConvLoader {
   }
 };
 
-struct RowsOut {  // C[m][col] row-major, ldc = ncols
+struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols
   float* c;
   uint64_t ldc;
   uint32_t M, N;
@@ -170,6 +180,27 @@ struct RowsOut {  // C[m][col] row-major, ldc = ncols
                                           bool add) const {
     if (m >= M || n0 >= N) return;
     store_row32(c + m * ldc + n0, n0, N, v, add);
+  }
+};
+
+// Accumulator row m = output column (oh, ow, n), columns = output channels:
+// out[co][col] (CHWN).  For each channel the 32 lanes of a warp hold 32
+// consecutive columns, so every store instruction is one coalesced 128 B line.
+struct ColsOut {
+  float* c;
+  uint32_t ncols, co;
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
+                                          bool add) const {
+    if (m >= ncols) return;
+    float* p = c + static_cast<uint64_t>(n0) * ncols + m;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (n0 + j >= co) break;
+      if (add)
+        atomicAdd(p + static_cast<uint64_t>(j) * ncols, v[j]);
+      else
+        __stcs(p + static_cast<uint64_t>(j) * ncols, v[j]);
+    }
   }
 };
 
@@ -556,6 +587,88 @@ TcPlan plan_tc(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, int layout, uint
 
 }  // namespace
 
+struct ConvTcArgs {
+  const ConvArgs& a;
+  const TcPlan& p;
+  const float *w_hi, *w_lo, *x_hi, *x_lo;
+};
+
+// Output-channel tile width when channels are the N side: one or two tiles of
+// <= 256, rounded to 32 (no padding of C_o = 96 / 192 to a 128-row tile).
+uint32_t co_tile_n(uint32_t co) {
+  const uint32_t nco = (co + kPBN - 1) / kPBN;
+  return ((co + nco - 1) / nco + 31) / 32 * 32;
+}
+
+// Orientation: the tcgen05 tiles here are bound by operand traffic (L2 ->
+// shared memory), so pick the one with more useful flops per operand byte.
+//   channels on M: 128 x 256 tile, operands (128 + 256) rows, useful co / 128-padded
+//   channels on N: 128 x bn tile,  operands (128 + bn) rows,  useful co / bn-padded
+bool choose_co_on_n(uint32_t co) {
+  const double mt = (co + kTcBM - 1) / kTcBM * double(kTcBM);
+  const double on_m = co / mt * (kTcBM * double(kPBN)) / (kTcBM + kPBN);
+  const uint32_t bn = co_tile_n(co);
+  const double nt = (co + bn - 1) / bn * double(bn);
+  const double on_n = co / nt * (kTcBM * double(bn)) / (kTcBM + bn);
+  return on_n > on_m * 1.02;
+}
+
+template <bool kCoOnN>
+cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
+  const ConvArgs& a = t.a;
+  const TcPlan& p = t.p;
+  const bool x3 = a.precision == LCNN_PREC_3XTF32;
+  const uint32_t bw = kCoOnN ? co_tile_n(a.co) : kTcBM;  // filter box rows
+  ChwnConvLoader<kCoOnN> L;
+  const uint64_t K = p.K;
+  if (!make_tmap_2d(&L.w[0], t.w_hi, K, a.co, K * 4, kTcBK, bw, false) ||
+      !make_tmap_2d(&L.w[1], t.w_lo, K, a.co, K * 4, kTcBK, bw, false))
+    return cudaErrorInvalidValue;
+  const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
+  const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
+                             static_cast<uint64_t>(a.h) * a.w * a.n * 4};
+  uint32_t box[4];
+  if (p.g.mode == kModeCI) {
+    box[0] = 32; box[1] = 1; box[2] = 1; box[3] = 32;
+  } else {
+    box[0] = 32; box[1] = p.g.FP; box[2] = 1; box[3] = p.g.CIB;
+  }
+  if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, true) ||
+      !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, true))
+    return cudaErrorInvalidValue;
+  L.g = p.g;
+  L.ncols = a.ho * a.wo * a.n;
+  const uint32_t segs = x3 ? 3 : 1;
+  const Sched sc =
+      kCoOnN ? make_sched((L.ncols + kTcBM - 1) / kTcBM, (a.co + bw - 1) / bw, p.K / kTcBK, segs,
+                          bw, true, false)
+             : make_sched((a.co + kTcBM - 1) / kTcBM, (L.ncols + kPBN - 1) / kPBN, p.K / kTcBK,
+                          segs, kPBN, false, true);
+  if (sc.dp_tiles < sc.mt * sc.nt) {
+    // zero the stream-K region (whole tiles inside it are overwritten anyway)
+    const uint32_t nt0 = sc.dp_tiles / sc.mt;
+    uint32_t row0, col0;  // in out[co][col]
+    if (kCoOnN) {
+      row0 = nt0 * bw;
+      col0 = nt0 == sc.nt - 1 ? (sc.dp_tiles % sc.mt) * kTcBM : 0;
+    } else {
+      row0 = 0;
+      col0 = nt0 * kPBN;
+    }
+    cudaError_t e = cudaMemset2DAsync(a.dst + uint64_t{row0} * L.ncols + col0,
+                                      uint64_t{L.ncols} * 4, 0, uint64_t{L.ncols - col0} * 4,
+                                      a.co - row0, s);
+    if (e != cudaSuccess) return e;
+  }
+  if constexpr (kCoOnN) {
+    ColsOut O{a.dst, L.ncols, a.co};
+    return launch_persistent(L, O, sc, s);
+  } else {
+    RowsOut O{a.dst, L.ncols, a.co, L.ncols};
+    return launch_persistent(L, O, sc, s);
+  }
+}
+
 size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, uint32_t co,
                             uint32_t fh, uint32_t fw, int precision) {
   // packed filters for the widest packing (WIN with FP=16, CiP rounded to 2)
@@ -606,44 +719,8 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
     b_lo = bl;
   }
   pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, p.K);
-  ChwnConvLoader L;
-  const uint64_t K = p.K;
-  if (!make_tmap_2d(&L.a[0], a_hi, K, a.co, K * 4, kTcBK, kTcBM, false) ||
-      !make_tmap_2d(&L.a[1], x3 ? a_lo : a_hi, K, a.co, K * 4, kTcBK, kTcBM, false))
-    return cudaErrorInvalidValue;
-  const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
-  const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
-                             static_cast<uint64_t>(a.h) * a.w * a.n * 4};
-  uint32_t box[4];
-  if (p.g.mode == kModeCI) {
-    box[0] = 32; box[1] = 1; box[2] = 1; box[3] = 32;
-  } else {
-    box[0] = 32; box[1] = p.g.FP; box[2] = 1; box[3] = p.g.CIB;
-  }
-  if (!make_tmap(&L.b[0], b_hi, 4, dims, pitch, box, nullptr, true) ||
-      !make_tmap(&L.b[1], b_lo, 4, dims, pitch, box, nullptr, true))
-    return cudaErrorInvalidValue;
-  L.g = p.g;
-  L.ncols = a.ho * a.wo * a.n;
-  Sched sc = make_sched((a.co + kTcBM - 1) / kTcBM, (L.ncols + kPBN - 1) / kPBN, p.K / kTcBK,
-                        x3 ? 3 : 1);
-  const uint32_t zc = sched_zero_col(sc, kPBN);
-  if (zc < L.ncols) {
-    cudaError_t e = cudaMemset2DAsync(a.dst + zc, uint64_t{L.ncols} * 4, 0,
-                                      uint64_t{L.ncols - zc} * 4, a.co, s);
-    if (e != cudaSuccess) return e;
-  }
-  RowsOut O{a.dst, L.ncols, a.co, L.ncols};
-  auto kern = tc_gemm_persistent<ChwnConvLoader, RowsOut>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kPSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  kern<<<sc.grid, kTcThreads, kPSmem, s>>>(L, O, sc);
-  return cudaGetLastError();
+  ConvTcArgs t{a, p, a_hi, x3 ? a_lo : a_hi, b_hi, b_lo};
+  return choose_co_on_n(a.co) ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
 }
 
 }  // namespace lcnn_impl

@@ -38,7 +38,7 @@ using namespace lcnn_tc;
 struct GemmLoader {
   CUtensorMap a[2];
   CUtensorMap b[2];
-  static constexpr bool kBMajorMN = true;
+  static constexpr bool kAMajorMN = false, kBMajorMN = true;
   __device__ void prefetch() const {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
@@ -246,23 +246,14 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
   Sched sc = make_sched(static_cast<uint32_t>((m + kTcBM - 1) / kTcBM),
                         static_cast<uint32_t>((n + kPBN - 1) / kPBN),
                         static_cast<uint32_t>((k + kTcBK - 1) / kTcBK),
-                        precision == LCNN_PREC_3XTF32 ? 3 : 1);
+                        precision == LCNN_PREC_3XTF32 ? 3 : 1, kPBN, false, true);
   const uint32_t zc = sched_zero_col(sc, kPBN);
   if (zc < n) {
     cudaError_t e = cudaMemset2DAsync(c + zc, n * sizeof(float), 0, (n - zc) * sizeof(float), m, s);
     if (e != cudaSuccess) return e;
   }
   GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
-  auto kern = tc_gemm_persistent<GemmLoader, GemmOut>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kPSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  kern<<<sc.grid, kTcThreads, kPSmem, s>>>(L, O, sc);
-  return cudaGetLastError();
+  return launch_persistent(L, O, sc, s);
 }
 
 cudaError_t launch_gemm_fp32(const float* a, const float* b, float* c, uint64_t m, uint64_t n,

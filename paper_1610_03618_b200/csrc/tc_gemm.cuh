@@ -44,18 +44,18 @@ struct TcCtl {
 // the TMA warp streams operands through a kPStages-deep shared-memory ring
 // without ever stopping between tiles.
 //
-// Loader concept (the producer thread calls begin() once per tile, then
-// load() for k-blocks 0..kblocks(z)-1 of each segment in order, so loaders can
-// decode K incrementally instead of dividing per stage):
-//   uint32_t kblocks(uint32_t z) const;      // k-blocks of BK in split z
-//   uint32_t segments() const;               // chained operand sets (1 or 3)
+// Loader concept (the producer thread calls begin() once per tile fragment,
+// then load() for consecutive (segment, k-block) pairs, so loaders decode K
+// incrementally instead of dividing per stage):
 //   void prefetch() const;                   // tensor-map prefetch
-//   State begin(uint32_t m0, uint32_t n0, uint32_t z) const;
+//   State begin(uint32_t m0, uint32_t n0, uint32_t kfirst) const;
 //   void load(State& st, uint32_t seg, uint32_t kb, void* sa, void* sb,
-//             uint64_t* bar) const;         // issues TMA, total kPStageBytes
-//   static constexpr bool kBMajorMN;         // B operand major-ness
+//             uint64_t* bar) const;         // issues TMA, Sched::stage_bytes
+//   static constexpr bool kAMajorMN, kBMajorMN;  // operand major-ness
+// Segments chain operand sets into one accumulator (3 for 3xTF32).
 // Out concept:
-//   void store32(uint32_t m, uint32_t n0, const float* v) const;  // 32 columns
+//   void store32(uint32_t m, uint32_t n0, const float* v, bool add) const;
+//       // row m, columns n0..n0+31; add = stream-K fragment (atomic add)
 constexpr int kPBN = 256, kPStages = 4;
 constexpr uint32_t kPBBytes = kTcBK * kPBN * 4;            // 32 KB
 constexpr uint32_t kPStageBytes = kTcABytes + kPBBytes;    // 48 KB
@@ -90,6 +90,9 @@ struct Sched {
   uint32_t sk_ctas;      // CTAs sharing the stream-K remainder
   uint64_t sk_iters;     // (tiles - dp_tiles) * iters
   uint32_t grid;         // CTAs to launch
+  uint32_t bn;           // N columns of a tile (multiple of 32, <= kPBN)
+  uint32_t idesc;        // tcgen05 instruction descriptor (M = 128, N = bn)
+  uint32_t stage_bytes;  // TMA bytes per pipeline stage
 };
 
 inline int tc_sm_count() {
@@ -107,10 +110,14 @@ inline int tc_sm_count() {
 // epilogue; fewer CTAs then share the remainder.
 constexpr uint32_t kMinSkIters = 8;
 
-inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs) {
+inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, uint32_t bn,
+                        bool a_mn, bool b_mn) {
   Sched s{};
   s.mt = mt;
   s.nt = nt;
+  s.bn = bn;
+  s.idesc = idesc_tf32(kTcBM, bn, a_mn, b_mn);
+  s.stage_bytes = kTcABytes + bn * kTcBK * 4;
   s.kbn = kbn;
   s.iters = kbn * segs;
   const uint32_t tiles = mt * nt;
@@ -193,11 +200,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     for_each_work(sc, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
       const uint32_t ntile = t / sc.mt;
       uint32_t seg = kbeg / sc.kbn, kb = kbeg - seg * sc.kbn;
-      auto st = ld.begin((t - ntile * sc.mt) * kTcBM, ntile * kPBN, kb);
+      auto st = ld.begin((t - ntile * sc.mt) * kTcBM, ntile * sc.bn, kb);
       for (uint32_t it = kbeg; it < kend; ++it) {
         mbar_wait(&ctl->empty[s], phase ^ 1);
         uint8_t* sa = smem + s * kPStageBytes;
-        mbar_arrive_expect_tx(&ctl->full[s], kPStageBytes);
+        mbar_arrive_expect_tx(&ctl->full[s], sc.stage_bytes);
         ld.load(st, seg, kb, sa, sa + kTcABytes, &ctl->full[s]);
         if (++kb == sc.kbn) {
           kb = 0;
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     });
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_tf32(kTcBM, kPBN, false, Loader::kBMajorMN);
+    const uint32_t idesc = sc.idesc;
     uint32_t s = 0, phase = 0, local = 0;
     for_each_work(sc, [&](uint32_t, uint32_t kbeg, uint32_t kend, bool) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
@@ -226,7 +233,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint8_t* sb = sa + kTcABytes;
 #pragma unroll
         for (int k = 0; k < kTcBK / 8; ++k) {
-          const uint64_t ad = smem_desc_sw128(sa + k * 32, 16, 1024);
+          const uint64_t ad = Loader::kAMajorMN ? smem_desc_sw128(sa + k * 1024, 4096, 512, 1)
+                                                : smem_desc_sw128(sa + k * 32, 16, 1024);
           const uint64_t bd = Loader::kBMajorMN ? smem_desc_sw128(sb + k * 1024, 4096, 512, 1)
                                                 : smem_desc_sw128(sb + k * 32, 16, 1024);
           mma_tf32(acc, ad, bd, idesc, (it != kbeg) || (k != 0));
@@ -252,10 +260,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t m = (t - ntile * sc.mt) * kTcBM + q * 32 + lane;
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < kPBN; c += 32) {
+      for (uint32_t c = 0; c < sc.bn; c += 32) {
         float v[32];
         tmem_ld32(base + c, v);
-        out.store32(m, ntile * kPBN + c, v, split);
+        out.store32(m, ntile * sc.bn + c, v, split);
       }
       tc_fence_before();
       __syncwarp();
@@ -295,6 +303,22 @@ __device__ __forceinline__ void store_row32(float* row, uint32_t n0, uint32_t N,
           row[j] = v[j];
       }
   }
+}
+
+// Host launch of the persistent kernel (one dynamic-smem opt-in per
+// Loader/Out instantiation).
+template <class Loader, class Out>
+cudaError_t launch_persistent(const Loader& ld, const Out& out, const Sched& sc, cudaStream_t s) {
+  auto kern = tc_gemm_persistent<Loader, Out>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kPSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<sc.grid, kTcThreads, kPSmem, s>>>(ld, out, sc);
+  return cudaGetLastError();
 }
 
 }  // namespace lcnn_tc
