@@ -30,6 +30,8 @@
 // 32, rectangular windows wider than 16).
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "../../include/lcnn_cuda.h"
 #include "common.cuh"
 #include "internal.h"
@@ -39,11 +41,12 @@ namespace lcnn_dev {
 
 using namespace lcnn_tc;
 
-enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2 };
+enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2, kModeROW = 3 };
 
 struct ConvGeomTc {
   uint32_t N, Ci, H, W, Co, FH, FW, S, P, Ho, Wo;
   uint32_t mode, FP, CIB, CiP;
+  uint32_t KR;  // ROW mode: k-rows per filter row (Ci*FW rounded up to 8)
 };
 
 // Wpack[co][k] in the loader's K order, zero for padded (ci, fw) slots.
@@ -61,6 +64,12 @@ __global__ void pack_filters_kernel(const float* __restrict__ f, float* __restri
       const uint32_t tap = k / g.Ci;
       fh = tap / g.FW;
       fw = tap % g.FW;
+    } else if (g.mode == kModeROW) {  // k = (fh, ci, fw), each fh row padded to KR
+      fh = k / g.KR;
+      const uint32_t r = k - fh * g.KR;
+      ci = r / g.FW;
+      fw = r - ci * g.FW;
+      valid = ci < g.Ci;
     } else if (g.mode == kModeNAT) {  // natural (ci, fh, fw) order, K padded
       fw = k % g.FW;
       fh = (k / g.FW) % g.FH;
@@ -100,8 +109,19 @@ struct ChwnConvLoader {
   CUtensorMap w[2];  // packed filters hi / lo (2D: {K, Co})
   ConvGeomTc g;
   uint32_t ncols;  // Ho*Wo*N
-  static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN;
+  static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN, kZeroSmem = false;
+  static constexpr int kSteps = kTcBK / 8;
   static constexpr int kBoxes = kCoOnN ? kTcBM / 32 : kPBN / 32;
+  // input image: SWIZZLE_128B_BASE32B, 32-column atoms of 32 k-rows (4 KB);
+  // filters: K-major SWIZZLE_128B, 8-row groups of 1 KB
+  __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
+    return kCoOnN ? smem_desc_sw128(sa + k * 1024, 4096, 512, 1)
+                  : smem_desc_sw128(sa + k * 32, 16, 1024);
+  }
+  __device__ uint64_t desc_b(const uint8_t* sb, int k) const {
+    return kCoOnN ? smem_desc_sw128(sb + k * 32, 16, 1024)
+                  : smem_desc_sw128(sb + k * 1024, 4096, 512, 1);
+  }
   __device__ void prefetch() const {
     tma_prefetch(&x[0]);
     tma_prefetch(&w[0]);
@@ -171,6 +191,95 @@ struct ChwnConvLoader {
     }
   }
 };
+
+// ROW mode (small C_i * F_w, e.g. AlexNet conv1: 3 x 11): a pipeline stage
+// is one whole filter row, k = (ci, fw) in the order a single box
+// {32 n, F_w w, 1 h, C_i c} lays rows down, padded only to the MMA K-step of
+// 8 (33 -> 40 rows instead of WIN's 3 -> 4 channels x 11 -> 16 taps = 64).
+// Channels are the N side.  The filters are pre-packed in global memory as
+// the exact shared-memory image of the B operand per (channel tile, filter
+// row) -- the SWIZZLE_NONE K-major core-matrix layout, [k/4][bn][4] -- so a
+// stage's B is ONE contiguous bulk copy of bn * KR * 4 bytes.  The padding
+// rows of the input boxes are never written by TMA; the kernel zeroes shared
+// memory once at start (kZeroSmem) and the padded weights are zero.
+struct ChwnRowLoader {
+  CUtensorMap x[2];         // input hi / lo (4D: {N, W, H, Ci}, box {32, FW, 1, Ci})
+  const float* wimg[2];     // filter images hi / lo: [co tile][fh][KR/4][bn][4]
+  ConvGeomTc g;
+  uint32_t ncols, bn;
+  static constexpr bool kAMajorMN = true, kBMajorMN = false, kZeroSmem = true;
+  static constexpr int kSteps = 0;
+  __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
+    return smem_desc_sw128(sa + k * 1024, g.KR * 128, 512, 1);
+  }
+  __device__ uint64_t desc_b(const uint8_t* sb, int k) const {
+    // K-step k = k-chunks 2k, 2k+1; LBO = next k-chunk, SBO = next 8 rows
+    return smem_desc_sw128(sb + 2 * k * bn * 16, bn * 16, 128, 0);
+  }
+  __device__ void prefetch() const { tma_prefetch(&x[0]); }
+  struct State {
+    uint32_t wofs, fh;  // filter image offset of this channel tile (floats), filter row
+    int32_t n0[kTcBM / 32], y0[kTcBM / 32], z0[kTcBM / 32];
+  };
+  __device__ State begin(uint32_t col0, uint32_t co0, uint32_t kfirst) const {
+    State st;
+    st.wofs = co0 / bn * g.FH * g.KR * bn;
+    st.fh = kfirst;
+#pragma unroll
+    for (int j = 0; j < kTcBM / 32; ++j) {
+      const uint32_t col = col0 + 32 * j;
+      const uint32_t pos = col / g.N;
+      const uint32_t oh = pos / g.Wo, ow = pos - oh * g.Wo;
+      st.n0[j] = static_cast<int32_t>(col - pos * g.N);
+      st.y0[j] = static_cast<int32_t>(ow * g.S) - static_cast<int32_t>(g.P);
+      st.z0[j] = col >= ncols ? -(1 << 20)
+                              : static_cast<int32_t>(oh * g.S) - static_cast<int32_t>(g.P);
+    }
+    return st;
+  }
+  __device__ void load(State& st, uint32_t seg, uint32_t k, void* sa, void* sb,
+                       uint64_t* bar) const {
+    if (k == 0) st.fh = 0;
+    const CUtensorMap* xm = &x[seg == 1 ? 1 : 0];
+#pragma unroll
+    for (int j = 0; j < kTcBM / 32; ++j)
+      tma_load_4d(static_cast<uint8_t*>(sa) + j * g.KR * 128, xm, bar, st.n0[j], st.y0[j],
+                  st.z0[j] + static_cast<int32_t>(st.fh), 0);
+    bulk_load(sb, wimg[seg == 2 ? 1 : 0] + st.wofs + st.fh * g.KR * bn, g.KR * bn * 4, bar);
+    ++st.fh;
+  }
+};
+
+// Filter image of ROW mode: img[((t * FH + fh) * KR/4 + q) * bn + r][e] =
+// W[co = t*bn + r][ci][fh][fw] with ci*FW + fw = 4q + e (zero when padded).
+__global__ void pack_filters_row_kernel(const float* __restrict__ f, float* __restrict__ hi,
+                                        float* __restrict__ lo, ConvGeomTc g, uint32_t bn,
+                                        uint64_t total) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = static_cast<uint32_t>(i & 3);
+    uint64_t rest = i >> 2;
+    const uint32_t r = static_cast<uint32_t>(rest % bn);
+    rest /= bn;
+    const uint32_t q = static_cast<uint32_t>(rest % (g.KR / 4));
+    rest /= g.KR / 4;
+    const uint32_t fh = static_cast<uint32_t>(rest % g.FH);
+    const uint32_t t = static_cast<uint32_t>(rest / g.FH);
+    const uint32_t kk = 4 * q + e, ci = kk / g.FW, fw = kk - ci * g.FW, co = t * bn + r;
+    float v = 0.0f;
+    if (co < g.Co && ci < g.Ci) v = f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw];
+    if (lo) {
+      uint32_t u;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
+      const float h = __uint_as_float(u);
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v - h));
+      hi[i] = h;
+      lo[i] = __uint_as_float(u);
+    } else {
+      hi[i] = v;
+    }
+  }
+}
 
 struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols
   float* c;
@@ -508,13 +617,24 @@ using namespace lcnn_dev;
 
 bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer,
                   uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer, bool mn_major);
+// swizzle: 0 = SWIZZLE_128B, 1 = SWIZZLE_128B_ATOM_32B, 2 = none
 bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t* dims,
                const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides,
-               bool mn_major);
+               int swizzle);
 cudaError_t launch_split_hilo(const float* x, float* hi, float* lo, uint64_t count,
                               cudaStream_t s);
 
 namespace {
+
+// Output-channel tile width when channels are the N side: one or two tiles of
+// <= 256, rounded to 32 (no padding of C_o = 96 / 192 to a 128-row tile).
+uint32_t co_tile_n(uint32_t co) {
+  const uint32_t nco = (co + kPBN - 1) / kPBN;
+  return ((co + nco - 1) / nco + 31) / 32 * 32;
+}
+
+// channel rows of a ROW-mode filter image (tiles of co_tile_n)
+uint32_t pack_rows(uint32_t co) { return (co + co_tile_n(co) - 1) / co_tile_n(co) * co_tile_n(co); }
 
 struct TcPlan {
   bool ok = false;
@@ -569,13 +689,22 @@ TcPlan plan_tc(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, int layout, uint
   g = ConvGeomTc{n, ci, h, w, co, fh, fw, stride, pad, ho, wo, 0, 0, 0, 0};
   const uint64_t ncols = static_cast<uint64_t>(ho) * wo * n;
   if (ncols >= (1ull << 31) || static_cast<uint64_t>(h) * w * n * ci >= (1ull << 32)) return p;
+  // padded K of the two small-channel packings
+  const uint32_t kr = (ci * fw + 7) / 8 * 8;                   // ROW
+  const uint32_t fp = fw <= 4 ? 4 : (fw <= 8 ? 8 : 16), cib = 32 / fp;
+  const uint32_t win_k = fw <= 16 ? fh * ((ci + cib - 1) / cib * cib) * fp : ~0u;  // WIN
   if (ci % 32 == 0) {
     g.mode = kModeCI;
     p.K = fh * fw * ci;
+  } else if (kr <= 64 && fh * kr < win_k &&
+             (kTcBM / 32) * kr * 128 + co_tile_n(co) * kr * 4 <= kPStageBytes) {
+    g.mode = kModeROW;
+    g.KR = kr;
+    p.K = fh * kr;
   } else if (fw <= 16) {
     g.mode = kModeWIN;
-    g.FP = fw <= 4 ? 4 : (fw <= 8 ? 8 : 16);
-    g.CIB = 32 / g.FP;
+    g.FP = fp;
+    g.CIB = cib;
     g.CiP = (ci + g.CIB - 1) / g.CIB * g.CIB;
     p.K = fh * g.CiP * g.FP;
   } else {
@@ -593,13 +722,6 @@ struct ConvTcArgs {
   const float *w_hi, *w_lo, *x_hi, *x_lo;
 };
 
-// Output-channel tile width when channels are the N side: one or two tiles of
-// <= 256, rounded to 32 (no padding of C_o = 96 / 192 to a 128-row tile).
-uint32_t co_tile_n(uint32_t co) {
-  const uint32_t nco = (co + kPBN - 1) / kPBN;
-  return ((co + nco - 1) / nco + 31) / 32 * 32;
-}
-
 // Orientation: the tcgen05 tiles here are bound by operand traffic (L2 ->
 // shared memory), so pick the one with more useful flops per operand byte.
 //   channels on M: 128 x 256 tile, operands (128 + 256) rows, useful co / 128-padded
@@ -611,6 +733,52 @@ bool choose_co_on_n(uint32_t co) {
   const double nt = (co + bn - 1) / bn * double(bn);
   const double on_n = co / nt * (kTcBM * double(bn)) / (kTcBM + bn);
   return on_n > on_m * 1.02;
+}
+
+// Zero the stream-K region of out[co][col] (whole tiles inside it are
+// overwritten by plain stores anyway).  co_on_n: tile rows are columns.
+cudaError_t zero_sk_region(const Sched& sc, bool co_on_n, uint32_t bw, float* dst,
+                           uint32_t ncols, uint32_t co, cudaStream_t s) {
+  if (sc.dp_tiles >= sc.mt * sc.nt) return cudaSuccess;
+  const uint32_t nt0 = sc.dp_tiles / sc.mt;
+  uint32_t row0, col0;
+  if (co_on_n) {
+    row0 = nt0 * bw;
+    col0 = nt0 == sc.nt - 1 ? (sc.dp_tiles % sc.mt) * kTcBM : 0;
+  } else {
+    row0 = 0;
+    col0 = nt0 * kPBN;
+  }
+  return cudaMemset2DAsync(dst + uint64_t{row0} * ncols + col0, uint64_t{ncols} * 4, 0,
+                           uint64_t{ncols - col0} * 4, co - row0, s);
+}
+
+cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
+  const ConvArgs& a = t.a;
+  const TcPlan& p = t.p;
+  const uint32_t kr = p.g.KR, bn = co_tile_n(a.co);
+  ChwnRowLoader L;
+  L.wimg[0] = t.w_hi;
+  L.wimg[1] = t.w_lo;
+  const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
+  const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
+                             static_cast<uint64_t>(a.h) * a.w * a.n * 4};
+  const uint32_t box[4] = {32, a.fw, 1, a.ci};
+  if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, 1) ||
+      !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, 1))
+    return cudaErrorInvalidValue;
+  L.g = p.g;
+  L.ncols = a.ho * a.wo * a.n;
+  L.bn = bn;
+  Sched sc = make_sched((L.ncols + kTcBM - 1) / kTcBM, (a.co + bn - 1) / bn, a.fh,
+                        a.precision == LCNN_PREC_3XTF32 ? 3 : 1, bn, true, false);
+  sc.a_bytes = (kTcBM / 32) * kr * 128;
+  sc.stage_bytes = (kTcBM / 32) * a.ci * a.fw * 128 + bn * kr * 4;
+  sc.ksteps = kr / 8;
+  if (cudaError_t e = zero_sk_region(sc, true, bn, a.dst, L.ncols, a.co, s); e != cudaSuccess)
+    return e;
+  ColsOut O{a.dst, L.ncols, a.co};
+  return launch_persistent(L, O, sc, s);
 }
 
 template <bool kCoOnN>
@@ -633,8 +801,8 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   } else {
     box[0] = 32; box[1] = p.g.FP; box[2] = 1; box[3] = p.g.CIB;
   }
-  if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, true) ||
-      !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, true))
+  if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, 1) ||
+      !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, 1))
     return cudaErrorInvalidValue;
   L.g = p.g;
   L.ncols = a.ho * a.wo * a.n;
@@ -644,22 +812,8 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
                           bw, true, false)
              : make_sched((a.co + kTcBM - 1) / kTcBM, (L.ncols + kPBN - 1) / kPBN, p.K / kTcBK,
                           segs, kPBN, false, true);
-  if (sc.dp_tiles < sc.mt * sc.nt) {
-    // zero the stream-K region (whole tiles inside it are overwritten anyway)
-    const uint32_t nt0 = sc.dp_tiles / sc.mt;
-    uint32_t row0, col0;  // in out[co][col]
-    if (kCoOnN) {
-      row0 = nt0 * bw;
-      col0 = nt0 == sc.nt - 1 ? (sc.dp_tiles % sc.mt) * kTcBM : 0;
-    } else {
-      row0 = 0;
-      col0 = nt0 * kPBN;
-    }
-    cudaError_t e = cudaMemset2DAsync(a.dst + uint64_t{row0} * L.ncols + col0,
-                                      uint64_t{L.ncols} * 4, 0, uint64_t{L.ncols - col0} * 4,
-                                      a.co - row0, s);
-    if (e != cudaSuccess) return e;
-  }
+  if (cudaError_t e = zero_sk_region(sc, kCoOnN, bw, a.dst, L.ncols, a.co, s); e != cudaSuccess)
+    return e;
   if constexpr (kCoOnN) {
     ColsOut O{a.dst, L.ncols, a.co};
     return launch_persistent(L, O, sc, s);
@@ -671,9 +825,11 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
 
 size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, uint32_t co,
                             uint32_t fh, uint32_t fw, int precision) {
-  // packed filters for the widest packing (WIN with FP=16, CiP rounded to 2)
+  // packed filters for the widest packing (WIN with FP=16, CiP rounded to 2;
+  // ROW images: channel rows rounded to the tile, <= 64 k-rows per filter row)
   const uint64_t kmax = static_cast<uint64_t>(fh) * ((ci + 1) / 2 * 2) * 16 + fh * fw * ci;
-  uint64_t bytes = static_cast<uint64_t>(co) * kmax * 4 + 256;
+  const uint64_t packed = std::max<uint64_t>(uint64_t{co} * kmax, uint64_t{pack_rows(co)} * fh * 64);
+  uint64_t bytes = packed * 4 + 256;
   if (precision == LCNN_PREC_3XTF32)
     bytes = 2 * bytes + 2ull * n * ci * h * w * 4 + 256;
   return bytes;
@@ -702,7 +858,8 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   }
   const bool x3 = a.precision == LCNN_PREC_3XTF32;
   float* ws = static_cast<float*>(a.workspace);
-  const uint64_t apack = static_cast<uint64_t>(a.co) * p.K;
+  // packed filter count: [co][K], or the ROW image [co tiles * bn][K]
+  const uint64_t apack = static_cast<uint64_t>(p.g.mode == kModeROW ? pack_rows(a.co) : a.co) * p.K;
   float* a_hi = ws;
   float* a_lo = x3 ? a_hi + apack : nullptr;
   const float* b_hi = a.src;
@@ -718,8 +875,13 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
     b_hi = bh;
     b_lo = bl;
   }
-  pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, p.K);
   ConvTcArgs t{a, p, a_hi, x3 ? a_lo : a_hi, b_hi, b_lo};
+  if (p.g.mode == kModeROW) {
+    pack_filters_row_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, co_tile_n(a.co),
+                                                    apack);
+    return launch_chwn_row(t, s);
+  }
+  pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, p.K);
   return choose_co_on_n(a.co) ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
 }
 

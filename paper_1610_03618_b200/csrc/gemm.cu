@@ -38,7 +38,14 @@ using namespace lcnn_tc;
 struct GemmLoader {
   CUtensorMap a[2];
   CUtensorMap b[2];
-  static constexpr bool kAMajorMN = false, kBMajorMN = true;
+  static constexpr bool kZeroSmem = false;
+  static constexpr int kSteps = kTcBK / 8;
+  __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
+    return smem_desc_sw128(sa + k * 32, 16, 1024);
+  }
+  __device__ uint64_t desc_b(const uint8_t* sb, int k) const {
+    return smem_desc_sw128(sb + k * 1024, 4096, 512, 1);
+  }
   __device__ void prefetch() const {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
@@ -165,6 +172,8 @@ EncodeTiledFn encode_fn() {
 }  // namespace
 
 // 2D fp32 tensor map: dims {inner, outer}, row pitch in bytes, box {bi, bo}.
+// swizzle: 0 = SWIZZLE_128B (K-major operands), 1 = SWIZZLE_128B_ATOM_32B
+// (MN-major 32-bit operands), 2 = none (interleaved core-matrix images)
 bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer,
                   uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer, bool mn_major) {
   EncodeTiledFn enc = encode_fn();
@@ -182,7 +191,7 @@ bool make_tmap_2d(CUtensorMap* m, const float* base, uint64_t inner, uint64_t ou
 
 bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t* dims,
                const uint64_t* pitches_bytes, const uint32_t* box, const uint32_t* estrides,
-               bool mn_major) {
+               int swizzle) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t d[5];
@@ -196,7 +205,9 @@ bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t*
   }
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base), d, s, b, e,
              CU_TENSOR_MAP_INTERLEAVE_NONE,
-             mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             swizzle == 1   ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+             : swizzle == 2 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                            : CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }

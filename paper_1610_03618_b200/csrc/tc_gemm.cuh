@@ -17,6 +17,8 @@
 // accumulator -- used by the 3xTF32 mode (hi*hi + hi*lo + lo*hi).
 #pragma once
 
+#include <cstdlib>
+
 #include "tc.cuh"
 
 namespace lcnn_tc {
@@ -51,7 +53,10 @@ struct TcCtl {
 //   State begin(uint32_t m0, uint32_t n0, uint32_t kfirst) const;
 //   void load(State& st, uint32_t seg, uint32_t kb, void* sa, void* sb,
 //             uint64_t* bar) const;         // issues TMA, Sched::stage_bytes
-//   static constexpr bool kAMajorMN, kBMajorMN;  // operand major-ness
+//   uint64_t desc_a(const uint8_t* sa, int step) const;  // MMA smem descriptors
+//   uint64_t desc_b(const uint8_t* sb, int step) const;  //   of K-step `step`
+//   static constexpr bool kZeroSmem;  // stages carry never-loaded zero rows
+//   static constexpr int kSteps;      // K-steps per stage, 0 = Sched::ksteps
 // Segments chain operand sets into one accumulator (3 for 3xTF32).
 // Out concept:
 //   void store32(uint32_t m, uint32_t n0, const float* v, bool add) const;
@@ -93,6 +98,9 @@ struct Sched {
   uint32_t bn;           // N columns of a tile (multiple of 32, <= kPBN)
   uint32_t idesc;        // tcgen05 instruction descriptor (M = 128, N = bn)
   uint32_t stage_bytes;  // TMA bytes per pipeline stage
+  uint32_t a_bytes;      // offset of the B operand inside a stage
+  uint32_t ksteps;       // MMA K-steps (8 tf32 each) per stage
+  uint32_t probe;        // profiling knob (LCNN_TC_PROBE): 1 = no MMAs, 2 = no stores
 };
 
 inline int tc_sm_count() {
@@ -118,6 +126,13 @@ inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, u
   s.bn = bn;
   s.idesc = idesc_tf32(kTcBM, bn, a_mn, b_mn);
   s.stage_bytes = kTcABytes + bn * kTcBK * 4;
+  s.a_bytes = kTcABytes;
+  s.ksteps = kTcBK / 8;
+  static const uint32_t probe = [] {
+    const char* e = std::getenv("LCNN_TC_PROBE");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  s.probe = probe;
   s.kbn = kbn;
   s.iters = kbn * segs;
   const uint32_t tiles = mt * nt;
@@ -173,6 +188,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  if constexpr (Loader::kZeroSmem) {
+    // K padding rows that no TMA box ever writes must read as zeros
+    float4* z = reinterpret_cast<float4*>(smem);
+    for (uint32_t i = threadIdx.x; i < kPStages * kPStageBytes / 16; i += blockDim.x)
+      z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (warp == 0) {
     if (lane == 0) {
       ld.prefetch();
@@ -201,11 +223,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t ntile = t / sc.mt;
       uint32_t seg = kbeg / sc.kbn, kb = kbeg - seg * sc.kbn;
       auto st = ld.begin((t - ntile * sc.mt) * kTcBM, ntile * sc.bn, kb);
+
       for (uint32_t it = kbeg; it < kend; ++it) {
         mbar_wait(&ctl->empty[s], phase ^ 1);
         uint8_t* sa = smem + s * kPStageBytes;
         mbar_arrive_expect_tx(&ctl->full[s], sc.stage_bytes);
-        ld.load(st, seg, kb, sa, sa + kTcABytes, &ctl->full[s]);
+        ld.load(st, seg, kb, sa, sa + sc.a_bytes, &ctl->full[s]);
         if (++kb == sc.kbn) {
           kb = 0;
           ++seg;
@@ -230,14 +253,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mbar_wait(&ctl->full[s], phase);
         tc_fence_after();
         const uint8_t* sa = smem + s * kPStageBytes;
-        const uint8_t* sb = sa + kTcABytes;
+        const uint8_t* sb = sa + sc.a_bytes;
+        if (sc.probe & 1) {
+        } else if constexpr (Loader::kSteps > 0) {
 #pragma unroll
-        for (int k = 0; k < kTcBK / 8; ++k) {
-          const uint64_t ad = Loader::kAMajorMN ? smem_desc_sw128(sa + k * 1024, 4096, 512, 1)
-                                                : smem_desc_sw128(sa + k * 32, 16, 1024);
-          const uint64_t bd = Loader::kBMajorMN ? smem_desc_sw128(sb + k * 1024, 4096, 512, 1)
-                                                : smem_desc_sw128(sb + k * 32, 16, 1024);
-          mma_tf32(acc, ad, bd, idesc, (it != kbeg) || (k != 0));
+          for (int k = 0; k < Loader::kSteps; ++k)
+            mma_tf32(acc, ld.desc_a(sa, k), ld.desc_b(sb, k), idesc, (it != kbeg) || (k != 0));
+        } else {
+#pragma unroll 1
+          for (uint32_t k = 0; k < sc.ksteps; ++k)
+            mma_tf32(acc, ld.desc_a(sa, k), ld.desc_b(sb, k), idesc, (it != kbeg) || (k != 0));
         }
         tc_commit(&ctl->empty[s]);
         if (++s == kPStages) {
@@ -263,7 +288,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (uint32_t c = 0; c < sc.bn; c += 32) {
         float v[32];
         tmem_ld32(base + c, v);
-        out.store32(m, ntile * sc.bn + c, v, split);
+        if (!(sc.probe & 2)) out.store32(m, ntile * sc.bn + c, v, split);
       }
       tc_fence_before();
       __syncwarp();

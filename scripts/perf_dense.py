@@ -26,8 +26,17 @@ def timeit(fn, reps=10):
     return ts[len(ts) // 2]
 
 
+only = sys.argv[1:]  # optional name filters, e.g. conv1_chwn
+
+
+def want(name):
+    return not only or any(o in name for o in only)
+
+
 res = {}
 for (m, n, k) in [(8192, 8192, 8192), (4096, 4096, 4096), (128, 4096, 9216), (1024, 4096, 9216)]:
+    if not want(f"gemm_{m}x{n}x{k}"):
+        continue
     a = torch.rand(m * k, device=dev)
     b = torch.rand(k * n, device=dev)
     c = torch.empty(m * n, device=dev)
@@ -40,6 +49,8 @@ convs = {"conv1": (3, 227, 96, 11, 4, 0), "conv2": (96, 27, 192, 5, 1, 2), "conv
 N = 128
 for layout, tag in ((lcnn.CHWN, "chwn"), (lcnn.NCHW, "nchw")):
     for name, (ci, hw, co, f, s, p) in convs.items():
+        if not want(f"{name}_{tag}"):
+            continue
         x = lcnn.DeviceTensor4D(N, ci, hw, hw, layout, torch.rand(N * ci * hw * hw, device=dev))
         w = torch.rand(co * ci * f * f, device=dev)
         ho = (hw + 2 * p - f) // s + 1
