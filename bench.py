@@ -727,6 +727,9 @@ def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
     ms = float(t[0])
     value = batch * world * K / (ms / 1e3)
 
+    # kernels one forward launches (CUPTI, outside the timed region)
+    per_fwd = count_kernels(torch, lambda: net.forward(x.data_ptr(), in_layout, y.data_ptr(), sh))
+
     # per-entry device times of one forward (dominant kernel = slowest entry)
     prof = net.profile(x.data_ptr(), in_layout, sh)
     name, ns = max(prof, key=lambda e: e[1])
@@ -788,8 +791,25 @@ def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
                            "logits_verified": ok_rows,
                            "l2_policy": "activations + 245 MB weights per step (> L2)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": None, "clocks": clocks.summary(), "impl": "ours"}
+                "gpu_launches": per_fwd * K if per_fwd is not None else None,
+                "gpu_launches_per_step": per_fwd, "clocks": clocks.summary(), "impl": "ours"}
         print(json.dumps(line))
+
+
+def count_kernels(torch, fn):
+    """Kernel launches of fn() as recorded by CUPTI (torch.profiler); memsets
+    and copies are not kernels.  None if the profiler is unavailable."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as p:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in p.events() if e.device_type.name == "CUDA"]
+        return sum(1 for n in names if "memset" not in n.lower() and "memcpy" not in n.lower())
+    except Exception:
+        return None
 
 
 def reference_alexnet_sample(c_t, n_t, batch_per_thread=1):

@@ -20,7 +20,7 @@ typedef struct lcnn_net lcnn_net;
 /* parse_network (net.cpp:51-118) + annotate_layouts (net.cpp:186-195) with
  * thresholds (c_t, n_t) for layers whose layout is "auto" (c_t == 0 selects
  * the titan-black preset), weights from the reference's seeded streams
- * (net.cpp:398-420) uploaded once.  Returns an lcnn_status. */
+ * (net.cpp:217-243) uploaded once.  Returns an lcnn_status. */
 int lcnn_net_create(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
                     lcnn_net** out);
 void lcnn_net_destroy(lcnn_net* net);

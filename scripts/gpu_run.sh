@@ -13,10 +13,11 @@ fi
 if [[ $STAGE == all || $STAGE == bench ]]; then
   : > gpurun_out/bench.jsonl
   timeout 600 python bench.py >> gpurun_out/bench.jsonl 2> gpurun_out/bench.err
-  for wl in pl5 pl5_nchw softmax softmax5 transform; do
+  for wl in vgg_pools_nchw pl5 pl5_nchw softmax softmax5 softmax_64k transform alexnet; do
     timeout 300 python bench.py --workload $wl --steps 50 >> gpurun_out/bench.jsonl 2>> gpurun_out/bench.err
   done
   timeout 300 python bench.py --impl reference --steps 3 --warmup 3 >> gpurun_out/bench.jsonl 2>> gpurun_out/bench.err
+  timeout 300 python bench.py --workload alexnet --impl reference --steps 2 --warmup 1 >> gpurun_out/bench.jsonl 2>> gpurun_out/bench.err
 fi
 if [[ $STAGE == all || $STAGE == ncu ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
