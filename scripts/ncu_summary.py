@@ -96,11 +96,36 @@ def traffic(full_json, dst, pairs):
     print(f"wrote {dst}: {out}")
 
 
+def sections(dst_prefix, details):
+    """`ncu --page details --csv` files -> {section: {metric: "value unit"}} JSON."""
+    keep = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Compute Workload Analysis",
+            "Launch Statistics", "Occupancy", "Warp State Statistics")
+    for path in details:
+        rows = list(csv.reader(open(path)))
+        if not rows:
+            continue
+        hdr = rows[0]
+        ix = {h: i for i, h in enumerate(hdr)}
+        out = {}
+        for r in rows[1:]:
+            sec = r[ix["Section Name"]]
+            if sec in keep:
+                out.setdefault(sec, {})[r[ix["Metric Name"]]] = \
+                    f"{r[ix['Metric Value']]} {r[ix['Metric Unit']]}".strip()
+        name = os.path.basename(path).replace("_details.csv", "")
+        dst = f"{dst_prefix}{name}_sections.json"
+        with open(dst, "w") as f:
+            json.dump(out, f, indent=1)
+        print(f"wrote {dst}")
+
+
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "launches":
         launches(sys.argv[2], sys.argv[3])
     elif cmd == "full":
         full(sys.argv[2], sys.argv[3:])
+    elif cmd == "sections":
+        sections(sys.argv[2], sys.argv[3:])
     elif cmd == "traffic":
         traffic(sys.argv[2], sys.argv[3], sys.argv[4:])
