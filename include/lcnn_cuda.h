@@ -210,6 +210,37 @@ lcnn_status lcnn_conv_forward(const float* src, const float* filters,
                               uint32_t pad, int precision, void* d_workspace,
                               size_t workspace_bytes, void* stream);
 
+/* Filter pre-packing for convolutions whose weights are reused (network
+ * layers; run_network re-reads the same FilterBank every forward,
+ * net.cpp:284-330): lcnn_conv_forward split into its two phases.  A packed
+ * image is the operand layout of the kernel the geometry + precision route
+ * to, valid only for that exact (n, c_i, h, w, layout, c_o, f_h, f_w,
+ * stride, pad, precision); d_packed must be 256-byte aligned.  Sizes return
+ * 0 for invalid geometry.  lcnn_conv_forward_packed == lcnn_conv_forward on
+ * the filters that were packed, bit for bit. */
+size_t lcnn_conv_packed_bytes(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                              int layout, uint32_t c_o, uint32_t f_h,
+                              uint32_t f_w, uint32_t stride, uint32_t pad,
+                              int precision);
+size_t lcnn_conv_packed_workspace_bytes(uint32_t n, uint32_t c_i, uint32_t h,
+                                        uint32_t w, int layout, uint32_t c_o,
+                                        uint32_t f_h, uint32_t f_w,
+                                        uint32_t stride, uint32_t pad,
+                                        int precision);
+lcnn_status lcnn_conv_pack_filters(const float* filters, void* d_packed,
+                                   size_t packed_bytes, uint32_t n,
+                                   uint32_t c_i, uint32_t h, uint32_t w,
+                                   int layout, uint32_t c_o, uint32_t f_h,
+                                   uint32_t f_w, uint32_t stride, uint32_t pad,
+                                   int precision, void* stream);
+lcnn_status lcnn_conv_forward_packed(const float* src, const void* d_packed,
+                                     float* dst, uint32_t n, uint32_t c_i,
+                                     uint32_t h, uint32_t w, int layout,
+                                     uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                     uint32_t stride, uint32_t pad,
+                                     int precision, void* d_workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* == conv_oracle (conv.cpp:53-93): fp64 accumulation, any input layout,
  * NCHW output.  Ground truth, not a hot op. */
 lcnn_status lcnn_conv_oracle(const float* src, const float* filters, float* dst,

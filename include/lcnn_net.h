@@ -40,6 +40,14 @@ int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout,
 /* Forward with host buffers: H2D, forward, D2H (synchronous). */
 int lcnn_net_forward_host(const lcnn_net* net, const float* h_input,
                           int in_layout, float* h_output);
+/* `count` forwards over host buffers h_inputs[i] -> h_outputs[i] (pinned
+ * memory for overlap), pipelined: the H2D of batch i+1 runs on a copy stream
+ * into the other of two device input buffers while batch i computes; each
+ * result is read back (D2H) on the compute stream.  Returns when every output
+ * has landed.  The streaming form of run_network's host-buffer contract
+ * (net.cpp:266-398) for a sequence of batches. */
+int lcnn_net_forward_host_many(const lcnn_net* net, const float* const* h_inputs,
+                               int in_layout, float* const* h_outputs, uint32_t count);
 
 /* One forward with per-entry CUDA-event device times (layers and inserted
  * transforms, in execution order): nanos[i], names comma-separated. */

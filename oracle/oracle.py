@@ -326,6 +326,18 @@ class Ref:
         return list(layouts), [(pos[i], src[i], dst[i]) for i in range(steps.value)]
 
     @classmethod
+    def run_network(cls, json_text, x, in_layout, c_t=0, n_t=0, seed=42, out_cap=1 << 24):
+        """The unmodified run_network on input x (flat, in in_layout) ->
+        (rows, cols) float32 matrix (ref_shim.cpp ref_run_network)."""
+        x = _f32(x)
+        out = np.empty(out_cap, np.float32)
+        rows, cols = c_uint32(), c_uint32()
+        cls._rc(cls.lib().ref_run_network(json_text.encode(), c_t, n_t, c_uint64(seed), _p(x),
+                                          in_layout, _p(out), c_uint64(out_cap),
+                                          ctypes.byref(rows), ctypes.byref(cols)))
+        return out[:rows.value * cols.value].reshape(rows.value, cols.value).copy()
+
+    @classmethod
     def session(cls, op, n, c, h, w, layout=NCHW, dst_layout=NCHW, wh=1, ww=1, s=1, avg=False,
                 fh=1, fw=1, threads=1):
         """A timed reference call over an n-image batch split into `threads`

@@ -410,4 +410,28 @@ double ref_time_network(const char* json, uint32_t c_t, uint32_t n_t, int thread
   }
 }
 
+// The unmodified run_network (net.cpp:266-398) on a caller-supplied input in
+// `in_layout` (flat order of that layout), network annotated with (c_t, n_t)
+// (c_t == 0: explicit fields only), default seeded weights.  The output
+// matrix goes to out (capacity out_cap floats), dims to *rows / *cols.
+int ref_run_network(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
+                    const float* input, int in_layout, float* out, uint64_t out_cap,
+                    uint32_t* rows, uint32_t* cols) {
+  GUARD({
+    R::NetworkSpec spec = R::parse_network(json);
+    if (c_t) spec = R::annotate_layouts(spec, R::HeuristicThresholds{c_t, n_t});
+    R::Tensor4D in(spec.n, spec.c, spec.h, spec.w, static_cast<R::Layout>(in_layout));
+    std::copy(input, input + in.size(), in.data());
+    R::RunOptions opt;
+    opt.seed = seed;
+    const R::RunResult res = R::run_network(spec, in, opt);
+    const auto* m = std::get_if<R::Matrix>(&res.output);
+    if (!m) throw std::runtime_error("ref_run_network: network does not end in a matrix");
+    if (m->data.size() > out_cap) throw std::runtime_error("ref_run_network: output too large");
+    *rows = m->rows;
+    *cols = m->cols;
+    std::copy(m->data.begin(), m->data.end(), out);
+  })
+}
+
 }  // extern "C"

@@ -68,6 +68,12 @@ _SIGNATURES = {
     "lcnn_conv_workspace_bytes": (c_size_t, [_U32] * 7 + [c_int]),
     "lcnn_conv_forward": (c_int, [_P, _P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32,
                                   _U32, c_int, _P, c_size_t, _P]),
+    "lcnn_conv_packed_bytes": (c_size_t, [_U32] * 4 + [c_int] + [_U32] * 5 + [c_int]),
+    "lcnn_conv_packed_workspace_bytes": (c_size_t, [_U32] * 4 + [c_int] + [_U32] * 5 + [c_int]),
+    "lcnn_conv_pack_filters": (c_int, [_P, _P, c_size_t] + [_U32] * 4 + [c_int] + [_U32] * 5 +
+                               [c_int, _P]),
+    "lcnn_conv_forward_packed": (c_int, [_P, _P, _P] + [_U32] * 4 + [c_int] + [_U32] * 5 +
+                                 [c_int, _P, c_size_t, _P]),
     "lcnn_conv_oracle": (c_int, [_P, _P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32,
                                  _U32, _P]),
     "lcnn_im2col": (c_int, [_P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32, _P]),

@@ -1,6 +1,8 @@
 // C ABI (include/lcnn_cuda.h): host-side validation with the reference's
 // rules and messages, analytic access/pass reports, kernel dispatch.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdio.h>
 #include <string.h>
 
@@ -347,15 +349,24 @@ lcnn_status lcnn_conv_output_extents(uint32_t h, uint32_t w, uint32_t f_h, uint3
 
 size_t lcnn_conv_workspace_bytes(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, uint32_t c_o,
                                  uint32_t f_h, uint32_t f_w, int precision) {
-  return lcnn_impl::conv_workspace_bytes(n, c_i, h, w, c_o, f_h, f_w, precision);
+  // the larger of the two layouts' needs (the route does not depend on the
+  // stride / padding except through 2^31-column limits, which only ever
+  // select the smaller fp32 path)
+  size_t best = 0;
+  for (int layout : {LCNN_CHWN, LCNN_NCHW}) {
+    lcnn_impl::ConvArgs a{nullptr, nullptr, nullptr, n, c_i, h, w, c_o, f_h, f_w, 1, 0, 1, 1,
+                          layout, precision, nullptr};
+    best = std::max(best, lcnn_impl::conv_workspace_bytes(a));
+  }
+  return best;
 }
 
-lcnn_status lcnn_conv_forward(const float* src, const float* filters, float* dst, uint32_t n,
-                              uint32_t c_i, uint32_t h, uint32_t w, int layout, uint32_t c_o,
-                              uint32_t f_h, uint32_t f_w, uint32_t stride, uint32_t pad,
-                              int precision, void* d_workspace, size_t workspace_bytes,
-                              void* stream) {
-  if (!src || !filters || !dst) return fail(LCNN_EINVAL, "conv: null pointer");
+namespace {
+
+// Shared validation of the conv entry points; fills a (pointers left null).
+lcnn_status conv_args(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, int layout, uint32_t c_o,
+                      uint32_t f_h, uint32_t f_w, uint32_t stride, uint32_t pad, int precision,
+                      lcnn_impl::ConvArgs* a) {
   if (precision < LCNN_PREC_TF32 || precision > LCNN_PREC_FP32)
     return fail(LCNN_EINVAL, "conv: bad precision");
   lcnn_status st = check_volume(n, c_i, h, w, "Tensor4D");
@@ -367,13 +378,88 @@ lcnn_status lcnn_conv_forward(const float* src, const float* filters, float* dst
   if (st != LCNN_OK) return st;
   if (layout != LCNN_CHWN && layout != LCNN_NCHW)
     return fail(LCNN_ELAYOUT, "conv_direct: only CHWN and NCHW kernels exist");  // conv.cpp:211
-  if (precision != LCNN_PREC_FP32 &&
-      workspace_bytes < lcnn_conv_workspace_bytes(n, c_i, h, w, c_o, f_h, f_w, precision))
+  *a = lcnn_impl::ConvArgs{nullptr, nullptr, nullptr, n, c_i, h, w, c_o, f_h, f_w, stride, pad,
+                           ho, wo, layout, precision, nullptr};
+  return LCNN_OK;
+}
+
+}  // namespace
+
+lcnn_status lcnn_conv_forward(const float* src, const float* filters, float* dst, uint32_t n,
+                              uint32_t c_i, uint32_t h, uint32_t w, int layout, uint32_t c_o,
+                              uint32_t f_h, uint32_t f_w, uint32_t stride, uint32_t pad,
+                              int precision, void* d_workspace, size_t workspace_bytes,
+                              void* stream) {
+  if (!src || !filters || !dst) return fail(LCNN_EINVAL, "conv: null pointer");
+  lcnn_impl::ConvArgs a;
+  lcnn_status st = conv_args(n, c_i, h, w, layout, c_o, f_h, f_w, stride, pad, precision, &a);
+  if (st != LCNN_OK) return st;
+  if (workspace_bytes < lcnn_impl::conv_workspace_bytes(a) || (!d_workspace && workspace_bytes))
     return fail(LCNN_EINVAL, "conv: workspace too small");
-  lcnn_impl::ConvArgs a{src, filters, dst, n, c_i, h, w, c_o, f_h, f_w, stride, pad, ho, wo,
-                        layout, precision, d_workspace};
+  a.src = src;
+  a.filters = filters;
+  a.dst = dst;
+  a.workspace = d_workspace;
   cudaError_t e = lcnn_impl::launch_conv(a, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "conv_forward");
+  return ok();
+}
+
+size_t lcnn_conv_packed_bytes(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, int layout,
+                              uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
+                              uint32_t pad, int precision) {
+  lcnn_impl::ConvArgs a;
+  if (conv_args(n, c_i, h, w, layout, c_o, f_h, f_w, stride, pad, precision, &a) != LCNN_OK)
+    return 0;
+  return lcnn_impl::conv_packed_bytes(a);
+}
+
+size_t lcnn_conv_packed_workspace_bytes(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                                        int layout, uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                        uint32_t stride, uint32_t pad, int precision) {
+  lcnn_impl::ConvArgs a;
+  if (conv_args(n, c_i, h, w, layout, c_o, f_h, f_w, stride, pad, precision, &a) != LCNN_OK)
+    return 0;
+  return lcnn_impl::conv_workspace_bytes(a) - lcnn_impl::conv_packed_bytes(a);
+}
+
+lcnn_status lcnn_conv_pack_filters(const float* filters, void* d_packed, size_t packed_bytes,
+                                   uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, int layout,
+                                   uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
+                                   uint32_t pad, int precision, void* stream) {
+  if (!filters || !d_packed) return fail(LCNN_EINVAL, "conv: null pointer");
+  if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
+    return fail(LCNN_EINVAL, "conv: packed filters must be 256-byte aligned");
+  lcnn_impl::ConvArgs a;
+  lcnn_status st = conv_args(n, c_i, h, w, layout, c_o, f_h, f_w, stride, pad, precision, &a);
+  if (st != LCNN_OK) return st;
+  if (packed_bytes < lcnn_impl::conv_packed_bytes(a))
+    return fail(LCNN_EINVAL, "conv: packed buffer too small");
+  a.filters = filters;
+  cudaError_t e = lcnn_impl::launch_conv_pack(a, d_packed, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "conv_pack_filters");
+  return ok();
+}
+
+lcnn_status lcnn_conv_forward_packed(const float* src, const void* d_packed, float* dst,
+                                     uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, int layout,
+                                     uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
+                                     uint32_t pad, int precision, void* d_workspace,
+                                     size_t workspace_bytes, void* stream) {
+  if (!src || !d_packed || !dst) return fail(LCNN_EINVAL, "conv: null pointer");
+  if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
+    return fail(LCNN_EINVAL, "conv: packed filters must be 256-byte aligned");
+  lcnn_impl::ConvArgs a;
+  lcnn_status st = conv_args(n, c_i, h, w, layout, c_o, f_h, f_w, stride, pad, precision, &a);
+  if (st != LCNN_OK) return st;
+  const size_t need = lcnn_impl::conv_workspace_bytes(a) - lcnn_impl::conv_packed_bytes(a);
+  if (workspace_bytes < need || (!d_workspace && workspace_bytes))
+    return fail(LCNN_EINVAL, "conv: workspace too small");
+  a.src = src;
+  a.dst = dst;
+  a.workspace = d_workspace;
+  cudaError_t e = lcnn_impl::launch_conv_packed(a, d_packed, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "conv_forward_packed");
   return ok();
 }
 

@@ -46,7 +46,7 @@ enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2, kModeROW = 3
 struct ConvGeomTc {
   uint32_t N, Ci, H, W, Co, FH, FW, S, P, Ho, Wo;
   uint32_t mode, FP, CIB, CiP;
-  uint32_t KR;  // ROW mode: k-rows per filter row (Ci*FW rounded up to 8)
+  uint32_t KR;  // ROW mode: k-rows per filter row (Ci*FP rounded up to 8; FP = row width)
 };
 
 // Wpack[co][k] in the loader's K order, zero for padded (ci, fw) slots.
@@ -105,10 +105,15 @@ __global__ void pack_filters_kernel(const float* __restrict__ f, float* __restri
 //   false: A = filters (128 channels),        B = input (8 boxes = 256 columns)
 template <bool kCoOnN>
 struct ChwnConvLoader {
-  CUtensorMap x[2];  // input hi / lo          (4D: {N, W, H, Ci})
+  CUtensorMap x[2];  // input hi / lo          (4D: {N, W, H, Ci}, or grouped 5D)
   CUtensorMap w[2];  // packed filters hi / lo (2D: {K, Co})
   ConvGeomTc g;
   uint32_t ncols;  // Ho*Wo*N
+  // grouped (N % 128 == 0): the input view {32 n, W, Ci, N/32, H} -- group
+  // stride 128 B -- so ONE 5D box {32, FP, CIB, 4, 1} lands a whole
+  // 128-column block (one output pixel, 4 MN-major atoms) instead of four
+  // 4D boxes; TMA cost is mostly per box (scripts/tma_bench.cu)
+  bool grouped;
   static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN, kZeroSmem = false;
   static constexpr int kSteps = kTcBK / 8;
   static constexpr int kBoxes = kCoOnN ? kTcBM / 32 : kPBN / 32;
@@ -126,9 +131,13 @@ struct ChwnConvLoader {
     tma_prefetch(&x[0]);
     tma_prefetch(&w[0]);
   }
+  __device__ uint32_t resident_bytes() const { return 0; }
+  __device__ void load_resident(void*, uint64_t*) const {}
+  __device__ uint32_t resident_offset(uint32_t) const { return 0; }
   // Per tile fragment: the column boxes' (n0, w origin, h origin) and the
   // first k-block's (fh, fw, channel) decoded once; per k-block the tap /
-  // channel-block counters advance incrementally.
+  // channel-block counters advance incrementally.  Grouped: entry j < kBoxes/4
+  // describes 128-column block j and n0 holds its first group index.
   struct State {
     uint32_t co0;
     int32_t n0[kBoxes], y0[kBoxes], z0[kBoxes];
@@ -138,12 +147,14 @@ struct ChwnConvLoader {
     State st;
     const uint32_t col0 = kCoOnN ? m0 : n0;
     st.co0 = kCoOnN ? n0 : m0;
+    const uint32_t span = grouped ? 128 : 32;
 #pragma unroll
     for (int j = 0; j < kBoxes; ++j) {
-      const uint32_t col = col0 + 32 * j;
+      const uint32_t col = col0 + span * j;
       const uint32_t pos = col / g.N;
       const uint32_t oh = pos / g.Wo, ow = pos - oh * g.Wo;
-      st.n0[j] = static_cast<int32_t>(col - pos * g.N);
+      const uint32_t nn = col - pos * g.N;
+      st.n0[j] = static_cast<int32_t>(grouped ? nn / 32 : nn);
       st.y0[j] = static_cast<int32_t>(ow * g.S) - static_cast<int32_t>(g.P);
       // beyond the last output: an all-out-of-bounds box (zeros)
       st.z0[j] = col >= ncols ? -(1 << 20)
@@ -167,10 +178,17 @@ struct ChwnConvLoader {
     if (k == 0) st.fh = st.wofs = st.c0 = 0;  // a new segment restarts K
     uint8_t* sx = static_cast<uint8_t*>(kCoOnN ? sa : sb);
     const CUtensorMap* xm = &x[seg == 1 ? 1 : 0];
+    if (grouped) {
 #pragma unroll
-    for (int j = 0; j < kBoxes; ++j)
-      tma_load_4d(sx + j * 4096, xm, bar, st.n0[j], st.y0[j] + static_cast<int32_t>(st.wofs),
-                  st.z0[j] + static_cast<int32_t>(st.fh), static_cast<int32_t>(st.c0));
+      for (int j = 0; j < kBoxes / 4; ++j)
+        tma_load_5d(sx + j * 16384, xm, bar, 0, st.y0[j] + static_cast<int32_t>(st.wofs),
+                    static_cast<int32_t>(st.c0), st.n0[j], st.z0[j] + static_cast<int32_t>(st.fh));
+    } else {
+#pragma unroll
+      for (int j = 0; j < kBoxes; ++j)
+        tma_load_4d(sx + j * 4096, xm, bar, st.n0[j], st.y0[j] + static_cast<int32_t>(st.wofs),
+                    st.z0[j] + static_cast<int32_t>(st.fh), static_cast<int32_t>(st.c0));
+    }
     tma_load_2d(kCoOnN ? sb : sa, &w[seg == 2 ? 1 : 0], bar, k * kTcBK, st.co0);
     // advance: CI mode k = (fh, fw, ci/32); WIN mode k = (fh, ci/CIB)
     if (g.mode == kModeCI) {
@@ -198,39 +216,69 @@ struct ChwnConvLoader {
 // 8 (33 -> 40 rows instead of WIN's 3 -> 4 channels x 11 -> 16 taps = 64).
 // Channels are the N side.  The filters are pre-packed in global memory as
 // the exact shared-memory image of the B operand per (channel tile, filter
-// row) -- the SWIZZLE_NONE K-major core-matrix layout, [k/4][bn][4] -- so a
-// stage's B is ONE contiguous bulk copy of bn * KR * 4 bytes.  The padding
-// rows of the input boxes are never written by TMA; the kernel zeroes shared
-// memory once at start (kZeroSmem) and the padded weights are zero.
+// row) -- the SWIZZLE_NONE K-major core-matrix layout, [k/4][bn][4].
+// Resident mode (one channel tile, TF32, image fits next to >= 3 ring
+// slots): the whole filter image -- 169 KB for conv1 -- is bulk-copied into
+// shared memory ONCE per CTA and every stage streams only the input boxes
+// (halving conv1's per-stage operand bytes); otherwise a stage's B is one
+// contiguous bulk copy of bn * KR * 4 bytes.  The padding rows of the input
+// boxes are never written by TMA; the kernel zeroes shared memory once at
+// start (kZeroSmem) and the padded weights are zero.
+template <bool kCoOnN>
 struct ChwnRowLoader {
   CUtensorMap x[2];         // input hi / lo (4D: {N, W, H, Ci}, box {32, FW, 1, Ci})
   const float* wimg[2];     // filter images hi / lo: [co tile][fh][KR/4][bn][4]
   ConvGeomTc g;
-  uint32_t ncols, bn;
-  static constexpr bool kAMajorMN = true, kBMajorMN = false, kZeroSmem = true;
+  uint32_t ncols, bn;       // bn: channel rows per filter-image tile (the N or M extent)
+  uint32_t res;             // resident filter image bytes (0 = streamed per stage)
+  // grouped (N % 128 == 0): 5D view {32 n, W, Ci, N/32, H}, one box
+  // {32, FP, Ci, 4, 1} per 128-column block; each group's rows are (ci, w)
+  // with w padded to FP so a group is exactly KR = Ci * FP rows (whole
+  // 1 KB swizzle atoms); the padded taps have zero weights
+  bool grouped;
+  static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN, kZeroSmem = true;
   static constexpr int kSteps = 0;
+  static constexpr int kBoxes = kCoOnN ? kTcBM / 32 : kPBN / 32;  // 32-column input boxes
+  // input operand: MN-major SWIZZLE_128B_BASE32B, kBoxes groups of KR rows;
+  // filter operand: K-major SWIZZLE_NONE core matrices [k/4][bn][4]
+  __device__ uint64_t desc_x(const uint8_t* p, int k) const {
+    return smem_desc_sw128(p + k * 1024, g.KR * 128, 512, 1);
+  }
+  __device__ uint64_t desc_w(const uint8_t* p, int k) const {
+    // K-step k = k-chunks 2k, 2k+1; LBO = next k-chunk, SBO = next 8 rows
+    return smem_desc_sw128(p + 2 * k * bn * 16, bn * 16, 128, 0);
+  }
   __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
-    return smem_desc_sw128(sa + k * 1024, g.KR * 128, 512, 1);
+    return kCoOnN ? desc_x(sa, k) : desc_w(sa, k);
   }
   __device__ uint64_t desc_b(const uint8_t* sb, int k) const {
-    // K-step k = k-chunks 2k, 2k+1; LBO = next k-chunk, SBO = next 8 rows
-    return smem_desc_sw128(sb + 2 * k * bn * 16, bn * 16, 128, 0);
+    return kCoOnN ? desc_w(sb, k) : desc_x(sb, k);
   }
   __device__ void prefetch() const { tma_prefetch(&x[0]); }
+  __device__ uint32_t resident_bytes() const { return res; }
+  __device__ void load_resident(void* dst, uint64_t* bar) const {
+    const uint32_t row = g.KR * bn * 4;  // one filter row per copy
+    for (uint32_t fh = 0; fh < g.FH; ++fh)
+      bulk_load(static_cast<uint8_t*>(dst) + fh * row, wimg[0] + fh * g.KR * bn, row, bar);
+  }
+  __device__ uint32_t resident_offset(uint32_t kb) const { return kb * g.KR * bn * 4; }
   struct State {
     uint32_t wofs, fh;  // filter image offset of this channel tile (floats), filter row
-    int32_t n0[kTcBM / 32], y0[kTcBM / 32], z0[kTcBM / 32];
+    int32_t n0[kBoxes], y0[kBoxes], z0[kBoxes];
   };
-  __device__ State begin(uint32_t col0, uint32_t co0, uint32_t kfirst) const {
+  __device__ State begin(uint32_t m0, uint32_t n0, uint32_t kfirst) const {
     State st;
+    const uint32_t col0 = kCoOnN ? m0 : n0, co0 = kCoOnN ? n0 : m0;
     st.wofs = co0 / bn * g.FH * g.KR * bn;
     st.fh = kfirst;
+    const uint32_t span = grouped ? 128 : 32;
 #pragma unroll
-    for (int j = 0; j < kTcBM / 32; ++j) {
-      const uint32_t col = col0 + 32 * j;
+    for (int j = 0; j < kBoxes; ++j) {
+      const uint32_t col = col0 + span * j;
       const uint32_t pos = col / g.N;
       const uint32_t oh = pos / g.Wo, ow = pos - oh * g.Wo;
-      st.n0[j] = static_cast<int32_t>(col - pos * g.N);
+      const uint32_t nn = col - pos * g.N;
+      st.n0[j] = static_cast<int32_t>(grouped ? nn / 32 : nn);
       st.y0[j] = static_cast<int32_t>(ow * g.S) - static_cast<int32_t>(g.P);
       st.z0[j] = col >= ncols ? -(1 << 20)
                               : static_cast<int32_t>(oh * g.S) - static_cast<int32_t>(g.P);
@@ -241,17 +289,28 @@ struct ChwnRowLoader {
                        uint64_t* bar) const {
     if (k == 0) st.fh = 0;
     const CUtensorMap* xm = &x[seg == 1 ? 1 : 0];
+    uint8_t* sx = static_cast<uint8_t*>(kCoOnN ? sa : sb);
+    if (grouped) {
 #pragma unroll
-    for (int j = 0; j < kTcBM / 32; ++j)
-      tma_load_4d(static_cast<uint8_t*>(sa) + j * g.KR * 128, xm, bar, st.n0[j], st.y0[j],
-                  st.z0[j] + static_cast<int32_t>(st.fh), 0);
-    bulk_load(sb, wimg[seg == 2 ? 1 : 0] + st.wofs + st.fh * g.KR * bn, g.KR * bn * 4, bar);
+      for (int j = 0; j < kBoxes / 4; ++j)
+        tma_load_5d(sx + j * 4 * g.KR * 128, xm, bar, 0, st.y0[j], 0, st.n0[j],
+                    st.z0[j] + static_cast<int32_t>(st.fh));
+    } else {
+#pragma unroll
+      for (int j = 0; j < kBoxes; ++j)
+        tma_load_4d(sx + j * g.KR * 128, xm, bar, st.n0[j], st.y0[j],
+                    st.z0[j] + static_cast<int32_t>(st.fh), 0);
+    }
+    if (!res)
+      bulk_load(kCoOnN ? sb : sa, wimg[seg == 2 ? 1 : 0] + st.wofs + st.fh * g.KR * bn,
+                g.KR * bn * 4, bar);
     ++st.fh;
   }
 };
 
 // Filter image of ROW mode: img[((t * FH + fh) * KR/4 + q) * bn + r][e] =
-// W[co = t*bn + r][ci][fh][fw] with ci*FW + fw = 4q + e (zero when padded).
+// W[co = t*bn + r][ci][fh][fw] with ci*FP + fw = 4q + e (FP = the row width:
+// F_w, or its padding in grouped mode; zero when padded).
 __global__ void pack_filters_row_kernel(const float* __restrict__ f, float* __restrict__ hi,
                                         float* __restrict__ lo, ConvGeomTc g, uint32_t bn,
                                         uint64_t total) {
@@ -265,9 +324,10 @@ __global__ void pack_filters_row_kernel(const float* __restrict__ f, float* __re
     rest /= g.KR / 4;
     const uint32_t fh = static_cast<uint32_t>(rest % g.FH);
     const uint32_t t = static_cast<uint32_t>(rest / g.FH);
-    const uint32_t kk = 4 * q + e, ci = kk / g.FW, fw = kk - ci * g.FW, co = t * bn + r;
+    const uint32_t kk = 4 * q + e, ci = kk / g.FP, fw = kk - ci * g.FP, co = t * bn + r;
     float v = 0.0f;
-    if (co < g.Co && ci < g.Ci) v = f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw];
+    if (co < g.Co && ci < g.Ci && fw < g.FW)
+      v = f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw];
     if (lo) {
       uint32_t u;
       asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
@@ -633,8 +693,57 @@ uint32_t co_tile_n(uint32_t co) {
   return ((co + nco - 1) / nco + 31) / 32 * 32;
 }
 
-// channel rows of a ROW-mode filter image (tiles of co_tile_n)
-uint32_t pack_rows(uint32_t co) { return (co + co_tile_n(co) - 1) / co_tile_n(co) * co_tile_n(co); }
+// Measured on B200 (scripts/mma_bench.cu, scripts/tma_bench.cu): one
+// tcgen05.mma.kind::tf32 with M = 128, K = 8 issues every ~150 cycles
+// whatever its N (32..256) -- so useful work per instruction is what counts --
+// and a TMA box costs ~80 cycles of fixed overhead plus ~0.9 cycle per
+// 128-byte row it moves.  A pipeline stage takes the longer of the two.
+double stage_cycles(uint32_t ksteps, uint32_t boxes, uint32_t rows) {
+  const double mma = 150.0 * ksteps, tma = 80.0 * boxes + 0.9 * rows;
+  return mma > tma ? mma : tma;
+}
+
+// Orientation by the cost model: channels on N (tiles of 128 columns x
+// co_tile_n channels, kTcBM/32 input boxes) or channels on M (128-channel
+// tiles x 256 columns, kPBN/32 input boxes) -- the cheaper whole-layer
+// estimate wins, ties go to channels on N (fewer boxes).  krows: k-rows per
+// stage; in_rows: 128-byte rows of one 32-column input box; w_rows: 128-byte
+// rows of one 128-row filter slice of a stage.
+bool choose_co_on_n(uint32_t co, uint64_t ncols, uint32_t krows, uint32_t in_rows,
+                    uint32_t w_rows_per_128, bool grouped) {
+  const uint32_t div = grouped ? 4 : 1;  // grouped: one box per four 32-column atoms
+  const uint32_t bn = co_tile_n(co);
+  const double tiles_n = double((ncols + kTcBM - 1) / kTcBM) * ((co + bn - 1) / bn);
+  const double tiles_m = double((co + kTcBM - 1) / kTcBM) * ((ncols + kPBN - 1) / kPBN);
+  const double on_n =
+      tiles_n * stage_cycles(krows / 8, kTcBM / 32 / div + 1,
+                             (kTcBM / 32) * in_rows + w_rows_per_128 * bn / kTcBM);
+  const double on_m =
+      tiles_m * stage_cycles(krows / 8, kPBN / 32 / div + 1,
+                             (kPBN / 32) * in_rows + w_rows_per_128);
+  return on_n <= on_m;
+}
+
+// CI / WIN orientation (measured better than the stage model above for
+// conv2-5, whose channels-on-N epilogue stores and stream-K adds are scalar):
+// the orientation with more useful flops per operand byte.
+//   channels on M: 128 x 256 tile, operands (128 + 256) rows, useful co / 128-padded
+//   channels on N: 128 x bn tile,  operands (128 + bn) rows,  useful co / bn-padded
+bool choose_co_on_n_traffic(uint32_t co) {
+  const double mt = (co + kTcBM - 1) / kTcBM * double(kTcBM);
+  const double on_m = co / mt * (kTcBM * double(kPBN)) / (kTcBM + kPBN);
+  const uint32_t bn = co_tile_n(co);
+  const double nt = (co + bn - 1) / bn * double(bn);
+  const double on_n = co / nt * (kTcBM * double(bn)) / (kTcBM + bn);
+  return on_n > on_m * 1.02;
+}
+
+// channel rows of a ROW-mode filter image: tiles of co_tile_n (channels on
+// N) or of 128 (channels on M)
+uint32_t pack_rows(uint32_t co, bool co_on_n) {
+  const uint32_t t = co_on_n ? co_tile_n(co) : kTcBM;
+  return (co + t - 1) / t * t;
+}
 
 struct TcPlan {
   bool ok = false;
@@ -642,12 +751,9 @@ struct TcPlan {
   uint32_t K = 0;  // packed K (multiple of 32)
 };
 
-cudaError_t launch_conv_nchw_tc(const ConvArgs& a, cudaStream_t s) {
-  ConvGeomTc g{a.n, a.ci, a.h, a.w, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo, kModeNAT, 0, 0, 0};
+cudaError_t launch_conv_nchw_tc(const ConvArgs& a, const float* wpack, uint32_t Kp,
+                               cudaStream_t s) {
   const uint32_t K = a.ci * a.fh * a.fw;
-  const uint32_t Kp = (K + kTcBK - 1) / kTcBK * kTcBK;
-  float* wpack = static_cast<float*>(a.workspace);
-  pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, wpack, nullptr, g, Kp);
   NchwConvParams prm;
   if (!make_tmap_2d(&prm.a, wpack, Kp, a.co, static_cast<uint64_t>(Kp) * 4, kTcBK, kTcBM, false))
     return cudaErrorInvalidValue;
@@ -696,11 +802,19 @@ TcPlan plan_tc(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, int layout, uint
   if (ci % 32 == 0) {
     g.mode = kModeCI;
     p.K = fh * fw * ci;
-  } else if (kr <= 64 && fh * kr < win_k &&
-             (kTcBM / 32) * kr * 128 + co_tile_n(co) * kr * 4 <= kPStageBytes) {
+  } else if (kr <= 64 && fh * kr < win_k) {
     g.mode = kModeROW;
     g.KR = kr;
-    p.K = fh * kr;
+    g.FP = fw;
+    if (n % 128 == 0) {  // grouped input boxes: rows per group a multiple of 8
+      uint32_t wb = fw;
+      while ((ci * wb) % 8) ++wb;
+      if (ci * wb <= 64) {
+        g.FP = wb;
+        g.KR = ci * wb;
+      }
+    }
+    p.K = fh * g.KR;
   } else if (fw <= 16) {
     g.mode = kModeWIN;
     g.FP = fp;
@@ -722,19 +836,6 @@ struct ConvTcArgs {
   const float *w_hi, *w_lo, *x_hi, *x_lo;
 };
 
-// Orientation: the tcgen05 tiles here are bound by operand traffic (L2 ->
-// shared memory), so pick the one with more useful flops per operand byte.
-//   channels on M: 128 x 256 tile, operands (128 + 256) rows, useful co / 128-padded
-//   channels on N: 128 x bn tile,  operands (128 + bn) rows,  useful co / bn-padded
-bool choose_co_on_n(uint32_t co) {
-  const double mt = (co + kTcBM - 1) / kTcBM * double(kTcBM);
-  const double on_m = co / mt * (kTcBM * double(kPBN)) / (kTcBM + kPBN);
-  const uint32_t bn = co_tile_n(co);
-  const double nt = (co + bn - 1) / bn * double(bn);
-  const double on_n = co / nt * (kTcBM * double(bn)) / (kTcBM + bn);
-  return on_n > on_m * 1.02;
-}
-
 // Zero the stream-K region of out[co][col] (whole tiles inside it are
 // overwritten by plain stores anyway).  co_on_n: tile rows are columns.
 cudaError_t zero_sk_region(const Sched& sc, bool co_on_n, uint32_t bw, float* dst,
@@ -753,32 +854,75 @@ cudaError_t zero_sk_region(const Sched& sc, bool co_on_n, uint32_t bw, float* ds
                            uint64_t{ncols - col0} * 4, co - row0, s);
 }
 
+template <bool kCoOnN>
 cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
   const ConvArgs& a = t.a;
   const TcPlan& p = t.p;
-  const uint32_t kr = p.g.KR, bn = co_tile_n(a.co);
-  ChwnRowLoader L;
+  const uint32_t kr = p.g.KR, bn = kCoOnN ? co_tile_n(a.co) : kTcBM;  // filter tile rows
+  ChwnRowLoader<kCoOnN> L;
   L.wimg[0] = t.w_hi;
   L.wimg[1] = t.w_lo;
   const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
   const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
                              static_cast<uint64_t>(a.h) * a.w * a.n * 4};
-  const uint32_t box[4] = {32, a.fw, 1, a.ci};
-  if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, 1) ||
-      !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, 1))
-    return cudaErrorInvalidValue;
+  L.grouped = a.n % 128 == 0 && p.g.KR == a.ci * p.g.FP;
+  if (L.grouped) {
+    const uint64_t gdims[5] = {32, a.w, a.ci, a.n / 32, a.h};
+    const uint64_t gpitch[4] = {pitch[0], pitch[2], 128, pitch[1]};
+    const uint32_t gbox[5] = {32, p.g.FP, a.ci, 4, 1};
+    if (!make_tmap(&L.x[0], t.x_hi, 5, gdims, gpitch, gbox, nullptr, 1) ||
+        !make_tmap(&L.x[1], t.x_lo, 5, gdims, gpitch, gbox, nullptr, 1))
+      return cudaErrorInvalidValue;
+  } else {
+    const uint32_t box[4] = {32, a.fw, 1, a.ci};
+    if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, 1) ||
+        !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, 1))
+      return cudaErrorInvalidValue;
+  }
   L.g = p.g;
   L.ncols = a.ho * a.wo * a.n;
   L.bn = bn;
-  Sched sc = make_sched((L.ncols + kTcBM - 1) / kTcBM, (a.co + bn - 1) / bn, a.fh,
-                        a.precision == LCNN_PREC_3XTF32 ? 3 : 1, bn, true, false);
-  sc.a_bytes = (kTcBM / 32) * kr * 128;
-  sc.stage_bytes = (kTcBM / 32) * a.ci * a.fw * 128 + bn * kr * 4;
+  const bool x3 = a.precision == LCNN_PREC_3XTF32;
+  const uint32_t ctiles = (a.co + bn - 1) / bn;
+  Sched sc = kCoOnN ? make_sched((L.ncols + kTcBM - 1) / kTcBM, ctiles, a.fh, x3 ? 3 : 1, bn,
+                                 true, false)
+                    : make_sched(ctiles, (L.ncols + kPBN - 1) / kPBN, a.fh, x3 ? 3 : 1, kPBN,
+                                 false, true);
+  const uint32_t x_region = L.kBoxes * kr * 128;                  // input groups of KR rows
+  const uint32_t in_bytes = L.kBoxes * a.ci * (L.grouped ? p.g.FP : a.fw) * 128;  // TMA bytes
+  const uint32_t w_region = bn * kr * 4;                          // one filter row of the tile
   sc.ksteps = kr / 8;
-  if (cudaError_t e = zero_sk_region(sc, true, bn, a.dst, L.ncols, a.co, s); e != cudaSuccess)
+  // resident filter image (channels on N): one channel tile, one segment,
+  // >= 3 ring slots; LCNN_TC_PROBE bit 4 disables it
+  const uint32_t img = a.fh * w_region;
+  uint32_t slots = 0;
+  if (kCoOnN && !x3 && sc.nt == 1 && !(sc.probe & 4))
+    for (uint32_t n = kPStages; n >= 3 && !slots; --n)
+      if (1024 + n * x_region + img + 16 + sizeof(PCtl) <= kMaxDynSmem) slots = n;
+  if (slots) {
+    L.res = img;
+    sc.a_bytes = x_region;
+    sc.stage_bytes = in_bytes;
+    sched_ring(sc, slots, x_region, img);
+  } else {
+    L.res = 0;
+    sc.a_bytes = kCoOnN ? x_region : w_region;
+    sc.stage_bytes = in_bytes + w_region;
+    const uint32_t stride = (x_region + w_region + 1023) / 1024 * 1024;
+    uint32_t n = kPStages;
+    while (n > 2 && 1024 + n * stride + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
+    sched_ring(sc, n, stride, 0);
+  }
+  if (cudaError_t e = zero_sk_region(sc, kCoOnN, kCoOnN ? bn : kTcBM, a.dst, L.ncols, a.co, s);
+      e != cudaSuccess)
     return e;
-  ColsOut O{a.dst, L.ncols, a.co};
-  return launch_persistent(L, O, sc, s);
+  if constexpr (kCoOnN) {
+    ColsOut O{a.dst, L.ncols, a.co};
+    return launch_persistent(L, O, sc, s);
+  } else {
+    RowsOut O{a.dst, L.ncols, a.co, L.ncols};
+    return launch_persistent(L, O, sc, s);
+  }
 }
 
 template <bool kCoOnN>
@@ -795,15 +939,21 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
   const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
                              static_cast<uint64_t>(a.h) * a.w * a.n * 4};
-  uint32_t box[4];
-  if (p.g.mode == kModeCI) {
-    box[0] = 32; box[1] = 1; box[2] = 1; box[3] = 32;
+  const uint32_t fp = p.g.mode == kModeCI ? 1 : p.g.FP, cib = p.g.mode == kModeCI ? 32 : p.g.CIB;
+  L.grouped = a.n % 128 == 0;
+  if (L.grouped) {
+    const uint64_t gdims[5] = {32, a.w, a.ci, a.n / 32, a.h};
+    const uint64_t gpitch[4] = {pitch[0], pitch[2], 128, pitch[1]};
+    const uint32_t gbox[5] = {32, fp, cib, 4, 1};
+    if (!make_tmap(&L.x[0], t.x_hi, 5, gdims, gpitch, gbox, nullptr, 1) ||
+        !make_tmap(&L.x[1], t.x_lo, 5, gdims, gpitch, gbox, nullptr, 1))
+      return cudaErrorInvalidValue;
   } else {
-    box[0] = 32; box[1] = p.g.FP; box[2] = 1; box[3] = p.g.CIB;
+    const uint32_t box[4] = {32, fp, 1, cib};
+    if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, 1) ||
+        !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, 1))
+      return cudaErrorInvalidValue;
   }
-  if (!make_tmap(&L.x[0], t.x_hi, 4, dims, pitch, box, nullptr, 1) ||
-      !make_tmap(&L.x[1], t.x_lo, 4, dims, pitch, box, nullptr, 1))
-    return cudaErrorInvalidValue;
   L.g = p.g;
   L.ncols = a.ho * a.wo * a.n;
   const uint32_t segs = x3 ? 3 : 1;
@@ -823,66 +973,154 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   }
 }
 
-size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w, uint32_t co,
-                            uint32_t fh, uint32_t fw, int precision) {
-  // packed filters for the widest packing (WIN with FP=16, CiP rounded to 2;
-  // ROW images: channel rows rounded to the tile, <= 64 k-rows per filter row)
-  const uint64_t kmax = static_cast<uint64_t>(fh) * ((ci + 1) / 2 * 2) * 16 + fh * fw * ci;
-  const uint64_t packed = std::max<uint64_t>(uint64_t{co} * kmax, uint64_t{pack_rows(co)} * fh * 64);
-  uint64_t bytes = packed * 4 + 256;
-  if (precision == LCNN_PREC_3XTF32)
-    bytes = 2 * bytes + 2ull * n * ci * h * w * 4 + 256;
-  return bytes;
+// ---- routing, filter packing and the packed launch ------------------------
+// A convolution runs in two phases: the filters are packed into the operand
+// image of the chosen kernel (once per weight set when the caller keeps the
+// pack, e.g. a network layer), then the packed launch runs.  Packed image:
+// [hi (apack floats) | lo (apack floats, 3xTF32 only)], each 256-B aligned.
+// Run workspace (3xTF32 CHWN only): the split input copies [x_hi | x_lo].
+namespace {
+
+enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM };
+
+struct ConvRoute {
+  RouteKind kind = kRouteSimt;
+  TcPlan p;
+  uint64_t apack = 0;  // floats of one packed filter image
+  uint32_t kp = 0;     // NCHW: K padded to the k-block
+};
+
+uint64_t align_floats(uint64_t f) { return (f + 63) / 64 * 64; }  // 256 B
+
+ConvRoute route_conv(const ConvArgs& a) {
+  ConvRoute r;
+  if (a.layout == LCNN_NCHW && a.precision == LCNN_PREC_TF32 &&
+      static_cast<uint64_t>(a.n) * a.ho * a.wo < (1ull << 31)) {
+    r.kind = kRouteNchwTc;
+    const uint32_t K = a.ci * a.fh * a.fw;
+    r.kp = (K + kTcBK - 1) / kTcBK * kTcBK;
+    r.apack = static_cast<uint64_t>(a.co) * r.kp;
+    return r;
+  }
+  if (a.precision != LCNN_PREC_FP32)
+    r.p = plan_tc(a.n, a.ci, a.h, a.w, a.layout, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo);
+  if (!r.p.ok) {
+    r.kind = kRouteSimt;
+    r.apack = static_cast<uint64_t>(a.co) * a.ci * a.fh * a.fw;  // the filters as given
+    return r;
+  }
+  const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
+  if (r.p.g.mode == kModeROW) {
+    const uint32_t kr = r.p.g.KR;
+    const bool grouped = a.n % 128 == 0 && kr == a.ci * r.p.g.FP;
+    const bool on_n = choose_co_on_n(a.co, ncols, kr, grouped ? kr : a.ci * a.fw, kr * 4, grouped);
+    r.kind = on_n ? kRouteRowOnN : kRouteRowOnM;
+    r.apack = static_cast<uint64_t>(pack_rows(a.co, on_n)) * r.p.K;
+  } else {
+    r.kind = choose_co_on_n_traffic(a.co) ? kRouteChwnOnN : kRouteChwnOnM;
+    r.apack = static_cast<uint64_t>(a.co) * r.p.K;
+  }
+  return r;
 }
 
-cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
-  if (a.layout == LCNN_NCHW && a.precision == LCNN_PREC_TF32 &&
-      static_cast<uint64_t>(a.n) * a.ho * a.wo < (1ull << 31))
-    return launch_conv_nchw_tc(a, s);
-  const bool want_tc = a.precision != LCNN_PREC_FP32;
-  TcPlan p = want_tc ? plan_tc(a.n, a.ci, a.h, a.w, a.layout, a.co, a.fh, a.fw, a.stride, a.pad,
-                               a.ho, a.wo)
-                     : TcPlan{};
-  if (!p.ok) {
+bool split_input(const ConvArgs& a, const ConvRoute& r) {
+  return a.precision == LCNN_PREC_3XTF32 && r.kind != kRouteSimt && r.kind != kRouteNchwTc;
+}
+
+size_t packed_bytes(const ConvArgs& a, const ConvRoute& r) {
+  // ROW images are sized for either orientation, so a bound computed without
+  // the output extents (lcnn_conv_workspace_bytes) covers the route taken
+  uint64_t floats = r.apack;
+  if (r.kind == kRouteRowOnN || r.kind == kRouteRowOnM)
+    floats = static_cast<uint64_t>(std::max(pack_rows(a.co, true), pack_rows(a.co, false))) * r.p.K;
+  const uint64_t one = align_floats(floats);
+  return (a.precision == LCNN_PREC_3XTF32 && r.kind != kRouteSimt ? 2 : 1) * one * 4;
+}
+
+size_t run_bytes(const ConvArgs& a, const ConvRoute& r) {
+  if (!split_input(a, r)) return 0;
+  return 2 * align_floats(static_cast<uint64_t>(a.n) * a.ci * a.h * a.w) * 4;
+}
+
+}  // namespace
+
+size_t conv_packed_bytes(const ConvArgs& a) { return packed_bytes(a, route_conv(a)); }
+
+size_t conv_workspace_bytes(const ConvArgs& a) {
+  const ConvRoute r = route_conv(a);
+  return packed_bytes(a, r) + run_bytes(a, r) + 256;
+}
+
+cudaError_t launch_conv_pack(const ConvArgs& a, void* packed, cudaStream_t s) {
+  const ConvRoute r = route_conv(a);
+  float* hi = static_cast<float*>(packed);
+  float* lo = a.precision == LCNN_PREC_3XTF32 ? hi + packed_bytes(a, r) / 8 : nullptr;
+  switch (r.kind) {
+    case kRouteSimt:
+      return cudaMemcpyAsync(hi, a.filters, r.apack * 4, cudaMemcpyDeviceToDevice, s);
+    case kRouteNchwTc: {
+      ConvGeomTc g{a.n, a.ci, a.h, a.w, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo,
+                   kModeNAT, 0, 0, 0};
+      pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, nullptr, g, r.kp);
+      break;
+    }
+    case kRouteRowOnN:
+    case kRouteRowOnM:
+      pack_filters_row_kernel<<<148 * 4, 256, 0, s>>>(
+          a.filters, hi, lo, r.p.g, r.kind == kRouteRowOnN ? co_tile_n(a.co) : kTcBM, r.apack);
+      break;
+    default:
+      pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, lo, r.p.g, r.p.K);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream_t s) {
+  const ConvRoute r = route_conv(a);
+  const float* w_hi = static_cast<const float*>(packed);
+  const float* w_lo = a.precision == LCNN_PREC_3XTF32 ? w_hi + packed_bytes(a, r) / 8 : w_hi;
+  if (r.kind == kRouteSimt) {
     ConvGeomSimt g{a.n, a.ci, a.h, a.w, a.co, a.fh, a.fw, a.stride, a.pad, a.ho, a.wo};
     const uint64_t total = static_cast<uint64_t>(a.n) * a.co * a.ho * a.wo;
     uint64_t blocks = (total + 255) / 256;
     if (blocks > 148ull * 32) blocks = 148ull * 32;
+    if (blocks == 0) blocks = 1;
     if (a.layout == LCNN_CHWN)
-      conv_chwn_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, a.filters,
-                                                                          a.dst, g);
+      conv_chwn_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, w_hi, a.dst, g);
     else
-      conv_nchw_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, a.filters,
-                                                                          a.dst, g);
+      conv_nchw_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, w_hi, a.dst, g);
     return cudaGetLastError();
   }
-  const bool x3 = a.precision == LCNN_PREC_3XTF32;
-  float* ws = static_cast<float*>(a.workspace);
-  // packed filter count: [co][K], or the ROW image [co tiles * bn][K]
-  const uint64_t apack = static_cast<uint64_t>(p.g.mode == kModeROW ? pack_rows(a.co) : a.co) * p.K;
-  float* a_hi = ws;
-  float* a_lo = x3 ? a_hi + apack : nullptr;
-  const float* b_hi = a.src;
-  const float* b_lo = a.src;
-  if (x3) {
-    float* bh = a_lo + apack;
-    bh = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(bh) + 255) & ~uintptr_t(255));
+  if (r.kind == kRouteNchwTc) return launch_conv_nchw_tc(a, w_hi, r.kp, s);
+  const float* x_hi = a.src;
+  const float* x_lo = a.src;
+  if (split_input(a, r)) {
     const uint64_t nx = static_cast<uint64_t>(a.n) * a.ci * a.h * a.w;
-    float* bl = bh + nx;
-    bl = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(bl) + 255) & ~uintptr_t(255));
+    float* bh = reinterpret_cast<float*>(
+        (reinterpret_cast<uintptr_t>(a.workspace) + 255) & ~uintptr_t(255));
+    float* bl = bh + align_floats(nx);
     cudaError_t e = launch_split_hilo(a.src, bh, bl, nx, s);
     if (e != cudaSuccess) return e;
-    b_hi = bh;
-    b_lo = bl;
+    x_hi = bh;
+    x_lo = bl;
   }
-  ConvTcArgs t{a, p, a_hi, x3 ? a_lo : a_hi, b_hi, b_lo};
-  if (p.g.mode == kModeROW) {
-    pack_filters_row_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, co_tile_n(a.co),
-                                                    apack);
-    return launch_chwn_row(t, s);
-  }
-  pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, a_hi, a_lo, p.g, p.K);
-  return choose_co_on_n(a.co) ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
+  ConvTcArgs t{a, r.p, w_hi, w_lo, x_hi, x_lo};
+  if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
+  if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
+  return r.kind == kRouteChwnOnN ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
+}
+
+// One-shot form: pack into the front of the workspace, run with the rest.
+cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
+  const ConvRoute r = route_conv(a);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(a.workspace) + 255) & ~uintptr_t(255));
+  cudaError_t e = launch_conv_pack(a, ws, s);
+  if (e != cudaSuccess) return e;
+  ConvArgs b = a;
+  b.workspace = ws + packed_bytes(a, r);
+  return launch_conv_packed(b, ws, s);
 }
 
 }  // namespace lcnn_impl

@@ -38,6 +38,11 @@ using namespace lcnn_tc;
 struct GemmLoader {
   CUtensorMap a[2];
   CUtensorMap b[2];
+  // grouped B (n % 32 == 0): one 3D box {32 n, 32 k, 8 groups} per stage over
+  // the view {32, k, n/32} whose group stride (128 B) is smaller than the row
+  // pitch -- it lands exactly as the 8 MN-major 32-column atoms, replacing 8
+  // 2D boxes (TMA cost is mostly per box: scripts/tma_bench.cu)
+  bool grouped;
   static constexpr bool kZeroSmem = false;
   static constexpr int kSteps = kTcBK / 8;
   __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
@@ -50,6 +55,9 @@ struct GemmLoader {
     tma_prefetch(&a[0]);
     tma_prefetch(&b[0]);
   }
+  __device__ uint32_t resident_bytes() const { return 0; }
+  __device__ void load_resident(void*, uint64_t*) const {}
+  __device__ uint32_t resident_offset(uint32_t) const { return 0; }
   struct State {
     uint32_t m0, n0;
   };
@@ -59,9 +67,13 @@ struct GemmLoader {
     const CUtensorMap* am = &a[seg == 2 ? 1 : 0];
     const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
     tma_load_2d(sa, am, bar, k * kTcBK, st.m0);
+    if (grouped) {
+      tma_load_3d(sb, bm, bar, 0, k * kTcBK, st.n0 / 32);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kPBN / 32; ++j)
-      tma_load_2d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, st.n0 + 32 * j, k * kTcBK);
+      for (int j = 0; j < kPBN / 32; ++j)
+        tma_load_2d(static_cast<uint8_t*>(sb) + j * 4096, bm, bar, st.n0 + 32 * j, k * kTcBK);
+    }
   }
 };
 
@@ -250,10 +262,20 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
     a0 = ahi; a1 = alo; b0 = bhi; b1 = blo;
   }
   if (!make_tmap_2d(&L.a[0], a0, k, m, k * 4, kTcBK, kTcBM, false) ||
-      !make_tmap_2d(&L.a[1], a1, k, m, k * 4, kTcBK, kTcBM, false) ||
-      !make_tmap_2d(&L.b[0], b0, n, k, n * 4, 32, kTcBK, true) ||
-      !make_tmap_2d(&L.b[1], b1, n, k, n * 4, 32, kTcBK, true))
+      !make_tmap_2d(&L.a[1], a1, k, m, k * 4, kTcBK, kTcBM, false))
     return cudaErrorInvalidValue;
+  L.grouped = n % 32 == 0;
+  if (L.grouped) {
+    const uint64_t dims[3] = {32, k, n / 32};
+    const uint64_t pitch[2] = {n * 4, 128};
+    const uint32_t box[3] = {32, kTcBK, kPBN / 32};
+    if (!make_tmap(&L.b[0], b0, 3, dims, pitch, box, nullptr, 1) ||
+        !make_tmap(&L.b[1], b1, 3, dims, pitch, box, nullptr, 1))
+      return cudaErrorInvalidValue;
+  } else if (!make_tmap_2d(&L.b[0], b0, n, k, n * 4, 32, kTcBK, true) ||
+             !make_tmap_2d(&L.b[1], b1, n, k, n * 4, 32, kTcBK, true)) {
+    return cudaErrorInvalidValue;
+  }
   Sched sc = make_sched(static_cast<uint32_t>((m + kTcBM - 1) / kTcBM),
                         static_cast<uint32_t>((n + kPBN - 1) / kPBN),
                         static_cast<uint32_t>((k + kTcBK - 1) / kTcBK),

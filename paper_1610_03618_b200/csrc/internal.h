@@ -57,8 +57,14 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s);
 cudaError_t launch_conv_oracle(const ConvArgs& a, uint64_t sn, uint64_t sc, uint64_t sh,
                                uint64_t sw, cudaStream_t s);
 cudaError_t launch_im2col(const ConvArgs& a, cudaStream_t s);
-size_t conv_workspace_bytes(uint32_t n, uint32_t ci, uint32_t h, uint32_t w,
-                            uint32_t co, uint32_t fh, uint32_t fw, int precision);
+// Workspace of the one-shot launch_conv (packed filters + run workspace).
+size_t conv_workspace_bytes(const ConvArgs& a);
+// Filter pre-packing: bytes of the packed operand image of a's route, the
+// pack itself (a.filters -> packed), and the launch on packed filters
+// (a.workspace: the run workspace, conv_workspace_bytes - conv_packed_bytes).
+size_t conv_packed_bytes(const ConvArgs& a);
+cudaError_t launch_conv_pack(const ConvArgs& a, void* packed, cudaStream_t s);
+cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream_t s);
 bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a,
                        const void* b);
 size_t gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k, int precision);

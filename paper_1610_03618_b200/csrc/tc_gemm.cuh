@@ -55,6 +55,9 @@ struct TcCtl {
 //             uint64_t* bar) const;         // issues TMA, Sched::stage_bytes
 //   uint64_t desc_a(const uint8_t* sa, int step) const;  // MMA smem descriptors
 //   uint64_t desc_b(const uint8_t* sb, int step) const;  //   of K-step `step`
+//   uint32_t resident_bytes() const;        // > 0: B is resident in smem, loaded
+//   void load_resident(void* dst, uint64_t* bar) const;  //   once per CTA, and
+//   uint32_t resident_offset(uint32_t kb) const;  //  k-block kb's B slice
 //   static constexpr bool kZeroSmem;  // stages carry never-loaded zero rows
 //   static constexpr int kSteps;      // K-steps per stage, 0 = Sched::ksteps
 // Segments chain operand sets into one accumulator (3 for 3xTF32).
@@ -64,15 +67,17 @@ struct TcCtl {
 constexpr int kPBN = 256, kPStages = 4;
 constexpr uint32_t kPBBytes = kTcBK * kPBN * 4;            // 32 KB
 constexpr uint32_t kPStageBytes = kTcABytes + kPBBytes;    // 48 KB
-constexpr size_t kPSmem = 1024 + kPStages * kPStageBytes + 256;
 
 struct PCtl {
   uint64_t full[kPStages];
   uint64_t empty[kPStages];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  uint64_t bres;  // resident B operand landed (Loader::resident_bytes() > 0)
   uint32_t tmem_addr;
 };
+// dynamic shared memory a CTA may opt into on sm_100
+constexpr uint32_t kMaxDynSmem = 232448;
 
 // Tile schedule: data-parallel waves of whole tiles, then "stream-K" for the
 // ragged last wave.  With T tiles on G resident CTAs, the first
@@ -101,7 +106,20 @@ struct Sched {
   uint32_t a_bytes;      // offset of the B operand inside a stage
   uint32_t ksteps;       // MMA K-steps (8 tf32 each) per stage
   uint32_t probe;        // profiling knob (LCNN_TC_PROBE): 1 = no MMAs, 2 = no stores
+  // shared-memory carve-up: a ring of `stages` slots of `stage_stride` bytes,
+  // then (optionally) the resident B operand at `resident_off`, then PCtl at
+  // `ctl_off`; `smem_bytes` is the dynamic allocation (+1 KB for alignment)
+  uint32_t stages, stage_stride, resident_off, ctl_off, smem_bytes;
 };
+
+// Default carve-up: kPStages slots of kPStageBytes, no resident operand.
+inline void sched_ring(Sched& s, uint32_t stages, uint32_t stride, uint32_t resident_bytes) {
+  s.stages = stages;
+  s.stage_stride = stride;
+  s.resident_off = stages * stride;
+  s.ctl_off = (s.resident_off + resident_bytes + 15) / 16 * 16;
+  s.smem_bytes = 1024 + s.ctl_off + static_cast<uint32_t>(sizeof(PCtl));
+}
 
 inline int tc_sm_count() {
   static int sms = 0;
@@ -150,6 +168,7 @@ inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, u
   }
   const uint32_t dp_grid = s.dp_tiles < g ? s.dp_tiles : g;
   s.grid = dp_grid > s.sk_ctas ? dp_grid : s.sk_ctas;
+  sched_ring(s, kPStages, kPStageBytes, 0);
   return s;
 }
 
@@ -184,24 +203,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   extern __shared__ uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
-  PCtl* ctl = reinterpret_cast<PCtl*>(smem + kPStages * kPStageBytes);
+  PCtl* ctl = reinterpret_cast<PCtl*>(smem + sc.ctl_off);
+  const uint32_t nst = sc.stages;
+  const uint32_t res_bytes = ld.resident_bytes();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if constexpr (Loader::kZeroSmem) {
     // K padding rows that no TMA box ever writes must read as zeros
     float4* z = reinterpret_cast<float4*>(smem);
-    for (uint32_t i = threadIdx.x; i < kPStages * kPStageBytes / 16; i += blockDim.x)
+    for (uint32_t i = threadIdx.x; i < sc.ctl_off / 16; i += blockDim.x)
       z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0) {
     if (lane == 0) {
       ld.prefetch();
-      for (int s = 0; s < kPStages; ++s) {
+      for (uint32_t s = 0; s < nst; ++s) {
         mbar_init(&ctl->full[s], 1);
         mbar_init(&ctl->empty[s], 1);
       }
+      mbar_init(&ctl->bres, 1);
       for (int a = 0; a < 2; ++a) {
         mbar_init(&ctl->tfull[a], 1);
         mbar_init(&ctl->tempty[a], 4);  // one arrive per epilogue warp
@@ -218,6 +240,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
+    if (res_bytes) {  // the B operand every tile of this CTA uses, loaded once
+      mbar_arrive_expect_tx(&ctl->bres, res_bytes);
+      ld.load_resident(smem + sc.resident_off, &ctl->bres);
+    }
     uint32_t s = 0, phase = 0;
     for_each_work(sc, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
       const uint32_t ntile = t / sc.mt;
@@ -226,14 +252,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
       for (uint32_t it = kbeg; it < kend; ++it) {
         mbar_wait(&ctl->empty[s], phase ^ 1);
-        uint8_t* sa = smem + s * kPStageBytes;
+        uint8_t* sa = smem + s * sc.stage_stride;
         mbar_arrive_expect_tx(&ctl->full[s], sc.stage_bytes);
         ld.load(st, seg, kb, sa, sa + sc.a_bytes, &ctl->full[s]);
         if (++kb == sc.kbn) {
           kb = 0;
           ++seg;
         }
-        if (++s == kPStages) {
+        if (++s == nst) {
           s = 0;
           phase ^= 1;
         }
@@ -243,6 +269,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = sc.idesc;
     uint32_t s = 0, phase = 0, local = 0;
+    if (res_bytes) {
+      mbar_wait(&ctl->bres, 0);
+      tc_fence_after();
+    }
     for_each_work(sc, [&](uint32_t, uint32_t kbeg, uint32_t kend, bool) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
       ++local;
@@ -252,8 +282,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (uint32_t it = kbeg; it < kend; ++it) {
         mbar_wait(&ctl->full[s], phase);
         tc_fence_after();
-        const uint8_t* sa = smem + s * kPStageBytes;
-        const uint8_t* sb = sa + sc.a_bytes;
+        const uint8_t* sa = smem + s * sc.stage_stride;
+        // resident B: the slice of k-block `it` (single segment when resident)
+        const uint8_t* sb = res_bytes ? smem + sc.resident_off + ld.resident_offset(it % sc.kbn)
+                                      : sa + sc.a_bytes;
         if (sc.probe & 1) {
         } else if constexpr (Loader::kSteps > 0) {
 #pragma unroll
@@ -265,7 +297,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mma_tf32(acc, ld.desc_a(sa, k), ld.desc_b(sb, k), idesc, (it != kbeg) || (k != 0));
         }
         tc_commit(&ctl->empty[s]);
-        if (++s == kPStages) {
+        if (++s == nst) {
           s = 0;
           phase ^= 1;
         }
@@ -338,11 +370,13 @@ cudaError_t launch_persistent(const Loader& ld, const Out& out, const Sched& sc,
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kPSmem));
+                                         static_cast<int>(kMaxDynSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<sc.grid, kTcThreads, kPSmem, s>>>(ld, out, sc);
+  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStages)
+    return cudaErrorInvalidConfiguration;
+  kern<<<sc.grid, kTcThreads, sc.smem_bytes, s>>>(ld, out, sc);
   return cudaGetLastError();
 }
 

@@ -43,4 +43,17 @@ DeviceTensor4D conv_forward(const DeviceTensor4D& in, const float* d_filters,
                             std::uint32_t f_w, const ConvParams& p,
                             int precision);
 
+// The two phases of conv_forward for weights that are reused (network
+// layers): the filters packed once into the operand image of the kernel this
+// input geometry + precision routes to (lcnn_conv_pack_filters), and the
+// convolution on that image (lcnn_conv_forward_packed) -- bit-identical to
+// conv_forward on the same filters.
+std::shared_ptr<DeviceBuffer> pack_conv_filters(const DeviceTensor4D& in, const float* d_filters,
+                                                std::uint32_t c_o, std::uint32_t f_h,
+                                                std::uint32_t f_w, const ConvParams& p,
+                                                int precision);
+DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packed,
+                                   std::uint32_t c_o, std::uint32_t f_h, std::uint32_t f_w,
+                                   const ConvParams& p, int precision);
+
 }  // namespace lcnn

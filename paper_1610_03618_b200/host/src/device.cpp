@@ -127,10 +127,12 @@ void* current_stream() {
 }
 
 void set_current_stream(void* stream) {
+  ThreadContext& c = ctx();
+  if (c.external == static_cast<cudaStream_t>(stream)) return;  // no change: stay async
   // drain the stream being left: pooled blocks freed on it may be reused on
   // the new one
   synchronize();
-  ctx().external = static_cast<cudaStream_t>(stream);
+  c.external = static_cast<cudaStream_t>(stream);
 }
 
 void synchronize() {

@@ -58,6 +58,10 @@ int status_of_current() {
 
 lcnn::Layout L(int code) { return static_cast<lcnn::Layout>(code); }
 
+// The ABI's stream argument is a cudaStream_t: 0 is the legacy default
+// stream (CUDA's convention), not the library's private stream.
+void* abi_stream(void* stream) { return stream ? stream : static_cast<void*>(cudaStreamLegacy); }
+
 }  // namespace
 
 extern "C" {
@@ -110,7 +114,7 @@ int lcnn_net_layouts(const lcnn_net* net, int* layouts, uint32_t max_layers) {
 int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout, float* d_output,
                      void* stream) {
   NET_GUARD({
-    lcnn::set_current_stream(stream);
+    lcnn::set_current_stream(abi_stream(stream));
     const lcnn::NetworkSpec& s = net->net->spec();
     const lcnn::DeviceTensor4D in = lcnn::DeviceTensor4D::wrap(const_cast<float*>(d_input), s.n,
                                                                s.c, s.h, s.w, L(in_layout));
@@ -140,11 +144,63 @@ int lcnn_net_forward_host(const lcnn_net* net, const float* h_input, int in_layo
   })
 }
 
+int lcnn_net_forward_host_many(const lcnn_net* net, const float* const* h_inputs, int in_layout,
+                               float* const* h_outputs, uint32_t count) {
+  struct Streams {  // copy stream + per-slot events, released on every exit path
+    cudaStream_t copy = nullptr;
+    cudaEvent_t loaded[2] = {}, consumed[2] = {};
+    ~Streams() {
+      for (int b = 0; b < 2; ++b) {
+        if (loaded[b]) cudaEventDestroy(loaded[b]);
+        if (consumed[b]) cudaEventDestroy(consumed[b]);
+      }
+      if (copy) cudaStreamDestroy(copy);
+    }
+  };
+  auto ck = [](cudaError_t e) {
+    if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+  };
+  NET_GUARD({
+    if (count && (!h_inputs || !h_outputs)) throw lcnn::ValidationError("null buffer array");
+    lcnn::set_current_stream(nullptr);
+    const lcnn::NetworkSpec& s = net->net->spec();
+    cudaStream_t st = static_cast<cudaStream_t>(lcnn::current_stream());
+    Streams r;
+    ck(cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      ck(cudaEventCreateWithFlags(&r.loaded[b], cudaEventDisableTiming));
+      ck(cudaEventCreateWithFlags(&r.consumed[b], cudaEventDisableTiming));
+    }
+    lcnn::DeviceTensor4D in[2] = {lcnn::DeviceTensor4D(s.n, s.c, s.h, s.w, L(in_layout)),
+                                  lcnn::DeviceTensor4D(s.n, s.c, s.h, s.w, L(in_layout))};
+    // the slots were allocated on the compute stream: the copy stream waits
+    // for that before its first write
+    for (int b = 0; b < 2; ++b) {
+      ck(cudaEventRecord(r.consumed[b], st));
+      ck(cudaStreamWaitEvent(r.copy, r.consumed[b], 0));
+    }
+    const std::size_t in_bytes = in[0].size() * sizeof(float);
+    for (uint32_t i = 0; i < count; ++i) {
+      const int b = static_cast<int>(i & 1);
+      ck(cudaStreamWaitEvent(r.copy, r.consumed[b], 0));  // forward i-2 is done with slot b
+      ck(cudaMemcpyAsync(in[b].data(), h_inputs[i], in_bytes, cudaMemcpyHostToDevice, r.copy));
+      ck(cudaEventRecord(r.loaded[b], r.copy));
+      ck(cudaStreamWaitEvent(st, r.loaded[b], 0));
+      const lcnn::DeviceMatrix out = net->net->forward(in[b]);
+      ck(cudaEventRecord(r.consumed[b], st));
+      ck(cudaMemcpyAsync(h_outputs[i], out.data(), std::size_t{out.rows} * out.cols * sizeof(float),
+                         cudaMemcpyDeviceToHost, st));
+    }
+    lcnn::synchronize();
+    ck(cudaStreamSynchronize(r.copy));
+  })
+}
+
 int lcnn_net_profile(const lcnn_net* net, const float* d_input, int in_layout, void* stream,
                      uint64_t* nanos, uint32_t max_entries, char* names, size_t names_len,
                      uint32_t* count) {
   NET_GUARD({
-    lcnn::set_current_stream(stream);
+    lcnn::set_current_stream(abi_stream(stream));
     const lcnn::NetworkSpec& s = net->net->spec();
     const lcnn::DeviceTensor4D in = lcnn::DeviceTensor4D::wrap(const_cast<float*>(d_input), s.n,
                                                                s.c, s.h, s.w, L(in_layout));

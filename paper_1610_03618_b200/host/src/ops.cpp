@@ -349,6 +349,40 @@ DeviceTensor4D conv_forward(const DeviceTensor4D& in, const float* d_filters, st
   return out;
 }
 
+std::shared_ptr<DeviceBuffer> pack_conv_filters(const DeviceTensor4D& in, const float* d_filters,
+                                                std::uint32_t c_o, std::uint32_t f_h,
+                                                std::uint32_t f_w, const ConvParams& p,
+                                                int precision) {
+  conv_output_extents(in.h(), in.w(), f_h, f_w, p);
+  const std::size_t bytes = lcnn_conv_packed_bytes(in.n(), in.c(), in.h(), in.w(), code(in.layout()),
+                                                   c_o, f_h, f_w, p.stride, p.pad, precision);
+  auto buf = std::make_shared<DeviceBuffer>(bytes ? bytes : 256);
+  check_status(lcnn_conv_pack_filters(d_filters, buf->get(), buf->bytes(), in.n(), in.c(), in.h(),
+                                      in.w(), code(in.layout()), c_o, f_h, f_w, p.stride, p.pad,
+                                      precision, current_stream()));
+  return buf;
+}
+
+DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packed,
+                                   std::uint32_t c_o, std::uint32_t f_h, std::uint32_t f_w,
+                                   const ConvParams& p, int precision) {
+  const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f_h, f_w, p);
+  DeviceTensor4D out(in.n(), c_o, ho, wo, in.layout());
+  const std::size_t ws = lcnn_conv_packed_workspace_bytes(
+      in.n(), in.c(), in.h(), in.w(), code(in.layout()), c_o, f_h, f_w, p.stride, p.pad, precision);
+  void* wsp = nullptr;
+  std::size_t wsb = 0;
+  if (ws) {
+    DeviceBuffer& buf = scratch(ws + 16);
+    wsp = buf.get();
+    wsb = buf.bytes();
+  }
+  check_status(lcnn_conv_forward_packed(in.data(), d_packed, out.data(), in.n(), in.c(), in.h(),
+                                        in.w(), code(in.layout()), c_o, f_h, f_w, p.stride, p.pad,
+                                        precision, wsp, wsb, current_stream()));
+  return out;
+}
+
 Tensor4D conv_oracle(const Tensor4D& in, const FilterBank& f, const ConvParams& p) {
   check_conv_inputs(in, f);
   const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f.f_h(), f.f_w(), p);

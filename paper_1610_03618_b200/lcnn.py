@@ -344,6 +344,39 @@ def conv_forward(x: DeviceTensor4D, filters, c_o, f_h, f_w, stride=1, pad=0, pre
     return out
 
 
+def pack_conv_filters(x: DeviceTensor4D, filters, c_o, f_h, f_w, stride=1, pad=0,
+                      precision=FP32, stream=None):
+    """The filters packed into the operand image of the kernel x's geometry
+    routes to (lcnn_conv_pack_filters) -> a CUDA uint8 tensor."""
+    torch = _torch()
+    geo = (x.n, x.c, x.h, x.w, x.layout, c_o, f_h, f_w, stride, pad, precision)
+    nbytes = capi.lib().lcnn_conv_packed_bytes(*geo)
+    if nbytes == 0:
+        conv_output_extents(x.h, x.w, f_h, f_w, stride, pad)  # raises the geometry error
+        raise ValueError("conv: no packed image for this geometry")
+    packed = torch.empty(nbytes, dtype=torch.uint8, device=x.data.device)
+    capi.call("lcnn_conv_pack_filters", filters.data_ptr(), packed.data_ptr(), nbytes, *geo,
+              _stream(stream))
+    return packed
+
+
+def conv_forward_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride=1, pad=0,
+                        precision=FP32, out=None, stream=None) -> DeviceTensor4D:
+    """conv_forward on filters made by pack_conv_filters for this geometry."""
+    torch = _torch()
+    ho, wo = conv_output_extents(x.h, x.w, f_h, f_w, stride, pad)
+    if out is None:
+        out = DeviceTensor4D(x.n, c_o, ho, wo, x.layout,
+                             torch.empty(x.n * c_o * ho * wo, dtype=torch.float32,
+                                         device=x.data.device))
+    geo = (x.n, x.c, x.h, x.w, x.layout, c_o, f_h, f_w, stride, pad, precision)
+    nbytes = capi.lib().lcnn_conv_packed_workspace_bytes(*geo)
+    ws = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32, device=x.data.device)
+    capi.call("lcnn_conv_forward_packed", x.ptr(), packed.data_ptr(), out.ptr(), *geo,
+              ws.data_ptr(), ws.numel() * 4, _stream(stream))
+    return out
+
+
 def gemm(a, b, m, n, k, precision=FP32, out=None, workspace=None, stream=None):
     """c (m x n) = a (m x k) * b (k x n), row-major fp32 CUDA tensors
     (gemm_blocked conv.cpp:252-304 / fc_forward softmax.cpp:182-184)."""
@@ -358,7 +391,8 @@ def gemm(a, b, m, n, k, precision=FP32, out=None, workspace=None, stream=None):
     return out
 
 
-__all__ = ["TF32", "X3TF32", "FP32", "conv_forward", "gemm", "conv_output_extents",
+__all__ = ["TF32", "X3TF32", "FP32", "conv_forward", "gemm", "pack_conv_filters",
+    "conv_forward_packed", "conv_output_extents",
     "NCHW", "CHWN", "NHWC", "HWCN", "MAX", "AVERAGE", "DeviceTensor4D", "DeviceMatrix",
     "TransformPlan", "PoolParams", "CoarseningPlan", "AccessReport", "PassReport",
     "flattenable_pair", "make_plan", "transform", "transform_tiled", "transform_naive",

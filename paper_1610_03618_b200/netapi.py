@@ -29,6 +29,8 @@ def lib():
         d.lcnn_net_layouts.argtypes = [c_void_p, POINTER(c_int), c_uint32]
         d.lcnn_net_forward.argtypes = [c_void_p, c_void_p, c_int, c_void_p, c_void_p]
         d.lcnn_net_forward_host.argtypes = [c_void_p, c_void_p, c_int, c_void_p]
+        d.lcnn_net_forward_host_many.argtypes = [c_void_p, POINTER(c_void_p), c_int,
+                                                 POINTER(c_void_p), c_uint32]
         d.lcnn_set_dense_precision.argtypes = [c_int]
         d.lcnn_net_profile.argtypes = [c_void_p, c_void_p, c_int, c_void_p, POINTER(c_uint64),
                                        c_uint32, c_char_p, ctypes.c_size_t, POINTER(c_uint32)]
@@ -69,6 +71,16 @@ class Network:
 
     def forward_host(self, h_input: int, in_layout: int, h_output: int):
         _check(lib().lcnn_net_forward_host(self._h, h_input, in_layout, h_output))
+
+    def forward_host_many(self, h_inputs, in_layout: int, h_outputs):
+        """Pipelined forwards over host buffers (pointer lists of equal length):
+        batch i+1's H2D overlaps batch i's forward."""
+        if len(h_inputs) != len(h_outputs):
+            raise ValueError("h_inputs and h_outputs differ in length")
+        n = len(h_inputs)
+        ins = (c_void_p * max(n, 1))(*h_inputs)
+        outs = (c_void_p * max(n, 1))(*h_outputs)
+        _check(lib().lcnn_net_forward_host_many(self._h, ins, in_layout, outs, n))
 
     def profile(self, d_input: int, in_layout: int, stream: int):
         """[(entry name, device nanoseconds)] of one forward."""

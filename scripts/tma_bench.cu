@@ -1,0 +1,413 @@
+// TMA delivery microbenchmark (sm_100a): how many bytes per second the
+// tensor-memory accelerator moves into shared memory for the box shapes the
+// implicit-GEMM convolutions use.  One CTA per SM; thread 0 issues the boxes
+// of a stage into a 4-deep ring (mbarrier complete_tx), thread 32 "consumes"
+// each stage as soon as it lands.  No MMA, no stores: pure operand delivery.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/tma_bench scripts/tma_bench.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <vector>
+
+#define CK(x)                                                              \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess) {                                               \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      exit(1);                                                             \
+    }                                                                      \
+  } while (0)
+
+constexpr int kStages = 4;
+constexpr int kMaxBoxes = 16;
+
+struct Cfg {
+  CUtensorMap map;
+  int rank;
+  int nbox;               // boxes per stage
+  uint32_t box_bytes;     // bytes one box writes
+  int32_t start[kMaxBoxes][5];  // coordinates of box j at iteration 0
+  int32_t step[5];        // per-iteration coordinate advance (wrapped by `wrap`)
+  int32_t wrap[5];        // coordinate wraps (0 = none)
+  int32_t cta_step[5];    // per-CTA offset
+  int iters;
+};
+
+__device__ __forceinline__ uint32_t sa(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int RANK, int NBOX>
+__global__ void __launch_bounds__(64, 1) tma_kernel(const __grid_constant__ Cfg c, uint64_t* sink) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kStages], empty[kStages];
+  const uint32_t stage_bytes = c.nbox * c.box_bytes;
+  const uint32_t stride = (stage_bytes + 1023) / 1024 * 1024;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // coordinates advance incrementally (one compare per dimension per box),
+    // so the issuing thread is never the bottleneck being measured
+    int32_t x[NBOX][5];
+#pragma unroll
+    for (int j = 0; j < NBOX; ++j)
+#pragma unroll
+      for (int d = 0; d < 5; ++d) {
+        int32_t v = c.start[j][d] + c.cta_step[d] * static_cast<int32_t>(blockIdx.x);
+        if (c.wrap[d]) v %= c.wrap[d];
+        x[j][d] = v;
+      }
+    const CUtensorMap* map = &c.map;
+    int s = 0, ph = 0;
+    for (int it = 0; it < c.iters; ++it) {
+      asm volatile(
+          "{\n.reg .pred p;\nW0:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W0;\n}\n" ::"r"(
+              sa(&empty[s])),
+          "r"(ph ^ 1)
+          : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])),
+                   "r"(stage_bytes)
+                   : "memory");
+      uint8_t* dst = smem + s * stride;
+#pragma unroll
+      for (int j = 0; j < NBOX; ++j, dst += c.box_bytes) {
+        int32_t* v = x[j];
+        if (RANK == 2)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+                  sa(dst)),
+              "l"(map), "r"(sa(&full[s])), "r"(v[0]), "r"(v[1])
+              : "memory");
+        else if (RANK == 3)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                  sa(dst)),
+              "l"(map), "r"(sa(&full[s])), "r"(v[0]), "r"(v[1]), "r"(v[2])
+              : "memory");
+        else if (RANK == 4)
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+                  sa(dst)),
+              "l"(map), "r"(sa(&full[s])), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+              : "memory");
+        else
+          asm volatile(
+              "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(
+                  sa(dst)),
+              "l"(map), "r"(sa(&full[s])), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4])
+              : "memory");
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          v[d] += c.step[d];
+          if (c.wrap[d] && v[d] >= c.wrap[d]) v[d] -= c.wrap[d];
+        }
+      }
+      if (++s == kStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    int s = 0, ph = 0;
+    uint64_t acc = 0;
+    for (int it = 0; it < c.iters; ++it) {
+      asm volatile(
+          "{\n.reg .pred p;\nW1:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W1;\n}\n" ::"r"(
+              sa(&full[s])),
+          "r"(ph)
+          : "memory");
+      acc += smem[s * stride + (it & 127)];
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[s])) : "memory");
+      if (++s == kStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    if (acc == 0x123456789ull) sink[blockIdx.x] = acc;
+  }
+}
+
+static bool encode(CUtensorMap* m, void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                   const uint32_t* box, CUtensorMapSwizzle sw) {
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i + 1 < rank) st[i] = strides_bytes[i];
+  }
+  CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, base, d, st, b, e,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) printf("encode failed %d\n", (int)r);
+  return r == CUDA_SUCCESS;
+}
+
+typedef void (*KernFn)(Cfg, uint64_t*);
+
+template <int R>
+KernFn pick_nbox(int n) {
+  switch (n) {
+    case 1: return tma_kernel<R, 1>;
+    case 2: return tma_kernel<R, 2>;
+    case 4: return tma_kernel<R, 4>;
+    case 8: return tma_kernel<R, 8>;
+    default: return tma_kernel<R, 12>;
+  }
+}
+
+static void run(const char* name, Cfg& c, uint64_t* sink) {
+  const uint32_t stage = c.nbox * c.box_bytes;
+  const uint32_t stride = (stage + 1023) / 1024 * 1024;
+  const size_t smem = kStages * stride + 1024;
+  KernFn k = c.rank == 2 ? pick_nbox<2>(c.nbox)
+             : (c.rank == 3 ? pick_nbox<3>(c.nbox)
+                            : (c.rank == 4 ? pick_nbox<4>(c.nbox) : pick_nbox<5>(c.nbox)));
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int rep = 0; rep < 2; ++rep) k<<<148, 64, smem>>>(c, sink);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  const int reps = 5;
+  for (int rep = 0; rep < reps; ++rep) k<<<148, 64, smem>>>(c, sink);
+  cudaEventRecord(b);
+  CK(cudaEventSynchronize(b));
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= reps;
+  const double bytes = 148.0 * c.iters * stage;
+  const double gbs = bytes / (ms * 1e6);
+  printf("%-44s stage %6u B  %8.3f ms  %8.1f GB/s  %6.1f B/clk/SM  %7.1f ns/stage\n", name, stage, ms,
+         gbs, gbs * 1e9 / 148 / 1.965e9, ms * 1e6 / c.iters);
+}
+
+int main() {
+  uint64_t* sink;
+  CK(cudaMalloc(&sink, 148 * 8));
+  // conv1 input, CHWN: N=128, W=H=227, C=3 (79 MB, L2-resident after warm-up)
+  const uint64_t N = 128, W = 227, H = 227, C = 3;
+  float* x;
+  CK(cudaMalloc(&x, N * W * H * C * 4 + 4096));
+  CK(cudaMemset(x, 0, N * W * H * C * 4));
+  const int iters = 2000;
+  auto zero = [](Cfg& c) { memset(&c, 0, sizeof(c)); };
+
+  // A: the conv1 ROW box {32 n, 11 w, 1 h, 3 c}, 4 n-groups per stage, walks (ow, oh)
+  for (int swz = 0; swz < 3; ++swz) {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[4] = {N, W, H, C};
+    const uint64_t str[3] = {N * 4, W * N * 4, H * W * N * 4};
+    const uint32_t box[4] = {32, 11, 1, 3};
+    CUtensorMapSwizzle sw = swz == 0 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                     : (swz == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+    encode(&c.map, x, 4, dims, str, box, sw);
+    c.rank = 4;
+    c.nbox = 4;
+    c.box_bytes = 32 * 11 * 3 * 4;
+    for (int j = 0; j < 4; ++j) c.start[j][0] = 32 * j;
+    c.step[1] = 4; c.wrap[1] = 216;   // ow * 4
+    c.step[2] = 1; c.wrap[2] = 216;   // oh*4+fh
+    c.cta_step[1] = 4; c.cta_step[2] = 1;
+    c.iters = iters;
+    run(swz == 0 ? "conv1 box{32,11,1,3} x4  ATOM_32B" : (swz == 1 ? "conv1 box{32,11,1,3} x4  SW128" : "conv1 box{32,11,1,3} x4  NONE"), c, sink);
+  }
+  // B: per channel boxes {32, 11, 1, 1} x 3 c x 4 n
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[4] = {N, W, H, C};
+    const uint64_t str[3] = {N * 4, W * N * 4, H * W * N * 4};
+    const uint32_t box[4] = {32, 11, 1, 1};
+    encode(&c.map, x, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    c.rank = 4;
+    c.nbox = 12;
+    c.box_bytes = 32 * 11 * 4;
+    for (int j = 0; j < 12; ++j) {
+      c.start[j][0] = 32 * (j % 4);
+      c.start[j][3] = j / 4;
+    }
+    c.step[1] = 4; c.wrap[1] = 216;
+    c.step[2] = 1; c.wrap[2] = 216;
+    c.cta_step[1] = 4; c.cta_step[2] = 1;
+    c.iters = iters;
+    run("conv1 box{32,11,1,1} x12 ATOM_32B", c, sink);
+  }
+  // C: 5D map folding the 4 n-groups: {32, 4, W, H, C}, box {32, 4, 11, 1, 3}
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[5] = {32, 4, W, H, C};
+    const uint64_t str[4] = {128, N * 4, W * N * 4, H * W * N * 4};
+    const uint32_t box[5] = {32, 4, 11, 1, 3};
+    encode(&c.map, x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    c.rank = 5;
+    c.nbox = 1;
+    c.box_bytes = 32 * 4 * 11 * 3 * 4;
+    c.step[2] = 4; c.wrap[2] = 216;
+    c.step[3] = 1; c.wrap[3] = 216;
+    c.cta_step[2] = 4; c.cta_step[3] = 1;
+    c.iters = iters;
+    run("conv1 5D box{32,4,11,1,3} x1 ATOM_32B", c, sink);
+  }
+  // D: a 2D view of the same bytes: rows of 128 floats (one pixel x 128 n), box {32, 33}
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t rows = W * H * C;
+    const uint64_t dims[2] = {N, rows};
+    const uint64_t str[1] = {N * 4};
+    const uint32_t box[2] = {32, 33};
+    encode(&c.map, x, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    c.rank = 2;
+    c.nbox = 4;
+    c.box_bytes = 32 * 33 * 4;
+    for (int j = 0; j < 4; ++j) c.start[j][0] = 32 * j;
+    c.step[1] = 4; c.wrap[1] = 150000;
+    c.cta_step[1] = 1000;
+    c.iters = iters;
+    run("2D box{32,33} x4 (contiguous rows) ATOM_32B", c, sink);
+  }
+  // E: 2D GEMM-B-like: [K=9216][N=4096] fp32, box {32 n, 32 k} x 8 (32 KB)
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[2] = {4096, 4608};
+    const uint64_t str[1] = {4096 * 4};
+    const uint32_t box[2] = {32, 32};
+    encode(&c.map, x, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    c.rank = 2;
+    c.nbox = 8;
+    c.box_bytes = 32 * 32 * 4;
+    for (int j = 0; j < 8; ++j) c.start[j][0] = 32 * j;
+    c.step[1] = 32; c.wrap[1] = 4576;
+    c.cta_step[0] = 256; c.wrap[0] = 4096;
+    c.iters = iters;
+    run("gemm-B box{32,32} x8 ATOM_32B", c, sink);
+  }
+  // F: 2D GEMM-A-like K-major: [M][K], box {32 k, 128 m} SW128
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[2] = {4096, 4608};
+    const uint64_t str[1] = {4096 * 4};
+    const uint32_t box[2] = {32, 128};
+    encode(&c.map, x, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    c.rank = 2;
+    c.nbox = 2;
+    c.box_bytes = 32 * 128 * 4;
+    c.start[1][1] = 128;
+    c.step[0] = 32; c.wrap[0] = 4064;
+    c.cta_step[1] = 256; c.wrap[1] = 4352;
+    c.iters = iters;
+    run("gemm-A box{32,128} x2 SW128", c, sink);
+  }
+  // G: conv2 CI box: input N=128, 27x27, C=96, box {32, 1, 1, 32} x 4
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t W2 = 27, H2 = 27, C2 = 96;
+    const uint64_t dims[4] = {N, W2, H2, C2};
+    const uint64_t str[3] = {N * 4, W2 * N * 4, H2 * W2 * N * 4};
+    const uint32_t box[4] = {32, 1, 1, 32};
+    encode(&c.map, x, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    c.rank = 4;
+    c.nbox = 4;
+    c.box_bytes = 32 * 32 * 4;
+    for (int j = 0; j < 4; ++j) c.start[j][0] = 32 * j;
+    c.step[1] = 1; c.wrap[1] = 27;
+    c.step[3] = 32; c.wrap[3] = 96;
+    c.cta_step[2] = 1; c.wrap[2] = 27;
+    c.iters = iters;
+    run("conv2 CI box{32,1,1,32} x4 ATOM_32B", c, sink);
+  }
+  // H: conv2 5D folding n-groups {32, 4, W, H, C} box {32, 4, 1, 1, 32}
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t W2 = 27, H2 = 27, C2 = 96;
+    const uint64_t dims[5] = {32, 4, W2, H2, C2};
+    const uint64_t str[4] = {128, N * 4, W2 * N * 4, H2 * W2 * N * 4};
+    const uint32_t box[5] = {32, 4, 1, 1, 32};
+    encode(&c.map, x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    c.rank = 5;
+    c.nbox = 1;
+    c.box_bytes = 32 * 4 * 32 * 4;
+    c.step[2] = 1; c.wrap[2] = 27;
+    c.step[4] = 32; c.wrap[4] = 96;
+    c.cta_step[3] = 1; c.wrap[3] = 27;
+    c.iters = iters;
+    run("conv2 5D box{32,4,1,1,32} x1 ATOM_32B", c, sink);
+  }
+  // I: fc-B grouped 3D view {32 n, K, N/32 groups} (group stride 128 B < k stride), box {32, 32, 8}
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[3] = {32, 4608, 128};
+    const uint64_t str[2] = {4096 * 4, 128};
+    const uint32_t box[3] = {32, 32, 8};
+    if (encode(&c.map, x, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+      c.rank = 3;
+      c.nbox = 1;
+      c.box_bytes = 32 * 32 * 8 * 4;
+      c.step[1] = 32; c.wrap[1] = 4576;
+      c.cta_step[2] = 8; c.wrap[2] = 128;
+      c.iters = iters;
+      run("fc-B grouped 3D box{32,32,8} x1", c, sink);
+    }
+  }
+  // J: conv2 CI grouped 5D view {32 n, C, G, W, H}, box {32, 32 c, 4 g, 1, 1}
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t W2 = 27, H2 = 27, C2 = 96;
+    const uint64_t dims[5] = {32, C2, 4, W2, H2};
+    const uint64_t str[4] = {H2 * W2 * N * 4, 128, N * 4, W2 * N * 4};
+    const uint32_t box[5] = {32, 32, 4, 1, 1};
+    if (encode(&c.map, x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+      c.rank = 5;
+      c.nbox = 2;
+      c.box_bytes = 32 * 32 * 4 * 4;
+      c.start[1][3] = 1;
+      c.step[1] = 32; c.wrap[1] = 96;
+      c.step[3] = 1; c.wrap[3] = 26;
+      c.cta_step[4] = 1; c.wrap[4] = 27;
+      c.iters = iters;
+      run("conv2 grouped 5D box{32,32,4,1,1} x2", c, sink);
+    }
+  }
+  // K: conv1 grouped 5D view {32 n, W, C, G, H}, box {32, 16 w, 3 c, 4 g, 1}, 2 pixels
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[5] = {32, W, C, 4, H};
+    const uint64_t str[4] = {N * 4, H * W * N * 4, 128, W * N * 4};
+    const uint32_t box[5] = {32, 16, 3, 4, 1};
+    if (encode(&c.map, x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+      c.rank = 5;
+      c.nbox = 2;
+      c.box_bytes = 32 * 16 * 3 * 4 * 4;
+      c.start[1][1] = 4;
+      c.step[1] = 8; c.wrap[1] = 208;
+      c.step[4] = 1; c.wrap[4] = 216;
+      c.cta_step[1] = 8; c.cta_step[4] = 1;
+      c.iters = iters;
+      run("conv1 grouped 5D box{32,16,3,4,1} x2", c, sink);
+    }
+  }
+  return 0;
+}

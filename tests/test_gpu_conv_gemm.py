@@ -39,14 +39,21 @@ def _check_conv(cuda, n, ci, h, w, co, f, stride, pad, layout, precision, seed=0
     bound = _torch_conv64(x.abs(), f.abs(), stride, pad)
     xin = x if layout == NCHW else x.permute(1, 2, 3, 0).contiguous()
     t = lcnn.DeviceTensor4D(n, ci, h, w, layout, xin.reshape(-1))
-    out = lcnn.conv_forward(t, f.contiguous(), co, fh, fw, stride, pad, precision)
+    one_shot = lcnn.conv_forward(t, f.contiguous(), co, fh, fw, stride, pad, precision)
+    # the pre-packed route (lcnn_conv_pack_filters + lcnn_conv_forward_packed)
+    packed = lcnn.pack_conv_filters(t, f.contiguous(), co, fh, fw, stride, pad, precision)
+    via_pack = lcnn.conv_forward_packed(t, packed, co, fh, fw, stride, pad, precision)
     ho, wo = want.shape[2], want.shape[3]
-    got = out.data.view(n, co, ho, wo) if layout == NCHW else \
-        out.data.view(co, ho, wo, n).permute(3, 0, 1, 2)
-    got = got.double()
-    err = (got - want).abs()
-    ok = bool((err <= tolerance(precision, got, want, bound)).all())
-    assert ok, (n, ci, h, w, co, fh, fw, stride, pad, layout, precision, float(err.max()))
+    for tag, out in (("one-shot", one_shot), ("packed", via_pack)):
+        got = out.data.view(n, co, ho, wo) if layout == NCHW else \
+            out.data.view(co, ho, wo, n).permute(3, 0, 1, 2)
+        got = got.double()
+        err = (got - want).abs()
+        ok = bool((err <= tolerance(precision, got, want, bound)).all())
+        assert ok, (tag, n, ci, h, w, co, fh, fw, stride, pad, layout, precision,
+                    float(err.max()))
+    if precision == lcnn.FP32:  # deterministic kernels: the two routes agree bit for bit
+        assert torch.equal(one_shot.data, via_pack.data)
 
 
 def tolerance(precision, got, want, bound):
@@ -71,6 +78,12 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     (96, 64, 7, 7, 64, 3, 2, 0),
     (128, 384, 13, 13, 256, 3, 1, 1),  # conv4: 170 tiles -> 148 whole + stream-K tail
     (32, 5, 15, 15, 130, 7, 2, 3),     # ROW mode, 35 -> 40 k-rows, ragged channel tile
+    # N % 128 == 0: grouped 5D input boxes (one box per 128-column block)
+    (128, 3, 35, 35, 96, 11, 4, 0),    # conv1-like ROW, row width 11 -> 16 (48 k-rows), channels on M
+    (256, 3, 19, 19, 64, 5, 2, 1),     # ROW, width 5 -> 8 (24 k-rows)
+    (128, 5, 15, 15, 130, 7, 2, 3),    # ROW, width 7 -> 8 (40 k-rows), ragged channel tile
+    (128, 16, 10, 10, 48, 5, 2, 2),    # WIN
+    (256, 64, 7, 7, 64, 3, 2, 0),      # CI, two blocks per pixel
 ]
 
 

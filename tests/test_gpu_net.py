@@ -1,0 +1,120 @@
+"""GPU parity of the network runtime (include/lcnn_net.h) against the
+UNMODIFIED reference run_network (net.cpp:266-398, via oracle/_ref):
+same JSON, same (c_t, n_t) annotation, same seeded default weights
+(net.cpp:217-243), same input.
+
+Tolerances:
+  FP32 dense precision : approx_equal 1e-5 -- the reference's own bar for
+                         layout independence (test_net.cpp:211-248,
+                         acceptance.cpp:328-401);
+  TF32 dense precision : |p - p_ref| <= 2e-3 absolute on the softmax
+                         probabilities (tf32 operand truncation, 2^-9 relative
+                         per product, through three fc layers).
+The pipelined host-buffer API (lcnn_net_forward_host_many) must return exactly
+what the device-buffer forward returns (FP32 is deterministic).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from oracle.oracle import CHWN, NCHW, Ref, approx_equal, rng_uniform
+from paper_1610_03618_b200 import capi, netapi
+
+pytestmark = pytest.mark.gpu
+
+# AlexNet's layer kinds and filter/stride pattern at a size the CPU reference
+# finishes in seconds (conv1 f11 s4, overlapping 3/2 max pools, 5x5 and 3x3
+# convs, two fc layers, softmax)
+MINI = {
+    "input": {"n": 32, "c": 3, "h": 67, "w": 67},
+    "layers": [
+        {"name": "conv1", "kind": "conv", "c_out": 32, "f": 11, "stride": 4, "pad": 0},
+        {"name": "pool1", "kind": "pool", "win": 3, "stride": 2, "mode": "max"},
+        {"name": "conv2", "kind": "conv", "c_out": 64, "f": 5, "stride": 1, "pad": 2},
+        {"name": "pool2", "kind": "pool", "win": 3, "stride": 2, "mode": "avg"},
+        {"name": "conv3", "kind": "conv", "c_out": 64, "f": 3, "stride": 1, "pad": 1},
+        {"name": "fc6", "kind": "fc", "out": 256},
+        {"name": "fc7", "kind": "fc", "out": 10},
+        {"name": "prob", "kind": "softmax"},
+    ],
+}
+THRESHOLDS = [(257, 32), (32, 128)]  # B200 calibration (all CHWN), titan-black preset (mixed)
+
+
+def _nets(text, c_t, n_t):
+    net = netapi.Network(text, c_t, n_t, seed=42)
+    return net, net.info(NCHW)
+
+
+@pytest.fixture(autouse=True)
+def _restore_precision():
+    yield
+    netapi.set_dense_precision(capi.PREC_FP32)
+
+
+@pytest.mark.parametrize("c_t,n_t", THRESHOLDS)
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_network_matches_reference(cuda, c_t, n_t, precision):
+    import torch
+
+    if not Ref.available():
+        pytest.fail("oracle/_ref/liblcnn_ref.so missing (build() makes it)")
+    text = json.dumps(MINI)
+    netapi.set_dense_precision(capi.PREC_FP32 if precision == "fp32" else capi.PREC_TF32)
+    net, info = _nets(text, c_t, n_t)
+    rows, cols = info["out"]
+    n, c, h, w = info["dims"]
+    x = rng_uniform(11, n * c * h * w)
+    want = Ref.run_network(text, x, NCHW, c_t, n_t, seed=42)
+    assert want.shape == (rows, cols)
+    # layouts: the same annotation as the reference
+    ref_layouts, _ = Ref.plan_network(text, c_t, n_t)
+    assert net.layouts[:len(MINI["layers"])] == ref_layouts[:len(MINI["layers"])]
+    dx = torch.from_numpy(x).to(cuda)
+    dy = torch.empty(rows * cols, device=cuda)
+    stream = torch.cuda.current_stream(cuda).cuda_stream
+    net.forward(dx.data_ptr(), NCHW, dy.data_ptr(), stream)
+    torch.cuda.synchronize()
+    got = dy.cpu().numpy().reshape(rows, cols)
+    if precision == "fp32":
+        assert approx_equal(got, want, 1e-5)
+    else:
+        assert np.abs(got - want).max() <= 2e-3
+    assert np.allclose(got.sum(1), 1.0, atol=1e-5)
+    net.close()
+
+
+@pytest.mark.parametrize("c_t,n_t", THRESHOLDS)
+def test_forward_host_many_matches_device_forward(cuda, c_t, n_t):
+    import torch
+
+    netapi.set_dense_precision(capi.PREC_FP32)
+    net, info = _nets(json.dumps(MINI), c_t, n_t)
+    rows, cols = info["out"]
+    n, c, h, w = info["dims"]
+    batches = [rng_uniform(100 + i, n * c * h * w) for i in range(5)]
+    stream = torch.cuda.current_stream(cuda).cuda_stream
+    want = []
+    for b in batches:
+        dy = torch.empty(rows * cols, device=cuda)
+        net.forward(torch.from_numpy(b).to(cuda).data_ptr(), NCHW, dy.data_ptr(), stream)
+        torch.cuda.synchronize()
+        want.append(dy.cpu().numpy())
+    hx = [torch.from_numpy(b).pin_memory() for b in batches]
+    hy = [torch.zeros(rows * cols).pin_memory() for _ in batches]
+    net.forward_host_many([t.data_ptr() for t in hx], NCHW, [t.data_ptr() for t in hy])
+    for got, exp in zip(hy, want):
+        assert np.array_equal(got.numpy(), exp)
+    # a single batch and an empty sequence
+    one = torch.zeros(rows * cols).pin_memory()
+    net.forward_host_many([hx[3].data_ptr()], NCHW, [one.data_ptr()])
+    assert np.array_equal(one.numpy(), want[3])
+    net.forward_host_many([], NCHW, [])
+    # forward_host (one batch) agrees too, in the other input layout
+    xc = np.ascontiguousarray(batches[2].reshape(n, c, h, w).transpose(1, 2, 3, 0)).ravel()
+    hc = torch.from_numpy(xc).pin_memory()
+    out = torch.zeros(rows * cols).pin_memory()
+    net.forward_host(hc.data_ptr(), CHWN, out.data_ptr())
+    assert approx_equal(out.numpy(), want[2], 1e-5)
+    net.close()
