@@ -268,6 +268,26 @@ lcnn_status lcnn_gemm(const float* a, const float* b, float* c, uint64_t m,
                       uint64_t n, uint64_t k, int precision, void* d_workspace,
                       size_t workspace_bytes, void* stream);
 
+/* fc_forward (softmax.cpp:182-184) with weights that are reused across calls
+ * (network fc layers; run_network re-reads the same weights every forward,
+ * net.cpp:338-383): the weights (k x n, row-major) are packed ONCE into the
+ * tensor-core operand image (W^T, K-major; + the 3xTF32 split), then
+ * y (m x n) = x . W runs on it.  x_layout LCNN_NCHW: x is m rows of k
+ * (the flattened NCHW activations); LCNN_CHWN: x is the CHWN producer itself,
+ * [k][m] with the m images contiguous, so the flatten (net.cpp:258-262) costs
+ * no transform.  TF32 / 3xTF32 only (packed_bytes 0 otherwise); k % 4 == 0,
+ * and m % 4 == 0 for CHWN.  d_packed 256-byte aligned. */
+size_t lcnn_fc_packed_bytes(uint64_t k, uint64_t n, int precision);
+size_t lcnn_fc_workspace_bytes(uint64_t m, uint64_t k, int precision);
+lcnn_status lcnn_fc_pack_weights(const float* weights, void* d_packed,
+                                 size_t packed_bytes, uint64_t k, uint64_t n,
+                                 int precision, void* stream);
+lcnn_status lcnn_fc_forward_packed(const float* x, int x_layout,
+                                   const void* d_packed, float* y, uint64_t m,
+                                   uint64_t n, uint64_t k, int precision,
+                                   void* d_workspace, size_t workspace_bytes,
+                                   void* stream);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -79,6 +79,11 @@ _SIGNATURES = {
     "lcnn_im2col": (c_int, [_P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32, _P]),
     "lcnn_gemm_workspace_bytes": (c_size_t, [c_uint64, c_uint64, c_uint64, c_int]),
     "lcnn_gemm": (c_int, [_P, _P, _P, c_uint64, c_uint64, c_uint64, c_int, _P, c_size_t, _P]),
+    "lcnn_fc_packed_bytes": (c_size_t, [c_uint64, c_uint64, c_int]),
+    "lcnn_fc_workspace_bytes": (c_size_t, [c_uint64, c_uint64, c_int]),
+    "lcnn_fc_pack_weights": (c_int, [_P, _P, c_size_t, c_uint64, c_uint64, c_int, _P]),
+    "lcnn_fc_forward_packed": (c_int, [_P, c_int, _P, _P, c_uint64, c_uint64, c_uint64, c_int, _P,
+                                       c_size_t, _P]),
 }
 
 _lib = None

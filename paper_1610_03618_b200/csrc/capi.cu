@@ -526,4 +526,51 @@ lcnn_status lcnn_gemm(const float* a, const float* b, float* c, uint64_t m, uint
   return ok();
 }
 
+size_t lcnn_fc_packed_bytes(uint64_t k, uint64_t n, int precision) {
+  if (k == 0 || n == 0 || (precision != LCNN_PREC_TF32 && precision != LCNN_PREC_3XTF32)) return 0;
+  return lcnn_impl::fc_packed_bytes(k, n, precision);
+}
+
+size_t lcnn_fc_workspace_bytes(uint64_t m, uint64_t k, int precision) {
+  return lcnn_impl::fc_workspace_bytes(m, k, precision);
+}
+
+lcnn_status lcnn_fc_pack_weights(const float* weights, void* d_packed, size_t packed_bytes,
+                                 uint64_t k, uint64_t n, int precision, void* stream) {
+  if (!weights || !d_packed) return fail(LCNN_EINVAL, "fc: null pointer");
+  if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
+    return fail(LCNN_EINVAL, "fc: packed weights must be 256-byte aligned");
+  if (k == 0 || n == 0) return fail(LCNN_ESHAPE, "gemm: empty operand");
+  if (precision != LCNN_PREC_TF32 && precision != LCNN_PREC_3XTF32)
+    return fail(LCNN_EINVAL, "fc: packed weights need TF32 or 3xTF32 precision");
+  if (packed_bytes < lcnn_impl::fc_packed_bytes(k, n, precision))
+    return fail(LCNN_EINVAL, "fc: packed buffer too small");
+  cudaError_t e = lcnn_impl::launch_fc_pack(weights, k, n, precision, d_packed, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fc_pack_weights");
+  return ok();
+}
+
+lcnn_status lcnn_fc_forward_packed(const float* x, int x_layout, const void* d_packed, float* y,
+                                   uint64_t m, uint64_t n, uint64_t k, int precision,
+                                   void* d_workspace, size_t workspace_bytes, void* stream) {
+  if (!x || !d_packed || !y) return fail(LCNN_EINVAL, "fc: null pointer");
+  if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
+    return fail(LCNN_EINVAL, "fc: packed weights must be 256-byte aligned");
+  if (m == 0 || n == 0 || k == 0) return fail(LCNN_ESHAPE, "gemm: empty operand");
+  if (precision != LCNN_PREC_TF32 && precision != LCNN_PREC_3XTF32)
+    return fail(LCNN_EINVAL, "fc: packed weights need TF32 or 3xTF32 precision");
+  if (x_layout != LCNN_NCHW && x_layout != LCNN_CHWN)
+    return fail(LCNN_ELAYOUT, "fc: input must be NCHW rows or a CHWN tensor");
+  const bool a_mn = x_layout == LCNN_CHWN;
+  if (!lcnn_impl::fc_tc_supported(m, n, k, a_mn) || (reinterpret_cast<uintptr_t>(x) & 15u))
+    return fail(LCNN_EUNSUPPORTED, "fc: shape not supported by the packed tensor-core path");
+  if (workspace_bytes < lcnn_impl::fc_workspace_bytes(m, k, precision) ||
+      (!d_workspace && workspace_bytes))
+    return fail(LCNN_EINVAL, "fc: workspace too small");
+  cudaError_t e = lcnn_impl::launch_fc_packed(x, a_mn, d_packed, y, m, n, k, precision,
+                                              d_workspace, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fc_forward_packed");
+  return ok();
+}
+
 }  // extern "C"

@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/lcnn_cuda.h"
 #include "common.cuh"
@@ -41,7 +42,7 @@ namespace lcnn_dev {
 
 using namespace lcnn_tc;
 
-enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2, kModeROW = 3 };
+enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2, kModeROW = 3, kModeSHARE = 4 };
 
 struct ConvGeomTc {
   uint32_t N, Ci, H, W, Co, FH, FW, S, P, Ho, Wo;
@@ -115,6 +116,7 @@ struct ChwnConvLoader {
   // 4D boxes; TMA cost is mostly per box (scripts/tma_bench.cu)
   bool grouped;
   static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN, kZeroSmem = false;
+  static constexpr bool kResidentA = false;
   static constexpr int kSteps = kTcBK / 8;
   static constexpr int kBoxes = kCoOnN ? kTcBM / 32 : kPBN / 32;
   // input image: SWIZZLE_128B_BASE32B, 32-column atoms of 32 k-rows (4 KB);
@@ -237,6 +239,7 @@ struct ChwnRowLoader {
   // 1 KB swizzle atoms); the padded taps have zero weights
   bool grouped;
   static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN, kZeroSmem = true;
+  static constexpr bool kResidentA = false;
   static constexpr int kSteps = 0;
   static constexpr int kBoxes = kCoOnN ? kTcBM / 32 : kPBN / 32;  // 32-column input boxes
   // input operand: MN-major SWIZZLE_128B_BASE32B, kBoxes groups of KR rows;
@@ -324,7 +327,15 @@ __global__ void pack_filters_row_kernel(const float* __restrict__ f, float* __re
     rest /= g.KR / 4;
     const uint32_t fh = static_cast<uint32_t>(rest % g.FH);
     const uint32_t t = static_cast<uint32_t>(rest / g.FH);
-    const uint32_t kk = 4 * q + e, ci = kk / g.FP, fw = kk - ci * g.FP, co = t * bn + r;
+    const uint32_t kk = 4 * q + e, co = t * bn + r;
+    uint32_t ci, fw;
+    if (g.mode == kModeSHARE) {  // k = (fw, ci): channels fastest
+      fw = kk / g.Ci;
+      ci = kk - fw * g.Ci;
+    } else {  // k = (ci, fw)
+      ci = kk / g.FP;
+      fw = kk - ci * g.FP;
+    }
     float v = 0.0f;
     if (co < g.Co && ci < g.Ci && fw < g.FW)
       v = f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw];
@@ -341,14 +352,18 @@ __global__ void pack_filters_row_kernel(const float* __restrict__ f, float* __re
   }
 }
 
-struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols
+struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a multiple of 32)
   float* c;
   uint64_t ldc;
   uint32_t M, N;
   __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
                                           bool add) const {
-    if (m >= M || n0 >= N) return;
-    store_row32(c + m * ldc + n0, n0, N, v, add);
+    if (n0 >= N) return;  // warp-uniform
+    if (n0 + 32 <= N) {
+      warp_store_rows32(m < M ? c + m * ldc + n0 : nullptr, v, add);
+    } else if (m < M) {
+      store_row32(c + m * ldc + n0, n0, N, v, add);
+    }
   }
 };
 
@@ -370,6 +385,90 @@ struct ColsOut {
       else
         __stcs(p + static_cast<uint64_t>(j) * ncols, v[j]);
     }
+  }
+};
+
+// SHARE mode (small C_i * F_w and C_o <= 128, e.g. AlexNet conv1: 3 x 11,
+// stride 4).  A tile is 8 consecutive output pixels of one output row x one
+// 32-image group, and ONE TMA box per filter row serves all 8 pixels: the
+// input view {32 n, C_i, W, N/32, H} lands the box {32, C_i, BW = S*7 + F_w,
+// 1, 1} as rows ordered (w, c), c fastest, so pixel p's receptive-field row
+// is the same K sequence k = fw * C_i + c shifted by p * S * C_i rows.  The 8
+// MN-major 32-column atoms of the UMMA B operand (N = 256) therefore overlap
+// in shared memory at a uniform pitch of S * C_i rows (the descriptor LBO):
+// TMA and tcgen05 both swizzle by shared-memory address (verified on B200,
+// scripts/swz_test.cu), so an atom may start at any 128-byte row.  The input
+// stream per 256 output columns is one box of BW * C_i rows (117 for conv1)
+// instead of ROW mode's eight 48-row atoms.  The filters are the A operand
+// (channels on M), K-major SWIZZLE_NONE core matrices [fh][KR/4][bn][4] with
+// bn = C_o rounded to 8.  The box is latency-bound (one
+// 128-B run per row), so the ring depth matters more than the filter bytes:
+// the filter row travels with each stage (one contiguous bulk copy, 15 KB for
+// conv1) and 7 slots fit, rather than a resident 169 KB image with 3 slots
+// (scripts/tma_bench.cu: 38 -> 75 B/clk/SM from 3 to 8 slots).  Rows
+// bn..127 of the M = 128 MMA read the next chunk's rows (finite), producing
+// accumulator rows no one stores.  K padding rows
+// (C_i*F_w .. KR) carry zero weights; the slot rows past the box are never
+// written and stay zero.
+constexpr uint32_t kSharePix = 8;  // output pixels per tile (8 x 32 columns = UMMA N 256)
+
+struct ChwnShareLoader {
+  CUtensorMap x;
+  const float* wimg;
+  ConvGeomTc g;
+  uint32_t bn;      // filter image rows (C_o rounded up to 8)
+  uint32_t owb;     // 8-pixel blocks per output row
+  uint32_t groups;  // N / 32
+  uint32_t res;     // resident filter image bytes
+  static constexpr bool kZeroSmem = true;
+  static constexpr bool kResidentA = true;
+  static constexpr int kSteps = 0;
+  __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
+    return smem_desc_sw128(sa + 2 * k * bn * 16, bn * 16, 128, 0);
+  }
+  __device__ uint64_t desc_b(const uint8_t* sb, int k) const {
+    return smem_desc_sw128(sb + k * 1024, g.S * g.Ci * 128, 512, 1);
+  }
+  __device__ void prefetch() const { tma_prefetch(&x); }
+  __device__ uint32_t resident_bytes() const { return res; }
+  __device__ void load_resident(void* dst, uint64_t* bar) const {
+    const uint32_t row = g.KR * bn * 4;  // one filter row per copy
+    for (uint32_t fh = 0; fh < g.FH; ++fh)
+      bulk_load(static_cast<uint8_t*>(dst) + fh * row, wimg + fh * g.KR * bn, row, bar);
+  }
+  __device__ uint32_t resident_offset(uint32_t kb) const { return kb * g.KR * bn * 4; }
+  struct State {
+    int32_t y0, z0, grp;
+  };
+  __device__ State begin(uint32_t, uint32_t n0, uint32_t) const {
+    const uint32_t t = n0 / (kSharePix * 32);
+    const uint32_t grp = t % groups, r = t / groups;
+    const uint32_t ob = r % owb, oh = r / owb;
+    return State{static_cast<int32_t>(ob * kSharePix * g.S) - static_cast<int32_t>(g.P),
+                 static_cast<int32_t>(oh * g.S) - static_cast<int32_t>(g.P),
+                 static_cast<int32_t>(grp)};
+  }
+  __device__ void load(State& st, uint32_t, uint32_t k, void* sa, void* sb, uint64_t* bar) const {
+    tma_load_5d(sb, &x, bar, 0, 0, st.y0, st.grp, st.z0 + static_cast<int32_t>(k));
+    if (!res) bulk_load(sa, wimg + k * g.KR * bn, g.KR * bn * 4, bar);
+  }
+};
+
+// Accumulator rows = channels, 32-column chunk j = pixel j of the tile's 8
+// (its 32 images): out[co][oh][ow][32 grp .. 32 grp + 31], one 128-B line.
+struct ShareOut {
+  float* c;
+  uint64_t plane;  // Ho * Wo * N
+  uint32_t co, n, wo, owb, groups;
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
+                                          bool add) const {
+    const uint32_t t = n0 / (kSharePix * 32), p = n0 % (kSharePix * 32) / 32;
+    const uint32_t grp = t % groups, r = t / groups;
+    const uint32_t ob = r % owb, oh = r / owb, ow = ob * kSharePix + p;
+    if (ow >= wo) return;  // warp-uniform
+    warp_store_rows32(
+        m < co ? c + m * plane + (static_cast<uint64_t>(oh) * wo + ow) * n + grp * 32 : nullptr, v,
+        add);
   }
 };
 
@@ -694,12 +793,14 @@ uint32_t co_tile_n(uint32_t co) {
 }
 
 // Measured on B200 (scripts/mma_bench.cu, scripts/tma_bench.cu): one
-// tcgen05.mma.kind::tf32 with M = 128, K = 8 issues every ~150 cycles
-// whatever its N (32..256) -- so useful work per instruction is what counts --
-// and a TMA box costs ~80 cycles of fixed overhead plus ~0.9 cycle per
-// 128-byte row it moves.  A pipeline stage takes the longer of the two.
-double stage_cycles(uint32_t ksteps, uint32_t boxes, uint32_t rows) {
-  const double mma = 150.0 * ksteps, tma = 80.0 * boxes + 0.9 * rows;
+// tcgen05.mma.kind::tf32 with M = 128, K = 8 occupies the tensor pipe for
+// max(~96, N/2) cycles (N = 256: 128 cycles = 1.1 PFLOP/s per chip; N <= 192:
+// a ~96-cycle floor, so narrow MMAs waste issue slots), and a TMA box costs
+// ~80 cycles of fixed overhead plus ~0.9 cycle per 128-byte row it moves.  A
+// pipeline stage takes the longer of the two.
+double stage_cycles(uint32_t ksteps, uint32_t bn, uint32_t boxes, uint32_t rows) {
+  const double per = bn / 2.0 > 96.0 ? bn / 2.0 : 96.0;
+  const double mma = per * ksteps, tma = 80.0 * boxes + 0.9 * rows;
   return mma > tma ? mma : tma;
 }
 
@@ -716,10 +817,10 @@ bool choose_co_on_n(uint32_t co, uint64_t ncols, uint32_t krows, uint32_t in_row
   const double tiles_n = double((ncols + kTcBM - 1) / kTcBM) * ((co + bn - 1) / bn);
   const double tiles_m = double((co + kTcBM - 1) / kTcBM) * ((ncols + kPBN - 1) / kPBN);
   const double on_n =
-      tiles_n * stage_cycles(krows / 8, kTcBM / 32 / div + 1,
+      tiles_n * stage_cycles(krows / 8, bn, kTcBM / 32 / div + 1,
                              (kTcBM / 32) * in_rows + w_rows_per_128 * bn / kTcBM);
   const double on_m =
-      tiles_m * stage_cycles(krows / 8, kPBN / 32 / div + 1,
+      tiles_m * stage_cycles(krows / 8, kPBN, kPBN / 32 / div + 1,
                              (kPBN / 32) * in_rows + w_rows_per_128);
   return on_n <= on_m;
 }
@@ -925,6 +1026,64 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
   }
 }
 
+// SHARE-mode geometry: filter image rows, input box width, ring slot
+// layout [filter row (A) | input box rows (B)] and how many slots fit.
+// resident (profiling knob LCNN_CONV_ROW=r): the whole filter image stays in
+// shared memory and slots carry only the input box.
+struct ShareGeom {
+  uint32_t bn, kr, bw, wbytes, slot, img, slots;
+  bool ok;
+};
+
+ShareGeom share_geom(const ConvArgs& a, bool resident) {
+  ShareGeom q{};
+  q.bn = (a.co + 7) / 8 * 8;
+  q.kr = (a.ci * a.fw + 7) / 8 * 8;
+  q.bw = a.stride * (kSharePix - 1) + a.fw;
+  const uint32_t rows = std::max(q.bw * a.ci, a.stride * a.ci * (kSharePix - 1) + q.kr);
+  q.wbytes = resident ? 0 : q.kr * q.bn * 4;  // one filter row (a multiple of 128 B)
+  q.slot = (q.wbytes + rows * 128 + 1023) / 1024 * 1024;
+  q.img = resident ? a.fh * q.kr * q.bn * 4 + 16 * 128 : 0;  // + slack for the M = 128 reads
+  q.slots = 0;
+  for (uint32_t n = kPStagesMax; n >= 3 && !q.slots; --n)
+    if (1024ull + n * q.slot + q.img + 16 + sizeof(PCtl) <= kMaxDynSmem) q.slots = n;
+  q.ok = a.precision == LCNN_PREC_TF32 && a.co <= kTcBM && a.n % 32 == 0 && a.ci <= 256 &&
+         q.bw <= 256 && q.kr <= 256 && a.stride * a.ci * 128 < (1u << 18) && q.slots >= 3;
+  return q;
+}
+
+cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s) {
+  const ConvArgs& a = t.a;
+  const ShareGeom q = share_geom(a, resident);
+  ChwnShareLoader L;
+  L.g = t.p.g;
+  L.bn = q.bn;
+  L.wimg = t.w_hi;
+  L.owb = (a.wo + kSharePix - 1) / kSharePix;
+  L.groups = a.n / 32;
+  L.res = resident ? a.fh * q.kr * q.bn * 4 : 0;
+  const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
+  const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
+                             static_cast<uint64_t>(a.n) * 4, 128,
+                             static_cast<uint64_t>(a.w) * a.n * 4};
+  const uint32_t box[5] = {32, a.ci, q.bw, 1, 1};
+  if (!make_tmap(&L.x, t.x_hi, 5, dims, pitch, box, nullptr, 1)) return cudaErrorInvalidValue;
+  const uint32_t tiles = a.ho * L.owb * L.groups;
+  Sched sc = make_sched(1, tiles, a.fh, 1, kSharePix * 32, false, true);
+  sc.ksteps = q.kr / 8;
+  sc.a_bytes = q.wbytes;
+  sc.stage_bytes = q.wbytes + q.bw * a.ci * 128;
+  sched_ring(sc, q.slots, q.slot, q.img);
+  if (sc.dp_tiles < tiles) {  // zero the stream-K tiles' output rows (oh >= first split row)
+    const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
+    const uint64_t col0 = static_cast<uint64_t>(sc.dp_tiles / (L.owb * L.groups)) * a.wo * a.n;
+    cudaError_t e = cudaMemset2DAsync(a.dst + col0, ncols * 4, 0, (ncols - col0) * 4, a.co, s);
+    if (e != cudaSuccess) return e;
+  }
+  ShareOut O{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, L.owb, L.groups};
+  return launch_persistent(L, O, sc, s);
+}
+
 template <bool kCoOnN>
 cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   const ConvArgs& a = t.a;
@@ -981,7 +1140,8 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
 // Run workspace (3xTF32 CHWN only): the split input copies [x_hi | x_lo].
 namespace {
 
-enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM };
+enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM,
+                 kRouteShare, kRouteShareRes };
 
 struct ConvRoute {
   RouteKind kind = kRouteSimt;
@@ -1011,9 +1171,34 @@ ConvRoute route_conv(const ConvArgs& a) {
   }
   const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
   if (r.p.g.mode == kModeROW) {
+    // profiling knob LCNN_CONV_ROW: "n" / "m" force ROW mode in that
+    // orientation instead of SHARE ("n" ungrouped, KR = C_i*F_w rounded to 8,
+    // so the filter image can stay resident)
+    static const int force = [] {
+      const char* e = std::getenv("LCNN_CONV_ROW");
+      return e ? (e[0] == 'n' ? 1 : (e[0] == 'm' ? 2 : (e[0] == 'r' ? 3 : 0))) : 0;
+    }();
+    if (!force || force == 3) {
+      const ShareGeom q = share_geom(a, force == 3);
+      if (q.ok) {
+        r.kind = force == 3 ? kRouteShareRes : kRouteShare;
+        r.p.g.mode = kModeSHARE;
+        r.p.g.KR = q.kr;
+        r.p.g.FP = a.fw;
+        r.p.K = a.fh * q.kr;
+        r.apack = static_cast<uint64_t>(a.fh) * q.kr * q.bn;
+        return r;
+      }
+    }
+    if (force == 1) {
+      r.p.g.KR = (a.ci * a.fw + 7) / 8 * 8;
+      r.p.g.FP = a.fw;
+      r.p.K = a.fh * r.p.g.KR;
+    }
     const uint32_t kr = r.p.g.KR;
     const bool grouped = a.n % 128 == 0 && kr == a.ci * r.p.g.FP;
-    const bool on_n = choose_co_on_n(a.co, ncols, kr, grouped ? kr : a.ci * a.fw, kr * 4, grouped);
+    bool on_n = choose_co_on_n(a.co, ncols, kr, grouped ? kr : a.ci * a.fw, kr * 4, grouped);
+    if (force) on_n = force == 1;
     r.kind = on_n ? kRouteRowOnN : kRouteRowOnM;
     r.apack = static_cast<uint64_t>(pack_rows(a.co, on_n)) * r.p.K;
   } else {
@@ -1069,6 +1254,11 @@ cudaError_t launch_conv_pack(const ConvArgs& a, void* packed, cudaStream_t s) {
       pack_filters_row_kernel<<<148 * 4, 256, 0, s>>>(
           a.filters, hi, lo, r.p.g, r.kind == kRouteRowOnN ? co_tile_n(a.co) : kTcBM, r.apack);
       break;
+    case kRouteShare:
+    case kRouteShareRes:
+      pack_filters_row_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, nullptr, r.p.g,
+                                                      (a.co + 7) / 8 * 8, r.apack);
+      break;
     default:
       pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, lo, r.p.g, r.p.K);
       break;
@@ -1106,6 +1296,8 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
     x_lo = bl;
   }
   ConvTcArgs t{a, r.p, w_hi, w_lo, x_hi, x_lo};
+  if (r.kind == kRouteShare || r.kind == kRouteShareRes)
+    return launch_chwn_share(t, r.kind == kRouteShareRes, s);
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
   return r.kind == kRouteChwnOnN ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);

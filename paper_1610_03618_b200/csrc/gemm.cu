@@ -45,6 +45,7 @@ struct GemmLoader {
   bool grouped;
   static constexpr bool kZeroSmem = false;
   static constexpr int kSteps = kTcBK / 8;
+  static constexpr bool kResidentA = false;
   __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
     return smem_desc_sw128(sa + k * 32, 16, 1024);
   }
@@ -83,10 +84,103 @@ struct GemmOut {
   uint32_t M, N;
   __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
                                           bool add) const {
-    if (m >= M || n0 >= N) return;
-    store_row32(c + m * ldc + n0, n0, N, v, add);
+    if (n0 >= N) return;  // warp-uniform
+    if (n0 + 32 <= N && ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(c) & 15u) == 0) {
+      warp_store_rows32(m < M ? c + m * ldc + n0 : nullptr, v, add);
+    } else if (m < M) {
+      store_row32(c + m * ldc + n0, n0, N, v, add);
+    }
   }
 };
+
+// fc layer on pre-packed weights (softmax.cpp:182-184 fc_forward with the
+// weights of a network layer, constant across forwards).  B = W^T packed once
+// K-major [n][k] (one 2D TMA box {32 k, 256 n} per stage, SWIZZLE_128B -- W
+// is row-major [k][n], and N = 1000-style widths would otherwise need eight
+// 32-column boxes per stage).  A = the activations, either K-major rows
+// [m][k] (an NCHW producer's flatten) or MN-major [k][m] (kAMn: a CHWN
+// producer -- the image index is contiguous, so the flatten the reference
+// performs before fc (net.cpp:258-262) becomes the operand load itself and
+// the transposing transform is skipped).
+template <bool kAMn>
+struct FcLoader {
+  CUtensorMap a[2];
+  CUtensorMap b[2];
+  bool a_grouped;  // MN-major A, m % 128 == 0: one 3D box {32, 32 k, 4 groups}
+  static constexpr bool kZeroSmem = false;
+  static constexpr bool kResidentA = false;
+  static constexpr int kSteps = kTcBK / 8;
+  __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
+    return kAMn ? smem_desc_sw128(sa + k * 1024, 4096, 512, 1) : smem_desc_sw128(sa + k * 32, 16, 1024);
+  }
+  __device__ uint64_t desc_b(const uint8_t* sb, int k) const {
+    return smem_desc_sw128(sb + k * 32, 16, 1024);
+  }
+  __device__ void prefetch() const {
+    tma_prefetch(&a[0]);
+    tma_prefetch(&b[0]);
+  }
+  __device__ uint32_t resident_bytes() const { return 0; }
+  __device__ void load_resident(void*, uint64_t*) const {}
+  __device__ uint32_t resident_offset(uint32_t) const { return 0; }
+  struct State {
+    uint32_t m0, n0;
+  };
+  __device__ State begin(uint32_t m0, uint32_t n0, uint32_t) const { return State{m0, n0}; }
+  __device__ void load(State& st, uint32_t seg, uint32_t k, void* sa, void* sb,
+                       uint64_t* bar) const {
+    const CUtensorMap* am = &a[seg == 2 ? 1 : 0];
+    const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
+    const int32_t k0 = static_cast<int32_t>(k * kTcBK);
+    if constexpr (kAMn) {
+      if (a_grouped) {
+        tma_load_3d(sa, am, bar, 0, k0, static_cast<int32_t>(st.m0 / 32));
+      } else {
+#pragma unroll
+        for (int j = 0; j < kTcBM / 32; ++j)
+          tma_load_2d(static_cast<uint8_t*>(sa) + j * 4096, am, bar,
+                      static_cast<int32_t>(st.m0 + 32 * j), k0);
+      }
+    } else {
+      tma_load_2d(sa, am, bar, k0, static_cast<int32_t>(st.m0));
+    }
+    tma_load_2d(sb, bm, bar, k0, static_cast<int32_t>(st.n0));
+  }
+};
+
+// packed[n][k] = W[k][n] (32 x 32 tiles through shared memory); with lo,
+// the 3xTF32 split of the same image
+__global__ void __launch_bounds__(256)
+    pack_fc_kernel(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo,
+                   uint32_t K, uint32_t N) {
+  __shared__ float t[32][33];
+  const uint32_t tiles_n = (N + 31) / 32, tiles = tiles_n * ((K + 31) / 32);
+  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint32_t k0 = tile / tiles_n * 32, n0 = tile % tiles_n * 32;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+      const uint32_t r = i / 32, c = i % 32;  // r: k, c: n (coalesced along n)
+      t[r][c] = (k0 + r < K && n0 + c < N) ? w[static_cast<uint64_t>(k0 + r) * N + n0 + c] : 0.0f;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+      const uint32_t r = i / 32, c = i % 32;  // r: n, c: k (coalesced along k)
+      if (n0 + r >= N || k0 + c >= K) continue;
+      const float v = t[c][r];
+      const uint64_t o = static_cast<uint64_t>(n0 + r) * K + k0 + c;
+      if (lo) {
+        uint32_t u;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
+        const float h = __uint_as_float(u);
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v - h));
+        hi[o] = h;
+        lo[o] = __uint_as_float(u);
+      } else {
+        hi[o] = v;
+      }
+    }
+  }
+}
 
 // 3xTF32 operand split: hi = x rounded to tf32 (low 13 mantissa bits zero,
 // so the tensor core consumes it exactly), lo = tf32(x - hi).
@@ -294,6 +388,94 @@ cudaError_t launch_gemm_fp32(const float* a, const float* b, float* c, uint64_t 
   const dim3 grid(static_cast<uint32_t>((n + 63) / 64), static_cast<uint32_t>((m + 63) / 64));
   gemm_fp32_simt_kernel<<<grid, 256, 0, s>>>(a, b, c, m, n, k);
   return cudaGetLastError();
+}
+
+// Packed fc weights: [hi | lo (3xTF32 only)], each n x k floats, 256-B aligned.
+size_t fc_packed_bytes(uint64_t k, uint64_t n, int precision) {
+  const uint64_t one = (n * k + 63) / 64 * 64 * sizeof(float);
+  return (precision == LCNN_PREC_3XTF32 ? 2 : 1) * one;
+}
+
+size_t fc_workspace_bytes(uint64_t m, uint64_t k, int precision) {
+  return precision == LCNN_PREC_3XTF32 ? 2 * ((m * k + 63) / 64 * 64) * sizeof(float) + 256 : 0;
+}
+
+cudaError_t launch_fc_pack(const float* w, uint64_t k, uint64_t n, int precision, void* packed,
+                           cudaStream_t s) {
+  float* hi = static_cast<float*>(packed);
+  float* lo = precision == LCNN_PREC_3XTF32 ? hi + fc_packed_bytes(k, n, precision) / 8 : nullptr;
+  const uint64_t tiles = ((n + 31) / 32) * ((k + 31) / 32);
+  const uint32_t grid = static_cast<uint32_t>(tiles < 148 * 8 ? tiles : 148 * 8);
+  pack_fc_kernel<<<grid, 256, 0, s>>>(w, hi, lo, static_cast<uint32_t>(k), static_cast<uint32_t>(n));
+  return cudaGetLastError();
+}
+
+namespace {
+
+// Skinny fc GEMMs (m = one batch) are pure stream-K; fragments as short as 4
+// k-blocks keep every SM streaming weights (fc8: 128 CTAs instead of 64).
+constexpr uint32_t kFcMinSkIters = 4;
+
+template <bool kAMn>
+cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t m, uint64_t n,
+                         uint64_t k, int precision, void* ws, cudaStream_t s) {
+  FcLoader<kAMn> L;
+  const float* b0 = static_cast<const float*>(packed);
+  const float* b1 = precision == LCNN_PREC_3XTF32 ? b0 + fc_packed_bytes(k, n, precision) / 8 : b0;
+  const float *a0 = x, *a1 = x;
+  if (precision == LCNN_PREC_3XTF32) {
+    float* ah = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+    float* al = ah + (m * k + 63) / 64 * 64;
+    cudaError_t e = launch_split_hilo(x, ah, al, m * k, s);
+    if (e != cudaSuccess) return e;
+    a0 = ah;
+    a1 = al;
+  }
+  if (!make_tmap_2d(&L.b[0], b0, k, n, k * 4, kTcBK, kPBN, false) ||
+      !make_tmap_2d(&L.b[1], b1, k, n, k * 4, kTcBK, kPBN, false))
+    return cudaErrorInvalidValue;
+  L.a_grouped = false;
+  if constexpr (kAMn) {
+    L.a_grouped = m % kTcBM == 0;
+    if (L.a_grouped) {
+      const uint64_t dims[3] = {32, k, m / 32};
+      const uint64_t pitch[2] = {m * 4, 128};
+      const uint32_t box[3] = {32, kTcBK, kTcBM / 32};
+      if (!make_tmap(&L.a[0], a0, 3, dims, pitch, box, nullptr, 1) ||
+          !make_tmap(&L.a[1], a1, 3, dims, pitch, box, nullptr, 1))
+        return cudaErrorInvalidValue;
+    } else if (!make_tmap_2d(&L.a[0], a0, m, k, m * 4, 32, kTcBK, true) ||
+               !make_tmap_2d(&L.a[1], a1, m, k, m * 4, 32, kTcBK, true)) {
+      return cudaErrorInvalidValue;
+    }
+  } else if (!make_tmap_2d(&L.a[0], a0, k, m, k * 4, kTcBK, kTcBM, false) ||
+             !make_tmap_2d(&L.a[1], a1, k, m, k * 4, kTcBK, kTcBM, false)) {
+    return cudaErrorInvalidValue;
+  }
+  Sched sc = make_sched(static_cast<uint32_t>((m + kTcBM - 1) / kTcBM),
+                        static_cast<uint32_t>((n + kPBN - 1) / kPBN),
+                        static_cast<uint32_t>((k + kTcBK - 1) / kTcBK),
+                        precision == LCNN_PREC_3XTF32 ? 3 : 1, kPBN, kAMn, false, kFcMinSkIters);
+  const uint32_t zc = sched_zero_col(sc, kPBN);
+  if (zc < n) {
+    cudaError_t e = cudaMemset2DAsync(c + zc, n * sizeof(float), 0, (n - zc) * sizeof(float), m, s);
+    if (e != cudaSuccess) return e;
+  }
+  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
+  return launch_persistent(L, O, sc, s);
+}
+
+}  // namespace
+
+bool fc_tc_supported(uint64_t m, uint64_t n, uint64_t k, bool a_mn) {
+  return m > 0 && n > 0 && k > 0 && k % 4 == 0 && (!a_mn || m % 4 == 0) && m < (1ull << 31) &&
+         n < (1ull << 31) && k < (1ull << 31);
+}
+
+cudaError_t launch_fc_packed(const float* x, bool a_mn, const void* packed, float* c, uint64_t m,
+                             uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s) {
+  return a_mn ? launch_fc_tc<true>(x, packed, c, m, n, k, precision, ws, s)
+              : launch_fc_tc<false>(x, packed, c, m, n, k, precision, ws, s);
 }
 
 }  // namespace lcnn_impl

@@ -68,6 +68,14 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
 bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a,
                        const void* b);
 size_t gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k, int precision);
+// fc on pre-packed weights (W^T, K-major); a_mn: x is [k][m] (CHWN producer)
+size_t fc_packed_bytes(uint64_t k, uint64_t n, int precision);
+size_t fc_workspace_bytes(uint64_t m, uint64_t k, int precision);
+bool fc_tc_supported(uint64_t m, uint64_t n, uint64_t k, bool a_mn);
+cudaError_t launch_fc_pack(const float* w, uint64_t k, uint64_t n, int precision, void* packed,
+                           cudaStream_t s);
+cudaError_t launch_fc_packed(const float* x, bool a_mn, const void* packed, float* c, uint64_t m,
+                             uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s);
 cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
                            uint64_t n, uint64_t k, int precision, void* ws,
                            cudaStream_t s);

@@ -59,18 +59,20 @@ struct TcCtl {
 //   void load_resident(void* dst, uint64_t* bar) const;  //   once per CTA, and
 //   uint32_t resident_offset(uint32_t kb) const;  //  k-block kb's B slice
 //   static constexpr bool kZeroSmem;  // stages carry never-loaded zero rows
+//   static constexpr bool kResidentA;  // the resident operand is A (else B)
 //   static constexpr int kSteps;      // K-steps per stage, 0 = Sched::ksteps
 // Segments chain operand sets into one accumulator (3 for 3xTF32).
 // Out concept:
 //   void store32(uint32_t m, uint32_t n0, const float* v, bool add) const;
 //       // row m, columns n0..n0+31; add = stream-K fragment (atomic add)
 constexpr int kPBN = 256, kPStages = 4;
+constexpr int kPStagesMax = 8;  // ring slots a Sched may ask for (small stages)
 constexpr uint32_t kPBBytes = kTcBK * kPBN * 4;            // 32 KB
 constexpr uint32_t kPStageBytes = kTcABytes + kPBBytes;    // 48 KB
 
 struct PCtl {
-  uint64_t full[kPStages];
-  uint64_t empty[kPStages];
+  uint64_t full[kPStagesMax];
+  uint64_t empty[kPStagesMax];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint64_t bres;  // resident B operand landed (Loader::resident_bytes() > 0)
@@ -137,7 +139,7 @@ inline int tc_sm_count() {
 constexpr uint32_t kMinSkIters = 8;
 
 inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, uint32_t bn,
-                        bool a_mn, bool b_mn) {
+                        bool a_mn, bool b_mn, uint32_t min_sk = kMinSkIters) {
   Sched s{};
   s.mt = mt;
   s.nt = nt;
@@ -163,7 +165,7 @@ inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, u
   } else {
     s.dp_tiles = tiles - rem;
     s.sk_iters = static_cast<uint64_t>(rem) * s.iters;
-    uint64_t c = s.sk_iters / kMinSkIters;
+    uint64_t c = s.sk_iters / min_sk;
     s.sk_ctas = static_cast<uint32_t>(c < 1 ? 1 : (c > g ? g : c));
   }
   const uint32_t dp_grid = s.dp_tiles < g ? s.dp_tiles : g;
@@ -265,9 +267,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     });
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // The whole warp walks the schedule (warp-uniform control flow keeps the
+    // descriptor arithmetic on the uniform datapath); one elected lane issues
+    // the MMAs and commits.  Every Loader's descriptors are affine in the
+    // K-step, so a stage needs two base descriptors and the per-step
+    // increments are kernel constants (the issue loop is then ~1 add per
+    // operand per MMA: at ~26 dependent instructions per MMA the issuing
+    // thread, not the tensor core, set the pace of narrow-K stages).
     const uint32_t idesc = sc.idesc;
+    const uint64_t dai = ld.desc_a(smem, 1) - ld.desc_a(smem, 0);
+    const uint64_t dbi = ld.desc_b(smem, 1) - ld.desc_b(smem, 0);
+    const uint32_t ksteps = Loader::kSteps > 0 ? static_cast<uint32_t>(Loader::kSteps) : sc.ksteps;
+    const bool mma_on = !(sc.probe & 1);
     uint32_t s = 0, phase = 0, local = 0;
     if (res_bytes) {
       mbar_wait(&ctl->bres, 0);
@@ -282,27 +295,44 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (uint32_t it = kbeg; it < kend; ++it) {
         mbar_wait(&ctl->full[s], phase);
         tc_fence_after();
-        const uint8_t* sa = smem + s * sc.stage_stride;
-        // resident B: the slice of k-block `it` (single segment when resident)
-        const uint8_t* sb = res_bytes ? smem + sc.resident_off + ld.resident_offset(it % sc.kbn)
-                                      : sa + sc.a_bytes;
-        if (sc.probe & 1) {
-        } else if constexpr (Loader::kSteps > 0) {
+        const uint8_t* slot = smem + s * sc.stage_stride;
+        // resident operand (B, or A when Loader::kResidentA): the slice of
+        // k-block `it` (single segment when resident)
+        const uint8_t* sres =
+            res_bytes ? smem + sc.resident_off + ld.resident_offset(it % sc.kbn) : nullptr;
+        const uint8_t* sa = Loader::kResidentA && res_bytes ? sres : slot;
+        const uint8_t* sb = Loader::kResidentA || !res_bytes ? slot + sc.a_bytes : sres;
+        const uint64_t da = ld.desc_a(sa, 0), db = ld.desc_b(sb, 0);
+        if (elect_one()) {
+          if (mma_on) {
+            mma_tf32(acc, da, db, idesc, it != kbeg);
+            uint64_t xa = da, xb = db;
+            if constexpr (Loader::kSteps > 0) {
 #pragma unroll
-          for (int k = 0; k < Loader::kSteps; ++k)
-            mma_tf32(acc, ld.desc_a(sa, k), ld.desc_b(sb, k), idesc, (it != kbeg) || (k != 0));
-        } else {
+              for (int k = 1; k < Loader::kSteps; ++k) {
+                xa += dai;
+                xb += dbi;
+                mma_tf32(acc, xa, xb, idesc, 1u);
+              }
+            } else {
 #pragma unroll 1
-          for (uint32_t k = 0; k < sc.ksteps; ++k)
-            mma_tf32(acc, ld.desc_a(sa, k), ld.desc_b(sb, k), idesc, (it != kbeg) || (k != 0));
+              for (uint32_t k = 1; k < ksteps; ++k) {
+                xa += dai;
+                xb += dbi;
+                mma_tf32(acc, xa, xb, idesc, 1u);
+              }
+            }
+          }
+          tc_commit(&ctl->empty[s]);
         }
-        tc_commit(&ctl->empty[s]);
+        __syncwarp();
         if (++s == nst) {
           s = 0;
           phase ^= 1;
         }
       }
-      tc_commit(&ctl->tfull[a]);
+      if (elect_one()) tc_commit(&ctl->tfull[a]);
+      __syncwarp();
     });
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
@@ -362,6 +392,58 @@ __device__ __forceinline__ void store_row32(float* row, uint32_t n0, uint32_t N,
   }
 }
 
+// Warp-cooperative store of 32 rows x 32 consecutive floats (lane = row, v =
+// its 32 accumulator columns) -- the channels-on-M epilogue, where a row is
+// an output channel and consecutive rows are far apart in memory.  Stored
+// lane by lane, every instruction would touch 32 lines with 16 B each; here
+// an 8 x 8 butterfly of 16-B chunks inside each 8-lane group (3 rounds of
+// shfl.xor) first gives lane l of group q chunk l of rows 8q..8q+7, so each
+// of the 8 store instructions writes 4 whole 128-byte lines.  rowp: this
+// lane's row start (16-B aligned) or nullptr to skip the row.  add: vector
+// atomic adds (stream-K fragments) -- those stay row-per-lane (one 16-B red
+// per line per instruction spreads over more L2 atomic units than 8 lanes
+// adding into the same line; measured on the fc layers).  All 32 lanes must
+// call it.
+__device__ __forceinline__ void warp_store_rows32(float* rowp, const float* v, bool add) {
+  if (add) {
+    if (rowp) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        atomicAdd(reinterpret_cast<float4*>(rowp + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+    }
+    return;
+  }
+  const uint32_t lane = threadIdx.x & 31, l8 = lane & 7, q8 = lane & ~7u;
+  float4 x[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+#pragma unroll
+  for (int b = 1; b < 8; b <<= 1) {
+    const bool hi = (l8 & b) != 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j & b) continue;
+      const float4 send = hi ? x[j] : x[j | b];
+      float4 r;
+      r.x = __shfl_xor_sync(0xffffffffu, send.x, b);
+      r.y = __shfl_xor_sync(0xffffffffu, send.y, b);
+      r.z = __shfl_xor_sync(0xffffffffu, send.z, b);
+      r.w = __shfl_xor_sync(0xffffffffu, send.w, b);
+      if (hi)
+        x[j] = r;
+      else
+        x[j | b] = r;
+    }
+  }
+  const unsigned long long mine = reinterpret_cast<unsigned long long>(rowp);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float* p = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, mine, q8 + j));
+    if (!p) continue;
+    __stcs(reinterpret_cast<float4*>(p) + l8, x[j]);
+  }
+}
+
 // Host launch of the persistent kernel (one dynamic-smem opt-in per
 // Loader/Out instantiation).
 template <class Loader, class Out>
@@ -374,7 +456,7 @@ cudaError_t launch_persistent(const Loader& ld, const Out& out, const Sched& sc,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStages)
+  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax)
     return cudaErrorInvalidConfiguration;
   kern<<<sc.grid, kTcThreads, sc.smem_bytes, s>>>(ld, out, sc);
   return cudaGetLastError();

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -35,5 +36,18 @@ Matrix fc_forward(const Matrix& in, const Matrix& weights);
 // raise DomainError; costs one 4-byte D2H + stream sync).
 DeviceMatrix softmax_fused(const DeviceMatrix& in, bool check_finite = true);
 DeviceMatrix fc_forward(const DeviceMatrix& in, const DeviceMatrix& weights);
+
+// fc with weights packed once (lcnn_fc_pack_weights; network layers reuse the
+// same weights every forward).  pack_fc_weights returns nullptr for FP32
+// precision (no packed path: fc_forward runs the reference-tolerance kernel).
+// The 4D form takes the producer tensor itself: CHWN is consumed in place as
+// the transposed operand (the flatten costs no transform), NCHW is already
+// the row-major matrix; other layouts are transformed to NCHW first.
+std::shared_ptr<DeviceBuffer> pack_fc_weights(const float* d_weights, std::uint32_t k,
+                                              std::uint32_t n, int precision);
+DeviceMatrix fc_forward_packed(const DeviceMatrix& in, const void* d_packed, std::uint32_t n,
+                               int precision);
+DeviceMatrix fc_forward_packed(const DeviceTensor4D& in, const void* d_packed, std::uint32_t n,
+                               int precision);
 
 }  // namespace lcnn

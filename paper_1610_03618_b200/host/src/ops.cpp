@@ -307,6 +307,50 @@ DeviceMatrix fc_forward(const DeviceMatrix& in, const DeviceMatrix& weights) {
 
 Matrix fc_forward(const Matrix& in, const Matrix& weights) { return gemm_blocked(in, weights); }
 
+std::shared_ptr<DeviceBuffer> pack_fc_weights(const float* d_weights, std::uint32_t k,
+                                              std::uint32_t n, int precision) {
+  const std::size_t bytes = lcnn_fc_packed_bytes(k, n, precision);
+  if (!bytes) return nullptr;
+  auto buf = std::make_shared<DeviceBuffer>(bytes);
+  check_status(lcnn_fc_pack_weights(d_weights, buf->get(), buf->bytes(), k, n, precision,
+                                    current_stream()));
+  return buf;
+}
+
+namespace {
+
+DeviceMatrix fc_packed_run(const float* x, int layout, std::uint32_t m, std::uint32_t k,
+                           const void* d_packed, std::uint32_t n, int precision) {
+  DeviceMatrix out(m, n);
+  const std::size_t ws = lcnn_fc_workspace_bytes(m, k, precision);
+  void* wsp = nullptr;
+  std::size_t wsb = 0;
+  if (ws) {
+    DeviceBuffer& buf = scratch(ws + 16);
+    wsp = buf.get();
+    wsb = buf.bytes();
+  }
+  check_status(lcnn_fc_forward_packed(x, layout, d_packed, out.data(), m, n, k, precision, wsp,
+                                      wsb, current_stream()));
+  return out;
+}
+
+}  // namespace
+
+DeviceMatrix fc_forward_packed(const DeviceMatrix& in, const void* d_packed, std::uint32_t n,
+                               int precision) {
+  return fc_packed_run(in.data(), LCNN_NCHW, in.rows, in.cols, d_packed, n, precision);
+}
+
+DeviceMatrix fc_forward_packed(const DeviceTensor4D& in, const void* d_packed, std::uint32_t n,
+                               int precision) {
+  const std::uint32_t k = in.c() * in.h() * in.w();
+  if (in.layout() == Layout::CHWN && in.n() % 4 == 0)
+    return fc_packed_run(in.data(), LCNN_CHWN, in.n(), k, d_packed, n, precision);
+  const DeviceTensor4D rows = in.layout() == Layout::NCHW ? in : transform(in, Layout::NCHW);
+  return fc_packed_run(rows.data(), LCNN_NCHW, rows.n(), k, d_packed, n, precision);
+}
+
 // ================================================================ conv ===
 std::pair<std::uint32_t, std::uint32_t> conv_output_extents(std::uint32_t h, std::uint32_t w,
                                                             std::uint32_t f_h, std::uint32_t f_w,

@@ -391,7 +391,34 @@ def gemm(a, b, m, n, k, precision=FP32, out=None, workspace=None, stream=None):
     return out
 
 
+def pack_fc_weights(weights, k, n, precision=TF32, stream=None):
+    """fc weights (k x n row-major CUDA tensor) packed once into the
+    tensor-core operand image (lcnn_fc_pack_weights) -> CUDA uint8 tensor."""
+    torch = _torch()
+    nbytes = capi.lib().lcnn_fc_packed_bytes(k, n, precision)
+    if nbytes == 0:
+        raise ValueError("fc: packed weights need TF32 or 3xTF32 precision")
+    packed = torch.empty(nbytes, dtype=torch.uint8, device=weights.device)
+    capi.call("lcnn_fc_pack_weights", weights.data_ptr(), packed.data_ptr(), nbytes, k, n,
+              precision, _stream(stream))
+    return packed
+
+
+def fc_forward_packed(x, x_layout, packed, m, n, k, precision=TF32, out=None, stream=None):
+    """y (m x n) = x . W on packed weights.  x_layout NCHW: x is m rows of k;
+    CHWN: x is [k][m] (a CHWN producer, flattened in the operand load)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(m * n, dtype=torch.float32, device=x.device)
+    nbytes = capi.lib().lcnn_fc_workspace_bytes(m, k, precision)
+    ws = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32, device=x.device)
+    capi.call("lcnn_fc_forward_packed", x.data_ptr(), x_layout, packed.data_ptr(), out.data_ptr(),
+              m, n, k, precision, ws.data_ptr(), ws.numel() * 4, _stream(stream))
+    return out
+
+
 __all__ = ["TF32", "X3TF32", "FP32", "conv_forward", "gemm", "pack_conv_filters",
+    "pack_fc_weights", "fc_forward_packed",
     "conv_forward_packed", "conv_output_extents",
     "NCHW", "CHWN", "NHWC", "HWCN", "MAX", "AVERAGE", "DeviceTensor4D", "DeviceMatrix",
     "TransformPlan", "PoolParams", "CoarseningPlan", "AccessReport", "PassReport",

@@ -18,6 +18,8 @@ struct Cfg {
   uint32_t a_layout, a_lbo, a_sbo, a_step;  // A descriptor: layout, LBO, SBO, K-step advance
   uint32_t b_layout, b_lbo, b_sbo, b_step;
   int per, iters;
+  int nacc = 1;  // independent accumulators the MMAs rotate over
+  int fused = 0;  // 1: the 4 MMAs of a group in one asm block (descriptor adds in PTX)
 };
 
 __global__ void __launch_bounds__(128, 1) mma_kernel(const __grid_constant__ Cfg c, unsigned long long* cyc) {
@@ -42,14 +44,38 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(const __grid_constant__ Cfg
   if (threadIdx.x == 0) {
     const uint8_t* sa = smem;
     const uint8_t* sb = smem + 48 * 1024;
+    // descriptors and accumulator addresses hoisted out of the loop, so the
+    // issue loop is just the MMAs (the first version of this bench rebuilt
+    // them per MMA and measured the single-thread issue cost, ~150 cycles)
+    uint64_t da[4], db[4];
+    uint32_t dt[4];
+    const uint32_t ncol = ((c.idesc >> 17) & 0x3F) * 8;
+    for (int k = 0; k < 4; ++k) {
+      da[k] = smem_desc_sw128(sa + k * c.a_step, c.a_lbo, c.a_sbo, c.a_layout);
+      db[k] = smem_desc_sw128(sb + k * c.b_step, c.b_lbo, c.b_sbo, c.b_layout);
+      dt[k] = taddr + (k % c.nacc) * ncol;
+    }
+    for (int k = 0; k < 4; ++k) mma_tf32(dt[k], da[k], db[k], c.idesc, 0u);
     const long long t0 = clock64();
     for (int it = 0; it < c.iters; ++it) {
       // a group may start once the group 4 back has completed (4-slot ring)
       if (it >= 4) mbar_wait(&bar[it & 3], ((it >> 2) - 1) & 1);
-      for (int k = 0; k < c.per; ++k)
-        mma_tf32(taddr, smem_desc_sw128(sa + (k % 4) * c.a_step, c.a_lbo, c.a_sbo, c.a_layout),
-                 smem_desc_sw128(sb + (k % 4) * c.b_step, c.b_lbo, c.b_sbo, c.b_layout), c.idesc,
-                 it | k);
+      if (c.fused) {
+        asm volatile(
+            "{\n.reg .b64 a1, a2, a3, b1, b2, b3;\n"
+            "add.s64 a1, %1, %3;\nadd.s64 a2, a1, %3;\nadd.s64 a3, a2, %3;\n"
+            "add.s64 b1, %2, %4;\nadd.s64 b2, b1, %4;\nadd.s64 b3, b2, %4;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %5, 1;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], a1, b1, %5, 1;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], a2, b2, %5, 1;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], a3, b3, %5, 1;\n}\n" ::"r"(dt[0]),
+            "l"(da[0]), "l"(db[0]), "l"(uint64_t(c.a_step >> 4)), "l"(uint64_t(c.b_step >> 4)),
+            "r"(c.idesc)
+            : "memory");
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mma_tf32(dt[k], da[k], db[k], c.idesc, 1u);
+      }
       tc_commit(&bar[it & 3]);
     }
     for (int it = c.iters - 4; it < c.iters; ++it) mbar_wait(&bar[it & 3], (it >> 2) & 1);
@@ -81,10 +107,10 @@ static void run(const char* name, Cfg c) {
   cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-  const double n_mma = double(c.iters) * c.per;
+  const double n_mma = double(c.iters) * 4;
   const uint32_t N = ((c.idesc >> 17) & 0x3F) * 8;
   const double tflops = 148.0 * n_mma * 2 * 128 * N * 8 / (ms * 1e9);
-  printf("%-40s N=%3u  %7.1f cyc/MMA  %7.1f TF/s  %s\n", name, N, double(h[0]) / n_mma, tflops,
+  printf("%-40s acc=%d N=%3u  %7.1f cyc/MMA  %7.1f TF/s  %s\n", name, c.nacc, N, double(h[0]) / n_mma, tflops,
          err == cudaSuccess ? "" : cudaGetErrorString(err));
   cudaFree(d);
 }
@@ -105,5 +131,33 @@ int main() {
     Cfg f{idesc_tf32(128, N, false, true), 2, 16, 1024, 32, 1, 4096, 512, 1024, 4, iters};
     run("A K-sw128       B MN-sw128_32b", f);
   }
+  for (uint32_t N : {32u, 64u, 96u, 128u, 192u, 256u}) {
+    Cfg c{idesc_tf32(128, N, true, false), 1, 4096, 512, 1024, 2, 16, 1024, 32, 4, iters, 1, 1};
+    run("fused-asm A MN-sw128_32b B K-sw128", c);
+  }
+  for (uint32_t N : {32u, 64u, 96u, 128u, 192u, 256u}) {
+    Cfg c{idesc_tf32(128, N, true, false), 1, 4096, 512, 1024, 2, 16, 1024, 32, 4, iters, 1, 1};
+    run("fused-asm A MN-sw128_32b B K-sw128", c);
+  }
+  // conv1 SHARE operands: A = filters K-major SWIZZLE_NONE core matrices
+  // (bn = 96 rows), B = input MN-major SW128_32B with overlapping atoms
+  // (LBO = 12 rows = 1536 B)
+  {
+    Cfg s{idesc_tf32(128, 256, false, true), 0, 1536, 128, 3072, 1, 1536, 512, 1024, 4, iters};
+    run("SHARE A K-none B MN-overlap(1536)", s);
+    Cfg t{idesc_tf32(128, 256, false, true), 0, 1536, 128, 3072, 1, 4096, 512, 1024, 4, iters};
+    run("SHARE A K-none B MN lbo4096", t);
+    Cfg u{idesc_tf32(128, 256, false, true), 2, 16, 1024, 32, 1, 1536, 512, 1024, 4, iters};
+    run("A K-sw128 B MN-overlap(1536)", u);
+    Cfg v{idesc_tf32(128, 256, false, true), 0, 2048, 128, 4096, 1, 4096, 512, 1024, 4, iters};
+    run("A K-none(bn=128) B MN lbo4096", v);
+  }
+  // independent accumulators: is ~150 cycles a per-MMA latency of one chain?
+  for (uint32_t N : {64u, 96u, 128u, 256u})
+    for (int nacc : {2, 4}) {
+      if (N * nacc > 512) continue;
+      Cfg c{idesc_tf32(128, N, true, false), 1, 4096, 512, 1024, 2, 16, 1024, 32, 4, iters, nacc};
+      run("A MN-sw128_32b  B K-sw128", c);
+    }
   return 0;
 }

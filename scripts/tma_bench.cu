@@ -22,7 +22,7 @@
     }                                                                      \
   } while (0)
 
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;  // ring slots (Cfg::stages, default 4)
 constexpr int kMaxBoxes = 16;
 
 struct Cfg {
@@ -35,6 +35,7 @@ struct Cfg {
   int32_t wrap[5];        // coordinate wraps (0 = none)
   int32_t cta_step[5];    // per-CTA offset
   int iters;
+  int stages;  // 0 = 4
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
@@ -45,7 +46,8 @@ template <int RANK, int NBOX>
 __global__ void __launch_bounds__(64, 1) tma_kernel(const __grid_constant__ Cfg c, uint64_t* sink) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kStages], empty[kStages];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  const int kStages = c.stages ? c.stages : 4;
   const uint32_t stage_bytes = c.nbox * c.box_bytes;
   const uint32_t stride = (stage_bytes + 1023) / 1024 * 1024;
   if (threadIdx.x == 0) {
@@ -171,7 +173,7 @@ KernFn pick_nbox(int n) {
 static void run(const char* name, Cfg& c, uint64_t* sink) {
   const uint32_t stage = c.nbox * c.box_bytes;
   const uint32_t stride = (stage + 1023) / 1024 * 1024;
-  const size_t smem = kStages * stride + 1024;
+  const size_t smem = (c.stages ? c.stages : 4) * stride + 1024;
   KernFn k = c.rank == 2 ? pick_nbox<2>(c.nbox)
              : (c.rank == 3 ? pick_nbox<3>(c.nbox)
                             : (c.rank == 4 ? pick_nbox<4>(c.nbox) : pick_nbox<5>(c.nbox)));
@@ -407,6 +409,47 @@ int main() {
       c.cta_step[1] = 8; c.cta_step[4] = 1;
       c.iters = iters;
       run("conv1 grouped 5D box{32,16,3,4,1} x2", c, sink);
+    }
+  }
+  // L: conv1 SHARE box: view {32 n, C, W, G, H} (rows ordered (w, c)), box
+  // {32, 3 c, 39 w, 1 g, 1 h}: 8 output pixels of one 32-image group per box
+  for (int slots : {3, 4, 6, 8}) {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[5] = {32, C, W, 4, H};
+    const uint64_t str[4] = {H * W * N * 4, N * 4, 128, W * N * 4};
+    const uint32_t box[5] = {32, 3, 39, 1, 1};
+    if (encode(&c.map, x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+      c.rank = 5;
+      c.nbox = 1;
+      c.box_bytes = 32 * 3 * 39 * 4;
+      c.step[4] = 1; c.wrap[4] = 216;   // filter rows / output rows
+      c.cta_step[2] = 32; c.wrap[2] = 190;
+      c.cta_step[3] = 1; c.wrap[3] = 4;
+      c.iters = iters;
+      c.stages = slots;
+      char name[64];
+      snprintf(name, sizeof(name), "conv1 SHARE box{32,3,39,1,1} x1 slots=%d", slots);
+      run(name, c, sink);
+    }
+  }
+  // M: same, 2 boxes per stage (2 groups)
+  {
+    Cfg c;
+    zero(c);
+    const uint64_t dims[5] = {32, C, W, 4, H};
+    const uint64_t str[4] = {H * W * N * 4, N * 4, 128, W * N * 4};
+    const uint32_t box[5] = {32, 3, 39, 1, 1};
+    if (encode(&c.map, x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+      c.rank = 5;
+      c.nbox = 2;
+      c.box_bytes = 32 * 3 * 39 * 4;
+      c.start[1][3] = 1;
+      c.step[4] = 1; c.wrap[4] = 216;
+      c.cta_step[2] = 32; c.wrap[2] = 190;
+      c.iters = iters;
+      c.stages = 4;
+      run("conv1 SHARE box x2 (2 groups) slots=4", c, sink);
     }
   }
   return 0;

@@ -155,3 +155,36 @@ def test_fc_identity_and_hand_product(cuda):
     b = torch.tensor([3.0, 4.0], device=cuda)
     for prec in (0, 1, 2):
         assert float(lcnn.gemm(a, b, 1, 1, 2, prec)[0]) == 11.0
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 4096, 9216), (128, 4096, 4096), (128, 1000, 4096),
+                                   (64, 1000, 4096), (256, 300, 96), (8, 37, 20), (132, 257, 36)])
+@pytest.mark.parametrize("precision", [0, 1])
+def test_fc_packed(cuda, m, n, k, precision):
+    """fc on packed weights (lcnn_fc_pack_weights + lcnn_fc_forward_packed),
+    x as NCHW rows [m][k] and as a CHWN producer [k][m]: same tolerances as
+    the GEMM (the operand bits are identical, only the load path differs)."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(m + n * k)
+    a = torch.rand(m, k, device=cuda, generator=g) * 2 - 1
+    w = torch.rand(k, n, device=cuda, generator=g) * 2 - 1
+    want = a.double() @ w.double()
+    bound = a.abs().double() @ w.abs().double()
+    packed = lcnn.pack_fc_weights(w.reshape(-1), k, n, precision)
+    for layout, x in ((NCHW, a.contiguous()), (CHWN, a.t().contiguous())):
+        if layout == CHWN and m % 4:
+            continue
+        got = lcnn.fc_forward_packed(x.reshape(-1), layout, packed, m, n, k, precision)
+        got = got.view(m, n).double()
+        err = (got - want).abs()
+        assert bool((err <= tolerance(precision, got, want, bound)).all()), \
+            (layout, float(err.max()))
+
+
+def test_fc_packed_rejects_fp32(cuda):
+    import torch
+
+    w = torch.zeros(64, device=cuda)
+    with pytest.raises(ValueError):
+        lcnn.pack_fc_weights(w, 8, 8, lcnn.FP32)
