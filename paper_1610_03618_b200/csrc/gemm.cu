@@ -105,7 +105,8 @@ struct GemmOut {
 template <bool kAMn>
 struct FcLoader {
   CUtensorMap a[2];
-  CUtensorMap b[2];
+  const float* bimg[2];  // packed weights hi / lo: swizzled stage images [nt][kb][256][32]
+  uint32_t kbn;          // k-blocks
   bool a_grouped;  // MN-major A, m % 128 == 0: one 3D box {32, 32 k, 4 groups}
   static constexpr bool kZeroSmem = false;
   static constexpr bool kResidentA = false;
@@ -116,10 +117,7 @@ struct FcLoader {
   __device__ uint64_t desc_b(const uint8_t* sb, int k) const {
     return smem_desc_sw128(sb + k * 32, 16, 1024);
   }
-  __device__ void prefetch() const {
-    tma_prefetch(&a[0]);
-    tma_prefetch(&b[0]);
-  }
+  __device__ void prefetch() const { tma_prefetch(&a[0]); }
   __device__ uint32_t resident_bytes() const { return 0; }
   __device__ void load_resident(void*, uint64_t*) const {}
   __device__ uint32_t resident_offset(uint32_t) const { return 0; }
@@ -130,7 +128,6 @@ struct FcLoader {
   __device__ void load(State& st, uint32_t seg, uint32_t k, void* sa, void* sb,
                        uint64_t* bar) const {
     const CUtensorMap* am = &a[seg == 2 ? 1 : 0];
-    const CUtensorMap* bm = &b[seg == 1 ? 1 : 0];
     const int32_t k0 = static_cast<int32_t>(k * kTcBK);
     if constexpr (kAMn) {
       if (a_grouped) {
@@ -144,39 +141,50 @@ struct FcLoader {
     } else {
       tma_load_2d(sa, am, bar, k0, static_cast<int32_t>(st.m0));
     }
-    tma_load_2d(sb, bm, bar, k0, static_cast<int32_t>(st.n0));
+    bulk_load(sb,
+              bimg[seg == 1 ? 1 : 0] + (static_cast<uint64_t>(st.n0 / kPBN) * kbn + k) * kPBN * kTcBK,
+              kPBN * kTcBK * 4, bar);
   }
 };
 
-// packed[n][k] = W[k][n] (32 x 32 tiles through shared memory); with lo,
-// the 3xTF32 split of the same image
+// The K-major SWIZZLE_128B stage images of W^T: img[((t * KB + kb) * 256 +
+// r) * 32 + (c ^ (r & 7)) * 4 + e] = W[k = kb*32 + 4c + e][n = t*256 + r]
+// (zero past k / n).  One thread per (n, 4-k chunk) group of the image; W is
+// read through a 32 x 33 shared tile so both sides stay coalesced.
 __global__ void __launch_bounds__(256)
     pack_fc_kernel(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo,
                    uint32_t K, uint32_t N) {
   __shared__ float t[32][33];
-  const uint32_t tiles_n = (N + 31) / 32, tiles = tiles_n * ((K + 31) / 32);
+  const uint32_t KB = (K + 31) / 32, NT = (N + kPBN - 1) / kPBN;
+  const uint32_t nblk = NT * (kPBN / 32);  // 32-row blocks of n
+  const uint32_t tiles = nblk * KB;
   for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const uint32_t k0 = tile / tiles_n * 32, n0 = tile % tiles_n * 32;
+    const uint32_t kb = tile % KB, nb = tile / KB;
+    const uint32_t k0 = kb * 32, n0 = nb * 32;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
       const uint32_t r = i / 32, c = i % 32;  // r: k, c: n (coalesced along n)
       t[r][c] = (k0 + r < K && n0 + c < N) ? w[static_cast<uint64_t>(k0 + r) * N + n0 + c] : 0.0f;
     }
     __syncthreads();
+    const uint32_t nt = n0 / kPBN, rbase = n0 % kPBN;
+    float* base_hi = hi + (static_cast<uint64_t>(nt) * KB + kb) * kPBN * 32;
+    float* base_lo = lo ? lo + (static_cast<uint64_t>(nt) * KB + kb) * kPBN * 32 : nullptr;
     for (uint32_t i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
-      const uint32_t r = i / 32, c = i % 32;  // r: n, c: k (coalesced along k)
-      if (n0 + r >= N || k0 + c >= K) continue;
-      const float v = t[c][r];
-      const uint64_t o = static_cast<uint64_t>(n0 + r) * K + k0 + c;
-      if (lo) {
+      const uint32_t rr = i / 32, slot = i % 32;  // image row (n) and float slot (coalesced)
+      const uint32_t r = rbase + rr;
+      const uint32_t kk = ((slot >> 2) ^ (r & 7)) * 4 + (slot & 3);
+      const float v = t[kk][rr];
+      const uint64_t o = static_cast<uint64_t>(r) * 32 + slot;
+      if (base_lo) {
         uint32_t u;
         asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
         const float h = __uint_as_float(u);
         asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v - h));
-        hi[o] = h;
-        lo[o] = __uint_as_float(u);
+        base_hi[o] = h;
+        base_lo[o] = __uint_as_float(u);
       } else {
-        hi[o] = v;
+        base_hi[o] = v;
       }
     }
   }
@@ -392,7 +400,7 @@ cudaError_t launch_gemm_fp32(const float* a, const float* b, float* c, uint64_t 
 
 // Packed fc weights: [hi | lo (3xTF32 only)], each n x k floats, 256-B aligned.
 size_t fc_packed_bytes(uint64_t k, uint64_t n, int precision) {
-  const uint64_t one = (n * k + 63) / 64 * 64 * sizeof(float);
+  const uint64_t one = ((n + kPBN - 1) / kPBN) * kPBN * ((k + 31) / 32) * 32 * sizeof(float);
   return (precision == LCNN_PREC_3XTF32 ? 2 : 1) * one;
 }
 
@@ -404,7 +412,7 @@ cudaError_t launch_fc_pack(const float* w, uint64_t k, uint64_t n, int precision
                            cudaStream_t s) {
   float* hi = static_cast<float*>(packed);
   float* lo = precision == LCNN_PREC_3XTF32 ? hi + fc_packed_bytes(k, n, precision) / 8 : nullptr;
-  const uint64_t tiles = ((n + 31) / 32) * ((k + 31) / 32);
+  const uint64_t tiles = ((n + kPBN - 1) / kPBN) * (kPBN / 32) * ((k + 31) / 32);
   const uint32_t grid = static_cast<uint32_t>(tiles < 148 * 8 ? tiles : 148 * 8);
   pack_fc_kernel<<<grid, 256, 0, s>>>(w, hi, lo, static_cast<uint32_t>(k), static_cast<uint32_t>(n));
   return cudaGetLastError();
@@ -431,9 +439,9 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
     a0 = ah;
     a1 = al;
   }
-  if (!make_tmap_2d(&L.b[0], b0, k, n, k * 4, kTcBK, kPBN, false) ||
-      !make_tmap_2d(&L.b[1], b1, k, n, k * 4, kTcBK, kPBN, false))
-    return cudaErrorInvalidValue;
+  L.bimg[0] = b0;
+  L.bimg[1] = b1;
+  L.kbn = static_cast<uint32_t>((k + kTcBK - 1) / kTcBK);
   L.a_grouped = false;
   if constexpr (kAMn) {
     L.a_grouped = m % kTcBM == 0;

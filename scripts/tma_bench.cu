@@ -36,6 +36,7 @@ struct Cfg {
   int32_t cta_step[5];    // per-CTA offset
   int iters;
   int stages;  // 0 = 4
+  const void* bulk_src;  // RANK 1: cp.async.bulk of box_bytes from bulk_src + v[0] * box_bytes
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
@@ -85,7 +86,14 @@ __global__ void __launch_bounds__(64, 1) tma_kernel(const __grid_constant__ Cfg 
 #pragma unroll
       for (int j = 0; j < NBOX; ++j, dst += c.box_bytes) {
         int32_t* v = x[j];
-        if (RANK == 2)
+        if (RANK == 1)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  sa(dst)),
+              "l"(reinterpret_cast<const uint8_t*>(c.bulk_src) + static_cast<uint64_t>(v[0]) * c.box_bytes),
+              "r"(c.box_bytes), "r"(sa(&full[s]))
+              : "memory");
+        else if (RANK == 2)
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
                   sa(dst)),
@@ -174,7 +182,7 @@ static void run(const char* name, Cfg& c, uint64_t* sink) {
   const uint32_t stage = c.nbox * c.box_bytes;
   const uint32_t stride = (stage + 1023) / 1024 * 1024;
   const size_t smem = (c.stages ? c.stages : 4) * stride + 1024;
-  KernFn k = c.rank == 2 ? pick_nbox<2>(c.nbox)
+  KernFn k = c.rank == 1 ? pick_nbox<1>(c.nbox) : c.rank == 2 ? pick_nbox<2>(c.nbox)
              : (c.rank == 3 ? pick_nbox<3>(c.nbox)
                             : (c.rank == 4 ? pick_nbox<4>(c.nbox) : pick_nbox<5>(c.nbox)));
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -203,8 +211,8 @@ int main() {
   // conv1 input, CHWN: N=128, W=H=227, C=3 (79 MB, L2-resident after warm-up)
   const uint64_t N = 128, W = 227, H = 227, C = 3;
   float* x;
-  CK(cudaMalloc(&x, N * W * H * C * 4 + 4096));
-  CK(cudaMemset(x, 0, N * W * H * C * 4));
+  CK(cudaMalloc(&x, 3000ull * 256 * 128 + 4096));
+  CK(cudaMemset(x, 0, 3000ull * 256 * 128));
   const int iters = 2000;
   auto zero = [](Cfg& c) { memset(&c, 0, sizeof(c)); };
 
@@ -409,6 +417,53 @@ int main() {
       c.cta_step[1] = 8; c.cta_step[4] = 1;
       c.iters = iters;
       run("conv1 grouped 5D box{32,16,3,4,1} x2", c, sink);
+    }
+  }
+  // N: contiguous weight images: 1D bulk copies vs a 2D tensor box over the
+  // same bytes ([rows][32] floats, pitch 128 B), 24 KB (192 rows) and 32 KB
+  for (int rows : {192, 256}) {
+    Cfg c;
+    zero(c);
+    c.rank = 1;
+    c.nbox = 1;
+    c.box_bytes = rows * 128;
+    c.bulk_src = x;
+    c.step[0] = 1; c.wrap[0] = 3000;
+    c.cta_step[0] = 20;
+    c.iters = iters;
+    char name[64];
+    snprintf(name, sizeof(name), "bulk 1D %d KB", rows / 8);
+    run(name, c, sink);
+    Cfg d;
+    zero(d);
+    const uint64_t dims[2] = {32, 3000ull * rows};
+    const uint64_t str[1] = {128};
+    const uint32_t box[2] = {32, (uint32_t)rows};
+    if (encode(&d.map, x, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
+      d.rank = 2;
+      d.nbox = 1;
+      d.box_bytes = rows * 128;
+      d.step[1] = rows; d.wrap[1] = 2990 * rows;
+      d.cta_step[1] = 20 * rows;
+      d.iters = iters;
+      snprintf(name, sizeof(name), "2D box{32,%d} contiguous SW128", rows);
+      run(name, d, sink);
+    }
+    // the strided original: box {32 k, rows} over a [rows][K] matrix with K = 2400
+    Cfg e;
+    zero(e);
+    const uint64_t dims2[2] = {2400, 1536};
+    const uint64_t str2[1] = {2400 * 4};
+    const uint32_t box2[2] = {32, (uint32_t)rows};
+    if (encode(&e.map, x, 2, dims2, str2, box2, CU_TENSOR_MAP_SWIZZLE_128B)) {
+      e.rank = 2;
+      e.nbox = 1;
+      e.box_bytes = rows * 128;
+      e.step[0] = 32; e.wrap[0] = 2400;
+      e.cta_step[1] = rows; e.wrap[1] = 1536 - rows;
+      e.iters = iters;
+      snprintf(name, sizeof(name), "2D box{32,%d} strided K=2400 SW128", rows);
+      run(name, e, sink);
     }
   }
   // L: conv1 SHARE box: view {32 n, C, W, G, H} (rows ordered (w, c)), box
