@@ -104,7 +104,10 @@ __global__ void pack_filters_kernel(const float* __restrict__ f, float* __restri
 // width) output channels.  kCoOnN picks the orientation:
 //   true : A = input (4 boxes = 128 columns), B = filters (N = bn channels)
 //   false: A = filters (128 channels),        B = input (8 boxes = 256 columns)
-template <bool kCoOnN>
+// kPair: the CTA-pair kernel (tc_gemm_pair) -- this CTA's 128 input columns
+// and half of the channel tile's filter rows, completing on the leader's
+// barrier (channels on N only).
+template <bool kCoOnN, bool kPair = false>
 struct ChwnConvLoader {
   CUtensorMap x[2];  // input hi / lo          (4D: {N, W, H, Ci}, or grouped 5D)
   CUtensorMap w[2];  // packed filters hi / lo (2D: {K, Co})
@@ -180,18 +183,34 @@ struct ChwnConvLoader {
     if (k == 0) st.fh = st.wofs = st.c0 = 0;  // a new segment restarts K
     uint8_t* sx = static_cast<uint8_t*>(kCoOnN ? sa : sb);
     const CUtensorMap* xm = &x[seg == 1 ? 1 : 0];
-    if (grouped) {
+    if constexpr (kPair) {
+      static_assert(kCoOnN, "pair mode puts the input columns on M");
+      const uint32_t lb = mapa_shared(smem_u32(bar), 0);  // the leader's full barrier
+      if (grouped) {
+        tma_load_5d_cg2(sx, xm, lb, 0, st.y0[0] + static_cast<int32_t>(st.wofs),
+                        static_cast<int32_t>(st.c0), st.n0[0],
+                        st.z0[0] + static_cast<int32_t>(st.fh));
+      } else {
 #pragma unroll
-      for (int j = 0; j < kBoxes / 4; ++j)
-        tma_load_5d(sx + j * 16384, xm, bar, 0, st.y0[j] + static_cast<int32_t>(st.wofs),
-                    static_cast<int32_t>(st.c0), st.n0[j], st.z0[j] + static_cast<int32_t>(st.fh));
+        for (int j = 0; j < kBoxes; ++j)
+          tma_load_4d_cg2(sx + j * 4096, xm, lb, st.n0[j], st.y0[j] + static_cast<int32_t>(st.wofs),
+                          st.z0[j] + static_cast<int32_t>(st.fh), static_cast<int32_t>(st.c0));
+      }
+      tma_load_2d_cg2(sb, &w[seg == 2 ? 1 : 0], lb, k * kTcBK, st.co0);
     } else {
+      if (grouped) {
 #pragma unroll
-      for (int j = 0; j < kBoxes; ++j)
-        tma_load_4d(sx + j * 4096, xm, bar, st.n0[j], st.y0[j] + static_cast<int32_t>(st.wofs),
-                    st.z0[j] + static_cast<int32_t>(st.fh), static_cast<int32_t>(st.c0));
+        for (int j = 0; j < kBoxes / 4; ++j)
+          tma_load_5d(sx + j * 16384, xm, bar, 0, st.y0[j] + static_cast<int32_t>(st.wofs),
+                      static_cast<int32_t>(st.c0), st.n0[j], st.z0[j] + static_cast<int32_t>(st.fh));
+      } else {
+#pragma unroll
+        for (int j = 0; j < kBoxes; ++j)
+          tma_load_4d(sx + j * 4096, xm, bar, st.n0[j], st.y0[j] + static_cast<int32_t>(st.wofs),
+                      st.z0[j] + static_cast<int32_t>(st.fh), static_cast<int32_t>(st.c0));
+      }
+      tma_load_2d(kCoOnN ? sb : sa, &w[seg == 2 ? 1 : 0], bar, k * kTcBK, st.co0);
     }
-    tma_load_2d(kCoOnN ? sb : sa, &w[seg == 2 ? 1 : 0], bar, k * kTcBK, st.co0);
     // advance: CI mode k = (fh, fw, ci/32); WIN mode k = (fh, ci/CIB)
     if (g.mode == kModeCI) {
       st.c0 += 32;
@@ -940,13 +959,13 @@ struct ConvTcArgs {
 // Zero the stream-K region of out[co][col] (whole tiles inside it are
 // overwritten by plain stores anyway).  co_on_n: tile rows are columns.
 cudaError_t zero_sk_region(const Sched& sc, bool co_on_n, uint32_t bw, float* dst,
-                           uint32_t ncols, uint32_t co, cudaStream_t s) {
+                           uint32_t ncols, uint32_t co, cudaStream_t s, uint32_t tm = kTcBM) {
   if (sc.dp_tiles >= sc.mt * sc.nt) return cudaSuccess;
   const uint32_t nt0 = sc.dp_tiles / sc.mt;
   uint32_t row0, col0;
   if (co_on_n) {
     row0 = nt0 * bw;
-    col0 = nt0 == sc.nt - 1 ? (sc.dp_tiles % sc.mt) * kTcBM : 0;
+    col0 = nt0 == sc.nt - 1 ? (sc.dp_tiles % sc.mt) * tm : 0;
   } else {
     row0 = 0;
     col0 = nt0 * kPBN;
@@ -1084,16 +1103,17 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
   return launch_persistent(L, O, sc, s);
 }
 
-template <bool kCoOnN>
+template <bool kCoOnN, bool kPair = false>
 cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   const ConvArgs& a = t.a;
   const TcPlan& p = t.p;
   const bool x3 = a.precision == LCNN_PREC_3XTF32;
-  const uint32_t bw = kCoOnN ? co_tile_n(a.co) : kTcBM;  // filter box rows
-  ChwnConvLoader<kCoOnN> L;
+  const uint32_t bw = kCoOnN ? co_tile_n(a.co) : kTcBM;  // filter tile rows
+  const uint32_t wbox = kPair ? bw / 2 : bw;              // rows one CTA loads
+  ChwnConvLoader<kCoOnN, kPair> L;
   const uint64_t K = p.K;
-  if (!make_tmap_2d(&L.w[0], t.w_hi, K, a.co, K * 4, kTcBK, bw, false) ||
-      !make_tmap_2d(&L.w[1], t.w_lo, K, a.co, K * 4, kTcBK, bw, false))
+  if (!make_tmap_2d(&L.w[0], t.w_hi, K, a.co, K * 4, kTcBK, wbox, false) ||
+      !make_tmap_2d(&L.w[1], t.w_lo, K, a.co, K * 4, kTcBK, wbox, false))
     return cudaErrorInvalidValue;
   const uint64_t dims[4] = {a.n, a.w, a.h, a.ci};
   const uint64_t pitch[3] = {static_cast<uint64_t>(a.n) * 4, static_cast<uint64_t>(a.w) * a.n * 4,
@@ -1116,6 +1136,25 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   L.g = p.g;
   L.ncols = a.ho * a.wo * a.n;
   const uint32_t segs = x3 ? 3 : 1;
+  if constexpr (kPair) {
+    // 256-column tiles on a CTA pair; per CTA a stage is its 128 input
+    // columns (16 KB) + half the filter tile
+    const uint32_t tm = 2 * kTcBM;
+    Sched sc = make_sched((L.ncols + tm - 1) / tm, (a.co + bw - 1) / bw, p.K / kTcBK, segs, bw,
+                          true, false, kMinSkIters, tc_sm_count() / 2);
+    sc.idesc = idesc_tf32(tm, bw, true, false);
+    sc.grid *= 2;
+    sc.a_bytes = kTcABytes;
+    sc.stage_bytes = kTcABytes + wbox * kTcBK * 4;
+    const uint32_t stride = (sc.stage_bytes + 1023) / 1024 * 1024;
+    uint32_t n = kPStagesMax;
+    while (n > 2 && 1024 + n * stride + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
+    sched_ring(sc, n, stride, 0);
+    if (cudaError_t e = zero_sk_region(sc, true, bw, a.dst, L.ncols, a.co, s, tm); e != cudaSuccess)
+      return e;
+    ColsOut O{a.dst, L.ncols, a.co};
+    return launch_pair(L, O, sc, s);
+  } else {
   const Sched sc =
       kCoOnN ? make_sched((L.ncols + kTcBM - 1) / kTcBM, (a.co + bw - 1) / bw, p.K / kTcBK, segs,
                           bw, true, false)
@@ -1130,6 +1169,7 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
     RowsOut O{a.dst, L.ncols, a.co, L.ncols};
     return launch_persistent(L, O, sc, s);
   }
+  }
 }
 
 // ---- routing, filter packing and the packed launch ------------------------
@@ -1141,7 +1181,7 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
 namespace {
 
 enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM,
-                 kRouteShare, kRouteShareRes };
+                 kRouteShare, kRouteShareRes, kRouteChwnPair };
 
 struct ConvRoute {
   RouteKind kind = kRouteSimt;
@@ -1202,7 +1242,24 @@ ConvRoute route_conv(const ConvArgs& a) {
     r.kind = on_n ? kRouteRowOnN : kRouteRowOnM;
     r.apack = static_cast<uint64_t>(pack_rows(a.co, on_n)) * r.p.K;
   } else {
-    r.kind = choose_co_on_n_traffic(a.co) ? kRouteChwnOnN : kRouteChwnOnM;
+    // CI / WIN: channels on N on a CTA pair (each SM streams half the filter
+    // tile) when the layer is long enough for >= 4 waves of 256-column pair
+    // tiles (measured on B200: conv2 137 -> 125 us; the 13x13 layers, 1-2
+    // ragged waves, run faster one CTA per tile); otherwise -- or with the
+    // profiling knob LCNN_CONV_PAIR=0 -- the orientation with more useful
+    // flops per operand byte
+    static const int pair_knob = [] {
+      const char* e = std::getenv("LCNN_CONV_PAIR");
+      return e ? (e[0] == '0' ? 0 : 2) : 1;  // 0 off, 2 forced on, 1 by waves
+    }();
+    const uint64_t pair_tiles =
+        (ncols + 2 * kTcBM - 1) / (2 * kTcBM) * ((a.co + co_tile_n(a.co) - 1) / co_tile_n(a.co));
+    const bool pair = pair_knob == 2 ||
+                      (pair_knob == 1 && pair_tiles >= 4ull * static_cast<uint64_t>(tc_sm_count() / 2));
+    if (pair)
+      r.kind = kRouteChwnPair;
+    else
+      r.kind = choose_co_on_n_traffic(a.co) ? kRouteChwnOnN : kRouteChwnOnM;
     r.apack = static_cast<uint64_t>(a.co) * r.p.K;
   }
   return r;
@@ -1300,6 +1357,7 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
     return launch_chwn_share(t, r.kind == kRouteShareRes, s);
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
+  if (r.kind == kRouteChwnPair) return launch_chwn_tc<true, true>(t, s);
   return r.kind == kRouteChwnOnN ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
 }
 

@@ -139,7 +139,7 @@ inline int tc_sm_count() {
 constexpr uint32_t kMinSkIters = 8;
 
 inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, uint32_t bn,
-                        bool a_mn, bool b_mn, uint32_t min_sk = kMinSkIters) {
+                        bool a_mn, bool b_mn, uint32_t min_sk = kMinSkIters, uint32_t units = 0) {
   Sched s{};
   s.mt = mt;
   s.nt = nt;
@@ -156,7 +156,7 @@ inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, u
   s.kbn = kbn;
   s.iters = kbn * segs;
   const uint32_t tiles = mt * nt;
-  const uint32_t g = static_cast<uint32_t>(tc_sm_count());
+  const uint32_t g = units ? units : static_cast<uint32_t>(tc_sm_count());
   const uint32_t rem = tiles % g;
   // a last wave that is >= 60% full (or a whole multiple) stays data-parallel:
   // measured on B200, the atomic tail beats an extra wave only below that
@@ -180,13 +180,14 @@ inline uint32_t sched_zero_col(const Sched& s, uint32_t bn) {
   return s.dp_tiles == s.mt * s.nt ? ~0u : (s.dp_tiles / s.mt) * bn;
 }
 
-// Calls f(tile, kbeg, kend, split) for this CTA's work, in order.
+// Calls f(tile, kbeg, kend, split) for work unit `id` of `count` (a CTA, or
+// a CTA pair), in order.
 template <class F>
-__device__ __forceinline__ void for_each_work(const Sched& s, F&& f) {
-  for (uint32_t t = blockIdx.x; t < s.dp_tiles; t += gridDim.x) f(t, 0u, s.iters, false);
-  if (blockIdx.x < s.sk_ctas) {
-    uint64_t lo = s.sk_iters * blockIdx.x / s.sk_ctas;
-    const uint64_t hi = s.sk_iters * (blockIdx.x + 1) / s.sk_ctas;
+__device__ __forceinline__ void for_each_work(const Sched& s, uint32_t id, uint32_t count, F&& f) {
+  for (uint32_t t = id; t < s.dp_tiles; t += count) f(t, 0u, s.iters, false);
+  if (id < s.sk_ctas) {
+    uint64_t lo = s.sk_iters * id / s.sk_ctas;
+    const uint64_t hi = s.sk_iters * (id + 1) / s.sk_ctas;
     while (lo < hi) {
       const uint32_t tr = static_cast<uint32_t>(lo / s.iters);
       const uint64_t base = static_cast<uint64_t>(tr) * s.iters;
@@ -196,6 +197,10 @@ __device__ __forceinline__ void for_each_work(const Sched& s, F&& f) {
       lo = base + ke;
     }
   }
+}
+template <class F>
+__device__ __forceinline__ void for_each_work(const Sched& s, F&& f) {
+  for_each_work(s, blockIdx.x, gridDim.x, static_cast<F&&>(f));
 }
 
 template <class Loader, class Out>
@@ -365,6 +370,151 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs (one TPC)
+// computes 256-row tiles (UMMA M = 256).  Each CTA loads its own 128 A rows
+// and HALF of the tile's B columns, so an SM ingests A + B/2 per stage
+// instead of A + B -- the lever for layers whose TMA delivery, not the tensor
+// pipe, sets the pace (conv2-5: filters are ~60% of each stage).  The leader
+// (rank 0) waits for both CTAs' bytes on its own full barrier (TMA
+// .cta_group::2 completes on a peer-CTA mbarrier), issues the M = 256 MMAs
+// and multicasts its commits to both CTAs' empty / tfull barriers; each CTA's
+// epilogue drains its own TMEM half and arrives on the leader's tempty.
+// Loader contract as above, plus: begin() receives this CTA's A-row and
+// B-column origins, and load() completes on the LEADER's barrier.
+template <class Loader, class Out>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+    tc_gemm_pair(const __grid_constant__ Loader ld, const __grid_constant__ Out out,
+                 const __grid_constant__ Sched sc) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  PCtl* ctl = reinterpret_cast<PCtl*>(smem + sc.ctl_off);
+  const uint32_t nst = sc.stages;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ld.prefetch();
+      for (uint32_t s = 0; s < nst; ++s) {
+        mbar_init(&ctl->full[s], 1);
+        mbar_init(&ctl->empty[s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&ctl->tfull[a], 1);
+        mbar_init(&ctl->tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc_cg2<512>(&ctl->tmem_addr);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers exist before any remote arrive or TMA completion
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_addr;
+  const uint32_t half_bn = sc.bn / 2;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    uint32_t s = 0, phase = 0;
+    for_each_work(sc, pair, npairs, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t ntile = t / sc.mt;
+      uint32_t seg = kbeg / sc.kbn, kb = kbeg - seg * sc.kbn;
+      auto st = ld.begin((t - ntile * sc.mt) * (2 * kTcBM) + rank * kTcBM,
+                         ntile * sc.bn + rank * half_bn, kb);
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        mbar_wait(&ctl->empty[s], phase ^ 1);
+        uint8_t* sa = smem + s * sc.stage_stride;
+        if (rank == 0) mbar_arrive_expect_tx(&ctl->full[s], 2 * sc.stage_bytes);
+        ld.load(st, seg, kb, sa, sa + sc.a_bytes, &ctl->full[s]);
+        if (++kb == sc.kbn) {
+          kb = 0;
+          ++seg;
+        }
+        if (++s == nst) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+    });
+  } else if (warp == 1 && rank == 0) {
+    // ---------------- MMA issuer (leader) ----------------
+    const uint32_t idesc = sc.idesc;
+    const uint64_t dai = ld.desc_a(smem, 1) - ld.desc_a(smem, 0);
+    const uint64_t dbi = ld.desc_b(smem, 1) - ld.desc_b(smem, 0);
+    const bool mma_on = !(sc.probe & 1);
+    uint32_t s = 0, phase = 0, local = 0;
+    for_each_work(sc, pair, npairs, [&](uint32_t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
+      mbar_wait(&ctl->tempty[a], aphase ^ 1);  // both epilogues drained this buffer
+      tc_fence_after();
+      const uint32_t acc = tmem + a * kPBN;
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        mbar_wait(&ctl->full[s], phase);
+        tc_fence_after();
+        const uint8_t* sa = smem + s * sc.stage_stride;
+        const uint64_t da = ld.desc_a(sa, 0), db = ld.desc_b(sa + sc.a_bytes, 0);
+        if (elect_one()) {
+          if (mma_on) {
+            mma_tf32_cg2(acc, da, db, idesc, it != kbeg);
+            uint64_t xa = da, xb = db;
+#pragma unroll
+            for (int k = 1; k < Loader::kSteps; ++k) {
+              xa += dai;
+              xb += dbi;
+              mma_tf32_cg2(acc, xa, xb, idesc, 1u);
+            }
+          }
+          tc_commit_cg2(&ctl->empty[s], 3);
+        }
+        __syncwarp();
+        if (++s == nst) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) tc_commit_cg2(&ctl->tfull[a], 3);
+      __syncwarp();
+    });
+  } else if (warp >= 2) {
+    // ---------------- epilogue (both CTAs: own TMEM half) ----------------
+    const int q = warp & 3;
+    const uint32_t leader_tempty = mapa_shared(smem_u32(&ctl->tempty[0]), 0);
+    uint32_t local = 0;
+    for_each_work(sc, pair, npairs, [&](uint32_t t, uint32_t, uint32_t, bool split) {
+      const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
+      const uint32_t ntile = t / sc.mt;
+      mbar_wait(&ctl->tfull[a], aphase);
+      tc_fence_after();
+      const uint32_t m = (t - ntile * sc.mt) * (2 * kTcBM) + rank * kTcBM + q * 32 + lane;
+      const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (uint32_t c = 0; c < sc.bn; c += 32) {
+        float v[32];
+        tmem_ld32(base + c, v);
+        if (!(sc.probe & 2)) out.store32(m, ntile * sc.bn + c, v, split);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty + a * 8);
+    });
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc_cg2<512>(tmem);
+  }
+}
+
 // Shared store of 32 consecutive accumulator columns of one row: plain
 // 128-bit stores for whole tiles, vector atomic adds for stream-K fragments.
 __device__ __forceinline__ void store_row32(float* row, uint32_t n0, uint32_t N, const float* v,
@@ -442,6 +592,22 @@ __device__ __forceinline__ void warp_store_rows32(float* rowp, const float* v, b
     if (!p) continue;
     __stcs(reinterpret_cast<float4*>(p) + l8, x[j]);
   }
+}
+
+template <class Loader, class Out>
+cudaError_t launch_pair(const Loader& ld, const Out& out, const Sched& sc, cudaStream_t s) {
+  auto kern = tc_gemm_pair<Loader, Out>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMaxDynSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax || sc.grid % 2)
+    return cudaErrorInvalidConfiguration;
+  kern<<<sc.grid, kTcThreads, sc.smem_bytes, s>>>(ld, out, sc);
+  return cudaGetLastError();
 }
 
 // Host launch of the persistent kernel (one dynamic-smem opt-in per

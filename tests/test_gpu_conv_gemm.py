@@ -84,6 +84,9 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     (128, 5, 15, 15, 130, 7, 2, 3),    # ROW, width 7 -> 8 (40 k-rows), ragged channel tile
     (128, 16, 10, 10, 48, 5, 2, 2),    # WIN
     (256, 64, 7, 7, 64, 3, 2, 0),      # CI, two blocks per pixel
+    # >= 4 waves of 256-column tiles: the CTA-pair (cta_group::2) kernel
+    (128, 32, 27, 27, 192, 3, 1, 1),   # CI, conv2-like channel tile (N = 192, 96 per CTA)
+    (128, 16, 27, 27, 48, 5, 1, 2),    # WIN
 ]
 
 
