@@ -294,7 +294,7 @@ lcnn_status lcnn_softmax_fused(const float* src, float* dst, uint32_t rows, uint
     return fail(LCNN_ESHAPE, "softmax: matrix too large");
   cudaError_t e = cudaSuccess;
   if (d_nonfinite) {
-    e = cudaMemsetAsync(d_nonfinite, 0, sizeof(int), S(stream));
+    e = lcnn_impl::launch_zero2d(d_nonfinite, 1, 1, 1, S(stream));
     if (e != cudaSuccess) return cuda_fail(e, "softmax_fused");
   }
   e = lcnn_impl::launch_softmax_fused(src, dst, rows, cols, d_nonfinite, S(stream));
@@ -321,7 +321,7 @@ lcnn_status lcnn_softmax_reference(const float* src, float* dst, uint32_t rows, 
     return fail(LCNN_EINVAL, "softmax_reference: scratch too small");
   cudaError_t e = cudaSuccess;
   if (d_nonfinite) {
-    e = cudaMemsetAsync(d_nonfinite, 0, sizeof(int), S(stream));
+    e = lcnn_impl::launch_zero2d(d_nonfinite, 1, 1, 1, S(stream));
     if (e != cudaSuccess) return cuda_fail(e, "softmax_reference");
   }
   e = lcnn_impl::launch_softmax_five_pass(src, dst, rows, cols, static_cast<float*>(d_scratch),

@@ -514,6 +514,7 @@ struct NchwConvParams {
 
 __global__ void __launch_bounds__(kNchwThreads, 1)
     tc_conv_nchw_kernel(const __grid_constant__ NchwConvParams prm) {
+  LCNN_PDL_ENTRY();
   extern __shared__ uint8_t raw_smem[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw_smem) + 1023) &
                                              ~uintptr_t(1023));
@@ -659,6 +660,7 @@ struct ConvGeomSimt {
 __global__ void __launch_bounds__(256)
     conv_chwn_simt_kernel(const float* __restrict__ x, const float* __restrict__ f,
                           float* __restrict__ y, ConvGeomSimt g) {
+  LCNN_PDL_ENTRY();
   const uint64_t total = static_cast<uint64_t>(g.Co) * g.Ho * g.Wo * g.N;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -691,6 +693,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     conv_nchw_simt_kernel(const float* __restrict__ x, const float* __restrict__ f,
                           float* __restrict__ y, ConvGeomSimt g) {
+  LCNN_PDL_ENTRY();
   const uint64_t total = static_cast<uint64_t>(g.N) * g.Co * g.Ho * g.Wo;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -902,7 +905,7 @@ cudaError_t launch_conv_nchw_tc(const ConvArgs& a, const float* wpack, uint32_t 
     attr = true;
   }
   const dim3 grid((prm.ncols + kTcBN - 1) / kTcBN, (a.co + kTcBM - 1) / kTcBM);
-  tc_conv_nchw_kernel<<<grid, kNchwThreads, kTcSmem, s>>>(prm);
+  lcnn_pdl::launch(tc_conv_nchw_kernel, grid, kNchwThreads, kTcSmem, s, prm);
   return cudaGetLastError();
 }
 
@@ -970,8 +973,7 @@ cudaError_t zero_sk_region(const Sched& sc, bool co_on_n, uint32_t bw, float* ds
     row0 = 0;
     col0 = nt0 * kPBN;
   }
-  return cudaMemset2DAsync(dst + uint64_t{row0} * ncols + col0, uint64_t{ncols} * 4, 0,
-                           uint64_t{ncols - col0} * 4, co - row0, s);
+  return launch_zero2d(dst + uint64_t{row0} * ncols + col0, ncols, ncols - col0, co - row0, s);
 }
 
 template <bool kCoOnN>
@@ -1096,7 +1098,7 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
   if (sc.dp_tiles < tiles) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
     const uint64_t col0 = static_cast<uint64_t>(sc.dp_tiles / (L.owb * L.groups)) * a.wo * a.n;
-    cudaError_t e = cudaMemset2DAsync(a.dst + col0, ncols * 4, 0, (ncols - col0) * 4, a.co, s);
+    cudaError_t e = launch_zero2d(a.dst + col0, ncols, ncols - col0, a.co, s);
     if (e != cudaSuccess) return e;
   }
   ShareOut O{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, L.owb, L.groups};
@@ -1334,9 +1336,9 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
     if (blocks > 148ull * 32) blocks = 148ull * 32;
     if (blocks == 0) blocks = 1;
     if (a.layout == LCNN_CHWN)
-      conv_chwn_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, w_hi, a.dst, g);
+      lcnn_pdl::launch(conv_chwn_simt_kernel, static_cast<uint32_t>(blocks), 256, 0, s, a.src, w_hi, a.dst, g);
     else
-      conv_nchw_simt_kernel<<<static_cast<uint32_t>(blocks), 256, 0, s>>>(a.src, w_hi, a.dst, g);
+      lcnn_pdl::launch(conv_nchw_simt_kernel, static_cast<uint32_t>(blocks), 256, 0, s, a.src, w_hi, a.dst, g);
     return cudaGetLastError();
   }
   if (r.kind == kRouteNchwTc) return launch_conv_nchw_tc(a, w_hi, r.kp, s);

@@ -190,6 +190,18 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Zero a 2D region of 32-bit words (stream-K output regions, the softmax
+// non-finite flag): a PDL kernel, so it does not break the layer chain the
+// way a cudaMemset node would.
+__global__ void __launch_bounds__(256)
+    zero2d_kernel(uint32_t* __restrict__ p, uint64_t pitch, uint64_t width, uint64_t total) {
+  LCNN_PDL_ENTRY();
+  for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
+    const uint64_t r = i / width;
+    p[r * pitch + (i - r * width)] = 0u;
+  }
+}
+
 // 3xTF32 operand split: hi = x rounded to tf32 (low 13 mantissa bits zero,
 // so the tensor core consumes it exactly), lo = tf32(x - hi).
 __device__ __forceinline__ float to_tf32(float x) {
@@ -200,6 +212,7 @@ __device__ __forceinline__ float to_tf32(float x) {
 
 __global__ void split_hilo_kernel(const float* __restrict__ x, float* __restrict__ hi,
                                   float* __restrict__ lo, uint64_t count) {
+  LCNN_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const float v = x[i];
@@ -216,6 +229,7 @@ __global__ void split_hilo_kernel(const float* __restrict__ x, float* __restrict
 __global__ void __launch_bounds__(256)
     gemm_fp32_simt_kernel(const float* __restrict__ a, const float* __restrict__ b,
                           float* __restrict__ c, uint64_t M, uint64_t N, uint64_t K) {
+  LCNN_PDL_ENTRY();
   __shared__ float sa[16][64 + 4];
   __shared__ float sb[16][64 + 4];
   const uint64_t m0 = blockIdx.y * 64ull, n0 = blockIdx.x * 64ull;
@@ -334,11 +348,21 @@ bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a, const 
          k < (1ull << 31);
 }
 
+cudaError_t launch_zero2d(void* p, uint64_t pitch_words, uint64_t width_words, uint64_t rows,
+                          cudaStream_t s) {
+  const uint64_t total = width_words * rows;
+  if (!total) return cudaSuccess;
+  uint64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  return lcnn_pdl::launch(zero2d_kernel, static_cast<uint32_t>(blocks), 256, 0, s,
+                          static_cast<uint32_t*>(p), pitch_words, width_words, total);
+}
+
 cudaError_t launch_split_hilo(const float* x, float* hi, float* lo, uint64_t count,
                               cudaStream_t s) {
   uint64_t blocks = (count + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  split_hilo_kernel<<<static_cast<uint32_t>(blocks ? blocks : 1), 256, 0, s>>>(x, hi, lo, count);
+  lcnn_pdl::launch(split_hilo_kernel, static_cast<uint32_t>(blocks ? blocks : 1), 256, 0, s, x, hi, lo, count);
   return cudaGetLastError();
 }
 
@@ -384,7 +408,7 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
                         precision == LCNN_PREC_3XTF32 ? 3 : 1, kPBN, false, true);
   const uint32_t zc = sched_zero_col(sc, kPBN);
   if (zc < n) {
-    cudaError_t e = cudaMemset2DAsync(c + zc, n * sizeof(float), 0, (n - zc) * sizeof(float), m, s);
+    cudaError_t e = launch_zero2d(c + zc, n, n - zc, m, s);
     if (e != cudaSuccess) return e;
   }
   GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
@@ -394,7 +418,7 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
 cudaError_t launch_gemm_fp32(const float* a, const float* b, float* c, uint64_t m, uint64_t n,
                              uint64_t k, cudaStream_t s) {
   const dim3 grid(static_cast<uint32_t>((n + 63) / 64), static_cast<uint32_t>((m + 63) / 64));
-  gemm_fp32_simt_kernel<<<grid, 256, 0, s>>>(a, b, c, m, n, k);
+  lcnn_pdl::launch(gemm_fp32_simt_kernel, grid, 256, 0, s, a, b, c, m, n, k);
   return cudaGetLastError();
 }
 
@@ -466,7 +490,7 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
                         precision == LCNN_PREC_3XTF32 ? 3 : 1, kPBN, kAMn, false, kFcMinSkIters);
   const uint32_t zc = sched_zero_col(sc, kPBN);
   if (zc < n) {
-    cudaError_t e = cudaMemset2DAsync(c + zc, n * sizeof(float), 0, (n - zc) * sizeof(float), m, s);
+    cudaError_t e = launch_zero2d(c + zc, n, n - zc, m, s);
     if (e != cudaSuccess) return e;
   }
   GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};

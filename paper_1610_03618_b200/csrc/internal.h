@@ -72,6 +72,9 @@ size_t gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k, int precision);
 size_t fc_packed_bytes(uint64_t k, uint64_t n, int precision);
 size_t fc_workspace_bytes(uint64_t m, uint64_t k, int precision);
 bool fc_tc_supported(uint64_t m, uint64_t n, uint64_t k, bool a_mn);
+// zero a region of rows x width 32-bit words, row pitch in words (PDL kernel)
+cudaError_t launch_zero2d(void* p, uint64_t pitch_words, uint64_t width_words, uint64_t rows,
+                          cudaStream_t s);
 cudaError_t launch_fc_pack(const float* w, uint64_t k, uint64_t n, int precision, void* packed,
                            cudaStream_t s);
 cudaError_t launch_fc_packed(const float* x, bool a_mn, const void* packed, float* c, uint64_t m,

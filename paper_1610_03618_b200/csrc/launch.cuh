@@ -1,0 +1,55 @@
+// Programmatic dependent launch (PDL) for the layer chain.  Every kernel of
+// the hot path is launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// and starts with lcnn_pdl::trigger() + lcnn_pdl::wait(): the next kernel in
+// the stream may be scheduled as soon as this one's CTAs retire, runs its
+// prologue (barrier init, TMEM allocation, tensor-map prefetch) on the freed
+// SMs, and blocks in griddepcontrol.wait until this grid has completed and
+// its memory is visible -- so layer i+1's ramp overlaps layer i's tail.  Every
+// PDL-launched kernel waits before its first global access, so a chain of
+// them stays ordered transitively.  LCNN_PDL=0 launches without the attribute
+// (griddepcontrol.wait is then a no-op).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <utility>
+
+namespace lcnn_pdl {
+
+__device__ __forceinline__ void wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LCNN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class... KArgs, class... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+}  // namespace lcnn_pdl
+
+#define LCNN_PDL_ENTRY()   \
+  do {                     \
+    lcnn_pdl::trigger();   \
+    lcnn_pdl::wait();      \
+  } while (0)

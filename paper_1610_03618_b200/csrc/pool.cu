@@ -64,6 +64,7 @@ __device__ __forceinline__ void store_out(float* p, typename Vec<VEC>::T v) {
 template <int WH, int WW, int S, int FH, int FW, int VEC, bool AVG>
 __global__ void __launch_bounds__(kThreads)
     pool_chwn_kernel(ChwnGeom g) {
+  LCNN_PDL_ENTRY();
   using T = typename Vec<VEC>::T;
   constexpr int UH = S * (FH - 1) + WH;
   constexpr int UW = S * (FW - 1) + WW;
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(kThreads)
 // Any window / stride, one output per thread (plain semantics).
 template <int VEC, bool AVG>
 __global__ void __launch_bounds__(kThreads) pool_chwn_generic_kernel(ChwnGeom g) {
+  LCNN_PDL_ENTRY();
   using T = typename Vec<VEC>::T;
   const uint32_t gid = blockIdx.x * kThreads + threadIdx.x;
   if (gid >= g.total) return;
@@ -199,6 +201,7 @@ __device__ __forceinline__ uint32_t stage_span(float* sm, const float* gp, uint3
 // for the auto-tuner to measure).
 template <int WH, int WW, int S, int FH, int FW, bool AVG>
 __global__ void __launch_bounds__(kThreads) pool_nchw_kernel(NchwGeom g) {
+  LCNN_PDL_ENTRY();
   extern __shared__ float sm[];
   constexpr int UH = S * (FH - 1) + WH;
   constexpr int UW = S * (FW - 1) + WW;
@@ -328,6 +331,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 template <int WH, int S, int FH, bool AVG>
 __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g) {
+  LCNN_PDL_ENTRY();
   extern __shared__ __align__(16) float ring[];
   __shared__ __align__(8) uint64_t bar[kPipe];
   __shared__ uint32_t meta[kPipe][2];  // (float offset of the span, floats copied)
@@ -438,6 +442,7 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
 // Runtime window, staged the same way, one output per thread.
 template <bool AVG>
 __global__ void __launch_bounds__(kThreads) pool_nchw_generic_kernel(NchwGeom g) {
+  LCNN_PDL_ENTRY();
   extern __shared__ float sm[];
   const uint32_t plane = blockIdx.x / g.nbands;
   const uint32_t b = blockIdx.x - plane * g.nbands;
@@ -473,6 +478,7 @@ __global__ void __launch_bounds__(kThreads)
                             uint64_t total, uint32_t H, uint32_t W, uint32_t Ho,
                             uint32_t Wo, uint32_t wh, uint32_t ww, uint32_t s,
                             float divisor) {
+  LCNN_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * kThreads) {
     const uint64_t ow = i % Wo;
@@ -532,8 +538,8 @@ inline uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
 template <int WH, int WW, int S, int FH, int FW, int VEC>
 cudaError_t chwn_launch(const ChwnGeom& g, bool avg, cudaStream_t st) {
   const uint32_t blocks = cdiv(g.total, kThreads);
-  if (avg) pool_chwn_kernel<WH, WW, S, FH, FW, VEC, true><<<blocks, kThreads, 0, st>>>(g);
-  else pool_chwn_kernel<WH, WW, S, FH, FW, VEC, false><<<blocks, kThreads, 0, st>>>(g);
+  if (avg) lcnn_pdl::launch(pool_chwn_kernel<WH, WW, S, FH, FW, VEC, true>, blocks, kThreads, 0, st, g);
+  else lcnn_pdl::launch(pool_chwn_kernel<WH, WW, S, FH, FW, VEC, false>, blocks, kThreads, 0, st, g);
   return cudaGetLastError();
 }
 
@@ -603,11 +609,11 @@ cudaError_t launch_pool_chwn(const PoolArgs& a, cudaStream_t st) {
   g.total = a.c * a.ho * a.wo * nv;
   const uint32_t blocks = cdiv(g.total, kThreads);
   if (vec) {
-    if (a.avg) pool_chwn_generic_kernel<4, true><<<blocks, kThreads, 0, st>>>(g);
-    else pool_chwn_generic_kernel<4, false><<<blocks, kThreads, 0, st>>>(g);
+    if (a.avg) lcnn_pdl::launch(pool_chwn_generic_kernel<4, true>, blocks, kThreads, 0, st, g);
+    else lcnn_pdl::launch(pool_chwn_generic_kernel<4, false>, blocks, kThreads, 0, st, g);
   } else {
-    if (a.avg) pool_chwn_generic_kernel<1, true><<<blocks, kThreads, 0, st>>>(g);
-    else pool_chwn_generic_kernel<1, false><<<blocks, kThreads, 0, st>>>(g);
+    if (a.avg) lcnn_pdl::launch(pool_chwn_generic_kernel<1, true>, blocks, kThreads, 0, st, g);
+    else lcnn_pdl::launch(pool_chwn_generic_kernel<1, false>, blocks, kThreads, 0, st, g);
   }
   return cudaGetLastError();
 }
@@ -623,7 +629,7 @@ cudaError_t nchw_launch(const NchwGeom& g, uint32_t blocks, uint32_t smem, bool 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<blocks, kThreads, smem, st>>>(g);
+  lcnn_pdl::launch(kern, blocks, kThreads, smem, st, g);
   return cudaGetLastError();
 }
 
@@ -651,7 +657,7 @@ cudaError_t pipe_launch(const NchwPipeGeom& g, uint32_t blocks, uint32_t smem, b
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<blocks, kThreads, smem, st>>>(g);
+  lcnn_pdl::launch(kern, blocks, kThreads, smem, st, g);
   return cudaGetLastError();
 }
 
@@ -733,10 +739,10 @@ cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t st) {
     if (blocks > 148ull * 64) blocks = 148ull * 64;
     const float div = static_cast<float>(a.win_h * a.win_w);
     if (a.avg)
-      pool_nchw_direct_kernel<true><<<static_cast<uint32_t>(blocks), kThreads, 0, st>>>(
+      lcnn_pdl::launch(pool_nchw_direct_kernel<true>, static_cast<uint32_t>(blocks), kThreads, 0, st,
           a.src, a.dst, total, a.h, a.w, a.ho, a.wo, a.win_h, a.win_w, a.stride, div);
     else
-      pool_nchw_direct_kernel<false><<<static_cast<uint32_t>(blocks), kThreads, 0, st>>>(
+      lcnn_pdl::launch(pool_nchw_direct_kernel<false>, static_cast<uint32_t>(blocks), kThreads, 0, st,
           a.src, a.dst, total, a.h, a.w, a.ho, a.wo, a.win_h, a.win_w, a.stride, div);
     return cudaGetLastError();
   }
@@ -777,7 +783,7 @@ cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t st) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem32);
     if (err != cudaSuccess) return err;
   }
-  kern<<<blocks, kThreads, smem32, st>>>(g);
+  lcnn_pdl::launch(kern, blocks, kThreads, smem32, st, g);
   return cudaGetLastError();
 }
 

@@ -52,6 +52,7 @@ template <int LPR, int VPL, bool VEC>
 __global__ void __launch_bounds__(kThreads, 4)
     softmax_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
                         uint32_t rows, uint32_t cols, int* flag) {
+  LCNN_PDL_ENTRY();
   constexpr int kGroups = kThreads / LPR;
   const uint32_t row = blockIdx.x * kGroups + threadIdx.x / LPR;
   const int lane = threadIdx.x % LPR;
@@ -149,6 +150,7 @@ template <int VPL, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     softmax_wide_kernel(const float* __restrict__ src, float* __restrict__ dst,
                         uint32_t cols, int* flag) {
+  LCNN_PDL_ENTRY();
   __shared__ float red[kThreads / 32];
   const float* in = src + static_cast<uint64_t>(blockIdx.x) * cols;
   float* out = dst + static_cast<uint64_t>(blockIdx.x) * cols;
@@ -211,6 +213,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     softmax_stream_kernel(const float* __restrict__ src, float* __restrict__ dst,
                           uint32_t cols, int* flag) {
+  LCNN_PDL_ENTRY();
   __shared__ float red_m[kThreads / 32], red_s[kThreads / 32];
   const float* in = src + static_cast<uint64_t>(blockIdx.x) * cols;
   float* out = dst + static_cast<uint64_t>(blockIdx.x) * cols;
@@ -257,6 +260,7 @@ template <int LPR>
 __global__ void __launch_bounds__(kThreads)
     row_max_kernel(const float* __restrict__ in, float* __restrict__ maxv, uint32_t rows,
                    uint32_t cols, int* flag) {
+  LCNN_PDL_ENTRY();
   const uint32_t row = blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
   const int lane = threadIdx.x % LPR;
   const int wl = threadIdx.x & 31;
@@ -279,6 +283,7 @@ template <int LPR>
 __global__ void __launch_bounds__(kThreads)
     row_sum_kernel(const float* __restrict__ in, float* __restrict__ sumv, uint32_t rows,
                    uint32_t cols) {
+  LCNN_PDL_ENTRY();
   const uint32_t row = blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
   const int lane = threadIdx.x % LPR;
   const int wl = threadIdx.x & 31;
@@ -294,6 +299,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     sub_rowvec_kernel(const float* __restrict__ in, const float* __restrict__ maxv,
                       float* __restrict__ out, uint64_t total, FastDiv div_cols) {
+  LCNN_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * kThreads)
     out[i] = in[i] - maxv[div_cols.div(static_cast<uint32_t>(i))];
@@ -301,6 +307,7 @@ __global__ void __launch_bounds__(kThreads)
 
 __global__ void __launch_bounds__(kThreads)
     exp_kernel(const float* __restrict__ in, float* __restrict__ out, uint64_t total) {
+  LCNN_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * kThreads)
     out[i] = expf(in[i]);
@@ -309,6 +316,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     scale_rowvec_kernel(const float* __restrict__ in, const float* __restrict__ sumv,
                         float* __restrict__ out, uint64_t total, FastDiv div_cols) {
+  LCNN_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * kThreads)
     out[i] = in[i] * (1.0f / sumv[div_cols.div(static_cast<uint32_t>(i))]);
@@ -327,16 +335,16 @@ cudaError_t rows_launch(const float* src, float* dst, uint32_t rows, uint32_t co
                         int* flag, cudaStream_t st) {
   constexpr int kGroups = kThreads / LPR;
   const uint32_t blocks = (rows + kGroups - 1) / kGroups;
-  if (vec) softmax_rows_kernel<LPR, VPL, true><<<blocks, kThreads, 0, st>>>(src, dst, rows, cols, flag);
-  else softmax_rows_kernel<LPR, VPL, false><<<blocks, kThreads, 0, st>>>(src, dst, rows, cols, flag);
+  if (vec) lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, true>, blocks, kThreads, 0, st, src, dst, rows, cols, flag);
+  else lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, false>, blocks, kThreads, 0, st, src, dst, rows, cols, flag);
   return cudaGetLastError();
 }
 
 template <int VPL>
 cudaError_t wide_launch(const float* src, float* dst, uint32_t rows, uint32_t cols, bool vec,
                         int* flag, cudaStream_t st) {
-  if (vec) softmax_wide_kernel<VPL, true><<<rows, kThreads, 0, st>>>(src, dst, cols, flag);
-  else softmax_wide_kernel<VPL, false><<<rows, kThreads, 0, st>>>(src, dst, cols, flag);
+  if (vec) lcnn_pdl::launch(softmax_wide_kernel<VPL, true>, rows, kThreads, 0, st, src, dst, cols, flag);
+  else lcnn_pdl::launch(softmax_wide_kernel<VPL, false>, rows, kThreads, 0, st, src, dst, cols, flag);
   return cudaGetLastError();
 }
 
@@ -363,7 +371,7 @@ cudaError_t launch_softmax_fused(const float* src, float* dst, uint32_t rows, ui
   if (cols <= 4096) return wide_launch<16>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 8192) return wide_launch<32>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 16384) return wide_launch<64>(src, dst, rows, cols, vec, flag, st);
-  softmax_stream_kernel<<<rows, kThreads, 0, st>>>(src, dst, cols, flag);
+  lcnn_pdl::launch(softmax_stream_kernel, rows, kThreads, 0, st, src, dst, cols, flag);
   return cudaGetLastError();
 }
 
@@ -377,11 +385,11 @@ cudaError_t launch_softmax_five_pass(const float* src, float* dst, uint32_t rows
   float* midv2 = midv1 + total;
   const FastDiv dc(cols);
   const uint32_t row_blocks = (rows + 7) / 8;  // 8 rows (warps) per CTA
-  row_max_kernel<32><<<row_blocks, kThreads, 0, st>>>(src, maxv, rows, cols, flag);
-  sub_rowvec_kernel<<<grid_for(total), kThreads, 0, st>>>(src, maxv, midv1, total, dc);
-  exp_kernel<<<grid_for(total), kThreads, 0, st>>>(midv1, midv2, total);
-  row_sum_kernel<32><<<row_blocks, kThreads, 0, st>>>(midv2, sumv, rows, cols);
-  scale_rowvec_kernel<<<grid_for(total), kThreads, 0, st>>>(midv2, sumv, dst, total, dc);
+  lcnn_pdl::launch(row_max_kernel<32>, row_blocks, kThreads, 0, st, src, maxv, rows, cols, flag);
+  lcnn_pdl::launch(sub_rowvec_kernel, grid_for(total), kThreads, 0, st, src, maxv, midv1, total, dc);
+  lcnn_pdl::launch(exp_kernel, grid_for(total), kThreads, 0, st, midv1, midv2, total);
+  lcnn_pdl::launch(row_sum_kernel<32>, row_blocks, kThreads, 0, st, midv2, sumv, rows, cols);
+  lcnn_pdl::launch(scale_rowvec_kernel, grid_for(total), kThreads, 0, st, midv2, sumv, dst, total, dc);
   return cudaGetLastError();
 }
 

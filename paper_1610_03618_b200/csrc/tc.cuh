@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "launch.cuh"
+
 namespace lcnn_tc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

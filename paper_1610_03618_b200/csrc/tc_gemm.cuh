@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = ctl->tmem_addr;
+  LCNN_PDL_ENTRY();  // the prologue above overlapped the previous kernel's tail
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
@@ -417,6 +418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   cluster_sync();  // the peer's barriers exist before any remote arrive or TMA completion
   tc_fence_after();
   const uint32_t tmem = ctl->tmem_addr;
+  LCNN_PDL_ENTRY();
   const uint32_t half_bn = sc.bn / 2;
 
   if (warp == 0 && lane == 0) {
@@ -606,8 +608,7 @@ cudaError_t launch_pair(const Loader& ld, const Out& out, const Sched& sc, cudaS
   }
   if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax || sc.grid % 2)
     return cudaErrorInvalidConfiguration;
-  kern<<<sc.grid, kTcThreads, sc.smem_bytes, s>>>(ld, out, sc);
-  return cudaGetLastError();
+  return lcnn_pdl::launch(kern, sc.grid, kTcThreads, sc.smem_bytes, s, ld, out, sc);
 }
 
 // Host launch of the persistent kernel (one dynamic-smem opt-in per
@@ -624,8 +625,7 @@ cudaError_t launch_persistent(const Loader& ld, const Out& out, const Sched& sc,
   }
   if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax)
     return cudaErrorInvalidConfiguration;
-  kern<<<sc.grid, kTcThreads, sc.smem_bytes, s>>>(ld, out, sc);
-  return cudaGetLastError();
+  return lcnn_pdl::launch(kern, sc.grid, kTcThreads, sc.smem_bytes, s, ld, out, sc);
 }
 
 }  // namespace lcnn_tc

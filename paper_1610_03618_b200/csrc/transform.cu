@@ -29,6 +29,7 @@ template <int TR, int TC, bool VLD, bool VST>
 __global__ void __launch_bounds__(kThreads)
     transpose2d_kernel(const float* __restrict__ src, float* __restrict__ dst,
                        uint32_t R, uint32_t C, uint32_t tiles_c) {
+  LCNN_PDL_ENTRY();
   static_assert(TR % 32 == 0 && TC % 32 == 0, "tile edges are warp multiples");
   constexpr int P = TC + 1;  // shared-memory pitch, == 1 (mod 32)
   __shared__ float tile[TR * P];
@@ -144,6 +145,7 @@ struct Dims4 {
 __global__ void __launch_bounds__(kThreads)
     permute4d_kernel(const float* __restrict__ src, float* __restrict__ dst,
                      uint64_t total, Dims4 d) {
+  LCNN_PDL_ENTRY();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
        i < total; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     // total < 2^32 (Tensor4D caps element counts at UINT32_MAX)
@@ -173,13 +175,13 @@ cudaError_t launch_tile(const float* src, float* dst, uint32_t R, uint32_t C,
   if (tiles > 0x7fffffffull) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<uint32_t>(tiles));
   if (vld && vst)
-    transpose2d_kernel<TR, TC, true, true><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+    lcnn_pdl::launch(transpose2d_kernel<TR, TC, true, true>, grid, kThreads, 0, s, src, dst, R, C, tiles_c);
   else if (vld)
-    transpose2d_kernel<TR, TC, true, false><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+    lcnn_pdl::launch(transpose2d_kernel<TR, TC, true, false>, grid, kThreads, 0, s, src, dst, R, C, tiles_c);
   else if (vst)
-    transpose2d_kernel<TR, TC, false, true><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+    lcnn_pdl::launch(transpose2d_kernel<TR, TC, false, true>, grid, kThreads, 0, s, src, dst, R, C, tiles_c);
   else
-    transpose2d_kernel<TR, TC, false, false><<<grid, kThreads, 0, s>>>(src, dst, R, C, tiles_c);
+    lcnn_pdl::launch(transpose2d_kernel<TR, TC, false, false>, grid, kThreads, 0, s, src, dst, R, C, tiles_c);
   return cudaGetLastError();
 }
 
@@ -237,7 +239,7 @@ cudaError_t launch_permute4d(const float* src, float* dst, uint32_t n,
   if (total == 0) return cudaSuccess;
   uint64_t blocks = (total + kThreads - 1) / kThreads;
   if (blocks > 148ull * 64) blocks = 148ull * 64;
-  permute4d_kernel<<<static_cast<uint32_t>(blocks), kThreads, 0, s>>>(src, dst, total, d);
+  lcnn_pdl::launch(permute4d_kernel, static_cast<uint32_t>(blocks), kThreads, 0, s, src, dst, total, d);
   return cudaGetLastError();
 }
 
