@@ -18,7 +18,7 @@ HOSTOBJ := $(patsubst $(PKG)/host/src/%.cpp,$(OBJDIR)/host_%.o,$(HOSTSRC))
 HOSTLIB := $(PKG)/lib/liblcnn.so
 HOSTFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -I$(PKG)/host/include -Iinclude -I$(CUDA)/include
 
-TOOLS   := build/tools/calibrate_b200
+TOOLS   := build/tools/calibrate_b200 build/tools/lcnn
 
 all: $(LIB) $(HOSTLIB) $(TOOLS) oracle
 

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "lcnn/conv.hpp"
+#include "lcnn/fixtures.hpp"
 #include "lcnn/layout.hpp"
 #include "lcnn/net.hpp"
 #include "lcnn/pool.hpp"
@@ -432,6 +433,48 @@ int ref_run_network(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
     *cols = m->cols;
     std::copy(m->data.begin(), m->data.end(), out);
   })
+}
+
+// fixture_list_csv (fixtures.cpp) -- the `lcnn fixtures --list` body
+const char* ref_fixture_list_csv(uint32_t scale) {
+  static std::string text;
+  try {
+    text = R::fixture_list_csv(scale);
+  } catch (...) {
+    map_current_exception();
+    return nullptr;
+  }
+  return text.c_str();
+}
+
+// The `lcnn run-net CONFIG --preset P --seed S` body of the reference CLI
+// (tools/lcnn.cpp:212-236): preset thresholds, annotation, a seeded input in
+// the first 4D layer's layout, run_network, timing_report_csv.
+const char* ref_run_net_cli(const char* json, const char* preset, uint64_t seed) {
+  static std::string text;
+  try {
+    R::NetworkSpec spec = R::parse_network(json);
+    const auto th = R::preset_by_name(preset);
+    if (!th) throw R::ValidationError("unknown preset");
+    spec = R::annotate_layouts(std::move(spec), *th);
+    R::Layout first = R::Layout::NCHW;
+    for (const R::LayerSpec& l : spec.layers)
+      if ((l.kind == R::LayerKind::Convolution || l.kind == R::LayerKind::Pooling) && l.layout_field) {
+        first = *l.layout_field;
+        break;
+      }
+    R::Tensor4D in(spec.n, spec.c, spec.h, spec.w, first);
+    std::mt19937 rng(static_cast<std::uint32_t>(seed));
+    std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+    for (std::uint64_t i = 0; i < in.size(); ++i) in.data()[i] = dist(rng);
+    R::RunOptions opt;
+    opt.seed = seed;
+    text = R::timing_report_csv(R::run_network(spec, in, opt).report);
+  } catch (...) {
+    map_current_exception();
+    return nullptr;
+  }
+  return text.c_str();
 }
 
 }  // extern "C"

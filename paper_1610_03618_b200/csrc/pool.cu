@@ -657,7 +657,7 @@ cudaError_t pipe_launch(const NchwPipeGeom& g, uint32_t blocks, uint32_t smem, b
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-  lcnn_pdl::launch(kern, blocks, kThreads, smem, st, g);
+  lcnn_pdl::launch_ex(false, kern, blocks, kThreads, smem, st, g);
   return cudaGetLastError();
 }
 
