@@ -745,11 +745,25 @@ def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     tf32_peak = float(peaks["bf16_tflops"]) / 2
     achieved = fl / (ns * 1e-9) / 1e12 if fl else None
+    # the tensor pipe's own TF32 rate, measured with back-to-back M=128 N=256
+    # tcgen05.mma on resident operands (scripts/mma_bench.cu, no memory traffic)
+    mma_peak = None
+    try:
+        import re as _re
+
+        rates = [float(m.group(1)) for m in _re.finditer(
+            r"N=256\s+\S+ cyc/MMA\s+(\S+) TF/s",
+            open(os.path.join(ROOT, "profiles", "r01_mma_bench.txt")).read())]
+        mma_peak = max(rates) if rates else None
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "kernel": f"{name} (tcgen05 kind::tf32 implicit GEMM)",
                 "achieved": round(achieved, 1) if achieved else None, "peak": tf32_peak,
                 "peak_source": "measured bf16 burst (MEASURED_PEAKS.json) / 2 = dense TF32",
                 "unit": "TFLOP/s", "frac": round(achieved / tf32_peak, 4) if achieved else None,
                 "traffic": (load_traffic("alexnet") or {}).get(name),
+                "mma_peak_measured": mma_peak,
+                "frac_of_mma_peak": round(achieved / mma_peak, 4) if achieved and mma_peak else None,
                 "avg_launch_ms": round(ns / 1e6, 4),
                 "forward_tflops": round(info["flops_per_image"] * batch / (ms / K / 1e3) / 1e12, 1),
                 "per_entry_us": {k: round(v / 1e3, 1) for k, v in prof}}
