@@ -72,6 +72,14 @@ class Op:
     name = "op"
     in_bytes = 0
     out_bytes = 0
+    rot = 1  # rotated input/output copies (single-op workloads smaller than 2x L2)
+    _i = 0   # launches so far (selects the copy)
+
+    def next_views(self):
+        """The (input, output) slices the next launch() will use."""
+        r = self._i % self.rot
+        nx, ny = self.in_bytes // 4, self.out_bytes // 4
+        return self.x[r * nx:(r + 1) * nx], self.y[r * ny:(r + 1) * ny]
 
     @property
     def bytes(self):
@@ -84,8 +92,17 @@ class Op:
         raise NotImplementedError
 
 
+def l2_rotations(torch, device, footprint):
+    """Input/output copies a single-op workload rotates over so that no
+    buffer is re-read from L2: enough to stream > 4x L2 between reuses when
+    one launch touches less than 2x L2 (SURVEY 8d timing method)."""
+    l2 = torch.cuda.get_device_properties(device).L2_cache_size or (126 << 20)
+    return max(1, min(16, -(-4 * l2 // footprint))) if footprint < 2 * l2 else 1
+
+
 class PoolOp(Op):
-    def __init__(self, torch, device, n, c, h, w, layout, win, stride, avg, plan, seed):
+    def __init__(self, torch, device, n, c, h, w, layout, win, stride, avg, plan, seed,
+                 rotate=False):
         from paper_1610_03618_b200 import capi
 
         self.capi = capi
@@ -96,10 +113,12 @@ class PoolOp(Op):
         self.ho = (h - win) // stride + 1
         self.wo = (w - win) // stride + 1
         g = torch.Generator(device=device).manual_seed(seed)
-        self.x = torch.rand(n * c * h * w, device=device, generator=g) * 2 - 1
-        self.y = torch.empty(n * c * self.ho * self.wo, device=device)
-        self.in_bytes = self.x.numel() * 4
-        self.out_bytes = self.y.numel() * 4
+        self.in_bytes = n * c * h * w * 4
+        self.out_bytes = n * c * self.ho * self.wo * 4
+        self.rot = l2_rotations(torch, device, self.in_bytes + self.out_bytes) if rotate else 1
+        self.x = torch.rand(self.rot * n * c * h * w, device=device, generator=g) * 2 - 1
+        self.y = torch.empty(self.rot * n * c * self.ho * self.wo, device=device)
+        self._i = 0
         kind = "plain" if plan is None else f"coarsened({plan[0]},{plan[1]})"
         lname = capi.LAYOUT_NAMES[layout]
         self.name = f"pool_{lname}_{kind}_{n}x{c}x{h}x{w}_w{win}s{stride}"
@@ -124,8 +143,11 @@ class PoolOp(Op):
 
     def launch(self, stream):
         if self._args is None:
-            self._args = self.bind(self.x.data_ptr(), self.y.data_ptr())
-        fn, args = self._args
+            self._args = [self.bind(self.x.data_ptr() + r * self.in_bytes,
+                                    self.y.data_ptr() + r * self.out_bytes)
+                          for r in range(self.rot)]
+        fn, args = self._args[self._i % self.rot]
+        self._i += 1
         st = fn(*args, stream)
         if st:
             self.capi.check(st, self.name)
@@ -149,8 +171,14 @@ class SoftmaxOp(Op):
         self.lib = capi.lib()
         self.rows, self.cols, self.fused = rows, cols, fused
         g = torch.Generator(device=device).manual_seed(seed)
-        self.x = torch.rand(rows * cols, device=device, generator=g) * 10 - 5
+        # L2 policy: a matrix pair smaller than the 126 MB L2 would stay
+        # resident between launches, so consecutive launches rotate over
+        # enough (input, output) pairs to stream > 2x L2 (>= 4
+        # rotated buffers larger than L2)
+        self.rot = l2_rotations(torch, device, 2 * rows * cols * 4)
+        self.x = torch.rand(self.rot * rows * cols, device=device, generator=g) * 10 - 5
         self.y = torch.empty_like(self.x)
+        self._i = 0
         nbytes = self.lib.lcnn_softmax_reference_scratch_bytes(rows, cols)
         self.scratch = None if fused else torch.empty(nbytes // 4, device=device)
         self.flag = torch.zeros(1, dtype=torch.int32, device=device)
@@ -170,8 +198,11 @@ class SoftmaxOp(Op):
 
     def launch(self, stream):
         if self._args is None:
-            self._args = self.bind(self.x.data_ptr(), self.y.data_ptr())
-        fn, args = self._args
+            step = self.rows * self.cols * 4
+            self._args = [self.bind(self.x.data_ptr() + r * step, self.y.data_ptr() + r * step)
+                          for r in range(self.rot)]
+        fn, args = self._args[self._i % self.rot]
+        self._i += 1
         st = fn(*args, stream)
         if st:
             self.capi.check(st, self.name)
@@ -238,10 +269,12 @@ def build_workload(name, torch, device, rank, plan):
     if name in ("pl5", "pl5_nchw"):
         layout = CHWN if name == "pl5" else NCHW
         p = plan or ((2, 2) if layout == CHWN else (3, 1))  # measured best (scripts/pool_plans.py)
-        ops = [PoolOp(torch, device, 128, 96, 55, 55, layout, 3, 2, False, p, seed)]
+        ops = [PoolOp(torch, device, 128, 96, 55, 55, layout, 3, 2, False, p, seed, rotate=True)]
         desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) max 3x3/s2, "
                             f"128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",
-                "batch_per_gpu": 128, "kernel": f"coarsened fh,fw={p[0]},{p[1]}"}
+                "batch_per_gpu": 128, "kernel": f"coarsened fh,fw={p[0]},{p[1]}",
+                "l2_policy": f"{ops[0].rot} rotated input/output pairs "
+                             f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB) between launches"}
         return ops, desc, 0, 128
     if name in ("softmax", "softmax5", "softmax_64k"):
         fused = name != "softmax5"
@@ -250,7 +283,10 @@ def build_workload(name, torch, device, rank, plan):
         desc = {"workload": f"BASELINE config 2: softmax classifier {rows}x1000, "
                             f"{'fused single kernel' if fused else 'five-kernel baseline'}"
                             + (" (HBM asymptote beyond the 4096-row config)" if rows > 4096 else ""),
-                "batch_per_gpu": rows}
+                "batch_per_gpu": rows,
+                "l2_policy": (f"{ops[0].rot} rotated input/output pairs "
+                              f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB > 2x L2) between launches"
+                              if ops[0].rot > 1 else "matrix pair > 2x L2")}
         return ops, desc, 0, rows
     if name == "transform":
         b = 128
@@ -588,10 +624,10 @@ def main():
                 "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (uniform[-1,1) from torch's on-device RNG)",
-                "config": dict(desc, parallelism=f"N-shard x{world} (no data-path collective)",
-                               l2_policy="each step streams "
-                                         f"{step_bytes / GB:.2f} GB per GPU (>> 126 MB L2) "
-                                         "between reuses of any buffer; no explicit flush"),
+                "config": {"l2_policy": f"each step streams {step_bytes / GB:.2f} GB per GPU "
+                                        "(>> 126 MB L2) between reuses of any buffer; no "
+                                        "explicit flush",
+                           **desc, "parallelism": f"N-shard x{world} (no data-path collective)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": K * len(ops), "clocks": clk, "impl": "ours",
                 "timing": "one CUDA graph of K launches" if use_graph else "stream launches"}
@@ -609,27 +645,28 @@ def run_e2e(torch, device, ops, world, steps, barrier, dist):
     comp = torch.cuda.current_stream(device)
     h2d = torch.cuda.Stream(device)
     d2h = torch.cuda.Stream(device)
-    hx = [op.x.cpu().pin_memory() for op in ops]
-    hy = [torch.empty(op.y.numel(), dtype=torch.float32).pin_memory() for op in ops]
+    hx = [op.next_views()[0].cpu().pin_memory() for op in ops]
+    hy = [torch.empty(op.out_bytes // 4, dtype=torch.float32).pin_memory() for op in ops]
     h2d_bytes = sum(op.in_bytes for op in ops)
     d2h_bytes = sum(op.out_bytes for op in ops)
 
     def one_step():
         done_in = []
-        for op, x in zip(ops, hx):
+        views = [op.next_views() for op in ops]
+        for (dx, _), x in zip(views, hx):
             with torch.cuda.stream(h2d):
-                op.x.copy_(x, non_blocking=True)
+                dx.copy_(x, non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(h2d)
             done_in.append(e)
-        for op, e, y in zip(ops, done_in, hy):
+        for op, (_, dy), e, y in zip(ops, views, done_in, hy):
             comp.wait_event(e)
             op.launch(comp.cuda_stream)
             k = torch.cuda.Event()
             k.record(comp)
             d2h.wait_event(k)
             with torch.cuda.stream(d2h):
-                y.copy_(op.y, non_blocking=True)
+                y.copy_(dy, non_blocking=True)
         fin = torch.cuda.Event()
         fin.record(d2h)
         comp.wait_event(fin)
