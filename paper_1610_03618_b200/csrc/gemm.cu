@@ -21,6 +21,9 @@
 // hi*hi + hi*lo + lo*hi into the same accumulator (hi = x rounded to tf32,
 // lo = tf32(x - hi), split by one elementwise kernel), giving ~fp32 accuracy.
 #include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
 #include <stdio.h>
 
 #include "../../include/lcnn_cuda.h"
@@ -107,6 +110,8 @@ struct FcLoader {
   CUtensorMap a[2];
   const float* bimg[2];  // packed weights hi / lo: swizzled stage images [nt][kb][256][32]
   uint32_t kbn;          // k-blocks
+  uint32_t bn;           // weight rows (output columns) one stage loads: 256, or 128
+  uint32_t pf_ahead;     // k-blocks of weights prefetched into L2 ahead of the TMA loads
   bool a_grouped;  // MN-major A, m % 128 == 0: one 3D box {32, 32 k, 4 groups}
   static constexpr bool kZeroSmem = false;
   static constexpr bool kResidentA = false;
@@ -141,9 +146,13 @@ struct FcLoader {
     } else {
       tma_load_2d(sa, am, bar, k0, static_cast<int32_t>(st.m0));
     }
-    bulk_load(sb,
-              bimg[seg == 1 ? 1 : 0] + (static_cast<uint64_t>(st.n0 / kPBN) * kbn + k) * kPBN * kTcBK,
-              kPBN * kTcBK * 4, bar);
+    // a 128-row half of a 256-row image tile keeps its swizzle phase (128 % 8 == 0)
+    const float* w = bimg[seg == 1 ? 1 : 0] +
+                     ((static_cast<uint64_t>(st.n0 / kPBN) * kbn + k) * kPBN + st.n0 % kPBN) * kTcBK;
+    bulk_load(sb, w, bn * kTcBK * 4, bar);
+    // the weight stage kPrefetch k-blocks ahead goes to L2 now
+    if (pf_ahead && k + pf_ahead < kbn)
+      bulk_prefetch_l2(w + static_cast<uint64_t>(pf_ahead) * kPBN * kTcBK, bn * kTcBK * 4);
   }
 };
 
@@ -466,6 +475,12 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
   L.bimg[0] = b0;
   L.bimg[1] = b1;
   L.kbn = static_cast<uint32_t>((k + kTcBK - 1) / kTcBK);
+  L.bn = kPBN;
+  static const uint32_t pf = [] {
+    const char* e = std::getenv("LCNN_FC_PREFETCH");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  L.pf_ahead = pf;  // measured: L2 prefetch ahead of the ring only slows fc (0 = off)
   L.a_grouped = false;
   if constexpr (kAMn) {
     L.a_grouped = m % kTcBM == 0;
@@ -484,10 +499,68 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
              !make_tmap_2d(&L.a[1], a1, k, m, k * 4, kTcBK, kTcBM, false)) {
     return cudaErrorInvalidValue;
   }
-  Sched sc = make_sched(static_cast<uint32_t>((m + kTcBM - 1) / kTcBM),
-                        static_cast<uint32_t>((n + kPBN - 1) / kPBN),
-                        static_cast<uint32_t>((k + kTcBK - 1) / kTcBK),
-                        precision == LCNN_PREC_3XTF32 ? 3 : 1, kPBN, kAMn, false, kFcMinSkIters);
+  const uint32_t mt = static_cast<uint32_t>((m + kTcBM - 1) / kTcBM);
+  const uint32_t segs = precision == LCNN_PREC_3XTF32 ? 3 : 1;
+  {
+    // cluster split-K when stream-K would leave each CTA fewer than 8
+    // k-iterations (fc8: 4 -- its fragment reductions then outweigh the
+    // loads; measured fc8 13.3 -> 10.8 us, while fc6 / fc7 at 31 / 14
+    // iterations per CTA stay faster on stream-K over all 148 SMs): the
+    // column tile (256 or 128) and split S <= 8 that put the most CTAs to
+    // work, each CTA keeping >= 4 k-iterations (ties: the wider tile)
+    const uint32_t sms = static_cast<uint32_t>(tc_sm_count()), iters = L.kbn * segs;
+    const uint64_t sk_total = static_cast<uint64_t>(mt) * ((n + kPBN - 1) / kPBN) * iters;
+    uint32_t best_bn = 0, best_s = 1, best_ctas = 0;
+    for (uint32_t bn : {static_cast<uint32_t>(kPBN), 128u}) {
+      const uint32_t tiles = mt * static_cast<uint32_t>((n + bn - 1) / bn);
+      uint32_t S = tiles ? sms / tiles : 0;
+      S = std::min({S, 8u, iters / 4});
+      if (S >= 2 && tiles * S > best_ctas) {
+        best_ctas = tiles * S;
+        best_bn = bn;
+        best_s = S;
+      }
+    }
+    static const bool splitk = [] {
+      const char* e = std::getenv("LCNN_FC_SPLITK");
+      return !(e && e[0] == '0');  // profiling knob: 0 = always stream-K
+    }();
+    if (best_s >= 2 && splitk && sk_total < 8ull * sms) {
+      L.bn = best_bn;
+      SplitK sk{};
+      sk.mt = mt;
+      sk.nt = static_cast<uint32_t>((n + best_bn - 1) / best_bn);
+      sk.kbn = L.kbn;
+      sk.iters = iters;
+      sk.S = best_s;
+      sk.bn = best_bn;
+      sk.idesc = idesc_tf32(kTcBM, best_bn, kAMn, false);
+      sk.a_bytes = kTcABytes;
+      sk.stage_bytes = kTcABytes + best_bn * kTcBK * 4;
+      sk.stage_stride = (sk.stage_bytes + 1023) / 1024 * 1024;
+      sk.stages = 0;
+      const uint32_t frag = kTcBM * kSplitPitch * 4;  // the parked fragment lives in the ring
+      for (uint32_t st = kPStagesMax; st >= 2 && !sk.stages; --st) {
+        const uint32_t ring = std::max(st * sk.stage_stride, (frag + 1023) / 1024 * 1024);
+        if (1024 + ring + 16 + sizeof(PCtl) <= kMaxDynSmem) {
+          sk.stages = st;
+          sk.ctl_off = ring;
+        }
+      }
+      sk.smem_bytes = 1024 + sk.ctl_off + static_cast<uint32_t>(sizeof(PCtl));
+      sk.M = static_cast<uint32_t>(m);
+      sk.N = static_cast<uint32_t>(n);
+      static const uint32_t probe = [] {
+        const char* e = std::getenv("LCNN_TC_PROBE");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+      }();
+      sk.probe = probe;
+      return launch_splitk(L, c, sk, s);
+    }
+  }
+  Sched sc = make_sched(mt, static_cast<uint32_t>((n + kPBN - 1) / kPBN),
+                        static_cast<uint32_t>((k + kTcBK - 1) / kTcBK), segs, kPBN, kAMn, false,
+                        kFcMinSkIters);
   const uint32_t zc = sched_zero_col(sc, kPBN);
   if (zc < n) {
     cudaError_t e = launch_zero2d(c + zc, n, n - zc, m, s);

@@ -596,6 +596,209 @@ __device__ __forceinline__ void warp_store_rows32(float* rowp, const float* v, b
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster split-K for skinny GEMMs (the fc layers: M = one batch of 128
+// rows): one output tile per cluster of S CTAs, CTA r accumulating the r-th
+// of S equal k-ranges in its own TMEM.  The S partial tiles are then summed
+// through distributed shared memory -- each CTA parks its fragment in its
+// (now idle) pipeline ring, and after a cluster barrier CTA r reduces rows
+// [r*128/S, (r+1)*128/S) of the tile by reading all S fragments over DSMEM
+// and writes them once with coalesced 128-bit stores.  No atomics, no
+// pre-zeroed output (so no memset node in the layer chain), and the sums are
+// bitwise reproducible (fixed order r = 0..S-1).
+struct SplitK {
+  uint32_t mt, nt;     // tiles along M (128 rows) and N (bn columns)
+  uint32_t iters;      // k-iterations per tile (k-blocks x segments)
+  uint32_t kbn;        // k-blocks per segment
+  uint32_t S;          // CTAs per cluster = k-ranges per tile
+  uint32_t bn, idesc, stage_bytes, a_bytes;
+  uint32_t stages, stage_stride, ctl_off, smem_bytes;
+  uint32_t M, N;       // output extents (row-major C, ldc = N)
+  uint32_t probe;
+};
+constexpr uint32_t kSplitPitch = kPBN + 4;  // fragment row pitch in floats (16-B skew per row)
+
+template <class Loader>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_gemm_splitk(const __grid_constant__ Loader ld, float* __restrict__ c,
+                   const __grid_constant__ SplitK sk) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  PCtl* ctl = reinterpret_cast<PCtl*>(smem + sk.ctl_off);
+  const uint32_t nst = sk.stages;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t tile = blockIdx.x / sk.S;
+  const uint32_t ntile = tile / sk.mt, m0 = (tile - ntile * sk.mt) * kTcBM, n0 = ntile * sk.bn;
+  const uint32_t kbeg = static_cast<uint32_t>(static_cast<uint64_t>(sk.iters) * rank / sk.S);
+  const uint32_t kend = static_cast<uint32_t>(static_cast<uint64_t>(sk.iters) * (rank + 1) / sk.S);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ld.prefetch();
+      for (uint32_t s = 0; s < nst; ++s) {
+        mbar_init(&ctl->full[s], 1);
+        mbar_init(&ctl->empty[s], 1);
+      }
+      mbar_init(&ctl->tfull[0], 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc<256>(&ctl->tmem_addr);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_addr;
+  LCNN_PDL_ENTRY();
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    uint32_t s = 0, phase = 0;
+    uint32_t seg = kbeg / sk.kbn, kb = kbeg - seg * sk.kbn;
+    auto st = ld.begin(m0, n0, kb);
+    for (uint32_t it = kbeg; it < kend; ++it) {
+      mbar_wait(&ctl->empty[s], phase ^ 1);
+      uint8_t* sa = smem + s * sk.stage_stride;
+      mbar_arrive_expect_tx(&ctl->full[s], sk.stage_bytes);
+      ld.load(st, seg, kb, sa, sa + sk.a_bytes, &ctl->full[s]);
+      if (++kb == sk.kbn) {
+        kb = 0;
+        ++seg;
+      }
+      if (++s == nst) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp-uniform, one elected lane) ----------------
+    const uint64_t dai = ld.desc_a(smem, 1) - ld.desc_a(smem, 0);
+    const uint64_t dbi = ld.desc_b(smem, 1) - ld.desc_b(smem, 0);
+    uint32_t s = 0, phase = 0;
+    for (uint32_t it = kbeg; it < kend; ++it) {
+      mbar_wait(&ctl->full[s], phase);
+      tc_fence_after();
+      const uint8_t* sa = smem + s * sk.stage_stride;
+      const uint64_t da = ld.desc_a(sa, 0), db = ld.desc_b(sa + sk.a_bytes, 0);
+      if (elect_one()) {
+        if (!(sk.probe & 1)) {
+          mma_tf32(tmem, da, db, sk.idesc, it != kbeg);
+          uint64_t xa = da, xb = db;
+#pragma unroll
+          for (int k = 1; k < Loader::kSteps; ++k) {
+            xa += dai;
+            xb += dbi;
+            mma_tf32(tmem, xa, xb, sk.idesc, 1u);
+          }
+        }
+        tc_commit(&ctl->empty[s]);
+      }
+      __syncwarp();
+      if (++s == nst) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+    if (elect_one()) tc_commit(&ctl->tfull[0]);
+    __syncwarp();
+  } else if (warp >= 2) {
+    // ---------------- park the fragment in the idle ring ----------------
+    // (every MMA -- the ring's last reader -- completed before tfull fires)
+    const int q = warp & 3;
+    mbar_wait(&ctl->tfull[0], 0);
+    tc_fence_after();
+    float* frag = reinterpret_cast<float*>(smem);
+    const uint32_t row = q * 32 + lane;
+    const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+    for (uint32_t col = 0; col < sk.bn; col += 32) {
+      float v[32];
+      tmem_ld32(base + col, v);
+      if (kend == kbeg || (sk.probe & 1)) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+      }
+      float4* d = reinterpret_cast<float4*>(frag + row * kSplitPitch + col);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // every fragment of the cluster is parked
+  // ---------------- DSMEM reduction: rows [rank*128/S, (rank+1)*128/S) ----------------
+  {
+    const uint32_t r0 = kTcBM * rank / sk.S, r1 = kTcBM * (rank + 1) / sk.S;
+    const uint32_t q4 = sk.bn / 4;  // float4 per row
+    const uint32_t frag0 = smem_u32(smem);
+    uint32_t src[16];
+    for (uint32_t j = 0; j < sk.S; ++j) src[j] = mapa_shared(frag0, j);
+    const bool vec = (sk.N % 4) == 0;
+    for (uint32_t i = threadIdx.x; i < (r1 - r0) * q4; i += blockDim.x) {
+      const uint32_t rr = r0 + i / q4, c4 = i % q4;
+      const uint32_t off = (rr * kSplitPitch + c4 * 4) * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t j = 0; j < sk.S; ++j) {
+        float4 v;
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "r"(src[j] + off));
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const uint32_t m = m0 + rr, n = n0 + c4 * 4;
+      if (m >= sk.M || n >= sk.N || (sk.probe & 2)) continue;
+      float* dst = c + static_cast<uint64_t>(m) * sk.N + n;
+      if (vec && n + 4 <= sk.N) {
+        __stcs(reinterpret_cast<float4*>(dst), acc);
+      } else {
+        const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (uint32_t e = 0; e < 4 && n + e < sk.N; ++e) dst[e] = a[e];
+      }
+    }
+  }
+  cluster_sync();  // peers finished reading this CTA's fragment
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+template <class Loader>
+cudaError_t launch_splitk(const Loader& ld, float* c, const SplitK& sk, cudaStream_t s) {
+  auto kern = tc_gemm_splitk<Loader>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMaxDynSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (sk.smem_bytes > kMaxDynSmem || sk.stages < 2 || sk.stages > kPStagesMax || sk.S < 1 ||
+      sk.S > 8)
+    return cudaErrorInvalidConfiguration;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sk.mt * sk.nt * sk.S);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = sk.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = sk.S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = lcnn_pdl::enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, ld, c, sk);
+}
+
 template <class Loader, class Out>
 cudaError_t launch_pair(const Loader& ld, const Out& out, const Sched& sc, cudaStream_t s) {
   auto kern = tc_gemm_pair<Loader, Out>;
