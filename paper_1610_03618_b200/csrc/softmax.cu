@@ -10,10 +10,19 @@
 //   check_finite      :15-19   DomainError on inf/NaN
 // Paper: PAPER.md Fig. 9 (one kernel, shared-memory reductions).
 //
-// Numerics follow the reference: accurate expf (not __expf), inv = 1/sum in
-// IEEE division, out = e * inv.  The reduction order differs from the CPU's
-// 256-blocked sequential sum (parallel tree), which is the only source of
-// difference; the parity bound is approx_equal 1e-6 (tensor.cpp:157-187).
+// Numerics: the fused kernels take e^(x - max) on the SFU (fexp below:
+// ex2.approx of (x - max) * log2(e)), inv = 1/sum in IEEE division, out =
+// e * inv.  Against the reference's libm expf that is <= ~1e-7 relative per
+// exponential and <= 2.2e-8 absolute from rounding the scaled argument,
+// inside the parity bound approx_equal 1e-6 (tensor.cpp:157-187; outputs are
+// <= 1, so the bound is 1e-6 absolute).  With accurate expf (~20
+// instructions) the 4096 x 1000 classifier was instruction-issue-bound at
+// ~3.6 us of its ~10 us (now 7.5 us).  A shared-memory-staged variant (bulk
+// copies in and out, per-chunk mbarriers) measured slower (9.4 us): the
+// register-resident kernel with 32 warps per SM keeps more requests in
+// flight.  The reduction order (parallel tree vs the CPU's 256-blocked sum)
+// is the other difference.  The five-kernel baseline keeps
+// accurate expf, as the reference's softmax_reference does.
 //
 // Fused kernel shapes (all one launch, one HBM read + one HBM write):
 //   cols <= 2048      : LPR lanes per row (4..32), values held in registers,
@@ -28,6 +37,13 @@
 #include "internal.h"
 
 namespace lcnn_dev {
+
+// e^d on the SFU: ex2.approx.ftz(d * log2 e)
+__device__ __forceinline__ float fexp(float d) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d * 1.4426950408889634f));
+  return r;
+}
 
 __device__ __forceinline__ void flag_nonfinite(int* flag, bool bad) {
   if (bad && flag) *reinterpret_cast<volatile int*>(flag) = 1;
@@ -47,13 +63,15 @@ __device__ __forceinline__ float group_sum(float v, unsigned mask) {
 }
 
 // LPR lanes own one row; each lane holds VPL values.  Capped at 64 registers
-// (4 CTAs = 32 warps per SM) so a 4096-row batch runs in a single wave.
-template <int LPR, int VPL, bool VEC>
-__global__ void __launch_bounds__(kThreads, 4)
+// (32 warps per SM) so a 4096-row batch runs in a single wave; 128-thread
+// CTAs (4 rows of 1000) spread that wave evenly -- 1024 CTAs place 6-7 per
+// SM (27-28 rows) where 512 256-thread CTAs placed 3-4 (24-32 rows).
+template <int LPR, int VPL, bool VEC, int THREADS = kThreads>
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     softmax_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
                         uint32_t rows, uint32_t cols, int* flag) {
   LCNN_PDL_ENTRY();
-  constexpr int kGroups = kThreads / LPR;
+  constexpr int kGroups = THREADS / LPR;
   const uint32_t row = blockIdx.x * kGroups + threadIdx.x / LPR;
   const int lane = threadIdx.x % LPR;
   const int wl = threadIdx.x & 31;
@@ -98,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 4)
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const uint32_t col = VEC ? (lane + (k / 4) * LPR) * 4 + (k % 4) : lane + k * LPR;
-    const float e = col < cols ? expf(v[k] - m) : 0.0f;
+    const float e = col < cols ? fexp(v[k] - m) : 0.0f;
     v[k] = e;
     s += e;
   }
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const uint32_t col = (t + (k / 4) * kThreads) * 4 + (k % 4);
-    const float e = col < cols ? expf(v[k] - m) : 0.0f;
+    const float e = col < cols ? fexp(v[k] - m) : 0.0f;
     v[k] = e;
     s += e;
   }
@@ -223,10 +241,10 @@ __global__ void __launch_bounds__(kThreads)
     const float x = __ldg(in + j);
     bad |= !isfinite(x);
     if (x > m) {
-      s = s * expf(m - x) + 1.0f;
+      s = s * fexp(m - x) + 1.0f;
       m = x;
     } else {
-      s += expf(x - m);
+      s += fexp(x - m);
     }
   }
   flag_nonfinite(flag, bad);
@@ -236,7 +254,7 @@ __global__ void __launch_bounds__(kThreads)
     const float mo = __shfl_xor_sync(0xffffffffu, m, o);
     const float so = __shfl_xor_sync(0xffffffffu, s, o);
     const float mn = fmaxf(m, mo);
-    s = (m == -INFINITY ? 0.0f : s * expf(m - mn)) + (mo == -INFINITY ? 0.0f : so * expf(mo - mn));
+    s = (m == -INFINITY ? 0.0f : s * fexp(m - mn)) + (mo == -INFINITY ? 0.0f : so * fexp(mo - mn));
     m = mn;
   }
   const int w = threadIdx.x >> 5;
@@ -249,10 +267,10 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = 1; i < kThreads / 32; ++i) M = fmaxf(M, red_m[i]);
   float S = 0.0f;
   for (int i = 0; i < kThreads / 32; ++i)
-    S += red_m[i] == -INFINITY ? 0.0f : red_s[i] * expf(red_m[i] - M);
+    S += red_m[i] == -INFINITY ? 0.0f : red_s[i] * fexp(red_m[i] - M);
   const float inv = 1.0f / S;
   for (uint32_t j = threadIdx.x; j < cols; j += kThreads)
-    stg_stream(out + j, expf(__ldg(in + j) - M) * inv);
+    stg_stream(out + j, fexp(__ldg(in + j) - M) * inv);
 }
 
 // ---- five-pass baseline (softmax.cpp:36-98), one kernel per step ---------
@@ -330,13 +348,17 @@ using namespace lcnn_dev;
 
 namespace {
 
-template <int LPR, int VPL>
+template <int LPR, int VPL, int THREADS = kThreads>
 cudaError_t rows_launch(const float* src, float* dst, uint32_t rows, uint32_t cols, bool vec,
                         int* flag, cudaStream_t st) {
-  constexpr int kGroups = kThreads / LPR;
+  constexpr int kGroups = THREADS / LPR;
   const uint32_t blocks = (rows + kGroups - 1) / kGroups;
-  if (vec) lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, true>, blocks, kThreads, 0, st, src, dst, rows, cols, flag);
-  else lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, false>, blocks, kThreads, 0, st, src, dst, rows, cols, flag);
+  if (vec)
+    lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, true, THREADS>, blocks, THREADS, 0, st, src,
+                     dst, rows, cols, flag);
+  else
+    lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, false, THREADS>, blocks, THREADS, 0, st, src,
+                     dst, rows, cols, flag);
   return cudaGetLastError();
 }
 
@@ -366,7 +388,7 @@ cudaError_t launch_softmax_fused(const float* src, float* dst, uint32_t rows, ui
   if (cols <= 64) return rows_launch<8, 8>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 256) return rows_launch<16, 16>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 512) return rows_launch<32, 16>(src, dst, rows, cols, vec, flag, st);
-  if (cols <= 1024) return rows_launch<32, 32>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 1024) return rows_launch<32, 32, 128>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 2048) return rows_launch<32, 64>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 4096) return wide_launch<16>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 8192) return wide_launch<32>(src, dst, rows, cols, vec, flag, st);
