@@ -35,6 +35,7 @@ Matrix fc_forward(const Matrix& in, const Matrix& weights);
 // Device-resident forms (check_finite = read the non-finite flag back and
 // raise DomainError; costs one 4-byte D2H + stream sync).
 DeviceMatrix softmax_fused(const DeviceMatrix& in, bool check_finite = true);
+void softmax_fused_into(const DeviceMatrix& in, DeviceMatrix& out, bool check_finite = true);
 DeviceMatrix fc_forward(const DeviceMatrix& in, const DeviceMatrix& weights);
 
 // fc with weights packed once (lcnn_fc_pack_weights; network layers reuse the

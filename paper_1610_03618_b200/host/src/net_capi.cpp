@@ -118,11 +118,15 @@ int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout, f
     const lcnn::NetworkSpec& s = net->net->spec();
     const lcnn::DeviceTensor4D in = lcnn::DeviceTensor4D::wrap(const_cast<float*>(d_input), s.n,
                                                                s.c, s.h, s.w, L(in_layout));
-    const lcnn::DeviceMatrix out = net->net->forward(in);
-    const cudaError_t e =
-        cudaMemcpyAsync(d_output, out.data(), std::size_t{out.rows} * out.cols * sizeof(float),
-                        cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+    // a network ending in softmax writes d_output directly (no copy node
+    // between forwards, which would also break the PDL chain)
+    const lcnn::DeviceMatrix out = net->net->forward(in, nullptr, d_output);
+    if (out.data() != d_output) {
+      const cudaError_t e =
+          cudaMemcpyAsync(d_output, out.data(), std::size_t{out.rows} * out.cols * sizeof(float),
+                          cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+      if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+    }
   })
 }
 

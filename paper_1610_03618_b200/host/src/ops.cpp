@@ -239,13 +239,18 @@ CoarseningPlan autotune_pool(std::uint32_t n, std::uint32_t c, std::uint32_t h, 
 }
 
 // ============================================================= softmax ===
-DeviceMatrix softmax_fused(const DeviceMatrix& in, bool check_finite) {
+void softmax_fused_into(const DeviceMatrix& in, DeviceMatrix& out, bool check_finite) {
   if (in.rows < 1 || in.cols < 1) throw ShapeError("softmax: empty matrix");
-  DeviceMatrix out(in.rows, in.cols);
+  if (out.rows != in.rows || out.cols != in.cols) throw ShapeError("softmax: output dims");
   int* flag = check_finite ? nonfinite_flag() : nullptr;
   check_status(lcnn_softmax_fused(in.data(), out.data(), in.rows, in.cols, 16384, flag, nullptr,
                                   current_stream()));
   if (flag && read_flag(flag)) throw DomainError("softmax: non-finite input");
+}
+
+DeviceMatrix softmax_fused(const DeviceMatrix& in, bool check_finite) {
+  DeviceMatrix out(in.rows, in.cols);
+  softmax_fused_into(in, out, check_finite);
   return out;
 }
 
