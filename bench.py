@@ -482,7 +482,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg_pools",
                     choices=["vgg_pools", "vgg_pools_nchw", "pl5", "pl5_nchw", "softmax", "softmax5",
-                             "softmax_64k", "transform", "alexnet"])
+                             "softmax_64k", "transform", "alexnet", "vgg16"])
     ap.add_argument("--plan", type=int, nargs=2, default=None,
                     help="coarsening fh fw (default: (1,1) for non-overlapping 2x2/s2 VGG pools, "
                          "(2,2) for overlapping 3x3/s2, measured best on B200)")
@@ -501,8 +501,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        if args.workload == "alexnet":
-            run_reference_alexnet(args, rank, world)
+        if args.workload in NETWORKS:
+            run_reference_network(args, rank, world)
         else:
             run_reference_arm(args, rank, world)
         return
@@ -519,8 +519,8 @@ def main():
         if world > 1:
             dist.barrier()
 
-    if args.workload == "alexnet":
-        run_alexnet(args, torch, dist, rank, world, local, device, barrier)
+    if args.workload in NETWORKS:
+        run_network_workload(args, torch, dist, rank, world, local, device, barrier)
         if world > 1:
             dist.destroy_process_group()
         return
@@ -697,11 +697,42 @@ def run_e2e(torch, device, ops, world, steps, barrier, dist):
                     "copy engines overlapped across layers"}
 
 
-# --------------------------------------------------------------- alexnet ---
-ALEXNET = os.path.join(ROOT, "configs", "alexnet.json")
-ALEXNET_CONV = {"conv1": (3, 96, 11, 55), "conv2": (96, 192, 5, 27), "conv3": (192, 384, 3, 13),
-                "conv4": (384, 256, 3, 13), "conv5": (256, 256, 3, 13)}
-ALEXNET_FC = {"fc6": (9216, 4096), "fc7": (4096, 4096), "fc8": (4096, 1000)}
+# ------------------------------------------------------ whole networks ---
+NETWORKS = {
+    "alexnet": (os.path.join(ROOT, "configs", "alexnet.json"),
+                "BASELINE config 5: whole AlexNet forward (conv/pool/fc/softmax chain of SURVEY "
+                "8d), 128 images per GPU"),
+    "vgg16": (os.path.join(ROOT, "configs", "vgg16.json"),
+              "whole VGG-16 forward (13 conv 3x3, 5 max pools, 3 fc, softmax), 128 images per "
+              "GPU (the AlexNet/VGG forward of the north star)"),
+}
+
+
+def layer_flops(cfg, weights=False):
+    """name -> forward flops of one image for every conv / fc layer of a
+    network config (shapes inferred as net.cpp infer_shapes does); with
+    weights=True, the total weight count instead."""
+    c, h, w = cfg["input"]["c"], cfg["input"]["h"], cfg["input"]["w"]
+    flat = None
+    out = {}
+    nw = 0
+    for L in cfg["layers"]:
+        k = L["kind"]
+        if k == "conv":
+            f, s, p, co = L["f"], L.get("stride", 1), L.get("pad", 0), L["c_out"]
+            ho, wo = (h + 2 * p - f) // s + 1, (w + 2 * p - f) // s + 1
+            out[L["name"]] = 2.0 * co * ho * wo * c * f * f
+            nw += co * c * f * f
+            c, h, w = co, ho, wo
+        elif k == "pool":
+            win, s = L["win"], L.get("stride", L["win"])
+            h, w = (h - win) // s + 1, (w - win) // s + 1
+        elif k == "fc":
+            kk = flat if flat is not None else c * h * w
+            out[L["name"]] = 2.0 * kk * L["out"]
+            nw += kk * L["out"]
+            flat = L["out"]
+    return nw if weights else out
 
 
 def thresholds():
@@ -717,22 +748,16 @@ def thresholds():
         return 32, 128, "titan-black preset"
 
 
-def entry_flops(name, batch):
-    if name in ALEXNET_CONV:
-        ci, co, f, ho = ALEXNET_CONV[name]
-        return 2.0 * batch * co * ho * ho * ci * f * f
-    if name in ALEXNET_FC:
-        k, n = ALEXNET_FC[name]
-        return 2.0 * batch * k * n
-    return 0.0
-
-
-def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
-    """BASELINE config 5: whole AlexNet forward, 128 images per GPU (batch 1024
-    at 8 GPUs), per-layer layout selection, conv/fc on tcgen05 (TF32)."""
+def run_network_workload(args, torch, dist, rank, world, local, device, barrier):
+    """Whole-network forward (BASELINE config 5 AlexNet, 128 images per GPU =
+    batch 1024 at 8 GPUs; or VGG-16), per-layer layout selection, conv/fc on
+    tcgen05 (TF32)."""
     from paper_1610_03618_b200 import capi, netapi
 
-    text = open(ALEXNET).read()
+    cfg_path, workload_desc = NETWORKS[args.workload]
+    text = open(cfg_path).read()
+    flops = layer_flops(json.loads(text))
+    weight_mb = layer_flops(json.loads(text), weights=True) * 4 / 1e6
     batch = json.loads(text)["input"]["n"]
     c_t, n_t, th_src = thresholds()
     netapi.set_dense_precision(capi.PREC_TF32)
@@ -778,7 +803,7 @@ def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
         runs.append(net.profile(x.data_ptr(), in_layout, sh))
     prof = [(runs[0][i][0], statistics.median(r[i][1] for r in runs)) for i in range(len(runs[0]))]
     name, ns = max(prof, key=lambda e: e[1])
-    fl = entry_flops(name, batch)
+    fl = flops.get(name, 0.0) * batch
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     tf32_peak = float(peaks["bf16_tflops"]) / 2
     achieved = fl / (ns * 1e-9) / 1e12 if fl else None
@@ -798,7 +823,7 @@ def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
                 "achieved": round(achieved, 1) if achieved else None, "peak": tf32_peak,
                 "peak_source": "measured bf16 burst (MEASURED_PEAKS.json) / 2 = dense TF32",
                 "unit": "TFLOP/s", "frac": round(achieved / tf32_peak, 4) if achieved else None,
-                "traffic": (load_traffic("alexnet") or {}).get(name),
+                "traffic": (load_traffic(args.workload) or {}).get(name),
                 "mma_peak_measured": mma_peak,
                 "frac_of_mma_peak": round(achieved / mma_peak, 4) if achieved and mma_peak else None,
                 "avg_launch_ms": round(ns / 1e6, 4),
@@ -842,7 +867,7 @@ def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = reference_alexnet_sample(c_t, n_t)
+            cpu = reference_network_sample(cfg_path, c_t, n_t)
         except Exception as e:
             cpu = {"value": None, "error": str(e)}
     if rank == 0:
@@ -851,14 +876,14 @@ def run_alexnet(args, torch, dist, rank, world, local, device, barrier):
                 "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "tf32",
                 "data": "synthetic (uniform[-1,1) input, reference-seeded weights)",
-                "config": {"workload": "BASELINE config 5: whole AlexNet forward (conv/pool/fc/"
-                                       "softmax chain of SURVEY 8d), 128 images per GPU",
+                "config": {"workload": workload_desc,
                            "batch_per_gpu": batch, "global_batch": batch * world,
                            "parallelism": f"N-shard x{world}, NCCL all_gather of logits only",
                            "layouts": layouts, "thresholds": [c_t, n_t],
                            "thresholds_source": th_src, "transforms": info["transforms"],
                            "logits_verified": ok_rows,
-                           "l2_policy": "activations + 245 MB weights per step (> L2)"},
+                           "l2_policy": f"activations + {weight_mb:.0f} MB of weights per step "
+                                        "(> L2)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": per_fwd * K if per_fwd is not None else None,
                 "gpu_launches_per_step": per_fwd, "clocks": clocks.summary(), "impl": "ours"}
@@ -881,13 +906,13 @@ def count_kernels(torch, fn):
         return None
 
 
-def reference_alexnet_sample(c_t, n_t, batch_per_thread=1):
+def reference_network_sample(cfg_path, c_t, n_t, batch_per_thread=1):
     from oracle.oracle import Ref, ref_time_network
 
     if not Ref.available():
         return None
     threads = os.cpu_count() or 1
-    cfg = json.loads(open(ALEXNET).read())
+    cfg = json.loads(open(cfg_path).read())
     cfg["input"]["n"] = batch_per_thread
     sec = ref_time_network(json.dumps(cfg), c_t, n_t, threads)
     return {"value": round(batch_per_thread * threads / sec, 3), "unit": "images/s",
@@ -896,7 +921,7 @@ def reference_alexnet_sample(c_t, n_t, batch_per_thread=1):
                       f"the unmodified run_network ({sec:.2f} s)"}
 
 
-def run_reference_alexnet(args, rank, world):
+def run_reference_network(args, rank, world):
     if rank != 0:
         return
     from oracle.oracle import Ref
@@ -906,8 +931,9 @@ def run_reference_alexnet(args, rank, world):
         return
     c_t, n_t, _ = thresholds()
     total_img, total_s = 0, 0.0
+    cfg_path, workload_desc = NETWORKS[args.workload]
     for i in range(args.warmup + args.steps):
-        r = reference_alexnet_sample(c_t, n_t)
+        r = reference_network_sample(cfg_path, c_t, n_t)
         if i >= args.warmup:
             total_img += r["cores"]
             total_s += r["cores"] / r["value"]
@@ -918,7 +944,7 @@ def run_reference_alexnet(args, rank, world):
                       "ms_per_step": round(1e3 * total_s / args.steps, 1),
                       "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                       "dtype": "f32", "data": "synthetic", "impl": "reference",
-                      "config": {"workload": "BASELINE config 5: whole AlexNet forward"},
+                      "config": {"workload": workload_desc},
                       "cpu_baseline": {"value": round(v, 3), "unit": "images/s", "cores": threads,
                                        "kind": "reference", "cpu": cpu_desc(),
                                        "sample": f"1 image per thread x {threads} threads"},

@@ -1256,8 +1256,13 @@ ConvRoute route_conv(const ConvArgs& a) {
     }();
     const uint64_t pair_tiles =
         (ncols + 2 * kTcBM - 1) / (2 * kTcBM) * ((a.co + co_tile_n(a.co) - 1) / co_tile_n(a.co));
+    // ... and only when the channel tile keeps the MMA efficient: N = C_o
+    // tile < 192 would sit on the ~96-cycle per-MMA floor (VGG conv1_2, C_o
+    // = 64: N = 64 runs at a third of the tensor rate; channels on M with
+    // 256-column tiles at half)
     const bool pair = pair_knob == 2 ||
-                      (pair_knob == 1 && pair_tiles >= 4ull * static_cast<uint64_t>(tc_sm_count() / 2));
+                      (pair_knob == 1 && co_tile_n(a.co) >= 192 &&
+                       pair_tiles >= 4ull * static_cast<uint64_t>(tc_sm_count() / 2));
     if (pair)
       r.kind = kRouteChwnPair;
     else

@@ -45,11 +45,15 @@ for (m, n, k) in [(8192, 8192, 8192), (4096, 4096, 4096), (128, 4096, 9216), (10
     res[f"gemm_{m}x{n}x{k}"] = {"ms": round(ms, 4), "tflops": round(2 * m * n * k / ms / 1e9, 1)}
 # AlexNet convs, CHWN, batch 128 (input dims = previous pool outputs)
 convs = {"conv1": (3, 227, 96, 11, 4, 0), "conv2": (96, 27, 192, 5, 1, 2), "conv3": (192, 13, 384, 3, 1, 1),
-         "conv4": (384, 13, 256, 3, 1, 1), "conv5": (256, 13, 256, 3, 1, 1)}
+         "conv4": (384, 13, 256, 3, 1, 1), "conv5": (256, 13, 256, 3, 1, 1),
+         # VGG-16 shapes (run only when named: `perf_dense.py vgg`)
+         "vgg1_1": (3, 224, 64, 3, 1, 1), "vgg1_2": (64, 224, 64, 3, 1, 1),
+         "vgg2_2": (128, 112, 128, 3, 1, 1), "vgg3_2": (256, 56, 256, 3, 1, 1),
+         "vgg4_2": (512, 28, 512, 3, 1, 1)}
 N = 128
 for layout, tag in ((lcnn.CHWN, "chwn"), (lcnn.NCHW, "nchw")):
     for name, (ci, hw, co, f, s, p) in convs.items():
-        if not want(f"{name}_{tag}"):
+        if not want(f"{name}_{tag}") or (name.startswith("vgg") and not only):
             continue
         x = lcnn.DeviceTensor4D(N, ci, hw, hw, layout, torch.rand(N * ci * hw * hw, device=dev))
         w = torch.rand(co * ci * f * f, device=dev)
