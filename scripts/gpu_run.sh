@@ -13,7 +13,7 @@ fi
 if [[ $STAGE == all || $STAGE == bench ]]; then
   : > gpurun_out/bench.jsonl
   timeout 600 python bench.py >> gpurun_out/bench.jsonl 2> gpurun_out/bench.err
-  for wl in vgg_pools_nchw pl5 pl5_nchw softmax softmax5 softmax_64k transform alexnet; do
+  for wl in vgg_pools_nchw pl5 pl5_nchw softmax softmax5 softmax_64k transform alexnet vgg16; do
     timeout 300 python bench.py --workload $wl --steps 50 >> gpurun_out/bench.jsonl 2>> gpurun_out/bench.err
   done
   timeout 300 python bench.py --impl reference --steps 3 --warmup 3 >> gpurun_out/bench.jsonl 2>> gpurun_out/bench.err
