@@ -42,7 +42,8 @@ namespace lcnn_dev {
 
 using namespace lcnn_tc;
 
-enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2, kModeROW = 3, kModeSHARE = 4 };
+enum ConvMode : uint32_t { kModeCI = 0, kModeWIN = 1, kModeNAT = 2, kModeROW = 3, kModeSHARE = 4,
+                          kModeTAPS = 5 };
 
 struct ConvGeomTc {
   uint32_t N, Ci, H, W, Co, FH, FW, S, P, Ho, Wo;
@@ -65,6 +66,12 @@ __global__ void pack_filters_kernel(const float* __restrict__ f, float* __restri
       const uint32_t tap = k / g.Ci;
       fh = tap / g.FW;
       fw = tap % g.FW;
+    } else if (g.mode == kModeTAPS) {  // k = (fh, channel block, fw, 32 channels)
+      const uint32_t c = k % 32, q = k / 32;
+      fw = q % g.FW;
+      const uint32_t t = q / g.FW, cb = t % (g.Ci / 32);
+      fh = t / (g.Ci / 32);
+      ci = cb * 32 + c;
     } else if (g.mode == kModeROW) {  // k = (fh, ci, fw), each fh row padded to KR
       fh = k / g.KR;
       const uint32_t r = k - fh * g.KR;
@@ -490,6 +497,178 @@ struct ShareOut {
         add);
   }
 };
+
+// ---- TAPS mode: tap-sharing input boxes for CI convolutions ----------------
+// A tile is 8 consecutive output pixels of one output row x one 32-image
+// group (UMMA N = 256, channels on M, the ShareOut mapping).  K runs (filter
+// row fh, 32-channel block cb, tap fw, channel): one input box {32 n, 32 c,
+// BW = 7*S + F_w w} per (fh, cb) -- rows ordered (w, c), c fastest -- serves
+// all F_w taps of that filter row, tap fw's 8 MN atoms starting fw*4 KB into
+// the box at a pitch of S*4 KB (address-swizzled atoms, scripts/swz_test.cu).
+// Versus one box per (tap, channel block) that is F_w times fewer input
+// bytes per MMA (3x for 3x3 layers, 5x for 5x5).  The filter slices ride a
+// separate, deeper ring (16 KB per tap), so an input box stays resident while
+// its F_w taps are consumed.
+struct TapsCtl {
+  uint64_t ifull[4], iempty[4];
+  uint64_t ffull[8], fempty[8];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_addr;
+};
+
+struct TapsParams {
+  CUtensorMap x;  // input view {32 n, Ci, W, N/32, H}, box {32, 32, BW, 1, 1}
+  CUtensorMap w;  // packed filters [Co][K], box {32 k, 128 co}
+  Sched sc;       // mt = channel tiles, nt = Ho * OWB * G, iters = FH * CB (stream-K ready)
+  ShareOut out;
+  uint32_t FW, S, P, CB, OWB, G;
+  uint32_t ni, nf, islot, ibox;  // input / filter ring slots, input slot and box bytes
+  uint32_t ctl_off;
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __grid_constant__ TapsParams prm) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw_smem) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* ibase = smem;
+  uint8_t* fbase = smem + prm.ni * prm.islot;
+  TapsCtl* ctl = reinterpret_cast<TapsCtl*>(smem + prm.ctl_off);
+  const Sched& sc = prm.sc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch(&prm.x);
+      tma_prefetch(&prm.w);
+      for (uint32_t i = 0; i < prm.ni; ++i) {
+        mbar_init(&ctl->ifull[i], 1);
+        mbar_init(&ctl->iempty[i], 1);
+      }
+      for (uint32_t i = 0; i < prm.nf; ++i) {
+        mbar_init(&ctl->ffull[i], 1);
+        mbar_init(&ctl->fempty[i], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&ctl->tfull[a], 1);
+        mbar_init(&ctl->tempty[a], 4);
+      }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(&ctl->tmem_addr);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_addr;
+  LCNN_PDL_ENTRY();
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: input boxes and filter slices ----------------
+    uint32_t is = 0, iph = 0, fs = 0, fph = 0;
+    for_each_work(sc, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t mi = t % sc.mt, ni = t / sc.mt;
+      const uint32_t g = ni % prm.G, r = ni / prm.G, ob = r % prm.OWB, oh = r / prm.OWB;
+      const int32_t y0 = static_cast<int32_t>(ob * kSharePix * prm.S) - static_cast<int32_t>(prm.P);
+      const int32_t z0 = static_cast<int32_t>(oh * prm.S) - static_cast<int32_t>(prm.P);
+      const int32_t co0 = static_cast<int32_t>(mi * kTcBM);
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        const uint32_t fh = it / prm.CB, cb = it - fh * prm.CB;
+        mbar_wait(&ctl->iempty[is], iph ^ 1);
+        mbar_arrive_expect_tx(&ctl->ifull[is], prm.ibox);
+        tma_load_5d(ibase + is * prm.islot, &prm.x, &ctl->ifull[is], 0,
+                    static_cast<int32_t>(cb * 32), y0, static_cast<int32_t>(g),
+                    z0 + static_cast<int32_t>(fh));
+        if (++is == prm.ni) {
+          is = 0;
+          iph ^= 1;
+        }
+        for (uint32_t fw = 0; fw < prm.FW; ++fw) {
+          mbar_wait(&ctl->fempty[fs], fph ^ 1);
+          mbar_arrive_expect_tx(&ctl->ffull[fs], kTcABytes);
+          tma_load_2d(fbase + fs * kTcABytes, &prm.w, &ctl->ffull[fs],
+                      static_cast<int32_t>((it * prm.FW + fw) * kTcBK), co0);
+          if (++fs == prm.nf) {
+            fs = 0;
+            fph ^= 1;
+          }
+        }
+      }
+    });
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp-uniform, one elected lane) ----------------
+    const bool mma_on = !(sc.probe & 1);
+    const uint32_t lbo = prm.S * 4096;
+    uint32_t is = 0, iph = 0, fs = 0, fph = 0, local = 0;
+    for_each_work(sc, [&](uint32_t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
+      mbar_wait(&ctl->tempty[a], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + a * kPBN;
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        mbar_wait(&ctl->ifull[is], iph);
+        tc_fence_after();
+        const uint8_t* xb = ibase + is * prm.islot;
+        for (uint32_t fw = 0; fw < prm.FW; ++fw) {
+          mbar_wait(&ctl->ffull[fs], fph);
+          tc_fence_after();
+          const uint64_t da = smem_desc_sw128(fbase + fs * kTcABytes, 16, 1024);
+          const uint64_t db = smem_desc_sw128(xb + fw * 4096, lbo, 512, 1);
+          if (elect_one()) {
+            if (mma_on) {
+#pragma unroll
+              for (int k = 0; k < kTcBK / 8; ++k)
+                mma_tf32(acc, da + 2 * k, db + 64 * k, sc.idesc,
+                         (it != kbeg || fw != 0 || k != 0) ? 1u : 0u);
+            }
+            tc_commit(&ctl->fempty[fs]);
+          }
+          __syncwarp();
+          if (++fs == prm.nf) {
+            fs = 0;
+            fph ^= 1;
+          }
+        }
+        if (elect_one()) tc_commit(&ctl->iempty[is]);
+        __syncwarp();
+        if (++is == prm.ni) {
+          is = 0;
+          iph ^= 1;
+        }
+      }
+      if (elect_one()) tc_commit(&ctl->tfull[a]);
+      __syncwarp();
+    });
+  } else if (warp >= 2) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;
+    uint32_t local = 0;
+    for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
+      const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
+      const uint32_t mi = t % sc.mt, ni = t / sc.mt;
+      mbar_wait(&ctl->tfull[a], aphase);
+      tc_fence_after();
+      const uint32_t m = mi * kTcBM + q * 32 + lane;
+      const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (uint32_t c = 0; c < kPBN; c += 32) {
+        float v[32];
+        tmem_ld32(base + c, v);
+        if (!(sc.probe & 2)) prm.out.store32(m, ni * kPBN + c, v, split);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl->tempty[a]);
+    });
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
 
 // ---- NCHW implicit GEMM on tcgen05 --------------------------------------
 //   D[co][(n, p)] = sum_k W[co][k] * X[k][(n, p)],  k = (ci, fh, fw),
@@ -1105,6 +1284,79 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
   return launch_persistent(L, O, sc, s);
 }
 
+// TAPS-mode geometry: input box width, ring slots that fit shared memory.
+struct TapsGeom {
+  uint32_t bw, ibox, islot, ni, nf;
+  bool ok;
+};
+
+TapsGeom taps_geom(const ConvArgs& a) {
+  TapsGeom q{};
+  q.bw = a.stride * (kSharePix - 1) + a.fw;
+  q.ibox = q.bw * 4096;
+  q.islot = (q.ibox + 1023) / 1024 * 1024;
+  const uint64_t avail = kMaxDynSmem - 1024 - sizeof(TapsCtl) - 16;
+  for (uint32_t ni = 3; ni >= 2 && !q.ni; --ni) {
+    if (ni * uint64_t{q.islot} >= avail) continue;
+    const uint64_t nf = std::min<uint64_t>(8, (avail - ni * uint64_t{q.islot}) / kTcABytes);
+    if (nf >= std::max<uint64_t>(4, a.fw + 1)) {
+      q.ni = ni;
+      q.nf = static_cast<uint32_t>(nf);
+    }
+  }
+  q.ok = a.precision == LCNN_PREC_TF32 && a.ci % 32 == 0 && a.n % 32 == 0 && q.bw <= 256 &&
+         q.ni >= 2 && a.stride * 4096u < (1u << 18);
+  return q;
+}
+
+cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s) {
+  const ConvArgs& a = t.a;
+  const TapsGeom q = taps_geom(a);
+  TapsParams prm;
+  const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
+  const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
+                             static_cast<uint64_t>(a.n) * 4, 128,
+                             static_cast<uint64_t>(a.w) * a.n * 4};
+  const uint32_t box[5] = {32, 32, q.bw, 1, 1};
+  if (!make_tmap(&prm.x, t.x_hi, 5, dims, pitch, box, nullptr, 1)) return cudaErrorInvalidValue;
+  const uint64_t K = t.p.K;
+  if (!make_tmap_2d(&prm.w, t.w_hi, K, a.co, K * 4, kTcBK, kTcBM, false))
+    return cudaErrorInvalidValue;
+  prm.FW = a.fw;
+  prm.S = a.stride;
+  prm.P = a.pad;
+  prm.CB = a.ci / 32;
+  prm.OWB = (a.wo + kSharePix - 1) / kSharePix;
+  prm.G = a.n / 32;
+  prm.ni = q.ni;
+  prm.nf = q.nf;
+  prm.islot = q.islot;
+  prm.ibox = q.ibox;
+  const uint32_t mt = (a.co + kTcBM - 1) / kTcBM, nt = a.ho * prm.OWB * prm.G;
+  prm.sc = make_sched(mt, nt, a.fh * prm.CB, 1, kSharePix * 32, false, true);
+  prm.ctl_off = q.ni * q.islot + q.nf * kTcABytes;
+  prm.out = ShareOut{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, prm.OWB,
+                     prm.G};
+  const Sched& sc = prm.sc;
+  if (sc.dp_tiles < mt * nt) {  // zero the stream-K tiles' output rows (oh >= first split row)
+    const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
+    const uint64_t col0 =
+        static_cast<uint64_t>(sc.dp_tiles / mt / (prm.OWB * prm.G)) * a.wo * a.n;
+    cudaError_t e = launch_zero2d(a.dst + col0, ncols, ncols - col0, a.co, s);
+    if (e != cudaSuccess) return e;
+  }
+  const uint32_t smem = 1024 + prm.ctl_off + static_cast<uint32_t>(sizeof(TapsCtl));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_taps_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMaxDynSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return lcnn_pdl::launch(tc_conv_taps_kernel, sc.grid, kTcThreads, smem, s, prm);
+}
+
 template <bool kCoOnN, bool kPair = false>
 cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   const ConvArgs& a = t.a;
@@ -1183,7 +1435,7 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
 namespace {
 
 enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM,
-                 kRouteShare, kRouteShareRes, kRouteChwnPair };
+                 kRouteShare, kRouteShareRes, kRouteChwnPair, kRouteTaps };
 
 struct ConvRoute {
   RouteKind kind = kRouteSimt;
@@ -1263,6 +1515,24 @@ ConvRoute route_conv(const ConvArgs& a) {
     const bool pair = pair_knob == 2 ||
                       (pair_knob == 1 && co_tile_n(a.co) >= 192 &&
                        pair_tiles >= 4ull * static_cast<uint64_t>(tc_sm_count() / 2));
+    // TAPS (tap-sharing boxes) for layers whose channel planes are large
+    // (H*W*N*4 >= 4 MB: activations far beyond L2, where the per-(tap,
+    // channel-block) boxes are DRAM-latency-bound): measured on B200, VGG-16
+    // conv1_2 / conv2_1 / conv2_2 3.9 / 1.05 / 1.9 ms -> 1.9 / 0.54 / 0.97 ms;
+    // neutral at 56x56 and slower on AlexNet's 27x27 / 13x13 layers.
+    // Profiling knob LCNN_CONV_TAPS: 0 off, 1 forced wherever supported.
+    static const int taps_knob = [] {
+      const char* e = std::getenv("LCNN_CONV_TAPS");
+      return e ? (e[0] == '1' ? 2 : 0) : 1;
+    }();
+    const bool big_planes = static_cast<uint64_t>(a.h) * a.w * a.n * 4 >= (4ull << 20);
+    if (r.p.g.mode == kModeCI && (taps_knob == 2 || (taps_knob == 1 && big_planes)) &&
+        taps_geom(a).ok) {
+      r.kind = kRouteTaps;
+      r.p.g.mode = kModeTAPS;
+      r.apack = static_cast<uint64_t>(a.co) * r.p.K;
+      return r;
+    }
     if (pair)
       r.kind = kRouteChwnPair;
     else
@@ -1364,6 +1634,7 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
     return launch_chwn_share(t, r.kind == kRouteShareRes, s);
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
+  if (r.kind == kRouteTaps) return launch_chwn_taps(t, s);
   if (r.kind == kRouteChwnPair) return launch_chwn_tc<true, true>(t, s);
   return r.kind == kRouteChwnOnN ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
 }

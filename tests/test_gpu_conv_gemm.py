@@ -87,6 +87,9 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     # >= 4 waves of 256-column tiles: the CTA-pair (cta_group::2) kernel
     (128, 32, 27, 27, 192, 3, 1, 1),   # CI, conv2-like channel tile (N = 192, 96 per CTA)
     (128, 16, 27, 27, 48, 5, 1, 2),    # WIN
+    # channel planes >= 4 MB: TAPS mode (one box per filter row serves all its taps)
+    (128, 32, 92, 92, 64, 3, 1, 1),    # C_o 64: half-empty 128-channel tile
+    (64, 32, 130, 130, 160, 3, 2, 1),  # stride 2, two channel tiles, 32-image groups x 2
 ]
 
 
