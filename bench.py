@@ -257,18 +257,20 @@ def build_workload(name, torch, device, rank, plan):
     if name in ("vgg_pools", "vgg_pools_nchw"):
         b = 256
         layout = CHWN if name == "vgg_pools" else NCHW
-        plan = plan or ((1, 1) if layout == CHWN else (3, 1))  # measured best (scripts/pool_plans.py)
-        ops = [PoolOp(torch, device, b, c, hw, hw, layout, 2, 2, False, plan, seed + i)
+        # measured best per layer (scripts/pool_plans.py [nchw vgg] on B200)
+        plans = [plan] * len(VGG_POOLS) if plan else (
+            [(1, 1)] * len(VGG_POOLS) if layout == CHWN else [(4, 2), (3, 1), (2, 1), (1, 2), (3, 1)])
+        ops = [PoolOp(torch, device, b, c, hw, hw, layout, 2, 2, False, plans[i], seed + i)
                for i, (c, hw) in enumerate(VGG_POOLS)]
         lname = "CHWN (selector's pooling layout)" if layout == CHWN else "NCHW"
         desc = {"workload": f"BASELINE config 4: VGG-16 pool1..pool5, max 2x2/s2, {lname}, "
                             "256 images per GPU, N-sharded",
                 "batch_per_gpu": b, "layers": [f"{b}x{c}x{hw}x{hw}" for c, hw in VGG_POOLS],
-                "kernel": f"coarsened fh,fw={plan[0]},{plan[1]}"}
+                "kernel": "coarsened fh,fw per layer " + ",".join(f"{p[0]}x{p[1]}" for p in plans)}
         return ops, desc, 0, b
     if name in ("pl5", "pl5_nchw"):
         layout = CHWN if name == "pl5" else NCHW
-        p = plan or ((2, 2) if layout == CHWN else (3, 1))  # measured best (scripts/pool_plans.py)
+        p = plan or ((2, 2) if layout == CHWN else (3, 2))  # measured best (scripts/pool_plans.py)
         ops = [PoolOp(torch, device, 128, 96, 55, 55, layout, 3, 2, False, p, seed, rotate=True)]
         desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) max 3x3/s2, "
                             f"128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",

@@ -216,8 +216,20 @@ lcnn_status lcnn_pool_layout(const float* src, float* dst, uint32_t n, uint32_t 
   if (st != LCNN_OK) return st;
   if (layout != LCNN_CHWN && layout != LCNN_NCHW)
     return fail(LCNN_ELAYOUT, "pool_layout: only CHWN and NCHW kernels exist");
+  // NCHW: the pipelined kernel's measured output block (scripts/pool_plans.py on B200:
+  // 3x3/s2 -> 3x2 (PL5 4204 -> 5386 GB/s); 2x2/s2 -> 4x2 on >= 200-wide planes, else 3x1);
+  // every output keeps its tap order, so the bits equal the plain kernel's and
+  // the report stays the plain one
+  uint32_t fh = 1, fw = 1;
+  if (layout == LCNN_NCHW && win_h == win_w && stride == 2 && win_h == 3) {
+    fh = 3;
+    fw = 2;
+  } else if (layout == LCNN_NCHW && win_h == win_w && stride == 2 && win_h == 2) {
+    fh = w >= 200 ? 4 : 3;
+    fw = w >= 200 ? 2 : 1;
+  }
   lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
-                        mode == LCNN_POOL_AVG, 1, 1};
+                        mode == LCNN_POOL_AVG, fh, fw};
   cudaError_t e = layout == LCNN_CHWN ? lcnn_impl::launch_pool_chwn(a, S(stream))
                                       : lcnn_impl::launch_pool_nchw(a, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pool_layout");

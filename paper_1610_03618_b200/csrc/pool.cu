@@ -329,7 +329,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-template <int WH, int S, int FH, bool AVG>
+template <int WH, int S, int FH, int FW, bool AVG>
 __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g) {
   LCNN_PDL_ENTRY();
   extern __shared__ __align__(16) float ring[];
@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
   __shared__ uint32_t meta[kPipe][2];  // (float offset of the span, floats copied)
   constexpr int WW = WH;
   constexpr int UH = S * (FH - 1) + WH;
+  constexpr int UW = S * (FW - 1) + WW;  // columns of one FW-wide output block's window union
   if (threadIdx.x == 0) {
     for (int k = 0; k < kPipe; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
@@ -390,40 +391,48 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
     const PipeUnit pu = pipe_unit(g, u, S, WH);
     const float* sbuf = ring + static_cast<size_t>(k) * g.stage_floats + meta[k][0];
     const uint32_t nrb = (pu.oh_cnt + FH - 1) / FH;
-    const uint32_t items = pu.np * nrb * g.Wo;
+    const uint32_t owc = (g.Wo + FW - 1) / FW;  // FW-wide output column blocks per row
+    const uint32_t items = pu.np * nrb * owc;
     for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
-      uint32_t p, rest, rb, ow;
+      uint32_t p, rest, rb, oc;
       if (pu.np == 1) {
         p = 0;
         rest = it;
       } else {
         g.div_plane_items.divmod(it, p, rest);
       }
-      g.div_wo.divmod(rest, rb, ow);
+      g.div_wo.divmod(rest, rb, oc);  // div_wo divides by owc
+      const uint32_t ow = oc * FW;
       const uint32_t r0 = rb * FH;
       const uint32_t prow = p * g.H;
-      float acc[FH];
+      // an output (by, bx) takes its taps in (y, x) order from the shared
+      // union rows / columns, the same order as an uncoarsened output
+      float acc[FH][FW];
 #pragma unroll
-      for (int by = 0; by < FH; ++by) acc[by] = AVG ? 0.0f : -INFINITY;
+      for (int by = 0; by < FH; ++by)
+#pragma unroll
+        for (int bx = 0; bx < FW; ++bx) acc[by][bx] = AVG ? 0.0f : -INFINITY;
 #pragma unroll
       for (int y = 0; y < UH; ++y) {
         const uint32_t rr = r0 * S + y;
         if (pu.np == 1 ? rr >= pu.ih_rows : rr >= g.H) break;  // rows of absent outputs
         const uint32_t e0 = (prow + rr) * g.W + ow * S;
-        float v[WW];
+        float v[UW];
 #pragma unroll
-        for (int x = 0; x < WW; ++x) {
-          v[x] = sbuf[e0 + x];
+        for (int x = 0; x < UW; ++x) {
+          v[x] = sbuf[e0 + x];  // past the row end only for absent outputs (never stored)
         }
 #pragma unroll
         for (int by = 0; by < FH; ++by) {
           const int dy = y - by * S;
           if (dy < 0 || dy >= WH) continue;
 #pragma unroll
-          for (int x = 0; x < WW; ++x) {
-            if constexpr (AVG) acc[by] = add_tap(acc[by], v[x]);
-            else acc[by] = max_tap(acc[by], v[x]);
-          }
+          for (int bx = 0; bx < FW; ++bx)
+#pragma unroll
+            for (int x = 0; x < WW; ++x) {
+              if constexpr (AVG) acc[by][bx] = add_tap(acc[by][bx], v[bx * S + x]);
+              else acc[by][bx] = max_tap(acc[by][bx], v[bx * S + x]);
+            }
         }
       }
       float* orow = g.dst + static_cast<uint64_t>(pu.plane0 + p) * g.Ho * g.Wo +
@@ -431,8 +440,12 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
 #pragma unroll
       for (int by = 0; by < FH; ++by) {
         if (r0 + by >= pu.oh_cnt) break;
-        const float o = AVG ? divide_out(acc[by], g.divisor) : acc[by];
-        stg_stream(orow + static_cast<uint64_t>(by) * g.Wo, o);
+#pragma unroll
+        for (int bx = 0; bx < FW; ++bx) {
+          if (ow + bx >= g.Wo) break;
+          const float o = AVG ? divide_out(acc[by][bx], g.divisor) : acc[by][bx];
+          stg_stream(orow + static_cast<uint64_t>(by) * g.Wo + bx, o);
+        }
       }
     }
     __syncthreads();  // slot k is refilled by the issue() of iteration i + 1
@@ -649,10 +662,11 @@ bool nchw_dispatch_f(uint32_t fh, uint32_t fw, const NchwGeom& g, uint32_t block
 
 }  // namespace
 
-template <int WH, int S, int FH>
+template <int WH, int S, int FH, int FW>
 cudaError_t pipe_launch(const NchwPipeGeom& g, uint32_t blocks, uint32_t smem, bool avg,
                         cudaStream_t st) {
-  auto kern = avg ? pool_nchw_pipe_kernel<WH, S, FH, true> : pool_nchw_pipe_kernel<WH, S, FH, false>;
+  auto kern = avg ? pool_nchw_pipe_kernel<WH, S, FH, FW, true>
+                  : pool_nchw_pipe_kernel<WH, S, FH, FW, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -676,7 +690,7 @@ cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
   g.Ho = a.ho;
   g.Wo = a.wo;
   g.planes = static_cast<uint32_t>(planes);
-  g.div_wo = FastDiv(a.wo);
+  g.div_wo = FastDiv((a.wo + a.fw - 1) / a.fw);  // FW-wide output column blocks per row
   g.divisor = static_cast<float>(a.win_h * a.win_w);  // pool.cpp:158
   uint64_t units, span_bytes;
   if (plane_bytes + 16 <= kSlot) {  // whole planes, as many as fit
@@ -697,7 +711,7 @@ cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
   g.units = static_cast<uint32_t>(units);
   g.stage_floats = static_cast<uint32_t>((span_bytes + 16 + 15) / 16 * 4);
   const uint32_t nrb = (g.band + a.fh - 1) / a.fh;
-  g.div_plane_items = FastDiv(nrb * a.wo);
+  g.div_plane_items = FastDiv(nrb * ((a.wo + a.fw - 1) / a.fw));
   const uint32_t smem = kPipe * g.stage_floats * 4;
   // persistent: up to 3 CTAs per SM (72 KB rings), never more CTAs than units
   int dev = 0, sms = 148;
@@ -705,12 +719,15 @@ cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t cap = static_cast<uint64_t>(sms) * 3;
   const uint32_t blocks = static_cast<uint32_t>(units < cap ? units : cap);
-#define LCNN_PIPE(WH_, S_, FH_)                                 \
-  if (a.win_h == WH_ && a.stride == S_ && a.fh == FH_)          \
-    return pipe_launch<WH_, S_, FH_>(g, blocks, smem, a.avg, st);
-  LCNN_PIPE(2, 2, 1) LCNN_PIPE(2, 2, 2) LCNN_PIPE(2, 2, 3) LCNN_PIPE(2, 2, 4)
-  LCNN_PIPE(3, 2, 1) LCNN_PIPE(3, 2, 2) LCNN_PIPE(3, 2, 3) LCNN_PIPE(3, 2, 4)
-  LCNN_PIPE(3, 1, 1) LCNN_PIPE(3, 1, 2) LCNN_PIPE(3, 1, 3) LCNN_PIPE(3, 1, 4)
+#define LCNN_PIPE(WH_, S_, FH_, FW_)                                        \
+  if (a.win_h == WH_ && a.stride == S_ && a.fh == FH_ && a.fw == FW_)       \
+    return pipe_launch<WH_, S_, FH_, FW_>(g, blocks, smem, a.avg, st);
+  LCNN_PIPE(2, 2, 1, 1) LCNN_PIPE(2, 2, 2, 1) LCNN_PIPE(2, 2, 3, 1) LCNN_PIPE(2, 2, 4, 1)
+  LCNN_PIPE(3, 2, 1, 1) LCNN_PIPE(3, 2, 2, 1) LCNN_PIPE(3, 2, 3, 1) LCNN_PIPE(3, 2, 4, 1)
+  LCNN_PIPE(3, 1, 1, 1) LCNN_PIPE(3, 1, 2, 1) LCNN_PIPE(3, 1, 3, 1) LCNN_PIPE(3, 1, 4, 1)
+  LCNN_PIPE(2, 2, 1, 2) LCNN_PIPE(2, 2, 2, 2) LCNN_PIPE(2, 2, 4, 2)
+  LCNN_PIPE(3, 2, 1, 2) LCNN_PIPE(3, 2, 2, 2) LCNN_PIPE(3, 2, 3, 2) LCNN_PIPE(3, 2, 4, 2)
+  LCNN_PIPE(3, 1, 2, 2) LCNN_PIPE(3, 1, 3, 2)
 #undef LCNN_PIPE
   return cudaErrorNotSupported;
 }
@@ -718,7 +735,7 @@ cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
 cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t st) {
   const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
   if (planes == 0 || a.ho == 0 || a.wo == 0) return cudaSuccess;
-  if (a.fw == 1 && a.fh <= 4 && a.win_h == a.win_w &&
+  if (a.fw <= 2 && a.fh <= 4 && a.win_h == a.win_w &&
       ((a.stride == 2 && (a.win_h == 2 || a.win_h == 3)) || (a.stride == 1 && a.win_h == 3))) {
     const cudaError_t e = launch_pool_nchw_pipe(a, st);
     if (e != cudaErrorNotSupported) return e;

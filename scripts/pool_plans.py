@@ -42,10 +42,18 @@ def gbs(layout, n, c, hw, win, s, fh, fw, K=50):
 
 
 out = {}
-for name, (n, c, hw, win, s) in {"PL5": (128, 96, 55, 3, 2), "VGG1": (256, 64, 224, 2, 2),
-                                 "PL7": (128, 256, 13, 3, 2)}.items():
+only = sys.argv[1:]
+shapes = {"PL5": (128, 96, 55, 3, 2), "VGG1": (256, 64, 224, 2, 2), "PL7": (128, 256, 13, 3, 2)}
+if "vgg" in only:
+    shapes = {"VGG1": (256, 64, 224, 2, 2), "VGG2": (256, 128, 112, 2, 2),
+              "VGG3": (256, 256, 56, 2, 2), "VGG4": (256, 512, 28, 2, 2),
+              "VGG5": (256, 512, 14, 2, 2)}
+for name, (n, c, hw, win, s) in shapes.items():
     for fh, fw in [(1, 1), (1, 2), (2, 1), (2, 2), (1, 3), (3, 1), (1, 4), (4, 1), (2, 4), (4, 2)]:
-        out[f"{name}_chwn_{fh}x{fw}"] = gbs(capi.CHWN, n, c, hw, win, s, fh, fw)
-    for fh in (1, 2, 3, 4):
-        out[f"{name}_nchw_{fh}x1"] = gbs(capi.NCHW, n, c, hw, win, s, fh, 1)
+        if "nchw" not in only:
+            out[f"{name}_chwn_{fh}x{fw}"] = gbs(capi.CHWN, n, c, hw, win, s, fh, fw)
+    for fh, fw in [(1, 1), (2, 1), (3, 1), (4, 1), (1, 2), (2, 2), (3, 2), (4, 2)]:
+        if name.startswith("VGG") and (fh, fw) == (3, 2):
+            continue  # no 2x2/s2 FH=3 FW=2 instantiation
+        out[f"{name}_nchw_{fh}x{fw}"] = gbs(capi.NCHW, n, c, hw, win, s, fh, fw)
 print(json.dumps(out, indent=1))

@@ -130,6 +130,11 @@ def test_pool_fixtures_full_size(cuda):
                 want, _ = C.pool_plain(xin, n, c, hw, hw, layout, win, win, s, avg)
                 got, _ = lcnn.pool_layout(t, P(win, win, s, avg))
                 assert bit_equal(got.to_host(), want), (name, layout, avg)
+                if layout == NCHW:  # the pipelined kernel's 2-wide output blocks at full size
+                    for fh, fw in ((3, 2), (2, 2), (4, 2)):
+                        got, _ = lcnn.pool_coarsened_nchw(t, P(win, win, s, avg),
+                                                          lcnn.CoarseningPlan(fh, fw))
+                        assert bit_equal(got.to_host(), want), (name, fh, fw, avg)
                 if layout == CHWN:
                     got, rep = lcnn.pool_coarsened(t, P(win, win, s, avg), lcnn.CoarseningPlan(2, 2))
                     assert bit_equal(got.to_host(), want)
