@@ -3,7 +3,7 @@
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
-           -Xptxas -warn-spills --expt-relaxed-constexpr
+           -Xptxas -warn-spills --expt-relaxed-constexpr $(EXTRA_NVFLAGS)
 PKG     := paper_1610_03618_b200
 SRC     := $(PKG)/csrc
 OBJDIR  := build/obj

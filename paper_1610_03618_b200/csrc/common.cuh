@@ -72,13 +72,13 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p) {
 }
 
 __device__ __forceinline__ void stg_stream(float4* p, float4 v) {
-  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+  asm volatile("st.global" LCNN_ST_HINT ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
                "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
 
 __device__ __forceinline__ void stg_stream(float* p, float v) {
-  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+  asm volatile("st.global" LCNN_ST_HINT ".f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
 template <int VEC>

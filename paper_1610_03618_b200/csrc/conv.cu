@@ -409,7 +409,7 @@ struct ColsOut {
       if (add)
         atomicAdd(p + static_cast<uint64_t>(j) * ncols, v[j]);
       else
-        __stcs(p + static_cast<uint64_t>(j) * ncols, v[j]);
+        lcnn_tc::st_out(p + static_cast<uint64_t>(j) * ncols, v[j]);
     }
   }
 };

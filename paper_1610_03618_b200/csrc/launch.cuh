@@ -15,6 +15,18 @@
 #include <cstdlib>
 #include <utility>
 
+// Cache hint of the kernels' output stores: ".cs" (streaming, evict-first)
+// when LCNN_CS_STORES=1, plain write-back stores otherwise (a layer's output
+// then competes normally for L2 and the next layer may hit it).
+#ifndef LCNN_CS_STORES
+#define LCNN_CS_STORES 1
+#endif
+#if LCNN_CS_STORES
+#define LCNN_ST_HINT ".cs"
+#else
+#define LCNN_ST_HINT ""
+#endif
+
 namespace lcnn_pdl {
 
 __device__ __forceinline__ void wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -21,6 +21,16 @@
 
 namespace lcnn_tc {
 
+// output stores of the tcgen05 epilogues (cache hint: LCNN_ST_HINT)
+__device__ __forceinline__ void st_out(float4* p, float4 v) {
+  asm volatile("st.global" LCNN_ST_HINT ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_out(float* p, float v) {
+  asm volatile("st.global" LCNN_ST_HINT ".f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -592,7 +592,7 @@ __device__ __forceinline__ void warp_store_rows32(float* rowp, const float* v, b
   for (int j = 0; j < 8; ++j) {
     float* p = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, mine, q8 + j));
     if (!p) continue;
-    __stcs(reinterpret_cast<float4*>(p) + l8, x[j]);
+    lcnn_tc::st_out(reinterpret_cast<float4*>(p) + l8, x[j]);
   }
 }
 
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (m >= sk.M || n >= sk.N || (sk.probe & 2)) continue;
       float* dst = c + static_cast<uint64_t>(m) * sk.N + n;
       if (vec && n + 4 <= sk.N) {
-        __stcs(reinterpret_cast<float4*>(dst), acc);
+        lcnn_tc::st_out(reinterpret_cast<float4*>(dst), acc);
       } else {
         const float a[4] = {acc.x, acc.y, acc.z, acc.w};
         for (uint32_t e = 0; e < 4 && n + e < sk.N; ++e) dst[e] = a[e];

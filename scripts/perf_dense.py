@@ -64,4 +64,4 @@ for layout, tag in ((lcnn.CHWN, "chwn"), (lcnn.NCHW, "nchw")):
         ms = timeit(lambda: lcnn.conv_forward(x, w, co, f, f, s, p, lcnn.TF32, out=out, workspace=ws))
         fl = 2 * N * co * ho * ho * ci * f * f
         res[f"{name}_{tag}"] = {"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1)}
-print(json.dumps(res, indent=1))
+print(json.dumps(res))
