@@ -486,6 +486,23 @@ struct ShareOut {
   float* c;
   uint64_t plane;  // Ho * Wo * N
   uint32_t co, n, wo, owb, groups;
+  // TMA-store epilogue: view {32 n, N/32, Wo, Ho, Co} of the output, box
+  // {32, 1, 1, 1, 32} = one 32-channel x 32-image chunk, SWIZZLE_128B
+  CUtensorMap y;
+  static constexpr bool kTmaStore = true;
+  __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
+                                            bool add) const {
+    const uint32_t t = n0 / (kSharePix * 32), p = n0 % (kSharePix * 32) / 32;
+    const uint32_t grp = t % groups, r = t / groups;
+    const uint32_t ob = r % owb, oh = r / owb, ow = ob * kSharePix + p;
+    if (ow >= wo || m0 >= co) return;  // (rows past C_o inside the box are clipped)
+    if (add)
+      tma_add_5d(&y, box, 0, static_cast<int32_t>(grp), static_cast<int32_t>(ow),
+                 static_cast<int32_t>(oh), static_cast<int32_t>(m0));
+    else
+      tma_store_5d(&y, box, 0, static_cast<int32_t>(grp), static_cast<int32_t>(ow),
+                   static_cast<int32_t>(oh), static_cast<int32_t>(m0));
+  }
   __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
                                           bool add) const {
     const uint32_t t = n0 / (kSharePix * 32), p = n0 % (kSharePix * 32) / 32;
@@ -1246,10 +1263,21 @@ ShareGeom share_geom(const ConvArgs& a, bool resident) {
   q.img = resident ? a.fh * q.kr * q.bn * 4 + 16 * 128 : 0;  // + slack for the M = 128 reads
   q.slots = 0;
   for (uint32_t n = kPStagesMax; n >= 3 && !q.slots; --n)
-    if (1024ull + n * q.slot + q.img + 16 + sizeof(PCtl) <= kMaxDynSmem) q.slots = n;
+    if (1024ull + n * q.slot + q.img + 1024 + kEpiStageBytes + sizeof(PCtl) <= kMaxDynSmem)
+      q.slots = n;
   q.ok = a.precision == LCNN_PREC_TF32 && a.co <= kTcBM && a.n % 32 == 0 && a.ci <= 256 &&
          q.bw <= 256 && q.kr <= 256 && a.stride * a.ci * 128 < (1u << 18) && q.slots >= 3;
   return q;
+}
+
+// Output view of the ShareOut TMA-store epilogue (see ShareOut::y).
+bool make_share_out_map(CUtensorMap* m, const ConvArgs& a) {
+  const uint64_t dims[5] = {32, a.n / 32, a.wo, a.ho, a.co};
+  const uint64_t pitch[4] = {128, static_cast<uint64_t>(a.n) * 4,
+                             static_cast<uint64_t>(a.wo) * a.n * 4,
+                             static_cast<uint64_t>(a.ho) * a.wo * a.n * 4};
+  const uint32_t box[5] = {32, 1, 1, 1, 32};
+  return make_tmap(m, a.dst, 5, dims, pitch, box, nullptr, 0);
 }
 
 cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s) {
@@ -1274,6 +1302,7 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
   sc.a_bytes = q.wbytes;
   sc.stage_bytes = q.wbytes + q.bw * a.ci * 128;
   sched_ring(sc, q.slots, q.slot, q.img);
+  sched_epi(sc, q.img);
   if (sc.dp_tiles < tiles) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
     const uint64_t col0 = static_cast<uint64_t>(sc.dp_tiles / (L.owb * L.groups)) * a.wo * a.n;
@@ -1281,6 +1310,7 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
     if (e != cudaSuccess) return e;
   }
   ShareOut O{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, L.owb, L.groups};
+  if (!make_share_out_map(&O.y, a)) return cudaErrorInvalidValue;
   return launch_persistent(L, O, sc, s);
 }
 

@@ -112,7 +112,21 @@ struct Sched {
   // then (optionally) the resident B operand at `resident_off`, then PCtl at
   // `ctl_off`; `smem_bytes` is the dynamic allocation (+1 KB for alignment)
   uint32_t stages, stage_stride, resident_off, ctl_off, smem_bytes;
+  // epilogue staging for TMA-store outputs (Out::kTmaStore): per epilogue
+  // warp two 4 KB boxes of 32 rows x 128 B (SWIZZLE_128B) at epi_off
+  uint32_t epi_off;
 };
+
+// Out types that write their 32 x 32 accumulator chunks with TMA stores
+template <class O, class = void>
+struct OutTma {
+  static constexpr bool value = false;
+};
+template <class O>
+struct OutTma<O, decltype(void(O::kTmaStore))> {
+  static constexpr bool value = O::kTmaStore;
+};
+constexpr uint32_t kEpiStageBytes = 4 * 2 * 4096;
 
 // Default carve-up: kPStages slots of kPStageBytes, no resident operand.
 inline void sched_ring(Sched& s, uint32_t stages, uint32_t stride, uint32_t resident_bytes) {
@@ -120,6 +134,13 @@ inline void sched_ring(Sched& s, uint32_t stages, uint32_t stride, uint32_t resi
   s.stage_stride = stride;
   s.resident_off = stages * stride;
   s.ctl_off = (s.resident_off + resident_bytes + 15) / 16 * 16;
+  s.smem_bytes = 1024 + s.ctl_off + static_cast<uint32_t>(sizeof(PCtl));
+  s.epi_off = 0;
+}
+// Append the TMA-store epilogue staging (1 KB aligned) before PCtl.
+inline void sched_epi(Sched& s, uint32_t resident_bytes) {
+  s.epi_off = (s.resident_off + resident_bytes + 1023) / 1024 * 1024;
+  s.ctl_off = s.epi_off + kEpiStageBytes;
   s.smem_bytes = 1024 + s.ctl_off + static_cast<uint32_t>(sizeof(PCtl));
 }
 
@@ -343,7 +364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;
-    uint32_t local = 0;
+    uint32_t local = 0, epi_buf = 0;
     for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
       ++local;
@@ -352,16 +373,44 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       const uint32_t m = (t - ntile * sc.mt) * kTcBM + q * 32 + lane;
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
+      if constexpr (OutTma<Out>::value) {
+        // registers -> swizzled 32 x 128 B smem box -> one TMA store (or
+        // f32 add-reduction for a stream-K fragment) per 32-column chunk
+        uint8_t* stg = smem + sc.epi_off + q * 8192;
 #pragma unroll 1
-      for (uint32_t c = 0; c < sc.bn; c += 32) {
-        float v[32];
-        tmem_ld32(base + c, v);
-        if (!(sc.probe & 2)) out.store32(m, ntile * sc.bn + c, v, split);
+        for (uint32_t c = 0; c < sc.bn; c += 32) {
+          float v[32];
+          tmem_ld32(base + c, v);
+          uint8_t* box = stg + (epi_buf & 1) * 4096;
+          ++epi_buf;
+          if (lane == 0) bulk_wait_read_n<1>();  // this buffer's previous store has read it
+          __syncwarp();
+          float4* row = reinterpret_cast<float4*>(box + lane * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            row[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && !(sc.probe & 2)) {
+            out.tma_chunk(box, m, ntile * sc.bn + c, split);
+            bulk_commit();
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (uint32_t c = 0; c < sc.bn; c += 32) {
+          float v[32];
+          tmem_ld32(base + c, v);
+          if (!(sc.probe & 2)) out.store32(m, ntile * sc.bn + c, v, split);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl->tempty[a]);
     });
+    if constexpr (OutTma<Out>::value) {
+      if (lane == 0) bulk_wait_read_n<0>();
+    }
   }
   tc_fence_before();
   __syncthreads();
