@@ -259,7 +259,7 @@ def build_workload(name, torch, device, rank, plan):
         layout = CHWN if name == "vgg_pools" else NCHW
         # measured best per layer (scripts/pool_plans.py [nchw vgg] on B200)
         plans = [plan] * len(VGG_POOLS) if plan else (
-            [(1, 1)] * len(VGG_POOLS) if layout == CHWN else [(4, 2), (3, 1), (2, 1), (1, 2), (3, 1)])
+            [(1, 1)] * len(VGG_POOLS) if layout == CHWN else [(2, 2), (4, 1), (2, 1), (2, 1), (1, 2)])
         ops = [PoolOp(torch, device, b, c, hw, hw, layout, 2, 2, False, plans[i], seed + i)
                for i, (c, hw) in enumerate(VGG_POOLS)]
         lname = "CHWN (selector's pooling layout)" if layout == CHWN else "NCHW"

@@ -216,8 +216,9 @@ lcnn_status lcnn_pool_layout(const float* src, float* dst, uint32_t n, uint32_t 
   if (st != LCNN_OK) return st;
   if (layout != LCNN_CHWN && layout != LCNN_NCHW)
     return fail(LCNN_ELAYOUT, "pool_layout: only CHWN and NCHW kernels exist");
-  // NCHW: the pipelined kernel's measured output block (scripts/pool_plans.py on B200:
-  // 3x3/s2 -> 3x2 (PL5 4204 -> 5386 GB/s); 2x2/s2 -> 4x2 on >= 200-wide planes, else 3x1);
+  // NCHW: the pipelined kernel's measured output block (scripts/pool_plans.py on B200,
+  // profiles/r01_pool_plans_nchw*.txt: 3x3/s2 -> 3x2 (PL5 3883 -> 5936 GB/s); 2x2/s2 ->
+  // 2x2 on >= 200-wide planes, 4x1 >= 100, 2x1 >= 20, else 1x2);
   // every output keeps its tap order, so the bits equal the plain kernel's and
   // the report stays the plain one
   uint32_t fh = 1, fw = 1;
@@ -225,8 +226,8 @@ lcnn_status lcnn_pool_layout(const float* src, float* dst, uint32_t n, uint32_t 
     fh = 3;
     fw = 2;
   } else if (layout == LCNN_NCHW && win_h == win_w && stride == 2 && win_h == 2) {
-    fh = w >= 200 ? 4 : 3;
-    fw = w >= 200 ? 2 : 1;
+    fh = w >= 200 ? 2 : w >= 100 ? 4 : w >= 20 ? 2 : 1;
+    fw = w >= 200 ? 2 : w >= 20 ? 1 : 2;
   }
   lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
                         mode == LCNN_POOL_AVG, fh, fw};

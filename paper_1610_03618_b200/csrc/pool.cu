@@ -27,6 +27,9 @@
 // and write contiguous output rows.
 #include <float.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -269,14 +272,14 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_kernel(NchwGeom g) {
 // Persistent, pipelined NCHW kernel (strides 1 and 2, vertical coarsening).
 // A work unit is either a group of whole (n,c) planes (small maps) or one
 // band of output rows of a large plane; either way one contiguous input
-// span.  One thread streams the spans of the next units into a kPipe-deep
+// span.  One thread streams the spans of the next units into a g.pipe-deep
 // shared-memory ring with TMA bulk copies (cp.async.bulk + mbarrier
 // complete_tx), so HBM reads of unit i+2 overlap the arithmetic of unit i.
 // Spans are copied 16-byte aligned; the issuing thread patches the <= 3
 // trailing floats a 16-byte granule cannot cover into the slot with plain
 // loads (visible to the consumers through the barriers that separate issue
 // from use), so the tap loop reads shared memory unconditionally.
-constexpr int kPipe = 3;
+constexpr int kPipeMax = 8;
 
 struct NchwPipeGeom {
   const float* src;
@@ -288,6 +291,7 @@ struct NchwPipeGeom {
   uint32_t nbands;    // bands per plane (1 in whole-plane mode)
   uint32_t units;
   uint32_t stage_floats;  // ring slot size (multiple of 4)
+  uint32_t pipe;          // ring slots (<= kPipeMax)
   FastDiv div_wo, div_plane_items;
   float divisor;
 };
@@ -333,27 +337,27 @@ template <int WH, int S, int FH, int FW, bool AVG>
 __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g) {
   LCNN_PDL_ENTRY();
   extern __shared__ __align__(16) float ring[];
-  __shared__ __align__(8) uint64_t bar[kPipe];
-  __shared__ uint32_t meta[kPipe][2];  // (float offset of the span, floats copied)
+  __shared__ __align__(8) uint64_t bar[kPipeMax];
+  __shared__ uint32_t meta[kPipeMax][2];  // (float offset of the span, floats copied)
   constexpr int WW = WH;
   constexpr int UH = S * (FH - 1) + WH;
   constexpr int UW = S * (FW - 1) + WW;  // columns of one FW-wide output block's window union
   if (threadIdx.x == 0) {
-    for (int k = 0; k < kPipe; ++k)
+    for (uint32_t k = 0; k < g.pipe; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
           static_cast<uint32_t>(__cvta_generic_to_shared(&bar[k]))));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  auto issue = [&](uint32_t i) {  // unit index i of this CTA -> ring slot i % kPipe
+  auto issue = [&](uint32_t i) {  // unit index i of this CTA -> ring slot i % g.pipe
     const uint32_t u = blockIdx.x + i * gridDim.x;
     if (u >= g.units) return;
     const PipeUnit pu = pipe_unit(g, u, S, WH);
     const uintptr_t addr = reinterpret_cast<uintptr_t>(pu.span);
     const uint32_t mis = static_cast<uint32_t>((addr >> 2) & 3u);
     const uint32_t bytes = ((mis + pu.count) * 4u) & ~15u;
-    const int k = i % kPipe;
+    const uint32_t k = i % g.pipe;
     meta[k][0] = mis;
     meta[k][1] = bytes / 4;
     float* slot = ring + static_cast<size_t>(k) * g.stage_floats;
@@ -371,16 +375,16 @@ __global__ void __launch_bounds__(kThreads) pool_nchw_pipe_kernel(NchwPipeGeom g
   };
 
   if (threadIdx.x == 0)
-    for (int i = 0; i < kPipe - 1; ++i) issue(i);
+    for (uint32_t i = 0; i + 1 < g.pipe; ++i) issue(i);
 
   for (uint32_t i = 0;; ++i) {
     const uint32_t u = blockIdx.x + i * gridDim.x;
     if (u >= g.units) break;
-    if (threadIdx.x == 0) issue(i + kPipe - 1);
-    const int k = i % kPipe;
+    if (threadIdx.x == 0) issue(i + g.pipe - 1);
+    const uint32_t k = i % g.pipe;
     {
       const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[k]));
-      const uint32_t parity = (i / kPipe) & 1;
+      const uint32_t parity = (i / g.pipe) & 1;
       asm volatile(
           "{\n.reg .pred p;\nWAIT_%=:\n"
           "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -679,7 +683,23 @@ cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
   const uint64_t planes = static_cast<uint64_t>(a.n) * a.c;
   const uint64_t row_bytes = static_cast<uint64_t>(a.w) * 4;
   const uint64_t plane_bytes = row_bytes * a.h;
-  constexpr uint64_t kSlot = 24 * 1024;  // bytes of input per ring slot
+  // Ring slot bytes, slots per CTA and CTAs per SM.  Measured on B200
+  // (scripts/nchw_pipe_sweep.sh, profiles/r01_nchw_pipe_sweep.txt): double
+  // buffering with more resident CTAs beats a deeper ring -- whole planes
+  // (PL5 55x55): 48 KB x 2 x 2 CTAs, 5.26 -> 5.92 TB/s; row bands (VGG):
+  // 24 KB x 2 x 4 CTAs, 6.03 -> 6.43 TB/s.  LCNN_NCHW_PIPE="slot_kb,slots,ctas"
+  // overrides both (profiling).
+  static const uint32_t* knob = [] {
+    static uint32_t v[3] = {0, 0, 0};
+    if (const char* e = std::getenv("LCNN_NCHW_PIPE"))
+      std::sscanf(e, "%u,%u,%u", &v[0], &v[1], &v[2]);
+    if (v[1] < 2 || v[1] > kPipeMax) v[0] = 0;
+    return v;
+  }();
+  const bool whole = plane_bytes + 16 <= 48 * 1024;
+  const uint32_t cfg[3] = {knob[0] ? knob[0] : (whole ? 48u : 24u), knob[0] ? knob[1] : 2u,
+                           knob[0] ? knob[2] : (whole ? 2u : 4u)};
+  const uint64_t kSlot = uint64_t{cfg[0]} * 1024;
   if (static_cast<uint64_t>(a.win_h) * row_bytes + 16 > kSlot) return cudaErrorNotSupported;
   if (planes > 0xffffffffull) return cudaErrorNotSupported;
   NchwPipeGeom g;
@@ -712,12 +732,13 @@ cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
   g.stage_floats = static_cast<uint32_t>((span_bytes + 16 + 15) / 16 * 4);
   const uint32_t nrb = (g.band + a.fh - 1) / a.fh;
   g.div_plane_items = FastDiv(nrb * ((a.wo + a.fw - 1) / a.fw));
-  const uint32_t smem = kPipe * g.stage_floats * 4;
-  // persistent: up to 3 CTAs per SM (72 KB rings), never more CTAs than units
+  g.pipe = cfg[1];
+  const uint32_t smem = g.pipe * g.stage_floats * 4;
+  // persistent: cfg[2] CTAs per SM, never more CTAs than units
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t cap = static_cast<uint64_t>(sms) * 3;
+  const uint64_t cap = static_cast<uint64_t>(sms) * cfg[2];
   const uint32_t blocks = static_cast<uint32_t>(units < cap ? units : cap);
 #define LCNN_PIPE(WH_, S_, FH_, FW_)                                        \
   if (a.win_h == WH_ && a.stride == S_ && a.fh == FH_ && a.fw == FW_)       \

@@ -109,14 +109,24 @@ static void run(const char* name, Cfg c) {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   const double n_mma = double(c.iters) * 4;
   const uint32_t N = ((c.idesc >> 17) & 0x3F) * 8;
-  const double tflops = 148.0 * n_mma * 2 * 128 * N * 8 / (ms * 1e9);
-  printf("%-40s acc=%d N=%3u  %7.1f cyc/MMA  %7.1f TF/s  %s\n", name, c.nacc, N, double(h[0]) / n_mma, tflops,
+  const uint32_t M = ((c.idesc >> 24) & 0x1F) * 16;
+  const double tflops = 148.0 * n_mma * 2 * M * N * 8 / (ms * 1e9);
+  printf("%-40s M=%3u acc=%d N=%3u  %7.1f cyc/MMA  %7.1f TF/s  %s\n", name, M, c.nacc, N, double(h[0]) / n_mma, tflops,
          err == cudaSuccess ? "" : cudaGetErrorString(err));
   cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int iters = 4000;
+  if (argc > 1) {  // M = 64 (half the tensor rows): does it cost half an M = 128 MMA?
+    for (uint32_t N : {64u, 128u, 192u, 256u}) {
+      Cfg k{idesc_tf32(64, N, false, true), 2, 16, 1024, 32, 1, 4096, 512, 1024, 4, iters};
+      run("M64 A K-sw128 B MN-sw128_32b", k);
+      Cfg c{idesc_tf32(128, N, false, true), 2, 16, 1024, 32, 1, 4096, 512, 1024, 4, iters};
+      run("M128 A K-sw128 B MN-sw128_32b", c);
+    }
+    return 0;
+  }
   for (uint32_t N : {32u, 64u, 96u, 128u, 192u, 256u}) {
     // A MN-major SW128_32B (the CHWN input operand), B K-major SW128 (packed filters)
     Cfg c{idesc_tf32(128, N, true, false), 1, 4096, 512, 1024, 2, 16, 1024, 32, 4, iters};
