@@ -382,6 +382,18 @@ struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a mul
   float* c;
   uint64_t ldc;
   uint32_t M, N;
+  // TMA-store epilogue: 2D view {N cols, M rows} (pitch ldc), box {32, 32},
+  // SWIZZLE_128B; out-of-range rows / columns of a box are clipped
+  CUtensorMap y;
+  static constexpr bool kTmaStore = true;
+  __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
+                                            bool add) const {
+    if (n0 >= N || m0 >= M) return;
+    if (add)
+      tma_add_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
+    else
+      tma_store_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
+  }
   __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
                                           bool add) const {
     if (n0 >= N) return;  // warp-uniform
@@ -1000,6 +1012,13 @@ bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t*
                int swizzle);
 cudaError_t launch_split_hilo(const float* x, float* hi, float* lo, uint64_t count,
                               cudaStream_t s);
+inline bool make_rows_out_map(CUtensorMap* m, const RowsOut& o) {
+  const uint64_t dims[2] = {o.N, o.M};
+  const uint64_t pitch[1] = {o.ldc * 4};
+  const uint32_t box[2] = {32, 32};
+  return make_tmap(m, o.c, 2, dims, pitch, box, nullptr, 0);
+}
+
 
 namespace {
 
@@ -1228,7 +1247,8 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
     sc.stage_bytes = in_bytes + w_region;
     const uint32_t stride = (x_region + w_region + 1023) / 1024 * 1024;
     uint32_t n = kPStages;
-    while (n > 2 && 1024 + n * stride + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
+    const uint32_t epi = kCoOnN ? 0 : 1024 + kEpiStageBytes;  // RowsOut TMA-store staging
+    while (n > 2 && 1024 + n * stride + epi + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
     sched_ring(sc, n, stride, 0);
   }
   if (cudaError_t e = zero_sk_region(sc, kCoOnN, kCoOnN ? bn : kTcBM, a.dst, L.ncols, a.co, s);
@@ -1239,7 +1259,10 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
     return launch_persistent(L, O, sc, s);
   } else {
     RowsOut O{a.dst, L.ncols, a.co, L.ncols};
-    return launch_persistent(L, O, sc, s);
+    if (!make_rows_out_map(&O.y, O)) return cudaErrorInvalidValue;
+    Sched se = sc;
+    sched_epi(se, 0);  // RowsOut never has a resident operand
+    return launch_persistent(L, O, se, s);
   }
 }
 
@@ -1451,7 +1474,10 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
     return launch_persistent(L, O, sc, s);
   } else {
     RowsOut O{a.dst, L.ncols, a.co, L.ncols};
-    return launch_persistent(L, O, sc, s);
+    if (!make_rows_out_map(&O.y, O)) return cudaErrorInvalidValue;
+    Sched se = sc;
+    sched_epi(se, 0);
+    return launch_persistent(L, O, se, s);
   }
   }
 }

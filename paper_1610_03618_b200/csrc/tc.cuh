@@ -112,6 +112,21 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap* m, const void* s
       "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(v)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t x,
+                                             int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_add_2d(const CUtensorMap* m, const void* src, int32_t x,
+                                           int32_t y) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::
+          "l"(reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(src)), "r"(x), "r"(y)
+      : "memory");
+}
 __device__ __forceinline__ void tma_add_5d(const CUtensorMap* m, const void* src, int32_t x,
                                            int32_t y, int32_t z, int32_t w, int32_t v) {
   asm volatile(
