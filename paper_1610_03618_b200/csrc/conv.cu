@@ -385,7 +385,7 @@ struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a mul
   // TMA-store epilogue: 2D view {N cols, M rows} (pitch ldc), box {32, 32},
   // SWIZZLE_128B; out-of-range rows / columns of a box are clipped
   CUtensorMap y;
-  static constexpr bool kTmaStore = true;
+  static constexpr bool kTmaStore = true, kTmaTransposed = false;
   __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
                                             bool add) const {
     if (n0 >= N || m0 >= M) return;
@@ -408,9 +408,22 @@ struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a mul
 // Accumulator row m = output column (oh, ow, n), columns = output channels:
 // out[co][col] (CHWN).  For each channel the 32 lanes of a warp hold 32
 // consecutive columns, so every store instruction is one coalesced 128 B line.
-struct ColsOut {
+template <bool kTma>
+struct ColsOutT {
   float* c;
   uint32_t ncols, co;
+  // TMA-store epilogue (kTma): the RowsOut view {ncols, C_o}; a chunk is
+  // 32 accumulator rows (columns of C) x 32 channels, staged transposed
+  CUtensorMap y;
+  static constexpr bool kTmaStore = kTma, kTmaTransposed = true;
+  __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
+                                            bool add) const {
+    if (m0 >= ncols || n0 >= co) return;
+    if (add)
+      tma_add_2d(&y, box, static_cast<int32_t>(m0), static_cast<int32_t>(n0));
+    else
+      tma_store_2d(&y, box, static_cast<int32_t>(m0), static_cast<int32_t>(n0));
+  }
   __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
                                           bool add) const {
     if (m >= ncols) return;
@@ -425,6 +438,8 @@ struct ColsOut {
     }
   }
 };
+using ColsOut = ColsOutT<true>;
+using ColsOutPlain = ColsOutT<false>;
 
 // SHARE mode (small C_i * F_w and C_o <= 128, e.g. AlexNet conv1: 3 x 11,
 // stride 4).  A tile is 8 consecutive output pixels of one output row x one
@@ -501,7 +516,7 @@ struct ShareOut {
   // TMA-store epilogue: view {32 n, N/32, Wo, Ho, Co} of the output, box
   // {32, 1, 1, 1, 32} = one 32-channel x 32-image chunk, SWIZZLE_128B
   CUtensorMap y;
-  static constexpr bool kTmaStore = true;
+  static constexpr bool kTmaStore = true, kTmaTransposed = false;
   __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
                                             bool add) const {
     const uint32_t t = n0 / (kSharePix * 32), p = n0 % (kSharePix * 32) / 32;
@@ -1012,6 +1027,12 @@ bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t*
                int swizzle);
 cudaError_t launch_split_hilo(const float* x, float* hi, float* lo, uint64_t count,
                               cudaStream_t s);
+inline bool make_cols_out_map(CUtensorMap* m, const ColsOut& o) {
+  const uint64_t dims[2] = {o.ncols, o.co};
+  const uint64_t pitch[1] = {static_cast<uint64_t>(o.ncols) * 4};
+  const uint32_t box[2] = {32, 32};
+  return make_tmap(m, o.c, 2, dims, pitch, box, nullptr, 0);
+}
 inline bool make_rows_out_map(CUtensorMap* m, const RowsOut& o) {
   const uint64_t dims[2] = {o.N, o.M};
   const uint64_t pitch[1] = {o.ldc * 4};
@@ -1255,7 +1276,7 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
       e != cudaSuccess)
     return e;
   if constexpr (kCoOnN) {
-    ColsOut O{a.dst, L.ncols, a.co};
+    ColsOutPlain O{a.dst, L.ncols, a.co};
     return launch_persistent(L, O, sc, s);
   } else {
     RowsOut O{a.dst, L.ncols, a.co, L.ncols};
@@ -1455,11 +1476,14 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
     sc.stage_bytes = kTcABytes + wbox * kTcBK * 4;
     const uint32_t stride = (sc.stage_bytes + 1023) / 1024 * 1024;
     uint32_t n = kPStagesMax;
-    while (n > 2 && 1024 + n * stride + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
+    constexpr uint32_t epi = 1024 + 4 * 4096;  // one TMA-store box per epilogue warp
+    while (n > 2 && 1024 + n * stride + epi + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
     sched_ring(sc, n, stride, 0);
+    sched_epi(sc, 0, 1);
     if (cudaError_t e = zero_sk_region(sc, true, bw, a.dst, L.ncols, a.co, s, tm); e != cudaSuccess)
       return e;
     ColsOut O{a.dst, L.ncols, a.co};
+    if (!make_cols_out_map(&O.y, O)) return cudaErrorInvalidValue;
     return launch_pair(L, O, sc, s);
   } else {
   const Sched sc =
@@ -1471,7 +1495,10 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
     return e;
   if constexpr (kCoOnN) {
     ColsOut O{a.dst, L.ncols, a.co};
-    return launch_persistent(L, O, sc, s);
+    if (!make_cols_out_map(&O.y, O)) return cudaErrorInvalidValue;
+    Sched se = sc;
+    sched_epi(se, 0);
+    return launch_persistent(L, O, se, s);
   } else {
     RowsOut O{a.dst, L.ncols, a.co, L.ncols};
     if (!make_rows_out_map(&O.y, O)) return cudaErrorInvalidValue;

@@ -113,8 +113,8 @@ struct Sched {
   // `ctl_off`; `smem_bytes` is the dynamic allocation (+1 KB for alignment)
   uint32_t stages, stage_stride, resident_off, ctl_off, smem_bytes;
   // epilogue staging for TMA-store outputs (Out::kTmaStore): per epilogue
-  // warp two 4 KB boxes of 32 rows x 128 B (SWIZZLE_128B) at epi_off
-  uint32_t epi_off;
+  // warp epi_bufs 4 KB boxes of 32 rows x 128 B (SWIZZLE_128B) at epi_off
+  uint32_t epi_off, epi_bufs;
 };
 
 // Out types that write their 32 x 32 accumulator chunks with TMA stores
@@ -126,7 +126,59 @@ template <class O>
 struct OutTma<O, decltype(void(O::kTmaStore))> {
   static constexpr bool value = O::kTmaStore;
 };
-constexpr uint32_t kEpiStageBytes = 4 * 2 * 4096;
+constexpr uint32_t kEpiStageBytes = 4 * 2 * 4096;  // 4 warps x 2 boxes
+
+// One tile's accumulator rows [q*32, q*32+32) (this warp's TMEM lane quarter)
+// out of TMEM, 32 columns at a time.  TMA outputs: registers -> a swizzled
+// 32 x 128 B shared-memory box -> one TMA store (or f32 add-reduction for a
+// stream-K fragment); the box holds the chunk as [row][32 columns]
+// (Out::kTmaTransposed = false: rows = accumulator rows) or transposed
+// (true: rows = accumulator columns, for outputs whose accumulator rows are
+// the contiguous dimension).  Other outputs: Out::store32.
+template <class Out>
+__device__ __forceinline__ void epilogue_tile(const Out& out, const Sched& sc, uint8_t* stg,
+                                              uint32_t taddr, uint32_t m, uint32_t ncol0,
+                                              bool split, uint32_t& epi_buf, int lane) {
+  if constexpr (OutTma<Out>::value) {
+#pragma unroll 1
+    for (uint32_t c = 0; c < sc.bn; c += 32) {
+      float v[32];
+      tmem_ld32(taddr + c, v);
+      uint8_t* box = stg + (sc.epi_bufs == 2 ? (epi_buf & 1) : 0u) * 4096;
+      ++epi_buf;
+      if (lane == 0) {  // this box's previous store has finished reading it
+        if (sc.epi_bufs == 2) bulk_wait_read_n<1>();
+        else bulk_wait_read_n<0>();
+      }
+      __syncwarp();
+      if constexpr (Out::kTmaTransposed) {
+        // column j of the accumulator chunk -> box row j; lane = box column
+        const uint32_t col = ((static_cast<uint32_t>(lane) >> 2) << 4) | ((lane & 3) << 2);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          *reinterpret_cast<float*>(box + j * 128 + (col ^ ((j & 7) << 4))) = v[j];
+      } else {
+        float4* row = reinterpret_cast<float4*>(box + lane * 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          row[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && !(sc.probe & 2)) {
+        out.tma_chunk(box, m, ncol0 + c, split);
+        bulk_commit();
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (uint32_t c = 0; c < sc.bn; c += 32) {
+      float v[32];
+      tmem_ld32(taddr + c, v);
+      if (!(sc.probe & 2)) out.store32(m, ncol0 + c, v, split);
+    }
+  }
+}
 
 // Default carve-up: kPStages slots of kPStageBytes, no resident operand.
 inline void sched_ring(Sched& s, uint32_t stages, uint32_t stride, uint32_t resident_bytes) {
@@ -136,11 +188,14 @@ inline void sched_ring(Sched& s, uint32_t stages, uint32_t stride, uint32_t resi
   s.ctl_off = (s.resident_off + resident_bytes + 15) / 16 * 16;
   s.smem_bytes = 1024 + s.ctl_off + static_cast<uint32_t>(sizeof(PCtl));
   s.epi_off = 0;
+  s.epi_bufs = 0;
 }
-// Append the TMA-store epilogue staging (1 KB aligned) before PCtl.
-inline void sched_epi(Sched& s, uint32_t resident_bytes) {
+// Append the TMA-store epilogue staging (1 KB aligned, `bufs` 4 KB boxes per
+// epilogue warp) before PCtl.
+inline void sched_epi(Sched& s, uint32_t resident_bytes, uint32_t bufs = 2) {
   s.epi_off = (s.resident_off + resident_bytes + 1023) / 1024 * 1024;
-  s.ctl_off = s.epi_off + kEpiStageBytes;
+  s.epi_bufs = bufs;
+  s.ctl_off = s.epi_off + 4 * bufs * 4096;
   s.smem_bytes = 1024 + s.ctl_off + static_cast<uint32_t>(sizeof(PCtl));
 }
 
@@ -373,37 +428,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       const uint32_t m = (t - ntile * sc.mt) * kTcBM + q * 32 + lane;
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
-      if constexpr (OutTma<Out>::value) {
-        // registers -> swizzled 32 x 128 B smem box -> one TMA store (or
-        // f32 add-reduction for a stream-K fragment) per 32-column chunk
-        uint8_t* stg = smem + sc.epi_off + q * 8192;
-#pragma unroll 1
-        for (uint32_t c = 0; c < sc.bn; c += 32) {
-          float v[32];
-          tmem_ld32(base + c, v);
-          uint8_t* box = stg + (epi_buf & 1) * 4096;
-          ++epi_buf;
-          if (lane == 0) bulk_wait_read_n<1>();  // this buffer's previous store has read it
-          __syncwarp();
-          float4* row = reinterpret_cast<float4*>(box + lane * 128);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            row[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && !(sc.probe & 2)) {
-            out.tma_chunk(box, m, ntile * sc.bn + c, split);
-            bulk_commit();
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (uint32_t c = 0; c < sc.bn; c += 32) {
-          float v[32];
-          tmem_ld32(base + c, v);
-          if (!(sc.probe & 2)) out.store32(m, ntile * sc.bn + c, v, split);
-        }
-      }
+      epilogue_tile(out, sc, smem + sc.epi_off + q * sc.epi_bufs * 4096, base, m, ntile * sc.bn,
+                    split, epi_buf, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl->tempty[a]);
@@ -537,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // ---------------- epilogue (both CTAs: own TMEM half) ----------------
     const int q = warp & 3;
     const uint32_t leader_tempty = mapa_shared(smem_u32(&ctl->tempty[0]), 0);
-    uint32_t local = 0;
+    uint32_t local = 0, epi_buf = 0;
     for_each_work(sc, pair, npairs, [&](uint32_t t, uint32_t, uint32_t, bool split) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
       ++local;
@@ -546,16 +572,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       const uint32_t m = (t - ntile * sc.mt) * (2 * kTcBM) + rank * kTcBM + q * 32 + lane;
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
-#pragma unroll 1
-      for (uint32_t c = 0; c < sc.bn; c += 32) {
-        float v[32];
-        tmem_ld32(base + c, v);
-        if (!(sc.probe & 2)) out.store32(m, ntile * sc.bn + c, v, split);
-      }
+      epilogue_tile(out, sc, smem + sc.epi_off + q * sc.epi_bufs * 4096, base, m, ntile * sc.bn,
+                    split, epi_buf, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + a * 8);
     });
+    if constexpr (OutTma<Out>::value) {
+      if (lane == 0) bulk_wait_read_n<0>();
+    }
   }
   tc_fence_before();
   __syncthreads();
