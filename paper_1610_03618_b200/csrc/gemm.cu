@@ -81,10 +81,24 @@ struct GemmLoader {
   }
 };
 
-struct GemmOut {
+template <bool kTma>
+struct GemmOutT {
   float* c;
   uint64_t ldc;
   uint32_t M, N;
+  // TMA-store epilogue (kTma; needs ldc % 4 == 0 and a 16-B aligned C): 2D
+  // view {N, M}, box {32, 32}, SWIZZLE_128B -- the stream-K fragments of the
+  // skinny fc GEMMs become TMA add-reductions instead of per-lane vector atomics
+  CUtensorMap y;
+  static constexpr bool kTmaStore = kTma, kTmaTransposed = false;
+  __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
+                                            bool add) const {
+    if (n0 >= N || m0 >= M) return;
+    if (add)
+      tma_add_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
+    else
+      tma_store_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
+  }
   __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
                                           bool add) const {
     if (n0 >= N) return;  // warp-uniform
@@ -95,6 +109,7 @@ struct GemmOut {
     }
   }
 };
+
 
 // fc layer on pre-packed weights (softmax.cpp:182-184 fc_forward with the
 // weights of a network layer, constant across forwards).  B = W^T packed once
@@ -349,6 +364,24 @@ bool make_tmap(CUtensorMap* m, const float* base, uint32_t rank, const uint64_t*
          CUDA_SUCCESS;
 }
 
+// Launch the persistent kernel with a TMA-store epilogue when C allows it.
+template <class Loader>
+cudaError_t launch_gemm_out(const Loader& L, float* c, uint64_t ldc, uint32_t m, uint32_t n,
+                            const Sched& sc, cudaStream_t s) {
+  if (ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(c) & 15u) == 0) {
+    lcnn_dev::GemmOutT<true> O{c, ldc, m, n};
+    const uint64_t dims[2] = {n, m};
+    const uint64_t pitch[1] = {ldc * 4};
+    const uint32_t box[2] = {32, 32};
+    Sched se = sc;
+    sched_epi(se, se.ctl_off - se.resident_off > 16 ? se.ctl_off - se.resident_off : 0);
+    if (se.smem_bytes <= kMaxDynSmem && make_tmap(&O.y, c, 2, dims, pitch, box, nullptr, 0))
+      return launch_persistent(L, O, se, s);
+  }
+  lcnn_dev::GemmOutT<false> O{c, ldc, m, n};
+  return launch_persistent(L, O, sc, s);
+}
+
 bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a, const void* b) {
   // TMA: 16-byte aligned bases and row pitches
   return m > 0 && n > 0 && k > 0 && (k % 4 == 0) && (n % 4 == 0) &&
@@ -420,8 +453,7 @@ cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
     cudaError_t e = launch_zero2d(c + zc, n, n - zc, m, s);
     if (e != cudaSuccess) return e;
   }
-  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
-  return launch_persistent(L, O, sc, s);
+  return launch_gemm_out(L, c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n), sc, s);
 }
 
 cudaError_t launch_gemm_fp32(const float* a, const float* b, float* c, uint64_t m, uint64_t n,
@@ -450,6 +482,7 @@ cudaError_t launch_fc_pack(const float* w, uint64_t k, uint64_t n, int precision
   pack_fc_kernel<<<grid, 256, 0, s>>>(w, hi, lo, static_cast<uint32_t>(k), static_cast<uint32_t>(n));
   return cudaGetLastError();
 }
+
 
 namespace {
 
@@ -566,8 +599,7 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
     cudaError_t e = launch_zero2d(c + zc, n, n - zc, m, s);
     if (e != cudaSuccess) return e;
   }
-  GemmOut O{c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n)};
-  return launch_persistent(L, O, sc, s);
+  return launch_gemm_out(L, c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n), sc, s);
 }
 
 }  // namespace
