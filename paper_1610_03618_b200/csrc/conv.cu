@@ -714,6 +714,215 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
   }
 }
 
+// ---- TAPS-N: tap-sharing boxes with channels on N, on a CTA pair ---------
+// The TAPS idea for the L2-resident CI layers (AlexNet conv2-5), oriented
+// like the pair kernel: the input is the MN-major A operand and the filters
+// the K-major B operand, N = a C_o tile (<= 256, no padding of 192 / 384).
+// A CTA's 128 accumulator rows are 4 consecutive output pixels of one output
+// row x its 32-image group; the two CTAs of a pair take the two 32-image
+// groups of a 64-image block (UMMA M = 256).  K runs (fh, 32-channel block,
+// fw, c), the TAPS pack order: one input box {32 n, 32 c, BW = 3*S + F_w w}
+// per (fh, block) -- rows (w, c), c fastest -- serves all F_w taps, tap fw's
+// 4 MN atoms starting fw * 4 KB into the box at a pitch of S * 4 KB; each
+// CTA streams HALF of the tap's filter slice (cta_group::2).  Per CTA and
+// (fh, block) that is BW*4 KB + F_w * (C_o tile / 2) * 128 B for 4*F_w MMAs:
+// conv2 92 KB per 20 MMAs where the pair CI kernel moves 140 KB.
+// Epilogue: warp q holds pixel q's 32 images x the C_o tile; each 32-channel
+// chunk is staged transposed (box rows = channels, 128 B of images) and TMA-
+// stored into the CHWN output (the ShareOut view), add-reduced for stream-K
+// fragments.
+struct TapsNCtl {
+  uint64_t ifull[4], iempty[4];
+  uint64_t ffull[8], fempty[8];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_addr;
+};
+
+struct TapsNParams {
+  CUtensorMap x;  // input view {32 n, Ci, W, N/32, H}, box {32, 32, BW, 1, 1}
+  CUtensorMap w;  // packed filters [Co][K] (TAPS order), box {32 k, bw/2 co}
+  CUtensorMap y;  // output view {32 n, N/32, Wo, Ho, Co}, box {32, 1, 1, 1, 32}
+  Sched sc;       // mt = C_o tiles, nt = Ho * OWB * G2, iters = FH * CB
+  uint32_t FW, S, P, CB, OWB, G2, Wo, bw;
+  uint32_t ni, nf, islot, ibox, fslot;  // ring slots, slot / box bytes (per CTA)
+  uint32_t epi_off, ctl_off;
+};
+
+constexpr uint32_t kTapsNPix = 4;  // output pixels per CTA tile (4 x 32 images = M 128)
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+    tc_conv_tapsn_pair_kernel(const __grid_constant__ TapsNParams prm) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw_smem) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* ibase = smem;
+  uint8_t* fbase = smem + prm.ni * prm.islot;
+  TapsNCtl* ctl = reinterpret_cast<TapsNCtl*>(smem + prm.ctl_off);
+  const Sched& sc = prm.sc;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch(&prm.x);
+      tma_prefetch(&prm.w);
+      for (uint32_t i = 0; i < prm.ni; ++i) {
+        mbar_init(&ctl->ifull[i], 1);
+        mbar_init(&ctl->iempty[i], 1);
+      }
+      for (uint32_t i = 0; i < prm.nf; ++i) {
+        mbar_init(&ctl->ffull[i], 1);
+        mbar_init(&ctl->fempty[i], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&ctl->tfull[a], 1);
+        mbar_init(&ctl->tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc_cg2<512>(&ctl->tmem_addr);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_addr;
+  LCNN_PDL_ENTRY();
+  const uint32_t half = prm.bw / 2;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs; completion on the leader) ----------------
+    const uint32_t lead_ifull = mapa_shared(smem_u32(&ctl->ifull[0]), 0);
+    const uint32_t lead_ffull = mapa_shared(smem_u32(&ctl->ffull[0]), 0);
+    uint32_t is = 0, iph = 0, fs = 0, fph = 0;
+    for_each_work(sc, pair, npairs, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t mi = t % sc.mt, ni = t / sc.mt;
+      const uint32_t g2 = ni % prm.G2, r = ni / prm.G2, ob = r % prm.OWB, oh = r / prm.OWB;
+      const int32_t x0 = static_cast<int32_t>(ob * kTapsNPix * prm.S) - static_cast<int32_t>(prm.P);
+      const int32_t z0 = static_cast<int32_t>(oh * prm.S) - static_cast<int32_t>(prm.P);
+      const int32_t grp = static_cast<int32_t>(2 * g2 + rank);
+      const int32_t co0 = static_cast<int32_t>(mi * prm.bw + rank * half);
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        const uint32_t fh = it / prm.CB, cb = it - fh * prm.CB;
+        mbar_wait(&ctl->iempty[is], iph ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&ctl->ifull[is], 2 * prm.ibox);
+        tma_load_5d_cg2(ibase + is * prm.islot, &prm.x, lead_ifull + is * 8, 0,
+                        static_cast<int32_t>(cb * 32), x0, grp, z0 + static_cast<int32_t>(fh));
+        if (++is == prm.ni) {
+          is = 0;
+          iph ^= 1;
+        }
+        for (uint32_t fw = 0; fw < prm.FW; ++fw) {
+          mbar_wait(&ctl->fempty[fs], fph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&ctl->ffull[fs], 2 * prm.fslot);
+          tma_load_2d_cg2(fbase + fs * prm.fslot, &prm.w, lead_ffull + fs * 8,
+                          static_cast<int32_t>((it * prm.FW + fw) * kTcBK), co0);
+          if (++fs == prm.nf) {
+            fs = 0;
+            fph ^= 1;
+          }
+        }
+      }
+    });
+  } else if (warp == 1 && rank == 0) {
+    // ---------------- MMA issuer (leader, M = 256) ----------------
+    const bool mma_on = !(sc.probe & 1);
+    const uint32_t lbo = prm.S * 4096;
+    uint32_t is = 0, iph = 0, fs = 0, fph = 0, local = 0;
+    for_each_work(sc, pair, npairs, [&](uint32_t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
+      mbar_wait(&ctl->tempty[a], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + a * kPBN;
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        mbar_wait(&ctl->ifull[is], iph);
+        tc_fence_after();
+        const uint8_t* xb = ibase + is * prm.islot;
+        for (uint32_t fw = 0; fw < prm.FW; ++fw) {
+          mbar_wait(&ctl->ffull[fs], fph);
+          tc_fence_after();
+          const uint64_t da = smem_desc_sw128(xb + fw * 4096, lbo, 512, 1);
+          const uint64_t db = smem_desc_sw128(fbase + fs * prm.fslot, 16, 1024);
+          if (elect_one()) {
+            if (mma_on) {
+#pragma unroll
+              for (int k = 0; k < kTcBK / 8; ++k)
+                mma_tf32_cg2(acc, da + 64 * k, db + 2 * k, sc.idesc,
+                             (it != kbeg || fw != 0 || k != 0) ? 1u : 0u);
+            }
+            tc_commit_cg2(&ctl->fempty[fs], 3);
+          }
+          __syncwarp();
+          if (++fs == prm.nf) {
+            fs = 0;
+            fph ^= 1;
+          }
+        }
+        if (elect_one()) tc_commit_cg2(&ctl->iempty[is], 3);
+        __syncwarp();
+        if (++is == prm.ni) {
+          is = 0;
+          iph ^= 1;
+        }
+      }
+      if (elect_one()) tc_commit_cg2(&ctl->tfull[a], 3);
+      __syncwarp();
+    });
+  } else if (warp >= 2) {
+    // ---------------- epilogue (both CTAs: own TMEM half) ----------------
+    const int q = warp & 3;  // TMEM lane quarter = output pixel q of the tile
+    const uint32_t leader_tempty = mapa_shared(smem_u32(&ctl->tempty[0]), 0);
+    uint8_t* box = smem + prm.epi_off + q * 4096;
+    const uint32_t col = ((static_cast<uint32_t>(lane) >> 2) << 4) | ((lane & 3) << 2);
+    uint32_t local = 0;
+    for_each_work(sc, pair, npairs, [&](uint32_t t, uint32_t, uint32_t, bool split) {
+      const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+      ++local;
+      const uint32_t mi = t % sc.mt, ni = t / sc.mt;
+      const uint32_t g2 = ni % prm.G2, r = ni / prm.G2, ob = r % prm.OWB, oh = r / prm.OWB;
+      const uint32_t ow = ob * kTapsNPix + q;
+      mbar_wait(&ctl->tfull[a], aphase);
+      tc_fence_after();
+      const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (uint32_t c = 0; c < prm.bw; c += 32) {
+        float v[32];
+        tmem_ld32(base + c, v);
+        if (lane == 0) bulk_wait_read_n<0>();  // the box's previous store has read it
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          *reinterpret_cast<float*>(box + j * 128 + (col ^ ((j & 7) << 4))) = v[j];
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && ow < prm.Wo && !(sc.probe & 2)) {
+          const int32_t cz = static_cast<int32_t>(mi * prm.bw + c);
+          if (split)
+            tma_add_5d(&prm.y, box, 0, static_cast<int32_t>(2 * g2 + rank),
+                       static_cast<int32_t>(ow), static_cast<int32_t>(oh), cz);
+          else
+            tma_store_5d(&prm.y, box, 0, static_cast<int32_t>(2 * g2 + rank),
+                         static_cast<int32_t>(ow), static_cast<int32_t>(oh), cz);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty + a * 8);
+    });
+    if (lane == 0) bulk_wait_read_n<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc_cg2<512>(tmem);
+  }
+}
+
 // ---- NCHW implicit GEMM on tcgen05 --------------------------------------
 //   D[co][(n, p)] = sum_k W[co][k] * X[k][(n, p)],  k = (ci, fh, fw),
 //   p = oh*Wo + ow.  NCHW rows of odd width cannot be TMA tensors (16-byte
@@ -1431,6 +1640,88 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s) {
   return lcnn_pdl::launch(tc_conv_taps_kernel, sc.grid, kTcThreads, smem, s, prm);
 }
 
+// TAPS-N geometry (tc_conv_tapsn_pair_kernel): C_o tile, input box width,
+// ring slots that fit next to the 16 KB epilogue staging.
+struct TapsNGeom {
+  uint32_t bw, bwid, ibox, fslot, ni, nf;
+  bool ok;
+};
+
+TapsNGeom tapsn_geom(const ConvArgs& a) {
+  TapsNGeom q{};
+  q.bw = co_tile_n(a.co);
+  q.bwid = a.stride * (kTapsNPix - 1) + a.fw;
+  q.ibox = q.bwid * 4096;
+  q.fslot = q.bw / 2 * 128;
+  const uint64_t avail = kMaxDynSmem - 1024 - 4 * 4096 - sizeof(TapsNCtl) - 16;
+  for (uint32_t ni = 3; ni >= 2 && !q.ni; --ni) {
+    if (ni * uint64_t{q.ibox} >= avail) continue;
+    const uint64_t nf = std::min<uint64_t>(8, (avail - ni * uint64_t{q.ibox}) / q.fslot);
+    if (nf >= std::max<uint64_t>(4, a.fw + 1)) {
+      q.ni = ni;
+      q.nf = static_cast<uint32_t>(nf);
+    }
+  }
+  q.ok = a.precision == LCNN_PREC_TF32 && a.ci % 32 == 0 && a.n % 64 == 0 && q.bwid <= 256 &&
+         q.bw % 32 == 0 && q.ni >= 2 && a.stride * 4096u < (1u << 18);
+  return q;
+}
+
+cudaError_t launch_chwn_tapsn(const ConvTcArgs& t, cudaStream_t s) {
+  const ConvArgs& a = t.a;
+  const TapsNGeom q = tapsn_geom(a);
+  TapsNParams prm;
+  const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
+  const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
+                             static_cast<uint64_t>(a.n) * 4, 128,
+                             static_cast<uint64_t>(a.w) * a.n * 4};
+  const uint32_t box[5] = {32, 32, q.bwid, 1, 1};
+  if (!make_tmap(&prm.x, t.x_hi, 5, dims, pitch, box, nullptr, 1)) return cudaErrorInvalidValue;
+  const uint64_t K = t.p.K;
+  if (!make_tmap_2d(&prm.w, t.w_hi, K, a.co, K * 4, kTcBK, q.bw / 2, false))
+    return cudaErrorInvalidValue;
+  if (!make_share_out_map(&prm.y, a)) return cudaErrorInvalidValue;
+  prm.FW = a.fw;
+  prm.S = a.stride;
+  prm.P = a.pad;
+  prm.CB = a.ci / 32;
+  prm.OWB = (a.wo + kTapsNPix - 1) / kTapsNPix;
+  prm.G2 = a.n / 64;
+  prm.Wo = a.wo;
+  prm.bw = q.bw;
+  prm.ni = q.ni;
+  prm.nf = q.nf;
+  prm.islot = q.ibox;
+  prm.ibox = q.ibox;
+  prm.fslot = q.fslot;
+  prm.epi_off = q.ni * q.ibox + q.nf * q.fslot;  // 1 KB multiples
+  prm.ctl_off = prm.epi_off + 4 * 4096;
+  const uint32_t mt = (a.co + q.bw - 1) / q.bw, nt = a.ho * prm.OWB * prm.G2;
+  prm.sc = make_sched(mt, nt, a.fh * prm.CB, 1, q.bw, true, false, kMinSkIters,
+                      static_cast<uint32_t>(tc_sm_count() / 2));
+  prm.sc.idesc = idesc_tf32(2 * kTcBM, q.bw, true, false);
+  prm.sc.grid *= 2;
+  const Sched& sc = prm.sc;
+  if (sc.dp_tiles < mt * nt) {  // zero the stream-K tiles' output rows (oh >= first split row)
+    const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
+    const uint64_t col0 =
+        static_cast<uint64_t>(sc.dp_tiles / mt / (prm.OWB * prm.G2)) * a.wo * a.n;
+    cudaError_t e = launch_zero2d(a.dst + col0, ncols, ncols - col0, a.co, s);
+    if (e != cudaSuccess) return e;
+  }
+  const uint32_t smem = 1024 + prm.ctl_off + static_cast<uint32_t>(sizeof(TapsNCtl));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_tapsn_pair_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMaxDynSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (smem > kMaxDynSmem || sc.grid % 2) return cudaErrorInvalidConfiguration;
+  return lcnn_pdl::launch(tc_conv_tapsn_pair_kernel, sc.grid, kTcThreads, smem, s, prm);
+}
+
 template <bool kCoOnN, bool kPair = false>
 cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
   const ConvArgs& a = t.a;
@@ -1518,7 +1809,7 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
 namespace {
 
 enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM,
-                 kRouteShare, kRouteShareRes, kRouteChwnPair, kRouteTaps };
+                 kRouteShare, kRouteShareRes, kRouteChwnPair, kRouteTaps, kRouteTapsN };
 
 struct ConvRoute {
   RouteKind kind = kRouteSimt;
@@ -1604,14 +1895,33 @@ ConvRoute route_conv(const ConvArgs& a) {
     // conv1_2 / conv2_1 / conv2_2 3.9 / 1.05 / 1.9 ms -> 1.9 / 0.54 / 0.97 ms;
     // neutral at 56x56 and slower on AlexNet's 27x27 / 13x13 layers.
     // Profiling knob LCNN_CONV_TAPS: 0 off, 1 forced wherever supported.
+    const bool big_planes = static_cast<uint64_t>(a.h) * a.w * a.n * 4 >= (4ull << 20);
     static const int taps_knob = [] {
       const char* e = std::getenv("LCNN_CONV_TAPS");
       return e ? (e[0] == '1' ? 2 : 0) : 1;
     }();
-    const bool big_planes = static_cast<uint64_t>(a.h) * a.w * a.n * 4 >= (4ull << 20);
     if (r.p.g.mode == kModeCI && (taps_knob == 2 || (taps_knob == 1 && big_planes)) &&
         taps_geom(a).ok) {
       r.kind = kRouteTaps;
+      r.p.g.mode = kModeTAPS;
+      r.apack = static_cast<uint64_t>(a.co) * r.p.K;
+      return r;
+    }
+    // TAPS-N (tap-sharing boxes, channels on N, CTA pair) for CI layers with
+    // output rows >= 28 wide whose planes are not TAPS-sized: measured on
+    // B200 (profiles/r01_conv_tapsn.txt), VGG-16 conv3_1 / conv3_2 / conv4_2
+    // 310 / 582 / 566 -> 289 / 539 / 526 us; slower on AlexNet's 27- and
+    // 13-wide layers (4-pixel blocks, L2-resident operands: conv2 103 ->
+    // 125 us in the chain).  Profiling knob LCNN_CONV_TAPSN: 0 off, 1 forced
+    // wherever supported.
+    static const int tapsn_knob = [] {
+      const char* e = std::getenv("LCNN_CONV_TAPSN");
+      return e ? (e[0] == '1' ? 2 : 0) : 1;
+    }();
+    if (r.p.g.mode == kModeCI &&
+        (tapsn_knob == 2 || (tapsn_knob == 1 && a.wo >= 28 && !big_planes)) &&
+        tapsn_geom(a).ok) {
+      r.kind = kRouteTapsN;
       r.p.g.mode = kModeTAPS;
       r.apack = static_cast<uint64_t>(a.co) * r.p.K;
       return r;
@@ -1718,6 +2028,7 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
   if (r.kind == kRouteTaps) return launch_chwn_taps(t, s);
+  if (r.kind == kRouteTapsN) return launch_chwn_tapsn(t, s);
   if (r.kind == kRouteChwnPair) return launch_chwn_tc<true, true>(t, s);
   return r.kind == kRouteChwnOnN ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
 }

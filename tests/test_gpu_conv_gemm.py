@@ -90,6 +90,11 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     # channel planes >= 4 MB: TAPS mode (one box per filter row serves all its taps)
     (128, 32, 92, 92, 64, 3, 1, 1),    # C_o 64: half-empty 128-channel tile
     (64, 32, 130, 130, 160, 3, 2, 1),  # stride 2, two channel tiles, 32-image groups x 2
+    # CI, output rows >= 28, planes < 4 MB: TAPS-N (4-pixel x 32-image tiles on a CTA pair)
+    (64, 32, 30, 30, 96, 3, 1, 1),     # C_o 96: 48-row filter halves per CTA
+    (128, 64, 28, 28, 384, 3, 1, 1),   # two 192-channel tiles, two 64-image blocks
+    (64, 32, 57, 57, 64, 3, 2, 1),     # stride 2, Wo 29: ragged last pixel block
+    (64, 32, 32, 32, 128, 5, 1, 2),    # 5x5: one box serves 5 taps
 ]
 
 
@@ -97,6 +102,28 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
 @pytest.mark.parametrize("precision", [0, 1, 2])
 def test_conv_chwn(cuda, case, precision):
     _check_conv(cuda, *case, CHWN, precision)
+
+
+def test_conv_tapsn_forced_on_alexnet_shapes(cuda):
+    """TAPS-N forced (LCNN_CONV_TAPSN=1, read once per process: a subprocess)
+    on the AlexNet conv2-5 shapes the router keeps on the CI kernels."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, torch; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+        "import test_gpu_conv_gemm as t; from paper_1610_03618_b200 import lcnn;"
+        "d = torch.device('cuda:0');"
+        "[t._check_conv(d, *c, t.CHWN, lcnn.TF32) for c in ["
+        "(128, 96, 27, 27, 192, 5, 1, 2), (128, 192, 13, 13, 384, 3, 1, 1),"
+        "(128, 384, 13, 13, 256, 3, 1, 1), (64, 32, 13, 13, 96, 3, 1, 1)]];"
+        "print('ok')")
+    env = dict(os.environ, LCNN_CONV_TAPSN="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
 @pytest.mark.parametrize("case", [(5, 3, 9, 9, 7, 3, 1, 1), (3, 4, 11, 11, 6, 5, 2, 2),
