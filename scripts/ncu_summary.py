@@ -35,7 +35,12 @@ def launches(src, dst):
     text = open(src).read()
     start = text.index('"ID"')
     rows = list(csv.DictReader(io.StringIO(text[start:])))
-    mine = [r for r in rows if ours(r["Kernel Name"])]
+    mine = [r for r in rows if ours(r["Kernel Name"]) and
+            r.get("Metric Name", "gpu__time_duration.sum") == "gpu__time_duration.sum"]
+    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6}
+    for r in mine:  # normalise to ns
+        r["Metric Value"] = str(float(r["Metric Value"].replace(",", "")) *
+                                scale.get(r.get("Metric Unit", "nsecond"), 1.0))
     total = sum(float(r["Metric Value"]) for r in mine)
     out = ["| # | kernel | grid | block | time (us) | share of our launches |", "|---|---|---|---|---|---|"]
     for i, r in enumerate(mine):
