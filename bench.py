@@ -96,6 +96,8 @@ def l2_rotations(torch, device, footprint):
     """Input/output copies a single-op workload rotates over so that no
     buffer is re-read from L2: enough to stream > 4x L2 between reuses when
     one launch touches less than 2x L2 (SURVEY 8d timing method)."""
+    if not hasattr(torch, "cuda"):  # the reference arm's CPU-only stand-in: nothing to rotate
+        return 1
     l2 = torch.cuda.get_device_properties(device).L2_cache_size or (126 << 20)
     return max(1, min(16, -(-4 * l2 // footprint))) if footprint < 2 * l2 else 1
 
