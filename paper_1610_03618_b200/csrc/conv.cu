@@ -516,12 +516,15 @@ struct ShareOut {
   // TMA-store epilogue: view {32 n, N/32, Wo, Ho, Co} of the output, box
   // {32, 1, 1, 1, 32} = one 32-channel x 32-image chunk, SWIZZLE_128B
   CUtensorMap y;
-  static constexpr bool kTmaStore = true, kTmaTransposed = false;
+  FastDiv fd_groups, fd_owb;  // set by the launcher (TMA-store epilogue)
+  static constexpr bool kTmaStore = true, kTmaTransposed = false, kTmaPairs = true;
   __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
                                             bool add) const {
     const uint32_t t = n0 / (kSharePix * 32), p = n0 % (kSharePix * 32) / 32;
-    const uint32_t grp = t % groups, r = t / groups;
-    const uint32_t ob = r % owb, oh = r / owb, ow = ob * kSharePix + p;
+    uint32_t r, grp, oh, ob;
+    fd_groups.divmod(t, r, grp);
+    fd_owb.divmod(r, oh, ob);
+    const uint32_t ow = ob * kSharePix + p;
     if (ow >= wo || m0 >= co) return;  // (rows past C_o inside the box are clipped)
     if (add)
       tma_add_5d(&y, box, 0, static_cast<int32_t>(grp), static_cast<int32_t>(ow),
@@ -1564,6 +1567,8 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
   }
   ShareOut O{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, L.owb, L.groups};
   if (!make_share_out_map(&O.y, a)) return cudaErrorInvalidValue;
+  O.fd_groups = FastDiv(L.groups);
+  O.fd_owb = FastDiv(L.owb);
   return launch_persistent(L, O, sc, s);
 }
 

@@ -126,6 +126,18 @@ template <class O>
 struct OutTma<O, decltype(void(O::kTmaStore))> {
   static constexpr bool value = O::kTmaStore;
 };
+// Out types whose chunks are staged in pairs (one async-proxy fence per two
+// boxes): the short-K SHARE convolutions, where the epilogue sets the pace
+// (measured: VGG conv1_1 625 -> 504 us; neutral to slightly slower on the
+// long-K layers, whose stores then wait for both previous boxes)
+template <class O, class = void>
+struct OutTmaPairs {
+  static constexpr bool value = false;
+};
+template <class O>
+struct OutTmaPairs<O, decltype(void(O::kTmaPairs))> {
+  static constexpr bool value = O::kTmaPairs;
+};
 constexpr uint32_t kEpiStageBytes = 4 * 2 * 4096;  // 4 warps x 2 boxes
 
 // One tile's accumulator rows [q*32, q*32+32) (this warp's TMEM lane quarter)
@@ -139,6 +151,35 @@ template <class Out>
 __device__ __forceinline__ void epilogue_tile(const Out& out, const Sched& sc, uint8_t* stg,
                                               uint32_t taddr, uint32_t m, uint32_t ncol0,
                                               bool split, uint32_t& epi_buf, int lane) {
+  if constexpr (OutTmaPairs<Out>::value) {
+    if (sc.epi_bufs == 2 && sc.bn % 64 == 0) {
+      // pairs of chunks: both boxes written, ONE async-proxy fence, two stores
+#pragma unroll 1
+      for (uint32_t c = 0; c < sc.bn; c += 64) {
+        float v[64];
+        tmem_ld32(taddr + c, v);
+        tmem_ld32(taddr + c + 32, v + 32);
+        if (lane == 0) bulk_wait_read_n<0>();  // both boxes' previous stores have read them
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float4* row = reinterpret_cast<float4*>(stg + h * 4096 + lane * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            row[j ^ (lane & 7)] = make_float4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1],
+                                              v[32 * h + 4 * j + 2], v[32 * h + 4 * j + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !(sc.probe & 2)) {
+          out.tma_chunk(stg, m, ncol0 + c, split);
+          out.tma_chunk(stg + 4096, m, ncol0 + c + 32, split);
+          bulk_commit();
+        }
+      }
+      return;
+    }
+  }
   if constexpr (OutTma<Out>::value) {
 #pragma unroll 1
     for (uint32_t c = 0; c < sc.bn; c += 32) {
