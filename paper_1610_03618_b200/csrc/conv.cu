@@ -1508,6 +1508,16 @@ struct ShareGeom {
   bool ok;
 };
 
+// TMA-store staging boxes per epilogue warp in SHARE mode (profiling knob
+// LCNN_SHARE_EPI=1: one box, a deeper input ring)
+uint32_t share_epi_bufs() {
+  static const uint32_t b = [] {
+    const char* e = std::getenv("LCNN_SHARE_EPI");
+    return e && e[0] == '1' ? 1u : 2u;
+  }();
+  return b;
+}
+
 ShareGeom share_geom(const ConvArgs& a, bool resident) {
   ShareGeom q{};
   q.bn = (a.co + 7) / 8 * 8;
@@ -1519,7 +1529,8 @@ ShareGeom share_geom(const ConvArgs& a, bool resident) {
   q.img = resident ? a.fh * q.kr * q.bn * 4 + 16 * 128 : 0;  // + slack for the M = 128 reads
   q.slots = 0;
   for (uint32_t n = kPStagesMax; n >= 3 && !q.slots; --n)
-    if (1024ull + n * q.slot + q.img + 1024 + kEpiStageBytes + sizeof(PCtl) <= kMaxDynSmem)
+    if (1024ull + n * q.slot + q.img + 1024 + share_epi_bufs() * 4 * 4096 + sizeof(PCtl) <=
+        kMaxDynSmem)
       q.slots = n;
   q.ok = a.precision == LCNN_PREC_TF32 && a.co <= kTcBM && a.n % 32 == 0 && a.ci <= 256 &&
          q.bw <= 256 && q.kr <= 256 && a.stride * a.ci * 128 < (1u << 18) && q.slots >= 3;
@@ -1558,7 +1569,7 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
   sc.a_bytes = q.wbytes;
   sc.stage_bytes = q.wbytes + q.bw * a.ci * 128;
   sched_ring(sc, q.slots, q.slot, q.img);
-  sched_epi(sc, q.img);
+  sched_epi(sc, q.img, share_epi_bufs());
   if (sc.dp_tiles < tiles) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
     const uint64_t col0 = static_cast<uint64_t>(sc.dp_tiles / (L.owb * L.groups)) * a.wo * a.n;
