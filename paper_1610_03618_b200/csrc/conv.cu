@@ -1862,7 +1862,12 @@ ConvRoute route_conv(const ConvArgs& a) {
       const char* e = std::getenv("LCNN_CONV_ROW");
       return e ? (e[0] == 'n' ? 1 : (e[0] == 'm' ? 2 : (e[0] == 'r' ? 3 : 0))) : 0;
     }();
-    if (!force || force == 3) {
+    // SHARE pays off with wide filter rows (AlexNet conv1, F_w = 11: 120 ->
+    // 88 us against ROW); with F_w <= 3 a SHARE box saves little and ROW
+    // with channels on M is faster (VGG conv1_1: 504 -> 446 us), so those
+    // layers take ROW on M
+    const bool narrow = !force && a.fw <= 3;
+    if ((!force && !narrow) || force == 3) {
       const ShareGeom q = share_geom(a, force == 3);
       if (q.ok) {
         r.kind = force == 3 ? kRouteShareRes : kRouteShare;
@@ -1883,6 +1888,7 @@ ConvRoute route_conv(const ConvArgs& a) {
     const bool grouped = a.n % 128 == 0 && kr == a.ci * r.p.g.FP;
     bool on_n = choose_co_on_n(a.co, ncols, kr, grouped ? kr : a.ci * a.fw, kr * 4, grouped);
     if (force) on_n = force == 1;
+    if (narrow) on_n = false;
     r.kind = on_n ? kRouteRowOnN : kRouteRowOnM;
     r.apack = static_cast<uint64_t>(pack_rows(a.co, on_n)) * r.p.K;
   } else {
