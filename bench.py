@@ -490,7 +490,7 @@ def main():
     ap.add_argument("--plan", type=int, nargs=2, default=None,
                     help="coarsening fh fw (default: (1,1) for non-overlapping 2x2/s2 VGG pools, "
                          "(2,2) for overlapping 3x3/s2, measured best on B200)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-sample-gb", type=float, default=1.0,
                     help="algorithmic GB per reference sample step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
