@@ -1929,19 +1929,20 @@ ConvRoute route_conv(const ConvArgs& a) {
       r.apack = static_cast<uint64_t>(a.co) * r.p.K;
       return r;
     }
-    // TAPS-N (tap-sharing boxes, channels on N, CTA pair) for CI layers with
-    // output rows >= 28 wide whose planes are not TAPS-sized: measured on
-    // B200 (profiles/r01_conv_tapsn.txt), VGG-16 conv3_1 / conv3_2 / conv4_2
-    // 310 / 582 / 566 -> 289 / 539 / 526 us; slower on AlexNet's 27- and
-    // 13-wide layers (4-pixel blocks, L2-resident operands: conv2 103 ->
-    // 125 us in the chain).  Profiling knob LCNN_CONV_TAPSN: 0 off, 1 forced
+    // TAPS-N (tap-sharing boxes, channels on N, CTA pair) for 3x3 CI layers
+    // whose planes are not TAPS-sized and whose rows fill 4-pixel blocks to
+    // >= 87 %: measured on B200 (profiles/r01_conv_tapsn.txt), VGG-16 conv3_1
+    // / conv3_2 / conv4_2 / conv5_1 310 / 582 / 566 / 187 -> 289 / 539 / 526 /
+    // 179 us; slower on AlexNet's 5x5 conv2 (103 -> 125 us in the chain) and
+    // its 13-wide layers (13 of 16 columns used).  Profiling knob LCNN_CONV_TAPSN: 0 off, 1 forced
     // wherever supported.
     static const int tapsn_knob = [] {
       const char* e = std::getenv("LCNN_CONV_TAPSN");
       return e ? (e[0] == '1' ? 2 : 0) : 1;
     }();
-    if (r.p.g.mode == kModeCI &&
-        (tapsn_knob == 2 || (tapsn_knob == 1 && a.wo >= 28 && !big_planes)) &&
+    const uint32_t owb4 = (a.wo + kTapsNPix - 1) / kTapsNPix * kTapsNPix;  // padded row
+    const bool tapsn_fit = a.wo >= 14 && a.fw <= 3 && owb4 * 100 <= a.wo * 115 && !big_planes;
+    if (r.p.g.mode == kModeCI && (tapsn_knob == 2 || (tapsn_knob == 1 && tapsn_fit)) &&
         tapsn_geom(a).ok) {
       r.kind = kRouteTapsN;
       r.p.g.mode = kModeTAPS;

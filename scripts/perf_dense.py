@@ -50,7 +50,7 @@ convs = {"conv1": (3, 227, 96, 11, 4, 0), "conv2": (96, 27, 192, 5, 1, 2), "conv
          "vgg1_1": (3, 224, 64, 3, 1, 1), "vgg1_2": (64, 224, 64, 3, 1, 1),
          "vgg2_1": (64, 112, 128, 3, 1, 1), "vgg2_2": (128, 112, 128, 3, 1, 1),
          "vgg3_1": (128, 56, 256, 3, 1, 1), "vgg3_2": (256, 56, 256, 3, 1, 1),
-         "vgg4_2": (512, 28, 512, 3, 1, 1)}
+         "vgg4_2": (512, 28, 512, 3, 1, 1), "vgg5_1": (512, 14, 512, 3, 1, 1)}
 N = 128
 for layout, tag in ((lcnn.CHWN, "chwn"), (lcnn.NCHW, "nchw")):
     for name, (ci, hw, co, f, s, p) in convs.items():
