@@ -256,7 +256,8 @@ inline int tc_sm_count() {
 constexpr uint32_t kMinSkIters = 8;
 
 inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, uint32_t bn,
-                        bool a_mn, bool b_mn, uint32_t min_sk = kMinSkIters, uint32_t units = 0) {
+                        bool a_mn, bool b_mn, uint32_t min_sk = kMinSkIters, uint32_t units = 0,
+                        uint32_t dp_waves = 8) {
   Sched s{};
   s.mt = mt;
   s.nt = nt;
@@ -284,7 +285,7 @@ inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, u
   // ... and with >= 8 whole waves the ragged tail is <= 1/9 of the layer:
   // cheaper than zeroing the split tiles' output and reducing fragments
   // (measured on B200: AlexNet conv1, 10.4 waves, 74 -> 68 us)
-  if (rem == 0 || rem * 5 >= g * 3 || tiles >= 8 * g || sk_off) {
+  if (rem == 0 || rem * 5 >= g * 3 || (dp_waves && tiles >= dp_waves * g) || sk_off) {
     s.dp_tiles = tiles;
   } else {
     s.dp_tiles = tiles - rem;
