@@ -285,7 +285,11 @@ inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, u
   // ... and with >= 8 whole waves the ragged tail is <= 1/9 of the layer:
   // cheaper than zeroing the split tiles' output and reducing fragments
   // (measured on B200: AlexNet conv1, 10.4 waves, 74 -> 68 us)
-  if (rem == 0 || rem * 5 >= g * 3 || (dp_waves && tiles >= dp_waves * g) || sk_off) {
+  static const uint32_t full_pct = [] {  // profiling knob LCNN_SK_FULL_PCT (default 60)
+    const char* e = std::getenv("LCNN_SK_FULL_PCT");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 60u;
+  }();
+  if (rem == 0 || rem * 100 >= g * full_pct || (dp_waves && tiles >= dp_waves * g) || sk_off) {
     s.dp_tiles = tiles;
   } else {
     s.dp_tiles = tiles - rem;
