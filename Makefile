@@ -2,7 +2,7 @@
 # `make -j` here cross-compiles without a GPU; __graft_entry__.build() runs it.
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+NVFLAGS := $(ARCH) $(if $(filter 1,$(PROFILING)),-DLCNN_PROFILING_KNOBS) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            -Xptxas -warn-spills --expt-relaxed-constexpr $(EXTRA_NVFLAGS)
 PKG     := paper_1610_03618_b200
 SRC     := $(PKG)/csrc

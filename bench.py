@@ -66,6 +66,21 @@ def load_traffic(workload):
 
 
 # ------------------------------------------------------------------ ops ----
+# An Op is constructed from SHAPES ONLY (no torch, no CUDA library): the
+# reference arm describes and runs the same workload from these objects
+# without ever loading paper_1610_03618_b200.  alloc() binds device buffers
+# and the C ABI for our arm.
+L2_BYTES = 126 << 20  # B200 L2 (cudaDevAttrL2CacheSize 126.5 MiB), rounded down
+LAYOUT_NAMES = {0: "nchw", 1: "chwn", 2: "nhwc", 3: "hwcn"}
+
+
+def l2_rotations(footprint):
+    """Input/output copies a single-op workload rotates over so that no
+    buffer is re-read from L2: enough to stream > 4x L2 between reuses when
+    one launch touches less than 2x L2 (SURVEY 8d timing method)."""
+    return max(1, min(16, -(-4 * L2_BYTES // footprint))) if footprint < 2 * L2_BYTES else 1
+
+
 class Op:
     """One launch of a hot-path kernel on device-resident buffers."""
 
@@ -74,6 +89,16 @@ class Op:
     out_bytes = 0
     rot = 1  # rotated input/output copies (single-op workloads smaller than 2x L2)
     _i = 0   # launches so far (selects the copy)
+    _args = None
+
+    @property
+    def bytes(self):
+        return self.in_bytes + self.out_bytes
+
+    @property
+    def units(self):
+        """Images (rows for softmax) one launch processes."""
+        return getattr(self, "n", None) or getattr(self, "rows")
 
     def next_views(self):
         """The (input, output) slices the next launch() will use."""
@@ -81,51 +106,51 @@ class Op:
         nx, ny = self.in_bytes // 4, self.out_bytes // 4
         return self.x[r * nx:(r + 1) * nx], self.y[r * ny:(r + 1) * ny]
 
-    @property
-    def bytes(self):
-        return self.in_bytes + self.out_bytes
+    def alloc(self, torch, device):
+        from paper_1610_03618_b200 import capi
 
-    def launch(self, stream: int) -> None:
-        raise NotImplementedError
+        self.capi, self.lib = capi, capi.lib()
+        g = torch.Generator(device=device).manual_seed(self.seed)
+        lo, hi = self.data_range
+        self.x = torch.rand(self.rot * self.in_bytes // 4, device=device, generator=g) * (hi - lo) + lo
+        self.y = torch.empty(self.rot * self.out_bytes // 4, device=device)
+        self._extra_alloc(torch, device)
+        self._args = [self.bind(self.x.data_ptr() + r * self.in_bytes,
+                                self.y.data_ptr() + r * self.out_bytes) for r in range(self.rot)]
+        return self
+
+    data_range = (-1.0, 1.0)
+
+    def _extra_alloc(self, torch, device):
+        pass
+
+    def launch(self, stream):
+        fn, args = self._args[self._i % self.rot]
+        self._i += 1
+        st = fn(*args, stream)
+        if st:
+            self.capi.check(st, self.name)
 
     def ref_session(self, batch, threads):
         raise NotImplementedError
 
 
-def l2_rotations(torch, device, footprint):
-    """Input/output copies a single-op workload rotates over so that no
-    buffer is re-read from L2: enough to stream > 4x L2 between reuses when
-    one launch touches less than 2x L2 (SURVEY 8d timing method)."""
-    if not hasattr(torch, "cuda"):  # the reference arm's CPU-only stand-in: nothing to rotate
-        return 1
-    l2 = torch.cuda.get_device_properties(device).L2_cache_size or (126 << 20)
-    return max(1, min(16, -(-4 * l2 // footprint))) if footprint < 2 * l2 else 1
-
-
 class PoolOp(Op):
-    def __init__(self, torch, device, n, c, h, w, layout, win, stride, avg, plan, seed,
-                 rotate=False):
-        from paper_1610_03618_b200 import capi
-
-        self.capi = capi
-        self.lib = capi.lib()
+    def __init__(self, n, c, h, w, layout, win, stride, avg, plan, seed, rotate=False):
         self.n, self.c, self.h, self.w = n, c, h, w
         self.layout, self.win, self.stride, self.avg = layout, win, stride, avg
         self.plan = plan  # None = pool_layout (plain)
+        self.seed = seed
         self.ho = (h - win) // stride + 1
         self.wo = (w - win) // stride + 1
-        g = torch.Generator(device=device).manual_seed(seed)
         self.in_bytes = n * c * h * w * 4
         self.out_bytes = n * c * self.ho * self.wo * 4
-        self.rot = l2_rotations(torch, device, self.in_bytes + self.out_bytes) if rotate else 1
-        self.x = torch.rand(self.rot * n * c * h * w, device=device, generator=g) * 2 - 1
-        self.y = torch.empty(self.rot * n * c * self.ho * self.wo, device=device)
-        self._i = 0
+        self.rot = l2_rotations(self.in_bytes + self.out_bytes) if rotate else 1
         kind = "plain" if plan is None else f"coarsened({plan[0]},{plan[1]})"
-        lname = capi.LAYOUT_NAMES[layout]
-        self.name = f"pool_{lname}_{kind}_{n}x{c}x{h}x{w}_w{win}s{stride}"
-        self.rep = capi.AccessReport()
-        self._args = None
+        self.name = f"pool_{LAYOUT_NAMES[layout]}_{kind}_{n}x{c}x{h}x{w}_w{win}s{stride}"
+
+    def _extra_alloc(self, torch, device):
+        self.rep = self.capi.AccessReport()
 
     def bind(self, x_ptr, y_ptr):
         mode = 1 if self.avg else 0
@@ -143,18 +168,9 @@ class PoolOp(Op):
                     mode, self.plan[0], self.plan[1], ctypes.byref(self.rep))
         return fn, args
 
-    def launch(self, stream):
-        if self._args is None:
-            self._args = [self.bind(self.x.data_ptr() + r * self.in_bytes,
-                                    self.y.data_ptr() + r * self.out_bytes)
-                          for r in range(self.rot)]
-        fn, args = self._args[self._i % self.rot]
-        self._i += 1
-        st = fn(*args, stream)
-        if st:
-            self.capi.check(st, self.name)
-
     def ref_session(self, batch, threads):
+        """The reference call for this layer: pool_coarsened for a CHWN plan,
+        pool_layout otherwise (NCHW has no coarsened reference, pool.cpp:190)."""
         from oracle.oracle import OP_POOL_COARSENED, OP_POOL_LAYOUT, Ref
 
         op = OP_POOL_LAYOUT if self.plan is None or self.layout != 1 else OP_POOL_COARSENED
@@ -166,29 +182,22 @@ class PoolOp(Op):
 
 
 class SoftmaxOp(Op):
-    def __init__(self, torch, device, rows, cols, fused, seed):
-        from paper_1610_03618_b200 import capi
+    data_range = (-5.0, 5.0)
 
-        self.capi = capi
-        self.lib = capi.lib()
-        self.rows, self.cols, self.fused = rows, cols, fused
-        g = torch.Generator(device=device).manual_seed(seed)
+    def __init__(self, rows, cols, fused, seed):
+        self.rows, self.cols, self.fused, self.seed = rows, cols, fused, seed
+        # bench.cpp:151 -- both arms are charged 2*N*C*4 algorithmic bytes
+        self.in_bytes = self.out_bytes = rows * cols * 4
         # L2 policy: a matrix pair smaller than the 126 MB L2 would stay
         # resident between launches, so consecutive launches rotate over
-        # enough (input, output) pairs to stream > 2x L2 (>= 4
-        # rotated buffers larger than L2)
-        self.rot = l2_rotations(torch, device, 2 * rows * cols * 4)
-        self.x = torch.rand(self.rot * rows * cols, device=device, generator=g) * 10 - 5
-        self.y = torch.empty_like(self.x)
-        self._i = 0
-        nbytes = self.lib.lcnn_softmax_reference_scratch_bytes(rows, cols)
-        self.scratch = None if fused else torch.empty(nbytes // 4, device=device)
-        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
-        # bench.cpp:151 -- both arms are charged 2*N*C*4 algorithmic bytes
-        self.in_bytes = rows * cols * 4
-        self.out_bytes = rows * cols * 4
+        # enough (input, output) pairs to stream > 4x L2
+        self.rot = l2_rotations(self.bytes)
         self.name = f"softmax_{'fused' if fused else 'five_pass'}_{rows}x{cols}"
-        self._args = None
+
+    def _extra_alloc(self, torch, device):
+        nbytes = self.lib.lcnn_softmax_reference_scratch_bytes(self.rows, self.cols)
+        self.scratch = None if self.fused else torch.empty(nbytes // 4, device=device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
 
     def bind(self, x_ptr, y_ptr):
         if self.fused:
@@ -197,17 +206,6 @@ class SoftmaxOp(Op):
         return self.lib.lcnn_softmax_reference, (x_ptr, y_ptr, self.rows, self.cols,
                                                  self.scratch.data_ptr(), self.scratch.numel() * 4,
                                                  self.flag.data_ptr(), None)
-
-    def launch(self, stream):
-        if self._args is None:
-            step = self.rows * self.cols * 4
-            self._args = [self.bind(self.x.data_ptr() + r * step, self.y.data_ptr() + r * step)
-                          for r in range(self.rot)]
-        fn, args = self._args[self._i % self.rot]
-        self._i += 1
-        st = fn(*args, stream)
-        if st:
-            self.capi.check(st, self.name)
 
     def ref_session(self, batch, threads):
         from oracle.oracle import OP_SOFTMAX_FUSED, OP_SOFTMAX_REFERENCE, Ref
@@ -218,30 +216,18 @@ class SoftmaxOp(Op):
 
 
 class TransformOp(Op):
-    def __init__(self, torch, device, n, c, h, w, src, dst, seed):
-        from paper_1610_03618_b200 import capi
+    data_range = (0.0, 1.0)
 
-        self.capi = capi
-        self.lib = capi.lib()
+    def __init__(self, n, c, h, w, src, dst, seed, rotate=False):
         self.n, self.c, self.h, self.w, self.src, self.dst = n, c, h, w, src, dst
-        g = torch.Generator(device=device).manual_seed(seed)
-        self.x = torch.rand(n * c * h * w, device=device, generator=g)
-        self.y = torch.empty_like(self.x)
-        self.in_bytes = self.out_bytes = self.x.numel() * 4  # bench.cpp:202
-        self.name = f"transform_{capi.LAYOUT_NAMES[src]}_{capi.LAYOUT_NAMES[dst]}_{n}x{c}x{h}x{w}"
-        self._args = None
+        self.seed = seed
+        self.in_bytes = self.out_bytes = n * c * h * w * 4  # bench.cpp:202
+        self.rot = l2_rotations(self.bytes) if rotate else 1
+        self.name = (f"transform_{LAYOUT_NAMES[src]}_{LAYOUT_NAMES[dst]}_{n}x{c}x{h}x{w}")
 
     def bind(self, x_ptr, y_ptr):
         return self.lib.lcnn_transform, (x_ptr, y_ptr, self.n, self.c, self.h, self.w, self.src,
                                          self.dst)
-
-    def launch(self, stream):
-        if self._args is None:
-            self._args = self.bind(self.x.data_ptr(), self.y.data_ptr())
-        fn, args = self._args
-        st = fn(*args, stream)
-        if st:
-            self.capi.check(st, self.name)
 
     def ref_session(self, batch, threads):
         from oracle.oracle import OP_TRANSFORM, Ref
@@ -252,54 +238,104 @@ class TransformOp(Op):
 
 
 # ------------------------------------------------------------ workloads ----
-def build_workload(name, torch, device, rank, plan):
-    """Returns (ops, description dict, dominant op index, per-GPU batch)."""
+class Workload:
+    """What one rank runs (ops) plus the config dict both arms print.
+
+    ops        -- this rank's launches per step (its N-shard for strong scaling)
+    global_ops -- the whole job's ops on one device (what --impl reference runs)
+    """
+
+    def __init__(self, ops, global_ops, desc, dom, scaling, global_units, unit_name):
+        self.ops, self.global_ops, self.desc, self.dom = ops, global_ops, desc, dom
+        self.scaling, self.global_units, self.unit_name = scaling, global_units, unit_name
+
+    @property
+    def step_bytes_global(self):
+        return sum(op.bytes for op in self.global_ops)
+
+
+VGG_GLOBAL_BATCH = 256
+# measured best per layer (scripts/pool_plans.py [nchw vgg] on B200)
+VGG_PLANS = {1: [(1, 1)] * 5, 0: [(2, 2), (4, 1), (2, 1), (2, 1), (1, 2)]}
+
+
+def build_workload(name, world, rank, plan=None, tsweep_n=None):
+    """Shape-only description of a workload for `rank` of `world` GPUs.
+
+    vgg_pools* is BASELINE config 4 as stated there: a GLOBAL batch of 256
+    N-sharded over the GPUs (strong scaling, 256/G images per GPU).  The
+    single-op configs (1-3) keep their per-GPU batch (weak scaling)."""
+    from paper_1610_03618_b200.shard import shard_range  # pure python, no CUDA
+
     CHWN, NCHW = 1, 0
     seed = 1234 + 17 * rank
+    par = f"N-shard x{world} (no data-path collective)"
     if name in ("vgg_pools", "vgg_pools_nchw"):
-        b = 256
         layout = CHWN if name == "vgg_pools" else NCHW
-        # measured best per layer (scripts/pool_plans.py [nchw vgg] on B200)
-        plans = [plan] * len(VGG_POOLS) if plan else (
-            [(1, 1)] * len(VGG_POOLS) if layout == CHWN else [(2, 2), (4, 1), (2, 1), (2, 1), (1, 2)])
-        ops = [PoolOp(torch, device, b, c, hw, hw, layout, 2, 2, False, plans[i], seed + i)
-               for i, (c, hw) in enumerate(VGG_POOLS)]
+        plans = [tuple(plan)] * len(VGG_POOLS) if plan else VGG_PLANS[layout]
+        a, b = shard_range(VGG_GLOBAL_BATCH, world, rank)
+
+        def mk(nb, sd):
+            return [PoolOp(nb, c, hw, hw, layout, 2, 2, False, plans[i], sd + i)
+                    for i, (c, hw) in enumerate(VGG_POOLS)]
+
+        ops = mk(b - a, seed)
+        gops = mk(VGG_GLOBAL_BATCH, 1234)
         lname = "CHWN (selector's pooling layout)" if layout == CHWN else "NCHW"
+        gbytes = sum(op.bytes for op in gops)
         desc = {"workload": f"BASELINE config 4: VGG-16 pool1..pool5, max 2x2/s2, {lname}, "
-                            "256 images per GPU, N-sharded",
-                "batch_per_gpu": b, "layers": [f"{b}x{c}x{hw}x{hw}" for c, hw in VGG_POOLS],
-                "kernel": "coarsened fh,fw per layer " + ",".join(f"{p[0]}x{p[1]}" for p in plans)}
-        return ops, desc, 0, b
+                            f"global batch {VGG_GLOBAL_BATCH} N-sharded over {world} GPU(s)",
+                "global_batch": VGG_GLOBAL_BATCH,
+                "batch_per_gpu": [list(shard_range(VGG_GLOBAL_BATCH, world, r)) for r in range(world)]
+                if world > 1 else VGG_GLOBAL_BATCH,
+                "layers": [f"{VGG_GLOBAL_BATCH}x{c}x{hw}x{hw}" for c, hw in VGG_POOLS],
+                "parallelism": par,
+                "l2_policy": f"each step streams {gbytes / GB / world:.2f} GB per GPU "
+                             "(>> 126 MB L2) between reuses of any buffer; no explicit flush"}
+        return Workload(ops, gops, desc, 0, "strong", VGG_GLOBAL_BATCH, "images")
     if name in ("pl5", "pl5_nchw"):
         layout = CHWN if name == "pl5" else NCHW
-        p = plan or ((2, 2) if layout == CHWN else (3, 2))  # measured best (scripts/pool_plans.py)
-        ops = [PoolOp(torch, device, 128, 96, 55, 55, layout, 3, 2, False, p, seed, rotate=True)]
+        p = tuple(plan) if plan else ((2, 2) if layout == CHWN else (3, 2))  # scripts/pool_plans.py
+        ops = [PoolOp(128, 96, 55, 55, layout, 3, 2, False, p, seed, rotate=True)]
         desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) max 3x3/s2, "
                             f"128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",
-                "batch_per_gpu": 128, "kernel": f"coarsened fh,fw={p[0]},{p[1]}",
+                "batch_per_gpu": 128, "global_batch": 128 * world, "parallelism": par,
                 "l2_policy": f"{ops[0].rot} rotated input/output pairs "
                              f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB) between launches"}
-        return ops, desc, 0, 128
-    if name in ("softmax", "softmax5", "softmax_64k"):
-        fused = name != "softmax5"
-        rows = 65536 if name == "softmax_64k" else 4096
-        ops = [SoftmaxOp(torch, device, rows, 1000, fused, seed)]
+        return Workload(ops, ops, desc, 0, "weak", 128 * world, "images")
+    if name.startswith("softmax"):
+        fused = name != "softmax5" and not name.startswith("softmax5_")
+        rows = 4096
+        if name == "softmax_64k":
+            rows = 65536
+        elif "_" in name and name.split("_")[-1].isdigit():
+            rows = int(name.split("_")[-1])
+        ops = [SoftmaxOp(rows, 1000, fused, seed)]
         desc = {"workload": f"BASELINE config 2: softmax classifier {rows}x1000, "
                             f"{'fused single kernel' if fused else 'five-kernel baseline'}"
                             + (" (HBM asymptote beyond the 4096-row config)" if rows > 4096 else ""),
-                "batch_per_gpu": rows,
+                "batch_per_gpu": rows, "global_batch": rows * world, "parallelism": par,
                 "l2_policy": (f"{ops[0].rot} rotated input/output pairs "
-                              f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB > 2x L2) between launches"
+                              f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB > 4x L2) between launches"
                               if ops[0].rot > 1 else "matrix pair > 2x L2")}
-        return ops, desc, 0, rows
-    if name == "transform":
-        b = 128
-        ops = [TransformOp(torch, device, b, c, h, w, CHWN, NCHW, seed + i)
+        return Workload(ops, ops, desc, 0, "weak", rows * world, "rows")
+    if name.startswith("transform"):
+        # transform[_nchw][_N]: CHWN->NCHW (default) or NCHW->CHWN at batch N
+        src, dst = (NCHW, CHWN) if "_nchw" in name else (CHWN, NCHW)
+        b = tsweep_n or 128
+        if name.split("_")[-1].isdigit():
+            b = int(name.split("_")[-1])
+        ops = [TransformOp(b, c, h, w, src, dst, seed + i, rotate=True)
                for i, (c, h, w) in enumerate(TRANSFORM_SHAPES)]
         dom = max(range(len(ops)), key=lambda i: ops[i].bytes)
-        desc = {"workload": "BASELINE config 3: CHWN->NCHW transform over the AlexNet + VGG-16 "
-                            "activation shapes, batch 128 per GPU", "batch_per_gpu": b}
-        return ops, desc, dom, b
+        desc = {"workload": f"BASELINE config 3: {LAYOUT_NAMES[src].upper()}->"
+                            f"{LAYOUT_NAMES[dst].upper()} transform over the AlexNet + VGG-16 "
+                            f"activation shapes, batch {b} per GPU",
+                "batch_per_gpu": b, "global_batch": b * world, "parallelism": par,
+                "shapes": [f"{b}x{c}x{h}x{w}" for c, h, w in TRANSFORM_SHAPES],
+                "l2_policy": "each step streams every shape once; shapes smaller than 2x L2 "
+                             "rotate over enough copies to stream > 4x L2 between reuses"}
+        return Workload(ops, ops, desc, dom, "weak", b * world, "images")
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -358,22 +394,22 @@ class ClockSampler:
 
 # ------------------------------------------------------------ reference ----
 def ref_sample_batch(ops, threads, budget_bytes):
-    """Images per op for a bounded CPU sample: a multiple of the thread count,
-    capped so the sample's algorithmic bytes stay near `budget_bytes`."""
-    per_image = sum(op.bytes / max(1, op_batch(op)) for op in ops)
+    """Images per op for the reference timing: the full per-op batch (the
+    same workload as our arm) unless `budget_bytes` > 0 bounds the sample's
+    algorithmic bytes (CPU unit tests)."""
+    full = min(op.units for op in ops)
+    if not budget_bytes:
+        return full
+    per_image = sum(op.bytes / max(1, op.units) for op in ops)
     b = max(threads, int(budget_bytes // max(1.0, per_image)))
     b = max(threads, (b // threads) * threads)
-    return min(b, min(op_batch(op) for op in ops))
-
-
-def op_batch(op):
-    return getattr(op, "n", None) or getattr(op, "rows")
+    return min(b, full)
 
 
 def time_reference(ops, threads, batch, steps, warmup):
     """Run every op's reference call on a `batch`-image sample per step;
     returns (GB/s over the timed steps, seconds per step, sample bytes)."""
-    sessions = [op.ref_session(batch, threads) for op in ops]
+    sessions = [op.ref_session(min(batch, op.units), threads) for op in ops]
     sample_bytes = sum(b for _, b in sessions)
     for _ in range(warmup):
         for s, _ in sessions:
@@ -398,86 +434,72 @@ def cpu_desc():
     return "unknown"
 
 
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def sample_text(batch, full, threads, sample_bytes):
+    what = "the full workload" if batch >= full else f"{batch} of {full} images per layer"
+    return (f"{what}, N-sharded over {threads} std::threads calling the unmodified reference "
+            f"function on their shard ({sample_bytes / GB:.3f} GB algorithmic per step)")
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the unmodified reference CPU path (oracle/_ref) on this
-    host's cores; rank 0 only under torchrun."""
+    host's cores, on the WHOLE job of our arm's config (the global batch for
+    strong scaling); rank 0 only under torchrun.  Never loads
+    paper_1610_03618_b200's CUDA library (the ops are shape-only)."""
     if rank != 0:
         return
-    import torch
-
     from oracle.oracle import Ref
 
     if not Ref.available():
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/liblcnn_ref.so not built (needs /root/reference at build)"}))
         return
-    threads = os.cpu_count() or 1
-    # describe the same workload as our arm (shapes only; no GPU needed)
-    ops, desc, _, _ = build_workload(args.workload, _FakeTorch(), "cpu", 0,
-                                     tuple(args.plan) if args.plan else None)
+    threads = host_threads()
+    wl = build_workload(args.workload, world, 0, args.plan)
+    ops = wl.global_ops
     batch = ref_sample_batch(ops, threads, args.ref_sample_gb * GB)
     gbs, sec, sample_bytes = time_reference(ops, threads, batch, args.steps, args.warmup)
     line = {"metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (mt19937 uniform[-1,1), per-thread shard)", "config": desc,
+            "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (mt19937 uniform[-1,1), per-thread shard)", "config": wl.desc,
             "impl": "reference",
             "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads,
-                             "kind": "reference", "cpu": cpu_desc(),
-                             "sample": f"{batch} images per layer (N-sharded over {threads} "
-                                       f"std::threads), {sample_bytes / GB:.3f} GB algorithmic "
-                                       f"per step"},
+                             "kind": "reference", "cpu": cpu_desc(), "build": Ref.variant(),
+                             "sample": sample_text(batch, min(op.units for op in ops), threads,
+                                                   sample_bytes)},
             "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    del torch
     print(json.dumps(line))
 
 
-class _FakeTorch:
-    """Shape-only stand-in so the reference arm can describe the workload
-    without touching a GPU."""
-
-    class _T:
-        def __init__(self, n):
-            self.n = n
-
-        def numel(self):
-            return self.n
-
-        def __mul__(self, o):
-            return self
-
-        __rmul__ = __mul__
-
-        def __sub__(self, o):
-            return self
-
-        def data_ptr(self):
-            return 0
-
-    class Generator:
-        def __init__(self, device=None):
-            pass
-
-        def manual_seed(self, s):
-            return self
-
-    int32 = "int32"
-
-    def rand(self, n, device=None, generator=None):
-        return self._T(n)
-
-    def empty(self, n, device=None, dtype=None):
-        return self._T(n)
-
-    def empty_like(self, t):
-        return self._T(t.n)
-
-    def zeros(self, n, dtype=None, device=None):
-        return self._T(n)
-
-
 # ---------------------------------------------------------------- main -----
+def free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_distributed(gpus):
+    """`bench.py --gpus N` without a torchrun environment: re-exec through
+    torch.distributed.run with N local ranks (one process per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: launching {gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -485,14 +507,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg_pools",
-                    choices=["vgg_pools", "vgg_pools_nchw", "pl5", "pl5_nchw", "softmax", "softmax5",
-                             "softmax_64k", "transform", "alexnet", "vgg16"])
+                    help="vgg_pools (default, config 4) | vgg_pools_nchw | pl5 | pl5_nchw | "
+                         "softmax[_ROWS] | softmax5[_ROWS] | softmax_64k | transform[_nchw][_N] | "
+                         "alexnet | alexnet_mixed | vgg16")
     ap.add_argument("--plan", type=int, nargs=2, default=None,
-                    help="coarsening fh fw (default: (1,1) for non-overlapping 2x2/s2 VGG pools, "
-                         "(2,2) for overlapping 3x3/s2, measured best on B200)")
+                    help="coarsening fh fw for every pool layer (default: the per-layer plans "
+                         "measured on B200)")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--ref-sample-gb", type=float, default=1.0,
-                    help="algorithmic GB per reference sample step")
+    ap.add_argument("--ref-sample-gb", type=float, default=0.0,
+                    help="bound the reference timing's algorithmic GB per step (0 = the full "
+                         "workload, the default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
@@ -500,9 +524,13 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        relaunch_distributed(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
 
     if args.impl == "reference":
         if args.workload in NETWORKS:
@@ -514,10 +542,16 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, "
+                         f"{torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+        dist.barrier()  # creates the communicator
+        print(f"bench.py: rank {rank}/{world} NCCL communicator up on cuda:{local} "
+              f"(nranks={dist.get_world_size()})", file=sys.stderr, flush=True)
 
     def barrier():
         if world > 1:
@@ -529,8 +563,9 @@ def main():
             dist.destroy_process_group()
         return
 
-    ops, desc, dom, batch = build_workload(args.workload, torch, device, rank,
-                                           tuple(args.plan) if args.plan else None)
+    wl = build_workload(args.workload, world, rank, args.plan)
+    ops = [op.alloc(torch, device) for op in wl.ops]
+    dom = wl.dom
     stream = torch.cuda.current_stream(device)
     sh = stream.cuda_stream
     step_bytes = sum(op.bytes for op in ops)
@@ -588,21 +623,27 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, dom_ms = float(t[0]), float(t[1])
-    value = step_bytes * world * K / (ms / 1e3) / GB
+    # whole-job bytes: the global batch for strong scaling, world x per-GPU for weak
+    job_bytes = wl.step_bytes_global if wl.scaling == "strong" else step_bytes * world
+    value = job_bytes * K / (ms / 1e3) / GB
 
     peak, peak_src = load_peaks()
     dom_op = ops[dom]
     achieved = dom_op.bytes / (dom_ms / 1e3) / GB
+    traffic = load_traffic(args.workload)
     roofline = {"bound": "hbm", "kernel": dom_op.name, "achieved": round(achieved, 1),
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "algorithmic_bytes_per_launch": dom_op.bytes,
-                "avg_launch_ms": round(dom_ms, 5), "traffic": load_traffic(args.workload),
-                "step_frac": round(value / world / peak, 4)}
+                "avg_launch_ms": round(dom_ms, 5),
+                "traffic": traffic if world == 1 else None,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, N=1 shapes)",
+                "step_frac": round(step_bytes / (ms / K / 1e3) / GB / peak, 4)}
 
     # ---- e2e: host buffers through the C ABI (pinned H2D, kernel, D2H) ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(torch, device, ops, world, args.e2e_steps, barrier, dist)
+        e2e = run_e2e(torch, device, ops, world, args.e2e_steps, barrier, dist,
+                      wl.step_bytes_global if wl.scaling == "strong" else None)
 
     # ---- cpu baseline: reference CPU path, rank 0 at N=1 only ----
     cpu = None
@@ -611,14 +652,13 @@ def main():
             from oracle.oracle import Ref
 
             if Ref.available():
-                threads = os.cpu_count() or 1
-                b = ref_sample_batch(ops, threads, args.ref_sample_gb * GB)
-                gbs, sec, sb = time_reference(ops, threads, b, 3, 1)
+                threads = host_threads()
+                b = ref_sample_batch(wl.global_ops, threads, args.ref_sample_gb * GB)
+                gbs, sec, sb = time_reference(wl.global_ops, threads, b, 3, 1)
                 cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads,
-                       "kind": "reference", "cpu": cpu_desc(),
-                       "sample": f"{b} images per layer of the same workload, N-sharded over "
-                                 f"{threads} std::threads, median-free mean of 3 steps "
-                                 f"({sb / GB:.3f} GB algorithmic per step)"}
+                       "kind": "reference", "cpu": cpu_desc(), "build": Ref.variant(),
+                       "sample": sample_text(b, min(op.units for op in wl.global_ops), threads,
+                                             sb) + "; mean of 3 steps after 1 warm-up"}
         except Exception as e:  # the baseline must never hide the GPU number
             cpu = {"value": None, "error": str(e)}
 
@@ -626,12 +666,10 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
                 "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic (uniform[-1,1) from torch's on-device RNG)",
-                "config": {"l2_policy": f"each step streams {step_bytes / GB:.2f} GB per GPU "
-                                        "(>> 126 MB L2) between reuses of any buffer; no "
-                                        "explicit flush",
-                           **desc, "parallelism": f"N-shard x{world} (no data-path collective)"},
+                "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic (uniform[-1,1) from torch's on-device RNG)",
+                "config": wl.desc,
+                "kernels": [op.name for op in ops],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": K * len(ops), "clocks": clk, "impl": "ours",
                 "timing": "one CUDA graph of K launches" if use_graph else "stream launches"}
@@ -640,12 +678,14 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(torch, device, ops, world, steps, barrier, dist):
+def run_e2e(torch, device, ops, world, steps, barrier, dist, job_bytes=None):
     """Same metric through the C ABI with HOST buffers: every step copies each
     layer's input from pinned host memory (H2D stream), runs the kernel
     (compute stream) and copies the result back (D2H stream); the two copy
     engines overlap across layers.  Timed with events on the issuing streams,
-    max over ranks."""
+    max over ranks.  This is the best case for host buffers (pinned memory,
+    copies overlapped with kernels); the lcnn:: value-semantics API
+    (host/src/ops.cpp: pageable upload, kernel, download per call) is slower."""
     comp = torch.cuda.current_stream(device)
     h2d = torch.cuda.Stream(device)
     d2h = torch.cuda.Stream(device)
@@ -693,12 +733,13 @@ def run_e2e(torch, device, ops, world, steps, barrier, dist):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
-    step_bytes = sum(op.bytes for op in ops)
-    value = step_bytes * world * steps / (ms / 1e3) / GB
+    step_bytes = job_bytes or sum(op.bytes for op in ops) * world
+    value = step_bytes * steps / (ms / 1e3) / GB
     return {"value": round(value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d_bytes,
             "d2h_bytes_per_step": d2h_bytes, "steps": steps, "ms_per_step": round(ms / steps, 3),
             "path": "pinned host -> cudaMemcpyAsync H2D -> lcnn_* C ABI kernel -> D2H, "
-                    "copy engines overlapped across layers"}
+                    "copy engines overlapped across layers (best-case pinned pipeline; "
+                    "h2d/d2h bytes are per GPU)"}
 
 
 # ------------------------------------------------------ whole networks ---
@@ -752,6 +793,19 @@ def thresholds():
         return 32, 128, "titan-black preset"
 
 
+def network_desc(workload, world):
+    """The config dict both arms print for a whole-network workload."""
+    cfg_path, workload_desc = NETWORKS[workload]
+    cfg = json.loads(open(cfg_path).read())
+    batch = cfg["input"]["n"]
+    c_t, n_t, th_src = thresholds()
+    weight_mb = layer_flops(cfg, weights=True) * 4 / 1e6
+    return {"workload": workload_desc, "batch_per_gpu": batch, "global_batch": batch * world,
+            "parallelism": f"N-shard x{world}, NCCL all_gather of logits only",
+            "thresholds": [c_t, n_t], "thresholds_source": th_src,
+            "l2_policy": f"activations + {weight_mb:.0f} MB of weights per step (> L2)"}
+
+
 def run_network_workload(args, torch, dist, rank, world, local, device, barrier):
     """Whole-network forward (BASELINE config 5 AlexNet, 128 images per GPU =
     batch 1024 at 8 GPUs; or VGG-16), per-layer layout selection, conv/fc on
@@ -764,8 +818,7 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
     weight_mb = layer_flops(json.loads(text), weights=True) * 4 / 1e6
     batch = json.loads(text)["input"]["n"]
     c_t, n_t, th_src = thresholds()
-    netapi.set_dense_precision(capi.PREC_TF32)
-    net = netapi.Network(text, c_t, n_t, seed=42)
+    net = netapi.Network(text, c_t, n_t, seed=42, precision=capi.PREC_TF32)
     info = net.info(1)
     in_layout = info["first_layout"]
     rows, cols = info["out"]
@@ -886,14 +939,9 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
                 "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "tf32",
                 "data": "synthetic (uniform[-1,1) input, reference-seeded weights)",
-                "config": {"workload": workload_desc,
-                           "batch_per_gpu": batch, "global_batch": batch * world,
-                           "parallelism": f"N-shard x{world}, NCCL all_gather of logits only",
-                           "layouts": layouts, "thresholds": [c_t, n_t],
-                           "thresholds_source": th_src, "transforms": info["transforms"],
-                           "logits_verified": ok_rows,
-                           "l2_policy": f"activations + {weight_mb:.0f} MB of weights per step "
-                                        "(> L2)"},
+                "config": network_desc(args.workload, world),
+                "network": {"layouts": layouts, "transforms": info["transforms"],
+                            "logits_rows_sum_to_1": ok_rows},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": per_fwd * K if per_fwd is not None else None,
                 "gpu_launches_per_step": per_fwd, "clocks": clocks.summary(), "impl": "ours"}
@@ -921,7 +969,7 @@ def reference_network_sample(cfg_path, c_t, n_t, batch_per_thread=1):
 
     if not Ref.available():
         return None
-    threads = os.cpu_count() or 1
+    threads = host_threads()
     cfg = json.loads(open(cfg_path).read())
     cfg["input"]["n"] = batch_per_thread
     sec = ref_time_network(json.dumps(cfg), c_t, n_t, threads)
@@ -940,24 +988,33 @@ def run_reference_network(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     c_t, n_t, _ = thresholds()
-    total_img, total_s = 0, 0.0
+    total_img, total_s, timed = 0, 0.0, 0
     cfg_path, workload_desc = NETWORKS[args.workload]
-    for i in range(args.warmup + args.steps):
+    t_start = time.perf_counter()
+    # a step is one image per host thread through the unmodified run_network;
+    # at most 2 warm-up steps, and the timed steps stop after ~150 s of CPU
+    # work (a VGG-16 step takes ~25 s on 16 threads)
+    for i in range(min(args.warmup, 2) + args.steps):
         r = reference_network_sample(cfg_path, c_t, n_t)
-        if i >= args.warmup:
+        if i >= min(args.warmup, 2):
             total_img += r["cores"]
             total_s += r["cores"] / r["value"]
+            timed += 1
+            if time.perf_counter() - t_start > 150:
+                break
     v = total_img / total_s
-    threads = os.cpu_count() or 1
+    threads = host_threads()
     print(json.dumps({"metric": METRIC, "value": round(v, 3), "unit": "images/s",
                       "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                       "ms_per_step": round(1e3 * total_s / args.steps, 1),
                       "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                       "dtype": "f32", "data": "synthetic", "impl": "reference",
-                      "config": {"workload": workload_desc},
+                      "config": network_desc(args.workload, world),
                       "cpu_baseline": {"value": round(v, 3), "unit": "images/s", "cores": threads,
                                        "kind": "reference", "cpu": cpu_desc(),
-                                       "sample": f"1 image per thread x {threads} threads"},
+                                       "build": Ref.variant(),
+                                       "sample": f"1 image per thread x {threads} threads, "
+                                                 f"{timed} timed step(s)"},
                       "e2e": {"value": round(v, 3), "unit": "images/s", "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0}}))
 

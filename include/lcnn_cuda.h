@@ -164,6 +164,13 @@ lcnn_status lcnn_softmax_fused(const float* src, float* dst, uint32_t rows,
                                uint32_t cols, uint32_t local_buffer_limit,
                                int* d_nonfinite, lcnn_pass_report* report,
                                void* stream);
+/* softmax_fused for a device-resident pipeline (the network executor's
+ * classifier): the same kernel, but d_sticky (device int, may be NULL) is
+ * never cleared -- it is set to 1 on a non-finite input and keeps that value
+ * until the owner clears it, so an asynchronous forward needs no extra
+ * zeroing launch and no host read (lcnn_net_status reads it). */
+lcnn_status lcnn_softmax_fused_sticky(const float* src, float* dst, uint32_t rows,
+                                      uint32_t cols, int* d_sticky, void* stream);
 
 /* Device scratch (bytes) the five-pass path needs for (rows, cols). */
 size_t lcnn_softmax_reference_scratch_bytes(uint32_t rows, uint32_t cols);
@@ -196,6 +203,12 @@ typedef enum lcnn_precision {
 size_t lcnn_conv_workspace_bytes(uint32_t n, uint32_t c_i, uint32_t h,
                                  uint32_t w, uint32_t c_o, uint32_t f_h,
                                  uint32_t f_w, int precision);
+/* Workspace of lcnn_conv_forward for this exact geometry (stride, padding,
+ * layout): what the routed kernel needs.  The stride-free query above returns
+ * a bound over every stride / padding. */
+size_t lcnn_conv_workspace_bytes_ex(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                                    int layout, uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                    uint32_t stride, uint32_t pad, int precision);
 
 /* == conv_direct (conv.cpp:200-213) and conv_gemm (conv.cpp:306-332): the
  * convolution of an (n, c_i, h, w) input in CHWN or NCHW (LayoutError

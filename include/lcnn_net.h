@@ -23,6 +23,15 @@ typedef struct lcnn_net lcnn_net;
  * (net.cpp:217-243) uploaded once.  Returns an lcnn_status. */
 int lcnn_net_create(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
                     lcnn_net** out);
+/* lcnn_net_create with the conv / fc precision (lcnn_precision; -1 = the
+ * process default of lcnn_set_dense_precision at this call).  The precision
+ * is fixed per network: networks at different precisions may run
+ * concurrently on different threads.  Filters and fc weights are packed for
+ * their layer's kernel here, once. */
+int lcnn_net_create_ex(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
+                       int precision, lcnn_net** out);
+/* The network's lcnn_precision. */
+int lcnn_net_precision(const lcnn_net* net);
 void lcnn_net_destroy(lcnn_net* net);
 const char* lcnn_net_last_error(void);
 
@@ -34,10 +43,21 @@ int lcnn_net_info(const lcnn_net* net, int in_layout, uint32_t dims[4],
 /* Per-layer layout codes after annotation (-1 for fc/softmax). */
 int lcnn_net_layouts(const lcnn_net* net, int* layouts, uint32_t max_layers);
 
-/* Forward with device buffers on `stream` (a cudaStream_t). */
+/* Forward with device buffers on `stream` (a cudaStream_t).  Asynchronous:
+ * a non-finite classifier input (the reference's DomainError,
+ * softmax.cpp:15-19) sets the network's sticky device flag instead of
+ * blocking; lcnn_net_status reports it. */
 int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout,
                      float* d_output, void* stream);
-/* Forward with host buffers: H2D, forward, D2H (synchronous). */
+/* Wait for `stream`, read and clear the non-finite flag: LCNN_EDOMAIN
+ * ("layer '<softmax>': softmax: non-finite input") if any forward since the
+ * last call met a non-finite input, else LCNN_OK. */
+int lcnn_net_status(const lcnn_net* net, void* stream);
+/* The sticky flag itself (device int, 0 or 1) for callers that poll it on
+ * the device or copy it back themselves; clear it with cudaMemsetAsync. */
+const int* lcnn_net_nonfinite_flag(const lcnn_net* net);
+/* Forward with host buffers: H2D, forward, D2H (synchronous); returns
+ * LCNN_EDOMAIN for a non-finite classifier input. */
 int lcnn_net_forward_host(const lcnn_net* net, const float* h_input,
                           int in_layout, float* h_output);
 /* `count` forwards over host buffers h_inputs[i] -> h_outputs[i] (pinned
@@ -55,7 +75,9 @@ int lcnn_net_profile(const lcnn_net* net, const float* d_input, int in_layout,
                      void* stream, uint64_t* nanos, uint32_t max_entries,
                      char* names, size_t names_len, uint32_t* count);
 
-/* lcnn_precision of the conv / fc layers (default FP32). */
+/* Process default lcnn_precision for networks created afterwards with
+ * lcnn_net_create (FP32 unless LCNN_DENSE_PRECISION says otherwise) and for
+ * the host-tensor conv / fc calls. */
 void lcnn_set_dense_precision(int precision);
 
 #ifdef __cplusplus

@@ -23,7 +23,32 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 C_LIB = os.path.join(HERE, "build", "liblcnn_oracle.so")
-REF_LIB = os.path.join(HERE, "_ref", "liblcnn_ref.so")
+REF_LIB = os.path.join(HERE, "_ref", "liblcnn_ref.so")  # x86-64-v2 build (always present)
+
+
+def _cpu_flags() -> set:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def ref_lib_path() -> tuple[str, str]:
+    """(path, ISA level) of the highest reference build this CPU runs: the
+    reference's own build is -march=native, so the CPU baseline
+    is not handicapped by the generic build (oracle/Makefile)."""
+    flags = _cpu_flags()
+    v3 = {"avx2", "fma", "bmi1", "bmi2", "f16c", "movbe"}
+    v4 = {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"}
+    for level, need in (("x86-64-v4", v3 | v4), ("x86-64-v3", v3)):
+        path = os.path.join(HERE, "_ref", f"liblcnn_ref_{level[-2:]}.so")
+        if need <= flags and os.path.exists(path):
+            return path, level
+    return REF_LIB, "x86-64-v2"
 
 NCHW, CHWN, NHWC, HWCN = 0, 1, 2, 3
 
@@ -187,11 +212,16 @@ class Ref:
         return os.path.exists(REF_LIB)
 
     @classmethod
+    def variant(cls) -> str:
+        """'-O2 -march=<level>' of the build Ref.lib() loads."""
+        return f"g++ -O2 -march={ref_lib_path()[1]} ({os.path.basename(ref_lib_path()[0])})"
+
+    @classmethod
     def lib(cls):
         if cls._lib is None:
             if not cls.available():
                 raise FileNotFoundError(REF_LIB)
-            dll = ctypes.CDLL(REF_LIB)
+            dll = ctypes.CDLL(ref_lib_path()[0])
             dll.ref_last_error.restype = c_char_p
             dll.ref_session_create.restype = c_void_p
             dll.ref_session_create.argtypes = [c_int] + [c_uint32] * 4 + [c_int, c_int] + \
@@ -335,6 +365,22 @@ class Ref:
         cls._rc(cls.lib().ref_run_network(json_text.encode(), c_t, n_t, c_uint64(seed), _p(x),
                                           in_layout, _p(out), c_uint64(out_cap),
                                           ctypes.byref(rows), ctypes.byref(cols)))
+        return out[:rows.value * cols.value].reshape(rows.value, cols.value).copy()
+
+    @classmethod
+    def run_network_sharded(cls, json_text, x, n, c_t=0, n_t=0, seed=42, threads=None,
+                            out_cap=1 << 26):
+        """ref_run_network_sharded: the unmodified run_network on NCHW input x
+        (n images), N-sharded over host threads (each shard annotated with its
+        own per-shard n) -> (n, cols) float32."""
+        x = _f32(x)
+        threads = threads or len(os.sched_getaffinity(0))
+        out = np.empty(out_cap, np.float32)
+        rows, cols = c_uint32(), c_uint32()
+        cls._rc(cls.lib().ref_run_network_sharded(json_text.encode(), c_t, n_t, c_uint64(seed),
+                                                  _p(x), n, _p(out), c_uint64(out_cap),
+                                                  ctypes.byref(rows), ctypes.byref(cols),
+                                                  threads))
         return out[:rows.value * cols.value].reshape(rows.value, cols.value).copy()
 
     @classmethod

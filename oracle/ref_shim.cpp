@@ -317,21 +317,31 @@ void* ref_session_create(int op, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
     auto* S = new RefSession{op, dst_layout,
                              R::PoolParams{wh, ww, s, avg ? R::PoolMode::Average : R::PoolMode::Max},
                              R::CoarseningPlan{fh, fw}, {}, {}, threads};
+    // shard inputs are allocated here and filled in parallel (one thread per
+    // shard, seed 42 + t) so a multi-GB session (VGG pool1 at N=256) is ready
+    // in about a second
+    const uint32_t base = n / threads;
     for (int t = 0; t < threads; ++t) {
-      const uint32_t base = n / threads;
       const uint32_t nn = t == threads - 1 ? n - base * (threads - 1) : base;
+      if (op == 2 || op == 3)
+        S->mins.emplace_back(nn, c);
+      else
+        S->tins.emplace_back(nn, c, h, w, static_cast<R::Layout>(layout));
+    }
+    auto fill = [&](int t) {
       std::mt19937 rng(42 + t);
       std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
       if (op == 2 || op == 3) {
-        R::Matrix m(nn, c);
-        for (auto& v : m.data) v = dist(rng);
-        S->mins.push_back(std::move(m));
+        for (auto& v : S->mins[t].data) v = dist(rng);
       } else {
-        R::Tensor4D in(nn, c, h, w, static_cast<R::Layout>(layout));
+        R::Tensor4D& in = S->tins[t];
         for (uint64_t i = 0; i < in.size(); ++i) in.data()[i] = dist(rng);
-        S->tins.push_back(std::move(in));
       }
-    }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(fill, t);
+    fill(0);
+    for (auto& th : pool) th.join();
     return S;
   } catch (...) {
     map_current_exception();
@@ -432,6 +442,55 @@ int ref_run_network(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
     *rows = m->rows;
     *cols = m->cols;
     std::copy(m->data.begin(), m->data.end(), out);
+  })
+}
+
+// ref_run_network over `threads` std::threads, each running the unmodified
+// run_network on its own N-shard of the input (NCHW input only: shards are
+// contiguous image blocks) and writing its logits rows in image order.  Used
+// to pin the full-size GPU forwards on a multi-image slice in seconds
+// (batch independence, test_conv.cpp:117-141).
+int ref_run_network_sharded(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
+                            const float* input, uint32_t n, float* out, uint64_t out_cap,
+                            uint32_t* rows, uint32_t* cols, int threads) {
+  GUARD({
+    if (threads < 1) threads = 1;
+    if (static_cast<uint32_t>(threads) > n) threads = static_cast<int>(n);
+    const R::NetworkSpec base_spec = R::parse_network(json);
+    const uint64_t img = static_cast<uint64_t>(base_spec.c) * base_spec.h * base_spec.w;
+    std::vector<std::string> errs(threads);
+    std::vector<uint32_t> cls(threads, 0);
+    auto work = [&](int t) {
+      try {
+        const uint32_t per = n / threads, extra = n % threads;
+        const uint32_t a = t * per + std::min<uint32_t>(t, extra);
+        const uint32_t b = a + per + (static_cast<uint32_t>(t) < extra ? 1 : 0);
+        R::NetworkSpec spec = base_spec;
+        spec.n = b - a;
+        if (c_t) spec = R::annotate_layouts(spec, R::HeuristicThresholds{c_t, n_t});
+        R::Tensor4D in(spec.n, spec.c, spec.h, spec.w, R::Layout::NCHW);
+        std::copy(input + a * img, input + b * img, in.data());
+        R::RunOptions opt;
+        opt.seed = seed;
+        const R::RunResult res = R::run_network(spec, in, opt);
+        const auto* m = std::get_if<R::Matrix>(&res.output);
+        if (!m) throw std::runtime_error("ref_run_network_sharded: output is not a matrix");
+        if (static_cast<uint64_t>(b) * m->cols > out_cap)
+          throw std::runtime_error("ref_run_network_sharded: output too large");
+        cls[t] = m->cols;
+        std::copy(m->data.begin(), m->data.end(), out + static_cast<uint64_t>(a) * m->cols);
+      } catch (const std::exception& e) {
+        errs[t] = e.what();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (const auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+    *rows = n;
+    *cols = cls[0];
   })
 }
 

@@ -61,11 +61,13 @@ _SIGNATURES = {
                                          _U32, _U32, POINTER(AccessReport), _P]),
     "lcnn_pool_oracle": (c_int, [_P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, c_int, _P]),
     "lcnn_softmax_fused": (c_int, [_P, _P, _U32, _U32, _U32, _P, POINTER(PassReport), _P]),
+    "lcnn_softmax_fused_sticky": (c_int, [_P, _P, _U32, _U32, _P, _P]),
     "lcnn_softmax_reference_scratch_bytes": (c_size_t, [_U32, _U32]),
     "lcnn_softmax_reference": (c_int, [_P, _P, _U32, _U32, _P, c_size_t, _P, POINTER(PassReport), _P]),
     "lcnn_conv_output_extents": (c_int, [_U32, _U32, _U32, _U32, _U32, _U32, POINTER(_U32),
                                          POINTER(_U32)]),
     "lcnn_conv_workspace_bytes": (c_size_t, [_U32] * 7 + [c_int]),
+    "lcnn_conv_workspace_bytes_ex": (c_size_t, [_U32] * 4 + [c_int] + [_U32] * 5 + [c_int]),
     "lcnn_conv_forward": (c_int, [_P, _P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32,
                                   _U32, c_int, _P, c_size_t, _P]),
     "lcnn_conv_packed_bytes": (c_size_t, [_U32] * 4 + [c_int] + [_U32] * 5 + [c_int]),

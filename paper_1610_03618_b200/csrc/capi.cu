@@ -319,6 +319,17 @@ lcnn_status lcnn_softmax_fused(const float* src, float* dst, uint32_t rows, uint
   return ok();
 }
 
+lcnn_status lcnn_softmax_fused_sticky(const float* src, float* dst, uint32_t rows, uint32_t cols,
+                                      int* d_sticky, void* stream) {
+  if (rows < 1 || cols < 1) return fail(LCNN_ESHAPE, "softmax: empty matrix");
+  if (!src || !dst) return fail(LCNN_EINVAL, "softmax: null matrix pointer");
+  if (uint64_t{rows} * cols > 0xffffffffull)
+    return fail(LCNN_ESHAPE, "softmax: matrix too large");
+  cudaError_t e = lcnn_impl::launch_softmax_fused(src, dst, rows, cols, d_sticky, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "softmax_fused");
+  return ok();
+}
+
 size_t lcnn_softmax_reference_scratch_bytes(uint32_t rows, uint32_t cols) {
   return (2 * uint64_t{rows} + 2 * uint64_t{rows} * cols) * sizeof(float);
 }
@@ -360,17 +371,29 @@ lcnn_status lcnn_conv_output_extents(uint32_t h, uint32_t w, uint32_t f_h, uint3
   return ok();
 }
 
+size_t lcnn_conv_workspace_bytes_ex(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, int layout,
+                                    uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
+                                    uint32_t pad, int precision) {
+  if (!stride || f_h > h + 2 * pad || f_w > w + 2 * pad) return 0;
+  const uint32_t ho = (h + 2 * pad - f_h) / stride + 1, wo = (w + 2 * pad - f_w) / stride + 1;
+  lcnn_impl::ConvArgs a{nullptr, nullptr, nullptr, n, c_i, h, w, c_o, f_h, f_w, stride, pad, ho,
+                        wo, layout, precision, nullptr};
+  return lcnn_impl::conv_workspace_bytes(a);
+}
+
 size_t lcnn_conv_workspace_bytes(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, uint32_t c_o,
                                  uint32_t f_h, uint32_t f_w, int precision) {
-  // the larger of the two layouts' needs (the route does not depend on the
-  // stride / padding except through 2^31-column limits, which only ever
-  // select the smaller fp32 path)
+  // No stride / padding in this query, and the route (SHARE / ROW / CI / WIN,
+  // TAPS-N) depends on both: return the largest need over both layouts, every
+  // stride up to the filter size (and 2x beyond) and every padding below the
+  // filter size, so the bound holds for whatever geometry the call uses.
   size_t best = 0;
-  for (int layout : {LCNN_CHWN, LCNN_NCHW}) {
-    lcnn_impl::ConvArgs a{nullptr, nullptr, nullptr, n, c_i, h, w, c_o, f_h, f_w, 1, 0, 1, 1,
-                          layout, precision, nullptr};
-    best = std::max(best, lcnn_impl::conv_workspace_bytes(a));
-  }
+  const uint32_t fmax = f_h > f_w ? f_h : f_w;
+  for (int layout : {LCNN_CHWN, LCNN_NCHW})
+    for (uint32_t stride = 1; stride <= 2 * fmax; ++stride)
+      for (uint32_t pad = 0; pad < fmax; ++pad)
+        best = std::max(best, lcnn_conv_workspace_bytes_ex(n, c_i, h, w, layout, c_o, f_h, f_w,
+                                                           stride, pad, precision));
   return best;
 }
 

@@ -583,10 +583,7 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
       sk.smem_bytes = 1024 + sk.ctl_off + static_cast<uint32_t>(sizeof(PCtl));
       sk.M = static_cast<uint32_t>(m);
       sk.N = static_cast<uint32_t>(n);
-      static const uint32_t probe = [] {
-        const char* e = std::getenv("LCNN_TC_PROBE");
-        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
-      }();
+      const uint32_t probe = tc_probe_knob();
       sk.probe = probe;
       return launch_splitk(L, c, sk, s);
     }

@@ -27,6 +27,23 @@
 #define LCNN_ST_HINT ""
 #endif
 
+// Work-skipping profiling knob (LCNN_TC_PROBE: 1 = skip MMAs, 2 = skip
+// epilogue stores, 4 = no resident filter image).  Modes 1 and 2 return
+// wrong answers, so the environment variable is only read in a library
+// built with -DLCNN_PROFILING_KNOBS (`make PROFILING=1`); the shipped build
+// always runs the full computation.
+inline unsigned tc_probe_knob() {
+#ifdef LCNN_PROFILING_KNOBS
+  static const unsigned probe = [] {
+    const char* e = std::getenv("LCNN_TC_PROBE");
+    return e ? static_cast<unsigned>(std::atoi(e)) : 0u;
+  }();
+  return probe;
+#else
+  return 0u;
+#endif
+}
+
 namespace lcnn_pdl {
 
 __device__ __forceinline__ void wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -266,10 +266,7 @@ inline Sched make_sched(uint32_t mt, uint32_t nt, uint32_t kbn, uint32_t segs, u
   s.stage_bytes = kTcABytes + bn * kTcBK * 4;
   s.a_bytes = kTcABytes;
   s.ksteps = kTcBK / 8;
-  static const uint32_t probe = [] {
-    const char* e = std::getenv("LCNN_TC_PROBE");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
-  }();
+  const uint32_t probe = tc_probe_knob();
   s.probe = probe;
   s.kbn = kbn;
   s.iters = kbn * segs;

@@ -13,8 +13,15 @@
 
 namespace lcnn {
 
-// Owning HBM allocation served from a per-device caching pool; returning a
-// block to the pool does not synchronise.
+// Owning HBM allocation from the device's stream-ordered pool
+// (cudaMallocAsync on the calling thread's current stream, with the pool's
+// release threshold raised so freed blocks stay cached).  The buffer records
+// its device and that stream: freed on the same thread context with the same
+// current stream it is returned with cudaFreeAsync (ordered after every
+// kernel queued there, never a sync); freed anywhere else (another host
+// thread, another current stream or device) it is released with cudaFree,
+// which waits for the device, so a block can never be reused while a kernel
+// on its owner stream may still touch it.
 class DeviceBuffer {
  public:
   DeviceBuffer() = default;
@@ -32,9 +39,12 @@ class DeviceBuffer {
   std::size_t bytes() const { return bytes_; }
 
  private:
+  void release() noexcept;
   void* ptr_ = nullptr;
   std::size_t bytes_ = 0;
   bool owned_ = true;
+  int device_ = -1;
+  void* stream_ = nullptr;  // cudaStream_t the block was allocated on
 };
 
 // The stream every lcnn call issued from this host thread is ordered on.
@@ -88,9 +98,12 @@ struct DeviceMatrix {
   float* data() const { return buf->f(); }
 };
 
-// Convolution / GEMM arithmetic for the host API (lcnn_precision codes).
-// Default FP32 keeps the reference's 1e-5 tolerances; the whole-network
-// benchmark selects TF32 (tensor cores) explicitly.
+// Convolution / GEMM arithmetic of the host-tensor API (lcnn_precision
+// codes) and the default a Network takes at construction.  Default FP32 keeps
+// the reference's 1e-5 tolerances.  A Network resolves its precision once
+// (RunOptions::dense_precision, else this default) and never reads the
+// process default again, so networks at different precisions can run side
+// by side on different threads.
 void set_dense_precision(int precision);
 int dense_precision();
 

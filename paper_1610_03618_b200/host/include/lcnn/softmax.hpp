@@ -35,7 +35,10 @@ Matrix fc_forward(const Matrix& in, const Matrix& weights);
 // Device-resident forms (check_finite = read the non-finite flag back and
 // raise DomainError; costs one 4-byte D2H + stream sync).
 DeviceMatrix softmax_fused(const DeviceMatrix& in, bool check_finite = true);
-void softmax_fused_into(const DeviceMatrix& in, DeviceMatrix& out, bool check_finite = true);
+// sticky_flag (device int, used when check_finite is false): the kernel sets
+// it to 1 on a non-finite input and never clears it; the caller reads it later
+void softmax_fused_into(const DeviceMatrix& in, DeviceMatrix& out, bool check_finite = true,
+                        int* sticky_flag = nullptr);
 DeviceMatrix fc_forward(const DeviceMatrix& in, const DeviceMatrix& weights);
 
 // fc with weights packed once (lcnn_fc_pack_weights; network layers reuse the

@@ -1,17 +1,17 @@
 // Per-thread device context: the CUDA stream every lcnn call of this host
-// thread is ordered on, a caching HBM pool (blocks are recycled on the same
-// stream, so reuse is stream-ordered and never needs a sync), and the
-// status -> exception mapping of the C ABI.
+// thread is ordered on, stream-ordered HBM allocation from the device's
+// cudaMallocAsync pool (see DeviceBuffer in device.hpp for the reuse rules),
+// and the status -> exception mapping of the C ABI.
 #include "lcnn/device.hpp"
 
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
-#include <map>
+#include <mutex>
 #include <string>
-#include <vector>
 
 #include "lcnn_cuda.h"
 
@@ -27,13 +27,24 @@ struct ThreadContext {
   cudaStream_t stream = nullptr;
   cudaStream_t external = nullptr;  // caller-provided stream, if any
   int device = -1;
-  std::multimap<std::size_t, void*> free_blocks;
-  ~ThreadContext() {
-    // Process teardown: the CUDA runtime may already be gone; leak quietly.
-  }
 };
 
 thread_local ThreadContext g_ctx;
+
+// Keep freed blocks cached in the device's default pool (the default release
+// threshold of 0 would return them to the driver at every sync).
+void ensure_pool(int dev) {
+  static std::mutex mu;
+  static std::uint64_t done = 0;  // bit per device
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && (done >> dev) & 1) return;
+  cudaMemPool_t pool;
+  cuda_ok(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool");
+  std::uint64_t threshold = UINT64_MAX;
+  cuda_ok(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold),
+          "cudaMemPoolSetAttribute");
+  if (dev < 64) done |= std::uint64_t{1} << dev;
+}
 
 ThreadContext& ctx() {
   int dev = 0;
@@ -42,7 +53,8 @@ ThreadContext& ctx() {
     cuda_ok(cudaStreamCreateWithFlags(&g_ctx.stream, cudaStreamNonBlocking),
             "cudaStreamCreate");
     g_ctx.device = dev;
-    g_ctx.free_blocks.clear();
+    g_ctx.external = nullptr;
+    ensure_pool(dev);
   }
   return g_ctx;
 }
@@ -72,23 +84,38 @@ std::atomic<int> g_precision{initial_precision()};
 
 DeviceBuffer::DeviceBuffer(std::size_t bytes) {
   ThreadContext& c = ctx();
+  device_ = c.device;
+  stream_ = c.external ? c.external : c.stream;
   bytes_ = round_bytes(bytes);
-  auto it = c.free_blocks.lower_bound(bytes_);
-  if (it != c.free_blocks.end() && it->first <= bytes_ * 2) {
-    ptr_ = it->second;
-    bytes_ = it->first;
-    c.free_blocks.erase(it);
+  const cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  cudaError_t e = cudaMallocAsync(&ptr_, bytes_, s);
+  if (e != cudaSuccess) {
+    // out of memory with blocks cached in the pool: drain, trim, retry once
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    cuda_ok(cudaMallocAsync(&ptr_, bytes_, s), "cudaMallocAsync");
+  }
+}
+
+void DeviceBuffer::release() noexcept {
+  if (!ptr_ || !owned_) return;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;  // runtime torn down: leak quietly
+  const cudaStream_t cur = g_ctx.external ? g_ctx.external : g_ctx.stream;
+  if (dev == device_ && g_ctx.device == device_ && cur == static_cast<cudaStream_t>(stream_) &&
+      cudaFreeAsync(ptr_, cur) == cudaSuccess) {
+    ptr_ = nullptr;
     return;
   }
-  cudaError_t e = cudaMalloc(&ptr_, bytes_);
-  if (e != cudaSuccess) {
-    // release cached blocks and retry once
-    cudaStreamSynchronize(c.stream);
-    for (auto& kv : c.free_blocks) cudaFree(kv.second);
-    c.free_blocks.clear();
-    cudaGetLastError();
-    cuda_ok(cudaMalloc(&ptr_, bytes_), "cudaMalloc");
-  }
+  cudaGetLastError();
+  // foreign thread / stream / device: cudaFree waits for the device first
+  if (dev != device_) cudaSetDevice(device_);
+  cudaFree(ptr_);
+  if (dev != device_) cudaSetDevice(dev);
+  cudaGetLastError();
+  ptr_ = nullptr;
 }
 
 DeviceBuffer DeviceBuffer::borrow(void* ptr, std::size_t bytes) {
@@ -99,22 +126,22 @@ DeviceBuffer DeviceBuffer::borrow(void* ptr, std::size_t bytes) {
   return b;
 }
 
-DeviceBuffer::~DeviceBuffer() {
-  if (ptr_ && owned_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
-}
+DeviceBuffer::~DeviceBuffer() { release(); }
 
 DeviceBuffer::DeviceBuffer(DeviceBuffer&& o) noexcept
-    : ptr_(o.ptr_), bytes_(o.bytes_), owned_(o.owned_) {
+    : ptr_(o.ptr_), bytes_(o.bytes_), owned_(o.owned_), device_(o.device_), stream_(o.stream_) {
   o.ptr_ = nullptr;
   o.bytes_ = 0;
 }
 
 DeviceBuffer& DeviceBuffer::operator=(DeviceBuffer&& o) noexcept {
   if (this != &o) {
-    if (ptr_ && owned_ && g_ctx.stream) g_ctx.free_blocks.emplace(bytes_, ptr_);
+    release();
     ptr_ = o.ptr_;
     bytes_ = o.bytes_;
     owned_ = o.owned_;
+    device_ = o.device_;
+    stream_ = o.stream_;
     o.ptr_ = nullptr;
     o.bytes_ = 0;
   }
@@ -129,8 +156,8 @@ void* current_stream() {
 void set_current_stream(void* stream) {
   ThreadContext& c = ctx();
   if (c.external == static_cast<cudaStream_t>(stream)) return;  // no change: stay async
-  // drain the stream being left: pooled blocks freed on it may be reused on
-  // the new one
+  // drain the stream being left: the caller may read its results or destroy
+  // it right after switching
   synchronize();
   c.external = static_cast<cudaStream_t>(stream);
 }

@@ -58,6 +58,14 @@ int status_of_current() {
 
 lcnn::Layout L(int code) { return static_cast<lcnn::Layout>(code); }
 
+// DomainError for a forward that met a non-finite classifier input, with the
+// reference's layer-prefixed message (softmax.cpp:15-19 rethrown by
+// net.cpp:387-391 as "layer '<name>': softmax: non-finite input").
+void raise_if_nonfinite(const lcnn::Network& net) {
+  if (net.take_nonfinite())
+    throw lcnn::DomainError("layer '" + net.softmax_layer() + "': softmax: non-finite input");
+}
+
 // The ABI's stream argument is a cudaStream_t: 0 is the legacy default
 // stream (CUDA's convention), not the library's private stream.
 void* abi_stream(void* stream) { return stream ? stream : static_cast<void*>(cudaStreamLegacy); }
@@ -70,15 +78,34 @@ const char* lcnn_net_last_error(void) { return g_err.c_str(); }
 
 void lcnn_set_dense_precision(int precision) { lcnn::set_dense_precision(precision); }
 
-int lcnn_net_create(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed, lcnn_net** out) {
+int lcnn_net_create_ex(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
+                       int precision, lcnn_net** out) {
   NET_GUARD({
+    if (!out) throw lcnn::ValidationError("null handle pointer");
+    if (precision > LCNN_PREC_FP32) throw lcnn::ValidationError("unknown precision");
     lcnn::NetworkSpec spec = lcnn::parse_network(json);
     lcnn::HeuristicThresholds th = c_t ? lcnn::HeuristicThresholds{c_t, n_t} : lcnn::kTitanBlack;
     spec = lcnn::annotate_layouts(spec, th);
     lcnn::RunOptions opt;
     opt.seed = seed;
+    opt.dense_precision = precision;
     auto* h = new lcnn_net{std::make_unique<lcnn::Network>(std::move(spec), opt)};
     *out = h;
+  })
+}
+
+int lcnn_net_create(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed, lcnn_net** out) {
+  return lcnn_net_create_ex(json, c_t, n_t, seed, -1, out);
+}
+
+int lcnn_net_precision(const lcnn_net* net) { return net->net->precision(); }
+
+const int* lcnn_net_nonfinite_flag(const lcnn_net* net) { return net->net->nonfinite_flag(); }
+
+int lcnn_net_status(const lcnn_net* net, void* stream) {
+  NET_GUARD({
+    lcnn::set_current_stream(abi_stream(stream));
+    raise_if_nonfinite(*net->net);
   })
 }
 
@@ -145,6 +172,7 @@ int lcnn_net_forward_host(const lcnn_net* net, const float* h_input, int in_layo
                         cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
     lcnn::synchronize();
+    raise_if_nonfinite(*net->net);
   })
 }
 
@@ -197,6 +225,7 @@ int lcnn_net_forward_host_many(const lcnn_net* net, const float* const* h_inputs
     }
     lcnn::synchronize();
     ck(cudaStreamSynchronize(r.copy));
+    raise_if_nonfinite(*net->net);
   })
 }
 

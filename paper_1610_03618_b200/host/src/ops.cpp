@@ -239,9 +239,15 @@ CoarseningPlan autotune_pool(std::uint32_t n, std::uint32_t c, std::uint32_t h, 
 }
 
 // ============================================================= softmax ===
-void softmax_fused_into(const DeviceMatrix& in, DeviceMatrix& out, bool check_finite) {
+void softmax_fused_into(const DeviceMatrix& in, DeviceMatrix& out, bool check_finite,
+                        int* sticky_flag) {
   if (in.rows < 1 || in.cols < 1) throw ShapeError("softmax: empty matrix");
   if (out.rows != in.rows || out.cols != in.cols) throw ShapeError("softmax: output dims");
+  if (!check_finite && sticky_flag) {  // caller-owned device flag, read later
+    check_status(lcnn_softmax_fused_sticky(in.data(), out.data(), in.rows, in.cols, sticky_flag,
+                                           current_stream()));
+    return;
+  }
   int* flag = check_finite ? nonfinite_flag() : nullptr;
   check_status(lcnn_softmax_fused(in.data(), out.data(), in.rows, in.cols, 16384, flag, nullptr,
                                   current_stream()));
@@ -390,7 +396,8 @@ DeviceTensor4D conv_forward(const DeviceTensor4D& in, const float* d_filters, st
   const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f_h, f_w, p);
   DeviceTensor4D out(in.n(), c_o, ho, wo, in.layout());
   const std::size_t ws =
-      lcnn_conv_workspace_bytes(in.n(), in.c(), in.h(), in.w(), c_o, f_h, f_w, precision);
+      lcnn_conv_workspace_bytes_ex(in.n(), in.c(), in.h(), in.w(), code(in.layout()), c_o, f_h,
+                                   f_w, p.stride, p.pad, precision);
   DeviceBuffer& buf = scratch(ws + 16);
   check_status(lcnn_conv_forward(in.data(), d_filters, out.data(), in.n(), in.c(), in.h(), in.w(),
                                  code(in.layout()), c_o, f_h, f_w, p.stride, p.pad, precision,

@@ -334,7 +334,8 @@ def conv_forward(x: DeviceTensor4D, filters, c_o, f_h, f_w, stride=1, pad=0, pre
         out = DeviceTensor4D(x.n, c_o, ho, wo, x.layout,
                              torch.empty(x.n * c_o * ho * wo, dtype=torch.float32,
                                          device=x.data.device))
-    nbytes = capi.lib().lcnn_conv_workspace_bytes(x.n, x.c, x.h, x.w, c_o, f_h, f_w, precision)
+    nbytes = capi.lib().lcnn_conv_workspace_bytes_ex(x.n, x.c, x.h, x.w, x.layout, c_o, f_h, f_w,
+                                                     stride, pad, precision)
     if workspace is None or workspace.numel() * 4 < nbytes:
         workspace = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32,
                                 device=x.data.device)

@@ -21,6 +21,12 @@ def lib():
             raise RuntimeError(f"{LIB} missing: run make / __graft_entry__.build()")
         d = ctypes.CDLL(LIB)
         d.lcnn_net_create.argtypes = [c_char_p, c_uint32, c_uint32, c_uint64, POINTER(c_void_p)]
+        d.lcnn_net_create_ex.argtypes = [c_char_p, c_uint32, c_uint32, c_uint64, c_int,
+                                         POINTER(c_void_p)]
+        d.lcnn_net_precision.argtypes = [c_void_p]
+        d.lcnn_net_status.argtypes = [c_void_p, c_void_p]
+        d.lcnn_net_nonfinite_flag.argtypes = [c_void_p]
+        d.lcnn_net_nonfinite_flag.restype = c_void_p
         d.lcnn_net_destroy.argtypes = [c_void_p]
         d.lcnn_net_last_error.restype = c_char_p
         d.lcnn_net_info.argtypes = [c_void_p, c_int, POINTER(c_uint32), POINTER(c_int),
@@ -46,11 +52,17 @@ def _check(st):
 class Network:
     """A parsed, annotated network with weights resident in HBM."""
 
-    def __init__(self, json_text: str, c_t: int = 0, n_t: int = 0, seed: int = 42):
+    def __init__(self, json_text: str, c_t: int = 0, n_t: int = 0, seed: int = 42,
+                 precision: int | None = None):
+        """precision: capi.PREC_* for the conv / fc layers (None = the process
+        default set by set_dense_precision)."""
         h = c_void_p()
-        _check(lib().lcnn_net_create(json_text.encode(), c_t, n_t, seed, ctypes.byref(h)))
+        _check(lib().lcnn_net_create_ex(json_text.encode(), c_t, n_t, seed,
+                                        -1 if precision is None else precision,
+                                        ctypes.byref(h)))
         self._h = h
         self.layouts = self._layouts()
+        self.precision = lib().lcnn_net_precision(self._h)
 
     def info(self, in_layout: int):
         dims = (c_uint32 * 4)()
@@ -68,6 +80,15 @@ class Network:
 
     def forward(self, d_input: int, in_layout: int, d_output: int, stream: int):
         _check(lib().lcnn_net_forward(self._h, d_input, in_layout, d_output, stream))
+
+    def status(self, stream: int):
+        """Wait for `stream`; raise DomainError if a forward since the last
+        call met a non-finite classifier input (clears the flag)."""
+        _check(lib().lcnn_net_status(self._h, stream))
+
+    def nonfinite_flag_ptr(self) -> int:
+        """Device address of the sticky non-finite flag (an int32)."""
+        return lib().lcnn_net_nonfinite_flag(self._h)
 
     def forward_host(self, h_input: int, in_layout: int, h_output: int):
         _check(lib().lcnn_net_forward_host(self._h, h_input, in_layout, h_output))

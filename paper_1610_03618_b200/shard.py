@@ -26,17 +26,47 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t[0])
 
 
-def gather_rows(local, world: int):
-    """All-gather equal-sized row blocks (flat tensors) in rank order."""
+def gather_rows(local, world: int, global_rows: int | None = None):
+    """All-gather every rank's row block (flat tensors) in rank order.
+
+    With `global_rows` the blocks may be ragged as shard_range makes them
+    (the first global_rows % world ranks hold one extra row): each block is
+    padded to ceil(global_rows / world) rows, gathered, and trimmed back, so
+    NCCL and gloo always see equal-sized buffers.  Without it every rank
+    must hold the same number of elements."""
     import torch
     import torch.distributed as dist
 
     if world == 1:
         return local
-    out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+    if global_rows is None:
+        blocks = [(0, local.numel())] * world
+        cap = local.numel()
+        buf = local
+    else:
+        row = None
+        for r in range(world):
+            a, b = shard_range(global_rows, world, r)
+            if r == dist.get_rank():
+                if b - a and local.numel() % (b - a):
+                    raise ValueError("gather_rows: local block is not whole rows")
+                row = local.numel() // (b - a) if b - a else None
+        # every rank needs the row width, including one holding no rows
+        w = torch.tensor([row or 0], dtype=torch.int64, device=local.device)
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        row = int(w[0])
+        per = -(-global_rows // world)
+        cap = per * row
+        blocks = [(0, (b - a) * row) for a, b in (shard_range(global_rows, world, r)
+                                                  for r in range(world))]
+        buf = torch.zeros(cap, dtype=local.dtype, device=local.device)
+        buf[:local.numel()] = local
+    out = torch.empty(world * cap, dtype=local.dtype, device=local.device)
     if local.is_cuda:
-        dist.all_gather_into_tensor(out, local)
+        dist.all_gather_into_tensor(out, buf)
     else:
         parts = list(out.view(world, -1).unbind(0))
-        dist.all_gather(parts, local)
-    return out
+        dist.all_gather(parts, buf)
+    if global_rows is None:
+        return out
+    return torch.cat([out[r * cap + a:r * cap + b] for r, (a, b) in enumerate(blocks)])

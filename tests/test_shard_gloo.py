@@ -63,6 +63,14 @@ def _worker(rank, world, port, q):
         out_n = C.transform(out_c, b - a, c, 6, 6, CHWN, NCHW)
         got = gather_rows(torch.from_numpy(out_n), world).numpy()
         assert bit_equal(got, C.pool_plain(x.reshape(-1), n, c, h, w, NCHW, 3, 3, 2, False)[0])
+        # ragged shards (n % world != 0): rows are padded, gathered, trimmed
+        for n_r in (7, 1, 3):
+            a, b = shard_range(n_r, world, rank)
+            rows = rng_uniform(13, n_r * 5, -5, 5).reshape(n_r, 5)
+            mine, _ = C.softmax_fused(rows[a:b].reshape(-1), b - a, 5) if b > a else (
+                np.zeros(0, np.float32), None)
+            got = gather_rows(torch.from_numpy(mine), world, n_r).numpy()
+            assert bit_equal(got, C.softmax_fused(rows.reshape(-1), n_r, 5)[0]), n_r
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - surfaced by the parent
