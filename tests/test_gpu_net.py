@@ -118,3 +118,80 @@ def test_forward_host_many_matches_device_forward(cuda, c_t, n_t):
     net.forward_host(hc.data_ptr(), CHWN, out.data_ptr())
     assert approx_equal(out.numpy(), want[2], 1e-5)
     net.close()
+
+
+def test_nonfinite_input_surfaces_domain_error(cuda):
+    """The reference raises DomainError for a non-finite classifier input
+    (softmax.cpp:15-19, rewrapped with the layer name by net.cpp:387-391).
+    Device forward: asynchronous, the sticky flag is reported by status();
+    host-buffer forwards: LCNN_EDOMAIN directly."""
+    import torch
+
+    from paper_1610_03618_b200.errors import DomainError
+
+    net = netapi.Network(json.dumps(MINI), 257, 32, seed=42, precision=capi.PREC_FP32)
+    info = net.info(NCHW)
+    rows, cols = info["out"]
+    n, c, h, w = info["dims"]
+    x = rng_uniform(5, n * c * h * w)
+    bad = x.copy()
+    bad[123] = np.inf
+    stream = torch.cuda.current_stream(cuda).cuda_stream
+    dy = torch.empty(rows * cols, device=cuda)
+    net.forward(torch.from_numpy(x).to(cuda).data_ptr(), NCHW, dy.data_ptr(), stream)
+    net.status(stream)  # finite: no error
+    net.forward(torch.from_numpy(bad).to(cuda).data_ptr(), NCHW, dy.data_ptr(), stream)
+    with pytest.raises(DomainError, match="layer 'prob': softmax: non-finite input"):
+        net.status(stream)
+    net.status(stream)  # the flag was cleared by the read
+    out = torch.zeros(rows * cols).pin_memory()
+    with pytest.raises(DomainError):
+        net.forward_host(torch.from_numpy(bad).pin_memory().data_ptr(), NCHW, out.data_ptr())
+    net.forward_host(torch.from_numpy(x).pin_memory().data_ptr(), NCHW, out.data_ptr())
+    net.close()
+
+
+def test_precision_is_per_network(cuda):
+    """Two networks at different precisions side by side (and the process
+    default changed in between) each keep the precision they were made with."""
+    import threading
+
+    import torch
+
+    text = json.dumps(MINI)
+    n, c, h, w = MINI["input"]["n"], 3, 67, 67
+    x = torch.from_numpy(rng_uniform(9, n * c * h * w)).to(cuda)
+    nets = {p: netapi.Network(text, 257, 32, seed=42, precision=p)
+            for p in (capi.PREC_FP32, capi.PREC_TF32)}
+    netapi.set_dense_precision(capi.PREC_TF32)  # must not affect the FP32 network
+    want = {}
+    for p, net in nets.items():
+        assert net.precision == p
+        y = torch.empty(n * 10, device=cuda)
+        net.forward(x.data_ptr(), NCHW, y.data_ptr(), torch.cuda.current_stream(cuda).cuda_stream)
+        torch.cuda.synchronize()
+        want[p] = y.cpu()
+    assert not torch.equal(want[capi.PREC_FP32], want[capi.PREC_TF32])
+    got, errs = {}, []
+
+    def run(p):
+        try:
+            s = torch.cuda.Stream(cuda)
+            y = torch.empty(n * 10, device=cuda)
+            for _ in range(20):
+                nets[p].forward(x.data_ptr(), NCHW, y.data_ptr(), s.cuda_stream)
+            s.synchronize()
+            got[p] = y.cpu()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(p,)) for p in nets]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert torch.equal(got[capi.PREC_FP32], want[capi.PREC_FP32])
+    assert torch.allclose(got[capi.PREC_TF32], want[capi.PREC_TF32], rtol=1e-4, atol=1e-7)
+    for net in nets.values():
+        net.close()
