@@ -139,7 +139,7 @@ class PoolOp(Op):
     def __init__(self, n, c, h, w, layout, win, stride, avg, plan, seed, rotate=False):
         self.n, self.c, self.h, self.w = n, c, h, w
         self.layout, self.win, self.stride, self.avg = layout, win, stride, avg
-        self.plan = plan  # None = pool_layout (plain)
+        self.plan = plan  # None = the GPU-tuned plan (lcnn_pool_tune at alloc)
         self.seed = seed
         self.ho = (h - win) // stride + 1
         self.wo = (w - win) // stride + 1
@@ -151,13 +151,25 @@ class PoolOp(Op):
 
     def _extra_alloc(self, torch, device):
         self.rep = self.capi.AccessReport()
+        if self.plan is None:
+            # the GPU autotuner (lcnn_pool_tune): every specialised kernel plan
+            # of this layout timed on this shape, fastest cached and used
+            self.tuned = self.capi.PoolPlan()
+            st = self.lib.lcnn_pool_tune(self.n, self.c, self.h, self.w, self.layout, self.win,
+                                         self.win, self.stride, 1 if self.avg else 0,
+                                         ctypes.byref(self.tuned),
+                                         torch.cuda.current_stream(device).cuda_stream)
+            self.capi.check(st, "pool_tune")
+            t = self.tuned
+            ring = f",ring{t.ring_kb}KBx{t.ring_slots}x{t.ring_ctas}" if t.ring_kb else ""
+            self.name = self.name.replace("_plain_", f"_tuned({t.fh},{t.fw}{ring})_")
 
     def bind(self, x_ptr, y_ptr):
         mode = 1 if self.avg else 0
         if self.plan is None:
-            fn = self.lib.lcnn_pool_layout
+            fn = self.lib.lcnn_pool_run_plan
             args = (x_ptr, y_ptr, self.n, self.c, self.h, self.w, self.layout, self.win, self.win,
-                    self.stride, mode, ctypes.byref(self.rep))
+                    self.stride, mode, ctypes.byref(self.tuned), ctypes.byref(self.rep))
         elif self.layout == 1:
             fn = self.lib.lcnn_pool_coarsened
             args = (x_ptr, y_ptr, self.n, self.c, self.h, self.w, self.layout, self.win, self.win,
@@ -173,8 +185,11 @@ class PoolOp(Op):
         pool_layout otherwise (NCHW has no coarsened reference, pool.cpp:190)."""
         from oracle.oracle import OP_POOL_COARSENED, OP_POOL_LAYOUT, Ref
 
-        op = OP_POOL_LAYOUT if self.plan is None or self.layout != 1 else OP_POOL_COARSENED
-        fh, fw = self.plan if self.plan else (1, 1)
+        # the reference's pool_layout (pool.cpp:172-176, its faster pooling
+        # entry on both layouts: PL5 2.60 vs 2.30 GB/s for pool_coarsened(2,2));
+        # an explicit CHWN --plan runs the reference's pool_coarsened
+        op = OP_POOL_COARSENED if self.plan and self.layout == 1 else OP_POOL_LAYOUT
+        fh, fw = self.plan or (1, 1)
         s = Ref.session(op, batch, self.c, self.h, self.w, self.layout, 0, self.win, self.win,
                         self.stride, self.avg, fh, fw, threads)
         sample_bytes = batch * (self.c * self.h * self.w + self.c * self.ho * self.wo) * 4
@@ -255,8 +270,6 @@ class Workload:
 
 
 VGG_GLOBAL_BATCH = 256
-# measured best per layer (scripts/pool_plans.py [nchw vgg] on B200)
-VGG_PLANS = {1: [(1, 1)] * 5, 0: [(2, 2), (4, 1), (2, 1), (2, 1), (1, 2)]}
 
 
 def build_workload(name, world, rank, plan=None, tsweep_n=None):
@@ -272,7 +285,7 @@ def build_workload(name, world, rank, plan=None, tsweep_n=None):
     par = f"N-shard x{world} (no data-path collective)"
     if name in ("vgg_pools", "vgg_pools_nchw"):
         layout = CHWN if name == "vgg_pools" else NCHW
-        plans = [tuple(plan)] * len(VGG_POOLS) if plan else VGG_PLANS[layout]
+        plans = [tuple(plan) if plan else None] * len(VGG_POOLS)  # None: GPU-tuned
         a, b = shard_range(VGG_GLOBAL_BATCH, world, rank)
 
         def mk(nb, sd):
@@ -295,7 +308,7 @@ def build_workload(name, world, rank, plan=None, tsweep_n=None):
         return Workload(ops, gops, desc, 0, "strong", VGG_GLOBAL_BATCH, "images")
     if name in ("pl5", "pl5_nchw"):
         layout = CHWN if name == "pl5" else NCHW
-        p = tuple(plan) if plan else ((2, 2) if layout == CHWN else (3, 2))  # scripts/pool_plans.py
+        p = tuple(plan) if plan else None  # None: GPU-tuned (lcnn_pool_tune)
         ops = [PoolOp(128, 96, 55, 55, layout, 3, 2, False, p, seed, rotate=True)]
         desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) max 3x3/s2, "
                             f"128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",

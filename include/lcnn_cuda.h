@@ -113,6 +113,39 @@ lcnn_status lcnn_pool_output_extents(uint32_t h, uint32_t w, uint32_t win_h,
                                      uint32_t win_w, uint32_t stride,
                                      uint32_t* h_out, uint32_t* w_out);
 
+/* ---- pooling plan tuner (PAPER.md:227 autotuned coarsening, pool.cpp:272-331) --
+ * The kernel plan of one pooling shape: the (fh, fw) output block each thread
+ * computes with register reuse of overlapping windows, and for the NCHW
+ * pipelined kernel the shared-memory ring (KB per slot, slots per CTA, CTAs
+ * per SM; 0 = the shape's default).  Any plan gives the same output bits (tap
+ * order is per output), so plans change speed only. */
+typedef struct lcnn_pool_plan {
+  uint32_t fh, fw;
+  uint32_t ring_kb, ring_slots, ring_ctas;
+  int tuned;  /* 1: measured by lcnn_pool_tune on this device */
+  float us;   /* measured time of the plan, microseconds (0 if untuned) */
+} lcnn_pool_plan;
+/* Measure every specialised plan of the layout's kernel family on scratch
+ * buffers of this shape (CUDA events on `stream`, median of 3 after a
+ * warm-up; CHWN fh, fw in 1..4; NCHW fh 1..4, fw 1..2, then 7 ring shapes),
+ * cache the fastest per (device, shape, window, mode) and return it.  A shape
+ * already tuned returns the cached plan without measuring.  Synchronises
+ * `stream`; allocates the shape's input + output transiently. */
+lcnn_status lcnn_pool_tune(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int layout,
+                           uint32_t win_h, uint32_t win_w, uint32_t stride, int mode,
+                           lcnn_pool_plan* plan, void* stream);
+/* The cached tuned plan, else the static default (no measurement). */
+lcnn_status lcnn_pool_plan_lookup(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int layout,
+                                  uint32_t win_h, uint32_t win_w, uint32_t stride, int mode,
+                                  lcnn_pool_plan* plan);
+/* Pool in CHWN or NCHW with an explicit plan; report = the coarsened access
+ * report of (fh, fw) (pool.cpp:236). */
+lcnn_status lcnn_pool_run_plan(const float* src, float* dst, uint32_t n, uint32_t c,
+                               uint32_t h, uint32_t w, int layout, uint32_t win_h,
+                               uint32_t win_w, uint32_t stride, int mode,
+                               const lcnn_pool_plan* plan, lcnn_access_report* report,
+                               void* stream);
+
 /* == pool_layout (pool.cpp:172-176 -> pool_plain :98-163).  layout must be
  * CHWN or NCHW (LayoutError otherwise, pool.cpp:165); output keeps the input
  * layout.  Max: bit-exact with acc = (acc < v) ? v : acc from -inf in (y,x)

@@ -11,6 +11,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "lcnn_cuda.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -32,6 +34,9 @@ int lcnn_net_create_ex(const char* json, uint32_t c_t, uint32_t n_t, uint64_t se
                        int precision, lcnn_net** out);
 /* The network's lcnn_precision. */
 int lcnn_net_precision(const lcnn_net* net);
+/* The GPU-tuned pooling plan of layer `layer` (lcnn_pool_tune, measured when
+ * the network was created; tuned == 0 for non-pool layers). */
+int lcnn_net_pool_plan(const lcnn_net* net, uint32_t layer, lcnn_pool_plan* plan);
 void lcnn_net_destroy(lcnn_net* net);
 const char* lcnn_net_last_error(void);
 

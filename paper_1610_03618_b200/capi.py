@@ -35,6 +35,21 @@ class AccessReport(ctypes.Structure):
         return (self.input_loads, self.output_stores, self.distinct_inputs)
 
 
+class PoolPlan(ctypes.Structure):
+    """== lcnn_pool_plan (include/lcnn_cuda.h): a pooling kernel plan."""
+
+    _fields_ = [("fh", c_uint32), ("fw", c_uint32), ("ring_kb", c_uint32),
+                ("ring_slots", c_uint32), ("ring_ctas", c_uint32), ("tuned", c_int),
+                ("us", ctypes.c_float)]
+
+    def as_tuple(self):
+        return (self.fh, self.fw, self.ring_kb, self.ring_slots, self.ring_ctas)
+
+    def __repr__(self):
+        ring = f" ring={self.ring_kb}KBx{self.ring_slots}x{self.ring_ctas}" if self.ring_kb else ""
+        return f"PoolPlan({self.fh}x{self.fw}{ring}{' tuned' if self.tuned else ''})"
+
+
 class PassReport(ctypes.Structure):
     """== lcnn::PassReport (softmax.hpp:21-24)."""
 
@@ -59,6 +74,11 @@ _SIGNATURES = {
                                     _U32, _U32, POINTER(AccessReport), _P]),
     "lcnn_pool_coarsened_nchw": (c_int, [_P, _P, _U32, _U32, _U32, _U32, _U32, _U32, _U32, c_int,
                                          _U32, _U32, POINTER(AccessReport), _P]),
+    "lcnn_pool_tune": (c_int, [_U32] * 4 + [c_int] + [_U32] * 3 + [c_int, POINTER(PoolPlan), _P]),
+    "lcnn_pool_plan_lookup": (c_int, [_U32] * 4 + [c_int] + [_U32] * 3 + [c_int,
+                                                                      POINTER(PoolPlan)]),
+    "lcnn_pool_run_plan": (c_int, [_P, _P] + [_U32] * 4 + [c_int] + [_U32] * 3 +
+                           [c_int, POINTER(PoolPlan), POINTER(AccessReport), _P]),
     "lcnn_pool_oracle": (c_int, [_P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, c_int, _P]),
     "lcnn_softmax_fused": (c_int, [_P, _P, _U32, _U32, _U32, _P, POINTER(PassReport), _P]),
     "lcnn_softmax_fused_sticky": (c_int, [_P, _P, _U32, _U32, _P, _P]),
@@ -132,7 +152,7 @@ def call(name: str, *args) -> int:
 
 
 __all__ = [
-    "AccessReport", "PassReport", "lib", "call", "check", "declared_symbols", "LIB_PATH",
+    "AccessReport", "PassReport", "PoolPlan", "lib", "call", "check", "declared_symbols", "LIB_PATH",
     "NCHW", "CHWN", "NHWC", "HWCN", "POOL_MAX", "POOL_AVG", "PREC_TF32", "PREC_3XTF32",
     "LAYOUT_NAMES", "c_double", "PREC_FP32",
 ]

@@ -6,7 +6,11 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
+#include <vector>
 
 #include "../../include/lcnn_cuda.h"
 #include "internal.h"
@@ -207,6 +211,191 @@ lcnn_status lcnn_pool_output_extents(uint32_t h, uint32_t w, uint32_t win_h, uin
   return ok();
 }
 
+// ---- pooling plans: static defaults, the GPU tuner and its cache ---------
+namespace {
+
+// The plan pool_layout uses before (or without) tuning.  NCHW: the pipelined
+// kernel's output block measured in round 1 (scripts/pool_plans.py,
+// profiles/r01_pool_plans_nchw*.txt: 3x3/s2 -> 3x2; 2x2/s2 -> 2x2 on >= 200-wide
+// planes, 4x1 >= 100, 2x1 >= 20, else 1x2).  CHWN: the plain kernel (1,1).
+lcnn_pool_plan static_plan(uint32_t w, int layout, uint32_t win_h, uint32_t win_w,
+                           uint32_t stride) {
+  lcnn_pool_plan p{1, 1, 0, 0, 0, 0, 0.0f};
+  if (layout == LCNN_NCHW && win_h == win_w && stride == 2 && win_h == 3) {
+    p.fh = 3;
+    p.fw = 2;
+  } else if (layout == LCNN_NCHW && win_h == win_w && stride == 2 && win_h == 2) {
+    p.fh = w >= 200 ? 2 : w >= 100 ? 4 : w >= 20 ? 2 : 1;
+    p.fw = w >= 200 ? 2 : w >= 20 ? 1 : 2;
+  }
+  return p;
+}
+
+using PlanKey = std::tuple<int, uint32_t, uint32_t, uint32_t, uint32_t, int, uint32_t, uint32_t,
+                           uint32_t, int>;
+std::mutex g_plan_mu;
+std::map<PlanKey, lcnn_pool_plan> g_plans;
+
+PlanKey plan_key(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int layout, uint32_t win_h,
+                 uint32_t win_w, uint32_t stride, int mode) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return PlanKey{dev, n, c, h, w, layout, win_h, win_w, stride, mode};
+}
+
+lcnn_impl::PoolArgs plan_args(const float* src, float* dst, uint32_t n, uint32_t c, uint32_t h,
+                              uint32_t w, uint32_t ho, uint32_t wo, uint32_t win_h,
+                              uint32_t win_w, uint32_t stride, int mode,
+                              const lcnn_pool_plan& p) {
+  lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
+                        mode == LCNN_POOL_AVG, p.fh, p.fw};
+  a.ring_kb = p.ring_kb;
+  a.ring_slots = p.ring_slots;
+  a.ring_ctas = p.ring_ctas;
+  return a;
+}
+
+cudaError_t launch_plan(const lcnn_impl::PoolArgs& a, int layout, cudaStream_t st) {
+  return layout == LCNN_CHWN ? lcnn_impl::launch_pool_chwn(a, st)
+                             : lcnn_impl::launch_pool_nchw(a, st);
+}
+
+}  // namespace
+
+lcnn_status lcnn_pool_plan_lookup(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int layout,
+                                  uint32_t win_h, uint32_t win_w, uint32_t stride, int mode,
+                                  lcnn_pool_plan* plan) {
+  if (!plan) return fail(LCNN_EINVAL, "pool_plan: null plan pointer");
+  lcnn_status st = check_window(h, w, win_h, win_w, stride);
+  if (st != LCNN_OK) return st;
+  if (layout != LCNN_CHWN && layout != LCNN_NCHW)
+    return fail(LCNN_ELAYOUT, "pool_layout: only CHWN and NCHW kernels exist");
+  {
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    const auto it = g_plans.find(plan_key(n, c, h, w, layout, win_h, win_w, stride, mode));
+    if (it != g_plans.end()) {
+      *plan = it->second;
+      return ok();
+    }
+  }
+  *plan = static_plan(w, layout, win_h, win_w, stride);
+  return ok();
+}
+
+lcnn_status lcnn_pool_tune(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int layout,
+                           uint32_t win_h, uint32_t win_w, uint32_t stride, int mode,
+                           lcnn_pool_plan* plan, void* stream) {
+  lcnn_status st = lcnn_pool_plan_lookup(n, c, h, w, layout, win_h, win_w, stride, mode, plan);
+  if (st != LCNN_OK || plan->tuned) return st;
+  st = check_volume(n, c, h, w, "Tensor4D");
+  if (st != LCNN_OK) return st;
+  if (mode != LCNN_POOL_MAX && mode != LCNN_POOL_AVG) return fail(LCNN_EINVAL, "pool: bad mode");
+  const uint32_t ho = (h - win_h) / stride + 1, wo = (w - win_w) / stride + 1;
+  const size_t in_bytes = size_t{n} * c * h * w * 4, out_bytes = size_t{n} * c * ho * wo * 4;
+  cudaStream_t s = S(stream);
+  float *src = nullptr, *dst = nullptr;
+  cudaError_t e = cudaMallocAsync(&src, in_bytes, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dst, out_bytes, s);
+  // the timing of max / average pooling does not depend on the values
+  if (e == cudaSuccess) e = cudaMemsetAsync(src, 0x3f, in_bytes, s);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  if (e != cudaSuccess) {
+    if (src) cudaFreeAsync(src, s);
+    if (dst) cudaFreeAsync(dst, s);
+    return cuda_fail(e, "pool_tune");
+  }
+  // median of 3 timed launches after one warm-up; a candidate whose launch
+  // fails (no specialisation, shared memory over the limit) is skipped
+  auto cost = [&](const lcnn_pool_plan& p) -> float {
+    const lcnn_impl::PoolArgs a =
+        plan_args(src, dst, n, c, h, w, ho, wo, win_h, win_w, stride, mode, p);
+    if (launch_plan(a, layout, s) != cudaSuccess) {
+      cudaGetLastError();
+      return -1.0f;
+    }
+    float t[3];
+    for (float& ti : t) {
+      cudaEventRecord(e0, s);
+      launch_plan(a, layout, s);
+      cudaEventRecord(e1, s);
+      if (cudaEventSynchronize(e1) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.0f;
+      }
+      cudaEventElapsedTime(&ti, e0, e1);
+    }
+    std::sort(t, t + 3);
+    return t[1] * 1e3f;
+  };
+  lcnn_pool_plan best = static_plan(w, layout, win_h, win_w, stride);
+  best.us = cost(best);
+  auto consider = [&](lcnn_pool_plan p) {
+    const float us = cost(p);
+    if (us > 0.0f && (best.us <= 0.0f || us < best.us)) {
+      p.us = us;
+      best = p;
+    }
+  };
+  // output blocks: every specialised (fh, fw) of the layout's kernel family
+  const uint32_t fw_max = layout == LCNN_CHWN ? 4 : 2;
+  const bool special = win_h == win_w && ((stride == 2 && (win_h == 2 || win_h == 3)) ||
+                                          (stride == 1 && win_h == 3));
+  if (special)
+    for (uint32_t fh = 1; fh <= 4; ++fh)
+      for (uint32_t fw = 1; fw <= fw_max; ++fw)
+        if (fh != best.fh || fw != best.fw) consider(lcnn_pool_plan{fh, fw, 0, 0, 0, 0, 0.0f});
+  // NCHW pipelined kernel: the shared-memory ring for the chosen block
+  // (KB per slot, slots, CTAs per SM); ineligible shapes ignore the ring
+  if (layout == LCNN_NCHW && special) {
+    static const uint32_t rings[][3] = {{48, 2, 2}, {24, 2, 4}, {32, 2, 3}, {16, 3, 4},
+                                        {24, 3, 3}, {64, 2, 1}, {12, 4, 4}};
+    const lcnn_pool_plan base = best;
+    for (const auto& r : rings) {
+      lcnn_pool_plan p = base;
+      p.ring_kb = r[0];
+      p.ring_slots = r[1];
+      p.ring_ctas = r[2];
+      consider(p);
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(src, s);
+  cudaFreeAsync(dst, s);
+  cudaGetLastError();
+  if (best.us <= 0.0f) return fail(LCNN_ECUDA, "pool_tune: no candidate launched");
+  best.tuned = 1;
+  {
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    g_plans[plan_key(n, c, h, w, layout, win_h, win_w, stride, mode)] = best;
+  }
+  *plan = best;
+  return ok();
+}
+
+lcnn_status lcnn_pool_run_plan(const float* src, float* dst, uint32_t n, uint32_t c, uint32_t h,
+                               uint32_t w, int layout, uint32_t win_h, uint32_t win_w,
+                               uint32_t stride, int mode, const lcnn_pool_plan* plan,
+                               lcnn_access_report* report, void* stream) {
+  uint32_t ho = 0, wo = 0;
+  lcnn_status st = pool_common(src, dst, n, c, h, w, win_h, win_w, stride, mode, &ho, &wo);
+  if (st != LCNN_OK) return st;
+  if (layout != LCNN_CHWN && layout != LCNN_NCHW)
+    return fail(LCNN_ELAYOUT, "pool_layout: only CHWN and NCHW kernels exist");
+  if (!plan) return fail(LCNN_EINVAL, "pool_plan: null plan pointer");
+  if (plan->fh < 1 || plan->fw < 1) return fail(LCNN_EPLAN, "pool_coarsened: factors must be >= 1");
+  if (uint64_t{plan->fh} * plan->fw > 64)
+    return fail(LCNN_EPLAN, "pool_coarsened: fh*fw exceeds accumulator cap of 64");
+  const lcnn_impl::PoolArgs a =
+      plan_args(src, dst, n, c, h, w, ho, wo, win_h, win_w, stride, mode, *plan);
+  cudaError_t e = launch_plan(a, layout, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pool_run_plan");
+  coarsened_report(report, n, c, ho, wo, win_h, win_w, stride, plan->fh, plan->fw);
+  return ok();
+}
+
 lcnn_status lcnn_pool_layout(const float* src, float* dst, uint32_t n, uint32_t c, uint32_t h,
                              uint32_t w, int layout, uint32_t win_h, uint32_t win_w,
                              uint32_t stride, int mode, lcnn_access_report* report,
@@ -216,23 +405,15 @@ lcnn_status lcnn_pool_layout(const float* src, float* dst, uint32_t n, uint32_t 
   if (st != LCNN_OK) return st;
   if (layout != LCNN_CHWN && layout != LCNN_NCHW)
     return fail(LCNN_ELAYOUT, "pool_layout: only CHWN and NCHW kernels exist");
-  // NCHW: the pipelined kernel's measured output block (scripts/pool_plans.py on B200,
-  // profiles/r01_pool_plans_nchw*.txt: 3x3/s2 -> 3x2 (PL5 3883 -> 5936 GB/s); 2x2/s2 ->
-  // 2x2 on >= 200-wide planes, 4x1 >= 100, 2x1 >= 20, else 1x2);
-  // every output keeps its tap order, so the bits equal the plain kernel's and
-  // the report stays the plain one
-  uint32_t fh = 1, fw = 1;
-  if (layout == LCNN_NCHW && win_h == win_w && stride == 2 && win_h == 3) {
-    fh = 3;
-    fw = 2;
-  } else if (layout == LCNN_NCHW && win_h == win_w && stride == 2 && win_h == 2) {
-    fh = w >= 200 ? 2 : w >= 100 ? 4 : w >= 20 ? 2 : 1;
-    fw = w >= 200 ? 2 : w >= 20 ? 1 : 2;
-  }
-  lcnn_impl::PoolArgs a{src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
-                        mode == LCNN_POOL_AVG, fh, fw};
-  cudaError_t e = layout == LCNN_CHWN ? lcnn_impl::launch_pool_chwn(a, S(stream))
-                                      : lcnn_impl::launch_pool_nchw(a, S(stream));
+  // the tuned plan of this shape if lcnn_pool_tune has measured it, else the
+  // static default.  Every output keeps its tap order under any plan, so the
+  // bits equal the plain kernel's and the report stays the plain one.
+  lcnn_pool_plan p;
+  st = lcnn_pool_plan_lookup(n, c, h, w, layout, win_h, win_w, stride, mode, &p);
+  if (st != LCNN_OK) return st;
+  const lcnn_impl::PoolArgs a = plan_args(src, dst, n, c, h, w, ho, wo, win_h, win_w, stride,
+                                          mode, p);
+  cudaError_t e = launch_plan(a, layout, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pool_layout");
   plain_report(report, n, c, ho, wo, win_h, win_w, stride);
   return ok();

@@ -26,6 +26,9 @@ struct PoolArgs {
   uint32_t win_h, win_w, stride;
   bool avg;
   uint32_t fh, fw;          // coarsening factors (1,1 = plain kernel)
+  // NCHW pipelined kernel's shared-memory ring: KB per slot, slots per CTA,
+  // CTAs per SM (0 = the measured default for the shape)
+  uint32_t ring_kb = 0, ring_slots = 0, ring_ctas = 0;
 };
 cudaError_t launch_pool_chwn(const PoolArgs& a, cudaStream_t s);
 cudaError_t launch_pool_nchw(const PoolArgs& a, cudaStream_t s);

@@ -697,8 +697,14 @@ cudaError_t launch_pool_nchw_pipe(const PoolArgs& a, cudaStream_t st) {
     return v;
   }();
   const bool whole = plane_bytes + 16 <= 48 * 1024;
-  const uint32_t cfg[3] = {knob[0] ? knob[0] : (whole ? 48u : 24u), knob[0] ? knob[1] : 2u,
-                           knob[0] ? knob[2] : (whole ? 2u : 4u)};
+  uint32_t cfg[3] = {knob[0] ? knob[0] : (whole ? 48u : 24u), knob[0] ? knob[1] : 2u,
+                     knob[0] ? knob[2] : (whole ? 2u : 4u)};
+  if (a.ring_kb) {  // a tuned ring (lcnn_pool_tune)
+    if (a.ring_slots < 2 || a.ring_slots > kPipeMax || !a.ring_ctas) return cudaErrorNotSupported;
+    cfg[0] = a.ring_kb;
+    cfg[1] = a.ring_slots;
+    cfg[2] = a.ring_ctas;
+  }
   const uint64_t kSlot = uint64_t{cfg[0]} * 1024;
   if (static_cast<uint64_t>(a.win_h) * row_bytes + 16 > kSlot) return cudaErrorNotSupported;
   if (planes > 0xffffffffull) return cudaErrorNotSupported;

@@ -100,6 +100,14 @@ int lcnn_net_create(const char* json, uint32_t c_t, uint32_t n_t, uint64_t seed,
 
 int lcnn_net_precision(const lcnn_net* net) { return net->net->precision(); }
 
+int lcnn_net_pool_plan(const lcnn_net* net, uint32_t layer, lcnn_pool_plan* plan) {
+  NET_GUARD({
+    if (!plan) throw lcnn::ValidationError("null plan pointer");
+    if (layer >= net->net->spec().layers.size()) throw lcnn::ValidationError("layer out of range");
+    *plan = net->net->pool_plan(layer);
+  })
+}
+
 const int* lcnn_net_nonfinite_flag(const lcnn_net* net) { return net->net->nonfinite_flag(); }
 
 int lcnn_net_status(const lcnn_net* net, void* stream) {

@@ -146,6 +146,27 @@ std::pair<DeviceTensor4D, AccessReport> pool_coarsened(const DeviceTensor4D& in,
   return {std::move(out), to_report(r)};
 }
 
+lcnn_pool_plan tune_pool_plan(std::uint32_t n, std::uint32_t c, std::uint32_t h,
+                              std::uint32_t w, Layout layout, const PoolParams& p) {
+  checked_extents(h, w, p);
+  lcnn_pool_plan plan{};
+  check_status(lcnn_pool_tune(n, c, h, w, code(layout), p.win_h, p.win_w, p.stride, mode_code(p),
+                              &plan, current_stream()));
+  return plan;
+}
+
+std::pair<DeviceTensor4D, AccessReport> pool_run_plan(const DeviceTensor4D& in,
+                                                      const PoolParams& p,
+                                                      const lcnn_pool_plan& plan) {
+  const auto [ho, wo] = checked_extents(in.h(), in.w(), p);
+  DeviceTensor4D out(in.n(), in.c(), ho, wo, in.layout());
+  lcnn_access_report r{};
+  check_status(lcnn_pool_run_plan(in.data(), out.data(), in.n(), in.c(), in.h(), in.w(),
+                                  code(in.layout()), p.win_h, p.win_w, p.stride, mode_code(p),
+                                  &plan, &r, current_stream()));
+  return {std::move(out), to_report(r)};
+}
+
 Tensor4D pool_oracle(const Tensor4D& in, const PoolParams& p) {
   const auto [ho, wo] = checked_extents(in.h(), in.w(), p);
   const DeviceTensor4D d = DeviceTensor4D::upload(in);

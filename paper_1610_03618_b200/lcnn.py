@@ -257,6 +257,32 @@ def pool_coarsened_nchw(t: DeviceTensor4D, p: PoolParams, plan: CoarseningPlan, 
     return o, rep
 
 
+def pool_tune(n, c, h, w, layout, p: PoolParams, stream=None) -> "capi.PoolPlan":
+    """GPU autotuner (lcnn_pool_tune): measure the layout's kernel plans for
+    this shape, cache and return the fastest.  Afterwards pool_layout on the
+    shape runs the tuned plan."""
+    plan = capi.PoolPlan()
+    capi.call("lcnn_pool_tune", n, c, h, w, layout, p.win_h, p.win_w, p.stride, p.mode,
+              ctypes.byref(plan), _stream(stream))
+    return plan
+
+
+def pool_plan_lookup(n, c, h, w, layout, p: PoolParams) -> "capi.PoolPlan":
+    plan = capi.PoolPlan()
+    capi.call("lcnn_pool_plan_lookup", n, c, h, w, layout, p.win_h, p.win_w, p.stride, p.mode,
+              ctypes.byref(plan))
+    return plan
+
+
+def pool_run_plan(t: DeviceTensor4D, p: PoolParams, plan, out=None, stream=None):
+    """Pool with an explicit kernel plan (either layout) -> (output, AccessReport)."""
+    o = _pool_out(t, p, t.layout, out)
+    rep = AccessReport()
+    capi.call("lcnn_pool_run_plan", t.ptr(), o.ptr(), t.n, t.c, t.h, t.w, t.layout, p.win_h,
+              p.win_w, p.stride, p.mode, ctypes.byref(plan), ctypes.byref(rep), _stream(stream))
+    return o, rep
+
+
 def pool_oracle(t: DeviceTensor4D, p: PoolParams, out=None, stream=None):
     """== pool_oracle (pool.cpp:49-84): fp64, NCHW out."""
     o = _pool_out(t, p, NCHW, out)

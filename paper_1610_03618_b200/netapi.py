@@ -7,7 +7,7 @@ import ctypes
 import os
 from ctypes import POINTER, c_char_p, c_int, c_uint32, c_uint64, c_void_p
 
-from .capi import PKG_DIR
+from .capi import PKG_DIR, PoolPlan
 from .errors import raise_for_status
 
 LIB = os.path.join(PKG_DIR, "lib", "liblcnn.so")
@@ -24,6 +24,7 @@ def lib():
         d.lcnn_net_create_ex.argtypes = [c_char_p, c_uint32, c_uint32, c_uint64, c_int,
                                          POINTER(c_void_p)]
         d.lcnn_net_precision.argtypes = [c_void_p]
+        d.lcnn_net_pool_plan.argtypes = [c_void_p, c_uint32, POINTER(PoolPlan)]
         d.lcnn_net_status.argtypes = [c_void_p, c_void_p]
         d.lcnn_net_nonfinite_flag.argtypes = [c_void_p]
         d.lcnn_net_nonfinite_flag.restype = c_void_p
@@ -80,6 +81,15 @@ class Network:
 
     def forward(self, d_input: int, in_layout: int, d_output: int, stream: int):
         _check(lib().lcnn_net_forward(self._h, d_input, in_layout, d_output, stream))
+
+    def pool_plans(self):
+        """{layer index: PoolPlan} of the network's pooling layers (tuned at creation)."""
+        out = {}
+        for i in range(len(self.layouts)):
+            p = PoolPlan()
+            if lib().lcnn_net_pool_plan(self._h, i, ctypes.byref(p)) == 0 and p.tuned:
+                out[i] = p
+        return out
 
     def status(self, stream: int):
         """Wait for `stream`; raise DomainError if a forward since the last
