@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import CHWN, NCHW, NHWC, C, approx_equal, bit_equal, rng_uniform
-from paper_1610_03618_b200 import errors, lcnn
+from paper_1610_03618_b200 import capi, errors, lcnn
 
 pytestmark = pytest.mark.gpu
 
@@ -194,3 +194,38 @@ def test_window_equals_image_and_generic_windows(cuda):
                 want, _ = C.pool_plain(x, n, c, h, w, layout, wh, ww, s, avg)
                 got, _ = lcnn.pool_layout(t, P(wh, ww, s, avg))
                 assert bit_equal(got.to_host(), want), (h, w, wh, ww, s, layout, avg)
+
+
+def test_pool_tuner_plans_are_cached_and_bit_exact(cuda):
+    """lcnn_pool_tune measures the layout's kernel plans on the shape, caches
+    the fastest (lookup returns it, pool_layout then runs it), and any plan it
+    can return gives the plain kernel's bits (PAPER.md:227 autotuning;
+    pool.cpp:272-331 is the reference's hill climb over the same space)."""
+    for layout, (n, c, h, win, s) in ((CHWN, (64, 32, 56, 2, 2)), (NCHW, (16, 24, 55, 3, 2)),
+                                      (NCHW, (8, 16, 112, 2, 2)), (CHWN, (32, 16, 27, 3, 2))):
+        p = P(win, win, s, False)
+        plan = lcnn.pool_tune(n, c, h, h, layout, p)
+        assert plan.tuned == 1 and plan.us > 0 and 1 <= plan.fh <= 4 and 1 <= plan.fw <= 4
+        again = lcnn.pool_plan_lookup(n, c, h, h, layout, p)
+        assert again.as_tuple() == plan.as_tuple() and again.tuned == 1
+        x = rng_uniform(h + c, n * c * h * h)
+        t = dev(x, (n, c, h, h), layout, cuda)
+        want, _ = C.pool_plain(x, n, c, h, h, layout, win, win, s, False)
+        got, rep = lcnn.pool_layout(t, p)  # runs the cached plan
+        assert bit_equal(got.to_host(), want), (layout, n, c, h, plan)
+        got, rep = lcnn.pool_run_plan(t, p, plan)
+        assert bit_equal(got.to_host(), want)
+        # every explicit plan of the search space, including NCHW ring shapes
+        for fh in (1, 2, 3, 4):
+            for fw in ((1, 2) if layout == NCHW else (1, 2, 3, 4)):
+                q = capi.PoolPlan(fh, fw, 0, 0, 0, 0, 0.0)
+                got, _ = lcnn.pool_run_plan(t, p, q)
+                assert bit_equal(got.to_host(), want), (layout, fh, fw)
+        if layout == NCHW:
+            for ring in ((48, 2, 2), (24, 2, 4), (16, 3, 4), (12, 4, 4)):
+                q = capi.PoolPlan(plan.fh, plan.fw, *ring, 0, 0.0)
+                try:
+                    got, _ = lcnn.pool_run_plan(t, p, q)
+                except Exception:
+                    continue  # a ring too small for this shape's rows is refused
+                assert bit_equal(got.to_host(), want), (layout, ring)
