@@ -216,11 +216,16 @@ class SoftmaxOp(Op):
 
     def bind(self, x_ptr, y_ptr):
         if self.fused:
-            return self.lib.lcnn_softmax_fused, (x_ptr, y_ptr, self.rows, self.cols, 16384,
-                                                 self.flag.data_ptr(), None)
+            # the classifier form the network executor runs: one kernel per
+            # step, the non-finite test ORed into a device flag that is never
+            # re-zeroed (lcnn_softmax_fused zeroes its flag with an extra launch)
+            return self.lib.lcnn_softmax_fused_sticky, (x_ptr, y_ptr, self.rows, self.cols,
+                                                        self.flag.data_ptr())
+        # the five-kernel baseline exactly (max, subtract, exp, sum, scale): no
+        # flag, so no zeroing launch is charged to it either
         return self.lib.lcnn_softmax_reference, (x_ptr, y_ptr, self.rows, self.cols,
                                                  self.scratch.data_ptr(), self.scratch.numel() * 4,
-                                                 self.flag.data_ptr(), None)
+                                                 None, None)
 
     def ref_session(self, batch, threads):
         from oracle.oracle import OP_SOFTMAX_FUSED, OP_SOFTMAX_REFERENCE, Ref
@@ -762,6 +767,10 @@ NETWORKS = {
     "alexnet": (os.path.join(ROOT, "configs", "alexnet.json"),
                 "BASELINE config 5: whole AlexNet forward (conv/pool/fc/softmax chain of SURVEY "
                 "8d), 128 images per GPU"),
+    "alexnet_mixed": (os.path.join(ROOT, "configs", "alexnet_mixed.json"),
+                      "BASELINE config 5 with the paper's mixed per-layer assignment "
+                      "(test_net.cpp:186-209: conv2, conv4, conv5 NCHW, the rest CHWN; 4 "
+                      "inserted transforms), 128 images per GPU"),
     "vgg16": (os.path.join(ROOT, "configs", "vgg16.json"),
               "whole VGG-16 forward (13 conv 3x3, 5 max pools, 3 fc, softmax), 128 images per "
               "GPU (the AlexNet/VGG forward of the north star)"),
@@ -838,7 +847,8 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
     in_layout = info["first_layout"]
     rows, cols = info["out"]
     g = torch.Generator(device=device).manual_seed(7 + rank)
-    x = torch.rand(batch * 3 * 227 * 227, device=device, generator=g) * 2 - 1
+    dn, dc, dh, dw = info["dims"]
+    x = torch.rand(dn * dc * dh * dw, device=device, generator=g) * 2 - 1
     y = torch.empty(rows * cols, device=device)
     stream = torch.cuda.current_stream(device)
     sh = stream.cuda_stream

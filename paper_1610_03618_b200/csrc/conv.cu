@@ -1834,12 +1834,36 @@ struct ConvRoute {
   TcPlan p;
   uint64_t apack = 0;  // floats of one packed filter image
   uint32_t kp = 0;     // NCHW: K padded to the k-block
+  // NCHW layer run as transpose -> the CHWN route `kind` -> transpose back
+  // (the run workspace then also holds the CHWN input and output copies)
+  bool via_chwn = false;
 };
 
 uint64_t align_floats(uint64_t f) { return (f + 63) / 64 * 64; }  // 256 B
 
 ConvRoute route_conv(const ConvArgs& a) {
   ConvRoute r;
+  // NCHW on the tensor cores: NCHW rows of odd width cannot be TMA tensors,
+  // and the gather-producer kernel below reaches ~50 TF/s, so an NCHW layer
+  // is run as NCHW->CHWN transpose (6+ TB/s), the CHWN route of the same
+  // geometry, and CHWN->NCHW transpose of the output: AlexNet conv2 in NCHW
+  // ~1.7 ms -> ~0.16 ms.  Profiling knob LCNN_CONV_NCHW=gather keeps the
+  // gather kernel.
+  static const bool nchw_gather = [] {
+    const char* e = std::getenv("LCNN_CONV_NCHW");
+    return e && e[0] == 'g';
+  }();
+  if (a.layout == LCNN_NCHW && a.precision != LCNN_PREC_FP32 && !nchw_gather &&
+      static_cast<uint64_t>(a.n) * a.ci * a.h * a.w < (1ull << 32) &&
+      static_cast<uint64_t>(a.n) * a.co * a.ho * a.wo < (1ull << 32)) {
+    ConvArgs c = a;
+    c.layout = LCNN_CHWN;
+    ConvRoute inner = route_conv(c);
+    if (inner.kind != kRouteSimt) {
+      inner.via_chwn = true;
+      return inner;
+    }
+  }
   if (a.layout == LCNN_NCHW && a.precision == LCNN_PREC_TF32 &&
       static_cast<uint64_t>(a.n) * a.ho * a.wo < (1ull << 31)) {
     r.kind = kRouteNchwTc;
@@ -1975,8 +1999,10 @@ size_t packed_bytes(const ConvArgs& a, const ConvRoute& r) {
 }
 
 size_t run_bytes(const ConvArgs& a, const ConvRoute& r) {
-  if (!split_input(a, r)) return 0;
-  return 2 * align_floats(static_cast<uint64_t>(a.n) * a.ci * a.h * a.w) * 4;
+  const uint64_t nx = align_floats(static_cast<uint64_t>(a.n) * a.ci * a.h * a.w);
+  const uint64_t ny = align_floats(static_cast<uint64_t>(a.n) * a.co * a.ho * a.wo);
+  // [x_hi | x_lo] (3xTF32 split input), then for via-CHWN [x_chwn | y_chwn]
+  return ((split_input(a, r) ? 2 * nx : 0) + (r.via_chwn ? nx + ny : 0)) * 4;
 }
 
 }  // namespace
@@ -1985,7 +2011,7 @@ size_t conv_packed_bytes(const ConvArgs& a) { return packed_bytes(a, route_conv(
 
 size_t conv_workspace_bytes(const ConvArgs& a) {
   const ConvRoute r = route_conv(a);
-  return packed_bytes(a, r) + run_bytes(a, r) + 256;
+  return packed_bytes(a, r) + run_bytes(a, r) + 512;
 }
 
 cudaError_t launch_conv_pack(const ConvArgs& a, void* packed, cudaStream_t s) {
@@ -2035,6 +2061,26 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
     return cudaGetLastError();
   }
   if (r.kind == kRouteNchwTc) return launch_conv_nchw_tc(a, w_hi, r.kp, s);
+  if (r.via_chwn) {
+    // workspace: [inner run bytes | x_chwn | y_chwn]; NCHW [N][CHW] is the
+    // transpose of CHWN [CHW][N]
+    ConvArgs b = a;
+    b.layout = LCNN_CHWN;
+    ConvRoute inner = r;
+    inner.via_chwn = false;
+    uint8_t* ws = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(a.workspace) + 255) & ~uintptr_t(255));
+    float* xc = reinterpret_cast<float*>(ws + run_bytes(b, inner));
+    float* yc = xc + align_floats(static_cast<uint64_t>(a.n) * a.ci * a.h * a.w);
+    cudaError_t e = launch_transpose2d(a.src, xc, a.n, static_cast<uint64_t>(a.ci) * a.h * a.w, s);
+    if (e != cudaSuccess) return e;
+    b.src = xc;
+    b.dst = yc;
+    b.workspace = ws;
+    e = launch_conv_packed(b, packed, s);
+    if (e != cudaSuccess) return e;
+    return launch_transpose2d(yc, a.dst, static_cast<uint64_t>(a.co) * a.ho * a.wo, a.n, s);
+  }
   const float* x_hi = a.src;
   const float* x_lo = a.src;
   if (split_input(a, r)) {

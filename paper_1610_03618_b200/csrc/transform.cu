@@ -132,6 +132,103 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Transpose with one short side (S = min(R, C) <= 16, the small batches of an
+// N-sharded run: CHWN [CHW][N] with N = 256/G).  The 32-edge tiles above
+// would be mostly empty (N = 8: 3/4 of every tile) with scalar side
+// accesses.  Here a CTA owns a run of B = kSmallChunk / S long-side indices;
+// both the read and the write of that run are S contiguous segments (or one
+// contiguous block), moved with 128-bit accesses when aligned:
+//   SMALL_C (C = S): src rows [l0, l0+B) are one block of B*S floats; dst
+//                     holds S runs dst[c*R + l0 .. +B)
+//   !SMALL_C (R = S): src holds S runs src[r*C + l0 .. +B); dst columns
+//                     [l0, l0+B) are one block of B*S floats.
+// Shared memory holds the run as [s][B + 1] (odd pitch for the transposed side).
+constexpr int kSmallChunk = 4096;  // floats per CTA (16 KB in + 16 KB out)
+
+template <bool SMALL_C, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    transpose_small_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                           uint32_t R, uint32_t C, uint32_t S, uint32_t B) {
+  LCNN_PDL_ENTRY();
+  extern __shared__ float sm[];
+  const uint32_t P = B + 1;
+  const uint32_t L = SMALL_C ? R : C;  // long side
+  const uint32_t l0 = blockIdx.x * B;
+  const uint32_t nb = min(B, L - l0);  // long-side indices in this run
+  const uint32_t blk = nb * S;         // floats of the contiguous block
+  // 1) the contiguous side -> smem[s][l]
+  const float* blk_src = SMALL_C ? src + static_cast<uint64_t>(l0) * S : nullptr;
+  if constexpr (SMALL_C) {
+    if (VEC) {
+      for (uint32_t i = threadIdx.x; i < blk / 4; i += kThreads) {
+        const float4 q = ldg_stream(reinterpret_cast<const float4*>(blk_src) + i);
+        const float e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t f = 4 * i + j, l = f / S, c = f - l * S;
+          sm[c * P + l] = e[j];
+        }
+      }
+    } else {
+      for (uint32_t f = threadIdx.x; f < blk; f += kThreads) {
+        const uint32_t l = f / S, c = f - l * S;
+        sm[c * P + l] = __ldg(blk_src + f);
+      }
+    }
+  } else {
+    // S runs of nb floats each: src[r*C + l0 ..]
+    for (uint32_t r = 0; r < S; ++r) {
+      const float* run = src + static_cast<uint64_t>(r) * C + l0;
+      if (VEC) {
+        for (uint32_t i = threadIdx.x; i < nb / 4; i += kThreads) {
+          const float4 q = ldg_stream(reinterpret_cast<const float4*>(run) + i);
+          float* d = sm + r * P + 4 * i;
+          d[0] = q.x; d[1] = q.y; d[2] = q.z; d[3] = q.w;
+        }
+        for (uint32_t l = nb / 4 * 4 + threadIdx.x; l < nb; l += kThreads) sm[r * P + l] = __ldg(run + l);
+      } else {
+        for (uint32_t l = threadIdx.x; l < nb; l += kThreads) sm[r * P + l] = __ldg(run + l);
+      }
+    }
+  }
+  __syncthreads();
+  // 2) smem -> the other side
+  if constexpr (SMALL_C) {
+    // S runs of nb floats: dst[c*R + l0 ..]
+    for (uint32_t c = 0; c < S; ++c) {
+      float* run = dst + static_cast<uint64_t>(c) * R + l0;
+      if (VEC) {
+        for (uint32_t i = threadIdx.x; i < nb / 4; i += kThreads) {
+          const float* q = sm + c * P + 4 * i;
+          stg_stream(reinterpret_cast<float4*>(run) + i, make_float4(q[0], q[1], q[2], q[3]));
+        }
+        for (uint32_t l = nb / 4 * 4 + threadIdx.x; l < nb; l += kThreads) stg_stream(run + l, sm[c * P + l]);
+      } else {
+        for (uint32_t l = threadIdx.x; l < nb; l += kThreads) stg_stream(run + l, sm[c * P + l]);
+      }
+    }
+  } else {
+    // one block: dst[(l0 + l)*S + r]
+    float* blk_dst = dst + static_cast<uint64_t>(l0) * S;
+    if (VEC) {
+      for (uint32_t i = threadIdx.x; i < blk / 4; i += kThreads) {
+        float e[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t f = 4 * i + j, l = f / S, r = f - l * S;
+          e[j] = sm[r * P + l];
+        }
+        stg_stream(reinterpret_cast<float4*>(blk_dst) + i, make_float4(e[0], e[1], e[2], e[3]));
+      }
+    } else {
+      for (uint32_t f = threadIdx.x; f < blk; f += kThreads) {
+        const uint32_t l = f / S, r = f - l * S;
+        stg_stream(blk_dst + f, sm[r * P + l]);
+      }
+    }
+  }
+}
+
 // Generic permutation: one thread per destination element, source offset from
 // the logical (n,c,h,w) coordinates (layout.cpp:77-97 semantics).
 struct Dims4 {
@@ -196,6 +293,35 @@ cudaError_t launch_transpose2d(const float* src, float* dst, uint64_t rows,
   if (rows == 0 || cols == 0) return cudaSuccess;
   const uint32_t R = static_cast<uint32_t>(rows);
   const uint32_t C = static_cast<uint32_t>(cols);
+  // a 1 x L (or L x 1) transpose is a copy (N = 1 after sharding)
+  if (R == 1 || C == 1)
+    return cudaMemcpyAsync(dst, src, rows * cols * sizeof(float), cudaMemcpyDeviceToDevice, s);
+  const uint32_t S = R < C ? R : C;
+  if (S <= 16) {
+    const bool small_c = C <= R;
+    const uint32_t L = small_c ? R : C;
+    // run length: a multiple of 4 (128-bit accesses) with B * S ~ kSmallChunk
+    uint32_t B = (kSmallChunk / S) / 4 * 4;
+    if (B < 4) B = 4;
+    const uint64_t blocks = (L + B - 1) / B;
+    const uint32_t smem = S * (B + 1) * 4;
+    // 128-bit accesses: run starts l0*S (block side) and r*C / c*R (run
+    // side) must be 16-byte aligned
+    const bool vec = aligned16(src) && aligned16(dst) && (L % 4 == 0) && (S % 4 == 0 || (B * S) % 4 == 0);
+    auto launch_small = [&](auto kern) {
+      if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+      }
+      lcnn_pdl::launch(kern, static_cast<uint32_t>(blocks), kThreads, smem, s, src, dst, R, C, S, B);
+      return cudaGetLastError();
+    };
+    if (small_c)
+      return vec ? launch_small(transpose_small_kernel<true, true>)
+                 : launch_small(transpose_small_kernel<true, false>);
+    return vec ? launch_small(transpose_small_kernel<false, true>)
+               : launch_small(transpose_small_kernel<false, false>);
+  }
   // 128-bit accesses need every row start 16-byte aligned.
   const bool vld = (C % 4 == 0) && aligned16(src);
   const bool vst = (R % 4 == 0) && aligned16(dst);

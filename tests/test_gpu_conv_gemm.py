@@ -126,6 +126,35 @@ def test_conv_tapsn_forced_on_alexnet_shapes(cuda):
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("case", CASES[:11] + [(128, 96, 27, 27, 192, 5, 1, 2)])
+@pytest.mark.parametrize("precision", [0, 1])
+def test_conv_nchw_via_chwn(cuda, case, precision):
+    """NCHW on the tensor cores: NCHW->CHWN transpose, the CHWN route of the
+    geometry, CHWN->NCHW transpose of the output (one-shot and packed)."""
+    _check_conv(cuda, *case, NCHW, precision)
+
+
+def test_conv_nchw_gather_kernel_still_correct(cuda):
+    """The NCHW gather-producer kernel (LCNN_CONV_NCHW=gather, read once per
+    process: a subprocess) stays parity-green as the measured alternative."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, torch; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+        "import test_gpu_conv_gemm as t; from paper_1610_03618_b200 import lcnn;"
+        "d = torch.device('cuda:0');"
+        "[t._check_conv(d, *c, t.NCHW, lcnn.TF32) for c in ["
+        "(32, 96, 27, 27, 64, 5, 1, 2), (16, 3, 35, 35, 32, 11, 4, 0), (5, 3, 9, 9, 7, 3, 1, 1)]];"
+        "print('ok')")
+    env = dict(os.environ, LCNN_CONV_NCHW="gather")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("case", [(5, 3, 9, 9, 7, 3, 1, 1), (3, 4, 11, 11, 6, 5, 2, 2),
                                   (32, 8, 13, 13, 16, 3, 1, 1), (7, 2, 7, 7, 5, 1, 1, 0)])
 @pytest.mark.parametrize("precision", [0, 2])

@@ -135,6 +135,22 @@ def test_alexnet_forward_fullsize_vs_reference(cuda, precision):
         assert dlog <= 5e-3, dlog
 
 
+def test_alexnet_mixed_layouts_fullsize_vs_reference(cuda):
+    """The paper's mixed per-layer assignment (test_net.cpp:186-209 mapped onto
+    AlexNet: conv2/conv4/conv5 NCHW, 4 inserted transforms) at the benched
+    size, against the reference running the same explicit layouts."""
+    got, want = _slice_vs_reference(cuda, "alexnet_mixed.json", capi.PREC_TF32)
+    dlog = np.abs(np.log(got.astype(np.float64)) - np.log(want.astype(np.float64))).max()
+    assert dlog <= 5e-3, dlog
+    text = open(os.path.join(ROOT, "configs", "alexnet_mixed.json")).read()
+    net = netapi.Network(text, *bench.thresholds()[:2], seed=42, precision=capi.PREC_TF32)
+    assert net.info(CHWN)["transforms"] == 4
+    ref_layouts, steps = Ref.plan_network(text)
+    assert [p for p, _, _ in steps] == [2, 3, 5, 7]
+    assert net.layouts[:8] == ref_layouts[:8]
+    net.close()
+
+
 def test_vgg16_forward_fullsize_vs_reference(cuda):
     got, want = _slice_vs_reference(cuda, "vgg16.json", capi.PREC_TF32)
     dlog = np.abs(np.log(got.astype(np.float64)) - np.log(want.astype(np.float64))).max()

@@ -132,3 +132,23 @@ def test_offset_pointers_and_odd_sizes(cuda):
     t = lcnn.DeviceTensor4D(n, c, h, w, CHWN, buf[1:])
     out = lcnn.transform(t, NCHW)
     assert bit_equal(out.to_host(), C.transform(x[1:], n, c, h, w, CHWN, NCHW))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 12, 16, 17, 32])
+def test_small_batch_paths_bit_exact(cuda, n):
+    """The short-side transpose (N <= 16 after sharding: contiguous runs both
+    ways, 128-bit when aligned) and the N = 1 copy, both directions, on the
+    AlexNet/VGG activation shapes of config 3 and on odd extents."""
+    import torch
+
+    for (c, h, w) in ((96, 55, 55), (3, 227, 227), (64, 56, 56), (7, 5, 3), (256, 6, 6)):
+        x = rng_uniform(n * c + h, n * c * h * w)
+        for src, dst in ((NCHW, CHWN), (CHWN, NCHW)):
+            t = dev(x, (n, c, h, w), src, cuda)
+            got = lcnn.transform(t, dst).to_host()
+            assert bit_equal(got, C.transform(x, n, c, h, w, src, dst)), (n, c, h, w, src)
+        # unaligned (4-byte offset) source: the scalar side of the kernel
+        buf = torch.from_numpy(np.concatenate([np.zeros(1, np.float32), x])).to(cuda)
+        t = lcnn.DeviceTensor4D(n, c, h, w, CHWN, buf[1:])
+        got = lcnn.transform(t, NCHW).to_host()
+        assert bit_equal(got, C.transform(x, n, c, h, w, CHWN, NCHW)), (n, c, h, w, "unaligned")
