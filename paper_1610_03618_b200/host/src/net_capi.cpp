@@ -190,6 +190,9 @@ int lcnn_net_forward_host_many(const lcnn_net* net, const float* const* h_inputs
     cudaStream_t copy = nullptr;
     cudaEvent_t loaded[2] = {}, consumed[2] = {};
     ~Streams() {
+      // drain the copy stream before the input slots (declared earlier, so
+      // destroyed later) go back to the allocator -- also on an error exit
+      if (copy) cudaStreamSynchronize(copy);
       for (int b = 0; b < 2; ++b) {
         if (loaded[b]) cudaEventDestroy(loaded[b]);
         if (consumed[b]) cudaEventDestroy(consumed[b]);
@@ -205,14 +208,14 @@ int lcnn_net_forward_host_many(const lcnn_net* net, const float* const* h_inputs
     lcnn::set_current_stream(nullptr);
     const lcnn::NetworkSpec& s = net->net->spec();
     cudaStream_t st = static_cast<cudaStream_t>(lcnn::current_stream());
+    lcnn::DeviceTensor4D in[2] = {lcnn::DeviceTensor4D(s.n, s.c, s.h, s.w, L(in_layout)),
+                                  lcnn::DeviceTensor4D(s.n, s.c, s.h, s.w, L(in_layout))};
     Streams r;
     ck(cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b) {
       ck(cudaEventCreateWithFlags(&r.loaded[b], cudaEventDisableTiming));
       ck(cudaEventCreateWithFlags(&r.consumed[b], cudaEventDisableTiming));
     }
-    lcnn::DeviceTensor4D in[2] = {lcnn::DeviceTensor4D(s.n, s.c, s.h, s.w, L(in_layout)),
-                                  lcnn::DeviceTensor4D(s.n, s.c, s.h, s.w, L(in_layout))};
     // the slots were allocated on the compute stream: the copy stream waits
     // for that before its first write
     for (int b = 0; b < 2; ++b) {

@@ -4,8 +4,9 @@ Names, argument meaning and error behaviour follow
 /root/reference/proj/include/lcnn/{tensor,layout,pool,softmax,select}.hpp so
 the parity tests read like the reference's own tests.  Tensors live in HBM
 (PyTorch is used only to own device memory and streams); every op is one call
-into liblcnn_cuda.so on the current CUDA stream.  Host-buffer (end-to-end)
-calls go through :mod:`paper_1610_03618_b200.hostapi`.
+into liblcnn_cuda.so on the current CUDA stream.  Whole networks (parse,
+annotate, device-resident forward, host-buffer forwards) are in
+:mod:`paper_1610_03618_b200.netapi` over liblcnn.so (include/lcnn_net.h).
 """
 from __future__ import annotations
 
