@@ -33,8 +33,6 @@
 //                       normalise pass (input read twice).
 #include <float.h>
 
-#include <cstdlib>
-
 #include "common.cuh"
 #include "internal.h"
 
@@ -72,39 +70,10 @@ __device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsig
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
-__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
-                                                     unsigned long long c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
 __device__ __forceinline__ float ex2_sfu(float t) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
   return r;
-}
-// 2^t for a pair on the FMA pipe instead of the SFU (t <= 0): n = rint(t) by
-// the 1.5*2^23 magic add, f = t - n in [-0.5, 0.5], 2^f by a degree-5
-// minimax polynomial (2.4e-7 relative incl. fp32 Horner rounding, measured
-// against float64 over 2e5 points -- the same order as ex2.approx), 2^n
-// added into the exponent field.  t is clamped at -126 (e^-87: far below
-// what a sum of >= 1 can notice).
-__device__ __forceinline__ void ex2_poly2(float t0, float t1, float& e0, float& e1) {
-  const unsigned long long magic = f2_pack(12582912.0f, 12582912.0f);
-  const unsigned long long t = f2_pack(fmaxf(t0, -126.0f), fmaxf(t1, -126.0f));
-  const unsigned long long j = f2_add(t, magic);
-  const unsigned long long f = f2_sub(t, f2_sub(j, magic));
-  unsigned long long p = f2_pack(0.001327647129073739f, 0.001327647129073739f);
-  p = f2_fma(p, f, f2_pack(0.009675540961325169f, 0.009675540961325169f));
-  p = f2_fma(p, f, f2_pack(0.05550713092088699f, 0.05550713092088699f));
-  p = f2_fma(p, f, f2_pack(0.24022120237350464f, 0.24022120237350464f));
-  p = f2_fma(p, f, f2_pack(0.6931469440460205f, 0.6931469440460205f));
-  p = f2_fma(p, f, f2_pack(1.0000001192092896f, 1.0000001192092896f));
-  float p0, p1, j0, j1;
-  f2_unpack(p, p0, p1);
-  f2_unpack(j, j0, j1);
-  e0 = __int_as_float(__float_as_int(p0) + (__float_as_int(j0) << 23));
-  e1 = __int_as_float(__float_as_int(p1) + (__float_as_int(j1) << 23));
 }
 
 __device__ __forceinline__ void flag_nonfinite(int* flag, bool bad) {
@@ -138,7 +107,7 @@ __device__ __forceinline__ float group_sum(float v, unsigned mask) {
 // -FLT_MAX: neutral for the max, invisible to the min test, e^-inf = 0 in
 // the sum.  Non-finite detection: +inf -> max = inf, -inf -> min = -inf, NaN
 // -> the sum is NaN (fmaxf / fminf skip NaN, the exponential does not).
-template <int LPR, int VPL, bool VEC, int THREADS = kThreads, int POLY = 0>
+template <int LPR, int VPL, bool VEC, int THREADS = kThreads>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     softmax_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
                         uint32_t rows, uint32_t cols, int* flag) {
@@ -181,8 +150,10 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
   }
   const bool neg_inf = !(mn >= -FLT_MAX);
   m = group_max<LPR>(m, mask);
-  // pairs: t = (x - m) * log2e with FADD2 + FMUL2, e = 2^t on the SFU (or,
-  // every POLY-th pair, on the FMA pipe), sums kept as a pair
+  // pairs: t = (x - m) * log2e with FADD2 + FMUL2, e = 2^t on the SFU, sums
+  // kept as a pair.  (2^t on the FMA pipe for every 2nd / 4th pair -- a
+  // degree-5 polynomial -- measured slower on B200: 4096 x 1000 6.39 ->
+  // 6.45 / 6.47 us; the SFU is not what bounds this kernel.)
   const unsigned long long mm = f2_pack(m, m);
   const unsigned long long l2e = f2_pack(1.4426950408889634f, 1.4426950408889634f);
   unsigned long long s2 = 0ull;  // (+0.0f, +0.0f)
@@ -190,12 +161,8 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
   for (int k = 0; k < VPL / 2; ++k) {
     float t0, t1, e0, e1;
     f2_unpack(f2_mul(f2_sub(f2_pack(v[2 * k], v[2 * k + 1]), mm), l2e), t0, t1);
-    if (POLY > 0 && k % POLY == POLY - 1) {
-      ex2_poly2(t0, t1, e0, e1);
-    } else {
-      e0 = ex2_sfu(t0);
-      e1 = ex2_sfu(t1);
-    }
+    e0 = ex2_sfu(t0);
+    e1 = ex2_sfu(t1);
     v[2 * k] = e0;
     v[2 * k + 1] = e1;
     s2 = f2_add(s2, f2_pack(e0, e1));
@@ -436,40 +403,18 @@ using namespace lcnn_dev;
 
 namespace {
 
-// profiling knob LCNN_SOFTMAX_POLY=k (k in {2, 4}): every k-th value pair of
-// the register-resident kernels takes 2^t on the FMA pipe (ex2_poly2)
-// instead of the SFU; 0 / unset = SFU only
-int poly_knob() {
-  static const int k = [] {
-    const char* e = std::getenv("LCNN_SOFTMAX_POLY");
-    const int v = e ? std::atoi(e) : 0;
-    return v == 2 || v == 4 ? v : 0;
-  }();
-  return k;
-}
-
-template <int LPR, int VPL, int THREADS = kThreads, int POLY = 0>
-cudaError_t rows_launch_p(const float* src, float* dst, uint32_t rows, uint32_t cols, bool vec,
-                          int* flag, cudaStream_t st) {
-  constexpr int kGroups = THREADS / LPR;
-  const uint32_t blocks = (rows + kGroups - 1) / kGroups;
-  if (vec)
-    lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, true, THREADS, POLY>, blocks, THREADS, 0, st,
-                     src, dst, rows, cols, flag);
-  else
-    lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, false, THREADS, POLY>, blocks, THREADS, 0, st,
-                     src, dst, rows, cols, flag);
-  return cudaGetLastError();
-}
-
 template <int LPR, int VPL, int THREADS = kThreads>
 cudaError_t rows_launch(const float* src, float* dst, uint32_t rows, uint32_t cols, bool vec,
                         int* flag, cudaStream_t st) {
-  switch (poly_knob()) {
-    case 2: return rows_launch_p<LPR, VPL, THREADS, 2>(src, dst, rows, cols, vec, flag, st);
-    case 4: return rows_launch_p<LPR, VPL, THREADS, 4>(src, dst, rows, cols, vec, flag, st);
-    default: return rows_launch_p<LPR, VPL, THREADS, 0>(src, dst, rows, cols, vec, flag, st);
-  }
+  constexpr int kGroups = THREADS / LPR;
+  const uint32_t blocks = (rows + kGroups - 1) / kGroups;
+  if (vec)
+    lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, true, THREADS>, blocks, THREADS, 0, st, src,
+                     dst, rows, cols, flag);
+  else
+    lcnn_pdl::launch(softmax_rows_kernel<LPR, VPL, false, THREADS>, blocks, THREADS, 0, st, src,
+                     dst, rows, cols, flag);
+  return cudaGetLastError();
 }
 
 template <int VPL>
