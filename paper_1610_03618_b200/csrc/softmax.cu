@@ -107,8 +107,10 @@ __device__ __forceinline__ float group_sum(float v, unsigned mask) {
 // -FLT_MAX: neutral for the max, invisible to the min test, e^-inf = 0 in
 // the sum.  Non-finite detection: +inf -> max = inf, -inf -> min = -inf, NaN
 // -> the sum is NaN (fmaxf / fminf skip NaN, the exponential does not).
+// (VPL = 64, rows of up to 2048: 128 registers, 16 warps per SM -- at the
+// 64-register cap those 64 values spilled ~370 bytes per thread)
 template <int LPR, int VPL, bool VEC, int THREADS = kThreads>
-__global__ void __launch_bounds__(THREADS, 1024 / THREADS)
+__global__ void __launch_bounds__(THREADS, (VPL > 32 ? 512 : 1024) / THREADS)
     softmax_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
                         uint32_t rows, uint32_t cols, int* flag) {
   LCNN_PDL_ENTRY();
@@ -174,23 +176,22 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
   flag_nonfinite(flag, neg_inf || !(fabsf(m) <= FLT_MAX) || !(s == s));
   const float inv = 1.0f / s;
   const unsigned long long inv2 = f2_pack(inv, inv);
-  float o[VPL];
 #pragma unroll
   for (int k = 0; k < VPL / 2; ++k)
-    f2_unpack(f2_mul(f2_pack(v[2 * k], v[2 * k + 1]), inv2), o[2 * k], o[2 * k + 1]);
+    f2_unpack(f2_mul(f2_pack(v[2 * k], v[2 * k + 1]), inv2), v[2 * k], v[2 * k + 1]);
   if constexpr (VEC) {
 #pragma unroll
     for (int k = 0; k < VPL / 4; ++k) {
       const uint32_t col = (lane + k * LPR) * 4;
       if (col < cols)
         stg_stream(reinterpret_cast<float4*>(out + col),
-                   make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]));
+                   make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
     }
   } else {
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const uint32_t col = lane + k * LPR;
-      if (col < cols) stg_stream(out + col, o[k]);
+      if (col < cols) stg_stream(out + col, v[k]);
     }
   }
 }
