@@ -859,12 +859,14 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     K = args.steps
+    torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clocks:
         e0.record(stream)
         for _ in range(K):
             net.forward(x.data_ptr(), in_layout, y.data_ptr(), sh)
         e1.record(stream)
         torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     barrier()
     t = torch.tensor([e0.elapsed_time(e1)], device=device, dtype=torch.float64)
     if world > 1:
