@@ -554,11 +554,12 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
         best_s = S;
       }
     }
-    static const bool splitk = [] {
+    static const int splitk = [] {
       const char* e = std::getenv("LCNN_FC_SPLITK");
-      return !(e && e[0] == '0');  // profiling knob: 0 = always stream-K
+      // profiling knob: 0 = always stream-K, 2 = cluster split-K whenever it fits
+      return e ? (e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1)) : 1;
     }();
-    if (best_s >= 2 && splitk && sk_total < 8ull * sms) {
+    if (best_s >= 2 && splitk && (sk_total < 8ull * sms || splitk == 2)) {
       L.bn = best_bn;
       SplitK sk{};
       sk.mt = mt;

@@ -46,4 +46,14 @@ case $WHAT in
     ;;
 esac
 done
+# keep gpurun_out small (the pull limit is 64 MiB): text exports of every
+# report, the .ncu-rep files themselves only with KEEP_REP=1
+for r in gpurun_out/*.ncu-rep; do
+  [ -e "$r" ] || continue
+  ncu -i "$r" --page details --csv > "${r%.ncu-rep}.details.csv" 2>/dev/null
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  ncu -i "$r" --page source --csv > "${r%.ncu-rep}.source.csv" 2>/dev/null
+  [ "${KEEP_REP:-0}" = 1 ] || rm -f "$r"
+done
+du -sh gpurun_out
 echo done
