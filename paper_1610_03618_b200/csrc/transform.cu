@@ -20,6 +20,8 @@
 // When a row length is not a multiple of 4 floats (e.g. AlexNet's 3x227x227
 // input, or odd batches) the affected side falls back to scalar 32-bit
 // accesses, still one full 128-byte line per warp instruction.
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -145,28 +147,39 @@ __global__ void __launch_bounds__(kThreads)
 // Shared memory holds the run as [s][B + 1] (odd pitch for the transposed side).
 constexpr int kSmallChunk = 4096;  // floats per CTA (16 KB in + 16 KB out)
 
-template <bool SMALL_C, bool VEC>
+template <int S, bool SMALL_C, bool VEC>
 __global__ void __launch_bounds__(kThreads)
-    transpose_small_kernel(const float* __restrict__ src, float* __restrict__ dst,
-                           uint32_t R, uint32_t C, uint32_t S, uint32_t B) {
+    transpose_small_kernel(const float* __restrict__ src, float* __restrict__ dst, uint32_t R,
+                           uint32_t C) {
   LCNN_PDL_ENTRY();
-  extern __shared__ float sm[];
-  const uint32_t P = B + 1;
+  constexpr uint32_t B = (kSmallChunk / S) / 4 * 4;  // long-side indices per CTA
+  constexpr uint32_t P = B + 1;                       // smem pitch (odd)
+  __shared__ float sm[S * P];
   const uint32_t L = SMALL_C ? R : C;  // long side
   const uint32_t l0 = blockIdx.x * B;
   const uint32_t nb = min(B, L - l0);  // long-side indices in this run
   const uint32_t blk = nb * S;         // floats of the contiguous block
   // 1) the contiguous side -> smem[s][l]
-  const float* blk_src = SMALL_C ? src + static_cast<uint64_t>(l0) * S : nullptr;
   if constexpr (SMALL_C) {
-    if (VEC) {
-      for (uint32_t i = threadIdx.x; i < blk / 4; i += kThreads) {
-        const float4 q = ldg_stream(reinterpret_cast<const float4*>(blk_src) + i);
-        const float e[4] = {q.x, q.y, q.z, q.w};
+    const float* blk_src = src + static_cast<uint64_t>(l0) * S;
+    if constexpr (VEC) {
+      constexpr uint32_t kIt = (B * S / 4 + kThreads - 1) / kThreads;
+      float4 q[kIt];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t f = 4 * i + j, l = f / S, c = f - l * S;
-          sm[c * P + l] = e[j];
+      for (uint32_t it = 0; it < kIt; ++it) {
+        const uint32_t i = threadIdx.x + it * kThreads;
+        if (i < blk / 4) q[it] = ldg_stream(reinterpret_cast<const float4*>(blk_src) + i);
+      }
+#pragma unroll
+      for (uint32_t it = 0; it < kIt; ++it) {
+        const uint32_t i = threadIdx.x + it * kThreads;
+        if (i < blk / 4) {
+          const float e[4] = {q[it].x, q[it].y, q[it].z, q[it].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t f = 4 * i + j, l = f / S, c = f - l * S;
+            sm[c * P + l] = e[j];
+          }
         }
       }
     } else {
@@ -177,15 +190,15 @@ __global__ void __launch_bounds__(kThreads)
     }
   } else {
     // S runs of nb floats each: src[r*C + l0 ..]
+#pragma unroll
     for (uint32_t r = 0; r < S; ++r) {
       const float* run = src + static_cast<uint64_t>(r) * C + l0;
-      if (VEC) {
+      if constexpr (VEC) {
         for (uint32_t i = threadIdx.x; i < nb / 4; i += kThreads) {
           const float4 q = ldg_stream(reinterpret_cast<const float4*>(run) + i);
           float* d = sm + r * P + 4 * i;
           d[0] = q.x; d[1] = q.y; d[2] = q.z; d[3] = q.w;
         }
-        for (uint32_t l = nb / 4 * 4 + threadIdx.x; l < nb; l += kThreads) sm[r * P + l] = __ldg(run + l);
       } else {
         for (uint32_t l = threadIdx.x; l < nb; l += kThreads) sm[r * P + l] = __ldg(run + l);
       }
@@ -195,14 +208,14 @@ __global__ void __launch_bounds__(kThreads)
   // 2) smem -> the other side
   if constexpr (SMALL_C) {
     // S runs of nb floats: dst[c*R + l0 ..]
+#pragma unroll
     for (uint32_t c = 0; c < S; ++c) {
       float* run = dst + static_cast<uint64_t>(c) * R + l0;
-      if (VEC) {
+      if constexpr (VEC) {
         for (uint32_t i = threadIdx.x; i < nb / 4; i += kThreads) {
           const float* q = sm + c * P + 4 * i;
           stg_stream(reinterpret_cast<float4*>(run) + i, make_float4(q[0], q[1], q[2], q[3]));
         }
-        for (uint32_t l = nb / 4 * 4 + threadIdx.x; l < nb; l += kThreads) stg_stream(run + l, sm[c * P + l]);
       } else {
         for (uint32_t l = threadIdx.x; l < nb; l += kThreads) stg_stream(run + l, sm[c * P + l]);
       }
@@ -210,7 +223,7 @@ __global__ void __launch_bounds__(kThreads)
   } else {
     // one block: dst[(l0 + l)*S + r]
     float* blk_dst = dst + static_cast<uint64_t>(l0) * S;
-    if (VEC) {
+    if constexpr (VEC) {
       for (uint32_t i = threadIdx.x; i < blk / 4; i += kThreads) {
         float e[4];
 #pragma unroll
@@ -300,27 +313,31 @@ cudaError_t launch_transpose2d(const float* src, float* dst, uint64_t rows,
   if (S <= 16) {
     const bool small_c = C <= R;
     const uint32_t L = small_c ? R : C;
-    // run length: a multiple of 4 (128-bit accesses) with B * S ~ kSmallChunk
-    uint32_t B = (kSmallChunk / S) / 4 * 4;
-    if (B < 4) B = 4;
-    const uint64_t blocks = (L + B - 1) / B;
-    const uint32_t smem = S * (B + 1) * 4;
-    // 128-bit accesses: run starts l0*S (block side) and r*C / c*R (run
-    // side) must be 16-byte aligned
-    const bool vec = aligned16(src) && aligned16(dst) && (L % 4 == 0) && (S % 4 == 0 || (B * S) % 4 == 0);
-    auto launch_small = [&](auto kern) {
-      if (smem > 48 * 1024) {
-        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
+    // 128-bit accesses: the block start l0*S and the run starts r*C / c*R
+    // (with l0 a multiple of 4) are 16-byte aligned when L % 4 == 0
+    const bool vec = aligned16(src) && aligned16(dst) && (L % 4 == 0);
+    cudaError_t err = cudaErrorNotSupported;
+    auto go = [&](auto s_tag) {
+      constexpr int SS = decltype(s_tag)::value;
+      constexpr uint32_t B = (kSmallChunk / SS) / 4 * 4;
+      const uint32_t blocks = (L + B - 1) / B;
+      if (small_c) {
+        if (vec) lcnn_pdl::launch(transpose_small_kernel<SS, true, true>, blocks, kThreads, 0, s, src, dst, R, C);
+        else lcnn_pdl::launch(transpose_small_kernel<SS, true, false>, blocks, kThreads, 0, s, src, dst, R, C);
+      } else {
+        if (vec) lcnn_pdl::launch(transpose_small_kernel<SS, false, true>, blocks, kThreads, 0, s, src, dst, R, C);
+        else lcnn_pdl::launch(transpose_small_kernel<SS, false, false>, blocks, kThreads, 0, s, src, dst, R, C);
       }
-      lcnn_pdl::launch(kern, static_cast<uint32_t>(blocks), kThreads, smem, s, src, dst, R, C, S, B);
-      return cudaGetLastError();
+      err = cudaGetLastError();
     };
-    if (small_c)
-      return vec ? launch_small(transpose_small_kernel<true, true>)
-                 : launch_small(transpose_small_kernel<true, false>);
-    return vec ? launch_small(transpose_small_kernel<false, true>)
-               : launch_small(transpose_small_kernel<false, false>);
+    switch (S) {
+#define LCNN_S(k) case k: go(std::integral_constant<int, k>{}); break;
+      LCNN_S(2) LCNN_S(3) LCNN_S(4) LCNN_S(5) LCNN_S(6) LCNN_S(7) LCNN_S(8) LCNN_S(9)
+      LCNN_S(10) LCNN_S(11) LCNN_S(12) LCNN_S(13) LCNN_S(14) LCNN_S(15) LCNN_S(16)
+#undef LCNN_S
+      default: break;
+    }
+    return err;
   }
   // 128-bit accesses need every row start 16-byte aligned.
   const bool vld = (C % 4 == 0) && aligned16(src);

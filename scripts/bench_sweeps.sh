@@ -10,7 +10,7 @@ mkdir -p gpurun_out
 OUT=gpurun_out/sweeps.jsonl
 : > $OUT
 run() { timeout 900 python bench.py "$@" >> $OUT 2>> gpurun_out/sweeps.err; }
-for what in ${@:-softmax transform pl5 nets}; do
+for what in ${@:-softmax transform transform_small pl5 nets}; do
 case $what in
   softmax)
     for n in 128 256 512 1024 2048 4096; do
@@ -23,6 +23,12 @@ case $what in
     for n in 32 64 128 256; do
       run --workload transform_$n --steps 10
       run --workload transform_nchw_$n --steps 10
+    done
+    ;;
+  transform_small)
+    for n in 1 2 4 8 16; do
+      run --workload transform_$n --steps 20 --no-cpu-baseline
+      run --workload transform_nchw_$n --steps 20 --no-cpu-baseline
     done
     ;;
   pl5)
