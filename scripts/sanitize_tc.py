@@ -19,4 +19,7 @@ cases = [(64, 3, 35, 35, 96, 11, 4, 0),      # SHARE
          (128, 32, 92, 92, 64, 3, 1, 1)]     # TAPS
 for c in cases:
     t._check_conv(d, *c, t.CHWN, lcnn.TF32)
+# NCHW through the CHWN route (transpose, conv, transpose in the workspace)
+for c in [(32, 64, 13, 13, 96, 3, 1, 1), (64, 3, 35, 35, 96, 11, 4, 0)]:
+    t._check_conv(d, *c, t.NCHW, lcnn.TF32)
 print("ok")
