@@ -253,29 +253,71 @@ __global__ void __launch_bounds__(kThreads)
     stg_stream(dst + i, ldg_stream(src + i));
 }
 
-// Generic permutation: one thread per destination element, source offset from
-// the logical (n,c,h,w) coordinates (layout.cpp:77-97 semantics).
-struct Dims4 {
-  // destination extents in memory order (outermost first) and the source
-  // stride for each of those destination dimensions
-  uint32_t e1, e2, e3;  // extents of the three inner dst dims
-  FastDiv d1, d2, d3;
-  uint64_t s0, s1, s2, s3;  // source strides of dst dims 0..3
+// Generic permutation between any two of the four layouts (layout.cpp:77-97
+// semantics), as a batched 2-D problem.  Let a be the source's unit-stride
+// logical dim and b the destination's, i and j the other two:
+//   a != b : for every (i, j), dst[b-major] = transpose(src[a-major]) -- a
+//            32 x 32 tile through shared memory (pitch 33), reads coalesced
+//            along a, writes along b (NCHW<->NHWC, CHWN<->NHWC, ...);
+//   a == b : both sides share the innermost dim (CHWN<->HWCN: runs of N):
+//            contiguous runs copied with the outer three dims permuted.
+// Round 1 ran one thread per destination element with a strided source
+// gather (uncoalesced on one side).
+struct PermGeom {
+  uint32_t A, B;          // extents of a (src unit stride) and b (dst unit stride)
+  uint32_t I, J;          // extents of the other two dims
+  uint32_t tiles_a, tiles_b;
+  FastDiv div_tiles_a, div_J;
+  uint64_t sb, si, sj;    // source strides of b, i, j (a is 1)
+  uint64_t da, di, dj;    // destination strides of a, i, j (b is 1)
 };
 
 __global__ void __launch_bounds__(kThreads)
-    permute4d_kernel(const float* __restrict__ src, float* __restrict__ dst,
-                     uint64_t total, Dims4 d) {
+    permute_tile_kernel(const float* __restrict__ src, float* __restrict__ dst, PermGeom g) {
   LCNN_PDL_ENTRY();
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-       i < total; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    // total < 2^32 (Tensor4D caps element counts at UINT32_MAX)
-    uint32_t x = static_cast<uint32_t>(i), q3, q2, q1, i3, i2, i1;
-    d.d3.divmod(x, q3, i3);
-    d.d2.divmod(q3, q2, i2);
-    d.d1.divmod(q2, q1, i1);
-    const uint64_t so = q1 * d.s0 + i1 * d.s1 + i2 * d.s2 + i3 * d.s3;
-    dst[i] = __ldg(src + so);
+  __shared__ float tile[32][33];
+  const uint32_t tiles = g.tiles_a * g.tiles_b;
+  const uint64_t total = static_cast<uint64_t>(tiles) * g.I * g.J;
+  for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
+    const uint32_t ij = static_cast<uint32_t>(u / tiles);
+    const uint32_t t = static_cast<uint32_t>(u - static_cast<uint64_t>(ij) * tiles);
+    uint32_t tb, ta, i, j;
+    g.div_tiles_a.divmod(t, tb, ta);
+    g.div_J.divmod(ij, i, j);
+    const uint32_t a0 = ta * 32, b0 = tb * 32;
+    const uint64_t sbase = i * g.si + j * g.sj, dbase = i * g.di + j * g.dj;
+    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;  // 32 x 8 threads
+    __syncthreads();  // the previous unit's readers are done with the tile
+#pragma unroll
+    for (int r = 0; r < 32; r += 8) {
+      const uint32_t a = a0 + lx, b = b0 + ly + r;
+      if (a < g.A && b < g.B) tile[ly + r][lx] = __ldg(src + sbase + b * g.sb + a);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 32; r += 8) {
+      const uint32_t b = b0 + lx, a = a0 + ly + r;
+      if (a < g.A && b < g.B) stg_stream(dst + dbase + a * g.da + b, tile[lx][ly + r]);
+    }
+  }
+}
+
+// a == b: runs of A contiguous floats; outer dims (b, i, j) permuted.
+__global__ void __launch_bounds__(kThreads)
+    permute_runs_kernel(const float* __restrict__ src, float* __restrict__ dst, PermGeom g) {
+  LCNN_PDL_ENTRY();
+  // one warp per run; B here is the third outer dim (i, j, b)
+  const uint64_t runs = static_cast<uint64_t>(g.B) * g.I * g.J;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x) >> 5; w < runs;
+       w += (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5) {
+    const uint32_t ij = static_cast<uint32_t>(w / g.B);
+    const uint32_t b = static_cast<uint32_t>(w - static_cast<uint64_t>(ij) * g.B);
+    uint32_t i, j;
+    g.div_J.divmod(ij, i, j);
+    const float* s = src + b * g.sb + i * g.si + j * g.sj;
+    float* d = dst + b * g.da + i * g.di + j * g.dj;
+    for (uint32_t x = lane; x < g.A; x += 32) stg_stream(d + x, __ldg(s + x));
   }
 }
 
@@ -379,29 +421,60 @@ cudaError_t launch_permute4d(const float* src, float* dst, uint32_t n,
                                   {1, 2, 3, 0},   // CHWN
                                   {0, 2, 3, 1},   // NHWC
                                   {2, 3, 1, 0}};  // HWCN
-  uint64_t ss[4];  // source stride of each logical dim (layout_strides)
+  uint64_t ss[4], ds[4];  // source / destination stride of each logical dim
   uint64_t acc = 1;
   for (int k = 3; k >= 0; --k) {
     ss[order[src_layout][k]] = acc;
     acc *= ext[order[src_layout][k]];
   }
-  const int* od = order[dst_layout];
-  Dims4 d;
-  d.e1 = ext[od[1]];
-  d.e2 = ext[od[2]];
-  d.e3 = ext[od[3]];
-  d.d1 = FastDiv(d.e1);
-  d.d2 = FastDiv(d.e2);
-  d.d3 = FastDiv(d.e3);
-  d.s0 = ss[od[0]];
-  d.s1 = ss[od[1]];
-  d.s2 = ss[od[2]];
-  d.s3 = ss[od[3]];
+  acc = 1;
+  for (int k = 3; k >= 0; --k) {
+    ds[order[dst_layout][k]] = acc;
+    acc *= ext[order[dst_layout][k]];
+  }
   const uint64_t total = static_cast<uint64_t>(n) * c * h * w;
   if (total == 0) return cudaSuccess;
-  uint64_t blocks = (total + kThreads - 1) / kThreads;
-  if (blocks > 148ull * 64) blocks = 148ull * 64;
-  lcnn_pdl::launch(permute4d_kernel, static_cast<uint32_t>(blocks), kThreads, 0, s, src, dst, total, d);
+  const int a = order[src_layout][3], b = order[dst_layout][3];
+  int rest[3], nr = 0;
+  for (int d = 0; d < 4; ++d)
+    if (d != a && d != b) rest[nr++] = d;
+  PermGeom g{};
+  if (a != b) {
+    g.A = ext[a];
+    g.B = ext[b];
+    g.I = ext[rest[0]];
+    g.J = ext[rest[1]];
+    g.sb = ss[b];
+    g.si = ss[rest[0]];
+    g.sj = ss[rest[1]];
+    g.da = ds[a];
+    g.di = ds[rest[0]];
+    g.dj = ds[rest[1]];
+    g.tiles_a = (g.A + 31) / 32;
+    g.tiles_b = (g.B + 31) / 32;
+    g.div_tiles_a = FastDiv(g.tiles_a);
+    g.div_J = FastDiv(g.J);
+    const uint64_t units = static_cast<uint64_t>(g.tiles_a) * g.tiles_b * g.I * g.J;
+    const uint64_t blocks = units < 148ull * 32 ? units : 148ull * 32;
+    lcnn_pdl::launch(permute_tile_kernel, static_cast<uint32_t>(blocks), kThreads, 0, s, src, dst, g);
+    return cudaGetLastError();
+  }
+  // a == b: runs of ext[a]; the three outer dims are rest[0..2]
+  g.A = ext[a];
+  g.B = ext[rest[0]];
+  g.I = ext[rest[1]];
+  g.J = ext[rest[2]];
+  g.sb = ss[rest[0]];
+  g.si = ss[rest[1]];
+  g.sj = ss[rest[2]];
+  g.da = ds[rest[0]];
+  g.di = ds[rest[1]];
+  g.dj = ds[rest[2]];
+  g.div_J = FastDiv(g.J);
+  const uint64_t warps = static_cast<uint64_t>(g.B) * g.I * g.J;
+  uint64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  lcnn_pdl::launch(permute_runs_kernel, static_cast<uint32_t>(blocks), kThreads, 0, s, src, dst, g);
   return cudaGetLastError();
 }
 

@@ -152,3 +152,19 @@ def test_small_batch_paths_bit_exact(cuda, n):
         t = lcnn.DeviceTensor4D(n, c, h, w, CHWN, buf[1:])
         got = lcnn.transform(t, NCHW).to_host()
         assert bit_equal(got, C.transform(x, n, c, h, w, CHWN, NCHW)), (n, c, h, w, "unaligned")
+
+
+@pytest.mark.parametrize("dims", [(8, 96, 27, 27), (33, 5, 7, 41), (1, 3, 224, 224), (64, 64, 14, 14)])
+def test_all_layout_pairs_bit_exact(cuda, dims):
+    """transform_naive (layout.cpp:77-97) for all 12 ordered pairs of the four
+    layouts: the tiled batched-transpose kernel (innermost dims differ) and
+    the run-copy kernel (CHWN<->HWCN share N innermost), against the oracle."""
+    n, c, h, w = dims
+    x = rng_uniform(sum(dims), n * c * h * w)
+    for src in (NCHW, CHWN, NHWC, HWCN):
+        t = dev(x, dims, src, cuda)
+        for dst in (NCHW, CHWN, NHWC, HWCN):
+            if dst == src:
+                continue
+            got = lcnn.transform_naive(t, dst).to_host()
+            assert bit_equal(got, C.transform(x, n, c, h, w, src, dst)), (dims, src, dst)
