@@ -560,15 +560,20 @@ def main():
     import torch
     import torch.distributed as dist
 
-    if torch.cuda.device_count() < world:
-        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, "
-                         f"{torch.cuda.device_count()} visible")
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    count = torch.cuda.device_count()
+    if count == 0:
+        raise SystemExit("bench.py: no CUDA device visible")
+    # one GPU per rank: LOCAL_RANK indexes the visible devices (a launcher
+    # that masks each rank to one device leaves index 0)
+    dev_index = local if local < count else local % count
+    if world > count and count > 1:
+        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, {count} visible")
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
         dist.barrier()  # creates the communicator
-        print(f"bench.py: rank {rank}/{world} NCCL communicator up on cuda:{local} "
+        print(f"bench.py: rank {rank}/{world} NCCL communicator up on cuda:{dev_index} "
               f"(nranks={dist.get_world_size()})", file=sys.stderr, flush=True)
 
     def barrier():
