@@ -195,3 +195,27 @@ def test_precision_is_per_network(cuda):
     assert torch.allclose(got[capi.PREC_TF32], want[capi.PREC_TF32], rtol=1e-4, atol=1e-7)
     for net in nets.values():
         net.close()
+
+
+def test_network_runs_tuned_pool_plans(cuda):
+    """Every pooling layer of a Network is tuned at creation (lcnn_pool_tune;
+    lcnn_net_pool_plan reports it) and the forward that runs those plans
+    still matches the reference run_network (pool.cpp tap order is kept)."""
+    import torch
+
+    text = json.dumps(MINI)
+    net = netapi.Network(text, 257, 32, seed=42, precision=capi.PREC_FP32)
+    plans = net.pool_plans()
+    pool_layers = [i for i, L in enumerate(MINI["layers"]) if L["kind"] == "pool"]
+    assert sorted(plans) == pool_layers and all(p.tuned == 1 for p in plans.values())
+    info = net.info(NCHW)
+    rows, cols = info["out"]
+    n, c, h, w = info["dims"]
+    x = rng_uniform(21, n * c * h * w)
+    dy = torch.empty(rows * cols, device=cuda)
+    net.forward(torch.from_numpy(x).to(cuda).data_ptr(), NCHW, dy.data_ptr(),
+                torch.cuda.current_stream(cuda).cuda_stream)
+    torch.cuda.synchronize()
+    want = Ref.run_network(text, x, NCHW, 257, 32, seed=42)
+    assert approx_equal(dy.cpu().numpy().reshape(rows, cols), want, 1e-5)
+    net.close()
