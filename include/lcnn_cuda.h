@@ -287,6 +287,30 @@ lcnn_status lcnn_conv_forward_packed(const float* src, const void* d_packed,
                                      int precision, void* d_workspace,
                                      size_t workspace_bytes, void* stream);
 
+/* Convolution followed by max pooling as ONE kernel (the run_network layer
+ * pair conv -> pool, net.cpp:284-353, when the pool consumes the conv output
+ * in the same layout): the conv output never reaches HBM.  Supported for
+ * CHWN, TF32, layers the SHARE route takes (small c_i * f_w, c_o <= 128,
+ * e.g. AlexNet conv1) and square max windows of 2 or 3 at stride 2.
+ * d_packed is the layer's lcnn_conv_pack_filters image (same geometry and
+ * precision); dst receives the (n, c_o, hp, wp) CHWN pooled output,
+ * hp/wp = pool_output_extents of the conv output.  Bit-identical to
+ * lcnn_conv_forward_packed followed by lcnn_pool_layout (max).
+ * lcnn_conv_maxpool_supported returns 1 when the fused kernel covers the
+ * geometry, 0 otherwise (callers then run the two layers). */
+int lcnn_conv_maxpool_supported(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                                int layout, uint32_t c_o, uint32_t f_h,
+                                uint32_t f_w, uint32_t stride, uint32_t pad,
+                                int precision, uint32_t pool_win,
+                                uint32_t pool_stride);
+lcnn_status lcnn_conv_maxpool_packed(const float* src, const void* d_packed,
+                                     float* dst, uint32_t n, uint32_t c_i,
+                                     uint32_t h, uint32_t w, int layout,
+                                     uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                     uint32_t stride, uint32_t pad,
+                                     int precision, uint32_t pool_win,
+                                     uint32_t pool_stride, void* stream);
+
 /* == conv_oracle (conv.cpp:53-93): fp64 accumulation, any input layout,
  * NCHW output.  Ground truth, not a hot op. */
 lcnn_status lcnn_conv_oracle(const float* src, const float* filters, float* dst,

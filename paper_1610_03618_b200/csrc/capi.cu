@@ -680,6 +680,38 @@ lcnn_status lcnn_conv_forward_packed(const float* src, const void* d_packed, flo
   return ok();
 }
 
+int lcnn_conv_maxpool_supported(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, int layout,
+                                uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
+                                uint32_t pad, int precision, uint32_t pool_win,
+                                uint32_t pool_stride) {
+  lcnn_impl::ConvArgs a;
+  if (conv_args(n, c_i, h, w, layout, c_o, f_h, f_w, stride, pad, precision, &a) != LCNN_OK)
+    return 0;
+  return lcnn_impl::conv_maxpool_fusable(a, pool_win, pool_stride) ? 1 : 0;
+}
+
+lcnn_status lcnn_conv_maxpool_packed(const float* src, const void* d_packed, float* dst,
+                                     uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, int layout,
+                                     uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
+                                     uint32_t pad, int precision, uint32_t pool_win,
+                                     uint32_t pool_stride, void* stream) {
+  if (!src || !d_packed || !dst) return fail(LCNN_EINVAL, "conv_maxpool: null pointer");
+  if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
+    return fail(LCNN_EINVAL, "conv_maxpool: packed filters must be 256-byte aligned");
+  lcnn_impl::ConvArgs a;
+  lcnn_status st = conv_args(n, c_i, h, w, layout, c_o, f_h, f_w, stride, pad, precision, &a);
+  if (st != LCNN_OK) return st;
+  if (!lcnn_impl::conv_maxpool_fusable(a, pool_win, pool_stride))
+    return fail(LCNN_EUNSUPPORTED, "conv_maxpool: geometry not covered by the fused kernel");
+  a.src = src;
+  a.dst = dst;
+  a.workspace = nullptr;
+  cudaError_t e = lcnn_impl::launch_conv_maxpool_packed(a, d_packed, pool_win, pool_stride,
+                                                        S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "conv_maxpool_packed");
+  return ok();
+}
+
 lcnn_status lcnn_conv_oracle(const float* src, const float* filters, float* dst, uint32_t n,
                              uint32_t c_i, uint32_t h, uint32_t w, int layout, uint32_t c_o,
                              uint32_t f_h, uint32_t f_w, uint32_t stride, uint32_t pad,

@@ -545,6 +545,122 @@ struct ShareOut {
   }
 };
 
+// ---- SHARE convolution with the max pooling that follows it fused in ------
+// (AlexNet conv1 -> pool1: conv 96 f11 s4 -> 55x55, max 3x3/s2 -> 27x27.)
+// The conv output never reaches HBM: a CTA owns one POOLING STRIP -- one
+// 32-image group x PC pool columns x a segment of pool rows -- and walks its
+// conv rows top to bottom, one tile per row.  A tile is the TPX = 2*(PC-1) +
+// PWIN conv pixels the strip's PC windows cover (7 for 3x3/s2: pixels
+// 6j..6j+6 serve pool columns 3j..3j+2), UMMA N = 32 * TPX, with the SHARE
+// operand layout (one input box per filter row, overlapping MN atoms).  The
+// epilogue warps keep the open pool row (PC x 32 images per channel lane) in
+// registers across tiles: per window u, h = max of the row's PWIN pixels,
+// then pool = max(running, h).  With the reference's compare-select
+// (max_tap: NaN never replaces, ties keep the earlier tap) the row-then-column
+// order is bit-identical to its (y, x) tap order (the first maximal tap of
+// the earlier row wins either way), and each conv value is the same
+// K-ordered tensor-core sum as in the unfused SHARE kernel, so the fused
+// layer equals conv -> pool_layout bit for bit.  Cost: the strip segments
+// recompute one conv row at each boundary and 7 conv pixels serve 6 columns
+// (~1.2x the MMA work of the unfused conv), against the unfused output
+// stream (149 MB for conv1) and the pooling pass that re-reads it.
+// Pooling stride 2 with windows 2 or 3 (one open pool row at a time).
+constexpr uint32_t kPoolStride = 2;
+template <int PWIN>
+struct SharePoolDims {
+  static constexpr uint32_t PC = (kSharePix - PWIN) / kPoolStride + 1;  // pool columns per tile
+  static constexpr uint32_t TPX = kPoolStride * (PC - 1) + PWIN;         // conv pixels per tile
+};
+
+struct ChwnSharePoolLoader : ChwnShareLoader {
+  uint32_t units, strips, segs, hp, tpx, pc;
+  FastDiv fd_units, fd_groups;
+  __device__ State begin(uint32_t, uint32_t n0, uint32_t) const {
+    uint32_t k, unit, j, grp;
+    fd_units.divmod(n0 / (tpx * 32), k, unit);
+    const uint32_t sg = unit / strips, strip = unit - sg * strips;
+    fd_groups.divmod(strip, j, grp);
+    const uint32_t ph0 = sg * hp / segs, ph1 = (sg + 1) * hp / segs;
+    const uint32_t rows = 2 * (ph1 - ph0) + (tpx - kPoolStride * (pc - 1)) - 2;
+    const uint32_t oh = kPoolStride * ph0 + (k < rows ? k : rows - 1);  // past the segment: reload its last row
+    return State{static_cast<int32_t>(j * pc * kPoolStride * g.S) - static_cast<int32_t>(g.P),
+                 static_cast<int32_t>(oh * g.S) - static_cast<int32_t>(g.P),
+                 static_cast<int32_t>(grp)};
+  }
+};
+
+template <int PWIN>
+struct SharePoolOut {
+  static constexpr bool kStateful = true;
+  static constexpr uint32_t PC = SharePoolDims<PWIN>::PC;
+  // pooled output view {32 n, N/32, Wp, Hp, Co}, box {32, 1, 1, 1, 32}: one
+  // 32-channel x 32-image chunk of one pool pixel, SWIZZLE_128B
+  CUtensorMap y;
+  uint32_t co, wp, hp, strips, segs;
+  FastDiv fd_units, fd_groups;
+  struct Acc {
+    float cur[PC][32];  // the open pool row: running max per window, 32 images
+  };
+  __device__ __forceinline__ void tile(Acc& acc, uint32_t t, uint32_t taddr, uint8_t* stg,
+                                       uint32_t& epi_buf, int q, int lane) const {
+    uint32_t k, unit, j, grp;
+    fd_units.divmod(t, k, unit);
+    const uint32_t sg = unit / strips, strip = unit - sg * strips;
+    fd_groups.divmod(strip, j, grp);
+    const uint32_t ph0 = sg * hp / segs, ph1 = (sg + 1) * hp / segs;
+    const uint32_t rows = 2 * (ph1 - ph0) + PWIN - 2;
+    const uint32_t m0 = static_cast<uint32_t>(q) * 32;
+    if (k >= rows || m0 >= co) return;  // warp-uniform: padding row of the segment / channels
+    const uint32_t d = k & 1, i = k >> 1;
+    // the pool row this conv row completes (d == 0: the row above's window
+    // for 3-wide windows; d == 1: its own for 2-wide ones)
+    const bool closes = PWIN == 3 ? (d == 0 && i >= 1) : (d == 1);
+    const uint32_t ph = ph0 + (PWIN == 3 ? i - 1 : i);
+#pragma unroll
+    for (uint32_t u = 0; u < PC; ++u) {
+      const uint32_t pw = j * PC + u;
+      if (pw >= wp) break;  // warp-uniform
+      float h[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) h[e] = -INFINITY;
+#pragma unroll
+      for (int p = 0; p < PWIN; ++p) {
+        float v[32];
+        tmem_ld32(taddr + (kPoolStride * u + p) * 32, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) h[e] = max_tap(h[e], v[e]);
+      }
+      if (closes) {
+        uint8_t* box = stg + (epi_buf & 1) * 4096;
+        ++epi_buf;
+        if (lane == 0) bulk_wait_read_n<1>();  // this box's previous store has read it
+        __syncwarp();
+        float4* row = reinterpret_cast<float4*>(box + lane * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          row[c ^ (lane & 7)] = make_float4(
+              max_tap(acc.cur[u][4 * c], h[4 * c]), max_tap(acc.cur[u][4 * c + 1], h[4 * c + 1]),
+              max_tap(acc.cur[u][4 * c + 2], h[4 * c + 2]),
+              max_tap(acc.cur[u][4 * c + 3], h[4 * c + 3]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_5d(&y, box, 0, static_cast<int32_t>(grp), static_cast<int32_t>(pw),
+                       static_cast<int32_t>(ph), static_cast<int32_t>(m0));
+          bulk_commit();
+        }
+      }
+      if (d == 0) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc.cur[u][e] = h[e];  // opens pool row ph0 + i
+      } else if (PWIN == 3) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc.cur[u][e] = max_tap(acc.cur[u][e], h[e]);
+      }
+    }
+  }
+};
+
 // ---- TAPS mode: tap-sharing input boxes for CI convolutions ----------------
 // A tile is 8 consecutive output pixels of one output row x one 32-image
 // group (UMMA N = 256, channels on M, the ShareOut mapping).  K runs (filter
@@ -1583,6 +1699,73 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
   return launch_persistent(L, O, sc, s);
 }
 
+// SHARE convolution + stride-2 max pooling (PWIN = 2 or 3) in one kernel
+// (SharePoolOut).  Units = pooling strips (32-image group x PC pool
+// columns) x row segments, one CTA each, so no split tiles and no zeroing.
+template <int PWIN>
+cudaError_t launch_chwn_share_pool(const ConvTcArgs& t, float* pooled, uint32_t hp, uint32_t wp,
+                                   cudaStream_t s) {
+  using D = SharePoolDims<PWIN>;
+  const ConvArgs& a = t.a;
+  const ShareGeom q = share_geom(a, false);
+  ChwnSharePoolLoader L;
+  L.g = t.p.g;
+  L.bn = q.bn;
+  L.wimg = t.w_hi;
+  L.groups = a.n / 32;
+  L.owb = 0;
+  L.res = 0;
+  L.tpx = D::TPX;
+  L.pc = D::PC;
+  L.hp = hp;
+  const uint32_t bw = a.stride * (D::TPX - 1) + a.fw;
+  const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
+  const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
+                             static_cast<uint64_t>(a.n) * 4, 128,
+                             static_cast<uint64_t>(a.w) * a.n * 4};
+  const uint32_t box[5] = {32, a.ci, bw, 1, 1};
+  if (!make_tmap(&L.x, t.x_hi, 5, dims, pitch, box, nullptr, 1)) return cudaErrorInvalidValue;
+  const uint32_t jc = (wp + D::PC - 1) / D::PC;
+  L.strips = L.groups * jc;
+  const uint32_t sms = static_cast<uint32_t>(tc_sm_count());
+  L.segs = std::max(1u, std::min(hp, sms / L.strips));
+  L.units = L.strips * L.segs;
+  uint32_t rmax = 0;
+  for (uint32_t sg = 0; sg < L.segs; ++sg)
+    rmax = std::max(rmax, 2 * ((sg + 1) * hp / L.segs - sg * hp / L.segs) + PWIN - 2);
+  L.fd_units = FastDiv(L.units);
+  L.fd_groups = FastDiv(L.groups);
+  Sched sc = make_sched(1, L.units * rmax, a.fh, 1, D::TPX * 32, false, true, kMinSkIters, L.units);
+  if (sc.dp_tiles != L.units * rmax || sc.grid != L.units) return cudaErrorInvalidConfiguration;
+  sc.ksteps = q.kr / 8;
+  sc.a_bytes = q.wbytes;
+  sc.stage_bytes = q.wbytes + bw * a.ci * 128;
+  uint32_t slots = 0;  // two staging boxes per epilogue warp (double-buffered pool stores)
+  for (uint32_t n = kPStagesMax; n >= 3 && !slots; --n)
+    if (1024ull + n * q.slot + 1024 + 2 * 4 * 4096 + sizeof(PCtl) <= kMaxDynSmem) slots = n;
+  if (!slots) return cudaErrorInvalidConfiguration;
+  sched_ring(sc, slots, q.slot, 0);
+  sched_epi(sc, 0, 2);
+  SharePoolOut<PWIN> O;
+  {
+    const uint64_t odims[5] = {32, a.n / 32, wp, hp, a.co};
+    const uint64_t opitch[4] = {128, static_cast<uint64_t>(a.n) * 4,
+                                static_cast<uint64_t>(wp) * a.n * 4,
+                                static_cast<uint64_t>(hp) * wp * a.n * 4};
+    const uint32_t obox[5] = {32, 1, 1, 1, 32};
+    if (!make_tmap(&O.y, pooled, 5, odims, opitch, obox, nullptr, 0))
+      return cudaErrorInvalidValue;
+  }
+  O.co = a.co;
+  O.wp = wp;
+  O.hp = hp;
+  O.strips = L.strips;
+  O.segs = L.segs;
+  O.fd_units = L.fd_units;
+  O.fd_groups = L.fd_groups;
+  return launch_persistent(L, O, sc, s);
+}
+
 // TAPS-mode geometry: input box width, ring slots that fit shared memory.
 struct TapsGeom {
   uint32_t bw, ibox, islot, ni, nf;
@@ -2102,6 +2285,27 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
   if (r.kind == kRouteTapsN) return launch_chwn_tapsn(t, s);
   if (r.kind == kRouteChwnPair) return launch_chwn_tc<true, true>(t, s);
   return r.kind == kRouteChwnOnN ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);
+}
+
+// Convolution + max pooling fused (SharePoolOut): CHWN, TF32, a layer the
+// SHARE route takes, pooling stride 2 with a 2- or 3-wide square window.
+bool conv_maxpool_fusable(const ConvArgs& a, uint32_t pwin, uint32_t pstride) {
+  if (a.layout != LCNN_CHWN || a.precision != LCNN_PREC_TF32) return false;
+  if (pstride != kPoolStride || (pwin != 2 && pwin != 3) || a.ho < pwin || a.wo < pwin)
+    return false;
+  const ConvRoute r = route_conv(a);
+  return r.kind == kRouteShare && !r.via_chwn;
+}
+
+cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, uint32_t pwin,
+                                       uint32_t pstride, cudaStream_t s) {
+  if (!conv_maxpool_fusable(a, pwin, pstride)) return cudaErrorInvalidValue;
+  const ConvRoute r = route_conv(a);
+  const float* w = static_cast<const float*>(packed);
+  ConvTcArgs t{a, r.p, w, w, a.src, a.src};
+  const uint32_t hp = (a.ho - pwin) / pstride + 1, wp = (a.wo - pwin) / pstride + 1;
+  return pwin == 3 ? launch_chwn_share_pool<3>(t, a.dst, hp, wp, s)
+                   : launch_chwn_share_pool<2>(t, a.dst, hp, wp, s);
 }
 
 // One-shot form: pack into the front of the workspace, run with the rest.

@@ -68,6 +68,12 @@ size_t conv_workspace_bytes(const ConvArgs& a);
 size_t conv_packed_bytes(const ConvArgs& a);
 cudaError_t launch_conv_pack(const ConvArgs& a, void* packed, cudaStream_t s);
 cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream_t s);
+// Convolution followed by a max pooling (window pwin, stride pstride) in one
+// kernel; a.dst receives the POOLED output.  The packed filters are the
+// layer's lcnn_conv_pack image.
+bool conv_maxpool_fusable(const ConvArgs& a, uint32_t pwin, uint32_t pstride);
+cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, uint32_t pwin,
+                                       uint32_t pstride, cudaStream_t s);
 bool tc_gemm_supported(uint64_t m, uint64_t n, uint64_t k, const void* a,
                        const void* b);
 size_t gemm_workspace_bytes(uint64_t m, uint64_t n, uint64_t k, int precision);

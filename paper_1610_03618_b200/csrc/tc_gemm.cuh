@@ -139,6 +139,18 @@ struct OutTmaPairs<O, decltype(void(O::kTmaPairs))> {
   static constexpr bool value = O::kTmaPairs;
 };
 constexpr uint32_t kEpiStageBytes = 4 * 2 * 4096;  // 4 warps x 2 boxes
+// Out types that carry state from tile to tile in the epilogue warps'
+// registers (Out::Acc) and consume each tile with Out::tile(): the max-pool
+// fused into the SHARE convolution, whose CTA walks the conv rows of one
+// pooling strip in order (conv.cu SharePoolOut)
+template <class O, class = void>
+struct OutStateful {
+  static constexpr bool value = false;
+};
+template <class O>
+struct OutStateful<O, decltype(void(O::kStateful))> {
+  static constexpr bool value = O::kStateful;
+};
 
 // One tile's accumulator rows [q*32, q*32+32) (this warp's TMEM lane quarter)
 // out of TMEM, 32 columns at a time.  TMA outputs: registers -> a swizzled
@@ -467,6 +479,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
     });
   } else if (warp >= 2) {
+    // ---------------- stateful epilogue (Out::tile) ----------------
+    if constexpr (OutStateful<Out>::value) {
+      const int q = warp & 3;
+      uint32_t local = 0, epi_buf = 0;
+      typename Out::Acc acc;
+      for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool) {
+        const uint32_t a = local & 1, aphase = (local >> 1) & 1;
+        ++local;
+        mbar_wait(&ctl->tfull[a], aphase);
+        tc_fence_after();
+        const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
+        out.tile(acc, t, base, smem + sc.epi_off + q * sc.epi_bufs * 4096, epi_buf, q, lane);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->tempty[a]);
+      });
+      if (lane == 0) bulk_wait_read_n<0>();
+    } else {
     // ---------------- epilogue ----------------
     const int q = warp & 3;
     uint32_t local = 0, epi_buf = 0;
@@ -486,6 +516,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     });
     if constexpr (OutTma<Out>::value) {
       if (lane == 0) bulk_wait_read_n<0>();
+    }
     }
   }
   tc_fence_before();

@@ -56,4 +56,17 @@ DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packe
                                    std::uint32_t c_o, std::uint32_t f_h, std::uint32_t f_w,
                                    const ConvParams& p, int precision);
 
+// Convolution and the max pooling that consumes it as one kernel
+// (lcnn_conv_maxpool_packed): returns the POOLED tensor, bit-identical to
+// conv_forward_packed followed by a max pool_layout with (pool_win, pool_win,
+// pool_stride).  conv_maxpool_supported says whether the fused kernel covers
+// the pair (CHWN, TF32, SHARE-routed conv, stride-2 windows of 2 or 3).
+bool conv_maxpool_supported(const DeviceTensor4D& in, std::uint32_t c_o, std::uint32_t f_h,
+                            std::uint32_t f_w, const ConvParams& p, int precision,
+                            std::uint32_t pool_win, std::uint32_t pool_stride);
+DeviceTensor4D conv_maxpool_forward_packed(const DeviceTensor4D& in, const void* d_packed,
+                                           std::uint32_t c_o, std::uint32_t f_h,
+                                           std::uint32_t f_w, const ConvParams& p, int precision,
+                                           std::uint32_t pool_win, std::uint32_t pool_stride);
+
 }  // namespace lcnn

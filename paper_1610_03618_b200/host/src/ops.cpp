@@ -460,6 +460,30 @@ DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packe
   return out;
 }
 
+bool conv_maxpool_supported(const DeviceTensor4D& in, std::uint32_t c_o, std::uint32_t f_h,
+                            std::uint32_t f_w, const ConvParams& p, int precision,
+                            std::uint32_t pool_win, std::uint32_t pool_stride) {
+  return lcnn_conv_maxpool_supported(in.n(), in.c(), in.h(), in.w(), code(in.layout()), c_o, f_h,
+                                     f_w, p.stride, p.pad, precision, pool_win,
+                                     pool_stride) == 1;
+}
+
+DeviceTensor4D conv_maxpool_forward_packed(const DeviceTensor4D& in, const void* d_packed,
+                                           std::uint32_t c_o, std::uint32_t f_h,
+                                           std::uint32_t f_w, const ConvParams& p, int precision,
+                                           std::uint32_t pool_win, std::uint32_t pool_stride) {
+  const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f_h, f_w, p);
+  if (pool_win == 0 || pool_stride == 0 || pool_win > ho || pool_win > wo)
+    throw ShapeError("conv_maxpool: pool window does not fit the conv output");
+  const std::uint32_t hp = (ho - pool_win) / pool_stride + 1;
+  const std::uint32_t wp = (wo - pool_win) / pool_stride + 1;
+  DeviceTensor4D out(in.n(), c_o, hp, wp, in.layout());
+  check_status(lcnn_conv_maxpool_packed(in.data(), d_packed, out.data(), in.n(), in.c(), in.h(),
+                                        in.w(), code(in.layout()), c_o, f_h, f_w, p.stride, p.pad,
+                                        precision, pool_win, pool_stride, current_stream()));
+  return out;
+}
+
 Tensor4D conv_oracle(const Tensor4D& in, const FilterBank& f, const ConvParams& p) {
   check_conv_inputs(in, f);
   const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f.f_h(), f.f_w(), p);

@@ -405,6 +405,33 @@ def conv_forward_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride=1, pad=
     return out
 
 
+def conv_maxpool_supported(x: DeviceTensor4D, c_o, f_h, f_w, stride, pad, precision, pool_win,
+                           pool_stride) -> bool:
+    """lcnn_conv_maxpool_supported: the fused conv -> max-pool kernel covers
+    this layer pair."""
+    return capi.lib().lcnn_conv_maxpool_supported(
+        x.n, x.c, x.h, x.w, x.layout, c_o, f_h, f_w, stride, pad, precision, pool_win,
+        pool_stride) == 1
+
+
+def conv_maxpool_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride, pad, precision,
+                        pool_win, pool_stride, out=None, stream=None) -> DeviceTensor4D:
+    """Convolution and the max pooling that consumes it as one kernel
+    (lcnn_conv_maxpool_packed): the pooled CHWN tensor, bit-identical to
+    conv_forward_packed followed by pool_layout (max)."""
+    torch = _torch()
+    ho, wo = conv_output_extents(x.h, x.w, f_h, f_w, stride, pad)
+    hp, wp = (ho - pool_win) // pool_stride + 1, (wo - pool_win) // pool_stride + 1
+    if out is None:
+        out = DeviceTensor4D(x.n, c_o, hp, wp, x.layout,
+                             torch.empty(x.n * c_o * hp * wp, dtype=torch.float32,
+                                         device=x.data.device))
+    capi.call("lcnn_conv_maxpool_packed", x.ptr(), packed.data_ptr(), out.ptr(), x.n, x.c, x.h,
+              x.w, x.layout, c_o, f_h, f_w, stride, pad, precision, pool_win, pool_stride,
+              _stream(stream))
+    return out
+
+
 def gemm(a, b, m, n, k, precision=FP32, out=None, workspace=None, stream=None):
     """c (m x n) = a (m x k) * b (k x n), row-major fp32 CUDA tensors
     (gemm_blocked conv.cpp:252-304 / fc_forward softmax.cpp:182-184)."""
@@ -447,7 +474,7 @@ def fc_forward_packed(x, x_layout, packed, m, n, k, precision=TF32, out=None, st
 
 __all__ = ["TF32", "X3TF32", "FP32", "conv_forward", "gemm", "pack_conv_filters",
     "pack_fc_weights", "fc_forward_packed",
-    "conv_forward_packed", "conv_output_extents",
+    "conv_forward_packed", "conv_maxpool_supported", "conv_maxpool_packed", "conv_output_extents",
     "NCHW", "CHWN", "NHWC", "HWCN", "MAX", "AVERAGE", "DeviceTensor4D", "DeviceMatrix",
     "TransformPlan", "PoolParams", "CoarseningPlan", "AccessReport", "PassReport",
     "flattenable_pair", "make_plan", "transform", "transform_tiled", "transform_naive",

@@ -1,0 +1,114 @@
+"""GPU parity for the fused convolution -> max pooling kernel
+(lcnn_conv_maxpool_packed, csrc/conv.cu SharePoolOut): the reference runs the
+two layers one after the other (run_network, net.cpp:284-353: conv_direct,
+then pool_coarsened / pool_layout), so the fused kernel must return exactly
+the bits of conv_forward_packed followed by pool_layout (max) -- every conv
+value is the same K-ordered tensor-core sum, and the pooling keeps the
+reference's compare-select tap order (pool.cpp:120).  Bit-exact (torch.equal),
+including NaN / +-0 patterns in the input.  The unfused conv itself is held to
+the TF32 bound against fp64 in test_gpu_conv_gemm.py.
+
+Bit-exactness against the two-layer run needs the unfused conv to sum each
+output whole: layers with at least a 60 %-full last wave of tiles (AlexNet
+conv1 at any batch of 32k images) run whole tiles; small layers put their
+tail on stream-K, whose fp32 fragments are added in another order, so there
+the fused output is held to the conv's TF32 bound instead (max pooling is
+1-Lipschitz: |max a - max b| <= max |a - b|, so the pooled bound is the
+max-pooled per-output bound).
+"""
+import pytest
+
+from oracle.oracle import CHWN
+from paper_1610_03618_b200 import lcnn
+
+pytestmark = pytest.mark.gpu
+
+# (n, c_i, h, w, c_o, f, stride, pad, pool window, pool stride)
+EXACT = [
+    (128, 3, 227, 227, 96, 11, 4, 0, 3, 2),  # AlexNet conv1 -> pool1, as benched
+    (32, 3, 227, 227, 96, 11, 4, 0, 3, 2),   # one 32-image group (strong-scaled shard)
+    (64, 3, 100, 100, 96, 11, 4, 0, 3, 2),   # 23x23 conv -> 11x11 (last strip partial)
+]
+CASES = EXACT + [
+    (32, 3, 67, 71, 40, 11, 4, 2, 3, 2),     # padding, c_o = 40 (one real channel warp + part)
+    (32, 3, 64, 64, 64, 7, 2, 3, 3, 2),      # 32x32 conv -> 15x15
+    (32, 3, 64, 64, 64, 5, 1, 2, 3, 2),      # stride-1 conv, 64x64 -> 31x31
+    (64, 3, 96, 96, 96, 11, 4, 0, 2, 2),     # 22x22 conv -> 11x11 with 2x2 windows
+    (32, 1, 45, 45, 128, 5, 2, 0, 2, 2),     # c_o = 128, odd conv extent (21 -> 10)
+]
+
+
+def _run(cuda, case, seed=0, special=False):
+    import torch
+
+    n, ci, h, w, co, f, s, p, pw, ps = case
+    g = torch.Generator(device=cuda).manual_seed(seed)
+    x = (torch.rand(ci, h, w, n, device=cuda, generator=g) * 2 - 1).reshape(-1)
+    if special:
+        # NaN and signed zeros in the input: the pooled bits must still match
+        idx = torch.randint(0, x.numel(), (64,), device=cuda, generator=g)
+        x[idx[:16]] = float("nan")
+        x[idx[16:40]] = 0.0
+        x[idx[40:]] = -0.0
+    filt = (torch.rand(co, ci, f, f, device=cuda, generator=g) * 2 - 1).contiguous()
+    t = lcnn.DeviceTensor4D(n, ci, h, w, CHWN, x)
+    assert lcnn.conv_maxpool_supported(t, co, f, f, s, p, lcnn.TF32, pw, ps), case
+    packed = lcnn.pack_conv_filters(t, filt, co, f, f, s, p, lcnn.TF32)
+    conv = lcnn.conv_forward_packed(t, packed, co, f, f, s, p, lcnn.TF32)
+    want, _ = lcnn.pool_layout(conv, lcnn.PoolParams(pw, pw, ps, lcnn.MAX))
+    got = lcnn.conv_maxpool_packed(t, packed, co, f, f, s, p, lcnn.TF32, pw, ps)
+    torch.cuda.synchronize()
+    assert (got.n, got.c, got.h, got.w) == (want.n, want.c, want.h, want.w)
+    if case in EXACT:
+        a, b = got.data.view(torch.int32), want.data.view(torch.int32)
+        bad = int((a != b).sum())
+        assert bad == 0, (case, bad, got.data.numel())
+    if special:  # non-finite inputs: the unfused SHARE route is the reference (DESIGN 8)
+        assert case in EXACT
+        return got
+    # against fp64: conv64 -> max pool, with the max-pooled TF32 bound
+    xn = x.view(ci, h, w, n).permute(3, 0, 1, 2).double()
+    conv64 = torch.nn.functional.conv2d(xn, filt.double(), stride=s, padding=p)
+    bound = torch.nn.functional.conv2d(xn.abs().nan_to_num(0.0), filt.double().abs(), stride=s,
+                                       padding=p)
+    ref = torch.nn.functional.max_pool2d(conv64, pw, ps)
+    tol = torch.nn.functional.max_pool2d(bound, pw, ps) * 2.0 ** -9 + 1e-6
+    g = got.data.view(co, got.h, got.w, n).permute(3, 0, 1, 2).double()
+    finite = torch.isfinite(ref)
+    assert bool((torch.isfinite(g) == finite).all()), case
+    err = (g - ref).abs()[finite]
+    assert bool((err <= tol[finite]).all()), (case, float(err.max()))
+    return got
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv_maxpool_fused_bit_exact(cuda, case):
+    _run(cuda, case)
+
+
+def test_conv_maxpool_fused_special_values(cuda):
+    _run(cuda, EXACT[1], seed=3, special=True)
+
+
+def test_conv_maxpool_fused_repeatable(cuda):
+    import torch
+
+    a = _run(cuda, CASES[1], seed=5)
+    b = _run(cuda, CASES[1], seed=5)
+    assert torch.equal(a.data.view(torch.int32), b.data.view(torch.int32))
+
+
+def test_conv_maxpool_unsupported_pairs(cuda):
+    import torch
+
+    x = torch.zeros(32 * 64 * 28 * 28, device=cuda)
+    t = lcnn.DeviceTensor4D(32, 64, 28, 28, CHWN, x)
+    # a CI-routed 3x3 layer, a stride-1 pool, FP32: not covered -> callers run two layers
+    assert not lcnn.conv_maxpool_supported(t, 64, 3, 3, 1, 1, lcnn.TF32, 2, 2)
+    x3 = torch.zeros(32 * 3 * 67 * 67, device=cuda)
+    t3 = lcnn.DeviceTensor4D(32, 3, 67, 67, CHWN, x3)
+    assert not lcnn.conv_maxpool_supported(t3, 96, 11, 11, 4, 0, lcnn.TF32, 3, 1)
+    assert not lcnn.conv_maxpool_supported(t3, 96, 11, 11, 4, 0, lcnn.FP32, 3, 2)
+    with pytest.raises(Exception):
+        lcnn.conv_maxpool_packed(t, torch.zeros(1 << 20, dtype=torch.uint8, device=cuda),
+                                 64, 3, 3, 1, 1, lcnn.TF32, 2, 2)
