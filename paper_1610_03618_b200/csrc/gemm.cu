@@ -394,6 +394,14 @@ cudaError_t launch_zero2d(void* p, uint64_t pitch_words, uint64_t width_words, u
                           cudaStream_t s) {
   const uint64_t total = width_words * rows;
   if (!total) return cudaSuccess;
+#ifdef LCNN_PROFILING_KNOBS
+  // LCNN_SKIP_ZERO=1: no stream-K zeroing launches (wrong sums; timing only)
+  static const bool skip = [] {
+    const char* e = std::getenv("LCNN_SKIP_ZERO");
+    return e && e[0] == '1';
+  }();
+  if (skip && pitch_words > 1) return cudaSuccess;
+#endif
   uint64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   return lcnn_pdl::launch(zero2d_kernel, static_cast<uint32_t>(blocks), 256, 0, s,
