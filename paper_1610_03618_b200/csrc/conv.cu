@@ -589,13 +589,18 @@ struct ChwnSharePoolLoader : ChwnShareLoader {
   }
 };
 
-template <int PWIN>
+// kDirect: each lane stores its channel's 32 pooled images (one 128-B line)
+// straight from registers -- no staging boxes, so the input ring gets their
+// 32 KB (one more slot); otherwise a swizzled box per warp and a TMA store.
+template <int PWIN, bool kDirect>
 struct SharePoolOut {
   static constexpr bool kStateful = true;
   static constexpr uint32_t PC = SharePoolDims<PWIN>::PC;
   // pooled output view {32 n, N/32, Wp, Hp, Co}, box {32, 1, 1, 1, 32}: one
   // 32-channel x 32-image chunk of one pool pixel, SWIZZLE_128B
   CUtensorMap y;
+  float* out;  // CHWN [co][hp][wp][n] (kDirect)
+  uint32_t n;
   uint32_t co, wp, hp, strips, segs;
   FastDiv fd_units, fd_groups;
   struct Acc {
@@ -630,7 +635,18 @@ struct SharePoolOut {
 #pragma unroll
         for (int e = 0; e < 32; ++e) h[e] = max_tap(h[e], v[e]);
       }
-      if (closes) {
+      if (closes && kDirect) {
+        if (m0 + lane < co) {
+          float4* dst = reinterpret_cast<float4*>(
+              out + ((static_cast<uint64_t>(m0 + lane) * hp + ph) * wp + pw) * n + grp * 32);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            dst[c] = make_float4(max_tap(acc.cur[u][4 * c], h[4 * c]),
+                                 max_tap(acc.cur[u][4 * c + 1], h[4 * c + 1]),
+                                 max_tap(acc.cur[u][4 * c + 2], h[4 * c + 2]),
+                                 max_tap(acc.cur[u][4 * c + 3], h[4 * c + 3]));
+        }
+      } else if (closes) {
         uint8_t* box = stg + (epi_buf & 1) * 4096;
         ++epi_buf;
         if (lane == 0) bulk_wait_read_n<1>();  // this box's previous store has read it
@@ -1702,7 +1718,7 @@ cudaError_t launch_chwn_share(const ConvTcArgs& t, bool resident, cudaStream_t s
 // SHARE convolution + stride-2 max pooling (PWIN = 2 or 3) in one kernel
 // (SharePoolOut).  Units = pooling strips (32-image group x PC pool
 // columns) x row segments, one CTA each, so no split tiles and no zeroing.
-template <int PWIN>
+template <int PWIN, bool kDirect>
 cudaError_t launch_chwn_share_pool(const ConvTcArgs& t, float* pooled, uint32_t hp, uint32_t wp,
                                    cudaStream_t s) {
   using D = SharePoolDims<PWIN>;
@@ -1740,13 +1756,20 @@ cudaError_t launch_chwn_share_pool(const ConvTcArgs& t, float* pooled, uint32_t 
   sc.ksteps = q.kr / 8;
   sc.a_bytes = q.wbytes;
   sc.stage_bytes = q.wbytes + bw * a.ci * 128;
-  uint32_t slots = 0;  // two staging boxes per epilogue warp (double-buffered pool stores)
+  // slots: the ring of input boxes, after the staging boxes (2 per epilogue
+  // warp, double-buffered TMA stores) unless the lanes store directly
+  const uint32_t slot = (q.wbytes + std::max(bw * a.ci, a.stride * a.ci * (D::TPX - 1) + q.kr) * 128 +
+                         1023) / 1024 * 1024;
+  const uint32_t epi = kDirect ? 0u : 2u;
+  uint32_t slots = 0;
   for (uint32_t n = kPStagesMax; n >= 3 && !slots; --n)
-    if (1024ull + n * q.slot + 1024 + 2 * 4 * 4096 + sizeof(PCtl) <= kMaxDynSmem) slots = n;
+    if (1024ull + n * slot + 1024 + epi * 4 * 4096 + sizeof(PCtl) <= kMaxDynSmem) slots = n;
   if (!slots) return cudaErrorInvalidConfiguration;
-  sched_ring(sc, slots, q.slot, 0);
-  sched_epi(sc, 0, 2);
-  SharePoolOut<PWIN> O;
+  sched_ring(sc, slots, slot, 0);
+  if (epi) sched_epi(sc, 0, epi);
+  SharePoolOut<PWIN, kDirect> O;
+  O.out = pooled;
+  O.n = a.n;
   {
     const uint64_t odims[5] = {32, a.n / 32, wp, hp, a.co};
     const uint64_t opitch[4] = {128, static_cast<uint64_t>(a.n) * 4,
@@ -2304,8 +2327,17 @@ cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, ui
   const float* w = static_cast<const float*>(packed);
   ConvTcArgs t{a, r.p, w, w, a.src, a.src};
   const uint32_t hp = (a.ho - pwin) / pstride + 1, wp = (a.wo - pwin) / pstride + 1;
-  return pwin == 3 ? launch_chwn_share_pool<3>(t, a.dst, hp, wp, s)
-                   : launch_chwn_share_pool<2>(t, a.dst, hp, wp, s);
+  // profiling knob LCNN_SHAREPOOL_STORE=tma: staged TMA stores of the pooled
+  // chunks (one ring slot fewer) instead of direct lane stores
+  static const bool tma = [] {
+    const char* e = std::getenv("LCNN_SHAREPOOL_STORE");
+    return e && e[0] == 't';
+  }();
+  // (2-wide windows keep 4 open pool columns: 128 accumulator registers,
+  // which the direct-store epilogue would spill -- they always stage)
+  if (pwin == 2) return launch_chwn_share_pool<2, false>(t, a.dst, hp, wp, s);
+  return tma ? launch_chwn_share_pool<3, false>(t, a.dst, hp, wp, s)
+             : launch_chwn_share_pool<3, true>(t, a.dst, hp, wp, s);
 }
 
 // One-shot form: pack into the front of the workspace, run with the rest.

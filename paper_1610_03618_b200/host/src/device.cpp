@@ -157,8 +157,15 @@ void set_current_stream(void* stream) {
   ThreadContext& c = ctx();
   if (c.external == static_cast<cudaStream_t>(stream)) return;  // no change: stay async
   // drain the stream being left: the caller may read its results or destroy
-  // it right after switching
-  synchronize();
+  // it right after switching -- unless the stream being entered is capturing
+  // a CUDA graph (a synchronize would invalidate the capture; the capturing
+  // caller orders the two streams itself, e.g. torch.cuda.graph's
+  // wait_stream)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (!(stream &&
+        cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cs) == cudaSuccess &&
+        cs != cudaStreamCaptureStatusNone))
+    synchronize();
   c.external = static_cast<cudaStream_t>(stream);
 }
 
