@@ -128,6 +128,7 @@ struct FcLoader {
   uint32_t bn;           // weight rows (output columns) one stage loads: 256, or 128
   uint32_t pf_ahead;     // k-blocks of weights prefetched into L2 ahead of the TMA loads
   bool a_grouped;  // MN-major A, m % 128 == 0: one 3D box {32, 32 k, 4 groups}
+  bool skip_a;     // profiling (LCNN_TC_PROBE bit 4): no activation loads
   static constexpr bool kZeroSmem = false;
   static constexpr bool kResidentA = false;
   static constexpr int kSteps = kTcBK / 8;
@@ -149,7 +150,8 @@ struct FcLoader {
                        uint64_t* bar) const {
     const CUtensorMap* am = &a[seg == 2 ? 1 : 0];
     const int32_t k0 = static_cast<int32_t>(k * kTcBK);
-    if constexpr (kAMn) {
+    if (skip_a) {
+    } else if constexpr (kAMn) {
       if (a_grouped) {
         tma_load_3d(sa, am, bar, 0, k0, static_cast<int32_t>(st.m0 / 32));
       } else {
@@ -523,6 +525,7 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
   }();
   L.pf_ahead = pf;  // measured: L2 prefetch ahead of the ring only slows fc (0 = off)
   L.a_grouped = false;
+  L.skip_a = false;
   if constexpr (kAMn) {
     L.a_grouped = m % kTcBM == 0;
     if (L.a_grouped) {
@@ -600,6 +603,8 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
   Sched sc = make_sched(mt, static_cast<uint32_t>((n + kPBN - 1) / kPBN),
                         static_cast<uint32_t>((k + kTcBK - 1) / kTcBK), segs, kPBN, kAMn, false,
                         kFcMinSkIters);
+  L.skip_a = (sc.probe & 4) != 0;
+  if (L.skip_a) sc.stage_bytes -= sc.a_bytes;
   const uint32_t zc = sched_zero_col(sc, kPBN);
   if (zc < n) {
     cudaError_t e = launch_zero2d(c + zc, n, n - zc, m, s);
