@@ -287,6 +287,26 @@ lcnn_status lcnn_conv_forward_packed(const float* src, const void* d_packed,
                                      int precision, void* d_workspace,
                                      size_t workspace_bytes, void* stream);
 
+/* lcnn_conv_forward_packed with caller-owned SYNC WORDS: d_sync is NULL
+ * (== lcnn_conv_forward_packed) or LCNN_SYNC_BYTES of 8-byte-aligned device
+ * memory, zero before its first use, that belongs to ONE call site (e.g. one
+ * network layer on one stream) whose launches never overlap in time.  A
+ * persistent tensor-core kernel whose stream-K tail adds fragments into the
+ * output then zeroes that output region itself, overlapped with its operand
+ * loads, instead of needing a separate zeroing launch ahead of it; the
+ * kernel leaves the words zero again.  Results are those of
+ * lcnn_conv_forward_packed. */
+#define LCNN_SYNC_BYTES 16
+lcnn_status lcnn_conv_forward_packed_ex(const float* src, const void* d_packed,
+                                        float* dst, uint32_t n, uint32_t c_i,
+                                        uint32_t h, uint32_t w, int layout,
+                                        uint32_t c_o, uint32_t f_h,
+                                        uint32_t f_w, uint32_t stride,
+                                        uint32_t pad, int precision,
+                                        void* d_workspace,
+                                        size_t workspace_bytes, void* d_sync,
+                                        void* stream);
+
 /* Convolution followed by max pooling as ONE kernel (the run_network layer
  * pair conv -> pool, net.cpp:284-353, when the pool consumes the conv output
  * in the same layout): the conv output never reaches HBM.  Supported for
@@ -357,6 +377,15 @@ lcnn_status lcnn_fc_forward_packed(const float* x, int x_layout,
                                    uint64_t n, uint64_t k, int precision,
                                    void* d_workspace, size_t workspace_bytes,
                                    void* stream);
+/* lcnn_fc_forward_packed with caller-owned sync words (d_sync: see
+ * lcnn_conv_forward_packed_ex): the stream-K output is zeroed inside the fc
+ * kernel instead of by a separate launch. */
+lcnn_status lcnn_fc_forward_packed_ex(const float* x, int x_layout,
+                                      const void* d_packed, float* y,
+                                      uint64_t m, uint64_t n, uint64_t k,
+                                      int precision, void* d_workspace,
+                                      size_t workspace_bytes, void* d_sync,
+                                      void* stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -96,6 +96,8 @@ _SIGNATURES = {
                                [c_int, _P]),
     "lcnn_conv_forward_packed": (c_int, [_P, _P, _P] + [_U32] * 4 + [c_int] + [_U32] * 5 +
                                  [c_int, _P, c_size_t, _P]),
+    "lcnn_conv_forward_packed_ex": (c_int, [_P, _P, _P] + [_U32] * 4 + [c_int] + [_U32] * 5 +
+                                    [c_int, _P, c_size_t, _P, _P]),
     "lcnn_conv_maxpool_supported": (c_int, [_U32] * 4 + [c_int] + [_U32] * 5 + [c_int] +
                                     [_U32] * 2),
     "lcnn_conv_maxpool_packed": (c_int, [_P, _P, _P] + [_U32] * 4 + [c_int] + [_U32] * 5 +
@@ -110,7 +112,10 @@ _SIGNATURES = {
     "lcnn_fc_pack_weights": (c_int, [_P, _P, c_size_t, c_uint64, c_uint64, c_int, _P]),
     "lcnn_fc_forward_packed": (c_int, [_P, c_int, _P, _P, c_uint64, c_uint64, c_uint64, c_int, _P,
                                        c_size_t, _P]),
+    "lcnn_fc_forward_packed_ex": (c_int, [_P, c_int, _P, _P, c_uint64, c_uint64, c_uint64, c_int,
+                                          _P, c_size_t, _P, _P]),
 }
+SYNC_BYTES = 16  # LCNN_SYNC_BYTES
 
 _lib = None
 
@@ -158,5 +163,5 @@ def call(name: str, *args) -> int:
 __all__ = [
     "AccessReport", "PassReport", "PoolPlan", "lib", "call", "check", "declared_symbols", "LIB_PATH",
     "NCHW", "CHWN", "NHWC", "HWCN", "POOL_MAX", "POOL_AVG", "PREC_TF32", "PREC_3XTF32",
-    "LAYOUT_NAMES", "c_double", "PREC_FP32",
+    "LAYOUT_NAMES", "c_double", "PREC_FP32", "SYNC_BYTES",
 ]

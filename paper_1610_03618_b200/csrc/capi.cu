@@ -663,7 +663,20 @@ lcnn_status lcnn_conv_forward_packed(const float* src, const void* d_packed, flo
                                      uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
                                      uint32_t pad, int precision, void* d_workspace,
                                      size_t workspace_bytes, void* stream) {
+  return lcnn_conv_forward_packed_ex(src, d_packed, dst, n, c_i, h, w, layout, c_o, f_h, f_w,
+                                     stride, pad, precision, d_workspace, workspace_bytes, nullptr,
+                                     stream);
+}
+
+lcnn_status lcnn_conv_forward_packed_ex(const float* src, const void* d_packed, float* dst,
+                                        uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                                        int layout, uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                        uint32_t stride, uint32_t pad, int precision,
+                                        void* d_workspace, size_t workspace_bytes, void* d_sync,
+                                        void* stream) {
   if (!src || !d_packed || !dst) return fail(LCNN_EINVAL, "conv: null pointer");
+  if (reinterpret_cast<uintptr_t>(d_sync) & 7u)
+    return fail(LCNN_EINVAL, "conv: sync word must be 8-byte aligned");
   if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
     return fail(LCNN_EINVAL, "conv: packed filters must be 256-byte aligned");
   lcnn_impl::ConvArgs a;
@@ -675,6 +688,7 @@ lcnn_status lcnn_conv_forward_packed(const float* src, const void* d_packed, flo
   a.src = src;
   a.dst = dst;
   a.workspace = d_workspace;
+  a.zsync = static_cast<unsigned long long*>(d_sync);
   cudaError_t e = lcnn_impl::launch_conv_packed(a, d_packed, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "conv_forward_packed");
   return ok();
@@ -802,7 +816,17 @@ lcnn_status lcnn_fc_pack_weights(const float* weights, void* d_packed, size_t pa
 lcnn_status lcnn_fc_forward_packed(const float* x, int x_layout, const void* d_packed, float* y,
                                    uint64_t m, uint64_t n, uint64_t k, int precision,
                                    void* d_workspace, size_t workspace_bytes, void* stream) {
+  return lcnn_fc_forward_packed_ex(x, x_layout, d_packed, y, m, n, k, precision, d_workspace,
+                                   workspace_bytes, nullptr, stream);
+}
+
+lcnn_status lcnn_fc_forward_packed_ex(const float* x, int x_layout, const void* d_packed,
+                                      float* y, uint64_t m, uint64_t n, uint64_t k,
+                                      int precision, void* d_workspace, size_t workspace_bytes,
+                                      void* d_sync, void* stream) {
   if (!x || !d_packed || !y) return fail(LCNN_EINVAL, "fc: null pointer");
+  if (reinterpret_cast<uintptr_t>(d_sync) & 7u)
+    return fail(LCNN_EINVAL, "fc: sync word must be 8-byte aligned");
   if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
     return fail(LCNN_EINVAL, "fc: packed weights must be 256-byte aligned");
   if (m == 0 || n == 0 || k == 0) return fail(LCNN_ESHAPE, "gemm: empty operand");
@@ -817,7 +841,8 @@ lcnn_status lcnn_fc_forward_packed(const float* x, int x_layout, const void* d_p
       (!d_workspace && workspace_bytes))
     return fail(LCNN_EINVAL, "fc: workspace too small");
   cudaError_t e = lcnn_impl::launch_fc_packed(x, a_mn, d_packed, y, m, n, k, precision,
-                                              d_workspace, S(stream));
+                                              d_workspace, S(stream),
+                                              static_cast<unsigned long long*>(d_sync));
   if (e != cudaSuccess) return cuda_fail(e, "fc_forward_packed");
   return ok();
 }

@@ -1541,8 +1541,12 @@ struct ConvTcArgs {
 
 // Zero the stream-K region of out[co][col] (whole tiles inside it are
 // overwritten by plain stores anyway).  co_on_n: tile rows are columns.
-cudaError_t zero_sk_region(const Sched& sc, bool co_on_n, uint32_t bw, float* dst,
-                           uint32_t ncols, uint32_t co, cudaStream_t s, uint32_t tm = kTcBM) {
+// With a caller-owned sync word (ConvArgs::zsync) the persistent kernel
+// zeroes the region itself (Sched::zsync); pass sync = nullptr for kernels
+// that do not implement it.
+cudaError_t zero_sk_region(Sched& sc, bool co_on_n, uint32_t bw, float* dst, uint32_t ncols,
+                           uint32_t co, cudaStream_t s, uint32_t tm = kTcBM,
+                           unsigned long long* sync = nullptr) {
   if (sc.dp_tiles >= sc.mt * sc.nt) return cudaSuccess;
   const uint32_t nt0 = sc.dp_tiles / sc.mt;
   uint32_t row0, col0;
@@ -1553,7 +1557,11 @@ cudaError_t zero_sk_region(const Sched& sc, bool co_on_n, uint32_t bw, float* ds
     row0 = 0;
     col0 = nt0 * kPBN;
   }
-  return launch_zero2d(dst + uint64_t{row0} * ncols + col0, ncols, ncols - col0, co - row0, s);
+  return sched_zero_region(sc, sync, dst + uint64_t{row0} * ncols + col0, ncols, ncols - col0,
+                           co - row0, nt0 * sc.mt,
+                           [s](float* p, uint64_t pitch, uint64_t width, uint64_t rows) {
+                             return launch_zero2d(p, pitch, width, rows, s);
+                           });
 }
 
 template <bool kCoOnN>
@@ -1616,7 +1624,8 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
     while (n > 2 && 1024 + n * stride + epi + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
     sched_ring(sc, n, stride, 0);
   }
-  if (cudaError_t e = zero_sk_region(sc, kCoOnN, kCoOnN ? bn : kTcBM, a.dst, L.ncols, a.co, s);
+  if (cudaError_t e = zero_sk_region(sc, kCoOnN, kCoOnN ? bn : kTcBM, a.dst, L.ncols, a.co, s,
+                                     kTcBM, a.zsync);
       e != cudaSuccess)
     return e;
   if constexpr (kCoOnN) {
@@ -2001,12 +2010,13 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
     if (!make_cols_out_map(&O.y, O)) return cudaErrorInvalidValue;
     return launch_pair(L, O, sc, s);
   } else {
-  const Sched sc =
+  Sched sc =
       kCoOnN ? make_sched((L.ncols + kTcBM - 1) / kTcBM, (a.co + bw - 1) / bw, p.K / kTcBK, segs,
                           bw, true, false)
              : make_sched((a.co + kTcBM - 1) / kTcBM, (L.ncols + kPBN - 1) / kPBN, p.K / kTcBK,
                           segs, kPBN, false, true);
-  if (cudaError_t e = zero_sk_region(sc, kCoOnN, bw, a.dst, L.ncols, a.co, s); e != cudaSuccess)
+  if (cudaError_t e = zero_sk_region(sc, kCoOnN, bw, a.dst, L.ncols, a.co, s, kTcBM, a.zsync);
+      e != cudaSuccess)
     return e;
   if constexpr (kCoOnN) {
     ColsOut O{a.dst, L.ncols, a.co};

@@ -502,7 +502,8 @@ constexpr uint32_t kFcMinSkIters = 4;
 
 template <bool kAMn>
 cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t m, uint64_t n,
-                         uint64_t k, int precision, void* ws, cudaStream_t s) {
+                         uint64_t k, int precision, void* ws, cudaStream_t s,
+                         unsigned long long* zsync) {
   FcLoader<kAMn> L;
   const float* b0 = static_cast<const float*>(packed);
   const float* b1 = precision == LCNN_PREC_3XTF32 ? b0 + fc_packed_bytes(k, n, precision) / 8 : b0;
@@ -607,7 +608,10 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
   if (L.skip_a) sc.stage_bytes -= sc.a_bytes;
   const uint32_t zc = sched_zero_col(sc, kPBN);
   if (zc < n) {
-    cudaError_t e = launch_zero2d(c + zc, n, n - zc, m, s);
+    cudaError_t e = sched_zero_region(sc, zsync, c + zc, n, n - zc, m, (zc / kPBN) * sc.mt,
+                                      [s](float* p, uint64_t pitch, uint64_t width, uint64_t rows) {
+                                        return launch_zero2d(p, pitch, width, rows, s);
+                                      });
     if (e != cudaSuccess) return e;
   }
   return launch_gemm_out(L, c, n, static_cast<uint32_t>(m), static_cast<uint32_t>(n), sc, s);
@@ -621,9 +625,10 @@ bool fc_tc_supported(uint64_t m, uint64_t n, uint64_t k, bool a_mn) {
 }
 
 cudaError_t launch_fc_packed(const float* x, bool a_mn, const void* packed, float* c, uint64_t m,
-                             uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s) {
-  return a_mn ? launch_fc_tc<true>(x, packed, c, m, n, k, precision, ws, s)
-              : launch_fc_tc<false>(x, packed, c, m, n, k, precision, ws, s);
+                             uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s,
+                             unsigned long long* zsync) {
+  return a_mn ? launch_fc_tc<true>(x, packed, c, m, n, k, precision, ws, s, zsync)
+              : launch_fc_tc<false>(x, packed, c, m, n, k, precision, ws, s, zsync);
 }
 
 }  // namespace lcnn_impl

@@ -55,6 +55,10 @@ struct ConvArgs {
   int layout;  // LCNN_CHWN or LCNN_NCHW
   int precision;
   void* workspace;
+  // caller-owned 64-bit sync word (zero before first use, reserved for
+  // launches of one call site that never overlap): stream-K output regions
+  // are zeroed inside the kernel instead of by a zero2d launch (nullptr: launch)
+  unsigned long long* zsync = nullptr;
 };
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s);
 cudaError_t launch_conv_oracle(const ConvArgs& a, uint64_t sn, uint64_t sc, uint64_t sh,
@@ -86,8 +90,11 @@ cudaError_t launch_zero2d(void* p, uint64_t pitch_words, uint64_t width_words, u
                           cudaStream_t s);
 cudaError_t launch_fc_pack(const float* w, uint64_t k, uint64_t n, int precision, void* packed,
                            cudaStream_t s);
+// zsync: as ConvArgs::zsync (nullptr: the stream-K output is zeroed by a
+// zero2d launch ahead of the kernel)
 cudaError_t launch_fc_packed(const float* x, bool a_mn, const void* packed, float* c, uint64_t m,
-                             uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s);
+                             uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s,
+                             unsigned long long* zsync = nullptr);
 cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
                            uint64_t n, uint64_t k, int precision, void* ws,
                            cudaStream_t s);

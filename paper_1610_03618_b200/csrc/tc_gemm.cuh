@@ -115,6 +115,17 @@ struct Sched {
   // epilogue staging for TMA-store outputs (Out::kTmaStore): per epilogue
   // warp epi_bufs 4 KB boxes of 32 rows x 128 B (SWIZZLE_128B) at epi_off
   uint32_t epi_off, epi_bufs;
+  // In-kernel zeroing of the stream-K output region (zsync != nullptr; the
+  // persistent kernel only): instead of a zero2d launch ahead of the kernel,
+  // the epilogue warps of every CTA zero a 1/grid share of the zrows x zwidth
+  // words at zp (row pitch zpitch words) right after the PDL wait, then
+  // arrive on the caller's two sync words (zsync[0..1], zero before the
+  // launch and left zero after it); an epilogue stores into a tile
+  // t >= ztile (the first n-tile the region covers) only after all grid
+  // arrivals.  Launches sharing the words must never overlap in time.
+  unsigned long long* zsync;
+  float* zp;
+  uint32_t zpitch, zwidth, zrows, ztile;
 };
 
 // Out types that write their 32 x 32 accumulator chunks with TMA stores
@@ -318,6 +329,29 @@ inline uint32_t sched_zero_col(const Sched& s, uint32_t bn) {
   return s.dp_tiles == s.mt * s.nt ? ~0u : (s.dp_tiles / s.mt) * bn;
 }
 
+// Zero the stream-K output region (rows x width words at p, row pitch
+// `pitch` words, covering the tiles from `first_tile` on): in the persistent
+// kernel itself when the caller owns a sync word (Sched::zsync), else as a
+// zero2d launch ahead of it.  The launcher (zero2d) is passed in so that this
+// header stays free of the host library.
+template <class ZeroFn>
+inline cudaError_t sched_zero_region(Sched& s, unsigned long long* sync, float* p,
+                                     uint64_t pitch, uint64_t width, uint64_t rows,
+                                     uint32_t first_tile, ZeroFn&& zero2d) {
+  if (!width || !rows) return cudaSuccess;
+  const bool fits = pitch < (1ull << 32) && width * rows < (1ull << 31);
+  if (sync && fits) {
+    s.zsync = sync;
+    s.zp = p;
+    s.zpitch = static_cast<uint32_t>(pitch);
+    s.zwidth = static_cast<uint32_t>(width);
+    s.zrows = static_cast<uint32_t>(rows);
+    s.ztile = first_tile;
+    return cudaSuccess;
+  }
+  return zero2d(p, pitch, width, rows);
+}
+
 // Calls f(tile, kbeg, kend, split) for work unit `id` of `count` (a CTA, or
 // a CTA pair), in order.
 template <class F>
@@ -339,6 +373,58 @@ __device__ __forceinline__ void for_each_work(const Sched& s, uint32_t id, uint3
 template <class F>
 __device__ __forceinline__ void for_each_work(const Sched& s, F&& f) {
   for_each_work(s, blockIdx.x, gridDim.x, static_cast<F&&>(f));
+}
+
+// In-kernel zeroing (Sched::zsync): sync[0] counts the CTAs that zeroed
+// their share, sync[1] the CTAs that finished; the last CTA to finish resets
+// both, so the words are zero again for the next launch of the call site
+// (whatever its grid size).  Epilogue warps (2..5) of every CTA zero this
+// CTA's 1/grid share of the region and arrive.
+__device__ __forceinline__ void zero_region_arrive(const Sched& sc) {
+  const uint32_t tid = threadIdx.x - 64, G = gridDim.x;
+  const bool vec = ((sc.zwidth | sc.zpitch) & 3u) == 0 && (reinterpret_cast<uintptr_t>(sc.zp) & 15u) == 0;
+  const uint32_t w = vec ? sc.zwidth / 4 : sc.zwidth;
+  const uint32_t total = w * sc.zrows;  // host guarantees < 2^31
+  const uint32_t lo = static_cast<uint32_t>(static_cast<uint64_t>(total) * blockIdx.x / G);
+  const uint32_t hi = static_cast<uint32_t>(static_cast<uint64_t>(total) * (blockIdx.x + 1) / G);
+  for (uint32_t i = lo + tid; i < hi; i += 128) {
+    const uint32_t r = i / w, c = i - r * w;
+    if (vec)
+      reinterpret_cast<float4*>(sc.zp + static_cast<uint64_t>(r) * sc.zpitch)[c] =
+          make_float4(0.f, 0.f, 0.f, 0.f);
+    else
+      sc.zp[static_cast<uint64_t>(r) * sc.zpitch + c] = 0.0f;
+  }
+  // the stream-K fragments land through the async proxy (TMA add-reductions)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(sc.zsync, 1ull);
+  }
+}
+// An epilogue warp waits until every CTA of the grid zeroed its share
+// (acquire), before its first store into the region.
+__device__ __forceinline__ void zero_region_wait(const unsigned long long* sync, int lane) {
+  if (lane == 0) {
+    const unsigned long long G = gridDim.x;
+    unsigned long long v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(sync) : "memory");
+      if (v >= G) break;
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// One thread per CTA after the CTA's last store: the grid's last CTA resets
+// both words (every CTA has passed its wait by then).
+__device__ __forceinline__ void zero_region_depart(unsigned long long* sync) {
+  if (atomicAdd(sync + 1, 1ull) == gridDim.x - 1ull) {
+    atomicExch(sync, 0ull);
+    atomicExch(sync + 1, 0ull);
+  }
 }
 
 template <class Loader, class Out>
@@ -500,12 +586,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- epilogue ----------------
     const int q = warp & 3;
     uint32_t local = 0, epi_buf = 0;
+    bool zwait = sc.zsync != nullptr;
+    if (zwait) zero_region_arrive(sc);
     for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
       ++local;
       const uint32_t ntile = t / sc.mt;
       mbar_wait(&ctl->tfull[a], aphase);
       tc_fence_after();
+      if (zwait && t >= sc.ztile) {
+        zero_region_wait(sc.zsync, lane);
+        zwait = false;
+      }
       const uint32_t m = (t - ntile * sc.mt) * kTcBM + q * 32 + lane;
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
       epilogue_tile(out, sc, smem + sc.epi_off + q * sc.epi_bufs * 4096, base, m, ntile * sc.bn,
@@ -524,6 +616,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+  } else if (threadIdx.x == 64 && sc.zsync) {
+    zero_region_depart(sc.zsync);
   }
 }
 
@@ -964,7 +1058,9 @@ cudaError_t launch_pair(const Loader& ld, const Out& out, const Sched& sc, cudaS
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax || sc.grid % 2)
+  // the pair kernel has no in-kernel zeroing (Sched::zsync)
+  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax || sc.grid % 2 ||
+      sc.zsync)
     return cudaErrorInvalidConfiguration;
   return lcnn_pdl::launch(kern, sc.grid, kTcThreads, sc.smem_bytes, s, ld, out, sc);
 }
@@ -981,7 +1077,8 @@ cudaError_t launch_persistent(const Loader& ld, const Out& out, const Sched& sc,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax)
+  if (sc.smem_bytes > kMaxDynSmem || sc.stages < 2 || sc.stages > kPStagesMax ||
+      (OutStateful<Out>::value && sc.zsync))  // stateful epilogues never split tiles
     return cudaErrorInvalidConfiguration;
   return lcnn_pdl::launch(kern, sc.grid, kTcThreads, sc.smem_bytes, s, ld, out, sc);
 }

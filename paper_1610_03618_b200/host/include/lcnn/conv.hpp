@@ -52,9 +52,10 @@ std::shared_ptr<DeviceBuffer> pack_conv_filters(const DeviceTensor4D& in, const 
                                                 std::uint32_t c_o, std::uint32_t f_h,
                                                 std::uint32_t f_w, const ConvParams& p,
                                                 int precision);
+// d_sync (optional): lcnn_conv_forward_packed_ex's per-call-site sync words
 DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packed,
                                    std::uint32_t c_o, std::uint32_t f_h, std::uint32_t f_w,
-                                   const ConvParams& p, int precision);
+                                   const ConvParams& p, int precision, void* d_sync = nullptr);
 
 // Convolution and the max pooling that consumes it as one kernel
 // (lcnn_conv_maxpool_packed): returns the POOLED tensor, bit-identical to

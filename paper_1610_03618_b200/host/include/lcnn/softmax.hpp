@@ -49,9 +49,12 @@ DeviceMatrix fc_forward(const DeviceMatrix& in, const DeviceMatrix& weights);
 // the row-major matrix; other layouts are transformed to NCHW first.
 std::shared_ptr<DeviceBuffer> pack_fc_weights(const float* d_weights, std::uint32_t k,
                                               std::uint32_t n, int precision);
+// d_sync (optional): LCNN_SYNC_BYTES of zeroed device memory owned by this
+// call site (lcnn_fc_forward_packed_ex): the fc zeroes its stream-K output
+// in-kernel instead of launching a zeroing kernel first.
 DeviceMatrix fc_forward_packed(const DeviceMatrix& in, const void* d_packed, std::uint32_t n,
-                               int precision);
+                               int precision, void* d_sync = nullptr);
 DeviceMatrix fc_forward_packed(const DeviceTensor4D& in, const void* d_packed, std::uint32_t n,
-                               int precision);
+                               int precision, void* d_sync = nullptr);
 
 }  // namespace lcnn

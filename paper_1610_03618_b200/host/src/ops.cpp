@@ -352,7 +352,7 @@ std::shared_ptr<DeviceBuffer> pack_fc_weights(const float* d_weights, std::uint3
 namespace {
 
 DeviceMatrix fc_packed_run(const float* x, int layout, std::uint32_t m, std::uint32_t k,
-                           const void* d_packed, std::uint32_t n, int precision) {
+                           const void* d_packed, std::uint32_t n, int precision, void* d_sync) {
   DeviceMatrix out(m, n);
   const std::size_t ws = lcnn_fc_workspace_bytes(m, k, precision);
   void* wsp = nullptr;
@@ -362,25 +362,25 @@ DeviceMatrix fc_packed_run(const float* x, int layout, std::uint32_t m, std::uin
     wsp = buf.get();
     wsb = buf.bytes();
   }
-  check_status(lcnn_fc_forward_packed(x, layout, d_packed, out.data(), m, n, k, precision, wsp,
-                                      wsb, current_stream()));
+  check_status(lcnn_fc_forward_packed_ex(x, layout, d_packed, out.data(), m, n, k, precision, wsp,
+                                         wsb, d_sync, current_stream()));
   return out;
 }
 
 }  // namespace
 
 DeviceMatrix fc_forward_packed(const DeviceMatrix& in, const void* d_packed, std::uint32_t n,
-                               int precision) {
-  return fc_packed_run(in.data(), LCNN_NCHW, in.rows, in.cols, d_packed, n, precision);
+                               int precision, void* d_sync) {
+  return fc_packed_run(in.data(), LCNN_NCHW, in.rows, in.cols, d_packed, n, precision, d_sync);
 }
 
 DeviceMatrix fc_forward_packed(const DeviceTensor4D& in, const void* d_packed, std::uint32_t n,
-                               int precision) {
+                               int precision, void* d_sync) {
   const std::uint32_t k = in.c() * in.h() * in.w();
   if (in.layout() == Layout::CHWN && in.n() % 4 == 0)
-    return fc_packed_run(in.data(), LCNN_CHWN, in.n(), k, d_packed, n, precision);
+    return fc_packed_run(in.data(), LCNN_CHWN, in.n(), k, d_packed, n, precision, d_sync);
   const DeviceTensor4D rows = in.layout() == Layout::NCHW ? in : transform(in, Layout::NCHW);
-  return fc_packed_run(rows.data(), LCNN_NCHW, rows.n(), k, d_packed, n, precision);
+  return fc_packed_run(rows.data(), LCNN_NCHW, rows.n(), k, d_packed, n, precision, d_sync);
 }
 
 // ================================================================ conv ===
@@ -442,7 +442,7 @@ std::shared_ptr<DeviceBuffer> pack_conv_filters(const DeviceTensor4D& in, const 
 
 DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packed,
                                    std::uint32_t c_o, std::uint32_t f_h, std::uint32_t f_w,
-                                   const ConvParams& p, int precision) {
+                                   const ConvParams& p, int precision, void* d_sync) {
   const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f_h, f_w, p);
   DeviceTensor4D out(in.n(), c_o, ho, wo, in.layout());
   const std::size_t ws = lcnn_conv_packed_workspace_bytes(
@@ -454,9 +454,10 @@ DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packe
     wsp = buf.get();
     wsb = buf.bytes();
   }
-  check_status(lcnn_conv_forward_packed(in.data(), d_packed, out.data(), in.n(), in.c(), in.h(),
-                                        in.w(), code(in.layout()), c_o, f_h, f_w, p.stride, p.pad,
-                                        precision, wsp, wsb, current_stream()));
+  check_status(lcnn_conv_forward_packed_ex(in.data(), d_packed, out.data(), in.n(), in.c(),
+                                           in.h(), in.w(), code(in.layout()), c_o, f_h, f_w,
+                                           p.stride, p.pad, precision, wsp, wsb, d_sync,
+                                           current_stream()));
   return out;
 }
 

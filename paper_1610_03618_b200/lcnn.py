@@ -389,8 +389,10 @@ def pack_conv_filters(x: DeviceTensor4D, filters, c_o, f_h, f_w, stride=1, pad=0
 
 
 def conv_forward_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride=1, pad=0,
-                        precision=FP32, out=None, stream=None) -> DeviceTensor4D:
-    """conv_forward on filters made by pack_conv_filters for this geometry."""
+                        precision=FP32, out=None, stream=None, sync=None) -> DeviceTensor4D:
+    """conv_forward on filters made by pack_conv_filters for this geometry.
+    sync: optional CUDA tensor of >= capi.SYNC_BYTES zeroed bytes owned by
+    this call site (lcnn_conv_forward_packed_ex: in-kernel stream-K zeroing)."""
     torch = _torch()
     ho, wo = conv_output_extents(x.h, x.w, f_h, f_w, stride, pad)
     if out is None:
@@ -400,8 +402,9 @@ def conv_forward_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride=1, pad=
     geo = (x.n, x.c, x.h, x.w, x.layout, c_o, f_h, f_w, stride, pad, precision)
     nbytes = capi.lib().lcnn_conv_packed_workspace_bytes(*geo)
     ws = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32, device=x.data.device)
-    capi.call("lcnn_conv_forward_packed", x.ptr(), packed.data_ptr(), out.ptr(), *geo,
-              ws.data_ptr(), ws.numel() * 4, _stream(stream))
+    capi.call("lcnn_conv_forward_packed_ex", x.ptr(), packed.data_ptr(), out.ptr(), *geo,
+              ws.data_ptr(), ws.numel() * 4, sync.data_ptr() if sync is not None else None,
+              _stream(stream))
     return out
 
 
@@ -459,16 +462,20 @@ def pack_fc_weights(weights, k, n, precision=TF32, stream=None):
     return packed
 
 
-def fc_forward_packed(x, x_layout, packed, m, n, k, precision=TF32, out=None, stream=None):
+def fc_forward_packed(x, x_layout, packed, m, n, k, precision=TF32, out=None, stream=None,
+                      sync=None):
     """y (m x n) = x . W on packed weights.  x_layout NCHW: x is m rows of k;
-    CHWN: x is [k][m] (a CHWN producer, flattened in the operand load)."""
+    CHWN: x is [k][m] (a CHWN producer, flattened in the operand load).
+    sync: optional zeroed CUDA tensor of >= capi.SYNC_BYTES bytes owned by this
+    call site (lcnn_fc_forward_packed_ex: in-kernel stream-K zeroing)."""
     torch = _torch()
     if out is None:
         out = torch.empty(m * n, dtype=torch.float32, device=x.device)
     nbytes = capi.lib().lcnn_fc_workspace_bytes(m, k, precision)
     ws = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32, device=x.device)
-    capi.call("lcnn_fc_forward_packed", x.data_ptr(), x_layout, packed.data_ptr(), out.data_ptr(),
-              m, n, k, precision, ws.data_ptr(), ws.numel() * 4, _stream(stream))
+    capi.call("lcnn_fc_forward_packed_ex", x.data_ptr(), x_layout, packed.data_ptr(),
+              out.data_ptr(), m, n, k, precision, ws.data_ptr(), ws.numel() * 4,
+              sync.data_ptr() if sync is not None else None, _stream(stream))
     return out
 
 

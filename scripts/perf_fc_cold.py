@@ -14,7 +14,11 @@ sys.path.insert(0, ".")
 from paper_1610_03618_b200 import lcnn  # noqa: E402
 
 dev = torch.device("cuda:0")
-res = {"probe": os.environ.get("LCNN_TC_PROBE", "0"), "splitk": os.environ.get("LCNN_FC_SPLITK", "1")}
+res = {"probe": os.environ.get("LCNN_TC_PROBE", "0"), "splitk": os.environ.get("LCNN_FC_SPLITK", "1"),
+       "sync": os.environ.get("LCNN_FC_SYNC", "0")}
+# LCNN_FC_SYNC=1: per-call-site sync words (lcnn_fc_forward_packed_ex), the
+# stream-K output zeroed in-kernel instead of by a zeroing launch
+sync = torch.zeros(2, dtype=torch.int64, device=dev) if res["sync"] == "1" else None
 for name, (k, n, lay) in {"fc6": (9216, 4096, lcnn.CHWN), "fc7": (4096, 4096, lcnn.NCHW),
                           "fc8": (4096, 1000, lcnn.NCHW)}.items():
     m = 128
@@ -25,7 +29,8 @@ for name, (k, n, lay) in {"fc6": (9216, 4096, lcnn.CHWN), "fc7": (4096, 4096, lc
     copies = max(1, -(-320 * 2**20 // pk0.numel()))
     pks = [pk0] + [pk0.clone() for _ in range(copies - 1)]
     y = torch.empty(m * n, device=dev)
-    runs = [lambda p=p: lcnn.fc_forward_packed(x, lay, p, m, n, k, lcnn.TF32, out=y) for p in pks]
+    runs = [lambda p=p: lcnn.fc_forward_packed(x, lay, p, m, n, k, lcnn.TF32, out=y, sync=sync)
+            for p in pks]
     for r in runs:
         r()
     torch.cuda.synchronize()

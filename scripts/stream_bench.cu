@@ -95,7 +95,7 @@ int main() {
   CK(cudaMalloc(&buf, sizes[1] * copies));
   CK(cudaMemset(buf, 1, sizes[1] * copies));
   CK(cudaMalloc(&sink, 8));
-  CK(cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+  CK(cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 231424));
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));

@@ -250,3 +250,67 @@ def test_fc_packed_rejects_fp32(cuda):
     w = torch.zeros(64, device=cuda)
     with pytest.raises(ValueError):
         lcnn.pack_fc_weights(w, 8, 8, lcnn.FP32)
+
+
+def test_fc_packed_sync_words_zero_in_kernel(cuda):
+    """lcnn_fc_forward_packed_ex: with caller-owned sync words the stream-K
+    output is zeroed inside the fc kernel (no zeroing launch).  The output
+    starts as NaN, so any element the kernel failed to zero before adding
+    fragments stays NaN; one set of words serves launches of different grid
+    sizes in a row and is left zero after each."""
+    import torch
+
+    from paper_1610_03618_b200 import capi
+
+    sync = torch.zeros(capi.SYNC_BYTES // 8, dtype=torch.int64, device=cuda)
+    for rep, (m, n, k) in enumerate([(128, 4096, 9216), (128, 4096, 4096), (256, 300, 96),
+                                     (132, 257, 36), (128, 4096, 9216)]):
+        g = torch.Generator(device=cuda).manual_seed(rep)
+        a = torch.rand(m, k, device=cuda, generator=g) * 2 - 1
+        w = torch.rand(k, n, device=cuda, generator=g) * 2 - 1
+        want = a.double() @ w.double()
+        bound = a.abs().double() @ w.abs().double()
+        packed = lcnn.pack_fc_weights(w.reshape(-1), k, n, lcnn.TF32)
+        for layout, x in ((NCHW, a.contiguous()), (CHWN, a.t().contiguous())):
+            if layout == CHWN and m % 4:
+                continue
+            out = torch.full((m * n,), float("nan"), device=cuda)
+            got = lcnn.fc_forward_packed(x.reshape(-1), layout, packed, m, n, k, lcnn.TF32,
+                                         out=out, sync=sync).view(m, n).double()
+            err = (got - want).abs()
+            assert bool((err <= tolerance(lcnn.TF32, got, want, bound)).all()), \
+                (m, n, k, layout, float(err.nan_to_num(1e30).max()))
+            torch.cuda.synchronize()
+            assert int(sync.abs().sum()) == 0, sync.tolist()
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[0] % 32 == 0])
+def test_conv_packed_sync_words_zero_in_kernel(cuda, case):
+    """lcnn_conv_forward_packed_ex on every CHWN route: the persistent
+    kernel's stream-K output region is zeroed in-kernel (NaN-filled output
+    before the launch), routes without in-kernel zeroing still launch the
+    zeroing kernel; the sync words end zero."""
+    import torch
+
+    from paper_1610_03618_b200 import capi
+
+    n, ci, h, w, co, f, stride, pad = case
+    g = torch.Generator(device=cuda).manual_seed(sum(case))
+    x = torch.rand(n, ci, h, w, device=cuda, generator=g) * 2 - 1
+    filt = torch.rand(co, ci, f, f, device=cuda, generator=g) * 2 - 1
+    want = _torch_conv64(x, filt, stride, pad)
+    bound = _torch_conv64(x.abs(), filt.abs(), stride, pad)
+    t = lcnn.DeviceTensor4D(n, ci, h, w, CHWN, x.permute(1, 2, 3, 0).contiguous().reshape(-1))
+    packed = lcnn.pack_conv_filters(t, filt.contiguous(), co, f, f, stride, pad, lcnn.TF32)
+    ho, wo = want.shape[2], want.shape[3]
+    sync = torch.zeros(capi.SYNC_BYTES // 8, dtype=torch.int64, device=cuda)
+    for _ in range(2):
+        out = lcnn.DeviceTensor4D(n, co, ho, wo, CHWN,
+                                  torch.full((n * co * ho * wo,), float("nan"), device=cuda))
+        lcnn.conv_forward_packed(t, packed, co, f, f, stride, pad, lcnn.TF32, out=out, sync=sync)
+        got = out.data.view(co, ho, wo, n).permute(3, 0, 1, 2).double()
+        err = (got - want).abs()
+        assert bool((err <= tolerance(lcnn.TF32, got, want, bound)).all()), \
+            (case, float(err.nan_to_num(1e30).max()))
+        torch.cuda.synchronize()
+        assert int(sync.abs().sum()) == 0, sync.tolist()
