@@ -105,6 +105,29 @@ __global__ void pack_filters_kernel(const float* __restrict__ f, float* __restri
   }
 }
 
+// TAPS row-pair filter image (C_o <= 64, stride 1): 128 rows x K2, K2 =
+// (FH + 1) * Ci * FW in the TAPS order with the filter row replaced by the
+// INPUT row offset dr = 0..FH of a two-output-row tile: row r < 64 is
+// channel r of output row oh (filter row fh = dr), row r >= 64 channel r - 64
+// of output row oh + 1 (fh = dr - 1); out-of-range filter rows and channels
+// are zero.
+__global__ void pack_filters_taps2_kernel(const float* __restrict__ f, float* __restrict__ out,
+                                          ConvGeomTc g, uint32_t K2) {
+  const uint64_t total = 128ull * K2;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t row = static_cast<uint32_t>(i / K2), k = static_cast<uint32_t>(i % K2);
+    const uint32_t c = k % 32, q = k / 32;
+    const uint32_t fw = q % g.FW, t = q / g.FW, cb = t % (g.Ci / 32), dr = t / (g.Ci / 32);
+    const uint32_t co = row & 63u, ci = cb * 32 + c;
+    const int fh = static_cast<int>(dr) - (row >= 64 ? 1 : 0);
+    float v = 0.0f;
+    if (co < g.Co && fh >= 0 && fh < static_cast<int>(g.FH))
+      v = f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw];
+    out[i] = v;
+  }
+}
+
 // The implicit im2col of the CHWN input is the MN-major operand: 4D TMA boxes
 // of 32 output columns (32 images of one output pixel) x 32 k-rows.  The
 // packed filters [co][K] are the K-major operand: one 2D box of 32 k x (tile
@@ -703,6 +726,11 @@ struct TapsParams {
   uint32_t FW, S, P, CB, OWB, G;
   uint32_t ni, nf, islot, ibox;  // input / filter ring slots, input slot and box bytes
   uint32_t ctl_off;
+  // ROW PAIRS (C_o <= 64, stride 1): a tile is two output rows; accumulator
+  // rows 0-63 are output row oh, 64-127 row oh + 1, the K loop runs over the
+  // FH + 1 input rows they share (pack_filters_taps2_kernel), so the 128-row
+  // MMA carries no padding rows and each input box serves both output rows
+  uint32_t rows2, Ho;
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __grid_constant__ TapsParams prm) {
@@ -746,7 +774,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
     uint32_t is = 0, iph = 0, fs = 0, fph = 0;
     for_each_work(sc, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
       const uint32_t mi = t % sc.mt, ni = t / sc.mt;
-      const uint32_t g = ni % prm.G, r = ni / prm.G, ob = r % prm.OWB, oh = r / prm.OWB;
+      const uint32_t g = ni % prm.G, r = ni / prm.G, ob = r % prm.OWB,
+                     oh = (r / prm.OWB) << prm.rows2;  // rows2: first row of the pair
       const int32_t y0 = static_cast<int32_t>(ob * kSharePix * prm.S) - static_cast<int32_t>(prm.P);
       const int32_t z0 = static_cast<int32_t>(oh * prm.S) - static_cast<int32_t>(prm.P);
       const int32_t co0 = static_cast<int32_t>(mi * kTcBM);
@@ -825,13 +854,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
     for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
       ++local;
-      const uint32_t mi = t % sc.mt, ni = t / sc.mt;
+      const uint32_t mi = t % sc.mt;
+      uint32_t ni = t / sc.mt;
       mbar_wait(&ctl->tfull[a], aphase);
       tc_fence_after();
-      const uint32_t m = mi * kTcBM + q * 32 + lane;
+      uint32_t m = mi * kTcBM + q * 32 + lane;
+      bool live = true;
+      if (prm.rows2) {  // warps 2-3 (lanes 64-127) hold output row oh + 1
+        const uint32_t og = prm.OWB * prm.G, pr = ni / og, rest = ni - pr * og;
+        const uint32_t oh = 2 * pr + (q >> 1);
+        live = oh < prm.Ho;  // warp-uniform
+        ni = oh * og + rest;
+        m = (q & 1) * 32 + lane;
+      }
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-      for (uint32_t c = 0; c < kPBN; c += 32) {
+      for (uint32_t c = 0; c < kPBN && live; c += 32) {
         float v[32];
         tmem_ld32(base + c, v);
         if (!(sc.probe & 2)) prm.out.store32(m, ni * kPBN + c, v, split);
@@ -1823,10 +1861,12 @@ TapsGeom taps_geom(const ConvArgs& a) {
   return q;
 }
 
-cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s) {
+cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = false) {
   const ConvArgs& a = t.a;
   const TapsGeom q = taps_geom(a);
   TapsParams prm;
+  prm.rows2 = rows2 ? 1u : 0u;
+  prm.Ho = a.ho;
   const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
   const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
                              static_cast<uint64_t>(a.n) * 4, 128,
@@ -1834,7 +1874,7 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s) {
   const uint32_t box[5] = {32, 32, q.bw, 1, 1};
   if (!make_tmap(&prm.x, t.x_hi, 5, dims, pitch, box, nullptr, 1)) return cudaErrorInvalidValue;
   const uint64_t K = t.p.K;
-  if (!make_tmap_2d(&prm.w, t.w_hi, K, a.co, K * 4, kTcBK, kTcBM, false))
+  if (!make_tmap_2d(&prm.w, t.w_hi, K, rows2 ? kTcBM : a.co, K * 4, kTcBK, kTcBM, false))
     return cudaErrorInvalidValue;
   prm.FW = a.fw;
   prm.S = a.stride;
@@ -1846,16 +1886,17 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s) {
   prm.nf = q.nf;
   prm.islot = q.islot;
   prm.ibox = q.ibox;
-  const uint32_t mt = (a.co + kTcBM - 1) / kTcBM, nt = a.ho * prm.OWB * prm.G;
-  prm.sc = make_sched(mt, nt, a.fh * prm.CB, 1, kSharePix * 32, false, true);
+  const uint32_t rows = rows2 ? (a.ho + 1) / 2 : a.ho;  // tile rows (row pairs)
+  const uint32_t mt = rows2 ? 1 : (a.co + kTcBM - 1) / kTcBM, nt = rows * prm.OWB * prm.G;
+  prm.sc = make_sched(mt, nt, (a.fh + prm.rows2) * prm.CB, 1, kSharePix * 32, false, true);
   prm.ctl_off = q.ni * q.islot + q.nf * kTcABytes;
   prm.out = ShareOut{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, prm.OWB,
                      prm.G};
   const Sched& sc = prm.sc;
   if (sc.dp_tiles < mt * nt) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
-    const uint64_t col0 =
-        static_cast<uint64_t>(sc.dp_tiles / mt / (prm.OWB * prm.G)) * a.wo * a.n;
+    const uint64_t col0 = (static_cast<uint64_t>(sc.dp_tiles / mt / (prm.OWB * prm.G))
+                           << prm.rows2) * a.wo * a.n;
     cudaError_t e = launch_zero2d(a.dst + col0, ncols, ncols - col0, a.co, s);
     if (e != cudaSuccess) return e;
   }
@@ -2043,7 +2084,8 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
 namespace {
 
 enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM,
-                 kRouteShare, kRouteShareRes, kRouteChwnPair, kRouteTaps, kRouteTapsN };
+                 kRouteShare, kRouteShareRes, kRouteChwnPair, kRouteTaps, kRouteTapsN,
+                 kRouteTaps2 };
 
 struct ConvRoute {
   RouteKind kind = kRouteSimt;
@@ -2169,6 +2211,19 @@ ConvRoute route_conv(const ConvArgs& a) {
       r.kind = kRouteTaps;
       r.p.g.mode = kModeTAPS;
       r.apack = static_cast<uint64_t>(a.co) * r.p.K;
+      // C_o <= 64 at stride 1: row pairs fill the 128-row MMA (output rows
+      // oh and oh + 1 on the two halves of M) instead of leaving half of it
+      // padding.  Profiling knob LCNN_CONV_TAPS2=0 keeps one row per tile.
+      static const bool taps2_off = [] {
+        const char* e = std::getenv("LCNN_CONV_TAPS2");
+        return e && e[0] == '0';
+      }();
+      if (!taps2_off && a.co <= 64 && a.stride == 1 && a.ho >= 2 &&
+          a.precision == LCNN_PREC_TF32) {
+        r.kind = kRouteTaps2;
+        r.p.K = (a.fh + 1) * a.ci * a.fw;
+        r.apack = static_cast<uint64_t>(kTcBM) * r.p.K;
+      }
       return r;
     }
     // TAPS-N (tap-sharing boxes, channels on N, CTA pair) for 3x3 CI layers
@@ -2253,6 +2308,9 @@ cudaError_t launch_conv_pack(const ConvArgs& a, void* packed, cudaStream_t s) {
       pack_filters_row_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, nullptr, r.p.g,
                                                       (a.co + 7) / 8 * 8, r.apack);
       break;
+    case kRouteTaps2:
+      pack_filters_taps2_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, r.p.g, r.p.K);
+      break;
     default:
       pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, lo, r.p.g, r.p.K);
       break;
@@ -2315,6 +2373,7 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
   if (r.kind == kRouteTaps) return launch_chwn_taps(t, s);
+  if (r.kind == kRouteTaps2) return launch_chwn_taps(t, s, true);
   if (r.kind == kRouteTapsN) return launch_chwn_tapsn(t, s);
   if (r.kind == kRouteChwnPair) return launch_chwn_tc<true, true>(t, s);
   return r.kind == kRouteChwnOnN ? launch_chwn_tc<true>(t, s) : launch_chwn_tc<false>(t, s);

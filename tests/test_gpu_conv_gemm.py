@@ -88,7 +88,10 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     (128, 32, 27, 27, 192, 3, 1, 1),   # CI, conv2-like channel tile (N = 192, 96 per CTA)
     (128, 16, 27, 27, 48, 5, 1, 2),    # WIN
     # channel planes >= 4 MB: TAPS mode (one box per filter row serves all its taps)
-    (128, 32, 92, 92, 64, 3, 1, 1),    # C_o 64: half-empty 128-channel tile
+    (128, 32, 92, 92, 64, 3, 1, 1),    # C_o 64: TAPS row pairs (rows oh, oh+1 on the two M halves)
+    (128, 32, 91, 91, 48, 3, 1, 1),    # row pairs, odd H_o (last pair has one row), C_o 48
+    (128, 64, 92, 92, 64, 5, 1, 2),    # row pairs, 5x5 (6 input rows per pair)
+    (64, 32, 130, 130, 64, 3, 1, 0),   # row pairs, no padding
     (64, 32, 130, 130, 160, 3, 2, 1),  # stride 2, two channel tiles, 32-image groups x 2
     # CI, output rows >= 28, planes < 4 MB: TAPS-N (4-pixel x 32-image tiles on a CTA pair)
     (64, 32, 30, 30, 96, 3, 1, 1),     # C_o 96: 48-row filter halves per CTA
