@@ -287,6 +287,9 @@ struct ChwnRowLoader {
   // with w padded to FP so a group is exactly KR = Ci * FP rows (whole
   // 1 KB swizzle atoms); the padded taps have zero weights
   bool grouped;
+  // row pairs (channels on M, C_o <= 64, stride 1): columns are (row pair,
+  // ow, n), g.FH counts the F_h + 1 input rows of a pair (RowsPairOut)
+  bool rows2;
   static constexpr bool kAMajorMN = kCoOnN, kBMajorMN = !kCoOnN, kZeroSmem = true;
   static constexpr bool kResidentA = false;
   static constexpr int kSteps = 0;
@@ -328,7 +331,7 @@ struct ChwnRowLoader {
     for (int j = 0; j < kBoxes; ++j) {
       const uint32_t col = col0 + span * j;
       const uint32_t pos = col / g.N;
-      const uint32_t oh = pos / g.Wo, ow = pos - oh * g.Wo;
+      const uint32_t ohp = pos / g.Wo, ow = pos - ohp * g.Wo, oh = rows2 ? 2 * ohp : ohp;
       const uint32_t nn = col - pos * g.N;
       st.n0[j] = static_cast<int32_t>(grouped ? nn / 32 : nn);
       st.y0[j] = static_cast<int32_t>(ow * g.S) - static_cast<int32_t>(g.P);
@@ -400,6 +403,60 @@ __global__ void pack_filters_row_kernel(const float* __restrict__ f, float* __re
     }
   }
 }
+
+// Row-pair ROW image (C_o <= 64, stride 1): img[(dr * KR/4 + q) * 128 + r][e]
+// for input row offset dr = 0..FH of a two-output-row tile; row r < 64 is
+// channel r of output row oh (filter row fh = dr), r >= 64 channel r - 64 of
+// row oh + 1 (fh = dr - 1); zero outside the filter.
+__global__ void pack_filters_row2_kernel(const float* __restrict__ f, float* __restrict__ hi,
+                                         ConvGeomTc g, uint64_t total) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = static_cast<uint32_t>(i & 3);
+    const uint64_t rest = i >> 2;
+    const uint32_t r = static_cast<uint32_t>(rest % 128);
+    const uint32_t q = static_cast<uint32_t>((rest / 128) % (g.KR / 4));
+    const uint32_t dr = static_cast<uint32_t>(rest / 128 / (g.KR / 4));
+    const uint32_t kk = 4 * q + e, co = r & 63u;
+    const int fh = static_cast<int>(dr) - (r >= 64 ? 1 : 0);
+    const uint32_t ci = kk / g.FP, fw = kk - ci * g.FP;
+    float v = 0.0f;
+    if (co < g.Co && ci < g.Ci && fw < g.FW && fh >= 0 && fh < static_cast<int>(g.FH))
+      v = f[((static_cast<uint64_t>(co) * g.Ci + ci) * g.FH + fh) * g.FW + fw];
+    hi[i] = v;
+  }
+}
+
+// Row-pair output (ChwnRowLoader::rows2): accumulator rows 0-63 are output
+// row 2p's channels, 64-127 row 2p + 1's; tile columns are (p, ow, n).  A
+// 32 x 32 chunk never straddles the halves or a pixel, so it maps to one
+// TMA box of the RowsOut view {ncols, C_o}.
+struct RowsPairOut {
+  float* c;
+  uint64_t ldc;       // real columns Ho * Wo * N
+  uint32_t M, span, ho;  // C_o, Wo * N, Ho
+  CUtensorMap y;
+  static constexpr bool kTmaStore = true, kTmaTransposed = false;
+  __device__ __forceinline__ bool remap(uint32_t& m, uint32_t& n) const {
+    const uint32_t pr = n / span, oh = 2 * pr + (m >= 64 ? 1u : 0u);
+    m &= 63u;
+    n = oh * span + (n - pr * span);
+    return oh < ho;
+  }
+  __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
+                                            bool add) const {
+    if (!remap(m0, n0) || m0 >= M) return;
+    if (add)
+      tma_add_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
+    else
+      tma_store_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
+  }
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
+                                          bool add) const {
+    if (!remap(m, n0)) return;  // warp-uniform (one pixel, one half)
+    warp_store_rows32(m < M ? c + m * ldc + n0 : nullptr, v, add);
+  }
+};
 
 struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a multiple of 32)
   float* c;
@@ -1603,7 +1660,7 @@ cudaError_t zero_sk_region(Sched& sc, bool co_on_n, uint32_t bw, float* dst, uin
 }
 
 template <bool kCoOnN>
-cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
+cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s, bool rows2 = false) {
   const ConvArgs& a = t.a;
   const TcPlan& p = t.p;
   const uint32_t kr = p.g.KR, bn = kCoOnN ? co_tile_n(a.co) : kTcBM;  // filter tile rows
@@ -1628,13 +1685,16 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
       return cudaErrorInvalidValue;
   }
   L.g = p.g;
-  L.ncols = a.ho * a.wo * a.n;
+  L.rows2 = rows2 && !kCoOnN;
+  const uint32_t span = a.wo * a.n;  // columns of one output row
+  L.ncols = L.rows2 ? (a.ho + 1) / 2 * span : a.ho * span;
+  if (L.rows2) L.g.FH = a.fh + 1;  // input rows per row pair
   L.bn = bn;
   const bool x3 = a.precision == LCNN_PREC_3XTF32;
   const uint32_t ctiles = (a.co + bn - 1) / bn;
   Sched sc = kCoOnN ? make_sched((L.ncols + kTcBM - 1) / kTcBM, ctiles, a.fh, x3 ? 3 : 1, bn,
                                  true, false)
-                    : make_sched(ctiles, (L.ncols + kPBN - 1) / kPBN, a.fh, x3 ? 3 : 1, kPBN,
+                    : make_sched(ctiles, (L.ncols + kPBN - 1) / kPBN, L.g.FH, x3 ? 3 : 1, kPBN,
                                  false, true);
   const uint32_t x_region = L.kBoxes * kr * 128;                  // input groups of KR rows
   const uint32_t in_bytes = L.kBoxes * a.ci * (L.grouped ? p.g.FP : a.fw) * 128;  // TMA bytes
@@ -1661,6 +1721,29 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s) {
     const uint32_t epi = kCoOnN ? 0 : 1024 + kEpiStageBytes;  // RowsOut TMA-store staging
     while (n > 2 && 1024 + n * stride + epi + 16 + sizeof(PCtl) > kMaxDynSmem) --n;
     sched_ring(sc, n, stride, 0);
+  }
+  if (L.rows2) {
+    if (sc.dp_tiles < sc.mt * sc.nt) {
+      // split tiles: zero every output row from the first split row pair on
+      // (tiles from the first one touching that pair wait for it)
+      const uint32_t pr0 = static_cast<uint32_t>(uint64_t{sc.dp_tiles / sc.mt} * kPBN / span);
+      const uint64_t ncols = uint64_t{a.ho} * span, col0 = uint64_t{2 * pr0} * span;
+      cudaError_t e = sched_zero_region(
+          sc, a.zsync, a.dst + col0, ncols, ncols - col0, a.co,
+          static_cast<uint32_t>(uint64_t{pr0} * span / kPBN) * sc.mt,
+          [s](float* z, uint64_t pitch, uint64_t width, uint64_t rows) {
+            return launch_zero2d(z, pitch, width, rows, s);
+          });
+      if (e != cudaSuccess) return e;
+    }
+    RowsPairOut O{a.dst, uint64_t{a.ho} * span, a.co, span, a.ho};
+    const uint64_t dims[2] = {O.ldc, a.co};
+    const uint64_t opitch[1] = {O.ldc * 4};
+    const uint32_t obox[2] = {32, 32};
+    if (!make_tmap(&O.y, a.dst, 2, dims, opitch, obox, nullptr, 0)) return cudaErrorInvalidValue;
+    Sched se = sc;
+    sched_epi(se, 0);
+    return launch_persistent(L, O, se, s);
   }
   if (cudaError_t e = zero_sk_region(sc, kCoOnN, kCoOnN ? bn : kTcBM, a.dst, L.ncols, a.co, s,
                                      kTcBM, a.zsync);
@@ -2085,7 +2168,7 @@ namespace {
 
 enum RouteKind { kRouteSimt, kRouteNchwTc, kRouteRowOnN, kRouteRowOnM, kRouteChwnOnN, kRouteChwnOnM,
                  kRouteShare, kRouteShareRes, kRouteChwnPair, kRouteTaps, kRouteTapsN,
-                 kRouteTaps2 };
+                 kRouteTaps2, kRouteRowPairs };
 
 struct ConvRoute {
   RouteKind kind = kRouteSimt;
@@ -2175,6 +2258,19 @@ ConvRoute route_conv(const ConvArgs& a) {
     if (narrow) on_n = false;
     r.kind = on_n ? kRouteRowOnN : kRouteRowOnM;
     r.apack = static_cast<uint64_t>(pack_rows(a.co, on_n)) * r.p.K;
+    // C_o <= 64 on M at stride 1: row pairs (output rows oh, oh + 1 on the
+    // two halves of the 128-row MMA, F_h + 1 shared input rows; as TAPS row
+    // pairs).  Profiling knob LCNN_CONV_ROW2=0 keeps one row per tile.
+    static const bool row2_off = [] {
+      const char* e = std::getenv("LCNN_CONV_ROW2");
+      return e && e[0] == '0';
+    }();
+    if (!on_n && !row2_off && !force && a.co <= 64 && a.stride == 1 && a.ho >= 2 &&
+        a.precision == LCNN_PREC_TF32) {
+      r.kind = kRouteRowPairs;
+      r.p.K = (a.fh + 1) * kr;
+      r.apack = static_cast<uint64_t>(kTcBM) * r.p.K;
+    }
   } else {
     // CI / WIN: channels on N on a CTA pair (each SM streams half the filter
     // tile) when the layer is long enough for >= 4 waves of 256-column pair
@@ -2311,6 +2407,9 @@ cudaError_t launch_conv_pack(const ConvArgs& a, void* packed, cudaStream_t s) {
     case kRouteTaps2:
       pack_filters_taps2_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, r.p.g, r.p.K);
       break;
+    case kRouteRowPairs:
+      pack_filters_row2_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, r.p.g, r.apack);
+      break;
     default:
       pack_filters_kernel<<<148 * 4, 256, 0, s>>>(a.filters, hi, lo, r.p.g, r.p.K);
       break;
@@ -2372,6 +2471,7 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
     return launch_chwn_share(t, r.kind == kRouteShareRes, s);
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
+  if (r.kind == kRouteRowPairs) return launch_chwn_row<false>(t, s, true);
   if (r.kind == kRouteTaps) return launch_chwn_taps(t, s);
   if (r.kind == kRouteTaps2) return launch_chwn_taps(t, s, true);
   if (r.kind == kRouteTapsN) return launch_chwn_tapsn(t, s);

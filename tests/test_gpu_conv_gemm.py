@@ -73,7 +73,9 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     (64, 3, 35, 35, 96, 11, 4, 0),    # conv1-like: ROW mode, 33 -> 40 k-rows per filter row
     (32, 96, 13, 13, 64, 5, 1, 2),    # WIN FP=8 (ci % 32 == 0 -> CI mode actually)
     (32, 16, 10, 10, 48, 5, 2, 2),    # WIN FP=8 (80 k-rows: too many for ROW)
-    (32, 3, 12, 12, 20, 3, 1, 1),     # ROW, co < 32
+    (32, 3, 12, 12, 20, 3, 1, 1),     # ROW row pairs, co < 32
+    (128, 3, 33, 33, 64, 3, 1, 1),    # ROW row pairs, grouped boxes, odd H_o
+    (64, 5, 20, 20, 48, 3, 1, 0),     # ROW row pairs, ungrouped, no padding
     (128, 32, 6, 6, 160, 1, 1, 0),    # 1x1, co > 128
     (96, 64, 7, 7, 64, 3, 2, 0),
     (128, 384, 13, 13, 256, 3, 1, 1),  # conv4: 170 tiles -> 148 whole + stream-K tail
