@@ -219,3 +219,57 @@ def test_network_runs_tuned_pool_plans(cuda):
     want = Ref.run_network(text, x, NCHW, 257, 32, seed=42)
     assert approx_equal(dy.cpu().numpy().reshape(rows, cols), want, 1e-5)
     net.close()
+
+
+def test_forward_concurrent_streams_and_graph_replay_agree(cuda):
+    """In-kernel stream-K zeroing keeps per-stream / per-capture sync words
+    (Network::sync_words): forwards on two streams at once, and a captured
+    CUDA graph replayed on a third stream while a stream forward runs, give
+    the single-stream logits.  AlexNet at batch 128, TF32: conv4 / conv5 /
+    fc6 / fc7 all have stream-K tails (the in-kernel zeroing path)."""
+    import os
+
+    import torch
+
+    text = open(os.path.join(os.path.dirname(__file__), "..", "configs", "alexnet.json")).read()
+    net = netapi.Network(text, 257, 32, seed=42, precision=capi.PREC_TF32)
+    info = net.info(NCHW)
+    rows, cols = info["out"]
+    dn, dc, dh, dw = info["dims"]
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x = torch.rand(dn * dc * dh * dw, device=cuda, generator=g) * 2 - 1
+    lay = info["first_layout"]
+    main = torch.cuda.current_stream(cuda)
+    ref = torch.empty(rows * cols, device=cuda)
+    net.forward(x.data_ptr(), lay, ref.data_ptr(), main.cuda_stream)
+    torch.cuda.synchronize()
+    s1, s2, s3 = (torch.cuda.Stream(cuda) for _ in range(3))
+    y1 = torch.empty_like(ref)
+    y2 = torch.empty_like(ref)
+    for _ in range(4):
+        y1.fill_(float("nan"))
+        y2.fill_(float("nan"))
+        torch.cuda.synchronize()
+        net.forward(x.data_ptr(), lay, y1.data_ptr(), s1.cuda_stream)
+        net.forward(x.data_ptr(), lay, y2.data_ptr(), s2.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.allclose(y1, ref, rtol=1e-4, atol=1e-7)
+        assert torch.allclose(y2, ref, rtol=1e-4, atol=1e-7)
+    yg = torch.empty_like(ref)
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(cuda)
+    cap.wait_stream(main)
+    with torch.cuda.graph(graph, stream=cap):
+        net.forward(x.data_ptr(), lay, yg.data_ptr(), cap.cuda_stream)
+    torch.cuda.synchronize()
+    for _ in range(4):
+        yg.fill_(float("nan"))
+        y1.fill_(float("nan"))
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s3):
+            graph.replay()
+        net.forward(x.data_ptr(), lay, y1.data_ptr(), s1.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.allclose(yg, ref, rtol=1e-4, atol=1e-7)
+        assert torch.allclose(y1, ref, rtol=1e-4, atol=1e-7)
+    net.close()
