@@ -908,6 +908,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
     // ---------------- epilogue ----------------
     const int q = warp & 3;
     uint32_t local = 0;
+    bool zwait = sc.zsync != nullptr;  // in-kernel stream-K zeroing (Sched::zsync)
+    if (zwait) zero_region_arrive(sc);
     for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
       ++local;
@@ -915,6 +917,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
       uint32_t ni = t / sc.mt;
       mbar_wait(&ctl->tfull[a], aphase);
       tc_fence_after();
+      if (zwait && t >= sc.ztile) {
+        zero_region_wait(sc.zsync, lane);
+        zwait = false;
+      }
       uint32_t m = mi * kTcBM + q * 32 + lane;
       bool live = true;
       if (prm.rows2) {  // warps 2-3 (lanes 64-127) hold output row oh + 1
@@ -941,6 +947,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+  } else if (threadIdx.x == 64 && sc.zsync) {
+    zero_region_depart(sc.zsync);
   }
 }
 
@@ -1107,6 +1115,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     uint8_t* box = smem + prm.epi_off + q * 4096;
     const uint32_t col = ((static_cast<uint32_t>(lane) >> 2) << 4) | ((lane & 3) << 2);
     uint32_t local = 0;
+    bool zwait = sc.zsync != nullptr;  // in-kernel stream-K zeroing (Sched::zsync)
+    if (zwait) zero_region_arrive(sc);
     for_each_work(sc, pair, npairs, [&](uint32_t t, uint32_t, uint32_t, bool split) {
       const uint32_t a = local & 1, aphase = (local >> 1) & 1;
       ++local;
@@ -1115,6 +1125,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       const uint32_t ow = ob * kTapsNPix + q;
       mbar_wait(&ctl->tfull[a], aphase);
       tc_fence_after();
+      if (zwait && t >= sc.ztile) {
+        zero_region_wait(sc.zsync, lane);
+        zwait = false;
+      }
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
       for (uint32_t c = 0; c < prm.bw; c += 32) {
@@ -1150,6 +1164,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc_cg2<512>(tmem);
+  } else if (threadIdx.x == 64 && sc.zsync) {
+    zero_region_depart(sc.zsync);
   }
 }
 
@@ -1978,9 +1994,13 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
   const Sched& sc = prm.sc;
   if (sc.dp_tiles < mt * nt) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
-    const uint64_t col0 = (static_cast<uint64_t>(sc.dp_tiles / mt / (prm.OWB * prm.G))
-                           << prm.rows2) * a.wo * a.n;
-    cudaError_t e = launch_zero2d(a.dst + col0, ncols, ncols - col0, a.co, s);
+    const uint32_t r0 = sc.dp_tiles / mt / (prm.OWB * prm.G);  // first split tile row
+    const uint64_t col0 = (static_cast<uint64_t>(r0) << prm.rows2) * a.wo * a.n;
+    cudaError_t e = sched_zero_region(prm.sc, a.zsync, a.dst + col0, ncols, ncols - col0, a.co,
+                                      r0 * prm.OWB * prm.G * mt,
+                                      [s](float* z, uint64_t pitch, uint64_t width, uint64_t rows) {
+                                        return launch_zero2d(z, pitch, width, rows, s);
+                                      });
     if (e != cudaSuccess) return e;
   }
   const uint32_t smem = 1024 + prm.ctl_off + static_cast<uint32_t>(sizeof(TapsCtl));
@@ -2061,9 +2081,13 @@ cudaError_t launch_chwn_tapsn(const ConvTcArgs& t, cudaStream_t s) {
   const Sched& sc = prm.sc;
   if (sc.dp_tiles < mt * nt) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
-    const uint64_t col0 =
-        static_cast<uint64_t>(sc.dp_tiles / mt / (prm.OWB * prm.G2)) * a.wo * a.n;
-    cudaError_t e = launch_zero2d(a.dst + col0, ncols, ncols - col0, a.co, s);
+    const uint32_t r0 = sc.dp_tiles / mt / (prm.OWB * prm.G2);  // first split tile row
+    const uint64_t col0 = static_cast<uint64_t>(r0) * a.wo * a.n;
+    cudaError_t e = sched_zero_region(prm.sc, a.zsync, a.dst + col0, ncols, ncols - col0, a.co,
+                                      r0 * prm.OWB * prm.G2 * mt,
+                                      [s](float* z, uint64_t pitch, uint64_t width, uint64_t rows) {
+                                        return launch_zero2d(z, pitch, width, rows, s);
+                                      });
     if (e != cudaSuccess) return e;
   }
   const uint32_t smem = 1024 + prm.ctl_off + static_cast<uint32_t>(sizeof(TapsNCtl));

@@ -409,9 +409,13 @@ __device__ __forceinline__ void zero_region_wait(const unsigned long long* sync,
   if (lane == 0) {
     const unsigned long long G = gridDim.x;
     unsigned long long v;
-    while (true) {
+    for (uint32_t spins = 0;; ++spins) {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(sync) : "memory");
       if (v >= G) break;
+      // every CTA of the grid is resident (grid <= SMs, one CTA per SM), so
+      // the arrivals come within microseconds; seconds mean a CTA can never
+      // be scheduled (e.g. SMs withheld from the context): fail loudly
+      if (spins > (1u << 26)) __trap();
       __nanosleep(64);
     }
   }

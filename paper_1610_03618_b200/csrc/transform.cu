@@ -245,12 +245,22 @@ __global__ void __launch_bounds__(kThreads)
 // N = 1 (or any 1 x L) transpose: a copy.  A vectorised kernel rather than
 // cudaMemcpyAsync: the D2D copy engine moved VGG's 12.8 MB activation at
 // ~1.8 TB/s (transform_1 sweep, round 2).
+// Each thread keeps kCopyUnroll 16-B loads in flight before its stores (one
+// load per thread per trip left ~1.8 us of a 25 MB copy's ~5 us as latency).
+constexpr int kCopyUnroll = 4;
 __global__ void __launch_bounds__(kThreads)
     copy_f4_kernel(const float4* __restrict__ src, float4* __restrict__ dst, uint64_t n4) {
   LCNN_PDL_ENTRY();
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < n4;
-       i += static_cast<uint64_t>(gridDim.x) * kThreads)
-    stg_stream(dst + i, ldg_stream(src + i));
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
+  uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x;
+  for (; i + (kCopyUnroll - 1) * stride < n4; i += kCopyUnroll * stride) {
+    float4 v[kCopyUnroll];
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) v[u] = ldg_stream(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) stg_stream(dst + i + u * stride, v[u]);
+  }
+  for (; i < n4; i += stride) stg_stream(dst + i, ldg_stream(src + i));
 }
 
 // Generic permutation between any two of the four layouts (layout.cpp:77-97
@@ -364,8 +374,8 @@ cudaError_t launch_transpose2d(const float* src, float* dst, uint64_t rows,
     const uint64_t n = rows * cols;
     if (n % 4 || !aligned16(src) || !aligned16(dst))
       return cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, s);
-    uint64_t blocks = (n / 4 + kThreads - 1) / kThreads;
-    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    uint64_t blocks = (n / 4 + kThreads * kCopyUnroll - 1) / (kThreads * kCopyUnroll);
+    if (blocks > 148ull * 8) blocks = 148ull * 8;
     lcnn_pdl::launch(copy_f4_kernel, static_cast<uint32_t>(blocks), kThreads, 0, s,
                      reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), n / 4);
     return cudaGetLastError();
