@@ -508,6 +508,36 @@ def free_port():
     return port
 
 
+# Collective backend: NCCL (one GPU per rank).  LCNN_BENCH_BACKEND=gloo is a
+# test mode for a box with fewer GPUs than ranks (ranks then share cuda:0 and
+# the collectives run on host copies); its numbers are not scaling numbers.
+BACKEND = os.environ.get("LCNN_BENCH_BACKEND", "nccl")
+
+
+def all_reduce_max(dist, t):
+    if BACKEND == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t
+    h = t.cpu()
+    dist.all_reduce(h, op=dist.ReduceOp.MAX)
+    t.copy_(h)
+    return t
+
+
+def all_gather_flat(dist, out, t):
+    if BACKEND == "nccl":
+        dist.all_gather_into_tensor(out, t)
+        return out
+    parts = [torch_empty_like_cpu(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t.cpu())
+    out.copy_(__import__("torch").cat(parts).to(out.device))
+    return out
+
+
+def torch_empty_like_cpu(t):
+    return __import__("torch").empty(t.numel(), dtype=t.dtype)
+
+
 def relaunch_distributed(gpus):
     """`bench.py --gpus N` without a torchrun environment: re-exec through
     torch.distributed.run with N local ranks (one process per GPU)."""
@@ -568,15 +598,18 @@ def main():
     # one GPU per rank: LOCAL_RANK indexes the visible devices (a launcher
     # that masks each rank to one device leaves index 0)
     dev_index = local if local < count else local % count
-    if world > count and count > 1:
+    if world > count and count > 1 and BACKEND == "nccl":
         raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, {count} visible")
     torch.cuda.set_device(dev_index)
     device = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(BACKEND)
         dist.barrier()  # creates the communicator
-        print(f"bench.py: rank {rank}/{world} NCCL communicator up on cuda:{dev_index} "
-              f"(nranks={dist.get_world_size()})", file=sys.stderr, flush=True)
+        print(f"bench.py: rank {rank}/{world} {BACKEND.upper()} communicator up on "
+              f"cuda:{dev_index} (nranks={dist.get_world_size()})", file=sys.stderr, flush=True)
 
     def barrier():
         if world > 1:
@@ -679,7 +712,7 @@ def main():
         dom_ms = sum(a.elapsed_time(b) for a, b in dev_ev) / K
     t = torch.tensor([ms, dom_ms], device=device, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_max(dist, t)
     ms, dom_ms = float(t[0]), float(t[1])
     # whole-job bytes: the global batch for strong scaling, world x per-GPU for weak
     job_bytes = wl.step_bytes_global if wl.scaling == "strong" else step_bytes * world
@@ -840,7 +873,7 @@ def run_e2e(torch, device, ops, world, steps, barrier, dist, job_bytes=None):
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], device=device, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_max(dist, t)
     ms = float(t[0])
     step_bytes = job_bytes or sum(op.bytes for op in ops) * world
     value = step_bytes * steps / (ms / 1e3) / GB
@@ -991,7 +1024,7 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
     barrier()
     t = torch.tensor([e0.elapsed_time(e1)], device=device, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_max(dist, t)
     ms = float(t[0])
     value = batch * world * K / (ms / 1e3)
 
@@ -1047,7 +1080,7 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
                                   torch.ones(rows, device=device, dtype=torch.float64), atol=1e-4))
     if world > 1:
         gathered = torch.empty(world * rows * cols, device=device)
-        dist.all_gather_into_tensor(gathered, y)
+        all_gather_flat(dist, gathered, y)
         ok_rows = ok_rows and bool(torch.equal(gathered.view(world, -1)[rank], y))
     # end to end: host buffers through lcnn_net_forward_host_many -- every
     # batch's H2D (pinned) and logits D2H inside the timed region; batch i+1's
@@ -1065,7 +1098,7 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
         net.forward_host_many(ins, in_layout, outs)
         dt = torch.tensor([time.perf_counter() - t0], device=device, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            all_reduce_max(dist, dt)
         # hy[0] holds the last even batch, whose input hx[0] is x (stream-K
         # tiles add in any order, so compare within the tf32 logits tolerance)
         ok_e2e = bool(torch.allclose(hy[0], y.cpu(), rtol=1e-3, atol=1e-6))
