@@ -1947,7 +1947,14 @@ TapsGeom taps_geom(const ConvArgs& a) {
   q.ibox = q.bw * 4096;
   q.islot = (q.ibox + 1023) / 1024 * 1024;
   const uint64_t avail = kMaxDynSmem - 1024 - sizeof(TapsCtl) - 16;
-  for (uint32_t ni = 3; ni >= 2 && !q.ni; --ni) {
+  // input-box slots: 3 (profiling knob LCNN_TAPS_NI = 2..4 tries other rings;
+  // fewer input slots leave more filter slots)
+  static const uint32_t ni_max = [] {
+    const char* e = std::getenv("LCNN_TAPS_NI");
+    const int v = e ? std::atoi(e) : 3;
+    return static_cast<uint32_t>(v < 2 ? 2 : (v > 4 ? 4 : v));
+  }();
+  for (uint32_t ni = ni_max; ni >= 2 && !q.ni; --ni) {
     if (ni * uint64_t{q.islot} >= avail) continue;
     const uint64_t nf = std::min<uint64_t>(8, (avail - ni * uint64_t{q.islot}) / kTcABytes);
     if (nf >= std::max<uint64_t>(4, a.fw + 1)) {
