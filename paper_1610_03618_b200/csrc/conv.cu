@@ -788,6 +788,9 @@ struct TapsParams {
   // FH + 1 input rows they share (pack_filters_taps2_kernel), so the 128-row
   // MMA carries no padding rows and each input box serves both output rows
   uint32_t rows2, Ho;
+  // TMA-store epilogue (ShareOut boxes staged at epi_off, two 4 KB boxes per
+  // epilogue warp) instead of per-lane stores
+  uint32_t tma, epi_off;
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __grid_constant__ TapsParams prm) {
@@ -907,7 +910,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;
-    uint32_t local = 0;
+    uint32_t local = 0, epi_buf = 0;
     bool zwait = sc.zsync != nullptr;  // in-kernel stream-K zeroing (Sched::zsync)
     if (zwait) zero_region_arrive(sc);
     for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
@@ -931,16 +934,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
         m = (q & 1) * 32 + lane;
       }
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
+      if (prm.tma) {
+        if (live)
+          epilogue_tile(prm.out, sc, smem + prm.epi_off + q * 2 * 4096, base, m, ni * kPBN, split,
+                        epi_buf, lane);
+      } else {
 #pragma unroll 1
-      for (uint32_t c = 0; c < kPBN && live; c += 32) {
-        float v[32];
-        tmem_ld32(base + c, v);
-        if (!(sc.probe & 2)) prm.out.store32(m, ni * kPBN + c, v, split);
+        for (uint32_t c = 0; c < kPBN && live; c += 32) {
+          float v[32];
+          tmem_ld32(base + c, v);
+          if (!(sc.probe & 2)) prm.out.store32(m, ni * kPBN + c, v, split);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl->tempty[a]);
     });
+    if (prm.tma && lane == 0) bulk_wait_read_n<0>();  // staged boxes read before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -1941,12 +1951,12 @@ struct TapsGeom {
   bool ok;
 };
 
-TapsGeom taps_geom(const ConvArgs& a) {
+TapsGeom taps_geom(const ConvArgs& a, uint32_t reserve = 0) {
   TapsGeom q{};
   q.bw = a.stride * (kSharePix - 1) + a.fw;
   q.ibox = q.bw * 4096;
   q.islot = (q.ibox + 1023) / 1024 * 1024;
-  const uint64_t avail = kMaxDynSmem - 1024 - sizeof(TapsCtl) - 16;
+  const uint64_t avail = kMaxDynSmem - 1024 - sizeof(TapsCtl) - 16 - reserve;
   // input-box slots: 3 (profiling knob LCNN_TAPS_NI = 2..4 tries other rings;
   // fewer input slots leave more filter slots)
   static const uint32_t ni_max = [] {
@@ -1969,10 +1979,22 @@ TapsGeom taps_geom(const ConvArgs& a) {
 
 cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = false) {
   const ConvArgs& a = t.a;
-  const TapsGeom q = taps_geom(a);
+  // TMA-store epilogue for row pairs (measured on B200, VGG conv1_2 1461 -> 1450 us; slower on
+  // the C_o = 128 layers: conv2_1 534 -> 577, conv2_2 949 -> 984 us, whose per-lane stores
+  // overlap better; profiles/r02_taps_tma_ab.jsonl).  Profiling knob LCNN_TAPS_TMA = 0 off,
+  // 1 row pairs only (default), 2 always.
+  static const int tma_knob = [] {
+    const char* e = std::getenv("LCNN_TAPS_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool tma = tma_knob == 2 || (tma_knob == 1 && rows2);
+  constexpr uint32_t kEpi = 4 * 2 * 4096;
+  TapsGeom q = taps_geom(a, tma ? kEpi + 1024 : 0);
+  if (!q.ok) q = taps_geom(a);
   TapsParams prm;
   prm.rows2 = rows2 ? 1u : 0u;
   prm.Ho = a.ho;
+  prm.tma = tma && q.ok && taps_geom(a, kEpi + 1024).ok ? 1u : 0u;
   const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
   const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
                              static_cast<uint64_t>(a.n) * 4, 128,
@@ -1996,8 +2018,19 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
   const uint32_t mt = rows2 ? 1 : (a.co + kTcBM - 1) / kTcBM, nt = rows * prm.OWB * prm.G;
   prm.sc = make_sched(mt, nt, (a.fh + prm.rows2) * prm.CB, 1, kSharePix * 32, false, true);
   prm.ctl_off = q.ni * q.islot + q.nf * kTcABytes;
+  prm.epi_off = 0;
+  if (prm.tma) {
+    prm.epi_off = (prm.ctl_off + 1023) / 1024 * 1024;
+    prm.ctl_off = prm.epi_off + kEpi;
+    prm.sc.epi_bufs = 2;
+  }
   prm.out = ShareOut{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, prm.OWB,
                      prm.G};
+  if (prm.tma) {
+    if (!make_share_out_map(&prm.out.y, a)) return cudaErrorInvalidValue;
+    prm.out.fd_groups = FastDiv(prm.G);
+    prm.out.fd_owb = FastDiv(prm.OWB);
+  }
   const Sched& sc = prm.sc;
   if (sc.dp_tiles < mt * nt) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
