@@ -462,6 +462,7 @@ struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a mul
   float* c;
   uint64_t ldc;
   uint32_t M, N;
+  uint32_t keep_l2 = 0;  // TMA stores with an L2 evict_last hint (the next layer reads them)
   // TMA-store epilogue: 2D view {N cols, M rows} (pitch ldc), box {32, 32},
   // SWIZZLE_128B; out-of-range rows / columns of a box are clipped
   CUtensorMap y;
@@ -471,6 +472,8 @@ struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a mul
     if (n0 >= N || m0 >= M) return;
     if (add)
       tma_add_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
+    else if (keep_l2)
+      tma_store_2d_keep(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
     else
       tma_store_2d(&y, box, static_cast<int32_t>(n0), static_cast<int32_t>(m0));
   }
@@ -492,6 +495,7 @@ template <bool kTma>
 struct ColsOutT {
   float* c;
   uint32_t ncols, co;
+  uint32_t keep_l2 = 0;  // TMA stores with an L2 evict_last hint (profiling knob LCNN_KEEP_L2)
   // TMA-store epilogue (kTma): the RowsOut view {ncols, C_o}; a chunk is
   // 32 accumulator rows (columns of C) x 32 channels, staged transposed
   CUtensorMap y;
@@ -501,6 +505,8 @@ struct ColsOutT {
     if (m0 >= ncols || n0 >= co) return;
     if (add)
       tma_add_2d(&y, box, static_cast<int32_t>(m0), static_cast<int32_t>(n0));
+    else if (keep_l2)
+      tma_store_2d_keep(&y, box, static_cast<int32_t>(m0), static_cast<int32_t>(n0));
     else
       tma_store_2d(&y, box, static_cast<int32_t>(m0), static_cast<int32_t>(n0));
   }
@@ -1508,6 +1514,20 @@ inline bool make_rows_out_map(CUtensorMap* m, const RowsOut& o) {
 
 namespace {
 
+// The CTA-pair conv outputs are TMA-stored with an L2 evict_last hint, so
+// the next layer finds them in L2: measured on B200 (two boxes, alternating
+// runs), AlexNet conv2 -> pool2 20.7 -> 18.7 us, forward +0.7 / +1.2 %
+// (profiles/r02_keep_l2_ab.jsonl).  The same hint on the single-CTA RowsOut
+// (conv3-5) measured neutral.  Profiling knob LCNN_KEEP_L2: 0 off, 1 the
+// CTA-pair outputs (default), 2 also RowsOut.
+int keep_l2_knob() {
+  static const int k = [] {
+    const char* e = std::getenv("LCNN_KEEP_L2");
+    return e ? std::atoi(e) : 1;
+  }();
+  return k;
+}
+
 // Output-channel tile width when channels are the N side: one or two tiles of
 // <= 256, rounded to 32 (no padding of C_o = 96 / 192 to a 128-row tile).
 uint32_t co_tile_n(uint32_t co) {
@@ -1780,6 +1800,7 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s, bool rows2 = fa
     return launch_persistent(L, O, sc, s);
   } else {
     RowsOut O{a.dst, L.ncols, a.co, L.ncols};
+    O.keep_l2 = keep_l2_knob() >= 2;
     if (!make_rows_out_map(&O.y, O)) return cudaErrorInvalidValue;
     Sched se = sc;
     sched_epi(se, 0);  // RowsOut never has a resident operand
@@ -2195,6 +2216,7 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
     if (cudaError_t e = zero_sk_region(sc, true, bw, a.dst, L.ncols, a.co, s, tm); e != cudaSuccess)
       return e;
     ColsOut O{a.dst, L.ncols, a.co};
+    O.keep_l2 = keep_l2_knob() >= 1;
     if (!make_cols_out_map(&O.y, O)) return cudaErrorInvalidValue;
     return launch_pair(L, O, sc, s);
   } else {
@@ -2214,6 +2236,7 @@ cudaError_t launch_chwn_tc(const ConvTcArgs& t, cudaStream_t s) {
     return launch_persistent(L, O, se, s);
   } else {
     RowsOut O{a.dst, L.ncols, a.co, L.ncols};
+    O.keep_l2 = keep_l2_knob() >= 2;
     if (!make_rows_out_map(&O.y, O)) return cudaErrorInvalidValue;
     Sched se = sc;
     sched_epi(se, 0);

@@ -119,6 +119,18 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+// as tma_store_2d with an L2 eviction-priority hint (createpolicy): evict_last
+// keeps an output in L2 for the kernel that consumes it next
+__device__ __forceinline__ void tma_store_2d_keep(const CUtensorMap* m, const void* src, int32_t x,
+                                                  int32_t y) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(src)), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tma_add_2d(const CUtensorMap* m, const void* src, int32_t x,
                                            int32_t y) {
   asm volatile(
