@@ -92,3 +92,19 @@ def test_make_plan_mirror(kats):
         assert (p.kind == lcnn.TILED_2D) == (case["kind"] == "tiled")
         if case["kind"] == "tiled":
             assert p.tile == case["tile"] and p.wide_copy == case["wide"]
+
+
+def test_sync_word_entry_points_validate_before_the_device():
+    """lcnn_*_forward_packed_ex reject a misaligned sync word (and the plain
+    entries' null checks) with LCNN_EINVAL (11) before any device work."""
+    lib = capi.lib()
+    odd = ctypes.c_void_p(256 + 4)
+    st = lib.lcnn_fc_forward_packed_ex(DUMMY, capi.NCHW, DUMMY, DUMMY, 128, 4096, 9216,
+                                       capi.PREC_TF32, None, 0, odd, None)
+    assert st == 11 and b"sync word" in lib.lcnn_last_error()
+    st = lib.lcnn_conv_forward_packed_ex(DUMMY, DUMMY, DUMMY, 128, 384, 13, 13, capi.CHWN, 256,
+                                         3, 3, 1, 1, capi.PREC_TF32, None, 0, odd, None)
+    assert st == 11 and b"sync word" in lib.lcnn_last_error()
+    st = lib.lcnn_fc_forward_packed_ex(None, capi.NCHW, DUMMY, DUMMY, 128, 4096, 9216,
+                                       capi.PREC_TF32, None, 0, None, None)
+    assert st == 11 and b"null" in lib.lcnn_last_error()
