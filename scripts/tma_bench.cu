@@ -215,6 +215,9 @@ int main() {
   CK(cudaMemset(x, 0, 3000ull * 256 * 128));
   const int iters = 2000;
   auto zero = [](Cfg& c) { memset(&c, 0, sizeof(c)); };
+  // TB_ONLY=conv4: only the conv3-5 input-box comparison at the end
+  const bool only_c4 = getenv("TB_ONLY") != nullptr;
+  if (only_c4) goto conv4_boxes;
 
   // A: the conv1 ROW box {32 n, 11 w, 1 h, 3 c}, 4 n-groups per stage, walks (ow, oh)
   for (int swz = 0; swz < 3; ++swz) {
@@ -505,6 +508,62 @@ int main() {
       c.iters = iters;
       c.stages = 4;
       run("conv1 SHARE box x2 (2 groups) slots=4", c, sink);
+    }
+  }
+conv4_boxes:
+  // P/Q/R: AlexNet conv4 input (N=128, 13x13, C=384, CHWN: 33 MB, L2-resident),
+  // the CI k-block of a RowsOut tile: 32 channels x 2 output pixels x 128 images.
+  {
+    const uint64_t W4 = 13, H4 = 13, C4 = 384, plane = H4 * W4 * N * 4;
+    // P: shipped grouped 5D view {32 n, C, 4 g, W, H}, box {32, 32 c, 4 g, 1, 1} x 2 pixels
+    {
+      Cfg c;
+      zero(c);
+      const uint64_t dims[5] = {32, C4, 4, W4, H4};
+      const uint64_t str[4] = {plane, 128, N * 4, W4 * N * 4};
+      const uint32_t box[5] = {32, 32, 4, 1, 1};
+      if (encode(&c.map, x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+        c.rank = 5; c.nbox = 2; c.box_bytes = 32 * 32 * 4 * 4;
+        c.start[1][3] = 1;
+        c.step[1] = 32; c.wrap[1] = 384;
+        c.step[3] = 2; c.wrap[3] = 12;
+        c.cta_step[4] = 1; c.wrap[4] = 13;
+        c.iters = iters;
+        run("conv4 grouped 5D box{32,32,4,1,1} x2", c, sink);
+      }
+    }
+    // Q: (w, g) merged into one dim of stride 128 B: 4D view {32 n, C, 4W, H},
+    // ONE box {32, 32 c, 8, 1} lands both pixels' 8 atoms in the same order
+    for (int nb : {1, 2}) {
+      Cfg c;
+      zero(c);
+      const uint64_t dims[4] = {32, C4, 4 * W4, H4};
+      const uint64_t str[3] = {plane, 128, W4 * N * 4};
+      const uint32_t box[4] = {32, 32, (uint32_t)(8 / nb), 1};
+      if (encode(&c.map, x, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+        c.rank = 4; c.nbox = nb; c.box_bytes = 32 * 32 * (8 / nb) * 4;
+        if (nb == 2) c.start[1][2] = 4;
+        c.step[1] = 32; c.wrap[1] = 384;
+        c.step[2] = 8; c.wrap[2] = 48;
+        c.cta_step[3] = 1; c.wrap[3] = 13;
+        c.iters = iters;
+        run(nb == 1 ? "conv4 merged 4D box{32,32,8,1} x1" : "conv4 merged 4D box{32,32,4,1} x2", c, sink);
+      }
+    }
+    // R: the filter tile of the same stage, K-major [Co=256][K=3456], box {32 k, 128 co}
+    {
+      Cfg c;
+      zero(c);
+      const uint64_t dims[2] = {3456, 256};
+      const uint64_t str[1] = {3456 * 4};
+      const uint32_t box[2] = {32, 128};
+      if (encode(&c.map, x, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) {
+        c.rank = 2; c.nbox = 1; c.box_bytes = 32 * 128 * 4;
+        c.step[0] = 32; c.wrap[0] = 3456;
+        c.cta_step[1] = 128; c.wrap[1] = 256;
+        c.iters = iters;
+        run("conv4 filter box{32,128} K-major SW128", c, sink);
+      }
     }
   }
   return 0;
