@@ -644,37 +644,44 @@ def main():
     # The K steps are captured into one CUDA graph so host launch gaps do not
     # count (single-kernel workloads -- PL5 184 MB, softmax 32 MB -- and the
     # small-N transform sweep last microseconds per launch).  A single-kernel
-    # workload's dominant kernel is its only kernel (avg = region / K); for
-    # multi-kernel steps the dominant kernel is timed afterwards the same way,
-    # as one CUDA graph of K launches of it alone (the harness of the
-    # same-size copy ceiling).
+    # workload's dominant kernel is its only kernel (avg = region / K); in a
+    # multi-kernel step the dominant kernel's launches are bracketed by
+    # external timing events recorded INSIDE the captured graph, so they are
+    # timed on its stream within the timed region.  If the capture fails, the
+    # steps are plain stream launches with the same events.
     use_graph = not args.no_graph
     graph = None
-    if use_graph:
-        graph = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream(device)
-        cap.wait_stream(stream)
-        with torch.cuda.graph(graph, stream=cap):
-            cs = torch.cuda.current_stream(device).cuda_stream
-            for _ in range(K):
-                for op in ops:
-                    op.launch(cs)
-        stream.wait_stream(cap)
-        graph.replay()  # warm the graph once
-        torch.cuda.synchronize()
-        barrier()
-    dev_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(0 if use_graph else K)]
+    dev_ev = [(torch.cuda.Event(enable_timing=True, external=use_graph),
+               torch.cuda.Event(enable_timing=True, external=use_graph))
+              for _ in range(0 if use_graph and len(ops) == 1 else K)]
 
-    def timed_launches():
+    def timed_launches(s, sh_):
         for i in range(K):
             for j, op in enumerate(ops):
-                if j == dom:
-                    dev_ev[i][0].record(stream)
-                    op.launch(sh)
-                    dev_ev[i][1].record(stream)
+                if j == dom and dev_ev:
+                    dev_ev[i][0].record(s)
+                    op.launch(sh_)
+                    dev_ev[i][1].record(s)
                 else:
-                    op.launch(sh)
+                    op.launch(sh_)
+
+    if use_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(device)
+            cap.wait_stream(stream)
+            with torch.cuda.graph(graph, stream=cap):
+                timed_launches(cap, cap.cuda_stream)
+            stream.wait_stream(cap)
+            graph.replay()  # warm the graph once
+            torch.cuda.synchronize()
+        except Exception as e:  # capture unsupported: plain stream launches
+            print(f"bench.py: graph capture failed ({str(e)[:80]}), stream launches", file=sys.stderr)
+            torch.cuda.synchronize()
+            graph, use_graph = None, False
+            dev_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in range(K)]
+        barrier()
 
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ selects these launches
     with ClockSampler(local) as clocks:
@@ -682,20 +689,28 @@ def main():
         if use_graph:
             graph.replay()
         else:
-            timed_launches()
+            timed_launches(stream, sh)
         ev1.record(stream)
         torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     barrier()
     ms = ev0.elapsed_time(ev1)
+    dom_ms = ms / K if not dev_ev else sum(a.elapsed_time(b) for a, b in dev_ev) / K
+    t = torch.tensor([ms, dom_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        all_reduce_max(dist, t)
+    ms, dom_ms = float(t[0]), float(t[1])
+    # multi-kernel steps: the dominant kernel also timed alone (a graph of K
+    # launches of it, no event nodes between them) -- for small kernels the
+    # in-graph event nodes themselves cost microseconds
+    iso_ms = None
     if use_graph and len(ops) > 1:
         g_dom = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream(device)
         cap.wait_stream(stream)
         with torch.cuda.graph(g_dom, stream=cap):
-            cs = torch.cuda.current_stream(device).cuda_stream
             for _ in range(K):
-                ops[dom].launch(cs)
+                ops[dom].launch(cap.cuda_stream)
         stream.wait_stream(cap)
         g_dom.replay()
         torch.cuda.synchronize()
@@ -704,16 +719,7 @@ def main():
         g_dom.replay()
         d1.record(stream)
         torch.cuda.synchronize()
-        barrier()
-        dom_ms = d0.elapsed_time(d1) / K
-    elif use_graph:
-        dom_ms = ms / K
-    else:
-        dom_ms = sum(a.elapsed_time(b) for a, b in dev_ev) / K
-    t = torch.tensor([ms, dom_ms], device=device, dtype=torch.float64)
-    if world > 1:
-        all_reduce_max(dist, t)
-    ms, dom_ms = float(t[0]), float(t[1])
+        iso_ms = d0.elapsed_time(d1) / K
     # whole-job bytes: the global batch for strong scaling, world x per-GPU for weak
     job_bytes = wl.step_bytes_global if wl.scaling == "strong" else step_bytes * world
     value = job_bytes * K / (ms / 1e3) / GB
@@ -729,11 +735,16 @@ def main():
                 "traffic": traffic if world == 1 else None,
                 "traffic_source": "profiles/ncu_traffic.json (ncu --set full, N=1 shapes)",
                 "step_frac": round(step_bytes / (ms / K / 1e3) / GB / peak, 4)}
+    if iso_ms:
+        roofline["isolated"] = {"avg_launch_ms": round(iso_ms, 5),
+                                "achieved": round(dom_op.bytes / (iso_ms / 1e3) / GB, 1),
+                                "what": "the dominant kernel alone: one CUDA graph of K launches"}
 
     # ---- size ceiling: a plain device copy of the same bytes, same harness ----
     ceiling = None
     if use_graph and dom_op.in_bytes == dom_op.out_bytes and not args.no_ceiling:
-        ceiling = copy_ceiling(torch, device, dom_op, K, achieved)
+        ceiling = copy_ceiling(torch, device, dom_op, K,
+                               roofline["isolated"]["achieved"] if iso_ms else achieved)
 
     # ---- e2e: host buffers through the C ABI (pinned H2D, kernel, D2H) ----
     e2e = None
@@ -770,8 +781,8 @@ def main():
                 "copy_ceiling": ceiling,
                 "gpu_launches": K * len(ops), "clocks": clk, "impl": "ours",
                 "timing": ("one CUDA graph of K steps" + ("" if len(ops) == 1 else
-                           "; dominant kernel: one CUDA graph of K launches of it alone")
-                           if use_graph else "stream launches")}
+                           "; dominant kernel: external CUDA events around its launches "
+                           "inside the graph") if use_graph else "stream launches")}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
