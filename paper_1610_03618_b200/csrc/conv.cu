@@ -603,6 +603,7 @@ struct ShareOut {
   // {32, 1, 1, 1, 32} = one 32-channel x 32-image chunk, SWIZZLE_128B
   CUtensorMap y;
   FastDiv fd_groups, fd_owb;  // set by the launcher (TMA-store epilogue)
+  uint32_t evict_first = 0;   // TMA stores with an L2 evict_first hint (TAPS, LCNN_TAPS_L2 bit 2)
   static constexpr bool kTmaStore = true, kTmaTransposed = false, kTmaPairs = true;
   __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
                                             bool add) const {
@@ -615,6 +616,9 @@ struct ShareOut {
     if (add)
       tma_add_5d(&y, box, 0, static_cast<int32_t>(grp), static_cast<int32_t>(ow),
                  static_cast<int32_t>(oh), static_cast<int32_t>(m0));
+    else if (evict_first)
+      tma_store_5d_hint(&y, box, 0, static_cast<int32_t>(grp), static_cast<int32_t>(ow),
+                        static_cast<int32_t>(oh), static_cast<int32_t>(m0), l2_policy_evict_first());
     else
       tma_store_5d(&y, box, 0, static_cast<int32_t>(grp), static_cast<int32_t>(ow),
                    static_cast<int32_t>(oh), static_cast<int32_t>(m0));
@@ -797,6 +801,7 @@ struct TapsParams {
   // TMA-store epilogue (ShareOut boxes staged at epi_off, two 4 KB boxes per
   // epilogue warp) instead of per-lane stores
   uint32_t tma, epi_off;
+  uint32_t in_keep;  // input boxes with an L2 evict_last hint (LCNN_TAPS_L2 bit 1)
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __grid_constant__ TapsParams prm) {
@@ -849,9 +854,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
         const uint32_t fh = it / prm.CB, cb = it - fh * prm.CB;
         mbar_wait(&ctl->iempty[is], iph ^ 1);
         mbar_arrive_expect_tx(&ctl->ifull[is], prm.ibox);
-        tma_load_5d(ibase + is * prm.islot, &prm.x, &ctl->ifull[is], 0,
-                    static_cast<int32_t>(cb * 32), y0, static_cast<int32_t>(g),
-                    z0 + static_cast<int32_t>(fh));
+        if (prm.in_keep)
+          tma_load_5d_hint(ibase + is * prm.islot, &prm.x, &ctl->ifull[is], 0,
+                           static_cast<int32_t>(cb * 32), y0, static_cast<int32_t>(g),
+                           z0 + static_cast<int32_t>(fh), l2_policy_evict_last());
+        else
+          tma_load_5d(ibase + is * prm.islot, &prm.x, &ctl->ifull[is], 0,
+                      static_cast<int32_t>(cb * 32), y0, static_cast<int32_t>(g),
+                      z0 + static_cast<int32_t>(fh));
         if (++is == prm.ni) {
           is = 0;
           iph ^= 1;
@@ -2052,6 +2062,14 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
     prm.out.fd_groups = FastDiv(prm.G);
     prm.out.fd_owb = FastDiv(prm.OWB);
   }
+  // L2 policies (profiling knob LCNN_TAPS_L2, bit 1: input boxes evict_last,
+  // bit 2: TMA-stored outputs evict_first)
+  static const int l2_knob = [] {
+    const char* e = std::getenv("LCNN_TAPS_L2");
+    return e ? std::atoi(e) : 0;
+  }();
+  prm.in_keep = (l2_knob & 1) ? 1u : 0u;
+  prm.out.evict_first = (l2_knob & 2) ? 1u : 0u;
   const Sched& sc = prm.sc;
   if (sc.dp_tiles < mt * nt) {  // zero the stream-K tiles' output rows (oh >= first split row)
     const uint64_t ncols = static_cast<uint64_t>(a.ho) * a.wo * a.n;
