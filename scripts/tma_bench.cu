@@ -510,6 +510,7 @@ int main() {
       run("conv1 SHARE box x2 (2 groups) slots=4", c, sink);
     }
   }
+  if (getenv("TB_VGG")) goto vgg_boxes;
 conv4_boxes:
   // P/Q/R: AlexNet conv4 input (N=128, 13x13, C=384, CHWN: 33 MB, L2-resident),
   // the CI k-block of a RowsOut tile: 32 channels x 2 output pixels x 128 images.
@@ -563,6 +564,51 @@ conv4_boxes:
         c.cta_step[1] = 128; c.wrap[1] = 256;
         c.iters = iters;
         run("conv4 filter box{32,128} K-major SW128", c, sink);
+      }
+    }
+  }
+  return 0;
+vgg_boxes:
+  // S/T: VGG conv1_2 input (N=128, 224x224, C=64, CHWN: 1.64 GB, DRAM-cold),
+  // the TAPS input box of one (filter row, 32-channel block):
+  //  S: shipped, 8 pixels x 32 images: view {32 n, C, W, 4 g, H}, box {32, 32 c, 10 w, 1, 1}
+  //     (40 KB: 320 runs of 128 B, one 32-image group per CTA, 4 CTAs per pixel block)
+  //  T: 2 pixels x 128 images: view {32 n, C, 4 g, W, H}, box {32, 32 c, 4 g, 4 w, 1}
+  //     (64 KB: per channel 2 KB contiguous -- 4 pixels x 4 groups -- in one box)
+  {
+    const uint64_t Nv = 128, Wv = 224, Hv = 224, Cv = 64, plane = Hv * Wv * Nv * 4;
+    float* xv;
+    CK(cudaMalloc(&xv, plane * Cv + 4096));
+    CK(cudaMemset(xv, 0, plane * Cv));
+    for (int st : {3, 4}) {
+      Cfg c;
+      zero(c);
+      const uint64_t dims[5] = {32, Cv, Wv, 4, Hv};
+      const uint64_t str[4] = {plane, Nv * 4, 128, Wv * Nv * 4};
+      const uint32_t box[5] = {32, 32, 10, 1, 1};
+      if (encode(&c.map, xv, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+        c.rank = 5; c.nbox = 1; c.box_bytes = 32 * 32 * 10 * 4; c.stages = st;
+        c.step[1] = 32; c.wrap[1] = 64;
+        c.step[4] = 1; c.wrap[4] = 222;
+        c.cta_step[3] = 1; c.wrap[3] = 4;
+        c.cta_step[2] = 2; c.wrap[2] = 210;
+        c.iters = 1500;
+        run(st == 3 ? "vgg1_2 TAPS box{32,32,10,1,1} 3 slots" : "vgg1_2 TAPS box{32,32,10,1,1} 4 slots", c, sink);
+      }
+    }
+    for (int st : {2, 3}) {
+      Cfg c;
+      zero(c);
+      const uint64_t dims[5] = {32, Cv, 4, Wv, Hv};
+      const uint64_t str[4] = {plane, 128, Nv * 4, Wv * Nv * 4};
+      const uint32_t box[5] = {32, 32, 4, 4, 1};
+      if (encode(&c.map, xv, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+        c.rank = 5; c.nbox = 1; c.box_bytes = 32 * 32 * 4 * 4 * 4; c.stages = st;
+        c.step[1] = 32; c.wrap[1] = 64;
+        c.step[4] = 1; c.wrap[4] = 222;
+        c.cta_step[3] = 3; c.wrap[3] = 219;
+        c.iters = 1500;
+        run(st == 2 ? "vgg1_2 wide box{32,32,4,4,1} 2 slots" : "vgg1_2 wide box{32,32,4,4,1} 3 slots", c, sink);
       }
     }
   }
