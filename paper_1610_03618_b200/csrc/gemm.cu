@@ -556,10 +556,16 @@ cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t 
     const uint32_t sms = static_cast<uint32_t>(tc_sm_count()), iters = L.kbn * segs;
     const uint64_t sk_total = static_cast<uint64_t>(mt) * ((n + kPBN - 1) / kPBN) * iters;
     uint32_t best_bn = 0, best_s = 1, best_ctas = 0;
+    // clusters of up to 16 CTAs (non-portable size) when the profiling knob
+    // LCNN_FC_S16=1 asks for them
+    static const uint32_t s_cap = [] {
+      const char* e = std::getenv("LCNN_FC_S16");
+      return (e && e[0] == '1') ? 16u : 8u;
+    }();
     for (uint32_t bn : {static_cast<uint32_t>(kPBN), 128u}) {
       const uint32_t tiles = mt * static_cast<uint32_t>((n + bn - 1) / bn);
       uint32_t S = tiles ? sms / tiles : 0;
-      S = std::min({S, 8u, iters / 4});
+      S = std::min({S, s_cap, iters / 4});
       if (S >= 2 && tiles * S > best_ctas) {
         best_ctas = tiles * S;
         best_bn = bn;

@@ -1033,8 +1033,14 @@ cudaError_t launch_splitk(const Loader& ld, float* c, const SplitK& sk, cudaStre
     attr = true;
   }
   if (sk.smem_bytes > kMaxDynSmem || sk.stages < 2 || sk.stages > kPStagesMax || sk.S < 1 ||
-      sk.S > 8)
+      sk.S > 16)
     return cudaErrorInvalidConfiguration;
+  static bool nonportable = false;
+  if (sk.S > 8 && !nonportable) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    nonportable = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sk.mt * sk.nt * sk.S);
   cfg.blockDim = dim3(kTcThreads);
