@@ -338,8 +338,11 @@ def build_workload(name, world, rank, plan=None, tsweep_n=None):
                               if ops[0].rot > 1 else "matrix pair > 2x L2")}
         return Workload(ops, ops, desc, 0, "weak", rows * world, "rows")
     if name.startswith("transform"):
-        # transform[_nchw][_N]: CHWN->NCHW (default) or NCHW->CHWN at batch N
-        src, dst = (NCHW, CHWN) if "_nchw" in name else (CHWN, NCHW)
+        # transform[_nchw|_nhwc|_hwcn][_N]: CHWN->NCHW (default), NCHW->CHWN,
+        # or the generic permutations NCHW->NHWC / CHWN->HWCN (transform_naive) at batch N
+        NHWC, HWCN = 2, 3
+        src, dst = ((NCHW, CHWN) if "_nchw" in name else (NCHW, NHWC) if "_nhwc" in name
+                    else (CHWN, HWCN) if "_hwcn" in name else (CHWN, NCHW))
         b = tsweep_n or 128
         if name.split("_")[-1].isdigit():
             b = int(name.split("_")[-1])
@@ -556,8 +559,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg_pools",
                     help="vgg_pools (default, config 4) | vgg_pools_nchw | pl5 | pl5_nchw | "
-                         "softmax[_ROWS] | softmax5[_ROWS] | softmax_64k | transform[_nchw][_N] | "
-                         "alexnet | alexnet_mixed | vgg16")
+                         "softmax[_ROWS] | softmax5[_ROWS] | softmax_64k | "
+                         "transform[_nchw|_nhwc|_hwcn][_N] | alexnet | alexnet_mixed | vgg16")
     ap.add_argument("--plan", type=int, nargs=2, default=None,
                     help="coarsening fh fw for every pool layer (default: the per-layer plans "
                          "measured on B200)")
