@@ -1004,34 +1004,31 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
     for _ in range(args.warmup):
         net.forward(x.data_ptr(), in_layout, y.data_ptr(), sh)
     torch.cuda.synchronize()
-    # One forward captured as a CUDA graph (the executor is stream-ordered:
-    # stream-ordered allocations become graph memory nodes, PDL edges stay
-    # programmatic), replayed K times: the host issues one call per step
-    # instead of ~15 launches plus tensor-map encodes, so a slow host CPU
-    # cannot open gaps between layers.  Checked against a stream forward.
-    graph, graph_note = None, "stream launches (--no-graph)"
+    # The forward replayed from the network's own CUDA graph
+    # (lcnn_net_forward_graph: captured once for these buffers; stream-ordered
+    # allocations become graph memory nodes, PDL edges stay programmatic): the
+    # host issues one call per step instead of ~11-30 launches plus tensor-map
+    # encodes, so a slow host CPU cannot open gaps between layers.  Checked
+    # against a stream forward first.
+    use_graph, graph_note = False, "stream launches (--no-graph)"
     if not args.no_graph:
         ref = y.clone()
         try:
-            cap = torch.cuda.Stream(device)
-            cap.wait_stream(stream)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=cap):
-                net.forward(x.data_ptr(), in_layout, y.data_ptr(), cap.cuda_stream)
-            stream.wait_stream(cap)
             y.zero_()
-            g.replay()
+            net.forward_graph(x.data_ptr(), in_layout, y.data_ptr(), sh)
             torch.cuda.synchronize()
             if torch.allclose(y, ref, rtol=1e-4, atol=1e-6):
-                graph, graph_note = g, "one CUDA graph per forward (captured lcnn_net_forward), replayed K times"
+                use_graph = True
+                graph_note = ("lcnn_net_forward_graph: the network's cached CUDA graph of one "
+                              "forward, replayed K times")
             else:
                 graph_note = "stream launches (graph replay disagreed with the stream forward)"
         except Exception as e:  # capture unsupported: keep stream launches
             graph_note = f"stream launches (graph capture failed: {str(e)[:80]})"
             torch.cuda.synchronize()
         for _ in range(2):
-            (graph.replay() if graph is not None else
-             net.forward(x.data_ptr(), in_layout, y.data_ptr(), sh))
+            (net.forward_graph if use_graph else net.forward)(x.data_ptr(), in_layout,
+                                                              y.data_ptr(), sh)
         torch.cuda.synchronize()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -1040,11 +1037,9 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
     torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clocks:
         e0.record(stream)
+        fwd = net.forward_graph if use_graph else net.forward
         for _ in range(K):
-            if graph is not None:
-                graph.replay()
-            else:
-                net.forward(x.data_ptr(), in_layout, y.data_ptr(), sh)
+            fwd(x.data_ptr(), in_layout, y.data_ptr(), sh)
         e1.record(stream)
         torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()

@@ -54,6 +54,16 @@ int lcnn_net_layouts(const lcnn_net* net, int* layouts, uint32_t max_layers);
  * blocking; lcnn_net_status reports it. */
 int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout,
                      float* d_output, void* stream);
+/* lcnn_net_forward replayed from a CUDA graph: the first call for a given
+ * (d_input, in_layout, d_output) captures one whole forward -- every layer,
+ * inserted transform and the classifier -- into a graph owned by the
+ * network (at most 16 cached; the oldest is dropped after a device sync);
+ * later calls with the same buffers are one cudaGraphLaunch on `stream`.
+ * Same results and non-finite-flag semantics as lcnn_net_forward.  Replays
+ * of one cached graph are serialised by CUDA; the buffers must stay valid
+ * while the network lives. */
+int lcnn_net_forward_graph(lcnn_net* net, const float* d_input, int in_layout,
+                           float* d_output, void* stream);
 /* Wait for `stream`, read and clear the non-finite flag: LCNN_EDOMAIN
  * ("layer '<softmax>': softmax: non-finite input") if any forward since the
  * last call met a non-finite input, else LCNN_OK. */

@@ -2,15 +2,36 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "lcnn/net.hpp"
 #include "lcnn_cuda.h"
 #include "lcnn_net.h"
 
+// Cached CUDA graphs of whole forwards (lcnn_net_forward_graph), one per
+// (input, layout, output) buffer triple: a replay is one cudaGraphLaunch
+// instead of the executor's ~11-30 launches and tensor-map encodes.
+struct NetGraphs {
+  using Key = std::tuple<const void*, int, void*>;
+  static constexpr std::size_t kMax = 16;
+  std::mutex mu;
+  cudaStream_t capture = nullptr;  // private stream the forwards are captured on
+  std::map<Key, cudaGraphExec_t> execs;
+  std::map<Key, cudaGraph_t> graphs;
+  ~NetGraphs() {
+    for (auto& kv : execs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : graphs) cudaGraphDestroy(kv.second);
+    if (capture) cudaStreamDestroy(capture);
+  }
+};
+
 struct lcnn_net {
   std::unique_ptr<lcnn::Network> net;
+  NetGraphs graphs;
 };
 
 namespace {
@@ -162,6 +183,76 @@ int lcnn_net_forward(const lcnn_net* net, const float* d_input, int in_layout, f
                           cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
       if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
     }
+  })
+}
+
+int lcnn_net_forward_graph(lcnn_net* net, const float* d_input, int in_layout, float* d_output,
+                           void* stream) {
+  NET_GUARD({
+    if (!net) throw lcnn::ValidationError("null network");
+    NetGraphs& g = net->graphs;
+    const NetGraphs::Key key{d_input, in_layout, d_output};
+    cudaGraphExec_t exec = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(g.mu);
+      const auto it = g.execs.find(key);
+      if (it != g.execs.end()) exec = it->second;
+    }
+    if (!exec) {
+      // capture one forward on a private stream (nothing executes during a
+      // capture, so the caller's stream needs no ordering against it), then
+      // instantiate; allocations become graph memory nodes, the stream-K
+      // sync words are a set of the capture's own (Network::sync_words)
+      std::lock_guard<std::mutex> lock(g.mu);
+      if (!g.capture) {
+        const cudaError_t e = cudaStreamCreateWithFlags(&g.capture, cudaStreamNonBlocking);
+        if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+      }
+      cudaError_t e = cudaStreamBeginCapture(g.capture, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+      cudaGraph_t graph = nullptr;
+      void* const prev = lcnn::current_stream();
+      struct Restore {
+        void* s;
+        ~Restore() { lcnn::set_current_stream(s); }
+      } restore{prev};
+      try {
+        lcnn::set_current_stream(g.capture);
+        const lcnn::NetworkSpec& sp = net->net->spec();
+        const lcnn::DeviceTensor4D in = lcnn::DeviceTensor4D::wrap(
+            const_cast<float*>(d_input), sp.n, sp.c, sp.h, sp.w, L(in_layout));
+        const lcnn::DeviceMatrix out = net->net->forward(in, nullptr, d_output);
+        if (out.data() != d_output) {
+          e = cudaMemcpyAsync(d_output, out.data(), std::size_t{out.rows} * out.cols * sizeof(float),
+                              cudaMemcpyDeviceToDevice, g.capture);
+          if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+        }
+      } catch (...) {
+        cudaStreamEndCapture(g.capture, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      e = cudaStreamEndCapture(g.capture, &graph);
+      if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        throw lcnn::Error(cudaGetErrorString(e));
+      }
+      if (g.execs.size() >= NetGraphs::kMax) {  // bounded cache: drop one entry
+        auto victim = g.execs.begin();
+        cudaStreamSynchronize(g.capture);
+        cudaDeviceSynchronize();  // its last replay may still run
+        cudaGraphExecDestroy(victim->second);
+        cudaGraphDestroy(g.graphs[victim->first]);
+        g.graphs.erase(victim->first);
+        g.execs.erase(victim);
+      }
+      g.execs[key] = exec;
+      g.graphs[key] = graph;
+    }
+    const cudaError_t e = cudaGraphLaunch(exec, static_cast<cudaStream_t>(abi_stream(stream)));
+    if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
   })
 }
 

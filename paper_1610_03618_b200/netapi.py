@@ -35,6 +35,7 @@ def lib():
                                     POINTER(c_uint32)]
         d.lcnn_net_layouts.argtypes = [c_void_p, POINTER(c_int), c_uint32]
         d.lcnn_net_forward.argtypes = [c_void_p, c_void_p, c_int, c_void_p, c_void_p]
+        d.lcnn_net_forward_graph.argtypes = [c_void_p, c_void_p, c_int, c_void_p, c_void_p]
         d.lcnn_net_forward_host.argtypes = [c_void_p, c_void_p, c_int, c_void_p]
         d.lcnn_net_forward_host_many.argtypes = [c_void_p, POINTER(c_void_p), c_int,
                                                  POINTER(c_void_p), c_uint32]
@@ -81,6 +82,11 @@ class Network:
 
     def forward(self, d_input: int, in_layout: int, d_output: int, stream: int):
         _check(lib().lcnn_net_forward(self._h, d_input, in_layout, d_output, stream))
+
+    def forward_graph(self, d_input: int, in_layout: int, d_output: int, stream: int):
+        """lcnn_net_forward_graph: the forward replayed from a CUDA graph the
+        network captures once per (input, layout, output) buffer triple."""
+        _check(lib().lcnn_net_forward_graph(self._h, d_input, in_layout, d_output, stream))
 
     def pool_plans(self):
         """{layer index: PoolPlan} of the network's pooling layers (tuned at creation)."""

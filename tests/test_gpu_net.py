@@ -273,3 +273,48 @@ def test_forward_concurrent_streams_and_graph_replay_agree(cuda):
         assert torch.allclose(yg, ref, rtol=1e-4, atol=1e-7)
         assert torch.allclose(y1, ref, rtol=1e-4, atol=1e-7)
     net.close()
+
+
+def test_forward_graph_replays_match_the_stream_forward(cuda):
+    """lcnn_net_forward_graph: captured once per buffer triple, replayed after;
+    the logits match lcnn_net_forward (TF32 AlexNet: stream-K tails, fused
+    conv1+pool1, in-kernel zeroing all inside the graph), a second buffer
+    pair gets its own graph, and a non-finite input still raises through
+    lcnn_net_status."""
+    import os
+
+    import torch
+
+    text = open(os.path.join(os.path.dirname(__file__), "..", "configs", "alexnet.json")).read()
+    net = netapi.Network(text, 257, 32, seed=42, precision=capi.PREC_TF32)
+    info = net.info(NCHW)
+    rows, cols = info["out"]
+    dn, dc, dh, dw = info["dims"]
+    lay = info["first_layout"]
+    g = torch.Generator(device=cuda).manual_seed(11)
+    xs = [torch.rand(dn * dc * dh * dw, device=cuda, generator=g) * 2 - 1 for _ in range(2)]
+    s = torch.cuda.current_stream(cuda).cuda_stream
+    refs = []
+    for x in xs:
+        r = torch.empty(rows * cols, device=cuda)
+        net.forward(x.data_ptr(), lay, r.data_ptr(), s)
+        refs.append(r)
+    ys = [torch.empty(rows * cols, device=cuda) for _ in xs]
+    for _ in range(3):
+        for x, y, r in zip(xs, ys, refs):
+            y.fill_(float("nan"))
+            net.forward_graph(x.data_ptr(), lay, y.data_ptr(), s)
+            torch.cuda.synchronize()
+            assert torch.allclose(y, r, rtol=1e-4, atol=1e-7)
+    # new input values in the same buffer: the replay reads them
+    xs[0].mul_(0.5)
+    net.forward(xs[0].data_ptr(), lay, refs[0].data_ptr(), s)
+    net.forward_graph(xs[0].data_ptr(), lay, ys[0].data_ptr(), s)
+    torch.cuda.synchronize()
+    assert torch.allclose(ys[0], refs[0], rtol=1e-4, atol=1e-7)
+    net.status(s)
+    xs[1][0] = float("inf")
+    net.forward_graph(xs[1].data_ptr(), lay, ys[1].data_ptr(), s)
+    with pytest.raises(Exception):
+        net.status(s)
+    net.close()
