@@ -193,17 +193,14 @@ int lcnn_net_forward_graph(lcnn_net* net, const float* d_input, int in_layout, f
     NetGraphs& g = net->graphs;
     const NetGraphs::Key key{d_input, in_layout, d_output};
     cudaGraphExec_t exec = nullptr;
-    {
-      std::lock_guard<std::mutex> lock(g.mu);
-      const auto it = g.execs.find(key);
-      if (it != g.execs.end()) exec = it->second;
-    }
+    std::lock_guard<std::mutex> lock(g.mu);  // held through a capture (rare) and the launch
+    const auto it = g.execs.find(key);
+    if (it != g.execs.end()) exec = it->second;
     if (!exec) {
       // capture one forward on a private stream (nothing executes during a
       // capture, so the caller's stream needs no ordering against it), then
       // instantiate; allocations become graph memory nodes, the stream-K
       // sync words are a set of the capture's own (Network::sync_words)
-      std::lock_guard<std::mutex> lock(g.mu);
       if (!g.capture) {
         const cudaError_t e = cudaStreamCreateWithFlags(&g.capture, cudaStreamNonBlocking);
         if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
@@ -251,6 +248,8 @@ int lcnn_net_forward_graph(lcnn_net* net, const float* d_input, int in_layout, f
       g.execs[key] = exec;
       g.graphs[key] = graph;
     }
+    // launched under the lock: an eviction by another thread cannot destroy
+    // the executable between the lookup and the launch
     const cudaError_t e = cudaGraphLaunch(exec, static_cast<cudaStream_t>(abi_stream(stream)));
     if (e != cudaSuccess) throw lcnn::Error(cudaGetErrorString(e));
   })
