@@ -346,12 +346,11 @@ __global__ void __launch_bounds__(kThreads)
 // contiguous in the destination -- so every warp stores 32 consecutive
 // 16-byte (VEC) or 4-byte words, and reads runs of A floats (CHWN -> HWCN at
 // N = 8: 32-byte runs, one sector each) instead of one warp per run.
-template <bool VEC>
+template <int W>  // floats per word: 4 (16 B), 2 (8 B) or 1
 __global__ void __launch_bounds__(kThreads)
     permute_runs_flat_kernel(const float* __restrict__ src, float* __restrict__ dst, PermGeom g,
                              FastDiv div_a, FastDiv div_b, uint64_t total) {
   LCNN_PDL_ENTRY();
-  constexpr uint32_t W = VEC ? 4 : 1;
   for (uint64_t e = (blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x); e < total;
        e += static_cast<uint64_t>(gridDim.x) * kThreads) {
     uint32_t run, x;
@@ -360,10 +359,13 @@ __global__ void __launch_bounds__(kThreads)
     div_b.divmod(run, ij, b);
     g.div_J.divmod(ij, i, j);
     const float* sp = src + b * g.sb + i * g.si + j * g.sj + static_cast<uint64_t>(x) * W;
-    if constexpr (VEC)
+    if constexpr (W == 4) {
       stg_stream(reinterpret_cast<float4*>(dst) + e, ldg_stream(reinterpret_cast<const float4*>(sp)));
-    else
+    } else if constexpr (W == 2) {
+      reinterpret_cast<float2*>(dst)[e] = __ldg(reinterpret_cast<const float2*>(sp));
+    } else {
       stg_stream(dst + e, __ldg(sp));
+    }
   }
 }
 
@@ -551,17 +553,23 @@ cudaError_t launch_permute4d(const float* src, float* dst, uint32_t n,
     g.sj = ss[r[1]];
     g.si = ss[r[2]];
     g.div_J = FastDiv(g.J);
-    const bool vec = g.A % 4 == 0 && aligned16(src) && aligned16(dst);
-    const uint32_t A = vec ? g.A / 4 : g.A;
-    const uint64_t words = total / (vec ? 4 : 1);
+    const bool al16 = aligned16(src) && aligned16(dst);
+    const bool al8 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7u) == 0;
+    const int W = g.A % 4 == 0 && al16 ? 4 : (g.A % 2 == 0 && al8 ? 2 : 1);
+    const uint32_t A = g.A / W;
+    const uint64_t words = total / W;
     uint64_t blocks = (words + kThreads - 1) / kThreads;
     if (blocks > 148ull * 16) blocks = 148ull * 16;
-    if (vec)
-      lcnn_pdl::launch(permute_runs_flat_kernel<true>, static_cast<uint32_t>(blocks), kThreads, 0, s,
-                       src, dst, g, FastDiv(A), FastDiv(g.B), words);
+    const uint32_t nb = static_cast<uint32_t>(blocks);
+    if (W == 4)
+      lcnn_pdl::launch(permute_runs_flat_kernel<4>, nb, kThreads, 0, s, src, dst, g, FastDiv(A),
+                       FastDiv(g.B), words);
+    else if (W == 2)
+      lcnn_pdl::launch(permute_runs_flat_kernel<2>, nb, kThreads, 0, s, src, dst, g, FastDiv(A),
+                       FastDiv(g.B), words);
     else
-      lcnn_pdl::launch(permute_runs_flat_kernel<false>, static_cast<uint32_t>(blocks), kThreads, 0,
-                       s, src, dst, g, FastDiv(A), FastDiv(g.B), words);
+      lcnn_pdl::launch(permute_runs_flat_kernel<1>, nb, kThreads, 0, s, src, dst, g, FastDiv(A),
+                       FastDiv(g.B), words);
     return cudaGetLastError();
   }
   const uint64_t warps = static_cast<uint64_t>(g.B) * g.I * g.J;
