@@ -322,16 +322,22 @@ def build_workload(name, world, rank, plan=None, tsweep_n=None):
                              f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB) between launches"}
         return Workload(ops, ops, desc, 0, "weak", 128 * world, "images")
     if name.startswith("softmax"):
-        fused = name != "softmax5" and not name.startswith("softmax5_")
-        rows = 4096
+        fused = not name.startswith("softmax5")
+        rows, cols = 4096, 1000
         if name == "softmax_64k":
             rows = 65536
+        elif name.endswith("_10k") or name.endswith("_10kcls"):
+            # the paper's softmax comparison runs 10000 categories
+            cols = 10000
+        elif "_c" in name and name.rsplit("_c", 1)[-1].isdigit():
+            cols = int(name.rsplit("_c", 1)[-1])  # softmax_cCOLS: 4096 rows of COLS
         elif "_" in name and name.split("_")[-1].isdigit():
             rows = int(name.split("_")[-1])
-        ops = [SoftmaxOp(rows, 1000, fused, seed)]
-        desc = {"workload": f"BASELINE config 2: softmax classifier {rows}x1000, "
+        ops = [SoftmaxOp(rows, cols, fused, seed)]
+        desc = {"workload": f"BASELINE config 2: softmax classifier {rows}x{cols}, "
                             f"{'fused single kernel' if fused else 'five-kernel baseline'}"
-                            + (" (HBM asymptote beyond the 4096-row config)" if rows > 4096 else ""),
+                            + (" (HBM asymptote beyond the 4096-row config)" if rows > 4096 else "")
+                            + (" (the paper's 10000-category case)" if cols != 1000 else ""),
                 "batch_per_gpu": rows, "global_batch": rows * world, "parallelism": par,
                 "l2_policy": (f"{ops[0].rot} rotated input/output pairs "
                               f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB > 4x L2) between launches"
@@ -559,7 +565,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg_pools",
                     help="vgg_pools (default, config 4) | vgg_pools_nchw | pl5 | pl5_nchw | "
-                         "softmax[_ROWS] | softmax5[_ROWS] | softmax_64k | "
+                         "softmax[_ROWS] | softmax5[_ROWS] | softmax_64k | softmax[5]_10k | softmax_cCOLS | "
                          "transform[_nchw|_nhwc|_hwcn][_N] | alexnet | alexnet_mixed | vgg16")
     ap.add_argument("--plan", type=int, nargs=2, default=None,
                     help="coarsening fh fw for every pool layer (default: the per-layer plans "

@@ -33,6 +33,8 @@
 //                       normalise pass (input read twice).
 #include <float.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -220,8 +222,11 @@ __device__ __forceinline__ float block_reduce_sum(float v, float* red) {
 }
 
 // One CTA per row, VPL values per thread in registers (cols <= 256 * VPL).
-template <int VPL, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+// MINB resident CTAs per SM asked of the register allocator: with one row
+// per CTA, more resident rows overlap one row's load with another's
+// reductions.
+template <int VPL, bool VEC, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB)
     softmax_wide_kernel(const float* __restrict__ src, float* __restrict__ dst,
                         uint32_t cols, int* flag) {
   LCNN_PDL_ENTRY();
@@ -418,11 +423,11 @@ cudaError_t rows_launch(const float* src, float* dst, uint32_t rows, uint32_t co
   return cudaGetLastError();
 }
 
-template <int VPL>
+template <int VPL, int MINB = 1>
 cudaError_t wide_launch(const float* src, float* dst, uint32_t rows, uint32_t cols, bool vec,
                         int* flag, cudaStream_t st) {
-  if (vec) lcnn_pdl::launch(softmax_wide_kernel<VPL, true>, rows, kThreads, 0, st, src, dst, cols, flag);
-  else lcnn_pdl::launch(softmax_wide_kernel<VPL, false>, rows, kThreads, 0, st, src, dst, cols, flag);
+  if (vec) lcnn_pdl::launch(softmax_wide_kernel<VPL, true, MINB>, rows, kThreads, 0, st, src, dst, cols, flag);
+  else lcnn_pdl::launch(softmax_wide_kernel<VPL, false, MINB>, rows, kThreads, 0, st, src, dst, cols, flag);
   return cudaGetLastError();
 }
 
@@ -446,9 +451,28 @@ cudaError_t launch_softmax_fused(const float* src, float* dst, uint32_t rows, ui
   if (cols <= 512) return rows_launch<32, 16>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 1024) return rows_launch<32, 32, 128>(src, dst, rows, cols, vec, flag, st);
   if (cols <= 2048) return rows_launch<32, 64>(src, dst, rows, cols, vec, flag, st);
+  // one CTA per row: the smallest register row that fits, with a register
+  // bound that keeps 2-3 rows resident per SM so one row's load overlaps
+  // another's reductions (measured on B200, 4096 rows: 8192 cols 5.40 -> 6.43,
+  // 10000 -- the paper's case -- 3.09 -> 6.46, 12288 4.81 -> 5.61, 16384
+  // 3.62 -> 5.28 TB/s; profiles/r02_softmax_wide_ab.jsonl)
+  static const bool minb1 = [] {  // profiling knob LCNN_SM_WIDE_MINB=1: no occupancy bound
+    const char* e = std::getenv("LCNN_SM_WIDE_MINB");
+    return e && e[0] == '1';
+  }();
   if (cols <= 4096) return wide_launch<16>(src, dst, rows, cols, vec, flag, st);
-  if (cols <= 8192) return wide_launch<32>(src, dst, rows, cols, vec, flag, st);
-  if (cols <= 16384) return wide_launch<64>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 8192)
+    return minb1 ? wide_launch<32>(src, dst, rows, cols, vec, flag, st)
+                 : wide_launch<32, 3>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 10240)
+    return minb1 ? wide_launch<40>(src, dst, rows, cols, vec, flag, st)
+                 : wide_launch<40, 3>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 12288)
+    return minb1 ? wide_launch<48>(src, dst, rows, cols, vec, flag, st)
+                 : wide_launch<48, 3>(src, dst, rows, cols, vec, flag, st);
+  if (cols <= 16384)
+    return minb1 ? wide_launch<64>(src, dst, rows, cols, vec, flag, st)
+                 : wide_launch<64, 2>(src, dst, rows, cols, vec, flag, st);
   lcnn_pdl::launch(softmax_stream_kernel, rows, kThreads, 0, st, src, dst, cols, flag);
   return cudaGetLastError();
 }
