@@ -35,8 +35,11 @@
 
 #include <cstdlib>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "internal.h"
+#include "tc.cuh"
 
 namespace lcnn_dev {
 
@@ -288,6 +291,84 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// Rows wider than the register kernels (> 16384 columns, up to ~56K):
+// persistent CTAs stage each row in shared memory with one cp.async.bulk
+// (double-buffered when two rows fit: the next row streams in while this one
+// is reduced), so the row is read from HBM once -- the stream kernel below
+// reads it twice.  Same arithmetic as softmax_wide_kernel: max, then
+// e = exp(x - max) kept in shared memory with its sum, then e * (1 / sum).
+__global__ void __launch_bounds__(kThreads)
+    softmax_smem_kernel(const float* __restrict__ src, float* __restrict__ dst, uint32_t rows,
+                        uint32_t cols, uint32_t nbuf, uint32_t pitch, int* flag) {
+  LCNN_PDL_ENTRY();
+  extern __shared__ __align__(128) float sm_rows[];
+  __shared__ uint64_t full[2];
+  __shared__ float red[kThreads / 32];
+  const uint32_t bytes = cols * 4, G = gridDim.x, c4 = cols / 4;
+  if (threadIdx.x == 0) {
+    lcnn_tc::mbar_init(&full[0], 1);
+    lcnn_tc::mbar_init(&full[1], 1);
+    lcnn_tc::mbar_fence_init();
+    for (uint32_t k = 0; k < nbuf; ++k) {
+      const uint32_t rr = blockIdx.x + k * G;
+      if (rr < rows) {
+        lcnn_tc::mbar_arrive_expect_tx(&full[k], bytes);
+        lcnn_tc::bulk_load(sm_rows + k * pitch, src + static_cast<uint64_t>(rr) * cols, bytes,
+                           &full[k]);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (uint32_t r = blockIdx.x; r < rows; r += G, ++it) {
+    const uint32_t b = nbuf == 2 ? (it & 1u) : 0u;
+    const uint32_t ph = nbuf == 2 ? ((it >> 1) & 1u) : (it & 1u);
+    lcnn_tc::mbar_wait(&full[b], ph);
+    float4* x = reinterpret_cast<float4*>(sm_rows + b * pitch);
+    float m = -INFINITY;
+    bool bad = false;
+    for (uint32_t j = threadIdx.x; j < c4; j += kThreads) {
+      const float4 v = x[j];
+      bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+      m = fmaxf(fmaxf(m, fmaxf(v.x, v.y)), fmaxf(v.z, v.w));
+    }
+    flag_nonfinite(flag, bad);
+    m = block_reduce_max(m, red);
+    float s = 0.0f;
+    for (uint32_t j = threadIdx.x; j < c4; j += kThreads) {
+      float4 v = x[j];
+      v.x = fexp(v.x - m);
+      v.y = fexp(v.y - m);
+      v.z = fexp(v.z - m);
+      v.w = fexp(v.w - m);
+      s += v.x;
+      s += v.y;
+      s += v.z;
+      s += v.w;
+      x[j] = v;
+    }
+    s = block_reduce_sum(s, red);  // its barriers also publish the e values
+    const float inv = 1.0f / s;
+    float4* out = reinterpret_cast<float4*>(dst + static_cast<uint64_t>(r) * cols);
+    for (uint32_t j = threadIdx.x; j < c4; j += kThreads) {
+      const float4 e = x[j];
+      stg_stream(out + j, make_float4(e.x * inv, e.y * inv, e.z * inv, e.w * inv));
+    }
+    // every thread is done with buffer b (generic-proxy reads / writes)
+    // before the async proxy refills it with the row nbuf * G further on
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t rn = r + nbuf * G;
+      if (rn < rows) {
+        lcnn_tc::mbar_arrive_expect_tx(&full[b], bytes);
+        lcnn_tc::bulk_load(sm_rows + b * pitch, src + static_cast<uint64_t>(rn) * cols, bytes,
+                           &full[b]);
+      }
+    }
+  }
+}
+
 // One CTA per row of any width: online (max, sum) then normalise.
 __global__ void __launch_bounds__(kThreads)
     softmax_stream_kernel(const float* __restrict__ src, float* __restrict__ dst,
@@ -473,6 +554,30 @@ cudaError_t launch_softmax_fused(const float* src, float* dst, uint32_t rows, ui
   if (cols <= 16384)
     return minb1 ? wide_launch<64>(src, dst, rows, cols, vec, flag, st)
                  : wide_launch<64, 2>(src, dst, rows, cols, vec, flag, st);
+  // rows that fit shared memory: staged once (double-buffered when two fit)
+  constexpr uint32_t kSmemMax = 227 * 1024 - 1024;
+  const uint32_t pitch = (cols + 31) / 32 * 32;  // floats per buffer, 128-B aligned
+  static const bool smem_off = [] {  // profiling knob LCNN_SM_SMEM=0: the two-pass stream kernel
+    const char* e = std::getenv("LCNN_SM_SMEM");
+    return e && e[0] == '0';
+  }();
+  if (vec && !smem_off && pitch * 4ull <= kSmemMax) {
+    const uint32_t nbuf = 2ull * pitch * 4 <= kSmemMax ? 2 : 1;
+    const uint32_t smem = nbuf * pitch * 4;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(softmax_smem_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kSmemMax));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const uint32_t per_sm = kSmemMax / smem >= 2 ? 2 : 1;
+    const uint32_t grid = rows < 148u * per_sm ? rows : 148u * per_sm;
+    lcnn_pdl::launch(softmax_smem_kernel, grid, kThreads, smem, st, src, dst, rows, cols, nbuf,
+                     pitch, flag);
+    return cudaGetLastError();
+  }
   lcnn_pdl::launch(softmax_stream_kernel, rows, kThreads, 0, st, src, dst, cols, flag);
   return cudaGetLastError();
 }

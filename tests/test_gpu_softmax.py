@@ -68,7 +68,8 @@ def test_reference_fixtures(cuda, ref_vectors):
 
 
 @pytest.mark.parametrize("cols", [1, 3, 10, 16, 17, 63, 64, 100, 256, 257, 512, 999, 1000, 1024,
-                                  1025, 2048, 2049, 4096, 4097, 8192, 10000, 16384, 16385, 40000])
+                                  1025, 2048, 2049, 4096, 4097, 8192, 10000, 12288, 16384, 16385,
+                                  16388, 28000, 40000, 56000, 60000])
 def test_every_kernel_shape(cuda, cols):
     for rows in (1, 7, 33):
         x = rng_uniform(rows * cols, rows * cols, -5, 5)
@@ -103,3 +104,20 @@ def test_shift_invariance_and_monotone(cuda):
     for i in range(6):
         order = np.argsort(x[i])
         assert np.all(np.diff(out[i][order]) > 0)
+
+
+@pytest.mark.parametrize("rows,cols", [(300, 20000), (457, 16388), (200, 40000)])
+def test_wide_rows_persistent_smem_kernel(cuda, rows, cols):
+    """Rows beyond the register kernels are staged in shared memory by
+    persistent CTAs (double-buffered bulk copies when two rows fit): more
+    rows than CTAs, so every buffer is refilled several times; within 1e-6 of
+    the oracle, and a non-finite entry still sets the flag."""
+    x = rng_uniform(rows + cols, rows * cols, -5, 5)
+    m = dev(x, rows, cols, cuda)
+    want, _ = C.softmax_fused(x, rows, cols)
+    got = lcnn.softmax_fused(m)[0].to_host()
+    assert approx_equal(got, want, TOL), (rows, cols)
+    x2 = x.copy()
+    x2[(rows - 1) * cols + 5] = np.inf
+    with pytest.raises(errors.DomainError):
+        lcnn.softmax_fused(dev(x2, rows, cols, cuda))
