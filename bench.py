@@ -311,12 +311,13 @@ def build_workload(name, world, rank, plan=None, tsweep_n=None):
                 "l2_policy": f"each step streams {gbytes / GB / world:.2f} GB per GPU "
                              "(>> 126 MB L2) between reuses of any buffer; no explicit flush"}
         return Workload(ops, gops, desc, 0, "strong", VGG_GLOBAL_BATCH, "images")
-    if name in ("pl5", "pl5_nchw"):
-        layout = CHWN if name == "pl5" else NCHW
+    if name in ("pl5", "pl5_nchw", "pl5_avg", "pl5_nchw_avg"):
+        layout = CHWN if name in ("pl5", "pl5_avg") else NCHW
+        avg = name.endswith("_avg")  # average pooling on the same shape (pool.cpp:98-134)
         p = tuple(plan) if plan else None  # None: GPU-tuned (lcnn_pool_tune)
-        ops = [PoolOp(128, 96, 55, 55, layout, 3, 2, False, p, seed, rotate=True)]
-        desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) max 3x3/s2, "
-                            f"128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",
+        ops = [PoolOp(128, 96, 55, 55, layout, 3, 2, avg, p, seed, rotate=True)]
+        desc = {"workload": f"BASELINE config 1: AlexNet pool1 (PL5) {'avg' if avg else 'max'} "
+                            f"3x3/s2, 128x96x55x55, {'CHWN' if layout == CHWN else 'NCHW'}",
                 "batch_per_gpu": 128, "global_batch": 128 * world, "parallelism": par,
                 "l2_policy": f"{ops[0].rot} rotated input/output pairs "
                              f"({ops[0].rot * ops[0].bytes / 1e6:.0f} MB) between launches"}
@@ -564,7 +565,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg_pools",
-                    help="vgg_pools (default, config 4) | vgg_pools_nchw | pl5 | pl5_nchw | "
+                    help="vgg_pools (default, config 4) | vgg_pools_nchw | pl5[_nchw][_avg] | "
                          "softmax[_ROWS] | softmax5[_ROWS] | softmax_64k | softmax[5]_10k | softmax_cCOLS | "
                          "transform[_nchw|_nhwc|_hwcn][_N] | alexnet | alexnet_mixed | vgg16")
     ap.add_argument("--plan", type=int, nargs=2, default=None,
