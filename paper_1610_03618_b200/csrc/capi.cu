@@ -306,17 +306,28 @@ lcnn_status lcnn_pool_tune(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int l
     if (dst) cudaFreeAsync(dst, s);
     return cuda_fail(e, "pool_tune");
   }
-  // median of 3 timed launches after one warm-up; a candidate whose launch
-  // fails (no specialisation, shared memory over the limit) is skipped
-  auto cost = [&](const lcnn_pool_plan& p) -> float {
+  // A layer too big to stay in L2 between layers (in + out > 96 MB) is timed
+  // DRAM-cold, as it runs: a 256 MB scratch write evicts L2 before every
+  // timed launch (repeated launches on one buffer otherwise hit L2 in part,
+  // and ranked the NCHW ring shapes of PL5 differently from a cold run).
+  void* flush = nullptr;
+  constexpr size_t kFlushBytes = size_t{256} << 20;
+  if (in_bytes + out_bytes > (size_t{96} << 20) && cudaMallocAsync(&flush, kFlushBytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    flush = nullptr;
+  }
+  // median of `reps` timed launches after one warm-up; a candidate whose
+  // launch fails (no specialisation, shared memory over the limit) is skipped
+  auto cost = [&](const lcnn_pool_plan& p, int reps = 3) -> float {
     const lcnn_impl::PoolArgs a =
         plan_args(src, dst, n, c, h, w, ho, wo, win_h, win_w, stride, mode, p);
     if (launch_plan(a, layout, s) != cudaSuccess) {
       cudaGetLastError();
       return -1.0f;
     }
-    float t[3];
-    for (float& ti : t) {
+    float t[9];
+    for (int i = 0; i < reps; ++i) {
+      if (flush) cudaMemsetAsync(flush, i, kFlushBytes, s);
       cudaEventRecord(e0, s);
       launch_plan(a, layout, s);
       cudaEventRecord(e1, s);
@@ -324,19 +335,25 @@ lcnn_status lcnn_pool_tune(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int l
         cudaGetLastError();
         return -1.0f;
       }
-      cudaEventElapsedTime(&ti, e0, e1);
+      cudaEventElapsedTime(&t[i], e0, e1);
     }
-    std::sort(t, t + 3);
-    return t[1] * 1e3f;
+    std::sort(t, t + reps);
+    return t[reps / 2] * 1e3f;
   };
+  // every candidate's screening cost is kept; the closest ones are re-timed
+  // with 9 launches at the end (3-launch medians of plans within a few
+  // percent of each other picked different winners on different boxes)
+  std::vector<lcnn_pool_plan> seen;
   lcnn_pool_plan best = static_plan(w, layout, win_h, win_w, stride);
   best.us = cost(best);
+  if (best.us > 0.0f) seen.push_back(best);
   auto consider = [&](lcnn_pool_plan p) {
     const float us = cost(p);
-    if (us > 0.0f && (best.us <= 0.0f || us < best.us)) {
+    if (us > 0.0f) {
       p.us = us;
-      best = p;
+      seen.push_back(p);
     }
+    if (us > 0.0f && (best.us <= 0.0f || us < best.us)) best = p;
   };
   // output blocks: every specialised (fh, fw) of the layout's kernel family
   const uint32_t fw_max = layout == LCNN_CHWN ? 4 : 2;
@@ -360,10 +377,26 @@ lcnn_status lcnn_pool_tune(uint32_t n, uint32_t c, uint32_t h, uint32_t w, int l
       consider(p);
     }
   }
+  // refine: the candidates within 5 % of the screening winner, 9 launches each
+  if (best.us > 0.0f) {
+    const float cut = best.us * 1.05f;
+    lcnn_pool_plan win = best;
+    win.us = -1.0f;
+    for (lcnn_pool_plan p : seen) {
+      if (p.us > cut) continue;
+      const float us = cost(p, 9);
+      if (us > 0.0f && (win.us <= 0.0f || us < win.us)) {
+        p.us = us;
+        win = p;
+      }
+    }
+    if (win.us > 0.0f) best = win;
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFreeAsync(src, s);
   cudaFreeAsync(dst, s);
+  if (flush) cudaFreeAsync(flush, s);
   cudaGetLastError();
   if (best.us <= 0.0f) return fail(LCNN_ECUDA, "pool_tune: no candidate launched");
   best.tuned = 1;
