@@ -274,7 +274,10 @@ class Workload:
         return sum(op.bytes for op in self.global_ops)
 
 
-VGG_GLOBAL_BATCH = 256
+# BASELINE config 4's global batch.  LCNN_BENCH_VGG_GLOBAL overrides it for
+# what-if runs (e.g. 32: one GPU's shard of an 8-GPU strong-scaled run); the
+# config dict then reports the batch actually run.
+VGG_GLOBAL_BATCH = int(os.environ.get("LCNN_BENCH_VGG_GLOBAL", "256"))
 
 
 def build_workload(name, world, rank, plan=None, tsweep_n=None):
