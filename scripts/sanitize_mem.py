@@ -26,6 +26,13 @@ for (n, c, h, w) in [(1, 4, 8, 8), (3, 5, 7, 9), (8, 16, 12, 12), (16, 3, 11, 13
     x = lcnn.DeviceTensor4D.from_host(rng.random(n * c * h * w, dtype=np.float32), n, c, h, w,
                                       lcnn.NCHW)
     lcnn.transform(lcnn.transform(x, lcnn.CHWN), lcnn.NCHW)
+# generic permutations: batched NCHW <-> NHWC transposes, short-run CHWN <-> HWCN copies
+for (n, c, h, w) in [(6, 20, 5, 7), (2, 33, 6, 6), (8, 4, 3, 5)]:
+    x = lcnn.DeviceTensor4D.from_host(rng.random(n * c * h * w, dtype=np.float32), n, c, h, w,
+                                      lcnn.NCHW)
+    lcnn.transform_naive(lcnn.transform_naive(x, lcnn.NHWC), lcnn.NCHW)
+    xc = lcnn.transform(x, lcnn.CHWN)
+    lcnn.transform_naive(lcnn.transform_naive(xc, lcnn.HWCN), lcnn.CHWN)
 # the pooling tuner (every candidate plan of both layouts) and a tuned launch
 for layout in (lcnn.CHWN, lcnn.NCHW):
     p = lcnn.PoolParams(3, 3, 2, 0)
@@ -33,7 +40,8 @@ for layout in (lcnn.CHWN, lcnn.NCHW):
     x = lcnn.DeviceTensor4D.from_host(rng.random(16 * 6 * 27 * 27, dtype=np.float32), 16, 6, 27,
                                       27, layout)
     lcnn.pool_run_plan(x, p, plan)
-for (r, cc) in [(7, 1000), (33, 5000), (3, 20000), (5, 2000)]:
+for (r, cc) in [(7, 1000), (33, 5000), (3, 20000), (5, 2000), (300, 20000), (160, 40000),
+                (9, 10000), (4, 12288)]:
     m = lcnn.DeviceMatrix.from_host(rng.random(r * cc, dtype=np.float32), r, cc)
     lcnn.softmax_fused(m)
     lcnn.softmax_reference(m)
