@@ -318,3 +318,33 @@ def test_forward_graph_replays_match_the_stream_forward(cuda):
     with pytest.raises(Exception):
         net.status(s)
     net.close()
+
+
+def test_forward_graph_cache_eviction_and_many_captures(cuda):
+    """More buffer pairs than the graph cache holds (16) and than the spare
+    sync-word sets (8): later captures run with zeroing launches instead of
+    in-kernel zeroing, the oldest graph is evicted and re-captured on reuse,
+    and every replay still matches the stream forward."""
+    import json as _json
+
+    import torch
+
+    net = netapi.Network(_json.dumps(MINI), 257, 32, seed=42, precision=capi.PREC_TF32)
+    info = net.info(NCHW)
+    rows, cols = info["out"]
+    dn, dc, dh, dw = info["dims"]
+    lay = info["first_layout"]
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.rand(dn * dc * dh * dw, device=cuda, generator=g) * 2 - 1
+    s = torch.cuda.current_stream(cuda).cuda_stream
+    ref = torch.empty(rows * cols, device=cuda)
+    net.forward(x.data_ptr(), lay, ref.data_ptr(), s)
+    outs = [torch.empty(rows * cols, device=cuda) for _ in range(20)]
+    for rep in range(2):
+        for y in outs:
+            y.fill_(float("nan"))
+            net.forward_graph(x.data_ptr(), lay, y.data_ptr(), s)
+        torch.cuda.synchronize()
+        for y in outs:
+            assert torch.allclose(y, ref, rtol=1e-4, atol=1e-7), rep
+    net.close()
