@@ -431,12 +431,16 @@ __global__ void pack_filters_row2_kernel(const float* __restrict__ f, float* __r
 // row 2p's channels, 64-127 row 2p + 1's; tile columns are (p, ow, n).  A
 // 32 x 32 chunk never straddles the halves or a pixel, so it maps to one
 // TMA box of the RowsOut view {ncols, C_o}.
-struct RowsPairOut {
+// kPairs: chunks staged two at a time with one async-proxy fence (the
+// short-K SHARE epilogue's scheme; VGG conv1_1 is store-bound: 424 us with
+// stores vs 188 us without, PROFILING probe)
+template <bool kPairs, bool kTma = true>
+struct RowsPairOutT {
   float* c;
   uint64_t ldc;       // real columns Ho * Wo * N
   uint32_t M, span, ho;  // C_o, Wo * N, Ho
   CUtensorMap y;
-  static constexpr bool kTmaStore = true, kTmaTransposed = false;
+  static constexpr bool kTmaStore = kTma, kTmaTransposed = false, kTmaPairs = kPairs;
   __device__ __forceinline__ bool remap(uint32_t& m, uint32_t& n) const {
     const uint32_t pr = n / span, oh = 2 * pr + (m >= 64 ? 1u : 0u);
     m &= 63u;
@@ -1792,13 +1796,26 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s, bool rows2 = fa
           });
       if (e != cudaSuccess) return e;
     }
-    RowsPairOut O{a.dst, uint64_t{a.ho} * span, a.co, span, a.ho};
-    const uint64_t dims[2] = {O.ldc, a.co};
-    const uint64_t opitch[1] = {O.ldc * 4};
+    static const int pairs = [] {  // profiling knob LCNN_ROW2_PAIRS: 0 one box per fence,
+      const char* e = std::getenv("LCNN_ROW2_PAIRS");  // 2 per-lane stores (no TMA)
+      return e ? std::atoi(e) : 1;
+    }();
+    if (pairs == 2) {
+      RowsPairOutT<false, false> O{a.dst, uint64_t{a.ho} * span, a.co, span, a.ho};
+      return launch_persistent(L, O, sc, s);
+    }
+    const uint64_t dims[2] = {uint64_t{a.ho} * span, a.co};
+    const uint64_t opitch[1] = {dims[0] * 4};
     const uint32_t obox[2] = {32, 32};
-    if (!make_tmap(&O.y, a.dst, 2, dims, opitch, obox, nullptr, 0)) return cudaErrorInvalidValue;
     Sched se = sc;
     sched_epi(se, 0);
+    if (pairs) {
+      RowsPairOutT<true> O{a.dst, uint64_t{a.ho} * span, a.co, span, a.ho};
+      if (!make_tmap(&O.y, a.dst, 2, dims, opitch, obox, nullptr, 0)) return cudaErrorInvalidValue;
+      return launch_persistent(L, O, se, s);
+    }
+    RowsPairOutT<false> O{a.dst, uint64_t{a.ho} * span, a.co, span, a.ho};
+    if (!make_tmap(&O.y, a.dst, 2, dims, opitch, obox, nullptr, 0)) return cudaErrorInvalidValue;
     return launch_persistent(L, O, se, s);
   }
   if (cudaError_t e = zero_sk_region(sc, kCoOnN, kCoOnN ? bn : kTcBM, a.dst, L.ncols, a.co, s,

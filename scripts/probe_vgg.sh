@@ -7,6 +7,6 @@ mkdir -p gpurun_out/pv
 touch paper_1610_03618_b200/csrc/*.cu; make PROFILING=1 -j16 > gpurun_out/pv/build.log 2>&1
 : > gpurun_out/pv/probe.txt
 for p in 0 1 2 3; do
-  echo "probe $p $(LCNN_TC_PROBE=$p timeout 300 python scripts/perf_dense.py vgg1_2_chwn vgg2_1_chwn vgg2_2_chwn 2>&1 | tail -1)" >> gpurun_out/pv/probe.txt
+  echo "probe $p $(LCNN_TC_PROBE=$p timeout 300 python scripts/perf_dense.py ${LAYERS:-vgg1_2_chwn vgg2_1_chwn vgg2_2_chwn} 2>&1 | tail -1)" >> gpurun_out/pv/probe.txt
 done
 echo done
