@@ -379,13 +379,18 @@ lcnn_status lcnn_fc_forward_packed(const float* x, int x_layout,
                                    void* stream);
 /* lcnn_fc_forward_packed with caller-owned sync words (d_sync: see
  * lcnn_conv_forward_packed_ex): the stream-K output is zeroed inside the fc
- * kernel instead of by a separate launch. */
+ * kernel instead of by a separate launch.  d_next_packed / next_bytes
+ * (optional, NULL / 0): the NEXT fc layer's packed weights; once a CTA has
+ * issued its own loads it prefetches its share of them into L2, so the next
+ * layer starts on L2 hits while this one drains (weights never depend on
+ * this layer's output). */
 lcnn_status lcnn_fc_forward_packed_ex(const float* x, int x_layout,
                                       const void* d_packed, float* y,
                                       uint64_t m, uint64_t n, uint64_t k,
                                       int precision, void* d_workspace,
                                       size_t workspace_bytes, void* d_sync,
-                                      void* stream);
+                                      const void* d_next_packed,
+                                      size_t next_bytes, void* stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

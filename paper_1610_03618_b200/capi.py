@@ -113,7 +113,7 @@ _SIGNATURES = {
     "lcnn_fc_forward_packed": (c_int, [_P, c_int, _P, _P, c_uint64, c_uint64, c_uint64, c_int, _P,
                                        c_size_t, _P]),
     "lcnn_fc_forward_packed_ex": (c_int, [_P, c_int, _P, _P, c_uint64, c_uint64, c_uint64, c_int,
-                                          _P, c_size_t, _P, _P]),
+                                          _P, c_size_t, _P, _P, c_size_t, _P]),
 }
 SYNC_BYTES = 16  # LCNN_SYNC_BYTES
 

@@ -850,13 +850,14 @@ lcnn_status lcnn_fc_forward_packed(const float* x, int x_layout, const void* d_p
                                    uint64_t m, uint64_t n, uint64_t k, int precision,
                                    void* d_workspace, size_t workspace_bytes, void* stream) {
   return lcnn_fc_forward_packed_ex(x, x_layout, d_packed, y, m, n, k, precision, d_workspace,
-                                   workspace_bytes, nullptr, stream);
+                                   workspace_bytes, nullptr, nullptr, 0, stream);
 }
 
 lcnn_status lcnn_fc_forward_packed_ex(const float* x, int x_layout, const void* d_packed,
                                       float* y, uint64_t m, uint64_t n, uint64_t k,
                                       int precision, void* d_workspace, size_t workspace_bytes,
-                                      void* d_sync, void* stream) {
+                                      void* d_sync, const void* d_next_packed, size_t next_bytes,
+                                      void* stream) {
   if (!x || !d_packed || !y) return fail(LCNN_EINVAL, "fc: null pointer");
   if (reinterpret_cast<uintptr_t>(d_sync) & 7u)
     return fail(LCNN_EINVAL, "fc: sync word must be 8-byte aligned");
@@ -875,7 +876,8 @@ lcnn_status lcnn_fc_forward_packed_ex(const float* x, int x_layout, const void* 
     return fail(LCNN_EINVAL, "fc: workspace too small");
   cudaError_t e = lcnn_impl::launch_fc_packed(x, a_mn, d_packed, y, m, n, k, precision,
                                               d_workspace, S(stream),
-                                              static_cast<unsigned long long*>(d_sync));
+                                              static_cast<unsigned long long*>(d_sync),
+                                              d_next_packed, d_next_packed ? next_bytes : 0);
   if (e != cudaSuccess) return cuda_fail(e, "fc_forward_packed");
   return ok();
 }

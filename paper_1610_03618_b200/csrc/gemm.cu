@@ -129,9 +129,26 @@ struct FcLoader {
   uint32_t pf_ahead;     // k-blocks of weights prefetched into L2 ahead of the TMA loads
   bool a_grouped;  // MN-major A, m % 128 == 0: one 3D box {32, 32 k, 4 groups}
   bool skip_a;     // profiling (LCNN_TC_PROBE bit 4): no activation loads
+  // the next fc layer's packed weights (nullptr: none): each CTA prefetches
+  // its 1/grid share into L2 after issuing its last load, so the next layer
+  // starts on L2 hits while this one drains
+  const uint8_t* next_w;
+  uint64_t next_bytes;
+  static constexpr bool kTailPrefetch = true;
   static constexpr bool kZeroSmem = false;
   static constexpr bool kResidentA = false;
   static constexpr int kSteps = kTcBK / 8;
+  __device__ void tail_prefetch(uint32_t cta, uint32_t grid) const {
+    if (!next_w) return;
+    const uint64_t share = (next_bytes / grid + 255) / 256 * 256;
+    const uint64_t lo = share * cta;
+    if (lo >= next_bytes) return;
+    uint64_t len = next_bytes - lo < share ? next_bytes - lo : share;
+    for (uint64_t off = 0; off < len; off += (1u << 20)) {
+      const uint64_t b = len - off < (1u << 20) ? len - off : (1u << 20);
+      bulk_prefetch_l2(next_w + lo + off, static_cast<uint32_t>(b) & ~15u);
+    }
+  }
   __device__ uint64_t desc_a(const uint8_t* sa, int k) const {
     return kAMn ? smem_desc_sw128(sa + k * 1024, 4096, 512, 1) : smem_desc_sw128(sa + k * 32, 16, 1024);
   }
@@ -503,8 +520,10 @@ constexpr uint32_t kFcMinSkIters = 4;
 template <bool kAMn>
 cudaError_t launch_fc_tc(const float* x, const void* packed, float* c, uint64_t m, uint64_t n,
                          uint64_t k, int precision, void* ws, cudaStream_t s,
-                         unsigned long long* zsync) {
+                         unsigned long long* zsync, const void* next_packed, uint64_t next_bytes) {
   FcLoader<kAMn> L;
+  L.next_w = static_cast<const uint8_t*>(next_packed);
+  L.next_bytes = next_packed ? next_bytes : 0;
   const float* b0 = static_cast<const float*>(packed);
   const float* b1 = precision == LCNN_PREC_3XTF32 ? b0 + fc_packed_bytes(k, n, precision) / 8 : b0;
   const float *a0 = x, *a1 = x;
@@ -632,9 +651,12 @@ bool fc_tc_supported(uint64_t m, uint64_t n, uint64_t k, bool a_mn) {
 
 cudaError_t launch_fc_packed(const float* x, bool a_mn, const void* packed, float* c, uint64_t m,
                              uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s,
-                             unsigned long long* zsync) {
-  return a_mn ? launch_fc_tc<true>(x, packed, c, m, n, k, precision, ws, s, zsync)
-              : launch_fc_tc<false>(x, packed, c, m, n, k, precision, ws, s, zsync);
+                             unsigned long long* zsync, const void* next_packed,
+                             uint64_t next_bytes) {
+  return a_mn ? launch_fc_tc<true>(x, packed, c, m, n, k, precision, ws, s, zsync, next_packed,
+                                   next_bytes)
+              : launch_fc_tc<false>(x, packed, c, m, n, k, precision, ws, s, zsync, next_packed,
+                                    next_bytes);
 }
 
 }  // namespace lcnn_impl

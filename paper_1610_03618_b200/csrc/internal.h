@@ -92,9 +92,12 @@ cudaError_t launch_fc_pack(const float* w, uint64_t k, uint64_t n, int precision
                            cudaStream_t s);
 // zsync: as ConvArgs::zsync (nullptr: the stream-K output is zeroed by a
 // zero2d launch ahead of the kernel)
+// next_packed / next_bytes: the next fc layer's packed weights, prefetched
+// into L2 by each CTA once its own loads are issued (nullptr: none)
 cudaError_t launch_fc_packed(const float* x, bool a_mn, const void* packed, float* c, uint64_t m,
                              uint64_t n, uint64_t k, int precision, void* ws, cudaStream_t s,
-                             unsigned long long* zsync = nullptr);
+                             unsigned long long* zsync = nullptr,
+                             const void* next_packed = nullptr, uint64_t next_bytes = 0);
 cudaError_t launch_gemm_tc(const float* a, const float* b, float* c, uint64_t m,
                            uint64_t n, uint64_t k, int precision, void* ws,
                            cudaStream_t s);

@@ -137,6 +137,17 @@ template <class O>
 struct OutTma<O, decltype(void(O::kTmaStore))> {
   static constexpr bool value = O::kTmaStore;
 };
+// Loaders that prefetch the NEXT layer's constant operand into L2 once this
+// CTA's loads are issued (Loader::kTailPrefetch, Loader::tail_prefetch()): the
+// fc chain, whose next weights never depend on this layer's output
+template <class L, class = void>
+struct LoaderTail {
+  static constexpr bool value = false;
+};
+template <class L>
+struct LoaderTail<L, decltype(void(L::kTailPrefetch))> {
+  static constexpr bool value = L::kTailPrefetch;
+};
 // Out types whose chunks are staged in pairs (one async-proxy fence per two
 // boxes): the short-K SHARE convolutions, where the epilogue sets the pace
 // (measured: VGG conv1_1 625 -> 504 us; neutral to slightly slower on the
@@ -501,6 +512,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     });
+    if constexpr (LoaderTail<Loader>::value) ld.tail_prefetch(blockIdx.x, gridDim.x);
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     // The whole warp walks the schedule (warp-uniform control flow keeps the

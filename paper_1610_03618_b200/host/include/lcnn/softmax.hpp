@@ -52,9 +52,13 @@ std::shared_ptr<DeviceBuffer> pack_fc_weights(const float* d_weights, std::uint3
 // d_sync (optional): LCNN_SYNC_BYTES of zeroed device memory owned by this
 // call site (lcnn_fc_forward_packed_ex): the fc zeroes its stream-K output
 // in-kernel instead of launching a zeroing kernel first.
+// next_packed (optional): the next fc layer's packed weights, prefetched into
+// L2 by this layer's CTAs once their own loads are issued.
 DeviceMatrix fc_forward_packed(const DeviceMatrix& in, const void* d_packed, std::uint32_t n,
-                               int precision, void* d_sync = nullptr);
+                               int precision, void* d_sync = nullptr,
+                               const DeviceBuffer* next_packed = nullptr);
 DeviceMatrix fc_forward_packed(const DeviceTensor4D& in, const void* d_packed, std::uint32_t n,
-                               int precision, void* d_sync = nullptr);
+                               int precision, void* d_sync = nullptr,
+                               const DeviceBuffer* next_packed = nullptr);
 
 }  // namespace lcnn

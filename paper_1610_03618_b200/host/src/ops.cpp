@@ -352,7 +352,8 @@ std::shared_ptr<DeviceBuffer> pack_fc_weights(const float* d_weights, std::uint3
 namespace {
 
 DeviceMatrix fc_packed_run(const float* x, int layout, std::uint32_t m, std::uint32_t k,
-                           const void* d_packed, std::uint32_t n, int precision, void* d_sync) {
+                           const void* d_packed, std::uint32_t n, int precision, void* d_sync,
+                           const DeviceBuffer* next) {
   DeviceMatrix out(m, n);
   const std::size_t ws = lcnn_fc_workspace_bytes(m, k, precision);
   void* wsp = nullptr;
@@ -363,24 +364,28 @@ DeviceMatrix fc_packed_run(const float* x, int layout, std::uint32_t m, std::uin
     wsb = buf.bytes();
   }
   check_status(lcnn_fc_forward_packed_ex(x, layout, d_packed, out.data(), m, n, k, precision, wsp,
-                                         wsb, d_sync, current_stream()));
+                                         wsb, d_sync, next ? next->get() : nullptr,
+                                         next ? next->bytes() : 0, current_stream()));
   return out;
 }
 
 }  // namespace
 
 DeviceMatrix fc_forward_packed(const DeviceMatrix& in, const void* d_packed, std::uint32_t n,
-                               int precision, void* d_sync) {
-  return fc_packed_run(in.data(), LCNN_NCHW, in.rows, in.cols, d_packed, n, precision, d_sync);
+                               int precision, void* d_sync, const DeviceBuffer* next_packed) {
+  return fc_packed_run(in.data(), LCNN_NCHW, in.rows, in.cols, d_packed, n, precision, d_sync,
+                       next_packed);
 }
 
 DeviceMatrix fc_forward_packed(const DeviceTensor4D& in, const void* d_packed, std::uint32_t n,
-                               int precision, void* d_sync) {
+                               int precision, void* d_sync, const DeviceBuffer* next_packed) {
   const std::uint32_t k = in.c() * in.h() * in.w();
   if (in.layout() == Layout::CHWN && in.n() % 4 == 0)
-    return fc_packed_run(in.data(), LCNN_CHWN, in.n(), k, d_packed, n, precision, d_sync);
+    return fc_packed_run(in.data(), LCNN_CHWN, in.n(), k, d_packed, n, precision, d_sync,
+                         next_packed);
   const DeviceTensor4D rows = in.layout() == Layout::NCHW ? in : transform(in, Layout::NCHW);
-  return fc_packed_run(rows.data(), LCNN_NCHW, rows.n(), k, d_packed, n, precision, d_sync);
+  return fc_packed_run(rows.data(), LCNN_NCHW, rows.n(), k, d_packed, n, precision, d_sync,
+                       next_packed);
 }
 
 // ================================================================ conv ===

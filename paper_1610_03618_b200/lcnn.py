@@ -463,11 +463,13 @@ def pack_fc_weights(weights, k, n, precision=TF32, stream=None):
 
 
 def fc_forward_packed(x, x_layout, packed, m, n, k, precision=TF32, out=None, stream=None,
-                      sync=None):
+                      sync=None, next_packed=None):
     """y (m x n) = x . W on packed weights.  x_layout NCHW: x is m rows of k;
     CHWN: x is [k][m] (a CHWN producer, flattened in the operand load).
     sync: optional zeroed CUDA tensor of >= capi.SYNC_BYTES bytes owned by this
-    call site (lcnn_fc_forward_packed_ex: in-kernel stream-K zeroing)."""
+    call site (lcnn_fc_forward_packed_ex: in-kernel stream-K zeroing).
+    next_packed: the next fc layer's packed weights, prefetched into L2 by the
+    CTAs of this one once their own loads are issued."""
     torch = _torch()
     if out is None:
         out = torch.empty(m * n, dtype=torch.float32, device=x.device)
@@ -475,7 +477,10 @@ def fc_forward_packed(x, x_layout, packed, m, n, k, precision=TF32, out=None, st
     ws = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32, device=x.device)
     capi.call("lcnn_fc_forward_packed_ex", x.data_ptr(), x_layout, packed.data_ptr(),
               out.data_ptr(), m, n, k, precision, ws.data_ptr(), ws.numel() * 4,
-              sync.data_ptr() if sync is not None else None, _stream(stream))
+              sync.data_ptr() if sync is not None else None,
+              next_packed.data_ptr() if next_packed is not None else None,
+              next_packed.numel() * next_packed.element_size() if next_packed is not None else 0,
+              _stream(stream))
     return out
 
 

@@ -100,11 +100,11 @@ def test_sync_word_entry_points_validate_before_the_device():
     lib = capi.lib()
     odd = ctypes.c_void_p(256 + 4)
     st = lib.lcnn_fc_forward_packed_ex(DUMMY, capi.NCHW, DUMMY, DUMMY, 128, 4096, 9216,
-                                       capi.PREC_TF32, None, 0, odd, None)
+                                       capi.PREC_TF32, None, 0, odd, None, 0, None)
     assert st == 11 and b"sync word" in lib.lcnn_last_error()
     st = lib.lcnn_conv_forward_packed_ex(DUMMY, DUMMY, DUMMY, 128, 384, 13, 13, capi.CHWN, 256,
                                          3, 3, 1, 1, capi.PREC_TF32, None, 0, odd, None)
     assert st == 11 and b"sync word" in lib.lcnn_last_error()
     st = lib.lcnn_fc_forward_packed_ex(None, capi.NCHW, DUMMY, DUMMY, 128, 4096, 9216,
-                                       capi.PREC_TF32, None, 0, None, None)
+                                       capi.PREC_TF32, None, 0, None, None, 0, None)
     assert st == 11 and b"null" in lib.lcnn_last_error()

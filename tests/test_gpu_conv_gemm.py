@@ -319,3 +319,23 @@ def test_conv_packed_sync_words_zero_in_kernel(cuda, case):
             (case, float(err.nan_to_num(1e30).max()))
         torch.cuda.synchronize()
         assert int(sync.abs().sum()) == 0, sync.tolist()
+
+
+def test_fc_packed_next_layer_prefetch_keeps_results(cuda):
+    """lcnn_fc_forward_packed_ex with the next layer's packed weights as an L2
+    prefetch target: the prefetch only warms L2, the product is unchanged
+    (same tolerance as the plain call), for an fc6/fc7-shaped pair."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(21)
+    m, k, n, n2 = 128, 4096, 4096, 1000
+    a = torch.rand(m, k, device=cuda, generator=g) * 2 - 1
+    w = torch.rand(k, n, device=cuda, generator=g) * 2 - 1
+    w2 = torch.rand(n, n2, device=cuda, generator=g) * 2 - 1
+    pk = lcnn.pack_fc_weights(w.reshape(-1), k, n, lcnn.TF32)
+    pk2 = lcnn.pack_fc_weights(w2.reshape(-1), n, n2, lcnn.TF32)
+    want = a.double() @ w.double()
+    bound = a.abs().double() @ w.abs().double()
+    got = lcnn.fc_forward_packed(a.reshape(-1), NCHW, pk, m, n, k, lcnn.TF32,
+                                 next_packed=pk2).view(m, n).double()
+    assert bool(((got - want).abs() <= tolerance(lcnn.TF32, got, want, bound)).all())
