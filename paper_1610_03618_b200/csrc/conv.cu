@@ -806,6 +806,13 @@ struct TapsParams {
   // epilogue warp) instead of per-lane stores
   uint32_t tma, epi_off;
   uint32_t in_keep;  // input boxes with an L2 evict_last hint (LCNN_TAPS_L2 bit 1)
+  // 2x2 / stride-2 max pooling fused into the row-pair epilogue: a row pair
+  // is exactly one pooled row, a 8-pixel block four pooled pixels, so every
+  // window lies inside one tile; the conv output never reaches HBM.  The
+  // pooled CHWN [co][hp][wp][n] goes to pool_out (whole tiles only, no
+  // stream-K); the two rows meet through the epi_off staging (2 x 16 KB)
+  float* pool_out;
+  uint32_t pool, hp, wp;
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __grid_constant__ TapsParams prm) {
@@ -930,7 +937,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
   } else if (warp >= 2) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;
-    uint32_t local = 0, epi_buf = 0;
+    uint32_t local = 0, epi_buf = 0, pool_buf = 0;
     bool zwait = sc.zsync != nullptr;  // in-kernel stream-K zeroing (Sched::zsync)
     if (zwait) zero_region_arrive(sc);
     for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool split) {
@@ -954,7 +961,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
         m = (q & 1) * 32 + lane;
       }
       const uint32_t base = tmem + a * kPBN + (static_cast<uint32_t>(q * 32) << 16);
-      if (prm.tma) {
+      if (prm.pool) {
+        // ni was remapped above; the pooled row is the row pair's index
+        const uint32_t og = prm.OWB * prm.G, ph = ni / og / 2, rest = ni % og;
+        const uint32_t ob = rest / prm.G, grp = rest - ob * prm.G;
+        float* stg = reinterpret_cast<float*>(smem + prm.epi_off);
+        // warp-uniform and the same for the four epilogue warps (one tile)
+        for (uint32_t u = 0; u < kSharePix / 2 && ph < prm.hp; ++u) {
+          const uint32_t pw = ob * (kSharePix / 2) + u;
+          if (pw >= prm.wp) break;
+          float v0[32], v1[32];
+          tmem_ld32(base + 2 * u * 32, v0);
+          tmem_ld32(base + (2 * u + 1) * 32, v1);
+          float4* row = reinterpret_cast<float4*>(stg + ((pool_buf & 1) * 4 + q) * 1024 + lane * 32);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float h[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              h[e] = max_tap(max_tap(-INFINITY, v0[4 * c + e]), v1[4 * c + e]);
+            row[c ^ (lane & 7)] = make_float4(h[0], h[1], h[2], h[3]);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          // warp q stores channels 16q .. 16q + 15: lanes 8 apart cover one
+          // channel's 32 images (128 B), the pooled max of rows oh and oh + 1
+          const float4* st4 = reinterpret_cast<const float4*>(stg + (pool_buf & 1) * 4096);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t c = q * 16 + k * 4 + (lane >> 3), j = lane & 7;
+            if (c >= prm.out.co) break;
+            const uint32_t off = (c & 31) * 8 + (j ^ (c & 7));
+            const float4 top = st4[(c >> 5) * 256 + off], bot = st4[(2 + (c >> 5)) * 256 + off];
+            float4* dst = reinterpret_cast<float4*>(
+                prm.pool_out + ((static_cast<uint64_t>(c) * prm.hp + ph) * prm.wp + pw) * prm.out.n +
+                grp * 32);
+            dst[j] = max_tap(top, bot);
+          }
+          ++pool_buf;
+        }
+      } else if (prm.tma) {
         if (live)
           epilogue_tile(prm.out, sc, smem + prm.epi_off + q * 2 * 4096, base, m, ni * kPBN, split,
                         epi_buf, lane);
@@ -2025,7 +2070,8 @@ TapsGeom taps_geom(const ConvArgs& a, uint32_t reserve = 0) {
   return q;
 }
 
-cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = false) {
+cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = false,
+                             float* pooled = nullptr, uint32_t hp = 0, uint32_t wp = 0) {
   const ConvArgs& a = t.a;
   // TMA-store epilogue for row pairs (measured on B200, VGG conv1_2 1461 -> 1450 us; slower on
   // the C_o = 128 layers: conv2_1 534 -> 577, conv2_2 949 -> 984 us, whose per-lane stores
@@ -2035,7 +2081,9 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
     const char* e = std::getenv("LCNN_TAPS_TMA");
     return e ? std::atoi(e) : 1;
   }();
-  const bool tma = tma_knob == 2 || (tma_knob == 1 && rows2);
+  const bool pool = pooled != nullptr;  // the 2x2 max pool in the epilogue (rows2 only)
+  if (pool && !rows2) return cudaErrorInvalidValue;
+  const bool tma = pool || tma_knob == 2 || (tma_knob == 1 && rows2);
   constexpr uint32_t kEpi = 4 * 2 * 4096;
   TapsGeom q = taps_geom(a, tma ? kEpi + 1024 : 0);
   if (!q.ok) q = taps_geom(a);
@@ -2043,6 +2091,11 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
   prm.rows2 = rows2 ? 1u : 0u;
   prm.Ho = a.ho;
   prm.tma = tma && q.ok && taps_geom(a, kEpi + 1024).ok ? 1u : 0u;
+  if (pool && !prm.tma) return cudaErrorInvalidConfiguration;  // no room for the staging
+  prm.pool_out = pooled;
+  prm.pool = pool ? 1u : 0u;
+  prm.hp = hp;
+  prm.wp = wp;
   const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
   const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
                              static_cast<uint64_t>(a.n) * 4, 128,
@@ -2065,6 +2118,13 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
   const uint32_t rows = rows2 ? (a.ho + 1) / 2 : a.ho;  // tile rows (row pairs)
   const uint32_t mt = rows2 ? 1 : (a.co + kTcBM - 1) / kTcBM, nt = rows * prm.OWB * prm.G;
   prm.sc = make_sched(mt, nt, (a.fh + prm.rows2) * prm.CB, 1, kSharePix * 32, false, true);
+  if (pool) {  // whole tiles only: a window needs the finished sums of its tile
+    Sched& z = prm.sc;
+    z.dp_tiles = mt * nt;
+    z.sk_iters = 0;
+    z.sk_ctas = 0;
+    z.grid = std::min<uint32_t>(z.dp_tiles, static_cast<uint32_t>(tc_sm_count()));
+  }
   prm.ctl_off = q.ni * q.islot + q.nf * kTcABytes;
   prm.epi_off = 0;
   if (prm.tma) {
@@ -2074,7 +2134,7 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
   }
   prm.out = ShareOut{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, prm.OWB,
                      prm.G};
-  if (prm.tma) {
+  if (prm.tma && !pool) {
     if (!make_share_out_map(&prm.out.y, a)) return cudaErrorInvalidValue;
     prm.out.fd_groups = FastDiv(prm.G);
     prm.out.fd_owb = FastDiv(prm.OWB);
@@ -2603,12 +2663,25 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
 
 // Convolution + max pooling fused (SharePoolOut): CHWN, TF32, a layer the
 // SHARE route takes, pooling stride 2 with a 2- or 3-wide square window.
+// profiling knob LCNN_TAPS_POOL=0: a TAPS row-pair conv and its 2x2 pool run as two kernels
+bool taps_pool_knob() {
+  static const bool on = [] {
+    const char* e = std::getenv("LCNN_TAPS_POOL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Also a TAPS row-pair layer (C_o <= 64, e.g. VGG conv1_2) with a 2x2 window:
+// the pool runs in the row-pair epilogue (TapsParams::pool).
 bool conv_maxpool_fusable(const ConvArgs& a, uint32_t pwin, uint32_t pstride) {
   if (a.layout != LCNN_CHWN || a.precision != LCNN_PREC_TF32) return false;
   if (pstride != kPoolStride || (pwin != 2 && pwin != 3) || a.ho < pwin || a.wo < pwin)
     return false;
   const ConvRoute r = route_conv(a);
-  return r.kind == kRouteShare && !r.via_chwn;
+  if (r.via_chwn) return false;
+  if (r.kind == kRouteTaps2) return pwin == 2 && taps_pool_knob();
+  return r.kind == kRouteShare;
 }
 
 cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, uint32_t pwin,
@@ -2618,6 +2691,7 @@ cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, ui
   const float* w = static_cast<const float*>(packed);
   ConvTcArgs t{a, r.p, w, w, a.src, a.src};
   const uint32_t hp = (a.ho - pwin) / pstride + 1, wp = (a.wo - pwin) / pstride + 1;
+  if (r.kind == kRouteTaps2) return launch_chwn_taps(t, s, true, a.dst, hp, wp);
   // profiling knob LCNN_SHAREPOOL_STORE=tma: staged TMA stores of the pooled
   // chunks (one ring slot fewer) instead of direct lane stores
   static const bool tma = [] {

@@ -36,6 +36,15 @@ CASES = EXACT + [
     (64, 3, 96, 96, 96, 11, 4, 0, 2, 2),     # 22x22 conv -> 11x11 with 2x2 windows
     (32, 1, 45, 45, 128, 5, 2, 0, 2, 2),     # c_o = 128, odd conv extent (21 -> 10)
 ]
+# TAPS row-pair layers (C_o <= 64, channel planes >= 4 MB) with a 2x2 pool:
+# the pool runs in the row-pair epilogue (TapsParams::pool); >= 8 waves of
+# whole tiles, so the unfused conv sums every output whole -> bit-exact
+TAPS = [
+    (32, 32, 193, 185, 48, 3, 1, 1, 2, 2),   # odd extents: last row pair / pixel block partial, c_o 48
+    (64, 32, 128, 160, 64, 3, 1, 1, 2, 2),   # two image groups
+]
+EXACT += TAPS
+CASES += TAPS
 
 
 def _run(cuda, case, seed=0, special=False):
@@ -118,3 +127,30 @@ def test_conv_maxpool_unsupported_pairs(cuda):
     with pytest.raises(Exception):
         lcnn.conv_maxpool_packed(t, torch.zeros(1 << 20, dtype=torch.uint8, device=cuda),
                                  64, 3, 3, 1, 1, lcnn.TF32, 2, 2)
+
+
+def test_conv_maxpool_taps_vgg_conv1_2_full_size(cuda):
+    """VGG-16 conv1_2 -> pool1 exactly as the VGG-16 forward runs it (128
+    images, 64 -> 64 channels, 224 x 224, 3 x 3 pad 1, then 2 x 2 / 2 max):
+    bit-equal to the two-layer run (the fp64 bound is checked on the smaller
+    TAPS cases; an fp64 conv of this size takes minutes)."""
+    import torch
+
+    n, ci, h, w, co = 128, 64, 224, 224, 64
+    g = torch.Generator(device=cuda).manual_seed(11)
+    x = (torch.rand(ci * h * w * n, device=cuda, generator=g) * 2 - 1)
+    filt = (torch.rand(co, ci, 3, 3, device=cuda, generator=g) * 2 - 1).contiguous()
+    t = lcnn.DeviceTensor4D(n, ci, h, w, CHWN, x)
+    assert lcnn.conv_maxpool_supported(t, co, 3, 3, 1, 1, lcnn.TF32, 2, 2)
+    packed = lcnn.pack_conv_filters(t, filt, co, 3, 3, 1, 1, lcnn.TF32)
+    conv = lcnn.conv_forward_packed(t, packed, co, 3, 3, 1, 1, lcnn.TF32)
+    want, _ = lcnn.pool_layout(conv, lcnn.PoolParams(2, 2, 2, lcnn.MAX))
+    del conv
+    got = lcnn.conv_maxpool_packed(t, packed, co, 3, 3, 1, 1, lcnn.TF32, 2, 2)
+    torch.cuda.synchronize()
+    assert (got.n, got.c, got.h, got.w) == (n, co, 112, 112)
+    assert torch.equal(got.data.view(torch.int32), want.data.view(torch.int32))
+
+
+def test_conv_maxpool_taps_special_values(cuda):
+    _run(cuda, TAPS[0], seed=4, special=True)
