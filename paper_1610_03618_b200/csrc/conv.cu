@@ -854,6 +854,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: input boxes and filter slices ----------------
     uint32_t is = 0, iph = 0, fs = 0, fph = 0;
+    // PROFILING probe bit 8: filter slices loaded for the first tile only
+    // (later tiles reuse whatever the ring holds): the cost of re-streaming them
+    bool reload = true;
     for_each_work(sc, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
       const uint32_t mi = t % sc.mt, ni = t / sc.mt;
       const uint32_t g = ni % prm.G, r = ni / prm.G, ob = r % prm.OWB,
@@ -879,15 +882,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
         }
         for (uint32_t fw = 0; fw < prm.FW; ++fw) {
           mbar_wait(&ctl->fempty[fs], fph ^ 1);
-          mbar_arrive_expect_tx(&ctl->ffull[fs], kTcABytes);
-          tma_load_2d(fbase + fs * kTcABytes, &prm.w, &ctl->ffull[fs],
-                      static_cast<int32_t>((it * prm.FW + fw) * kTcBK), co0);
+          if (reload) {
+            mbar_arrive_expect_tx(&ctl->ffull[fs], kTcABytes);
+            tma_load_2d(fbase + fs * kTcABytes, &prm.w, &ctl->ffull[fs],
+                        static_cast<int32_t>((it * prm.FW + fw) * kTcBK), co0);
+          } else {
+            mbar_arrive(&ctl->ffull[fs]);
+          }
           if (++fs == prm.nf) {
             fs = 0;
             fph ^= 1;
           }
         }
       }
+      if (sc.probe & 8) reload = false;
     });
   } else if (warp == 1) {
     // ---------------- MMA issuer (warp-uniform, one elected lane) ----------------

@@ -611,6 +611,40 @@ vgg_boxes:
         run(st == 2 ? "vgg1_2 wide box{32,32,4,4,1} 2 slots" : "vgg1_2 wide box{32,32,4,4,1} 3 slots", c, sink);
       }
     }
+    CK(cudaFree(xv));
+  }
+  // U: the same TAPS box with the channel-plane pitch padded (plane + pad bytes): are the 32
+  // rows of one box, a plane (a multiple of 512 KB) apart, camping on the same L2 slice / DRAM
+  // bank?  DRAM-cold (224 rows) and L2-resident (8 rows, 58 MB) versions.
+  {
+    const uint64_t Nv = 128, Wv = 224, Cv = 64;
+    for (uint64_t Hv : {224ull, 8ull}) {
+      for (uint64_t pad : {0ull, 128ull, 1152ull, 4224ull}) {
+        if (Hv == 8 && (pad == 128 || pad == 4224)) continue;
+        const uint64_t plane = Hv * Wv * Nv * 4 + pad;
+        float* xv;
+        CK(cudaMalloc(&xv, plane * Cv + 4096));
+        CK(cudaMemset(xv, 0, plane * Cv));
+        Cfg c;
+        zero(c);
+        const uint64_t dims[5] = {32, Cv, Wv, 4, Hv};
+        const uint64_t str[4] = {plane, Nv * 4, 128, Wv * Nv * 4};
+        const uint32_t box[5] = {32, 32, 10, 1, 1};
+        if (encode(&c.map, xv, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+          c.rank = 5; c.nbox = 1; c.box_bytes = 32 * 32 * 10 * 4; c.stages = 3;
+          c.step[1] = 32; c.wrap[1] = 64;
+          c.step[4] = 1; c.wrap[4] = (int)Hv - 2;
+          c.cta_step[3] = 1; c.wrap[3] = 4;
+          c.cta_step[2] = 2; c.wrap[2] = 210;
+          c.iters = Hv == 8 ? 3000 : 1500;
+          char name[96];
+          snprintf(name, sizeof name, "vgg1_2 TAPS box H=%llu plane pad %llu B", (unsigned long long)Hv,
+                   (unsigned long long)pad);
+          run(name, c, sink);
+        }
+        CK(cudaFree(xv));
+      }
+    }
   }
   return 0;
 }
