@@ -1093,7 +1093,14 @@ def run_network_workload(args, torch, dist, rank, world, local, device, barrier)
     # it on this part: our kind::tf32 N=256 MMAs issue at 1111 TF/s, above
     # half the library's bf16 burst); the bf16/2 figure is kept beside it
     peak = mma_peak or tf32_peak
-    roofline = {"bound": "tensor", "kernel": f"{name} (tcgen05 kind::tf32 implicit GEMM)",
+    # a conv whose max pool runs in its epilogue (Network fuse_pools): the
+    # pool's own entry is an empty span right after it
+    ix = [e[0] for e in prof].index(name)
+    fused = (ix + 1 < len(prof) and prof[ix + 1][0].startswith("pool") and
+             prof[ix + 1][1] < 0.02 * ns)
+    label = (f"{name} + {prof[ix + 1][0]} (tcgen05 kind::tf32 implicit GEMM, max pool fused "
+             "into the epilogue)") if fused else f"{name} (tcgen05 kind::tf32 implicit GEMM)"
+    roofline = {"bound": "tensor", "kernel": label,
                 "achieved": round(achieved, 1) if achieved else None, "peak": peak,
                 "peak_source": ("measured tcgen05.mma kind::tf32 M=128 N=256 issue rate, 148 SMs "
                                 "(scripts/mma_bench.cu, profiles/r01_mma_bench.txt)") if mma_peak

@@ -52,6 +52,14 @@ case $WHAT in
     timeout 900 ncu $NV --set full --clock-control none --import-source on -k regex:tc_conv_taps_kernel -c 1 \
       -o gpurun_out/r02_vgg_conv1_2 -f python bench.py --workload vgg16 --steps 1 --warmup 3 $B > /dev/null 2>&1
     ;;
+  vggfused)  # VGG-16 with conv1_2 -> pool1 fused (TAPS row-pair epilogue pool)
+    timeout 900 ncu $NV --metrics $LM --clock-control none -c 200 --csv \
+      --log-file gpurun_out/r02_launches_vgg16.csv python bench.py --workload vgg16 --steps 1 --warmup 3 $B > /dev/null 2>&1
+    timeout 900 ncu $NV --set full --clock-control none --import-source on -k regex:tc_conv_taps_kernel -c 1 \
+      -o gpurun_out/r02_vgg_conv1_2_pool -f python bench.py --workload vgg16 --steps 1 --warmup 3 $B > /dev/null 2>&1
+    timeout 600 ncu $NV --metrics $LM --clock-control none -c 200 --csv \
+      --log-file gpurun_out/r02_launches_alexnet.csv python bench.py --workload alexnet --steps 1 --warmup 3 $B > /dev/null 2>&1
+    ;;
 esac
 done
 # keep gpurun_out small (the pull limit is 64 MiB): text exports of every
