@@ -462,6 +462,20 @@ struct RowsPairOutT {
   }
 };
 
+// Row-pair output with quad-chunk stores (OutTmaQuads): a tile's 128
+// consecutive columns of one output row (one pixel x 128 images at N = 128)
+// go out as one box per 32 channels, 512 B per channel, through the 3D view
+// yq {32, ncols / 32, C_o}; split tiles (stream-K fragments) and tiles whose
+// columns are not 128-aligned use the 2D chunk path of RowsPairOutT.
+struct RowsQuadOut : RowsPairOutT<false> {
+  CUtensorMap yq;
+  static constexpr bool kTmaQuads = true;
+  __device__ __forceinline__ void tma_quad(const void* box, uint32_t m0, uint32_t n0) const {
+    if (!remap(m0, n0) || m0 >= M) return;
+    tma_store_3d(&yq, box, 0, static_cast<int32_t>(n0 / 32), static_cast<int32_t>(m0));
+  }
+};
+
 struct RowsOut {  // accumulator rows = channels: C[co][col], ldc = ncols (a multiple of 32)
   float* c;
   uint64_t ldc;
@@ -1850,9 +1864,37 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s, bool rows2 = fa
       if (e != cudaSuccess) return e;
     }
     static const int pairs = [] {  // profiling knob LCNN_ROW2_PAIRS: 0 one box per fence,
-      const char* e = std::getenv("LCNN_ROW2_PAIRS");  // 2 per-lane stores (no TMA)
-      return e ? std::atoi(e) : 1;
+      const char* e = std::getenv("LCNN_ROW2_PAIRS");  // 2 per-lane stores (no TMA),
+      return e ? std::atoi(e) : 3;                      // 1 paired boxes, 3 quad boxes
     }();
+    if (pairs == 3 && span % 128 == 0) {
+      // quad boxes: 64 KB of staging; the ring gives up slots for it
+      Sched se = sc;
+      uint32_t n = se.stages;
+      while (n > 2 && 1024 + n * se.stage_stride + 1024 + 4 * 4 * 4096 + 16 + sizeof(PCtl) >
+                          kMaxDynSmem)
+        --n;
+      if (1024 + n * se.stage_stride + 1024 + 4 * 4 * 4096 + 16 + sizeof(PCtl) <= kMaxDynSmem) {
+        sched_ring(se, n, se.stage_stride, 0);
+        sched_epi(se, 0, 4);
+        RowsQuadOut O;
+        O.c = a.dst;
+        O.ldc = uint64_t{a.ho} * span;
+        O.M = a.co;
+        O.span = span;
+        O.ho = a.ho;
+        const uint64_t dims[2] = {uint64_t{a.ho} * span, a.co};
+        const uint64_t opitch[1] = {dims[0] * 4};
+        const uint32_t obox[2] = {32, 32};
+        const uint64_t qdims[3] = {32, dims[0] / 32, a.co};
+        const uint64_t qpitch[2] = {128, dims[0] * 4};
+        const uint32_t qbox[3] = {32, 4, 32};
+        if (!make_tmap(&O.y, a.dst, 2, dims, opitch, obox, nullptr, 0) ||
+            !make_tmap(&O.yq, a.dst, 3, qdims, qpitch, qbox, nullptr, 0))
+          return cudaErrorInvalidValue;
+        return launch_persistent(L, O, se, s);
+      }
+    }
     if (pairs == 2) {
       RowsPairOutT<false, false> O{a.dst, uint64_t{a.ho} * span, a.co, span, a.ho};
       return launch_persistent(L, O, sc, s);

@@ -160,6 +160,18 @@ template <class O>
 struct OutTmaPairs<O, decltype(void(O::kTmaPairs))> {
   static constexpr bool value = O::kTmaPairs;
 };
+// Out types whose tma_quad() stores four consecutive 32-column chunks (128
+// columns) of 32 rows as ONE box {32, 4 chunks, 32 rows}: each row's 512 B
+// reach memory as one run instead of four 128-B lines written at different
+// times (CHWN outputs: a row is a channel plane; profiles/r02_store_pattern_bench.txt)
+template <class O, class = void>
+struct OutTmaQuads {
+  static constexpr bool value = false;
+};
+template <class O>
+struct OutTmaQuads<O, decltype(void(O::kTmaQuads))> {
+  static constexpr bool value = O::kTmaQuads;
+};
 constexpr uint32_t kEpiStageBytes = 4 * 2 * 4096;  // 4 warps x 2 boxes
 // Out types that carry state from tile to tile in the epilogue warps'
 // registers (Out::Acc) and consume each tile with Out::tile(): the max-pool
@@ -185,6 +197,34 @@ template <class Out>
 __device__ __forceinline__ void epilogue_tile(const Out& out, const Sched& sc, uint8_t* stg,
                                               uint32_t taddr, uint32_t m, uint32_t ncol0,
                                               bool split, uint32_t& epi_buf, int lane) {
+  if constexpr (OutTmaQuads<Out>::value) {
+    if (sc.epi_bufs == 4 && sc.bn % 128 == 0 && !split) {
+      // staging [row][chunk][32 floats] (16 KB per warp), SWIZZLE_128B on the
+      // box row index row * 4 + chunk; single-buffered
+#pragma unroll 1
+      for (uint32_t c = 0; c < sc.bn; c += 128) {
+        if (lane == 0) bulk_wait_read_n<0>();  // the previous quad's store has read the staging
+        __syncwarp();
+#pragma unroll 1
+        for (uint32_t h = 0; h < 4; ++h) {
+          float v[32];
+          tmem_ld32(taddr + c + 32 * h, v);
+          const uint32_t r = static_cast<uint32_t>(lane) * 4 + h;
+          float4* row = reinterpret_cast<float4*>(stg + r * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            row[j ^ (r & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !(sc.probe & 2)) {
+          out.tma_quad(stg, m, ncol0 + c);
+          bulk_commit();
+        }
+      }
+      return;
+    }
+  }
   if constexpr (OutTmaPairs<Out>::value) {
     if (sc.epi_bufs == 2 && sc.bn % 64 == 0) {
       // pairs of chunks: both boxes written, ONE async-proxy fence, two stores

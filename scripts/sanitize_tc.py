@@ -1,6 +1,7 @@
 """Small tcgen05 routes under compute-sanitizer (memcheck / racecheck):
 SHARE, ROW-on-M, CI channels-on-M (RowsOut), CTA pair (ColsOut), TAPS-N,
-TAPS, the fused SHARE conv + max pool, and the packed fc, each once at a
+TAPS, the fused SHARE conv + max pool, the packed fc, ROW row pairs with
+quad-chunk stores and TAPS row pairs with the fused 2x2 pool, each once at a
 small shape."""
 import sys
 
@@ -45,4 +46,9 @@ torch.cuda.synchronize()
 assert int(sync.abs().sum()) == 0
 for c in [(128, 3, 33, 33, 64, 3, 1, 1), (128, 32, 91, 91, 48, 3, 1, 1)]:
     t._check_conv(d, *c, t.CHWN, lcnn.TF32)
+# round 2, later: ROW row pairs with quad-chunk TMA stores (whole tiles and a
+# stream-K tail), TAPS row pairs with the 2x2 max pool in the epilogue
+for c in [(64, 3, 40, 40, 64, 3, 1, 1), (128, 3, 24, 24, 64, 3, 1, 1)]:
+    t._check_conv(d, *c, t.CHWN, lcnn.TF32)
+tp._run(d, (32, 32, 182, 182, 64, 3, 1, 1, 2, 2))
 print("ok")

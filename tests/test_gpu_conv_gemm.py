@@ -76,6 +76,8 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     (32, 3, 12, 12, 20, 3, 1, 1),     # ROW row pairs, co < 32
     (128, 3, 33, 33, 64, 3, 1, 1),    # ROW row pairs, grouped boxes, odd H_o
     (64, 5, 20, 20, 48, 3, 1, 0),     # ROW row pairs, ungrouped, no padding
+    (64, 3, 40, 40, 64, 3, 1, 1),     # ROW row pairs, quad-chunk stores + stream-K tail (chunk path)
+    (128, 3, 24, 24, 64, 3, 1, 1),    # ROW row pairs, quad-chunk stores, whole tiles
     (128, 32, 6, 6, 160, 1, 1, 0),    # 1x1, co > 128
     (96, 64, 7, 7, 64, 3, 2, 0),
     (128, 384, 13, 13, 256, 3, 1, 1),  # conv4: 170 tiles -> 148 whole + stream-K tail
