@@ -827,6 +827,7 @@ struct TapsParams {
   // stream-K); the two rows meet through the epi_off staging (2 x 16 KB)
   float* pool_out;
   uint32_t pool, hp, wp;
+  uint32_t FH;  // filter rows (tc_conv_taps_acc2_kernel)
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __grid_constant__ TapsParams prm) {
@@ -1046,6 +1047,235 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_conv_taps_kernel(const __gri
     tmem_dealloc<512>(tmem);
   } else if (threadIdx.x == 64 && sc.zsync) {
     zero_region_depart(sc.zsync);
+  }
+}
+
+// ---- TAPS with two accumulators: row pairs for C_o > 64 -------------------
+// A tile is two output rows (oh, oh + 1) x 8 pixels x one 32-image group x a
+// 128-channel tile, one 256-column TMEM accumulator per row.  K walks the
+// F_h + 1 input rows the pair shares: input row r's box feeds accumulator 0
+// with filter row r (r < F_h) and accumulator 1 with filter row r - 1
+// (r >= 1), so each input box serves both rows -- (F_h + 1) / 2 boxes per
+// output row instead of F_h -- with the usual TAPS filter image and the same
+// MMA count.  The 512 columns hold no second buffer; instead each accumulator
+// has its own full / empty barrier pair: accumulator 0 is finished one input
+// row before accumulator 1, and the next tile needs accumulator 1 only from
+// its second input row on, so each drain overlaps MMAs of the other.  Stride
+// 1, whole tiles (no stream-K).  pool: the 2 x 2 / stride-2 max pool of the
+// two rows, horizontal max per accumulator (row oh's staged in shared memory,
+// 16 KB per epilogue warp), pooled rows stored with the coalesced 32-row
+// store; the conv output never reaches HBM.
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_conv_taps_acc2_kernel(const __grid_constant__ TapsParams prm) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw_smem) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* ibase = smem;
+  uint8_t* fbase = smem + prm.ni * prm.islot;
+  TapsCtl* ctl = reinterpret_cast<TapsCtl*>(smem + prm.ctl_off);
+  const Sched& sc = prm.sc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch(&prm.x);
+      tma_prefetch(&prm.w);
+      for (uint32_t i = 0; i < prm.ni; ++i) {
+        mbar_init(&ctl->ifull[i], 1);
+        mbar_init(&ctl->iempty[i], 1);
+      }
+      for (uint32_t i = 0; i < prm.nf; ++i) {
+        mbar_init(&ctl->ffull[i], 1);
+        mbar_init(&ctl->fempty[i], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&ctl->tfull[a], 1);
+        mbar_init(&ctl->tempty[a], 4);
+      }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(&ctl->tmem_addr);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ctl->tmem_addr;
+  LCNN_PDL_ENTRY();
+  const uint32_t FH = prm.FH;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    uint32_t is = 0, iph = 0, fs = 0, fph = 0;
+    auto filter = [&](uint32_t fit, uint32_t fw, int32_t co0) {
+      mbar_wait(&ctl->fempty[fs], fph ^ 1);
+      mbar_arrive_expect_tx(&ctl->ffull[fs], kTcABytes);
+      tma_load_2d(fbase + fs * kTcABytes, &prm.w, &ctl->ffull[fs],
+                  static_cast<int32_t>((fit * prm.FW + fw) * kTcBK), co0);
+      if (++fs == prm.nf) {
+        fs = 0;
+        fph ^= 1;
+      }
+    };
+    for_each_work(sc, [&](uint32_t t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t mi = t % sc.mt, ni = t / sc.mt;
+      const uint32_t g = ni % prm.G, r = ni / prm.G, ob = r % prm.OWB, oh = 2 * (r / prm.OWB);
+      const int32_t y0 = static_cast<int32_t>(ob * kSharePix) - static_cast<int32_t>(prm.P);
+      const int32_t z0 = static_cast<int32_t>(oh) - static_cast<int32_t>(prm.P);
+      const int32_t co0 = static_cast<int32_t>(mi * kTcBM);
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        const uint32_t rr = it / prm.CB, cb = it - rr * prm.CB;
+        mbar_wait(&ctl->iempty[is], iph ^ 1);
+        mbar_arrive_expect_tx(&ctl->ifull[is], prm.ibox);
+        tma_load_5d(ibase + is * prm.islot, &prm.x, &ctl->ifull[is], 0,
+                    static_cast<int32_t>(cb * 32), y0, static_cast<int32_t>(g),
+                    z0 + static_cast<int32_t>(rr));
+        if (++is == prm.ni) {
+          is = 0;
+          iph ^= 1;
+        }
+        for (uint32_t fw = 0; fw < prm.FW; ++fw) {
+          if (rr < FH) filter(rr * prm.CB + cb, fw, co0);
+          if (rr >= 1) filter((rr - 1) * prm.CB + cb, fw, co0);
+        }
+      }
+    });
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t lbo = 4096;  // stride 1
+    uint32_t is = 0, iph = 0, fs = 0, fph = 0, local = 0;
+    for_each_work(sc, [&](uint32_t, uint32_t kbeg, uint32_t kend, bool) {
+      const uint32_t ph = local & 1;
+      ++local;
+      for (uint32_t it = kbeg; it < kend; ++it) {
+        const uint32_t rr = it / prm.CB, cb = it - rr * prm.CB;
+        if (cb == 0 && rr <= 1) {  // first MMA into accumulator rr: its drain is done
+          mbar_wait(&ctl->tempty[rr], ph ^ 1);
+          tc_fence_after();
+        }
+        mbar_wait(&ctl->ifull[is], iph);
+        tc_fence_after();
+        const uint8_t* xb = ibase + is * prm.islot;
+        for (uint32_t fw = 0; fw < prm.FW; ++fw) {
+          const uint64_t db = smem_desc_sw128(xb + fw * 4096, lbo, 512, 1);
+#pragma unroll
+          for (uint32_t acc = 0; acc < 2; ++acc) {
+            if (acc == 0 ? rr >= FH : rr == 0) continue;
+            mbar_wait(&ctl->ffull[fs], fph);
+            tc_fence_after();
+            const uint64_t da = smem_desc_sw128(fbase + fs * kTcABytes, 16, 1024);
+            const bool first = cb == 0 && fw == 0 && rr == acc;
+            if (elect_one()) {
+              if (!(sc.probe & 1)) {
+#pragma unroll
+                for (int k = 0; k < kTcBK / 8; ++k)
+                  mma_tf32(tmem + acc * kPBN, da + 2 * k, db + 64 * k, sc.idesc,
+                           (first && k == 0) ? 0u : 1u);
+              }
+              tc_commit(&ctl->fempty[fs]);
+            }
+            __syncwarp();
+            if (++fs == prm.nf) {
+              fs = 0;
+              fph ^= 1;
+            }
+          }
+        }
+        if (elect_one()) {
+          tc_commit(&ctl->iempty[is]);
+          if (cb == prm.CB - 1 && rr == FH - 1) tc_commit(&ctl->tfull[0]);
+          if (cb == prm.CB - 1 && rr == FH) tc_commit(&ctl->tfull[1]);
+        }
+        __syncwarp();
+        if (++is == prm.ni) {
+          is = 0;
+          iph ^= 1;
+        }
+      }
+    });
+  } else if (warp >= 2) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;
+    uint32_t local = 0;
+    float* stg = reinterpret_cast<float*>(smem + prm.epi_off) + q * 4096;  // pool: [u][lane][32]
+    for_each_work(sc, [&](uint32_t t, uint32_t, uint32_t, bool) {
+      const uint32_t ph = local & 1;
+      ++local;
+      const uint32_t mi = t % sc.mt, ni = t / sc.mt;
+      const uint32_t og = prm.OWB * prm.G, pr = ni / og, rest = ni - pr * og;
+      const uint32_t m = mi * kTcBM + q * 32 + lane;
+      const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+      if (!prm.pool) {
+#pragma unroll 1
+        for (uint32_t acc = 0; acc < 2; ++acc) {
+          mbar_wait(&ctl->tfull[acc], ph);
+          tc_fence_after();
+          const uint32_t oh = 2 * pr + acc;
+          if (oh < prm.Ho) {
+            const uint32_t n0 = (oh * og + rest) * kPBN;
+#pragma unroll 1
+            for (uint32_t c = 0; c < kPBN; c += 32) {
+              float v[32];
+              tmem_ld32(tmem + acc * kPBN + lanes + c, v);
+              if (!(sc.probe & 2)) prm.out.store32(m, n0 + c, v, false);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctl->tempty[acc]);
+        }
+      } else {
+        const uint32_t ob = rest / prm.G, grp = rest - ob * prm.G;
+#pragma unroll 1
+        for (uint32_t acc = 0; acc < 2; ++acc) {
+          mbar_wait(&ctl->tfull[acc], ph);
+          tc_fence_after();
+#pragma unroll 1
+          for (uint32_t u = 0; u < kSharePix / 2; ++u) {
+            float v0[32], v1[32];
+            tmem_ld32(tmem + acc * kPBN + lanes + 2 * u * 32, v0);
+            tmem_ld32(tmem + acc * kPBN + lanes + (2 * u + 1) * 32, v1);
+            float4* row = reinterpret_cast<float4*>(stg + (u * 32 + lane) * 32);
+            if (acc == 0) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                float h[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  h[e] = max_tap(max_tap(-INFINITY, v0[4 * c + e]), v1[4 * c + e]);
+                row[c ^ (lane & 7)] = make_float4(h[0], h[1], h[2], h[3]);
+              }
+            } else {
+              const uint32_t pw = ob * (kSharePix / 2) + u;
+              float o[32];
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const float4 top = row[c ^ (lane & 7)];
+                const float tv[4] = {top.x, top.y, top.z, top.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  o[4 * c + e] =
+                      max_tap(tv[e], max_tap(max_tap(-INFINITY, v0[4 * c + e]), v1[4 * c + e]));
+              }
+              if (pr < prm.hp && pw < prm.wp && !(sc.probe & 2))  // warp-uniform
+                warp_store_rows32(m < prm.out.co ? prm.pool_out +
+                                                       ((static_cast<uint64_t>(m) * prm.hp + pr) *
+                                                            prm.wp + pw) * prm.out.n + grp * 32
+                                                 : nullptr,
+                                  o, false);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctl->tempty[acc]);
+        }
+      }
+    });
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
   }
 }
 
@@ -2221,6 +2451,80 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
   return lcnn_pdl::launch(tc_conv_taps_kernel, sc.grid, kTcThreads, smem, s, prm);
 }
 
+// TAPS with two accumulators (tc_conv_taps_acc2_kernel): a TAPS-routed layer
+// (not the C_o <= 64 row pairs) at stride 1 with >= 2 output rows.
+// Profiling knob LCNN_TAPS_ACC2=0: one output row per tile.
+bool taps_acc2_ok(const ConvArgs& a) {
+  static const bool on = [] {
+    const char* e = std::getenv("LCNN_TAPS_ACC2");
+    return !(e && e[0] == '0');
+  }();
+  return on && a.stride == 1 && a.ho >= 2 && a.precision == LCNN_PREC_TF32;
+}
+
+cudaError_t launch_chwn_taps_acc2(const ConvTcArgs& t, cudaStream_t s, float* pooled = nullptr,
+                                  uint32_t hp = 0, uint32_t wp = 0) {
+  const ConvArgs& a = t.a;
+  const bool pool = pooled != nullptr;
+  constexpr uint32_t kPoolStg = 4 * 4 * 4096;  // 16 KB per epilogue warp
+  const TapsGeom q = taps_geom(a, pool ? kPoolStg + 1024 : 0);
+  if (!q.ok || a.stride != 1) return cudaErrorInvalidConfiguration;
+  TapsParams prm{};
+  const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
+  const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
+                             static_cast<uint64_t>(a.n) * 4, 128,
+                             static_cast<uint64_t>(a.w) * a.n * 4};
+  const uint32_t box[5] = {32, 32, q.bw, 1, 1};
+  if (!make_tmap(&prm.x, t.x_hi, 5, dims, pitch, box, nullptr, 1)) return cudaErrorInvalidValue;
+  const uint64_t K = t.p.K;
+  if (!make_tmap_2d(&prm.w, t.w_hi, K, a.co, K * 4, kTcBK, kTcBM, false))
+    return cudaErrorInvalidValue;
+  prm.FW = a.fw;
+  prm.S = 1;
+  prm.P = a.pad;
+  prm.CB = a.ci / 32;
+  prm.OWB = (a.wo + kSharePix - 1) / kSharePix;
+  prm.G = a.n / 32;
+  prm.ni = q.ni;
+  prm.nf = q.nf;
+  prm.islot = q.islot;
+  prm.ibox = q.ibox;
+  prm.Ho = a.ho;
+  prm.FH = a.fh;
+  const uint32_t mt = (a.co + kTcBM - 1) / kTcBM, nt = (a.ho + 1) / 2 * prm.OWB * prm.G;
+  prm.sc = make_sched(mt, nt, (a.fh + 1) * prm.CB, 1, kSharePix * 32, false, true);
+  {  // whole tiles only
+    Sched& z = prm.sc;
+    z.dp_tiles = mt * nt;
+    z.sk_iters = 0;
+    z.sk_ctas = 0;
+    z.grid = std::min<uint32_t>(z.dp_tiles, static_cast<uint32_t>(tc_sm_count()));
+  }
+  prm.ctl_off = q.ni * q.islot + q.nf * kTcABytes;
+  prm.epi_off = 0;
+  if (pool) {
+    prm.epi_off = (prm.ctl_off + 1023) / 1024 * 1024;
+    prm.ctl_off = prm.epi_off + kPoolStg;
+  }
+  prm.out = ShareOut{a.dst, static_cast<uint64_t>(a.ho) * a.wo * a.n, a.co, a.n, a.wo, prm.OWB,
+                     prm.G};
+  prm.pool_out = pooled;
+  prm.pool = pool ? 1u : 0u;
+  prm.hp = hp;
+  prm.wp = wp;
+  const uint32_t smem = 1024 + prm.ctl_off + static_cast<uint32_t>(sizeof(TapsCtl));
+  if (smem > kMaxDynSmem) return cudaErrorInvalidConfiguration;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_conv_taps_acc2_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMaxDynSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return lcnn_pdl::launch(tc_conv_taps_acc2_kernel, prm.sc.grid, kTcThreads, smem, s, prm);
+}
+
 // TAPS-N geometry (tc_conv_tapsn_pair_kernel): C_o tile, input box width,
 // ring slots that fit next to the 16 KB epilogue staging.
 struct TapsNGeom {
@@ -2704,7 +3008,7 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
   if (r.kind == kRouteRowPairs) return launch_chwn_row<false>(t, s, true);
-  if (r.kind == kRouteTaps) return launch_chwn_taps(t, s);
+  if (r.kind == kRouteTaps) return taps_acc2_ok(a) ? launch_chwn_taps_acc2(t, s) : launch_chwn_taps(t, s);
   if (r.kind == kRouteTaps2) return launch_chwn_taps(t, s, true);
   if (r.kind == kRouteTapsN) return launch_chwn_tapsn(t, s);
   if (r.kind == kRouteChwnPair) return launch_chwn_tc<true, true>(t, s);
@@ -2731,6 +3035,7 @@ bool conv_maxpool_fusable(const ConvArgs& a, uint32_t pwin, uint32_t pstride) {
   const ConvRoute r = route_conv(a);
   if (r.via_chwn) return false;
   if (r.kind == kRouteTaps2) return pwin == 2 && taps_pool_knob();
+  if (r.kind == kRouteTaps) return pwin == 2 && taps_pool_knob() && taps_acc2_ok(a);
   return r.kind == kRouteShare;
 }
 
@@ -2742,6 +3047,7 @@ cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, ui
   ConvTcArgs t{a, r.p, w, w, a.src, a.src};
   const uint32_t hp = (a.ho - pwin) / pstride + 1, wp = (a.wo - pwin) / pstride + 1;
   if (r.kind == kRouteTaps2) return launch_chwn_taps(t, s, true, a.dst, hp, wp);
+  if (r.kind == kRouteTaps) return launch_chwn_taps_acc2(t, s, a.dst, hp, wp);
   // profiling knob LCNN_SHAREPOOL_STORE=tma: staged TMA stores of the pooled
   // chunks (one ring slot fewer) instead of direct lane stores
   static const bool tma = [] {

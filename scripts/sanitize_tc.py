@@ -51,4 +51,7 @@ for c in [(128, 3, 33, 33, 64, 3, 1, 1), (128, 32, 91, 91, 48, 3, 1, 1)]:
 for c in [(64, 3, 40, 40, 64, 3, 1, 1), (128, 3, 24, 24, 64, 3, 1, 1)]:
     t._check_conv(d, *c, t.CHWN, lcnn.TF32)
 tp._run(d, (32, 32, 182, 182, 64, 3, 1, 1, 2, 2))
+# TAPS with two accumulators (C_o > 64 row pairs), plain and with the fused pool
+t._check_conv(d, 32, 32, 182, 182, 128, 3, 1, 1, t.CHWN, lcnn.TF32)
+tp._run(d, (32, 32, 182, 182, 128, 3, 1, 1, 2, 2))
 print("ok")

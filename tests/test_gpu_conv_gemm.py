@@ -97,6 +97,9 @@ CASES = [  # (n, ci, h, w, co, f, stride, pad)
     (128, 64, 92, 92, 64, 5, 1, 2),    # row pairs, 5x5 (6 input rows per pair)
     (64, 32, 130, 130, 64, 3, 1, 0),   # row pairs, no padding
     (64, 32, 130, 130, 160, 3, 2, 1),  # stride 2, two channel tiles, 32-image groups x 2
+    (32, 32, 182, 182, 128, 3, 1, 1),  # TAPS, two accumulators (rows oh, oh+1 share input boxes)
+    (64, 64, 129, 131, 160, 3, 1, 1),  # two accumulators: odd H_o, ragged pixel block, 2 channel tiles
+    (32, 32, 200, 190, 96, 5, 1, 2),   # two accumulators, 5x5 (6 input rows per pair)
     # CI, output rows >= 28, planes < 4 MB: TAPS-N (4-pixel x 32-image tiles on a CTA pair)
     (64, 32, 30, 30, 96, 3, 1, 1),     # C_o 96: 48-row filter halves per CTA
     (128, 64, 28, 28, 384, 3, 1, 1),   # two 192-channel tiles, two 64-image blocks

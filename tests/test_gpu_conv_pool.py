@@ -42,6 +42,8 @@ CASES = EXACT + [
 TAPS = [
     (32, 32, 193, 185, 48, 3, 1, 1, 2, 2),   # odd extents: last row pair / pixel block partial, c_o 48
     (64, 32, 128, 160, 64, 3, 1, 1, 2, 2),   # two image groups
+    (32, 32, 182, 182, 128, 3, 1, 1, 2, 2),  # C_o 128: two-accumulator row pairs
+    (64, 64, 129, 131, 160, 3, 1, 1, 2, 2),  # two accumulators, odd extents, 2 channel tiles
 ]
 EXACT += TAPS
 CASES += TAPS
@@ -154,3 +156,24 @@ def test_conv_maxpool_taps_vgg_conv1_2_full_size(cuda):
 
 def test_conv_maxpool_taps_special_values(cuda):
     _run(cuda, TAPS[0], seed=4, special=True)
+
+
+def test_conv_maxpool_taps_vgg_conv2_2_full_size(cuda):
+    """VGG-16 conv2_2 -> pool2 as the forward runs it (128 images, 128 -> 128
+    channels, 112 x 112): bit-equal to the two-layer run."""
+    import torch
+
+    n, ci, h, w, co = 128, 128, 112, 112, 128
+    g = torch.Generator(device=cuda).manual_seed(12)
+    x = (torch.rand(ci * h * w * n, device=cuda, generator=g) * 2 - 1)
+    filt = (torch.rand(co, ci, 3, 3, device=cuda, generator=g) * 2 - 1).contiguous()
+    t = lcnn.DeviceTensor4D(n, ci, h, w, CHWN, x)
+    assert lcnn.conv_maxpool_supported(t, co, 3, 3, 1, 1, lcnn.TF32, 2, 2)
+    packed = lcnn.pack_conv_filters(t, filt, co, 3, 3, 1, 1, lcnn.TF32)
+    conv = lcnn.conv_forward_packed(t, packed, co, 3, 3, 1, 1, lcnn.TF32)
+    want, _ = lcnn.pool_layout(conv, lcnn.PoolParams(2, 2, 2, lcnn.MAX))
+    del conv
+    got = lcnn.conv_maxpool_packed(t, packed, co, 3, 3, 1, 1, lcnn.TF32, 2, 2)
+    torch.cuda.synchronize()
+    assert (got.n, got.c, got.h, got.w) == (n, co, 56, 56)
+    assert torch.equal(got.data.view(torch.int32), want.data.view(torch.int32))

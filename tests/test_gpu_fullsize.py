@@ -162,6 +162,8 @@ def test_vgg16_forward_fullsize_vs_reference(cuda):
     ("alexnet_conv1_share", 128, 3, 227, 96, 11, 4, 0),
     ("vgg_conv1_1", 128, 3, 224, 64, 3, 1, 1),
     ("vgg_conv1_2", 128, 64, 224, 64, 3, 1, 1),
+    ("vgg_conv2_1", 128, 64, 112, 128, 3, 1, 1),
+    ("vgg_conv2_2", 128, 128, 112, 128, 3, 1, 1),
 ])
 def test_conv_routes_fullsize(cuda, geom):
     import torch
