@@ -312,9 +312,8 @@ lcnn_status lcnn_conv_forward_packed_ex(const float* src, const void* d_packed,
  * in the same layout): the conv output never reaches HBM.  Supported for
  * CHWN, TF32, layers the SHARE route takes (small c_i * f_w, c_o <= 128,
  * e.g. AlexNet conv1) with square max windows of 2 or 3 at stride 2, and
- * layers the TAPS row-pair route takes (c_i % 32 == 0, c_o <= 64, stride 1,
- * channel planes >= 4 MB, e.g. VGG-16 conv1_2) with a 2 x 2 window at
- * stride 2.
+ * layers the TAPS route takes at stride 1 (c_i % 32 == 0, channel planes
+ * >= 4 MB, e.g. VGG-16 conv1_2, conv2_2) with a 2 x 2 window at stride 2.
  * d_packed is the layer's lcnn_conv_pack_filters image (same geometry and
  * precision); dst receives the (n, c_o, hp, wp) CHWN pooled output,
  * hp/wp = pool_output_extents of the conv output.  Bit-identical to
