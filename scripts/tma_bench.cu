@@ -510,6 +510,7 @@ int main() {
       run("conv1 SHARE box x2 (2 groups) slots=4", c, sink);
     }
   }
+  if (getenv("TB_BLK")) goto blocked_boxes;
   if (getenv("TB_VGG")) goto vgg_boxes;
 conv4_boxes:
   // P/Q/R: AlexNet conv4 input (N=128, 13x13, C=384, CHWN: 33 MB, L2-resident),
@@ -644,6 +645,49 @@ vgg_boxes:
         }
         CK(cudaFree(xv));
       }
+    }
+  }
+blocked_boxes:
+  // V: the same TAPS box {32 n, 32 c, 10 w} of VGG conv1_2's input (N=128, C=64, 224 x 224)
+  // over three HBM layouts of the same tensor, DRAM-cold (H=224) and L2-resident (H=8):
+  //   CHWN           [c][h][w][n]      a (c, w) row is 128 B of a 512-B (c,h,w) line
+  //   CHWN32 blocked [g][c][h][w][32]  a box row-run is 10 w x 128 B = 1280 B contiguous
+  //   HWCN32 blocked [g][h][w][c][32]  a box is 10 runs of 32 c x 128 B = 4 KB contiguous
+  {
+    const uint64_t Nv = 128, Wv = 224, Cv = 64, G = Nv / 32;
+    for (uint64_t Hv : {224ull, 8ull}) {
+      const uint64_t bytes = Hv * Wv * Nv * 4 * Cv;
+      float* xv;
+      CK(cudaMalloc(&xv, bytes + 4096));
+      CK(cudaMemset(xv, 0, bytes));
+      for (int lay = 0; lay < 3; ++lay) {
+        Cfg c;
+        zero(c);
+        // dims {32 n, C, W, G, H}; strides of c, w, g, h in bytes
+        uint64_t str[4];
+        if (lay == 0) {
+          str[0] = Hv * Wv * Nv * 4; str[1] = Nv * 4; str[2] = 128; str[3] = Wv * Nv * 4;
+        } else if (lay == 1) {
+          str[0] = Hv * Wv * 128; str[1] = 128; str[2] = Cv * Hv * Wv * 128; str[3] = Wv * 128;
+        } else {
+          str[0] = 128; str[1] = Cv * 128; str[2] = Hv * Wv * Cv * 128; str[3] = Wv * Cv * 128;
+        }
+        const uint64_t dims[5] = {32, Cv, Wv, G, Hv};
+        const uint32_t box[5] = {32, 32, 10, 1, 1};
+        if (encode(&c.map, xv, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+          c.rank = 5; c.nbox = 1; c.box_bytes = 32 * 32 * 10 * 4; c.stages = 3;
+          c.step[1] = 32; c.wrap[1] = 64;
+          c.step[4] = 1; c.wrap[4] = (int)Hv - 2;
+          c.cta_step[3] = 1; c.wrap[3] = 4;
+          c.cta_step[2] = 2; c.wrap[2] = 210;
+          c.iters = Hv == 8 ? 3000 : 1500;
+          char name[96];
+          snprintf(name, sizeof name, "vgg1_2 TAPS box H=%llu layout %s", (unsigned long long)Hv,
+                   lay == 0 ? "CHWN" : lay == 1 ? "CHWN32 blocked" : "HWCN32 blocked");
+          run(name, c, sink);
+        }
+      }
+      CK(cudaFree(xv));
     }
   }
   return 0;
