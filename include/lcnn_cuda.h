@@ -333,6 +333,38 @@ lcnn_status lcnn_conv_maxpool_packed(const float* src, const void* d_packed,
                                      int precision, uint32_t pool_win,
                                      uint32_t pool_stride, void* stream);
 
+/* Blocked activation layout between two convolutions inside run_network (not
+ * a reference layout; never crosses the API): [N/32][H][W][C][32].  A TAPS
+ * row-pair convolution reads its input boxes from it as runs of 4 KB instead
+ * of 128-B lines of 32 channel planes (VGG conv1_2 + pool1 1.42 -> 0.93 ms,
+ * profiles/r02_tma_bench_blocked_layouts.txt); the ROW row-pair producer
+ * writes it through its quad-box epilogue.  Flags of the two _blk calls: */
+#define LCNN_CONV_IN_HWCN32 1u  /* src is blocked (conv_maxpool, TAPS row pairs) */
+#define LCNN_CONV_OUT_HWCN32 2u /* dst is blocked (conv_forward, ROW row pairs) */
+/* 1 when the route of this CHWN geometry reads / writes the blocked layout the
+ * flags name (pool_win = 0: plain conv) */
+int lcnn_conv_hwcn32_supported(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                               uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                               uint32_t stride, uint32_t pad, int precision,
+                               uint32_t pool_win, uint32_t pool_stride,
+                               uint32_t flags);
+lcnn_status lcnn_conv_forward_packed_blk(const float* src, const void* d_packed,
+                                         float* dst, uint32_t n, uint32_t c_i,
+                                         uint32_t h, uint32_t w, int layout,
+                                         uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                         uint32_t stride, uint32_t pad,
+                                         int precision, void* d_workspace,
+                                         size_t workspace_bytes, void* d_sync,
+                                         uint32_t flags, void* stream);
+lcnn_status lcnn_conv_maxpool_packed_blk(const float* src, const void* d_packed,
+                                         float* dst, uint32_t n, uint32_t c_i,
+                                         uint32_t h, uint32_t w, int layout,
+                                         uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                         uint32_t stride, uint32_t pad,
+                                         int precision, uint32_t pool_win,
+                                         uint32_t pool_stride, uint32_t flags,
+                                         void* stream);
+
 /* == conv_oracle (conv.cpp:53-93): fp64 accumulation, any input layout,
  * NCHW output.  Ground truth, not a hot op. */
 lcnn_status lcnn_conv_oracle(const float* src, const float* filters, float* dst,

@@ -102,6 +102,11 @@ _SIGNATURES = {
                                     [_U32] * 2),
     "lcnn_conv_maxpool_packed": (c_int, [_P, _P, _P] + [_U32] * 4 + [c_int] + [_U32] * 5 +
                                  [c_int] + [_U32] * 2 + [_P]),
+    "lcnn_conv_hwcn32_supported": (c_int, [_U32] * 4 + [_U32] * 5 + [c_int] + [_U32] * 3),
+    "lcnn_conv_forward_packed_blk": (c_int, [_P, _P, _P] + [_U32] * 4 + [c_int] + [_U32] * 5 +
+                                     [c_int, _P, c_size_t, _P, _U32, _P]),
+    "lcnn_conv_maxpool_packed_blk": (c_int, [_P, _P, _P] + [_U32] * 4 + [c_int] + [_U32] * 5 +
+                                     [c_int] + [_U32] * 3 + [_P]),
     "lcnn_conv_oracle": (c_int, [_P, _P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32,
                                  _U32, _P]),
     "lcnn_im2col": (c_int, [_P, _P, _U32, _U32, _U32, _U32, c_int, _U32, _U32, _U32, _U32, _P]),

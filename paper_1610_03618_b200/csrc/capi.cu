@@ -707,6 +707,17 @@ lcnn_status lcnn_conv_forward_packed_ex(const float* src, const void* d_packed, 
                                         uint32_t stride, uint32_t pad, int precision,
                                         void* d_workspace, size_t workspace_bytes, void* d_sync,
                                         void* stream) {
+  return lcnn_conv_forward_packed_blk(src, d_packed, dst, n, c_i, h, w, layout, c_o, f_h, f_w,
+                                      stride, pad, precision, d_workspace, workspace_bytes,
+                                      d_sync, 0u, stream);
+}
+
+lcnn_status lcnn_conv_forward_packed_blk(const float* src, const void* d_packed, float* dst,
+                                         uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                                         int layout, uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                         uint32_t stride, uint32_t pad, int precision,
+                                         void* d_workspace, size_t workspace_bytes, void* d_sync,
+                                         uint32_t flags, void* stream) {
   if (!src || !d_packed || !dst) return fail(LCNN_EINVAL, "conv: null pointer");
   if (reinterpret_cast<uintptr_t>(d_sync) & 7u)
     return fail(LCNN_EINVAL, "conv: sync word must be 8-byte aligned");
@@ -722,6 +733,9 @@ lcnn_status lcnn_conv_forward_packed_ex(const float* src, const void* d_packed, 
   a.dst = dst;
   a.workspace = d_workspace;
   a.zsync = static_cast<unsigned long long*>(d_sync);
+  a.blk = flags;
+  if (flags && !lcnn_impl::conv_hwcn32_ok(a, 0, 0))
+    return fail(LCNN_EUNSUPPORTED, "conv: blocked activation layout not covered by this route");
   cudaError_t e = lcnn_impl::launch_conv_packed(a, d_packed, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "conv_forward_packed");
   return ok();
@@ -742,6 +756,27 @@ lcnn_status lcnn_conv_maxpool_packed(const float* src, const void* d_packed, flo
                                      uint32_t c_o, uint32_t f_h, uint32_t f_w, uint32_t stride,
                                      uint32_t pad, int precision, uint32_t pool_win,
                                      uint32_t pool_stride, void* stream) {
+  return lcnn_conv_maxpool_packed_blk(src, d_packed, dst, n, c_i, h, w, layout, c_o, f_h, f_w,
+                                      stride, pad, precision, pool_win, pool_stride, 0u, stream);
+}
+
+int lcnn_conv_hwcn32_supported(uint32_t n, uint32_t c_i, uint32_t h, uint32_t w, uint32_t c_o,
+                               uint32_t f_h, uint32_t f_w, uint32_t stride, uint32_t pad,
+                               int precision, uint32_t pool_win, uint32_t pool_stride,
+                               uint32_t flags) {
+  lcnn_impl::ConvArgs a;
+  if (conv_args(n, c_i, h, w, LCNN_CHWN, c_o, f_h, f_w, stride, pad, precision, &a) != LCNN_OK)
+    return 0;
+  a.blk = flags;
+  return lcnn_impl::conv_hwcn32_ok(a, pool_win, pool_stride) ? 1 : 0;
+}
+
+lcnn_status lcnn_conv_maxpool_packed_blk(const float* src, const void* d_packed, float* dst,
+                                         uint32_t n, uint32_t c_i, uint32_t h, uint32_t w,
+                                         int layout, uint32_t c_o, uint32_t f_h, uint32_t f_w,
+                                         uint32_t stride, uint32_t pad, int precision,
+                                         uint32_t pool_win, uint32_t pool_stride, uint32_t flags,
+                                         void* stream) {
   if (!src || !d_packed || !dst) return fail(LCNN_EINVAL, "conv_maxpool: null pointer");
   if (reinterpret_cast<uintptr_t>(d_packed) & 255u)
     return fail(LCNN_EINVAL, "conv_maxpool: packed filters must be 256-byte aligned");
@@ -753,6 +788,9 @@ lcnn_status lcnn_conv_maxpool_packed(const float* src, const void* d_packed, flo
   a.src = src;
   a.dst = dst;
   a.workspace = nullptr;
+  a.blk = flags;
+  if (flags && !lcnn_impl::conv_hwcn32_ok(a, pool_win, pool_stride))
+    return fail(LCNN_EUNSUPPORTED, "conv_maxpool: blocked input layout not covered by this route");
   cudaError_t e = lcnn_impl::launch_conv_maxpool_packed(a, d_packed, pool_win, pool_stride,
                                                         S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "conv_maxpool_packed");

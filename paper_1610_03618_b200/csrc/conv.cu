@@ -467,12 +467,39 @@ struct RowsPairOutT {
 // go out as one box per 32 channels, 512 B per channel, through the 3D view
 // yq {32, ncols / 32, C_o}; split tiles (stream-K fragments) and tiles whose
 // columns are not 128-aligned use the 2D chunk path of RowsPairOutT.
+//
+// Blocked output (nimg != 0, LCNN_CONV_OUT_HWCN32): the activation is
+// [N/32][H][W][C][32], so a (pixel, 32-image group) holds its C channels' 128-B
+// lines contiguously and a quad box is four 4 KB runs.  y / yq are then 4D
+// views {32 i, N/32 g, H*W pixel, C} (boxes {32, 1, 1, 32} / {32, 4, 1, 32}).
 struct RowsQuadOut : RowsPairOutT<false> {
   CUtensorMap yq;
+  uint32_t nimg = 0, hw = 0;  // blocked: images N, pixels Ho * Wo
   static constexpr bool kTmaQuads = true;
   __device__ __forceinline__ void tma_quad(const void* box, uint32_t m0, uint32_t n0) const {
     if (!remap(m0, n0) || m0 >= M) return;
-    tma_store_3d(&yq, box, 0, static_cast<int32_t>(n0 / 32), static_cast<int32_t>(m0));
+    if (nimg)
+      tma_store_4d(&yq, box, 0, static_cast<int32_t>(n0 % nimg / 32),
+                   static_cast<int32_t>(n0 / nimg), static_cast<int32_t>(m0));
+    else
+      tma_store_3d(&yq, box, 0, static_cast<int32_t>(n0 / 32), static_cast<int32_t>(m0));
+  }
+  __device__ __forceinline__ void tma_chunk(const void* box, uint32_t m0, uint32_t n0,
+                                            bool add) const {
+    if (!nimg) return RowsPairOutT<false>::tma_chunk(box, m0, n0, add);
+    if (!remap(m0, n0) || m0 >= M) return;
+    const int32_t g = static_cast<int32_t>(n0 % nimg / 32), px = static_cast<int32_t>(n0 / nimg);
+    if (add)
+      tma_add_4d(&y, box, 0, g, px, static_cast<int32_t>(m0));
+    else
+      tma_store_4d(&y, box, 0, g, px, static_cast<int32_t>(m0));
+  }
+  __device__ __forceinline__ void store32(uint32_t m, uint32_t n0, const float* v,
+                                          bool add) const {
+    if (!nimg) return RowsPairOutT<false>::store32(m, n0, v, add);
+    if (!remap(m, n0)) return;  // warp-uniform
+    const uint64_t line = (uint64_t{n0 % nimg / 32} * hw + n0 / nimg) * M + m;
+    warp_store_rows32(m < M ? c + line * 32 : nullptr, v, add);
   }
 };
 
@@ -2085,8 +2112,12 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s, bool rows2 = fa
       // (tiles from the first one touching that pair wait for it)
       const uint32_t pr0 = static_cast<uint32_t>(uint64_t{sc.dp_tiles / sc.mt} * kPBN / span);
       const uint64_t ncols = uint64_t{a.ho} * span, col0 = uint64_t{2 * pr0} * span;
+      // blocked output: from pixel col0 / N on, in each of the N/32 groups
+      const bool blk = a.blk & LCNN_CONV_OUT_HWCN32;
+      const uint64_t hw = uint64_t{a.ho} * a.wo, px0 = col0 / a.n, run = uint64_t{a.co} * 32;
       cudaError_t e = sched_zero_region(
-          sc, a.zsync, a.dst + col0, ncols, ncols - col0, a.co,
+          sc, a.zsync, blk ? a.dst + px0 * run : a.dst + col0, blk ? hw * run : ncols,
+          blk ? (hw - px0) * run : ncols - col0, blk ? a.n / 32 : a.co,
           static_cast<uint32_t>(uint64_t{pr0} * span / kPBN) * sc.mt,
           [s](float* z, uint64_t pitch, uint64_t width, uint64_t rows) {
             return launch_zero2d(z, pitch, width, rows, s);
@@ -2119,12 +2150,23 @@ cudaError_t launch_chwn_row(const ConvTcArgs& t, cudaStream_t s, bool rows2 = fa
         const uint64_t qdims[3] = {32, dims[0] / 32, a.co};
         const uint64_t qpitch[2] = {128, dims[0] * 4};
         const uint32_t qbox[3] = {32, 4, 32};
-        if (!make_tmap(&O.y, a.dst, 2, dims, opitch, obox, nullptr, 0) ||
-            !make_tmap(&O.yq, a.dst, 3, qdims, qpitch, qbox, nullptr, 0))
+        if (a.blk & LCNN_CONV_OUT_HWCN32) {  // 4D views {32 i, N/32, Ho*Wo, C}
+          O.nimg = a.n;
+          O.hw = a.ho * a.wo;
+          const uint64_t bdims[4] = {32, a.n / 32, uint64_t{O.hw}, a.co};
+          const uint64_t bpitch[3] = {uint64_t{O.hw} * a.co * 128, uint64_t{a.co} * 128, 128};
+          const uint32_t cbox[4] = {32, 1, 1, 32}, bqbox[4] = {32, 4, 1, 32};
+          if (a.n % 128 || !make_tmap(&O.y, a.dst, 4, bdims, bpitch, cbox, nullptr, 0) ||
+              !make_tmap(&O.yq, a.dst, 4, bdims, bpitch, bqbox, nullptr, 0))
+            return cudaErrorInvalidValue;
+        } else if (!make_tmap(&O.y, a.dst, 2, dims, opitch, obox, nullptr, 0) ||
+                   !make_tmap(&O.yq, a.dst, 3, qdims, qpitch, qbox, nullptr, 0)) {
           return cudaErrorInvalidValue;
+        }
         return launch_persistent(L, O, se, s);
       }
     }
+    if (a.blk) return cudaErrorNotSupported;  // the blocked output needs the quad epilogue
     if (pairs == 2) {
       RowsPairOutT<false, false> O{a.dst, uint64_t{a.ho} * span, a.co, span, a.ho};
       return launch_persistent(L, O, sc, s);
@@ -2377,9 +2419,18 @@ cudaError_t launch_chwn_taps(const ConvTcArgs& t, cudaStream_t s, bool rows2 = f
   prm.hp = hp;
   prm.wp = wp;
   const uint64_t dims[5] = {32, a.ci, a.w, a.n / 32, a.h};
-  const uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
-                             static_cast<uint64_t>(a.n) * 4, 128,
-                             static_cast<uint64_t>(a.w) * a.n * 4};
+  uint64_t pitch[4] = {static_cast<uint64_t>(a.h) * a.w * a.n * 4,
+                       static_cast<uint64_t>(a.n) * 4, 128,
+                       static_cast<uint64_t>(a.w) * a.n * 4};
+  if (a.blk & LCNN_CONV_IN_HWCN32) {  // [N/32][H][W][C][32]: strides of c, w, g, h
+    // (the box {32 n, 32 c, BW w} lands in shared memory exactly as from CHWN;
+    // in HBM it is BW runs of 4 KB: 11.6 against 4.6 TB/s DRAM-cold,
+    // profiles/r02_tma_bench_blocked_layouts.txt)
+    pitch[0] = 128;
+    pitch[1] = uint64_t{a.ci} * 128;
+    pitch[2] = uint64_t{a.h} * a.w * a.ci * 128;
+    pitch[3] = uint64_t{a.w} * a.ci * 128;
+  }
   const uint32_t box[5] = {32, 32, q.bw, 1, 1};
   if (!make_tmap(&prm.x, t.x_hi, 5, dims, pitch, box, nullptr, 1)) return cudaErrorInvalidValue;
   const uint64_t K = t.p.K;
@@ -3005,6 +3056,8 @@ cudaError_t launch_conv_packed(const ConvArgs& a, const void* packed, cudaStream
   ConvTcArgs t{a, r.p, w_hi, w_lo, x_hi, x_lo};
   if (r.kind == kRouteShare || r.kind == kRouteShareRes)
     return launch_chwn_share(t, r.kind == kRouteShareRes, s);
+  if (a.blk && (a.blk != LCNN_CONV_OUT_HWCN32 || r.kind != kRouteRowPairs))
+    return cudaErrorNotSupported;  // blocked activations: row-pair producer only here
   if (r.kind == kRouteRowOnN) return launch_chwn_row<true>(t, s);
   if (r.kind == kRouteRowOnM) return launch_chwn_row<false>(t, s);
   if (r.kind == kRouteRowPairs) return launch_chwn_row<false>(t, s, true);
@@ -3046,6 +3099,8 @@ cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, ui
   const float* w = static_cast<const float*>(packed);
   ConvTcArgs t{a, r.p, w, w, a.src, a.src};
   const uint32_t hp = (a.ho - pwin) / pstride + 1, wp = (a.wo - pwin) / pstride + 1;
+  if (a.blk && (a.blk != LCNN_CONV_IN_HWCN32 || r.kind != kRouteTaps2))
+    return cudaErrorNotSupported;  // blocked input: the TAPS row-pair consumer only
   if (r.kind == kRouteTaps2) return launch_chwn_taps(t, s, true, a.dst, hp, wp);
   if (r.kind == kRouteTaps) return launch_chwn_taps_acc2(t, s, a.dst, hp, wp);
   // profiling knob LCNN_SHAREPOOL_STORE=tma: staged TMA stores of the pooled
@@ -3059,6 +3114,17 @@ cudaError_t launch_conv_maxpool_packed(const ConvArgs& a, const void* packed, ui
   if (pwin == 2) return launch_chwn_share_pool<2, false>(t, a.dst, hp, wp, s);
   return tma ? launch_chwn_share_pool<3, false>(t, a.dst, hp, wp, s)
              : launch_chwn_share_pool<3, true>(t, a.dst, hp, wp, s);
+}
+
+bool conv_hwcn32_ok(const ConvArgs& a, uint32_t pwin, uint32_t pstride) {
+  if (a.layout != LCNN_CHWN || a.precision != LCNN_PREC_TF32 || a.n % 128 || !a.blk) return false;
+  const ConvRoute r = route_conv(a);
+  if (a.blk == LCNN_CONV_OUT_HWCN32)  // ROW row pairs with the quad-box epilogue
+    return pwin == 0 && r.kind == kRouteRowPairs && !r.via_chwn &&
+           (uint64_t{a.wo} * a.n) % 128 == 0;
+  if (a.blk == LCNN_CONV_IN_HWCN32)  // TAPS row pairs with the fused pool
+    return pwin != 0 && conv_maxpool_fusable(a, pwin, pstride) && r.kind == kRouteTaps2;
+  return false;
 }
 
 // One-shot form: pack into the front of the workspace, run with the rest.

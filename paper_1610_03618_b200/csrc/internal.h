@@ -59,7 +59,14 @@ struct ConvArgs {
   // launches of one call site that never overlap): stream-K output regions
   // are zeroed inside the kernel instead of by a zero2d launch (nullptr: launch)
   unsigned long long* zsync = nullptr;
+  // LCNN_CONV_IN_HWCN32 / LCNN_CONV_OUT_HWCN32: the input / output activation
+  // is in the blocked [N/32][H][W][C][32] layout (run_network-internal, between
+  // a ROW row-pair producer and a TAPS row-pair consumer)
+  uint32_t blk = 0;
 };
+// 1 when the route of `a` (and the fused pool when pwin != 0) reads / writes
+// the blocked layout the flags name
+bool conv_hwcn32_ok(const ConvArgs& a, uint32_t pwin, uint32_t pstride);
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s);
 cudaError_t launch_conv_oracle(const ConvArgs& a, uint64_t sn, uint64_t sc, uint64_t sh,
                                uint64_t sw, cudaStream_t s);

@@ -55,7 +55,8 @@ std::shared_ptr<DeviceBuffer> pack_conv_filters(const DeviceTensor4D& in, const 
 // d_sync (optional): lcnn_conv_forward_packed_ex's per-call-site sync words
 DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packed,
                                    std::uint32_t c_o, std::uint32_t f_h, std::uint32_t f_w,
-                                   const ConvParams& p, int precision, void* d_sync = nullptr);
+                                   const ConvParams& p, int precision, void* d_sync = nullptr,
+                                   std::uint32_t blk_flags = 0);
 
 // Convolution and the max pooling that consumes it as one kernel
 // (lcnn_conv_maxpool_packed): returns the POOLED tensor, bit-identical to
@@ -68,6 +69,14 @@ bool conv_maxpool_supported(const DeviceTensor4D& in, std::uint32_t c_o, std::ui
 DeviceTensor4D conv_maxpool_forward_packed(const DeviceTensor4D& in, const void* d_packed,
                                            std::uint32_t c_o, std::uint32_t f_h,
                                            std::uint32_t f_w, const ConvParams& p, int precision,
-                                           std::uint32_t pool_win, std::uint32_t pool_stride);
+                                           std::uint32_t pool_win, std::uint32_t pool_stride,
+                                           std::uint32_t blk_flags = 0);
+// blk_flags (LCNN_CONV_IN_HWCN32 / LCNN_CONV_OUT_HWCN32 of lcnn_cuda.h): the
+// run_network-internal blocked activation between a ROW row-pair conv and the
+// TAPS row-pair conv + pool that consumes it; the tensor keeps its CHWN tag.
+bool conv_hwcn32_supported(const DeviceTensor4D& in, std::uint32_t c_o, std::uint32_t f_h,
+                           std::uint32_t f_w, const ConvParams& p, int precision,
+                           std::uint32_t pool_win, std::uint32_t pool_stride,
+                           std::uint32_t blk_flags);
 
 }  // namespace lcnn

@@ -447,7 +447,8 @@ std::shared_ptr<DeviceBuffer> pack_conv_filters(const DeviceTensor4D& in, const 
 
 DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packed,
                                    std::uint32_t c_o, std::uint32_t f_h, std::uint32_t f_w,
-                                   const ConvParams& p, int precision, void* d_sync) {
+                                   const ConvParams& p, int precision, void* d_sync,
+                                   std::uint32_t blk_flags) {
   const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f_h, f_w, p);
   DeviceTensor4D out(in.n(), c_o, ho, wo, in.layout());
   const std::size_t ws = lcnn_conv_packed_workspace_bytes(
@@ -459,10 +460,10 @@ DeviceTensor4D conv_forward_packed(const DeviceTensor4D& in, const void* d_packe
     wsp = buf.get();
     wsb = buf.bytes();
   }
-  check_status(lcnn_conv_forward_packed_ex(in.data(), d_packed, out.data(), in.n(), in.c(),
-                                           in.h(), in.w(), code(in.layout()), c_o, f_h, f_w,
-                                           p.stride, p.pad, precision, wsp, wsb, d_sync,
-                                           current_stream()));
+  check_status(lcnn_conv_forward_packed_blk(in.data(), d_packed, out.data(), in.n(), in.c(),
+                                            in.h(), in.w(), code(in.layout()), c_o, f_h, f_w,
+                                            p.stride, p.pad, precision, wsp, wsb, d_sync,
+                                            blk_flags, current_stream()));
   return out;
 }
 
@@ -477,17 +478,28 @@ bool conv_maxpool_supported(const DeviceTensor4D& in, std::uint32_t c_o, std::ui
 DeviceTensor4D conv_maxpool_forward_packed(const DeviceTensor4D& in, const void* d_packed,
                                            std::uint32_t c_o, std::uint32_t f_h,
                                            std::uint32_t f_w, const ConvParams& p, int precision,
-                                           std::uint32_t pool_win, std::uint32_t pool_stride) {
+                                           std::uint32_t pool_win, std::uint32_t pool_stride,
+                                           std::uint32_t blk_flags) {
   const auto [ho, wo] = conv_output_extents(in.h(), in.w(), f_h, f_w, p);
   if (pool_win == 0 || pool_stride == 0 || pool_win > ho || pool_win > wo)
     throw ShapeError("conv_maxpool: pool window does not fit the conv output");
   const std::uint32_t hp = (ho - pool_win) / pool_stride + 1;
   const std::uint32_t wp = (wo - pool_win) / pool_stride + 1;
   DeviceTensor4D out(in.n(), c_o, hp, wp, in.layout());
-  check_status(lcnn_conv_maxpool_packed(in.data(), d_packed, out.data(), in.n(), in.c(), in.h(),
-                                        in.w(), code(in.layout()), c_o, f_h, f_w, p.stride, p.pad,
-                                        precision, pool_win, pool_stride, current_stream()));
+  check_status(lcnn_conv_maxpool_packed_blk(in.data(), d_packed, out.data(), in.n(), in.c(),
+                                            in.h(), in.w(), code(in.layout()), c_o, f_h, f_w,
+                                            p.stride, p.pad, precision, pool_win, pool_stride,
+                                            blk_flags, current_stream()));
   return out;
+}
+
+bool conv_hwcn32_supported(const DeviceTensor4D& in, std::uint32_t c_o, std::uint32_t f_h,
+                           std::uint32_t f_w, const ConvParams& p, int precision,
+                           std::uint32_t pool_win, std::uint32_t pool_stride,
+                           std::uint32_t blk_flags) {
+  if (in.layout() != Layout::CHWN) return false;
+  return lcnn_conv_hwcn32_supported(in.n(), in.c(), in.h(), in.w(), c_o, f_h, f_w, p.stride,
+                                    p.pad, precision, pool_win, pool_stride, blk_flags) == 1;
 }
 
 Tensor4D conv_oracle(const Tensor4D& in, const FilterBank& f, const ConvParams& p) {

@@ -389,10 +389,13 @@ def pack_conv_filters(x: DeviceTensor4D, filters, c_o, f_h, f_w, stride=1, pad=0
 
 
 def conv_forward_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride=1, pad=0,
-                        precision=FP32, out=None, stream=None, sync=None) -> DeviceTensor4D:
+                        precision=FP32, out=None, stream=None, sync=None,
+                        blk=0) -> DeviceTensor4D:
     """conv_forward on filters made by pack_conv_filters for this geometry.
     sync: optional CUDA tensor of >= capi.SYNC_BYTES zeroed bytes owned by
-    this call site (lcnn_conv_forward_packed_ex: in-kernel stream-K zeroing)."""
+    this call site (lcnn_conv_forward_packed_ex: in-kernel stream-K zeroing).
+    blk = OUT_HWCN32: the output is written in the run_network-internal
+    blocked [N/32][H][W][C][32] layout (lcnn_conv_forward_packed_blk)."""
     torch = _torch()
     ho, wo = conv_output_extents(x.h, x.w, f_h, f_w, stride, pad)
     if out is None:
@@ -402,10 +405,22 @@ def conv_forward_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride=1, pad=
     geo = (x.n, x.c, x.h, x.w, x.layout, c_o, f_h, f_w, stride, pad, precision)
     nbytes = capi.lib().lcnn_conv_packed_workspace_bytes(*geo)
     ws = torch.empty(max(1, (nbytes + 3) // 4), dtype=torch.float32, device=x.data.device)
-    capi.call("lcnn_conv_forward_packed_ex", x.ptr(), packed.data_ptr(), out.ptr(), *geo,
+    capi.call("lcnn_conv_forward_packed_blk", x.ptr(), packed.data_ptr(), out.ptr(), *geo,
               ws.data_ptr(), ws.numel() * 4, sync.data_ptr() if sync is not None else None,
-              _stream(stream))
+              blk, _stream(stream))
     return out
+
+
+IN_HWCN32, OUT_HWCN32 = 1, 2  # lcnn_cuda.h LCNN_CONV_IN_HWCN32 / LCNN_CONV_OUT_HWCN32
+
+
+def conv_hwcn32_supported(x: DeviceTensor4D, c_o, f_h, f_w, stride, pad, precision, pool_win,
+                          pool_stride, blk) -> bool:
+    """lcnn_conv_hwcn32_supported: this CHWN layer's route reads (IN) or
+    writes (OUT) the blocked layout."""
+    return capi.lib().lcnn_conv_hwcn32_supported(
+        x.n, x.c, x.h, x.w, c_o, f_h, f_w, stride, pad, precision, pool_win, pool_stride,
+        blk) == 1
 
 
 def conv_maxpool_supported(x: DeviceTensor4D, c_o, f_h, f_w, stride, pad, precision, pool_win,
@@ -418,7 +433,7 @@ def conv_maxpool_supported(x: DeviceTensor4D, c_o, f_h, f_w, stride, pad, precis
 
 
 def conv_maxpool_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride, pad, precision,
-                        pool_win, pool_stride, out=None, stream=None) -> DeviceTensor4D:
+                        pool_win, pool_stride, out=None, stream=None, blk=0) -> DeviceTensor4D:
     """Convolution and the max pooling that consumes it as one kernel
     (lcnn_conv_maxpool_packed): the pooled CHWN tensor, bit-identical to
     conv_forward_packed followed by pool_layout (max)."""
@@ -429,9 +444,9 @@ def conv_maxpool_packed(x: DeviceTensor4D, packed, c_o, f_h, f_w, stride, pad, p
         out = DeviceTensor4D(x.n, c_o, hp, wp, x.layout,
                              torch.empty(x.n * c_o * hp * wp, dtype=torch.float32,
                                          device=x.data.device))
-    capi.call("lcnn_conv_maxpool_packed", x.ptr(), packed.data_ptr(), out.ptr(), x.n, x.c, x.h,
-              x.w, x.layout, c_o, f_h, f_w, stride, pad, precision, pool_win, pool_stride,
-              _stream(stream))
+    capi.call("lcnn_conv_maxpool_packed_blk", x.ptr(), packed.data_ptr(), out.ptr(), x.n, x.c,
+              x.h, x.w, x.layout, c_o, f_h, f_w, stride, pad, precision, pool_win, pool_stride,
+              blk, _stream(stream))
     return out
 
 

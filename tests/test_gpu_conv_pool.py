@@ -177,3 +177,68 @@ def test_conv_maxpool_taps_vgg_conv2_2_full_size(cuda):
     torch.cuda.synchronize()
     assert (got.n, got.c, got.h, got.w) == (n, co, 56, 56)
     assert torch.equal(got.data.view(torch.int32), want.data.view(torch.int32))
+
+
+def _to_blocked(t, n, c, h, w):
+    """CHWN [c][h][w][n] -> the blocked [n/32][h][w][c][32] (flat)."""
+    return t.view(c, h, w, n // 32, 32).permute(3, 1, 2, 0, 4).contiguous().view(-1)
+
+
+def _from_blocked(t, n, c, h, w):
+    return t.view(n // 32, h, w, c, 32).permute(3, 1, 2, 0, 4).contiguous().view(-1)
+
+
+def test_hwcn32_vgg_conv1_1_to_conv1_2_pool1_full_size(cuda):
+    """The run_network-internal blocked activation between VGG conv1_1 (ROW row
+    pairs, quad-box epilogue writing [N/32][H][W][C][32]) and conv1_2 + pool1
+    (TAPS row pairs reading it as 4 KB runs): the producer writes the same
+    values as the CHWN route, permuted (fp32 stream-K fragments may add in
+    another order: 1e-6 relative), and the consumer returns exactly the bits
+    of the CHWN conv1_2 + pool1 on the same values."""
+    import torch
+
+    n, h, w = 128, 224, 224
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x = torch.rand(3 * h * w * n, device=cuda, generator=g) * 2 - 1
+    f1 = (torch.rand(64, 3, 3, 3, device=cuda, generator=g) * 2 - 1).contiguous()
+    f2 = (torch.rand(64, 64, 3, 3, device=cuda, generator=g) * 0.2 - 0.1).contiguous()
+    t = lcnn.DeviceTensor4D(n, 3, h, w, CHWN, x)
+    assert lcnn.conv_hwcn32_supported(t, 64, 3, 3, 1, 1, lcnn.TF32, 0, 0, lcnn.OUT_HWCN32)
+    assert not lcnn.conv_hwcn32_supported(t, 64, 3, 3, 1, 1, lcnn.TF32, 0, 0, lcnn.IN_HWCN32)
+    assert not lcnn.conv_hwcn32_supported(t, 64, 3, 3, 1, 1, lcnn.FP32, 0, 0, lcnn.OUT_HWCN32)
+    p1 = lcnn.pack_conv_filters(t, f1, 64, 3, 3, 1, 1, lcnn.TF32)
+    c11 = lcnn.conv_forward_packed(t, p1, 64, 3, 3, 1, 1, lcnn.TF32)
+    c11b = lcnn.conv_forward_packed(t, p1, 64, 3, 3, 1, 1, lcnn.TF32, blk=lcnn.OUT_HWCN32)
+    torch.cuda.synchronize()
+    ref = _to_blocked(c11.data, n, 64, h, w)
+    scale = ref.abs().max().item()
+    assert (c11b.data - ref).abs().max().item() <= 1e-6 * scale
+    del c11, ref
+    assert lcnn.conv_hwcn32_supported(c11b, 64, 3, 3, 1, 1, lcnn.TF32, 2, 2, lcnn.IN_HWCN32)
+    p2 = lcnn.pack_conv_filters(c11b, f2, 64, 3, 3, 1, 1, lcnn.TF32)
+    got = lcnn.conv_maxpool_packed(c11b, p2, 64, 3, 3, 1, 1, lcnn.TF32, 2, 2,
+                                   blk=lcnn.IN_HWCN32)
+    plain = lcnn.DeviceTensor4D(n, 64, h, w, CHWN, _from_blocked(c11b.data, n, 64, h, w))
+    want = lcnn.conv_maxpool_packed(plain, p2, 64, 3, 3, 1, 1, lcnn.TF32, 2, 2)
+    torch.cuda.synchronize()
+    assert (got.n, got.c, got.h, got.w) == (n, 64, 112, 112)
+    assert torch.equal(got.data.view(torch.int32), want.data.view(torch.int32))
+
+
+def test_hwcn32_unsupported_routes_fail_loudly(cuda):
+    """A blocked flag on a route that cannot honour it is an error, never a
+    silent CHWN run (AlexNet conv1 SHARE route; a pool-fused SHARE consumer)."""
+    import torch
+
+    from paper_1610_03618_b200 import errors
+
+    n = 32
+    x = torch.rand(3 * 227 * 227 * n, device=cuda)
+    f = torch.rand(96, 3, 11, 11, device=cuda).contiguous()
+    t = lcnn.DeviceTensor4D(n, 3, 227, 227, CHWN, x)
+    assert not lcnn.conv_hwcn32_supported(t, 96, 11, 11, 4, 0, lcnn.TF32, 0, 0, lcnn.OUT_HWCN32)
+    p = lcnn.pack_conv_filters(t, f, 96, 11, 11, 4, 0, lcnn.TF32)
+    with pytest.raises(errors.Error):
+        lcnn.conv_forward_packed(t, p, 96, 11, 11, 4, 0, lcnn.TF32, blk=lcnn.OUT_HWCN32)
+    with pytest.raises(errors.Error):
+        lcnn.conv_maxpool_packed(t, p, 96, 11, 11, 4, 0, lcnn.TF32, 3, 2, blk=lcnn.IN_HWCN32)
